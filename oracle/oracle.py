@@ -1,0 +1,335 @@
+"""ctypes wrapper around the CPU ORACLE (oracle/liboracle.so).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / ``--impl reference`` leg as the checker and the CPU
+baseline.  The product package (paper_1410_0986_b200) never imports it.
+See hydot_oracle.cpp for the restated reference lines and the parity-pin
+status ("pinned by the reference's known-answer tests; Eigen numerics pinned
+by bounds").
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = None
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+_i64p = C.POINTER(C.c_int64)
+_u64p = C.POINTER(C.c_uint64)
+
+
+def build() -> str:
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return os.path.join(_HERE, "liboracle.so")
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        path = os.path.join(_HERE, "liboracle.so")
+        if not os.path.exists(path):
+            build()
+        L = C.CDLL(path)
+        L.oracle_last_error.restype = C.c_char_p
+        L.oracle_tolerance_schedule.restype = C.c_double
+        L.oracle_tolerance_schedule.argtypes = [C.c_double, C.c_int, C.c_int]
+        L.oracle_gaussian.argtypes = [C.c_uint64, C.c_int64, _dp]
+        L.oracle_mt19937_64.argtypes = [C.c_uint64, C.c_int64, _u64p]
+        L.oracle_born_block.argtypes = [C.c_int64, C.c_int, _dp, C.POINTER(_dp), C.c_int, _dp,
+                                        C.c_double, _dp]
+        L.oracle_apply7.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                    C.c_double, _dp, _dp]
+        L.oracle_fields.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, _dp, _dp,
+                                    _dp, _i64p, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
+                                    _dp, _ip, _dp]
+        L.oracle_factor_free.argtypes = [C.c_void_p]
+        L.oracle_factor_info.argtypes = [C.c_void_p, _i64p, _i64p, _i64p, _dp, _ip, _ip]
+        L.oracle_factor_get.argtypes = [C.c_void_p, _dp, _dp]
+        L.oracle_factor_meta.argtypes = [C.c_void_p, _ip, _ip, _ip, _dp]
+        L.oracle_factor_perm_len.argtypes = [C.c_void_p]
+        L.oracle_factor_perm_len.restype = C.c_int64
+        L.oracle_factor_make.argtypes = [_dp, _dp, C.c_int64, C.c_int64, C.c_int64, C.c_double,
+                                         C.c_int, C.c_int]
+        L.oracle_factor_make.restype = C.c_void_p
+        L.oracle_randsvd.argtypes = [_dp, C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_int,
+                                     C.c_int, C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        L.oracle_agglomerate.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_uint64, C.c_int,
+                                         C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        L.oracle_recompress.argtypes = [C.c_void_p, C.c_double, C.c_int, C.POINTER(C.c_void_p)]
+        L.oracle_build_cluster_tree.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp,
+                                                C.POINTER(C.c_void_p)]
+        L.oracle_tree_free.argtypes = [C.c_void_p]
+        for n in ("oracle_tree_num_nodes", "oracle_tree_root", "oracle_tree_depth"):
+            getattr(L, n).argtypes = [C.c_void_p]
+        L.oracle_tree_node.argtypes = [C.c_void_p, C.c_int, _ip, _ip, _ip]
+        L.oracle_tree_node_idx.argtypes = [C.c_void_p, C.c_int, _ip]
+        L.oracle_tree_leaf_order.argtypes = [C.c_void_p, _ip]
+        L.oracle_recursive_lowrank.argtypes = [C.c_void_p, C.c_double, _dp, C.c_int64, C.c_int64,
+                                               C.c_int64, C.c_int, C.c_uint64, C.c_int, C.c_int,
+                                               C.POINTER(C.c_void_p)]
+        L.oracle_recursive_lowrank_born.argtypes = [C.c_void_p, C.c_double, C.c_int64, C.c_int,
+                                                    C.c_int, C.POINTER(_dp), C.POINTER(_dp), _dp,
+                                                    C.c_double, C.c_uint64, C.c_int, C.c_int,
+                                                    C.POINTER(C.c_void_p)]
+        L.oracle_lr_matmat.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, _dp]
+        L.oracle_j_matmat.argtypes = [C.c_void_p, C.c_int, C.c_int, _ip, _dp, C.c_int, C.c_int,
+                                      _dp, _dp]
+        L.oracle_fast_thin_svd.argtypes = [_dp, C.c_int64, C.c_int64, _dp, _dp, _dp]
+        L.oracle_save_factor.argtypes = [C.c_char_p, C.c_void_p, _ip, C.c_int64]
+        L.oracle_set_threads.argtypes = [C.c_int]
+        _LIB = L
+        L.oracle_set_threads(1)  # reference hot path is single-threaded
+    return _LIB
+
+
+def _d(a):
+    return a.ctypes.data_as(_dp)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _check(rc):
+    if rc != 0:
+        msg = lib().oracle_last_error().decode()
+        raise (ValueError if rc == 1 else RuntimeError)(msg)
+
+
+def set_threads(n: int) -> None:
+    lib().oracle_set_threads(int(n))
+
+
+LEAF, AGGLOMERATION, RECOMPRESS, OTHER = 0, 1, 2, 3
+
+
+def tolerance_schedule(eps_d, L, N_r):
+    v = lib().oracle_tolerance_schedule(eps_d, L, N_r)
+    if v < 0:
+        raise ValueError("tolerance_schedule: bad arguments")
+    return v
+
+
+def gaussian(seed, count):
+    out = np.empty(count, dtype=np.float64)
+    _check(lib().oracle_gaussian(C.c_uint64(seed & (2**64 - 1)), count, _d(out)))
+    return out
+
+
+def mt19937_64(seed, count):
+    out = np.empty(count, dtype=np.uint64)
+    _check(lib().oracle_mt19937_64(C.c_uint64(seed & (2**64 - 1)), count,
+                                   out.ctypes.data_as(_u64p)))
+    return out
+
+
+def born_block(incident, adjoint_list, w, nu):
+    """incident N x nl (F-order), adjoint_list[d] N x nl -> block (nd*nl) x N."""
+    N, nl = incident.shape
+    inc = np.asfortranarray(incident, dtype=np.float64)
+    adj = [np.asfortranarray(a, dtype=np.float64) for a in adjoint_list]
+    arr = (_dp * len(adj))(*[_d(a) for a in adj])
+    out = np.empty((len(adj) * nl, N), dtype=np.float64)  # row-major
+    w = _f64(w)
+    _check(lib().oracle_born_block(N, nl, _d(inc), arr, len(adj), _d(w), nu, _d(out)))
+    return out
+
+
+def apply7(shape, h, sigma, sigmap, x):
+    nx, ny, nz = shape
+    x = _f64(x)
+    y = np.empty_like(x)
+    _check(lib().oracle_apply7(nx, ny, nz, h, sigma, sigmap, _d(x), _d(y)))
+    return y
+
+
+def fields(shape, h, sigma, sigmap, inv_D, rhs_vertex, tol=1e-10, max_iter=10000,
+           fixed_iters=0, threads=1):
+    nx, ny, nz = shape
+    N = nx * ny * nz
+    nl = len(sigma)
+    rv = np.ascontiguousarray(rhs_vertex, dtype=np.int64)
+    out = np.empty((N, len(rv) * nl), dtype=np.float64, order="F")
+    iters = np.zeros(len(rv) * nl, dtype=np.int32)
+    rel = np.zeros(len(rv) * nl, dtype=np.float64)
+    _check(lib().oracle_fields(nx, ny, nz, h, nl, _d(_f64(sigma)), _d(_f64(sigmap)),
+                               _d(_f64(inv_D)), rv.ctypes.data_as(_i64p), len(rv), tol, max_iter,
+                               fixed_iters, threads, _d(out), iters.ctypes.data_as(_ip),
+                               _d(rel)))
+    return out, iters, rel
+
+
+class Factor:
+    """LowRankFactor (lowrank.hpp:25-36) held by the oracle."""
+
+    def __init__(self, handle):
+        self.h = C.c_void_p(handle)
+        r, c, k = C.c_int64(), C.c_int64(), C.c_int64()
+        tol, meth, flag = C.c_double(), C.c_int(), C.c_int()
+        lib().oracle_factor_info(self.h, C.byref(r), C.byref(c), C.byref(k), C.byref(tol),
+                                 C.byref(meth), C.byref(flag))
+        self.rows, self.cols, self.rank = r.value, c.value, k.value
+        self.tol, self.method, self.flagged = tol.value, meth.value, bool(flag.value)
+        U = np.empty((self.rows, self.rank), order="F")
+        V = np.empty((self.cols, self.rank), order="F")
+        lib().oracle_factor_get(self.h, _d(U), _d(V))
+        self.U, self.V = U, V
+        plen = lib().oracle_factor_perm_len(self.h)
+        self.row_perm = np.zeros(plen, dtype=np.int32)
+        self.ledger = np.zeros(5)
+        lib().oracle_factor_meta(self.h, self.row_perm.ctypes.data_as(_ip), None, None,
+                                 _d(self.ledger))
+
+    @classmethod
+    def make(cls, U, V, tol=0.0, method=0, flagged=False):
+        U = np.asfortranarray(U, dtype=np.float64)
+        V = np.asfortranarray(V, dtype=np.float64)
+        h = lib().oracle_factor_make(_d(U), _d(V), U.shape[0], V.shape[0], U.shape[1], tol,
+                                     method, int(flagged))
+        return cls(h)
+
+    def dense(self):
+        return self.U @ self.V.T
+
+    def __del__(self):
+        try:
+            lib().oracle_factor_free(self.h)
+        except Exception:
+            pass
+
+
+def randsvd(A, eps, p=20, kprobe=10, seed=0, cat=OTHER, r0=1):
+    A = np.asfortranarray(A, dtype=np.float64)
+    h = C.c_void_p()
+    m, n = A.shape
+    _check(lib().oracle_randsvd(_d(A), m, n, max(m, 1), eps, p, kprobe,
+                                C.c_uint64(seed & (2**64 - 1)), cat, r0, C.byref(h)))
+    return Factor(h.value)
+
+
+def agglomerate(f1, f2, eps, seed=0, rank_hint=-1, p=20, kprobe=10):
+    h = C.c_void_p()
+    _check(lib().oracle_agglomerate(f1.h, f2.h, eps, C.c_uint64(seed & (2**64 - 1)), rank_hint,
+                                    p, kprobe, C.byref(h)))
+    return Factor(h.value)
+
+
+def recompress(f, eps, rank=-1):
+    h = C.c_void_p()
+    _check(lib().oracle_recompress(f.h, eps, rank, C.byref(h)))
+    return Factor(h.value)
+
+
+class ClusterTree:
+    def __init__(self, positions, lo, hi):
+        P = np.asfortranarray(positions, dtype=np.float64)
+        if P.ndim == 1:
+            P = P.reshape(-1, 1, order="F")
+        n, d = P.shape
+        h = C.c_void_p()
+        _check(lib().oracle_build_cluster_tree(_d(P), n, d, _d(_f64(lo)), _d(_f64(hi)),
+                                               C.byref(h)))
+        self.h = h
+        L = lib()
+        self.root = L.oracle_tree_root(h)
+        self.nodes = []
+        for v in range(L.oracle_tree_num_nodes(h)):
+            l, r, k = C.c_int(), C.c_int(), C.c_int()
+            L.oracle_tree_node(h, v, C.byref(l), C.byref(r), C.byref(k))
+            idx = np.zeros(k.value, dtype=np.int32)
+            L.oracle_tree_node_idx(h, v, idx.ctypes.data_as(_ip))
+            self.nodes.append(dict(left=l.value, right=r.value, idx=idx.tolist()))
+        self._n = n
+
+    def depth(self):
+        return lib().oracle_tree_depth(self.h)
+
+    def leaf_order(self):
+        out = np.zeros(self._n, dtype=np.int32)
+        lib().oracle_tree_leaf_order(self.h, out.ctypes.data_as(_ip))
+        return out.tolist()
+
+    def __del__(self):
+        try:
+            lib().oracle_tree_free(self.h)
+        except Exception:
+            pass
+
+
+class RecResult:
+    def __init__(self, handle, n_nodes):
+        self.factor = Factor(handle)
+        self.node_rank = np.zeros(n_nodes, dtype=np.int32)
+        self.node_depth = np.zeros(n_nodes, dtype=np.int32)
+        lib().oracle_factor_meta(self.factor.h, None, self.node_rank.ctypes.data_as(_ip),
+                                 self.node_depth.ctypes.data_as(_ip), None)
+        self.row_perm = self.factor.row_perm
+        self.ledger = self.factor.ledger
+
+
+def recursive_lowrank(tree, eps, H, rows_per, seed=0, p=20, kprobe=10):
+    H = np.asfortranarray(H, dtype=np.float64)
+    M, N = H.shape
+    h = C.c_void_p()
+    _check(lib().oracle_recursive_lowrank(tree.h, eps, _d(H), M, N, M, rows_per,
+                                          C.c_uint64(seed & (2**64 - 1)), p, kprobe,
+                                          C.byref(h)))
+    return RecResult(h.value, len(tree.nodes))
+
+
+def recursive_lowrank_born(tree, eps, incident, adjoint, w, nu, seed=0, p=20, kprobe=10):
+    """incident[s]: N x nl; adjoint[s][d]: N x nl (F-order arrays)."""
+    ns = len(incident)
+    nd = len(adjoint[0])
+    N, nl = incident[0].shape
+    inc = [np.asfortranarray(a, dtype=np.float64) for a in incident]
+    adj = [np.asfortranarray(a, dtype=np.float64) for s in range(ns) for a in adjoint[s]]
+    ia = (_dp * ns)(*[_d(a) for a in inc])
+    aa = (_dp * len(adj))(*[_d(a) for a in adj])
+    h = C.c_void_p()
+    _check(lib().oracle_recursive_lowrank_born(tree.h, eps, N, nl, nd, ia, aa, _d(_f64(w)), nu,
+                                               C.c_uint64(seed & (2**64 - 1)), p, kprobe,
+                                               C.byref(h)))
+    return RecResult(h.value, len(tree.nodes))
+
+
+def lr_matmat(f, X, trans=False):
+    X = np.asfortranarray(X, dtype=np.float64)
+    if X.ndim == 1:
+        X = X.reshape(-1, 1, order="F")
+    b = X.shape[1]
+    out = np.empty((f.cols if trans else f.rows, b), order="F")
+    _check(lib().oracle_lr_matmat(f.h, int(trans), b, _d(X), _d(out)))
+    return out
+
+
+def j_matmat(f, X, row_perm, eps_c, trans=False):
+    """eps_c: nl x nc (F-order).  trans=0: X (N*nc) x b -> M x b."""
+    eps_c = np.asfortranarray(eps_c, dtype=np.float64)
+    nl, nc = eps_c.shape
+    X = np.asfortranarray(X, dtype=np.float64)
+    if X.ndim == 1:
+        X = X.reshape(-1, 1, order="F")
+    b = X.shape[1]
+    rp = np.ascontiguousarray(row_perm, dtype=np.int32)
+    out = np.empty((f.cols * nc if trans else f.rows, b), order="F")
+    _check(lib().oracle_j_matmat(f.h, int(trans), b, rp.ctypes.data_as(_ip), _d(eps_c), nl, nc,
+                                 _d(X), _d(out)))
+    return out
+
+
+def fast_thin_svd(A):
+    A = np.asfortranarray(A, dtype=np.float64)
+    m, n = A.shape
+    k = min(m, n)
+    U = np.empty((m, k), order="F")
+    s = np.empty(k)
+    V = np.empty((n, k), order="F")
+    _check(lib().oracle_fast_thin_svd(_d(A), m, n, _d(U), _d(s), _d(V)))
+    return U, s, V
