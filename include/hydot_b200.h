@@ -1,0 +1,257 @@
+/* hydot_b200.h -- C ABI of the B200-native hydot hot path.
+ *
+ * Drop-in boundary for the reference's Born -> low-rank -> matvec path
+ * (/root/reference/proj, arXiv 1410.0986).  Every entry point names the
+ * reference interface it replaces (file:line, relative to /root/reference).
+ * Plain pointers and sizes only: no Eigen, no torch types.
+ *
+ * Conventions
+ *  - Matrices are column-major doubles with an explicit leading dimension,
+ *    like Eigen::MatrixXd (proj/include/hydot/grid.hpp:12-14), unless a
+ *    parameter says "row-major".
+ *  - "_dev" pointers are device (cudaMalloc) memory on the context's GPU;
+ *    "_h" pointers are host memory.  No borrowed pointer is retained after a
+ *    call returns.
+ *  - Every call is stream-ordered on the context's stream and synchronous
+ *    from the caller's view for its host outputs.
+ *  - Errors: a status code; hydot_last_error(ctx) returns the message.
+ *    HYDOT_EINVAL  <-> std::invalid_argument in the reference,
+ *    HYDOT_ERUNTIME<-> std::runtime_error (messages keep the reference
+ *    prefixes, e.g. "recursive_lowrank at node v: ", lowrank.cpp:503-506).
+ */
+#ifndef HYDOT_B200_H
+#define HYDOT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HYDOT_OK = 0,
+    HYDOT_EINVAL = 1,   /* std::invalid_argument */
+    HYDOT_ERUNTIME = 2, /* std::runtime_error */
+    HYDOT_ENOMEM = 3,
+    HYDOT_ECUDA = 4,
+    HYDOT_ENCCL = 5
+} hydot_status;
+
+typedef struct hydot_ctx_s* hydot_ctx;
+typedef struct hydot_factor_s* hydot_factor;
+typedef struct hydot_tree_s* hydot_tree;
+
+/* lowrank::Method (proj/include/hydot/lowrank.hpp:14-22) */
+enum {
+    HYDOT_METHOD_NONE = 0,
+    HYDOT_METHOD_RANDSVD = 1,
+    HYDOT_METHOD_ACA_FULL = 2,
+    HYDOT_METHOD_ACA_PARTIAL = 3,
+    HYDOT_METHOD_AGGLOMERATE = 4,
+    HYDOT_METHOD_RECURSIVE = 5,
+    HYDOT_METHOD_RECOMPRESS = 6
+};
+
+/* lowrank::FlopCategory (lowrank.hpp:54) */
+enum { HYDOT_CAT_LEAF = 0, HYDOT_CAT_AGGLOMERATION = 1, HYDOT_CAT_RECOMPRESS = 2, HYDOT_CAT_OTHER = 3 };
+
+/* lowrank::FlopLedger (lowrank.hpp:38-52) */
+typedef struct {
+    double leaf, agglomeration, recompress, other, kernel_tally;
+} hydot_ledger;
+
+/* ------------------------------------------------------------ context -- */
+int hydot_version(void);
+hydot_status hydot_ctx_create(int device, hydot_ctx* out);
+hydot_status hydot_ctx_destroy(hydot_ctx ctx);
+const char* hydot_last_error(hydot_ctx ctx);
+/* run on a caller-owned cudaStream_t (NULL = the legacy default stream, e.g.
+ * torch's default stream); the context starts on its own stream. */
+hydot_status hydot_ctx_set_stream(hydot_ctx ctx, void* cuda_stream);
+hydot_status hydot_ctx_synchronize(hydot_ctx ctx);
+/* number of kernels this context launched so far (evidence counter) */
+int64_t hydot_ctx_launch_count(hydot_ctx ctx);
+
+/* ------------------------------------------------------------- fields -- */
+/* 7-point vertex-centred FV operator on an nx*ny*nz vertex grid (spacing h,
+ * x-fastest n = ix + nx*(iy + ny*iz), grid.hpp:22-28); side faces Dirichlet,
+ * z faces Robin (grid.hpp:18-21).  Replaces the FEM K/M/R of
+ * grid.cpp:112-174 per BASELINE.json. */
+typedef struct {
+    int nx, ny, nz;
+    double h;
+} hydot_grid7;
+
+/* Fields for unit-vertex sources: replaces born::compute_fields
+ * (born.hpp:54-56, born.cpp:39-80; solver krylov::solve_family,
+ * krylov.cpp:400-463) by batched matrix-free CG on the SPD systems
+ * (K + sigma_l M + sigma'_l R) x = e_v, then x *= inv_D[l] (born.cpp:62-63).
+ * out_dev: N x (n_rhs*n_lambda), column k*n_lambda + l, ld = N.
+ * fixed_iters > 0 runs exactly that many iterations (parity mode).
+ * iters_h / relres_h (optional): per system. */
+hydot_status hydot_fields_solve(hydot_ctx ctx, const hydot_grid7* grid, int n_lambda,
+                                const double* sigma_h, const double* sigma_prime_h,
+                                const double* inv_D_h, const int64_t* rhs_vertex_h, int n_rhs,
+                                double tol, int max_iter, int fixed_iters, double* out_dev,
+                                int* iters_h, double* relres_h);
+
+/* y = A_l x for one shift (the operator the CG applies; for tests). */
+hydot_status hydot_apply7(hydot_ctx ctx, const hydot_grid7* grid, double sigma,
+                          double sigma_prime, const double* x_dev, double* y_dev);
+
+/* --------------------------------------------------------------- born -- */
+/* born::assemble_H_block (born.hpp:61-62, born.cpp:82-98):
+ *   out[(d*n_lambda + l)*ld + v] = (-nu) * ((phi_d[v,l] * phi_s[v,l]) * w[v])
+ * i.e. the (n_det*n_lambda) x N block stored ROW-major (rows contiguous over
+ * voxels; the save_block file order, born.cpp:156-167).
+ * incident_dev: N x n_lambda (ld N); adjoint_dev_h: host array of n_det
+ * device pointers, each N x n_lambda. */
+hydot_status hydot_born_block(hydot_ctx ctx, int64_t N, int n_lambda, const double* incident_dev,
+                              const double* const* adjoint_dev_h, int n_det, const double* w_dev,
+                              double nu, double* out_dev, int64_t ld);
+
+/* --------------------------------------------------------- generator -- */
+/* The Gaussian stream of randsvd (lowrank.cpp:136-143): deviates
+ * [offset, offset+count) of std::normal_distribution<double> (libstdc++
+ * polar method) driven by std::mt19937_64(seed), generated on the GPU with
+ * MT19937-64 jump-ahead. */
+hydot_status hydot_gaussian(hydot_ctx ctx, uint64_t seed, int64_t offset, int64_t count,
+                            double* out_dev);
+/* raw tempered engine outputs [offset, offset+count) */
+hydot_status hydot_mt19937_64(hydot_ctx ctx, uint64_t seed, int64_t offset, int64_t count,
+                              uint64_t* out_dev);
+/* host-only self check of the jump-ahead tables against a sequential
+ * engine (no GPU needed); returns HYDOT_OK when they agree. */
+hydot_status hydot_rng_selftest(void);
+
+/* ------------------------------------------------------------- factor -- */
+/* lowrank::LowRankFactor (lowrank.hpp:25-36), device resident: U rows x r,
+ * V cols x r (column-major), singular values folded into V. */
+hydot_status hydot_factor_create(hydot_ctx ctx, int64_t rows, int64_t cols, int64_t rank,
+                                 const double* U, int64_t ldu, const double* V, int64_t ldv,
+                                 int from_host, double tol, int method, int flagged,
+                                 hydot_factor* out);
+hydot_status hydot_factor_info(hydot_factor f, int64_t* rows, int64_t* cols, int64_t* rank,
+                               double* tol, int* method, int* flagged);
+/* copy U (rows x r) and V (cols x r) out; to_host selects host/device dst */
+hydot_status hydot_factor_download(hydot_ctx ctx, hydot_factor f, double* U, double* V,
+                                   int to_host);
+hydot_status hydot_factor_device_ptrs(hydot_factor f, const double** U_dev, const double** V_dev);
+void hydot_factor_free(hydot_factor f);
+
+/* ------------------------------------------------------------ lowrank -- */
+/* lowrank::randsvd (lowrank.hpp:70-72, lowrank.cpp:131-199) on a dense
+ * device operator A (dense_op, lowrank.cpp:111-120) of m x n stored
+ * ROW-major (a_dev[i*lda + j]; lda >= n).  category: HYDOT_CAT_*. */
+hydot_status hydot_randsvd(hydot_ctx ctx, int64_t m, int64_t n, const double* a_dev, int64_t lda,
+                           double eps, int p, int kprobe, uint64_t seed, int category, int r0,
+                           hydot_factor* out, hydot_ledger* ledger_h);
+
+/* lowrank::agglomerate (lowrank.hpp:98-100, lowrank.cpp:321-359); the
+ * reference hard-codes p=20, kprobe=10 (lowrank.cpp:344). */
+hydot_status hydot_agglomerate(hydot_ctx ctx, hydot_factor f1, hydot_factor f2, double eps,
+                               uint64_t seed, int rank_hint, int p, int kprobe,
+                               hydot_factor* out, hydot_ledger* ledger_h);
+
+/* lowrank::tolerance_schedule (lowrank.cpp:540-545) */
+hydot_status hydot_tolerance_schedule(double eps_d, int L, int N_r, double* out);
+
+/* lowrank::build_cluster_tree / ClusterTree (lowrank.hpp:103-119,
+ * lowrank.cpp:361-438).  positions_h: n x d column-major. */
+hydot_status hydot_tree_build(const double* positions_h, int n, int d, const double* lo_h,
+                              const double* hi_h, hydot_tree* out);
+int hydot_tree_num_nodes(hydot_tree t);
+int hydot_tree_root(hydot_tree t);
+int hydot_tree_depth(hydot_tree t);
+/* node v: children (-1 for a leaf) and source count; idx_h may be NULL */
+hydot_status hydot_tree_node(hydot_tree t, int v, int* left, int* right, int* n_idx, int* idx_h);
+hydot_status hydot_tree_leaf_order(hydot_tree t, int* order_h);
+void hydot_tree_free(hydot_tree t);
+
+/* lowrank::BlockProvider (lowrank.hpp:122-126): fills the rows_per_source x
+ * cols block of source s ROW-major into out_dev (ld >= cols); returns 0 on
+ * success. */
+typedef int (*hydot_block_fn)(void* user, int source, double* out_dev, int64_t ld);
+typedef struct {
+    int rows_per_source;
+    int64_t cols;
+    hydot_block_fn block;
+    void* user;
+} hydot_provider;
+
+/* Built-in device provider forming Born blocks from resident fields
+ * (compress_H's provider, experiments.cpp:235-240, without a dense H):
+ * incident_dev_h[s] (N x n_lambda), adjoint_dev_h[s*n_det + d]. */
+typedef struct {
+    int64_t N;
+    int n_lambda, n_sources, n_det;
+    const double* const* incident_dev_h;
+    const double* const* adjoint_dev_h;
+    const double* w_dev;
+    double nu;
+} hydot_born_fields;
+
+/* RecursiveOptions (lowrank.hpp:128-131) + knobs the reference hard-codes
+ * (p=20, kprobe=10, lowrank.cpp:344,448).  hint_mode 0 = the reference's
+ * sequential warm-start chains (lowrank.cpp:466-471). */
+typedef struct {
+    uint64_t seed;
+    int p;
+    int kprobe;
+    int hint_mode;
+} hydot_rec_opts;
+
+/* lowrank::recursive_lowrank (lowrank.hpp:142-144, lowrank.cpp:459-521).
+ * Exactly one of provider / born must be non-NULL.  Outputs: factor (rows
+ * in leaf order), row_perm_h (M), node_rank_h / node_depth_h (num_nodes),
+ * ledger_h; any output pointer may be NULL. */
+hydot_status hydot_recursive_lowrank(hydot_ctx ctx, hydot_tree tree, double eps,
+                                     const hydot_provider* provider, const hydot_born_fields* born,
+                                     const hydot_rec_opts* opts, hydot_factor* out,
+                                     int* row_perm_h, int* node_rank_h, int* node_depth_h,
+                                     hydot_ledger* ledger_h);
+
+/* lowrank::recompress (lowrank.hpp:157-158, lowrank.cpp:547-587) */
+hydot_status hydot_recompress(hydot_ctx ctx, hydot_factor f, double eps, int rank,
+                              hydot_factor* out, hydot_ledger* ledger_h);
+
+/* lowrank::lr_matvec / lr_rmatvec (lowrank.cpp:589-599) on b columns:
+ * trans=0: Y (rows x b) = U (V^T X), X cols x b;  trans=1: Y = V (U^T X). */
+hydot_status hydot_lr_matmat(hydot_ctx ctx, hydot_factor f, int trans, int b, const double* X_dev,
+                             int64_t ldx, double* Y_dev, int64_t ldy);
+
+/* J~ = [E_1 H~, ..., E_nc H~] products with the measurement permutation
+ * (permuted_matvec, experiments.cpp:255-262) and the chromophore scaling
+ * (forward_measure, born.cpp:118-127; pals.cpp:124-135):
+ *  trans=0: X_dev (N*n_c) x b (chromophore-major blocks of N) ->
+ *           Y_dev (M x b): y[row_perm[i]] = sum_c eps_c[l, c] (U V^T x_c)[i],
+ *           l = row_perm[i] % n_lambda;
+ *  trans=1: X_dev (M x b) -> Y_dev (N*n_c) x b: y_c = V U^T gather(E_c x).
+ * row_perm_dev: M ints; eps_c_dev: n_lambda x n_c (column-major). */
+hydot_status hydot_j_matmat(hydot_ctx ctx, hydot_factor f, int trans, int b, const int* row_perm_dev,
+                            const double* eps_c_dev, int n_lambda, int n_c, const double* X_dev,
+                            int64_t ldx, double* Y_dev, int64_t ldy);
+
+/* Thin SVD of a dense device matrix (m x n column-major) by the path of
+ * fast_thin_svd (lowrank.cpp:62-93); U m x k, s k (host), V n x k,
+ * k = min(m,n).  Exposed for kernel-level parity tests. */
+hydot_status hydot_thin_svd(hydot_ctx ctx, int64_t m, int64_t n, const double* a_dev, int64_t lda,
+                            double* U_dev, double* s_h, double* V_dev);
+
+/* Householder QR (Eigen::HouseholderQR as used at lowrank.cpp:77-83,
+ * 564-566): R (n x n upper, device, ld n) and thin Q (m x n, device) of a
+ * device m x n matrix, m >= n. */
+hydot_status hydot_householder_qr(hydot_ctx ctx, int64_t m, int64_t n, const double* a_dev,
+                                  int64_t lda, double* R_dev, double* Q_dev);
+
+/* C = alpha op(A) op(B) + beta C, FP64 DMMA tensor-core GEMM (column-major;
+ * transa/transb 0 or 1).  The kernel behind every GEMM of the path. */
+hydot_status hydot_dgemm(hydot_ctx ctx, int transa, int transb, int64_t m, int64_t n, int64_t k,
+                         double alpha, const double* A_dev, int64_t lda, const double* B_dev,
+                         int64_t ldb, double beta, double* C_dev, int64_t ldc);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HYDOT_B200_H */

@@ -1,0 +1,142 @@
+"""Loader for the in-tree C-ABI library libhydot_b200.so (include/hydot_b200.h).
+
+There is no fallback: if the library is missing the import fails loudly with
+the build command.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhydot_b200.so")
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+_i64p = C.POINTER(C.c_int64)
+_vp = C.c_void_p
+
+HYDOT_OK, HYDOT_EINVAL, HYDOT_ERUNTIME, HYDOT_ENOMEM, HYDOT_ECUDA, HYDOT_ENCCL = range(6)
+
+
+class Grid7(C.Structure):
+    _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("h", C.c_double)]
+
+
+class Ledger(C.Structure):
+    _fields_ = [("leaf", C.c_double), ("agglomeration", C.c_double),
+                ("recompress", C.c_double), ("other", C.c_double),
+                ("kernel_tally", C.c_double)]
+
+    def category_total(self):
+        return self.leaf + self.agglomeration + self.recompress + self.other
+
+
+BLOCK_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, _dp, C.c_int64)
+
+
+class Provider(C.Structure):
+    _fields_ = [("rows_per_source", C.c_int), ("cols", C.c_int64), ("block", BLOCK_FN),
+                ("user", C.c_void_p)]
+
+
+class BornFields(C.Structure):
+    _fields_ = [("N", C.c_int64), ("n_lambda", C.c_int), ("n_sources", C.c_int),
+                ("n_det", C.c_int), ("incident_dev_h", C.POINTER(_dp)),
+                ("adjoint_dev_h", C.POINTER(_dp)), ("w_dev", _dp), ("nu", C.c_double)]
+
+
+class RecOpts(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("p", C.c_int), ("kprobe", C.c_int),
+                ("hint_mode", C.c_int)]
+
+
+# name -> (restype, argtypes); exactly the declarations of include/hydot_b200.h
+SIGNATURES = {
+    "hydot_version": (C.c_int, []),
+    "hydot_ctx_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+    "hydot_ctx_destroy": (C.c_int, [_vp]),
+    "hydot_last_error": (C.c_char_p, [_vp]),
+    "hydot_ctx_set_stream": (C.c_int, [_vp, _vp]),
+    "hydot_ctx_synchronize": (C.c_int, [_vp]),
+    "hydot_ctx_launch_count": (C.c_int64, [_vp]),
+    "hydot_fields_solve": (C.c_int, [_vp, C.POINTER(Grid7), C.c_int, _dp, _dp, _dp, _i64p, C.c_int,
+                                     C.c_double, C.c_int, C.c_int, _dp, _ip, _dp]),
+    "hydot_apply7": (C.c_int, [_vp, C.POINTER(Grid7), C.c_double, C.c_double, _dp, _dp]),
+    "hydot_born_block": (C.c_int, [_vp, C.c_int64, C.c_int, _dp, C.POINTER(_dp), C.c_int, _dp,
+                                   C.c_double, _dp, C.c_int64]),
+    "hydot_gaussian": (C.c_int, [_vp, C.c_uint64, C.c_int64, C.c_int64, _dp]),
+    "hydot_mt19937_64": (C.c_int, [_vp, C.c_uint64, C.c_int64, C.c_int64, C.c_void_p]),
+    "hydot_rng_selftest": (C.c_int, []),
+    "hydot_factor_create": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, _dp, C.c_int64, _dp,
+                                      C.c_int64, C.c_int, C.c_double, C.c_int, C.c_int,
+                                      C.POINTER(_vp)]),
+    "hydot_factor_info": (C.c_int, [_vp, _i64p, _i64p, _i64p, _dp, _ip, _ip]),
+    "hydot_factor_download": (C.c_int, [_vp, _vp, _dp, _dp, C.c_int]),
+    "hydot_factor_device_ptrs": (C.c_int, [_vp, C.POINTER(_dp), C.POINTER(_dp)]),
+    "hydot_factor_free": (None, [_vp]),
+    "hydot_randsvd": (C.c_int, [_vp, C.c_int64, C.c_int64, _dp, C.c_int64, C.c_double, C.c_int,
+                                C.c_int, C.c_uint64, C.c_int, C.c_int, C.POINTER(_vp),
+                                C.POINTER(Ledger)]),
+    "hydot_agglomerate": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_uint64, C.c_int, C.c_int,
+                                    C.c_int, C.POINTER(_vp), C.POINTER(Ledger)]),
+    "hydot_tolerance_schedule": (C.c_int, [C.c_double, C.c_int, C.c_int, _dp]),
+    "hydot_tree_build": (C.c_int, [_dp, C.c_int, C.c_int, _dp, _dp, C.POINTER(_vp)]),
+    "hydot_tree_num_nodes": (C.c_int, [_vp]),
+    "hydot_tree_root": (C.c_int, [_vp]),
+    "hydot_tree_depth": (C.c_int, [_vp]),
+    "hydot_tree_node": (C.c_int, [_vp, C.c_int, _ip, _ip, _ip, _ip]),
+    "hydot_tree_leaf_order": (C.c_int, [_vp, _ip]),
+    "hydot_tree_free": (None, [_vp]),
+    "hydot_recursive_lowrank": (C.c_int, [_vp, _vp, C.c_double, C.POINTER(Provider),
+                                          C.POINTER(BornFields), C.POINTER(RecOpts),
+                                          C.POINTER(_vp), _ip, _ip, _ip, C.POINTER(Ledger)]),
+    "hydot_recompress": (C.c_int, [_vp, _vp, C.c_double, C.c_int, C.POINTER(_vp),
+                                   C.POINTER(Ledger)]),
+    "hydot_lr_matmat": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _dp, C.c_int64, _dp, C.c_int64]),
+    "hydot_j_matmat": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _ip, _dp, C.c_int, C.c_int, _dp,
+                                 C.c_int64, _dp, C.c_int64]),
+    "hydot_thin_svd": (C.c_int, [_vp, C.c_int64, C.c_int64, _dp, C.c_int64, _dp, _dp, _dp]),
+    "hydot_householder_qr": (C.c_int, [_vp, C.c_int64, C.c_int64, _dp, C.c_int64, _dp, _dp]),
+    "hydot_dgemm": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_double,
+                              _dp, C.c_int64, _dp, C.c_int64, C.c_double, _dp, C.c_int64]),
+}
+
+_LIB = None
+
+
+def build():
+    import subprocess
+    subprocess.run(["make", "-s", "-j8", "-C", os.path.join(_HERE, "csrc")], check=True)
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build the CUDA extension first "
+                "(python -c 'import __graft_entry__ as g; g.build()' or make -C "
+                "paper_1410_0986_b200/csrc).  There is no CPU fallback.")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = L
+    return _LIB
+
+
+class HydotError(RuntimeError):
+    pass
+
+
+def check(rc, ctx=None):
+    if rc == HYDOT_OK:
+        return
+    msg = lib().hydot_last_error(ctx).decode(errors="replace")
+    if rc == HYDOT_EINVAL:
+        raise ValueError(msg)
+    if rc == HYDOT_ENOMEM:
+        raise MemoryError(msg)
+    raise HydotError(f"[status {rc}] {msg}")

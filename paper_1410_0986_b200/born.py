@@ -1,0 +1,113 @@
+"""hydot::born on the B200 (mirror of proj/include/hydot/born.hpp).
+
+Fields come from the batched matrix-free 7-point CG (hydot_fields_solve);
+Born blocks from the Hadamard kernel (hydot_born_block).  Device tensors are
+row-major torch float64 tensors: a field set of one point is (n_lambda, N)
+(each wavelength row voxel-contiguous, i.e. the reference's N x N_lambda
+column-major Mat), a Born block is (n_det*n_lambda, N).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, lib
+from .core import Context, dptr
+
+
+@dataclass
+class Grid7:
+    """Vertex grid, x-fastest (grid.hpp:22-28), spacing h; side faces
+    Dirichlet, z faces Robin (grid.hpp:18-21)."""
+    nx: int
+    ny: int
+    nz: int
+    h: float
+
+    @property
+    def N(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    def index(self, ix, iy, iz) -> int:
+        return ix + self.nx * (iy + self.ny * iz)
+
+    def c(self):
+        return _lib.Grid7(self.nx, self.ny, self.nz, self.h)
+
+
+@dataclass
+class FieldStats:
+    iters: np.ndarray
+    relres: np.ndarray
+
+
+def compute_fields(ctx: Context, grid: Grid7, sigma, sigma_prime, inv_D, points: Sequence[int],
+                   tol: float = 1e-10, max_iter: int = 20000, fixed_iters: int = 0,
+                   out: torch.Tensor = None):
+    """Fields of unit point sources at vertex ids `points` for every
+    wavelength: returns (len(points), n_lambda, N) = x_l / D_l with
+    (K + sigma_l M + sigma'_l R) x_l = e_v (born.cpp:39-80, born.cpp:62-63).
+    Raises HydotError when a system misses tol (born.cpp:58-61)."""
+    sig = np.ascontiguousarray(sigma, dtype=np.float64)
+    sigp = np.ascontiguousarray(sigma_prime, dtype=np.float64)
+    invd = np.ascontiguousarray(inv_D, dtype=np.float64)
+    nl = sig.size
+    if nl == 0:
+        raise ValueError("compute_fields: no wavelengths")
+    pts = np.ascontiguousarray(points, dtype=np.int64)
+    if out is None:
+        out = ctx.empty(len(pts), nl, grid.N)
+    iters = np.zeros(len(pts) * nl, dtype=np.int32)
+    rel = np.zeros(len(pts) * nl, dtype=np.float64)
+    g = grid.c()
+    dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+    check(lib().hydot_fields_solve(ctx.h, C.byref(g), nl, dp(sig), dp(sigp), dp(invd),
+                                   pts.ctypes.data_as(C.POINTER(C.c_int64)), len(pts), tol,
+                                   max_iter, fixed_iters, dptr(out),
+                                   iters.ctypes.data_as(C.POINTER(C.c_int)), dp(rel)), ctx.h)
+    return out, FieldStats(iters.reshape(len(pts), nl), rel.reshape(len(pts), nl))
+
+
+def apply_operator(ctx: Context, grid: Grid7, sigma: float, sigma_prime: float,
+                   x: torch.Tensor) -> torch.Tensor:
+    y = torch.empty_like(x)
+    g = grid.c()
+    check(lib().hydot_apply7(ctx.h, C.byref(g), sigma, sigma_prime, dptr(x), dptr(y)), ctx.h)
+    return y
+
+
+def assemble_H_block(ctx: Context, incident: torch.Tensor, adjoint: List[torch.Tensor],
+                     lumped_w: torch.Tensor, nu: float = 1.0, out: torch.Tensor = None):
+    """assemble_H_block (born.hpp:61-62, born.cpp:82-98): rows (d*nl + l) =
+    (-nu) * phi_d[:, l] .* phi_s[:, l] .* w.  incident (nl, N), adjoint[d]
+    (nl, N) CUDA tensors; returns (n_det*nl, N)."""
+    nl, N = incident.shape
+    nd = len(adjoint)
+    if lumped_w.numel() != N:
+        raise ValueError("assemble_H_block: weight size mismatch")
+    for a in adjoint:
+        if tuple(a.shape) != (nl, N):
+            raise ValueError("assemble_H_block: adjoint field shape mismatch")
+    if out is None:
+        out = ctx.empty(nd * nl, N)
+    arr = (_lib._dp * max(nd, 1))(*[dptr(a) for a in adjoint])
+    check(lib().hydot_born_block(ctx.h, N, nl, dptr(incident.contiguous()), arr, nd,
+                                 dptr(lumped_w.contiguous()), nu, dptr(out), out.stride(0)), ctx.h)
+    return out
+
+
+def assemble_H_dense(ctx: Context, incident: List[torch.Tensor], adjoint: List[List[torch.Tensor]],
+                     lumped_w: torch.Tensor, nu: float = 1.0) -> torch.Tensor:
+    """All blocks stacked in source order (born.cpp:100-108; fixture scale)."""
+    nl, N = incident[0].shape
+    nd = len(adjoint[0])
+    H = ctx.empty(len(incident) * nd * nl, N)
+    for s in range(len(incident)):
+        assemble_H_block(ctx, incident[s], adjoint[s], lumped_w, nu,
+                         out=H[s * nd * nl:(s + 1) * nd * nl])
+    return H

@@ -1,0 +1,154 @@
+"""Seeded synthetic inputs for the BASELINE.json configurations (host side).
+
+BASELINE.json configs 0-4 fix the distributions, not the draws; this module
+pins them: numpy Generator(seed 20240811), draw order spectra
+(chromophore-major, Gaussian-major: centre U[650,950], width U[30,80],
+amplitude U[0.1,1]) then concentrations C_c = U[0.5,1.5] x 0.01.
+Physics: D = 1/(3(mu_a + mu_s')), mu_s' = (lambda/800)^-1.3,
+sigma = mu_a/D, sigma' = 1/(2D), inv_D = 1/D, nu = 1, Born weight w = h^3.
+Sources: cell-centred lattice on the top plane z=0 snapped to vertices;
+detectors: the N_ds nearest points (x,y Euclidean, ties by lattice index) of
+a bottom-plane lattice of pitch 3h.  All synthetic (no dataset exists).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+SEED = 20240811
+
+
+@dataclass
+class Config:
+    name: str
+    n: int
+    ns_x: int
+    ns_y: int
+    n_det: int
+    n_lambda: int
+    n_chrom: int = 4
+    h: float = 2.0
+    eps_d: float = 1e-6
+    seed: int = SEED
+
+    @property
+    def N(self):
+        return self.n ** 3
+
+    @property
+    def n_sources(self):
+        return self.ns_x * self.ns_y
+
+    @property
+    def rows_per_source(self):
+        return self.n_det * self.n_lambda
+
+    @property
+    def M(self):
+        return self.n_sources * self.rows_per_source
+
+
+CONFIGS = {
+    0: Config("cfg0", 32, 4, 2, 4, 20),
+    1: Config("cfg1", 48, 4, 4, 6, 50),
+    2: Config("cfg2", 64, 8, 4, 8, 100),
+    3: Config("cfg3", 100, 8, 8, 10, 200),
+}
+
+
+def small_config(n=12, ns_x=2, ns_y=2, n_det=2, n_lambda=4):
+    """Fixture-scale setup with the same recipe (for parity tests)."""
+    return Config(f"small{n}", n, ns_x, ns_y, n_det, n_lambda)
+
+
+@dataclass
+class Setup:
+    cfg: Config
+    wavelengths: np.ndarray
+    eps_c: np.ndarray        # n_lambda x n_chrom (extinction per wavelength)
+    conc: np.ndarray         # n_chrom background concentrations
+    sigma: np.ndarray
+    sigma_prime: np.ndarray
+    inv_D: np.ndarray
+    source_vertex: np.ndarray      # n_sources
+    source_xy: np.ndarray          # n_sources x 2 (mm, for the cluster tree)
+    detector_vertex: np.ndarray    # n_sources x n_det
+    points: np.ndarray             # unique field points (sources then detectors)
+    source_point: np.ndarray       # index into points per source
+    detector_point: np.ndarray     # n_sources x n_det indices into points
+    box_lo: np.ndarray = field(default_factory=lambda: np.zeros(2))
+    box_hi: np.ndarray = field(default_factory=lambda: np.zeros(2))
+
+    @property
+    def w(self):
+        return np.full(self.cfg.N, self.cfg.h ** 3)
+
+    def grid(self):
+        from .born import Grid7
+        n = self.cfg.n
+        return Grid7(n, n, n, self.cfg.h)
+
+
+def make_setup(cfg: Config) -> Setup:
+    rng = np.random.default_rng(cfg.seed)
+    nl, nc, n, h = cfg.n_lambda, cfg.n_chrom, cfg.n, cfg.h
+    lam = 650.0 + 300.0 * np.arange(nl) / max(nl - 1, 1)
+    eps_c = np.zeros((nl, nc))
+    for c in range(nc):
+        for _ in range(3):
+            centre = rng.uniform(650.0, 950.0)
+            width = rng.uniform(30.0, 80.0)
+            amp = rng.uniform(0.1, 1.0)
+            eps_c[:, c] += amp * np.exp(-0.5 * ((lam - centre) / width) ** 2)
+    conc = rng.uniform(0.5, 1.5, size=nc) * 0.01
+    mu_a = eps_c @ conc
+    mu_s = (lam / 800.0) ** -1.3
+    D = 1.0 / (3.0 * (mu_a + mu_s))
+    sigma = mu_a / D
+    sigma_p = 1.0 / (2.0 * D)
+    inv_D = 1.0 / D
+
+    def idx(ix, iy, iz):
+        return ix + n * (iy + n * iz)
+
+    # sources: cell-centred lattice on z = 0, interior in x, y
+    src_v, src_xy = [], []
+    for j in range(cfg.ns_y):
+        for i in range(cfg.ns_x):
+            ix = int(np.clip(round((i + 0.5) * (n - 1) / cfg.ns_x), 1, n - 2))
+            iy = int(np.clip(round((j + 0.5) * (n - 1) / cfg.ns_y), 1, n - 2))
+            src_v.append(idx(ix, iy, 0))
+            src_xy.append((ix * h - (n - 1) * h / 2, iy * h - (n - 1) * h / 2))
+    # detectors: bottom-plane lattice of pitch 3 vertices, N_ds nearest
+    lat = np.arange(1, n - 1, 3)
+    det_lat = [(ix, iy) for iy in lat for ix in lat]
+    det_v = []
+    for s in range(cfg.n_sources):
+        sx = src_v[s] % n
+        sy = (src_v[s] // n) % n
+        d2 = [((ix - sx) ** 2 + (iy - sy) ** 2, k) for k, (ix, iy) in enumerate(det_lat)]
+        d2.sort()
+        det_v.append([idx(*det_lat[k], n - 1) for _, k in d2[: cfg.n_det]])
+    det_v = np.array(det_v, dtype=np.int64)
+    # unique field points (detectors shared between sources are solved once;
+    # identical systems give identical fields, so this is exact)
+    points, where = [], {}
+    for v in list(src_v) + list(det_v.reshape(-1)):
+        if v not in where:
+            where[v] = len(points)
+            points.append(v)
+    src_pt = np.array([where[v] for v in src_v], dtype=np.int64)
+    det_pt = np.array([[where[v] for v in row] for row in det_v], dtype=np.int64)
+    half = (n - 1) * h / 2
+    return Setup(cfg, lam, eps_c, conc, sigma, sigma_p, inv_D, np.array(src_v, dtype=np.int64),
+                 np.array(src_xy), det_v, np.array(points, dtype=np.int64), src_pt, det_pt,
+                 np.array([-half, -half]), np.array([half, half]))
+
+
+def compression_tolerance(setup: Setup, tree_depth: int) -> float:
+    """Leaf/merge tolerance as compress_H computes it (experiments.cpp:230-233):
+    eps = tolerance_schedule(eps_d, L, min(M, N))."""
+    cfg = setup.cfg
+    Nr = min(cfg.M, cfg.N)
+    return cfg.eps_d / (2.0 ** (tree_depth / 2.0) * (tree_depth + 1) * np.sqrt(Nr))

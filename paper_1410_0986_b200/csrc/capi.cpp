@@ -1,0 +1,524 @@
+// capi.cpp -- the C ABI (include/hydot_b200.h) over the device drivers.
+// Status mapping keeps the reference's exception classes:
+// std::invalid_argument -> HYDOT_EINVAL, std::runtime_error -> HYDOT_ERUNTIME.
+#include <cstring>
+#include <mutex>
+
+#include "lowrank.h"
+
+using namespace hydot;
+
+struct hydot_ctx_s {
+    std::shared_ptr<Ctx> c;
+};
+struct hydot_factor_s {
+    std::shared_ptr<Ctx> owner;
+    Factor f;
+};
+struct hydot_tree_s {
+    Tree t;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+hydot_status guard(Ctx* c, F&& fn) {
+    std::string msg;
+    hydot_status st = HYDOT_OK;
+    try {
+        if (c) HYDOT_CUDA(cudaSetDevice(c->device));
+        fn();
+    } catch (const CudaError& e) {
+        msg = e.what();
+        st = HYDOT_ECUDA;
+    } catch (const std::bad_alloc&) {
+        msg = "out of device memory";
+        st = HYDOT_ENOMEM;
+    } catch (const std::invalid_argument& e) {
+        msg = e.what();
+        st = HYDOT_EINVAL;
+    } catch (const std::exception& e) {
+        msg = e.what();
+        st = HYDOT_ERUNTIME;
+    }
+    if (st != HYDOT_OK) {
+        if (c) c->err = msg;
+        g_err = msg;
+    }
+    return st;
+}
+
+Ctx& ctx_of(hydot_ctx ctx) {
+    if (!ctx || !ctx->c) throw std::invalid_argument("null hydot_ctx");
+    return *ctx->c;
+}
+
+void ledger_out(const Ledger& l, hydot_ledger* out) {
+    if (!out) return;
+    out->leaf += l.leaf;
+    out->agglomeration += l.agglomeration;
+    out->recompress += l.recompress;
+    out->other += l.other;
+    out->kernel_tally += l.kernel_tally;
+}
+
+hydot_factor wrap(const std::shared_ptr<Ctx>& owner, Factor&& f) {
+    auto* h = new hydot_factor_s;
+    h->owner = owner;
+    h->f = std::move(f);
+    return h;
+}
+}  // namespace
+
+extern "C" {
+
+int hydot_version(void) { return 1; }
+
+hydot_status hydot_ctx_create(int device, hydot_ctx* out) {
+    if (!out) return HYDOT_EINVAL;
+    *out = nullptr;
+    return guard(nullptr, [&] {
+        auto c = std::make_shared<Ctx>();
+        c->device = device;
+        HYDOT_CUDA(cudaSetDevice(device));
+        HYDOT_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+        c->stream = c->own_stream;
+        int sms = 0;
+        HYDOT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        c->num_sms = sms;
+        // keep freed pool memory cached (the path allocates per node)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        auto* h = new hydot_ctx_s;
+        h->c = c;
+        *out = h;
+    });
+}
+
+hydot_status hydot_ctx_destroy(hydot_ctx ctx) {
+    if (!ctx) return HYDOT_OK;
+    hydot_status st = guard(ctx->c.get(), [&] {
+        Ctx& c = *ctx->c;
+        c.sync();
+        if (c.pinned) cudaFreeHost(c.pinned);
+        c.pinned = nullptr;
+        if (c.jump_dev) cudaFree(c.jump_dev);
+        c.jump_dev = nullptr;
+    });
+    delete ctx;
+    return st;
+}
+
+const char* hydot_last_error(hydot_ctx ctx) {
+    if (ctx && ctx->c && !ctx->c->err.empty()) return ctx->c->err.c_str();
+    return g_err.c_str();
+}
+
+hydot_status hydot_ctx_set_stream(hydot_ctx ctx, void* s) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        c.sync();
+        c.stream = static_cast<cudaStream_t>(s);  // NULL = the legacy default stream
+    });
+}
+
+hydot_status hydot_ctx_synchronize(hydot_ctx ctx) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] { ctx_of(ctx).sync(); });
+}
+
+int64_t hydot_ctx_launch_count(hydot_ctx ctx) { return ctx && ctx->c ? ctx->c->launches : -1; }
+
+// ------------------------------------------------------------- fields ----
+hydot_status hydot_fields_solve(hydot_ctx ctx, const hydot_grid7* grid, int n_lambda,
+                                const double* sigma_h, const double* sigma_prime_h,
+                                const double* inv_D_h, const int64_t* rhs_vertex_h, int n_rhs,
+                                double tol, int max_iter, int fixed_iters, double* out_dev,
+                                int* iters_h, double* relres_h) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!grid || !sigma_h || !sigma_prime_h || !inv_D_h || !rhs_vertex_h || !out_dev)
+            throw std::invalid_argument("hydot_fields_solve: null argument");
+        CGStats st;
+        fields_solve(c, *grid, n_lambda, sigma_h, sigma_prime_h, inv_D_h, rhs_vertex_h, n_rhs, tol,
+                     max_iter, fixed_iters, out_dev, &st);
+        const int total = n_rhs * n_lambda;
+        if (iters_h) std::memcpy(iters_h, st.iters.data(), size_t(total) * sizeof(int));
+        if (relres_h) std::memcpy(relres_h, st.relres.data(), size_t(total) * sizeof(double));
+        if (fixed_iters <= 0)
+            for (int k = 0; k < total; ++k)
+                if (!(st.relres[size_t(k)] <= tol))
+                    throw std::runtime_error("field solve failed at rhs " + std::to_string(k / n_lambda) +
+                                             ", wavelength index " + std::to_string(k % n_lambda));
+    });
+}
+
+hydot_status hydot_apply7(hydot_ctx ctx, const hydot_grid7* grid, double sigma,
+                          double sigma_prime, const double* x_dev, double* y_dev) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!grid || !x_dev || !y_dev) throw std::invalid_argument("hydot_apply7: null argument");
+        apply7(c, *grid, sigma, sigma_prime, x_dev, y_dev);
+        c.sync();
+    });
+}
+
+// --------------------------------------------------------------- born ----
+hydot_status hydot_born_block(hydot_ctx ctx, int64_t N, int n_lambda, const double* incident_dev,
+                              const double* const* adjoint_dev_h, int n_det, const double* w_dev,
+                              double nu, double* out_dev, int64_t ld) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (N < 0 || n_lambda < 0 || n_det < 0) throw std::invalid_argument("assemble_H_block: negative size");
+        if (!incident_dev || !adjoint_dev_h || !w_dev || !out_dev)
+            throw std::invalid_argument("assemble_H_block: null argument");
+        born_block(c, N, n_lambda, incident_dev, adjoint_dev_h, n_det, w_dev, nu, out_dev, ld);
+        c.sync();
+    });
+}
+
+// ---------------------------------------------------------- generator ----
+hydot_status hydot_gaussian(hydot_ctx ctx, uint64_t seed, int64_t offset, int64_t count,
+                            double* out_dev) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (offset < 0 || count < 0) throw std::invalid_argument("hydot_gaussian: negative range");
+        if (count == 0) return;
+        RngStream rs(c, seed);
+        rs.fill(offset, count, out_dev);
+        c.sync();
+    });
+}
+
+hydot_status hydot_mt19937_64(hydot_ctx ctx, uint64_t seed, int64_t offset, int64_t count,
+                              uint64_t* out_dev) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (offset < 0 || count < 0) throw std::invalid_argument("hydot_mt19937_64: negative range");
+        RngStream rs(c, seed);
+        rs.raw(offset, count, out_dev);
+        c.sync();
+    });
+}
+
+hydot_status hydot_rng_selftest(void) {
+    return guard(nullptr, [&] {
+        if (!rng_selftest_host()) throw std::runtime_error("MT19937-64 jump-ahead self test failed");
+    });
+}
+
+// ------------------------------------------------------------- factor ----
+hydot_status hydot_factor_create(hydot_ctx ctx, int64_t rows, int64_t cols, int64_t rank,
+                                 const double* U, int64_t ldu, const double* V, int64_t ldv,
+                                 int from_host, double tol, int method, int flagged,
+                                 hydot_factor* out) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!out || rows < 0 || cols < 0 || rank < 0 || rank > std::min(rows, cols) ||
+            (rank > 0 && (!U || !V || ldu < rows || ldv < cols)))
+            throw std::invalid_argument("hydot_factor_create: bad dimensions");
+        Factor f;
+        f.rows = rows;
+        f.cols = cols;
+        f.rank = rank;
+        f.tol = tol;
+        f.method = method;
+        f.flagged = flagged != 0;
+        f.U = dalloc(c, size_t(std::max<int64_t>(rows * rank, 1)));
+        f.V = dalloc(c, size_t(std::max<int64_t>(cols * rank, 1)));
+        auto kind = from_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+        if (rank > 0) {
+            HYDOT_CUDA(cudaMemcpy2DAsync(f.U.d(), size_t(rows) * 8, U, size_t(ldu) * 8,
+                                         size_t(rows) * 8, size_t(rank), kind, c.stream));
+            HYDOT_CUDA(cudaMemcpy2DAsync(f.V.d(), size_t(cols) * 8, V, size_t(ldv) * 8,
+                                         size_t(cols) * 8, size_t(rank), kind, c.stream));
+        }
+        c.sync();
+        *out = wrap(ctx->c, std::move(f));
+    });
+}
+
+hydot_status hydot_factor_info(hydot_factor f, int64_t* rows, int64_t* cols, int64_t* rank,
+                               double* tol, int* method, int* flagged) {
+    if (!f) return HYDOT_EINVAL;
+    if (rows) *rows = f->f.rows;
+    if (cols) *cols = f->f.cols;
+    if (rank) *rank = f->f.rank;
+    if (tol) *tol = f->f.tol;
+    if (method) *method = f->f.method;
+    if (flagged) *flagged = f->f.flagged ? 1 : 0;
+    return HYDOT_OK;
+}
+
+hydot_status hydot_factor_download(hydot_ctx ctx, hydot_factor f, double* U, double* V,
+                                   int to_host) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!f) throw std::invalid_argument("null factor");
+        auto kind = to_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+        if (f->f.rank > 0) {
+            if (U)
+                HYDOT_CUDA(cudaMemcpyAsync(U, f->f.U.d(), size_t(f->f.rows * f->f.rank) * 8, kind,
+                                           c.stream));
+            if (V)
+                HYDOT_CUDA(cudaMemcpyAsync(V, f->f.V.d(), size_t(f->f.cols * f->f.rank) * 8, kind,
+                                           c.stream));
+        }
+        c.sync();
+    });
+}
+
+hydot_status hydot_factor_device_ptrs(hydot_factor f, const double** U_dev, const double** V_dev) {
+    if (!f) return HYDOT_EINVAL;
+    if (U_dev) *U_dev = f->f.U.d();
+    if (V_dev) *V_dev = f->f.V.d();
+    return HYDOT_OK;
+}
+
+void hydot_factor_free(hydot_factor f) {
+    if (!f) return;
+    if (f->owner) cudaSetDevice(f->owner->device);
+    delete f;
+}
+
+// ------------------------------------------------------------ lowrank ----
+hydot_status hydot_randsvd(hydot_ctx ctx, int64_t m, int64_t n, const double* a_dev, int64_t lda,
+                           double eps, int p, int kprobe, uint64_t seed, int category, int r0,
+                           hydot_factor* out, hydot_ledger* ledger_h) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!out || m < 0 || n < 0 || (m > 0 && n > 0 && (!a_dev || lda < n)))
+            throw std::invalid_argument("randsvd: bad operator");
+        Ledger l;
+        Factor f = randsvd(c, m, n, a_dev, lda, eps, p, kprobe, seed, &l, category, r0);
+        c.sync();
+        ledger_out(l, ledger_h);
+        *out = wrap(ctx->c, std::move(f));
+    });
+}
+
+hydot_status hydot_agglomerate(hydot_ctx ctx, hydot_factor f1, hydot_factor f2, double eps,
+                               uint64_t seed, int rank_hint, int p, int kprobe, hydot_factor* out,
+                               hydot_ledger* ledger_h) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!f1 || !f2 || !out) throw std::invalid_argument("agglomerate: null factor");
+        Ledger l;
+        Factor f = agglomerate(c, f1->f, f2->f, eps, seed, &l, rank_hint, p, kprobe);
+        c.sync();
+        ledger_out(l, ledger_h);
+        *out = wrap(ctx->c, std::move(f));
+    });
+}
+
+hydot_status hydot_tolerance_schedule(double eps_d, int L, int N_r, double* out) {
+    return guard(nullptr, [&] {
+        if (!out) throw std::invalid_argument("tolerance_schedule: null output");
+        *out = tolerance_schedule(eps_d, L, N_r);
+    });
+}
+
+hydot_status hydot_tree_build(const double* positions_h, int n, int d, const double* lo_h,
+                              const double* hi_h, hydot_tree* out) {
+    if (out) *out = nullptr;
+    return guard(nullptr, [&] {
+        if (!positions_h || !lo_h || !hi_h || !out)
+            throw std::invalid_argument("build_cluster_tree: null argument");
+        auto* t = new hydot_tree_s;
+        try {
+            t->t = build_cluster_tree(positions_h, n, d, lo_h, hi_h);
+        } catch (...) {
+            delete t;
+            throw;
+        }
+        *out = t;
+    });
+}
+int hydot_tree_num_nodes(hydot_tree t) { return t ? int(t->t.nodes.size()) : -1; }
+int hydot_tree_root(hydot_tree t) { return t ? t->t.root : -1; }
+int hydot_tree_depth(hydot_tree t) { return t ? t->t.depth() : -1; }
+hydot_status hydot_tree_node(hydot_tree t, int v, int* left, int* right, int* n_idx, int* idx_h) {
+    if (!t || v < 0 || v >= int(t->t.nodes.size())) return HYDOT_EINVAL;
+    const TreeNode& nd = t->t.nodes[size_t(v)];
+    if (left) *left = nd.left;
+    if (right) *right = nd.right;
+    if (n_idx) *n_idx = int(nd.idx.size());
+    if (idx_h) std::memcpy(idx_h, nd.idx.data(), nd.idx.size() * sizeof(int));
+    return HYDOT_OK;
+}
+hydot_status hydot_tree_leaf_order(hydot_tree t, int* order_h) {
+    if (!t || !order_h) return HYDOT_EINVAL;
+    auto o = t->t.leaf_order();
+    std::memcpy(order_h, o.data(), o.size() * sizeof(int));
+    return HYDOT_OK;
+}
+void hydot_tree_free(hydot_tree t) { delete t; }
+
+hydot_status hydot_recursive_lowrank(hydot_ctx ctx, hydot_tree tree, double eps,
+                                     const hydot_provider* provider, const hydot_born_fields* born,
+                                     const hydot_rec_opts* opts, hydot_factor* out,
+                                     int* row_perm_h, int* node_rank_h, int* node_depth_h,
+                                     hydot_ledger* ledger_h) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!tree || !out || (!provider == !born))
+            throw std::invalid_argument("recursive_lowrank: need a tree and exactly one provider");
+        hydot_rec_opts o{0, 20, 10, 0};
+        if (opts) o = *opts;
+        if (o.hint_mode != 0) throw std::invalid_argument("recursive_lowrank: unknown hint_mode");
+        int rows_per;
+        int64_t cols;
+        BlockFn fn;
+        if (provider) {
+            rows_per = provider->rows_per_source;
+            cols = provider->cols;
+            if (!provider->block) throw std::invalid_argument("BlockProvider: null block function");
+            fn = [&](int s, double* dst, int64_t ld) {
+                if (provider->block(provider->user, s, dst, ld) != 0)
+                    throw std::runtime_error("BlockProvider failed for source " + std::to_string(s));
+            };
+        } else {
+            rows_per = born->n_det * born->n_lambda;
+            cols = born->N;
+            fn = [&](int s, double* dst, int64_t ld) {
+                if (s < 0 || s >= born->n_sources) throw std::invalid_argument("source out of range");
+                born_block(c, born->N, born->n_lambda, born->incident_dev_h[s],
+                           born->adjoint_dev_h + int64_t(s) * born->n_det, born->n_det, born->w_dev,
+                           born->nu, dst, ld);
+            };
+        }
+        RecOut r = recursive_lowrank(c, tree->t, eps, rows_per, cols, fn, o.seed, o.p, o.kprobe);
+        c.sync();
+        if (row_perm_h) std::memcpy(row_perm_h, r.row_perm.data(), r.row_perm.size() * sizeof(int));
+        if (node_rank_h) std::memcpy(node_rank_h, r.node_rank.data(), r.node_rank.size() * sizeof(int));
+        if (node_depth_h)
+            std::memcpy(node_depth_h, r.node_depth.data(), r.node_depth.size() * sizeof(int));
+        ledger_out(r.ledger, ledger_h);
+        *out = wrap(ctx->c, std::move(r.factor));
+    });
+}
+
+hydot_status hydot_recompress(hydot_ctx ctx, hydot_factor f, double eps, int rank,
+                              hydot_factor* out, hydot_ledger* ledger_h) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!f || !out) throw std::invalid_argument("recompress: null factor");
+        Ledger l;
+        Factor g = recompress(c, f->f, eps, rank, &l);
+        c.sync();
+        ledger_out(l, ledger_h);
+        *out = wrap(ctx->c, std::move(g));
+    });
+}
+
+hydot_status hydot_lr_matmat(hydot_ctx ctx, hydot_factor f, int trans, int b, const double* X_dev,
+                             int64_t ldx, double* Y_dev, int64_t ldy) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!f) throw std::invalid_argument("lr_matvec: null factor");
+        const Factor& F = f->f;
+        const int64_t in_rows = trans ? F.rows : F.cols, out_rows = trans ? F.cols : F.rows;
+        if (b < 0 || ldx < in_rows || ldy < out_rows)
+            throw std::invalid_argument(trans ? "lr_rmatvec: dimension mismatch"
+                                              : "lr_matvec: dimension mismatch");
+        if (b == 0) return;
+        if (F.rank == 0) {
+            fill(c, out_rows, b, 0.0, Y_dev, ldy);
+            c.sync();
+            return;
+        }
+        DBuf Z = dalloc(c, size_t(F.rank) * size_t(b));
+        const double* A1 = trans ? F.U.d() : F.V.d();  // contract against X
+        const double* A2 = trans ? F.V.d() : F.U.d();
+        dgemm(c, true, false, F.rank, b, in_rows, 1.0, A1, in_rows, X_dev, ldx, 0.0, Z.d(), F.rank);
+        dgemm(c, false, false, out_rows, b, F.rank, 1.0, A2, out_rows, Z.d(), F.rank, 0.0, Y_dev, ldy);
+        c.sync();
+    });
+}
+
+hydot_status hydot_j_matmat(hydot_ctx ctx, hydot_factor f, int trans, int b, const int* row_perm_dev,
+                            const double* eps_c_dev, int n_lambda, int n_c, const double* X_dev,
+                            int64_t ldx, double* Y_dev, int64_t ldy) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!f || !row_perm_dev || !eps_c_dev || n_lambda < 1 || n_c < 1 || b < 0)
+            throw std::invalid_argument("J matmat: bad arguments");
+        const Factor& F = f->f;
+        const int64_t M = F.rows, N = F.cols, R = F.rank;
+        const int64_t q = int64_t(b) * n_c;
+        if (b == 0) return;
+        if (!trans) {
+            if (ldx != N * n_c || ldy < M) throw std::invalid_argument("J matvec: dimension mismatch");
+            if (R == 0) {
+                fill(c, M, b, 0.0, Y_dev, ldy);
+                c.sync();
+                return;
+            }
+            DBuf Z = dalloc(c, size_t(R * q)), T = dalloc(c, size_t(M * q));
+            dgemm(c, true, false, R, q, N, 1.0, F.V.d(), N, X_dev, N, 0.0, Z.d(), R);
+            dgemm(c, false, false, M, q, R, 1.0, F.U.d(), M, Z.d(), R, 0.0, T.d(), M);
+            j_combine(c, M, b, n_c, n_lambda, T.d(), M, row_perm_dev, eps_c_dev, Y_dev, ldy);
+        } else {
+            if (ldx < M || ldy != N * n_c) throw std::invalid_argument("J rmatvec: dimension mismatch");
+            if (R == 0) {
+                fill(c, N * n_c, b, 0.0, Y_dev, ldy);
+                c.sync();
+                return;
+            }
+            DBuf G = dalloc(c, size_t(M * q)), W = dalloc(c, size_t(R * q));
+            j_gather_scale(c, M, b, n_c, n_lambda, X_dev, ldx, row_perm_dev, eps_c_dev, G.d(), M);
+            dgemm(c, true, false, R, q, M, 1.0, F.U.d(), M, G.d(), M, 0.0, W.d(), R);
+            dgemm(c, false, false, N, q, R, 1.0, F.V.d(), N, W.d(), R, 0.0, Y_dev, N);
+        }
+        c.sync();
+    });
+}
+
+hydot_status hydot_thin_svd(hydot_ctx ctx, int64_t m, int64_t n, const double* a_dev, int64_t lda,
+                            double* U_dev, double* s_h, double* V_dev) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (m < 0 || n < 0 || lda < m) throw std::invalid_argument("thin_svd: bad dimensions");
+        SVDd s = fast_thin_svd(c, a_dev, lda, false, m, n, nullptr, HYDOT_CAT_OTHER);
+        const int64_t k = s.k;
+        if (k > 0) {
+            HYDOT_CUDA(cudaMemcpyAsync(U_dev, s.U.d(), size_t(m * k) * 8, cudaMemcpyDeviceToDevice, c.stream));
+            HYDOT_CUDA(cudaMemcpyAsync(V_dev, s.V.d(), size_t(n * k) * 8, cudaMemcpyDeviceToDevice, c.stream));
+            std::memcpy(s_h, s.s.data(), size_t(k) * 8);
+        }
+        c.sync();
+    });
+}
+
+hydot_status hydot_householder_qr(hydot_ctx ctx, int64_t m, int64_t n, const double* a_dev,
+                                  int64_t lda, double* R_dev, double* Q_dev) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (m < n || n < 0 || lda < m) throw std::invalid_argument("householder_qr: needs m >= n");
+        QRFact qf;
+        geqrf(c, m, n, a_dev, lda, qf);
+        if (R_dev) extract_upper(c, n, qf.a.d(), m, R_dev, n);
+        if (Q_dev) {
+            fill(c, m, n, 0.0, Q_dev, m);
+            set_identity(c, n, n, Q_dev, m);
+            apply_q(c, qf, false, n, Q_dev, m);
+        }
+        c.sync();
+    });
+}
+
+hydot_status hydot_dgemm(hydot_ctx ctx, int transa, int transb, int64_t m, int64_t n, int64_t k,
+                         double alpha, const double* A_dev, int64_t lda, const double* B_dev,
+                         int64_t ldb, double beta, double* C_dev, int64_t ldc) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (m < 0 || n < 0 || k < 0 || ldc < m) throw std::invalid_argument("dgemm: bad dimensions");
+        dgemm(c, transa != 0, transb != 0, m, n, k, alpha, A_dev, lda, B_dev, ldb, beta, C_dev, ldc);
+        c.sync();
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,205 @@
+// internal.h -- shared host-side declarations of the B200 hydot library.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hydot_b200.h"
+
+namespace hydot {
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define HYDOT_CUDA(call)                                                                   \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            throw ::hydot::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct RngTables;
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    std::string err;
+    int64_t launches = 0;
+    int num_sms = 148;
+    // host-pinned scratch for small D2H reads
+    double* pinned = nullptr;
+    size_t pinned_len = 0;
+    // MT19937-64 jump polynomials on the device (rng.cu)
+    uint64_t* jump_dev = nullptr;
+    int64_t jump_n = 0;
+    void count(int64_t n = 1) { launches += n; }
+    void check_launch() {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) throw CudaError(std::string("kernel launch: ") + cudaGetErrorString(e));
+        ++launches;
+    }
+    void sync() { HYDOT_CUDA(cudaStreamSynchronize(stream)); }
+    // copy n doubles device->host through pinned scratch (synchronises)
+    void d2h(double* dst, const double* src, size_t n);
+};
+
+// Stream-ordered device buffer (cudaMallocAsync / cudaFreeAsync pool).
+class DBuf {
+   public:
+    DBuf() = default;
+    DBuf(Ctx& c, size_t bytes) { alloc(c, bytes); }
+    ~DBuf() { release(); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept { *this = std::move(o); }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p_ = o.p_;
+            n_ = o.n_;
+            s_ = o.s_;
+            o.p_ = nullptr;
+            o.n_ = 0;
+        }
+        return *this;
+    }
+    void alloc(Ctx& c, size_t bytes) {
+        release();
+        s_ = c.stream;
+        n_ = bytes;
+        if (bytes) {
+            cudaError_t e = cudaMallocAsync(&p_, bytes, s_);
+            if (e != cudaSuccess) {
+                p_ = nullptr;
+                throw std::bad_alloc();
+            }
+        }
+    }
+    void release() {
+        if (p_) cudaFreeAsync(p_, s_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    template <class T = double>
+    T* as() const {
+        return static_cast<T*>(p_);
+    }
+    double* d() const { return static_cast<double*>(p_); }
+    size_t bytes() const { return n_; }
+
+   private:
+    void* p_ = nullptr;
+    size_t n_ = 0;
+    cudaStream_t s_ = nullptr;
+};
+
+inline DBuf dalloc(Ctx& c, size_t n_doubles) { return DBuf(c, n_doubles * sizeof(double)); }
+
+// ---------------------------------------------------------------- ledger --
+struct Ledger {
+    double leaf = 0, agglomeration = 0, recompress = 0, other = 0, kernel_tally = 0;
+    void charge(int cat, double f) {
+        kernel_tally += f;
+        switch (cat) {
+            case HYDOT_CAT_LEAF: leaf += f; break;
+            case HYDOT_CAT_AGGLOMERATION: agglomeration += f; break;
+            case HYDOT_CAT_RECOMPRESS: recompress += f; break;
+            default: other += f; break;
+        }
+    }
+};
+
+// --------------------------------------------------------------- kernels --
+// gemm.cu
+void dgemm(Ctx& c, bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alpha,
+           const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+           int64_t ldc);
+
+// util.cu
+void copy2d(Ctx& c, int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst,
+            int64_t ldd);
+void transpose(Ctx& c, int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst,
+               int64_t ldd);  // dst (cols x rows) = src^T
+void fill(Ctx& c, int64_t rows, int64_t cols, double v, double* dst, int64_t ldd);
+void set_identity(Ctx& c, int64_t rows, int64_t cols, double* dst, int64_t ldd);
+void scale_cols(Ctx& c, int64_t rows, int64_t cols, double* A, int64_t lda,
+                const double* s_dev);  // A(:,j) *= s[j]
+void extract_upper(Ctx& c, int64_t n, const double* A, int64_t lda, double* R,
+                   int64_t ldr);  // R = triu(A[0:n,0:n])
+void gather_cols(Ctx& c, int64_t rows, int64_t cols, const double* src, int64_t lds,
+                 const int* idx_dev, double* dst, int64_t ldd);
+double frob_diff(Ctx& c, int64_t rows, int64_t cols, const double* A, int64_t lda,
+                 const double* B, int64_t ldb);  // ||A - B||_F (synchronises)
+
+// born.cu
+void born_block(Ctx& c, int64_t N, int nl, const double* inc, const double* const* adj_h, int nd,
+                const double* w, double nu, double* out, int64_t ld);
+
+// qr.cu : blocked Householder QR (LAPACK dgeqrf/dorgqr semantics)
+struct QRFact {
+    int64_t m = 0, n = 0;
+    DBuf a;    // m x n: R in the upper triangle, Householder vectors below
+    DBuf tau;  // n
+    DBuf T;    // nb x n : block reflector triangles per panel
+};
+constexpr int kQRPanel = 32;
+void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f);
+// Y (m x k) := Q Y (trans=false) or Q^T Y
+void apply_q(Ctx& c, const QRFact& f, bool trans, int64_t k, double* Y, int64_t ldy);
+
+// svd.cu : one-sided Jacobi thin SVD of X (m x n, m >= n); s descending.
+void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, double* U,
+                int64_t ldu, std::vector<double>& s, double* V, int64_t ldv);
+
+// cg.cu
+struct CGStats {
+    std::vector<int> iters;
+    std::vector<double> relres;
+};
+void fields_solve(Ctx& c, const hydot_grid7& g, int nl, const double* sigma,
+                  const double* sigmap, const double* inv_D, const int64_t* rhs_vertex, int n_rhs,
+                  double tol, int max_iter, int fixed_iters, double* out, CGStats* stats);
+void apply7(Ctx& c, const hydot_grid7& g, double sigma, double sigmap, const double* x,
+            double* y);
+
+// matmat.cu
+void j_combine(Ctx& c, int64_t M, int b, int nc, int nl, const double* T, int64_t ldt,
+               const int* row_perm, const double* eps_c, double* Y, int64_t ldy);
+void j_gather_scale(Ctx& c, int64_t M, int b, int nc, int nl, const double* X, int64_t ldx,
+                    const int* row_perm, const double* eps_c, double* G, int64_t ldg);
+
+// rng.cu
+class RngStream {
+   public:
+    RngStream(Ctx& c, uint64_t seed);
+    ~RngStream();
+    // pointer to the next `count` normals of the libstdc++ stream (valid until
+    // the next take()); advances the stream.
+    const double* take(int64_t count);
+    // fill out with normals [offset, offset+count) (random access)
+    void fill(int64_t offset, int64_t count, double* out);
+    void raw(int64_t offset, int64_t count, uint64_t* out);
+
+   private:
+    void ensure_normals(int64_t upto);
+    void generate_chunks(int64_t c_end);
+    Ctx& c_;
+    uint64_t seed_;
+    DBuf prefix_;       // z_0 .. z_{kPrefix-1}
+    DBuf normals_;      // all normals generated so far
+    int64_t n_chunks_ = 0;
+    int64_t n_normals_ = 0;
+    int64_t consumed_ = 0;
+    DBuf chunk_counts_;  // accepted attempts per chunk (device)
+    std::vector<int64_t> chunk_offsets_;
+};
+bool rng_selftest_host();
+
+}  // namespace hydot

@@ -1,0 +1,436 @@
+// lowrank.cpp -- host drivers of the device compression path: randsvd,
+// agglomerate, recursive_lowrank, recompress (lowrank.cpp:131-199, 321-359,
+// 385-521, 540-587 of the reference).  All matrices stay in HBM; the host
+// only sees singular values, the probe error and ranks (one small D2H read
+// per decision, exactly the quantities the reference branches on).
+#include "lowrank.h"
+
+#include <algorithm>
+#include <cmath>
+#include <map>
+
+namespace hydot {
+
+namespace {
+double svd_flops(double m, double n) {  // lowrank.cpp:38-41
+    double mn = std::min(m, n), mx = std::max(m, n);
+    return 14.0 * mx * mn * mn;
+}
+double qr_flops(double m, double n) { return 2.0 * m * n * n; }  // lowrank.cpp:51
+void charge(Ledger* l, int cat, double f) {
+    if (l) l->charge(cat, f);
+}
+
+// materialise L = S^T (S stored n x m) as column-major m x n
+DBuf materialise_t(Ctx& c, const double* S, int64_t ld, int64_t m, int64_t n) {
+    DBuf t = dalloc(c, size_t(std::max<int64_t>(m * n, 1)));
+    transpose(c, n, m, S, ld, t.d(), m);
+    return t;
+}
+
+// plain thin SVD of L (m x n) by Jacobi on the taller orientation
+SVDd direct_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, int64_t n) {
+    SVDd o;
+    o.m = m;
+    o.n = n;
+    o.k = std::min(m, n);
+    o.U = dalloc(c, size_t(std::max<int64_t>(m * o.k, 1)));
+    o.V = dalloc(c, size_t(std::max<int64_t>(n * o.k, 1)));
+    if (o.k == 0) return o;
+    if (m >= n) {
+        // need L column-major (m x n)
+        DBuf tmp;
+        const double* Lp = S;
+        int64_t ldl = ld;
+        if (trans) {
+            tmp = materialise_t(c, S, ld, m, n);
+            Lp = tmp.d();
+            ldl = m;
+        }
+        jacobi_svd(c, m, n, Lp, ldl, o.U.d(), m, o.s, o.V.d(), n);
+    } else {
+        // Jacobi on L^T (n x m): L^T = U' S V'^T  =>  L = V' S U'^T
+        DBuf tmp;
+        const double* Lt = S;
+        int64_t ldt = ld;
+        if (!trans) {
+            tmp = materialise_t(c, S, ld, n, m);  // L^T as n x m
+            Lt = tmp.d();
+            ldt = n;
+        }
+        jacobi_svd(c, n, m, Lt, ldt, o.V.d(), n, o.s, o.U.d(), m);
+    }
+    return o;
+}
+}  // namespace
+
+SVDd thin_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, int64_t n, Ledger* l,
+              int cat) {
+    charge(l, cat, svd_flops(double(m), double(n)));  // lowrank.cpp:43-49
+    return direct_svd(c, S, ld, trans, m, n);
+}
+
+SVDd fast_thin_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, int64_t n,
+                   Ledger* l, int cat) {
+    if (n >= 2 * m && m > 0) {  // lowrank.cpp:66-72
+        SVDd t = fast_thin_svd(c, S, ld, !trans, n, m, l, cat);
+        SVDd o;
+        o.m = m;
+        o.n = n;
+        o.k = t.k;
+        o.U = std::move(t.V);
+        o.V = std::move(t.U);
+        o.s = std::move(t.s);
+        return o;
+    }
+    if (m >= 2 * n && n > 0) {  // lowrank.cpp:73-87
+        charge(l, cat, 2.0 * qr_flops(double(m), double(n)) + svd_flops(double(n), double(n)));
+        DBuf tmp;
+        const double* Lp = S;
+        int64_t ldl = ld;
+        if (trans) {
+            tmp = materialise_t(c, S, ld, m, n);
+            Lp = tmp.d();
+            ldl = m;
+        }
+        QRFact qf;
+        geqrf(c, m, n, Lp, ldl, qf);
+        tmp.release();
+        DBuf R = dalloc(c, size_t(n * n));
+        extract_upper(c, n, qf.a.d(), m, R.d(), n);
+        SVDd o;
+        o.m = m;
+        o.n = n;
+        o.k = n;
+        o.V = dalloc(c, size_t(n * n));
+        DBuf Ur = dalloc(c, size_t(n * n));
+        jacobi_svd(c, n, n, R.d(), n, Ur.d(), n, o.s, o.V.d(), n);
+        // U = Q [Ur; 0]
+        o.U = dalloc(c, size_t(m * n));
+        fill(c, m, n, 0.0, o.U.d(), m);
+        copy2d(c, n, n, Ur.d(), n, o.U.d(), m);
+        apply_q(c, qf, false, n, o.U.d(), m);
+        return o;
+    }
+    return thin_svd(c, S, ld, trans, m, n, l, cat);  // lowrank.cpp:88-92
+}
+
+Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, double eps, int p,
+               int kprobe, uint64_t seed, Ledger* l, int cat, int r0) {
+    Factor f;
+    f.rows = m;
+    f.cols = n;
+    f.tol = eps;
+    f.method = HYDOT_METHOD_RANDSVD;
+    if (m == 0 || n == 0) return f;  // lowrank.cpp:148-152
+    if (p < 0 || kprobe < 1) throw std::invalid_argument("randsvd: p >= 0 and kprobe >= 1 required");
+    const int64_t nmax = std::min(m, n);
+    int64_t r = std::clamp<int64_t>(r0, 1, nmax);
+    std::unique_ptr<RngStream> rng;
+    SVDd svdY;
+    DBuf YP;
+    int64_t qc = 0;
+    bool identity = false;
+    while (true) {
+        const int64_t rs = std::min<int64_t>(r + p, nmax);
+        if (rs >= nmax && m <= n) {  // lowrank.cpp:159-164: Q = I_m
+            identity = true;
+            break;
+        }
+        if (!rng) rng.reset(new RngStream(c, seed));
+        const int64_t w = rs + kprobe;
+        const double* Om = rng->take(n * w);  // [Omega1 | Omega2], n x (rs+k)
+        YP = dalloc(c, size_t(m * w));
+        dgemm(c, true, false, m, w, n, 1.0, At, lda, Om, n, 0.0, YP.d(), m);
+        charge(l, cat, 2.0 * double(m) * double(n) * double(rs));      // apply_mm Y
+        charge(l, cat, 2.0 * double(m) * double(n) * double(kprobe));  // apply_mm P
+        svdY = fast_thin_svd(c, YP.d(), m, false, m, rs, l, cat);
+        qc = std::min<int64_t>(r, svdY.k);
+        const double sigma_top = svdY.s.empty() ? 0.0 : svdY.s[0];
+        const double* Q = svdY.U.d();
+        const double* P = YP.d() + m * rs;
+        DBuf QtP = dalloc(c, size_t(std::max<int64_t>(qc * kprobe, 1)));
+        DBuf QQtP = dalloc(c, size_t(m * kprobe));
+        dgemm(c, true, false, qc, kprobe, m, 1.0, Q, m, P, m, 0.0, QtP.d(), qc);
+        charge(l, cat, 2.0 * double(qc) * double(kprobe) * double(m));
+        dgemm(c, false, false, m, kprobe, qc, 1.0, Q, m, QtP.d(), qc, 0.0, QQtP.d(), m);
+        charge(l, cat, 2.0 * double(m) * double(kprobe) * double(qc));
+        const double er = frob_diff(c, m, kprobe, P, m, QQtP.d(), m);
+        if (er <= eps * sigma_top) break;  // lowrank.cpp:176
+        if (r >= nmax) {                   // :177-180
+            f.flagged = true;
+            break;
+        }
+        r = std::min<int64_t>(2 * r, nmax);  // :181
+    }
+    // B = (A^T Q)^T (lowrank.cpp:184), held as B^T (n x qc)
+    DBuf Bt;
+    const double* Btp;
+    int64_t ldb;
+    if (identity) {
+        qc = m;
+        Btp = At;  // A^T I = A^T (exact)
+        ldb = lda;
+    } else {
+        Bt = dalloc(c, size_t(n * qc));
+        dgemm(c, false, false, n, qc, m, 1.0, At, lda, svdY.U.d(), m, 0.0, Bt.d(), n);
+        Btp = Bt.d();
+        ldb = n;
+    }
+    charge(l, cat, 2.0 * double(m) * double(n) * double(qc));
+    SVDd svdB = fast_thin_svd(c, Btp, ldb, true, qc, n, l, cat);
+    const std::vector<double>& s = svdB.s;
+    const double s1 = s.empty() ? 0.0 : s[0];
+    int64_t keep = 0;
+    for (size_t i = 0; i < s.size(); ++i)
+        if (s[i] > eps * s1 && s[i] > 0) keep = int64_t(i) + 1;  // :187-190
+    f.rank = keep;
+    f.U = dalloc(c, size_t(std::max<int64_t>(m * keep, 1)));
+    f.V = dalloc(c, size_t(std::max<int64_t>(n * keep, 1)));
+    if (keep > 0) {
+        if (identity) {
+            copy2d(c, m, keep, svdB.U.d(), qc, f.U.d(), m);  // I * U (exact)
+        } else {
+            dgemm(c, false, false, m, keep, qc, 1.0, svdY.U.d(), m, svdB.U.d(), qc, 0.0, f.U.d(),
+                  m);  // :191
+        }
+        copy2d(c, n, keep, svdB.V.d(), n, f.V.d(), n);  // :192
+        DBuf sd = dalloc(c, size_t(keep));
+        HYDOT_CUDA(cudaMemcpyAsync(sd.d(), s.data(), size_t(keep) * 8, cudaMemcpyHostToDevice,
+                                   c.stream));
+        scale_cols(c, n, keep, f.V.d(), n, sd.d());
+        c.sync();
+    }
+    charge(l, cat, 2.0 * double(m) * double(keep) * double(qc));
+    charge(l, cat, 1.0 * double(n) * double(keep));  // :193-197
+    return f;
+}
+
+Factor agglomerate(Ctx& c, const Factor& f1, const Factor& f2, double eps, uint64_t seed,
+                   Ledger* l, int rank_hint, int p, int kprobe) {
+    if (f1.cols != f2.cols)
+        throw std::invalid_argument("agglomerate: column dimension mismatch");  // :324-325
+    const int64_t n = f1.cols, r1 = f1.rank, r2 = f2.rank, m1 = f1.rows, m2 = f2.rows;
+    Factor out;
+    out.rows = m1 + m2;
+    out.cols = n;
+    out.tol = eps;
+    out.method = HYDOT_METHOD_AGGLOMERATE;
+    if (r1 + r2 == 0) {  // :333-337
+        out.flagged = f1.flagged || f2.flagged;
+        return out;
+    }
+    // W = [V1^T; V2^T] held as W^T = [V1 V2] (n x (r1+r2))  :339-341
+    DBuf Wt = dalloc(c, size_t(n * (r1 + r2)));
+    copy2d(c, n, r1, f1.V.d(), n, Wt.d(), n);
+    copy2d(c, n, r2, f2.V.d(), n, Wt.d() + n * r1, n);
+    const int hint = int(std::max<int64_t>({r1, r2, int64_t(rank_hint)}));
+    Factor inner = randsvd(c, r1 + r2, n, Wt.d(), n, eps, p, kprobe, seed, l,
+                           HYDOT_CAT_AGGLOMERATION, hint);  // :344-346
+    Wt.release();
+    const int64_t rp = inner.rank;
+    out.rank = rp;
+    out.U = dalloc(c, size_t(std::max<int64_t>((m1 + m2) * rp, 1)));
+    if (rp > 0) {  // :349-356
+        dgemm(c, false, false, m1, rp, r1, 1.0, f1.U.d(), m1, inner.U.d(), r1 + r2, 0.0, out.U.d(),
+              m1 + m2);
+        charge(l, HYDOT_CAT_AGGLOMERATION, 2.0 * double(m1) * double(rp) * double(r1));
+        dgemm(c, false, false, m2, rp, r2, 1.0, f2.U.d(), m2, inner.U.d() + r1, r1 + r2, 0.0,
+              out.U.d() + m1, m1 + m2);
+        charge(l, HYDOT_CAT_AGGLOMERATION, 2.0 * double(m2) * double(rp) * double(r2));
+    }
+    out.V = std::move(inner.V);
+    out.flagged = f1.flagged || f2.flagged || inner.flagged;  // :357
+    return out;
+}
+
+Factor recompress(Ctx& c, const Factor& f, double eps, int rank, Ledger* l) {
+    const int64_t r = f.rank, M = f.rows, N = f.cols;
+    Factor out;
+    out.rows = M;
+    out.cols = N;
+    out.tol = eps;
+    out.method = HYDOT_METHOD_RECOMPRESS;
+    out.flagged = f.flagged;
+    if (r == 0) return out;  // :554-558
+    if (M < r || N < r) throw std::invalid_argument("recompress: rank exceeds a factor dimension");
+    charge(l, HYDOT_CAT_RECOMPRESS, qr_flops(double(M), double(r)) + qr_flops(double(N), double(r)));
+    QRFact qu, qv;
+    geqrf(c, M, r, f.U.d(), M, qu);  // :564
+    geqrf(c, N, r, f.V.d(), N, qv);
+    DBuf Ru = dalloc(c, size_t(r * r)), Rv = dalloc(c, size_t(r * r)), core = dalloc(c, size_t(r * r));
+    extract_upper(c, r, qu.a.d(), M, Ru.d(), r);
+    extract_upper(c, r, qv.a.d(), N, Rv.d(), r);
+    dgemm(c, false, true, r, r, r, 1.0, Ru.d(), r, Rv.d(), r, 0.0, core.d(), r);  // :567
+    charge(l, HYDOT_CAT_RECOMPRESS, 2.0 * double(r) * double(r) * double(r));
+    SVDd svd = thin_svd(c, core.d(), r, false, r, r, l, HYDOT_CAT_RECOMPRESS);  // :568
+    const std::vector<double>& s = svd.s;
+    const double s1 = s.empty() ? 0.0 : s[0];
+    int64_t keep;
+    if (rank >= 0) {
+        keep = std::min<int64_t>(rank, int64_t(s.size()));
+    } else {
+        keep = 0;
+        for (size_t i = 0; i < s.size(); ++i)
+            if (s[i] > eps * s1 && s[i] > 0) keep = int64_t(i) + 1;
+    }
+    out.rank = keep;
+    // U = Q_U [U~_k; 0], V = Q_V [V~_k S_k; 0]  (:579-585)
+    out.U = dalloc(c, size_t(std::max<int64_t>(M * keep, 1)));
+    out.V = dalloc(c, size_t(std::max<int64_t>(N * keep, 1)));
+    if (keep > 0) {
+        fill(c, M, keep, 0.0, out.U.d(), M);
+        copy2d(c, r, keep, svd.U.d(), r, out.U.d(), M);
+        apply_q(c, qu, false, keep, out.U.d(), M);
+        fill(c, N, keep, 0.0, out.V.d(), N);
+        copy2d(c, r, keep, svd.V.d(), r, out.V.d(), N);
+        DBuf sd = dalloc(c, size_t(keep));
+        HYDOT_CUDA(cudaMemcpyAsync(sd.d(), s.data(), size_t(keep) * 8, cudaMemcpyHostToDevice,
+                                   c.stream));
+        scale_cols(c, r, keep, out.V.d(), N, sd.d());
+        apply_q(c, qv, false, keep, out.V.d(), N);
+        c.sync();
+    }
+    charge(l, HYDOT_CAT_RECOMPRESS, 2.0 * double(M) * double(keep) * double(r));
+    charge(l, HYDOT_CAT_RECOMPRESS, 2.0 * double(N) * double(keep) * double(r));
+    return out;
+}
+
+// ------------------------------------------------------------------ tree --
+int Tree::depth() const {  // lowrank.cpp:361-368
+    std::function<int(int)> go = [&](int v) -> int {
+        const TreeNode& nd = nodes[size_t(v)];
+        return nd.is_leaf() ? 0 : 1 + std::max(go(nd.left), go(nd.right));
+    };
+    return nodes.empty() ? 0 : go(root);
+}
+
+std::vector<int> Tree::leaf_order() const {  // lowrank.cpp:370-383
+    std::vector<int> out;
+    std::function<void(int)> go = [&](int v) {
+        const TreeNode& nd = nodes[size_t(v)];
+        if (nd.is_leaf()) {
+            out.insert(out.end(), nd.idx.begin(), nd.idx.end());
+        } else {
+            go(nd.left);
+            go(nd.right);
+        }
+    };
+    if (!nodes.empty()) go(root);
+    return out;
+}
+
+// geometric bisection (lowrank.cpp:385-438): widest extent (ties -> lowest
+// axis), "<= midpoint" goes left, <= 2 sources per leaf, median fallback.
+Tree build_cluster_tree(const double* pos, int n, int d, const double* lo, const double* hi) {
+    if (n < 1) throw std::invalid_argument("build_cluster_tree: no sources");
+    if (d < 1) throw std::invalid_argument("build_cluster_tree: box dimension");
+    Tree t;
+    auto P = [&](int i, int j) { return pos[i + int64_t(j) * n]; };
+    std::function<int(std::vector<int>, std::vector<double>, std::vector<double>)> rec =
+        [&](std::vector<int> idx, std::vector<double> a, std::vector<double> b) -> int {
+        const int me = int(t.nodes.size());
+        t.nodes.push_back(TreeNode{idx, -1, -1, a, b});
+        if (idx.size() <= 2) return me;
+        int ax = 0;
+        for (int j = 1; j < d; ++j)
+            if (b[size_t(j)] - a[size_t(j)] > b[size_t(ax)] - a[size_t(ax)]) ax = j;
+        const double mid = 0.5 * (a[size_t(ax)] + b[size_t(ax)]);
+        std::vector<int> left, right;
+        for (int i : idx) {
+            if (P(i, ax) <= mid) left.push_back(i);
+            else right.push_back(i);
+        }
+        std::vector<double> bl = b, ar = a;
+        bl[size_t(ax)] = mid;
+        ar[size_t(ax)] = mid;
+        if (left.empty() || right.empty()) {
+            std::vector<int> srt = idx;
+            std::stable_sort(srt.begin(), srt.end(), [&](int x, int y) { return P(x, ax) < P(y, ax); });
+            const size_t h = srt.size() / 2;
+            left.assign(srt.begin(), srt.begin() + long(h));
+            right.assign(srt.begin() + long(h), srt.end());
+            bl = b;
+            ar = a;
+        }
+        const int lc = rec(std::move(left), a, bl);
+        const int rc = rec(std::move(right), ar, b);
+        t.nodes[size_t(me)].left = lc;
+        t.nodes[size_t(me)].right = rc;
+        return me;
+    };
+    std::vector<int> all(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) all[size_t(i)] = i;
+    t.root = rec(all, std::vector<double>(lo, lo + d), std::vector<double>(hi, hi + d));
+    return t;
+}
+
+double tolerance_schedule(double eps_d, int L, int N_r) {  // lowrank.cpp:540-545
+    if (eps_d <= 0 || L < 0 || N_r < 1)
+        throw std::invalid_argument("tolerance_schedule: bad arguments");
+    return eps_d / (std::pow(2.0, 0.5 * L) * (L + 1) * std::sqrt(double(N_r)));
+}
+
+// recursive_lowrank (lowrank.cpp:459-521) with the reference's warm-start
+// chains (leaf_hint across leaves in DFS order, depth_hint per depth).
+RecOut recursive_lowrank(Ctx& c, const Tree& t, double eps, int rows_per, int64_t cols,
+                         const BlockFn& block, uint64_t seed, int p, int kprobe) {
+    RecOut res;
+    res.node_rank.assign(t.nodes.size(), -1);
+    res.node_depth.assign(t.nodes.size(), 0);
+    int leaf_hint = -1;
+    std::map<int, int> depth_hint;
+    auto node_hint = [&](int depth) {
+        auto it = depth_hint.find(depth);
+        return it == depth_hint.end() ? -1 : it->second + 2;
+    };
+    DBuf blk = dalloc(c, size_t(rows_per) * size_t(cols));
+    std::function<Factor(int, int)> go = [&](int v, int depth) -> Factor {
+        const TreeNode& nd = t.nodes[size_t(v)];
+        res.node_depth[size_t(v)] = depth;
+        Factor f;
+        try {
+            if (nd.is_leaf()) {
+                std::vector<Factor> parts;
+                for (int s : nd.idx) {
+                    block(s, blk.d(), cols);
+                    parts.push_back(randsvd(c, rows_per, cols, blk.d(), cols, eps, p, kprobe,
+                                            seed + 0x9e3779b97f4a7c15ULL * uint64_t(s + 1),
+                                            &res.ledger, HYDOT_CAT_LEAF,
+                                            std::max(1, leaf_hint + 2)));
+                    leaf_hint = int(parts.back().rank);
+                }
+                if (parts.empty()) throw std::runtime_error("empty leaf cluster");
+                f = std::move(parts[0]);
+                for (size_t i = 1; i < parts.size(); ++i)
+                    f = agglomerate(c, f, parts[i], eps,
+                                    seed + 0x517cc1b727220a95ULL * uint64_t(v + 1), &res.ledger,
+                                    node_hint(depth), p, kprobe);
+            } else {
+                Factor fl = go(nd.left, depth + 1);
+                Factor fr = go(nd.right, depth + 1);
+                f = agglomerate(c, fl, fr, eps, seed + 0x2545f4914f6cdd1dULL * uint64_t(v + 1),
+                                &res.ledger, node_hint(depth), p, kprobe);
+            }
+        } catch (const CudaError&) {
+            throw;
+        } catch (const std::bad_alloc&) {
+            throw;
+        } catch (const std::exception& e) {
+            throw std::runtime_error("recursive_lowrank at node " + std::to_string(v) + ": " +
+                                     e.what());
+        }
+        res.node_rank[size_t(v)] = int(f.rank);
+        depth_hint[depth] = int(f.rank);
+        return f;
+    };
+    res.factor = go(t.root, 0);
+    res.factor.method = HYDOT_METHOD_RECURSIVE;
+    res.factor.tol = eps;
+    res.source_order = t.leaf_order();
+    for (int s : res.source_order)
+        for (int q = 0; q < rows_per; ++q) res.row_perm.push_back(s * rows_per + q);
+    return res;
+}
+
+}  // namespace hydot

@@ -1,0 +1,70 @@
+// lowrank.h -- device-resident low-rank factors and the compression drivers.
+#pragma once
+
+#include <functional>
+
+#include "internal.h"
+
+namespace hydot {
+
+// lowrank::LowRankFactor (lowrank.hpp:25-36) with U, V in device memory.
+struct Factor {
+    int64_t rows = 0, cols = 0, rank = 0;
+    DBuf U, V;  // rows x rank (ld rows), cols x rank (ld cols)
+    double tol = 0.0;
+    int method = HYDOT_METHOD_NONE;
+    bool flagged = false;
+};
+
+// thin SVD result: U m x k, s (host), V n x k
+struct SVDd {
+    int64_t m = 0, n = 0, k = 0;
+    DBuf U, V;
+    std::vector<double> s;
+};
+
+// fast_thin_svd (lowrank.cpp:62-93) of the logical matrix L (m x n):
+// trans=false: L = S (column-major m x n, ld); trans=true: L = S^T with S
+// stored n x m.
+SVDd fast_thin_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, int64_t n,
+                   Ledger* l, int cat);
+SVDd thin_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, int64_t n, Ledger* l,
+              int cat);
+
+// randsvd (lowrank.cpp:131-199) on A (m x n) given row-major: A(i,j) =
+// At[j + i*lda].
+Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, double eps, int p,
+               int kprobe, uint64_t seed, Ledger* l, int cat, int r0);
+
+Factor agglomerate(Ctx& c, const Factor& f1, const Factor& f2, double eps, uint64_t seed,
+                   Ledger* l, int rank_hint, int p, int kprobe);
+
+Factor recompress(Ctx& c, const Factor& f, double eps, int rank, Ledger* l);
+
+// ClusterTree (lowrank.hpp:103-119)
+struct TreeNode {
+    std::vector<int> idx;
+    int left = -1, right = -1;
+    std::vector<double> lo, hi;
+    bool is_leaf() const { return left < 0; }
+};
+struct Tree {
+    std::vector<TreeNode> nodes;
+    int root = 0;
+    int depth() const;
+    std::vector<int> leaf_order() const;
+};
+Tree build_cluster_tree(const double* pos, int n, int d, const double* lo, const double* hi);
+double tolerance_schedule(double eps_d, int L, int N_r);
+
+struct RecOut {
+    Factor factor;
+    std::vector<int> source_order, row_perm, node_rank, node_depth;
+    Ledger ledger;
+};
+// block(s, out, ld): fill rows_per x cols block of source s row-major
+using BlockFn = std::function<void(int, double*, int64_t)>;
+RecOut recursive_lowrank(Ctx& c, const Tree& t, double eps, int rows_per, int64_t cols,
+                         const BlockFn& block, uint64_t seed, int p, int kprobe);
+
+}  // namespace hydot

@@ -1,0 +1,195 @@
+// util.cu -- small data-movement kernels used between the hot-path stages
+// (copies, transposes, column scaling, triangle extraction, norms).
+#include "internal.h"
+
+namespace hydot {
+namespace {
+
+inline int grid_for(Ctx& c, int64_t n, int threads = 256) {
+    int64_t b = (n + threads - 1) / threads;
+    return int(std::max<int64_t>(1, std::min<int64_t>(b, int64_t(c.num_sms) * 16)));
+}
+
+__global__ void copy2d_k(int64_t rows, int64_t cols, const double* __restrict__ s, int64_t lds,
+                         double* __restrict__ d, int64_t ldd) {
+    int64_t total = rows * cols;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        int64_t i = e % rows, j = e / rows;
+        d[i + j * ldd] = s[i + j * lds];
+    }
+}
+
+// 32x32 tiled transpose through shared memory
+__global__ void transpose_k(int64_t rows, int64_t cols, const double* __restrict__ s, int64_t lds,
+                            double* __restrict__ d, int64_t ldd) {
+    __shared__ double tile[32][33];
+    int64_t i0 = int64_t(blockIdx.x) * 32, j0 = int64_t(blockIdx.y) * 32;
+    for (int jj = threadIdx.y; jj < 32; jj += blockDim.y) {
+        int64_t i = i0 + threadIdx.x, j = j0 + jj;
+        if (i < rows && j < cols) tile[jj][threadIdx.x] = s[i + j * lds];
+    }
+    __syncthreads();
+    for (int ii = threadIdx.y; ii < 32; ii += blockDim.y) {
+        int64_t j = j0 + threadIdx.x, i = i0 + ii;
+        if (i < rows && j < cols) d[j + i * ldd] = tile[threadIdx.x][ii];
+    }
+}
+
+__global__ void fill_k(int64_t rows, int64_t cols, double v, double* d, int64_t ldd, int ident) {
+    int64_t total = rows * cols;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        int64_t i = e % rows, j = e / rows;
+        d[i + j * ldd] = ident ? (i == j ? 1.0 : 0.0) : v;
+    }
+}
+
+__global__ void scale_cols_k(int64_t rows, int64_t cols, double* A, int64_t lda,
+                             const double* __restrict__ s) {
+    int64_t total = rows * cols;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        int64_t i = e % rows, j = e / rows;
+        A[i + j * lda] *= s[j];
+    }
+}
+
+__global__ void upper_k(int64_t n, const double* __restrict__ A, int64_t lda, double* R,
+                        int64_t ldr) {
+    int64_t total = n * n;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        int64_t i = e % n, j = e / n;
+        R[i + j * ldr] = i <= j ? A[i + j * lda] : 0.0;
+    }
+}
+
+__global__ void gather_cols_k(int64_t rows, int64_t cols, const double* __restrict__ s,
+                              int64_t lds, const int* __restrict__ idx, double* __restrict__ d,
+                              int64_t ldd) {
+    int64_t total = rows * cols;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        int64_t i = e % rows, j = e / rows;
+        d[i + j * ldd] = s[i + int64_t(idx[j]) * lds];
+    }
+}
+
+// per-block partial sums of (A-B)^2 in fixed order; final sum on one block
+__global__ void diff2_partial(int64_t rows, int64_t cols, const double* __restrict__ A,
+                              int64_t lda, const double* __restrict__ B, int64_t ldb,
+                              double* __restrict__ part) {
+    __shared__ double sh[256];
+    double acc = 0.0;
+    int64_t total = rows * cols;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        int64_t i = e % rows, j = e / rows;
+        double dlt = A[i + j * lda] - (B ? B[i + j * ldb] : 0.0);
+        acc += dlt * dlt;
+    }
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void sum_partials(int n, const double* __restrict__ part, double* out) {
+    __shared__ double sh[256];
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) acc += part[i];
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+
+}  // namespace
+
+void Ctx::d2h(double* dst, const double* src, size_t n) {
+    if (pinned_len < n) {
+        if (pinned) cudaFreeHost(pinned);
+        size_t want = std::max<size_t>(n, 4096);
+        HYDOT_CUDA(cudaMallocHost(&pinned, want * sizeof(double)));
+        pinned_len = want;
+    }
+    HYDOT_CUDA(cudaMemcpyAsync(pinned, src, n * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    sync();
+    std::copy(pinned, pinned + n, dst);
+}
+
+void copy2d(Ctx& c, int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst,
+            int64_t ldd) {
+    if (rows <= 0 || cols <= 0) return;
+    if (lds == rows && ldd == rows) {
+        HYDOT_CUDA(cudaMemcpyAsync(dst, src, size_t(rows * cols) * 8, cudaMemcpyDeviceToDevice,
+                                   c.stream));
+        return;
+    }
+    copy2d_k<<<grid_for(c, rows * cols), 256, 0, c.stream>>>(rows, cols, src, lds, dst, ldd);
+    c.check_launch();
+}
+
+void transpose(Ctx& c, int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst,
+               int64_t ldd) {
+    if (rows <= 0 || cols <= 0) return;
+    dim3 grid = dim3(unsigned((rows + 31) / 32), unsigned((cols + 31) / 32));
+    if (grid.y > 65535) throw std::invalid_argument("transpose: too many columns");
+    transpose_k<<<grid, dim3(32, 8), 0, c.stream>>>(rows, cols, src, lds, dst, ldd);
+    c.check_launch();
+}
+
+void fill(Ctx& c, int64_t rows, int64_t cols, double v, double* dst, int64_t ldd) {
+    if (rows <= 0 || cols <= 0) return;
+    fill_k<<<grid_for(c, rows * cols), 256, 0, c.stream>>>(rows, cols, v, dst, ldd, 0);
+    c.check_launch();
+}
+
+void set_identity(Ctx& c, int64_t rows, int64_t cols, double* dst, int64_t ldd) {
+    if (rows <= 0 || cols <= 0) return;
+    fill_k<<<grid_for(c, rows * cols), 256, 0, c.stream>>>(rows, cols, 0.0, dst, ldd, 1);
+    c.check_launch();
+}
+
+void scale_cols(Ctx& c, int64_t rows, int64_t cols, double* A, int64_t lda, const double* s) {
+    if (rows <= 0 || cols <= 0) return;
+    scale_cols_k<<<grid_for(c, rows * cols), 256, 0, c.stream>>>(rows, cols, A, lda, s);
+    c.check_launch();
+}
+
+void extract_upper(Ctx& c, int64_t n, const double* A, int64_t lda, double* R, int64_t ldr) {
+    if (n <= 0) return;
+    upper_k<<<grid_for(c, n * n), 256, 0, c.stream>>>(n, A, lda, R, ldr);
+    c.check_launch();
+}
+
+void gather_cols(Ctx& c, int64_t rows, int64_t cols, const double* src, int64_t lds,
+                 const int* idx, double* dst, int64_t ldd) {
+    if (rows <= 0 || cols <= 0) return;
+    gather_cols_k<<<grid_for(c, rows * cols), 256, 0, c.stream>>>(rows, cols, src, lds, idx, dst,
+                                                                   ldd);
+    c.check_launch();
+}
+
+double frob_diff(Ctx& c, int64_t rows, int64_t cols, const double* A, int64_t lda,
+                 const double* B, int64_t ldb) {
+    if (rows <= 0 || cols <= 0) return 0.0;
+    int blocks = std::min(grid_for(c, rows * cols), 256);
+    DBuf part = dalloc(c, size_t(blocks) + 1);
+    diff2_partial<<<blocks, 256, 0, c.stream>>>(rows, cols, A, lda, B, ldb, part.d());
+    c.check_launch();
+    sum_partials<<<1, 256, 0, c.stream>>>(blocks, part.d(), part.d() + blocks);
+    c.check_launch();
+    double v = 0;
+    c.d2h(&v, part.d() + blocks, 1);
+    return std::sqrt(v);
+}
+
+}  // namespace hydot

@@ -1,0 +1,103 @@
+"""C-ABI library: loads, exports every declared symbol, host-side logic
+(jump-ahead tables, cluster tree, tolerance schedule) matches the oracle and
+the reference's known answers.  No GPU needed."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "hydot_b200.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = set(re.findall(r"\b(hydot_[a-z0-9_]+)\s*\(", src))
+    return sorted(names)
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1410_0986_b200 import _lib
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    names = declared_functions()
+    assert len(names) >= 30
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    # the Python mirror binds exactly the declared set
+    assert set(_lib.SIGNATURES) == set(names)
+
+
+def test_jump_ahead_tables_match_sequential_engine():
+    import paper_1410_0986_b200 as h
+    assert h.rng_selftest()
+
+
+def test_tolerance_schedule_matches_oracle(oracle):
+    from paper_1410_0986_b200 import lowrank as lr
+    for L in (0, 1, 2, 3, 4, 5):
+        for Nr in (16, 400, 4800, 25600):
+            assert lr.tolerance_schedule(1e-6, L, Nr) == oracle.tolerance_schedule(1e-6, L, Nr)
+    with pytest.raises(ValueError):
+        lr.tolerance_schedule(-1.0, 1, 1)
+
+
+def _tree_tuple(t):
+    return [(n["left"], n["right"], tuple(n["idx"])) for n in t.nodes]
+
+
+def test_cluster_tree_known_answer():
+    # test_lowrank.cpp:139-159
+    from paper_1410_0986_b200 import lowrank as lr
+    t = lr.ClusterTree(np.array([0.1, 0.2, 0.6, 0.7, 0.95]), [0.0], [1.0])
+    root = t.nodes[t.root]
+    L, R = t.nodes[root["left"]], t.nodes[root["right"]]
+    assert L["idx"] == [0, 1] and L["left"] < 0
+    assert t.nodes[R["left"]]["idx"] == [2, 3] and t.nodes[R["right"]]["idx"] == [4]
+    assert t.depth() == 2 and t.leaf_order() == [0, 1, 2, 3, 4]
+
+
+@pytest.mark.parametrize("cfg_id", [0, 1, 2, 3])
+def test_cluster_tree_matches_oracle_on_baseline_lattices(oracle, cfg_id):
+    from paper_1410_0986_b200 import configs, lowrank as lr
+    st = configs.make_setup(configs.CONFIGS[cfg_id])
+    a = lr.ClusterTree(st.source_xy, st.box_lo, st.box_hi)
+    b = oracle.ClusterTree(st.source_xy, st.box_lo, st.box_hi)
+    assert _tree_tuple(a) == [(n["left"], n["right"], tuple(n["idx"])) for n in b.nodes]
+    assert a.depth() == b.depth() == {0: 2, 1: 3, 2: 4, 3: 5}[cfg_id]
+
+
+def test_cluster_tree_random_and_degenerate(oracle):
+    from paper_1410_0986_b200 import lowrank as lr
+    rng = np.random.default_rng(0)
+    for t in range(20):
+        n = int(rng.integers(1, 40))
+        d = int(rng.integers(1, 4))
+        pos = rng.random((n, d))
+        if t % 3 == 0:
+            pos[: n // 2] = pos[0]  # coincident points -> median fallback
+        a = lr.ClusterTree(pos, np.zeros(d), np.ones(d))
+        b = oracle.ClusterTree(pos, np.zeros(d), np.ones(d))
+        assert _tree_tuple(a) == [(x["left"], x["right"], tuple(x["idx"])) for x in b.nodes]
+    with pytest.raises(ValueError):
+        lr.ClusterTree(np.zeros((0, 2)), [0, 0], [1, 1])
+
+
+def test_setup_generation_deterministic():
+    from paper_1410_0986_b200 import configs
+    a = configs.make_setup(configs.CONFIGS[1])
+    b = configs.make_setup(configs.CONFIGS[1])
+    assert np.array_equal(a.sigma, b.sigma) and np.array_equal(a.detector_vertex, b.detector_vertex)
+    cfg = configs.CONFIGS[1]
+    assert a.detector_vertex.shape == (cfg.n_sources, cfg.n_det)
+    n = cfg.n
+    # sources on z = 0 interior, detectors on z = n-1 interior
+    for v in a.source_vertex:
+        ix, iy, iz = v % n, (v // n) % n, v // (n * n)
+        assert iz == 0 and 0 < ix < n - 1 and 0 < iy < n - 1
+    for v in a.detector_vertex.reshape(-1):
+        ix, iy, iz = v % n, (v // n) % n, v // (n * n)
+        assert iz == n - 1 and 0 < ix < n - 1 and 0 < iy < n - 1
+    assert np.all(a.sigma > 0) and np.all(a.sigma_prime > 0)
