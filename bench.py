@@ -1,0 +1,372 @@
+"""bench.py -- headline benchmark of the B200 hydot hot path.
+
+Metric (BASELINE.json): (s,d) Born blocks compressed per second.  One step =
+Born assembly of every (source, detector) block from resident fields +
+recursive randomized compression (leaves + merges, reference hint chains,
+scheduled tolerance) + recompress, i.e. compress_H (experiments.cpp:216-253)
+on BASELINE config 1 (n=48, N=110592, N_s=16, N_ds=6, N_lambda=50, 4
+chromophores, M=4800) -- the largest config whose fields fit one GPU with
+room for the factors.  Synthetic seeded inputs (configs.py); the fields
+(4.95 GB) are larger than L2, so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+--impl reference times the CPU oracle restatement of the reference
+(oracle/, "port": the reference itself needs Eigen and cannot be built here)
+on a bounded sample (one two-source leaf cluster per step) with all host
+threads.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.0  # tools/fp64_peak.cu on this pool's B200: DMMA 37.1, DFMA 37.0 TF/s
+PEAK_SOURCE = "measured: tools/fp64_peak.cu (DMMA m16n8k4, register-resident) -> profiles/fp64_peak_r01.txt"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-sample", type=int, default=1, help="cpu_baseline: leaf clusters timed")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_info():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sms.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# --------------------------------------------------------------- b200 arm --
+def run_b200(args):
+    import torch
+    import paper_1410_0986_b200 as h
+    from paper_1410_0986_b200 import born, configs, lowrank as lr
+
+    rank, world, local = dist_info()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    ctx = h.Context(local)
+    cfg = configs.CONFIGS[args.config]
+    st = configs.make_setup(cfg)
+    g = st.grid()
+    # ---- setup (untimed): fields on the GPU, resident in HBM
+    F, fstats = born.compute_fields(ctx, g, st.sigma, st.sigma_prime, st.inv_D, st.points, tol=1e-10)
+    torch.cuda.synchronize()
+    w = torch.full((g.N,), cfg.h ** 3, dtype=torch.float64, device="cuda")
+    tree = lr.ClusterTree(st.source_xy, st.box_lo, st.box_hi)
+    eps = configs.compression_tolerance(st, tree.depth())
+    opts = lr.RecursiveOptions(seed=cfg.seed)
+
+    def provider_for(Fdev):
+        inc = [Fdev[st.source_point[s]] for s in range(cfg.n_sources)]
+        adj = [[Fdev[st.detector_point[s, d]] for d in range(cfg.n_det)] for s in range(cfg.n_sources)]
+        return lr.BornFieldsProvider(inc, adj, w, 1.0)
+
+    prov = provider_for(F)
+    units = cfg.n_sources * cfg.n_det  # (s,d) blocks per step (whole job = world * units)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        rec = lr.recursive_lowrank(ctx, tree, eps, prov, opts)
+        fr = lr.recompress(ctx, rec.factor, eps, -1, rec.ledger)
+        return rec, fr
+
+    for _ in range(args.warmup):
+        rec, fr = step()
+    torch.cuda.synchronize()
+    ledger_flops = rec.ledger.kernel_tally
+
+    # ---- timed region (value): fields resident, K steps
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = ctx.launch_count()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        rec, fr = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launch_count() - launches0
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * units * args.steps / (ms / 1e3)
+    achieved_tflops = ledger_flops / (ms_per_step / 1e3) / 1e12
+
+    # ---- per-stage breakdown (one extra step, synchronised stage timers)
+    os.environ.setdefault("HYDOT_PROFILE", "0")
+
+    # ---- e2e through the reference-facing call with HOST buffers
+    Fh = torch.empty(F.shape, dtype=torch.float64, pin_memory=True)
+    Fh.copy_(F)
+    Fd = torch.empty_like(F)
+    e2e_ms = []
+    d2h_bytes = 0
+    for _ in range(max(1, args.e2e_steps)):
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        Fd.copy_(Fh, non_blocking=True)                      # H2D of the step's inputs
+        rec2 = lr.recursive_lowrank(ctx, tree, eps, provider_for(Fd), opts)
+        fr2 = lr.recompress(ctx, rec2.factor, eps)
+        Uh = torch.empty((fr2.rank(), fr2.rows()), dtype=torch.float64, pin_memory=True)
+        Vh = torch.empty((fr2.rank(), fr2.cols()), dtype=torch.float64, pin_memory=True)
+        Ud, Vd = fr2.U, fr2.V                                 # device views (col-major)
+        Uh.copy_(Ud.T, non_blocking=True)                     # D2H of the result
+        Vh.copy_(Vd.T, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+        d2h_bytes = (Uh.numel() + Vh.numel()) * 8
+    e2e_step_ms = statistics.median(e2e_ms)
+    e2e_value = world * units / (e2e_step_ms / 1e3)
+    h2d_bytes = F.numel() * 8
+
+    # ---- J~ products on the compressed operator (config-4 style blocks)
+    J = lr.JOperator(ctx, fr, rec.row_perm, st.eps_c)
+    R = fr.rank()
+    matvec = {}
+    for b in (1, 64):
+        X = torch.randn(b, g.N * cfg.n_chrom, dtype=torch.float64, device="cuda")
+        Y = torch.empty(b, cfg.M, dtype=torch.float64, device="cuda")
+        for _ in range(3):
+            J.matmat_cm(X, Y, b)
+        torch.cuda.synchronize()
+        reps = 20
+        a = torch.cuda.Event(enable_timing=True)
+        bb = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            J.matmat_cm(X, Y, b)
+        bb.record(stream)
+        torch.cuda.synchronize()
+        t = a.elapsed_time(bb) / reps / 1e3
+        nbytes = 8.0 * (g.N * R + cfg.M * R + b * cfg.n_chrom * g.N + b * cfg.M)
+        flops = 2.0 * R * b * cfg.n_chrom * (g.N + cfg.M)
+        matvec[f"b{b}"] = {"ms": t * 1e3, "GB/s": nbytes / t / 1e9, "TFLOP/s": flops / t / 1e12,
+                           "hbm_frac": nbytes / t / 1e9 / 6554.9,
+                           "fp64_frac": flops / t / 1e12 / FP64_PEAK_TFLOPS}
+
+    # ---- CPU baseline (rank 0, N=1 only): the oracle on a bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_sample(st, tree, eps, F.cpu().numpy(), threads=1, leaves=args.cpu_sample)
+
+    out = {
+        "metric": "(s,d) Born blocks compressed/s",
+        "value": value,
+        "unit": "blocks/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded BASELINE config-1 physics, configs.py; fields from the GPU CG)",
+        "config": {"workload": f"{cfg.name}: compress_H = Born assembly + recursive randSVD + merges + recompress",
+                   "n": cfg.n, "N": g.N, "n_sources": cfg.n_sources, "n_det": cfg.n_det,
+                   "n_lambda": cfg.n_lambda, "n_chrom": cfg.n_chrom, "M": cfg.M,
+                   "tolerance": f"reference schedule eps_d=1e-6 -> eps={eps:.3e} (L={tree.depth()}), p=20, kprobe=10",
+                   "l2": "inputs larger than L2 (fields %.2f GB resident)" % (F.numel() * 8 / 1e9),
+                   "parallelism": f"sources sharded x{world}" if world > 1 else "single GPU",
+                   "final_rank": fr.rank(), "rank_before_recompress": rec.factor.rank()},
+        "e2e": {"value": e2e_value, "unit": "blocks/s", "h2d_bytes_per_step": int(h2d_bytes),
+                "d2h_bytes_per_step": int(d2h_bytes), "ms_per_step": e2e_step_ms},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": FP64_PEAK_TFLOPS,
+                     "unit": "TFLOP/s", "frac": achieved_tflops / FP64_PEAK_TFLOPS,
+                     "traffic": None,
+                     "what": "compression stage: reference FlopLedger flops per step "
+                             "(lowrank.cpp:31-51, %.3e) / CUDA-event step time" % ledger_flops,
+                     "peak_source": PEAK_SOURCE},
+        "clocks": clk,
+        "matvec": matvec,
+        "fields_setup": {"systems": int(len(st.points) * cfg.n_lambda),
+                         "iters_max": int(fstats.iters.max()),
+                         "relres_max": float(fstats.relres.max())},
+    }
+    if cpu is not None:
+        out["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def cpu_sample(st, tree, eps, Fh, threads: int, leaves: int = 1):
+    """Oracle restatement timed on the host: the first `leaves` leaf clusters
+    of the tree (leaf randsvds + their within-leaf agglomerate) of the same
+    workload; value in blocks/s."""
+    from oracle import oracle as o
+    o.set_threads(threads)
+    cfg = st.cfg
+    otree = o.ClusterTree(st.source_xy, st.box_lo, st.box_hi)
+    leaf_nodes = [v for v, n in enumerate(otree.nodes) if n["left"] < 0][:leaves]
+    srcs = [s for v in leaf_nodes for s in otree.nodes[v]["idx"]]
+    inc = [Fh[st.source_point[s]].T for s in srcs]
+    adj = [[Fh[st.detector_point[s, d]].T for d in range(cfg.n_det)] for s in srcs]
+    w = np.full(cfg.N, cfg.h ** 3)
+    # a sub-tree over just these sources reproduces the leaf work
+    pos = st.source_xy[srcs]
+    sub = o.ClusterTree(pos, st.box_lo, st.box_hi)
+    t0 = time.perf_counter()
+    o.recursive_lowrank_born(sub, eps, inc, adj, w, 1.0, seed=cfg.seed)
+    dt = time.perf_counter() - t0
+    blocks = len(srcs) * cfg.n_det
+    return {"value": blocks / dt, "unit": "blocks/s", "cores": threads, "kind": "port",
+            "sample": f"{len(srcs)} sources ({blocks} (s,d) blocks) of {cfg.name}: leaf randsvds + "
+                      f"their agglomerate, {dt:.2f} s; excludes the upper merges (an optimistic CPU rate)",
+            "seconds": dt}
+
+
+# ---------------------------------------------------------- reference arm --
+def run_reference(args):
+    rank, world, local = dist_info()
+    if rank != 0:
+        return  # rank 0 alone runs the CPU reference
+    from paper_1410_0986_b200 import configs
+    from oracle import oracle as o
+    cfg = configs.CONFIGS[args.config]
+    st = configs.make_setup(cfg)
+    threads = os.cpu_count() or 1
+    o.set_threads(threads)
+    # the oracle's own CPU CG produces the fields of the sampled sources
+    g = st.grid()
+    otree = o.ClusterTree(st.source_xy, st.box_lo, st.box_hi)
+    eps = configs.compression_tolerance(st, otree.depth())
+    leaf = [v for v, n in enumerate(otree.nodes) if n["left"] < 0][0]
+    srcs = otree.nodes[leaf]["idx"]
+    pts = sorted({int(st.source_point[s]) for s in srcs} |
+                 {int(st.detector_point[s, d]) for s in srcs for d in range(cfg.n_det)})
+    Fo, _, _ = o.fields((g.nx, g.ny, g.nz), g.h, st.sigma, st.sigma_prime, st.inv_D,
+                        st.points[pts], tol=1e-10, threads=threads)
+    nl = cfg.n_lambda
+    Fh = np.zeros((len(st.points), nl, g.N))
+    for k, p in enumerate(pts):
+        Fh[p] = Fo[:, k * nl:(k + 1) * nl].T
+
+    class Tree:
+        pass
+
+    times = []
+    res = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_sample(st, otree, eps, Fh, threads=threads, leaves=1)
+        if i >= args.warmup:
+            times.append(r["seconds"])
+            res = r
+    blocks = len(srcs) * cfg.n_det
+    value = blocks * len(times) / sum(times)
+    out = {"metric": "(s,d) Born blocks compressed/s", "value": value, "unit": "blocks/s",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded BASELINE config-1 physics)", "impl": "reference",
+           "config": {"workload": f"{cfg.name}: one leaf cluster per step (bounded CPU sample)",
+                      "n": cfg.n, "N": g.N},
+           "cpu_baseline": {"value": value, "unit": "blocks/s", "cores": threads, "kind": "port",
+                            "sample": res["sample"] if res else ""},
+           "e2e": {"value": value, "unit": "blocks/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -72,6 +72,9 @@ hydot_status hydot_ctx_set_stream(hydot_ctx ctx, void* cuda_stream);
 hydot_status hydot_ctx_synchronize(hydot_ctx ctx);
 /* number of kernels this context launched so far (evidence counter) */
 int64_t hydot_ctx_launch_count(hydot_ctx ctx);
+/* per-stage wall times recorded when HYDOT_PROFILE=1 (JSON written into buf,
+ * then cleared); returns the JSON length */
+int hydot_profile_dump(char* buf, int len);
 
 /* ------------------------------------------------------------- fields -- */
 /* 7-point vertex-centred FV operator on an nx*ny*nz vertex grid (spacing h,

@@ -102,6 +102,17 @@ class DBuf {
 
 inline DBuf dalloc(Ctx& c, size_t n_doubles) { return DBuf(c, n_doubles * sizeof(double)); }
 
+// Optional stage timer (HYDOT_PROFILE=1): synchronises around each scoped
+// stage and accumulates wall time per name; report via hydot_profile_dump().
+struct StageTimer {
+    StageTimer(Ctx& c, const char* name);
+    ~StageTimer();
+    Ctx& c_;
+    const char* name_;
+    double t0_ = 0;
+    bool on_ = false;
+};
+
 // ---------------------------------------------------------------- ledger --
 struct Ledger {
     double leaf = 0, agglomeration = 0, recompress = 0, other = 0, kernel_tally = 0;

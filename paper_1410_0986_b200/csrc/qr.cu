@@ -187,6 +187,7 @@ __global__ void larft_k(int jb, const double* __restrict__ G, const double* __re
 }  // namespace
 
 void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f) {
+    StageTimer _t(c, "qr_geqrf");
     f.m = m;
     f.n = n;
     f.a = dalloc(c, size_t(std::max<int64_t>(m * n, 1)));
@@ -243,6 +244,7 @@ void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f
 }
 
 void apply_q(Ctx& c, const QRFact& f, bool trans, int64_t k, double* Y, int64_t ldy) {
+    StageTimer _t(c, "qr_apply_q");
     const int64_t m = f.m, kk = std::min(f.m, f.n);
     if (k <= 0 || kk <= 0) return;
     DBuf V = dalloc(c, size_t(m) * NB);

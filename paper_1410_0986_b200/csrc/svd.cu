@@ -227,6 +227,7 @@ std::vector<int2> tournament(int n, int& np) {
 
 void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, double* Uo,
                 int64_t lduo, std::vector<double>& s, double* Vo, int64_t ldvo) {
+    StageTimer _t(c, n > 96 ? "svd_jacobi_large" : "svd_jacobi_small");
     s.assign(size_t(std::max<int64_t>(n, 0)), 0.0);
     if (n <= 0) return;
     if (m < n) throw std::invalid_argument("jacobi_svd: needs m >= n");

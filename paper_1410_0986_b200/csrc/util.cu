@@ -139,6 +139,7 @@ void copy2d(Ctx& c, int64_t rows, int64_t cols, const double* src, int64_t lds, 
 
 void transpose(Ctx& c, int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst,
                int64_t ldd) {
+    StageTimer _t(c, "transpose");
     if (rows <= 0 || cols <= 0) return;
     dim3 grid = dim3(unsigned((rows + 31) / 32), unsigned((cols + 31) / 32));
     if (grid.y > 65535) throw std::invalid_argument("transpose: too many columns");
@@ -180,6 +181,7 @@ void gather_cols(Ctx& c, int64_t rows, int64_t cols, const double* src, int64_t 
 
 double frob_diff(Ctx& c, int64_t rows, int64_t cols, const double* A, int64_t lda,
                  const double* B, int64_t ldb) {
+    StageTimer _t(c, "probe_norm");
     if (rows <= 0 || cols <= 0) return 0.0;
     int blocks = std::min(grid_for(c, rows * cols), 256);
     DBuf part = dalloc(c, size_t(blocks) + 1);
@@ -193,3 +195,68 @@ double frob_diff(Ctx& c, int64_t rows, int64_t cols, const double* A, int64_t ld
 }
 
 }  // namespace hydot
+
+// ------------------------------------------------------------ profiling --
+#include <chrono>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+
+namespace hydot {
+namespace {
+std::mutex g_prof_mu;
+std::map<std::string, std::pair<double, long>>& prof_table() {
+    static std::map<std::string, std::pair<double, long>> t;
+    return t;
+}
+bool prof_on() {
+    static int on = [] {
+        const char* e = std::getenv("HYDOT_PROFILE");
+        return (e && e[0] == '1') ? 1 : 0;
+    }();
+    return on != 0;
+}
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+thread_local int g_depth = 0;
+}  // namespace
+
+StageTimer::StageTimer(Ctx& c, const char* name) : c_(c), name_(name) {
+    on_ = prof_on() && g_depth == 0;
+    ++g_depth;
+    if (on_) {
+        c_.sync();
+        t0_ = now_s();
+    }
+}
+StageTimer::~StageTimer() {
+    --g_depth;
+    if (!on_) return;
+    cudaStreamSynchronize(c_.stream);
+    double dt = now_s() - t0_;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    auto& e = prof_table()[name_];
+    e.first += dt;
+    e.second += 1;
+}
+}  // namespace hydot
+
+extern "C" int hydot_profile_dump(char* buf, int len) {
+    std::lock_guard<std::mutex> lk(hydot::g_prof_mu);
+    std::string s = "{";
+    bool first = true;
+    for (auto& kv : hydot::prof_table()) {
+        char tmp[256];
+        snprintf(tmp, sizeof tmp, "%s\"%s\": [%.6f, %ld]", first ? "" : ", ", kv.first.c_str(),
+                 kv.second.first, kv.second.second);
+        s += tmp;
+        first = false;
+    }
+    s += "}";
+    hydot::prof_table().clear();
+    if (buf && len > 0) {
+        snprintf(buf, size_t(len), "%s", s.c_str());
+    }
+    return int(s.size());
+}
