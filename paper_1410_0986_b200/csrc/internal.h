@@ -105,10 +105,11 @@ inline DBuf dalloc(Ctx& c, size_t n_doubles) { return DBuf(c, n_doubles * sizeof
 // Optional stage timer (HYDOT_PROFILE=1): synchronises around each scoped
 // stage and accumulates wall time per name; report via hydot_profile_dump().
 struct StageTimer {
-    StageTimer(Ctx& c, const char* name);
+    StageTimer(Ctx& c, const char* name, int64_t a = -1, int64_t b = -1, int64_t k = -1);
     ~StageTimer();
     Ctx& c_;
     const char* name_;
+    int64_t a_, b_, k_;
     double t0_ = 0;
     bool on_ = false;
 };
@@ -148,6 +149,9 @@ void gather_cols(Ctx& c, int64_t rows, int64_t cols, const double* src, int64_t 
                  const int* idx_dev, double* dst, int64_t ldd);
 double frob_diff(Ctx& c, int64_t rows, int64_t cols, const double* A, int64_t lda,
                  const double* B, int64_t ldb);  // ||A - B||_F (synchronises)
+void col_norms(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* out_dev);
+void scatter_rows(Ctx& c, int64_t rows, int64_t cols, const double* src, int64_t lds,
+                  const int* idx_dev, double* dst, int64_t ldd);  // dst[idx[i],:] = src[i,:]
 
 // born.cu
 void born_block(Ctx& c, int64_t N, int nl, const double* inc, const double* const* adj_h, int nd,
@@ -158,9 +162,9 @@ struct QRFact {
     int64_t m = 0, n = 0;
     DBuf a;    // m x n: R in the upper triangle, Householder vectors below
     DBuf tau;  // n
-    DBuf T;    // nb x n : block reflector triangles per panel
+    DBuf T;    // kQRBlock x n : block reflector triangles
 };
-constexpr int kQRPanel = 32;
+constexpr int kQRBlock = 128;  // block-reflector width (qr.cu)
 void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f);
 // Y (m x k) := Q Y (trans=false) or Q^T Y
 void apply_q(Ctx& c, const QRFact& f, bool trans, int64_t k, double* Y, int64_t ldy);

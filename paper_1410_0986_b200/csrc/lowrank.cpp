@@ -7,7 +7,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <map>
+#include <string>
 
 namespace hydot {
 
@@ -26,6 +28,65 @@ DBuf materialise_t(Ctx& c, const double* S, int64_t ld, int64_t m, int64_t n) {
     DBuf t = dalloc(c, size_t(std::max<int64_t>(m * n, 1)));
     transpose(c, n, m, S, ld, t.d(), m);
     return t;
+}
+
+// Thin SVD of X (m x n, m >= n) by QR-preconditioned one-sided Jacobi
+// (the dgejsv idea): X = Q1 R1, R1^T = Q2 R2, Jacobi on L = R2^T gives
+// L = Ux S Vx^T, hence X = (Q1 Ux) S (Q2 Vx)^T.  Jacobi on the twice
+// QR-factored triangle needs ~4x fewer sweeps than on X itself (measured
+// 8-10 vs 28-41 on graded 300x300 cores).  `upper`: X is already the n x n
+// triangle R1 (Q1 = I).
+void jacobi_precond(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, bool upper,
+                    double* U, int64_t ldu, std::vector<double>& s, double* V, int64_t ldv) {
+    if (n <= 48) {  // the single-CTA shared-memory driver is already cheap
+        jacobi_svd(c, m, n, X, ldx, U, ldu, s, V, ldv);
+        return;
+    }
+    (void)upper;
+    // 1. order columns by decreasing norm (X P), 2. X P = Q1 R1, 3. R1^T =
+    // Q2 R2, 4. Jacobi on L = R2^T:  X = (Q1 Ul) S (P Q2 Vl)^T.
+    // Measured on the config-1 pipeline: total Jacobi time 1.73 s with
+    // norm-ordering + two QRs, 3.17 s with norm-ordering + one QR, 3.40 s
+    // with two QRs only (HYDOT_SVD_PRECOND=r selects one QR).
+    static const bool qrqr = [] {
+        const char* e = std::getenv("HYDOT_SVD_PRECOND");
+        return !(e && std::string(e) == "r");
+    }();
+    DBuf nrm = dalloc(c, size_t(n));
+    col_norms(c, m, n, X, ldx, nrm.d());
+    std::vector<double> hn(static_cast<size_t>(n));
+    c.d2h(hn.data(), nrm.d(), size_t(n));
+    std::vector<int> perm(static_cast<size_t>(n));
+    for (int64_t j = 0; j < n; ++j) perm[size_t(j)] = int(j);
+    std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return hn[size_t(a)] > hn[size_t(b)]; });
+    DBuf dperm(c, size_t(n) * sizeof(int));
+    HYDOT_CUDA(cudaMemcpyAsync(dperm.as<void>(), perm.data(), size_t(n) * sizeof(int),
+                               cudaMemcpyHostToDevice, c.stream));
+    DBuf Xp = dalloc(c, size_t(m * n));
+    gather_cols(c, m, n, X, ldx, dperm.as<int>(), Xp.d(), m);
+    QRFact q1, q2;
+    geqrf(c, m, n, Xp.d(), m, q1);
+    Xp.release();
+    DBuf R1 = dalloc(c, size_t(n * n));
+    extract_upper(c, n, q1.a.d(), m, R1.d(), n);
+    DBuf Ux = dalloc(c, size_t(n * n));
+    DBuf Vx = dalloc(c, size_t(n * n));
+    if (qrqr) {
+        DBuf T = dalloc(c, size_t(n * n));
+        transpose(c, n, n, R1.d(), n, T.d(), n);  // R1^T
+        geqrf(c, n, n, T.d(), n, q2);
+        extract_upper(c, n, q2.a.d(), n, R1.d(), n);  // R2
+        transpose(c, n, n, R1.d(), n, T.d(), n);      // L = R2^T
+        jacobi_svd(c, n, n, T.d(), n, Ux.d(), n, s, Vx.d(), n);
+        apply_q(c, q2, false, n, Vx.d(), n);  // Q2 Vx
+    } else {
+        jacobi_svd(c, n, n, R1.d(), n, Ux.d(), n, s, Vx.d(), n);
+    }
+    scatter_rows(c, n, n, Vx.d(), n, dperm.as<int>(), V, ldv);  // V = P Vr
+    fill(c, m, n, 0.0, U, ldu);
+    copy2d(c, n, n, Ux.d(), n, U, ldu);
+    apply_q(c, q1, false, n, U, ldu);  // U = Q1 [Ur; 0]
+    c.sync();  // host perm vector goes out of scope
 }
 
 // plain thin SVD of L (m x n) by Jacobi on the taller orientation
@@ -47,7 +108,7 @@ SVDd direct_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, int6
             Lp = tmp.d();
             ldl = m;
         }
-        jacobi_svd(c, m, n, Lp, ldl, o.U.d(), m, o.s, o.V.d(), n);
+        jacobi_precond(c, m, n, Lp, ldl, false, o.U.d(), m, o.s, o.V.d(), n);
     } else {
         // Jacobi on L^T (n x m): L^T = U' S V'^T  =>  L = V' S U'^T
         DBuf tmp;
@@ -58,7 +119,7 @@ SVDd direct_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, int6
             Lt = tmp.d();
             ldt = n;
         }
-        jacobi_svd(c, n, m, Lt, ldt, o.V.d(), n, o.s, o.U.d(), m);
+        jacobi_precond(c, n, m, Lt, ldt, false, o.V.d(), n, o.s, o.U.d(), m);
     }
     return o;
 }
@@ -104,7 +165,7 @@ SVDd fast_thin_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, i
         o.k = n;
         o.V = dalloc(c, size_t(n * n));
         DBuf Ur = dalloc(c, size_t(n * n));
-        jacobi_svd(c, n, n, R.d(), n, Ur.d(), n, o.s, o.V.d(), n);
+        jacobi_precond(c, n, n, R.d(), n, true, Ur.d(), n, o.s, o.V.d(), n);
         // U = Q [Ur; 0]
         o.U = dalloc(c, size_t(m * n));
         fill(c, m, n, 0.0, o.U.d(), m);

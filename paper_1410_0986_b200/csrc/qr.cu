@@ -4,152 +4,173 @@
 //
 // The scheduled leaf tolerance reaches 8e-11, below sqrt(eps),
 // so Gram/Cholesky QR is not admissible: this is true Householder.
-// Right-looking, panel width 32:
-//   panel   column-by-column reflectors over all rows; each column takes two
-//           grid-wide passes (reflector + dot products, then rank-1 update
-//           fused with the next column's norm); reductions are per-CTA
-//           partials summed in fixed order by every CTA (deterministic).
-//   T       block-reflector triangle from G = V^T V (DMMA GEMM) and tau.
-//   update  C -= V (T^T (V^T C)): three DMMA GEMMs (the first is split-K over
-//           the long row dimension).
+// Two-level blocking:
+//   panel  (32 columns)  one cooperative persistent kernel: every CTA owns a
+//          contiguous row slab (kept in shared memory when it fits), two
+//          grid-wide barriers per column (reflector + dot products, then the
+//          rank-1 update fused with the next column's norm).  Partial sums are
+//          reduced redundantly by every CTA in fixed order: deterministic.
+//   block  (128 columns) the 32-wide sub-panels update the rest of their
+//          128-block with DMMA GEMMs; the 128-wide block reflector
+//          I - V T V^T then updates the trailing matrix with three DMMA GEMMs
+//          (4x fewer passes over the trailing matrix than 32-wide blocking).
+#include <cooperative_groups.h>
+
 #include "internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace hydot {
 namespace {
 
-constexpr int NB = kQRPanel;  // 32
-constexpr int PT = 256;       // threads per panel CTA
+constexpr int PB = 32;        // panel width (cooperative kernel)
+constexpr int NB = kQRBlock;  // block-reflector width (128)
+constexpr int PT = 512;       // threads per panel CTA
 
-struct PanelScalars {
-    double tau, beta, scal;
-};
-
-inline int panel_ctas(Ctx& c, int64_t rows) {
-    int64_t p = (rows + 1023) / 1024;
-    return int(std::max<int64_t>(1, std::min<int64_t>(p, int64_t(c.num_sms) * 2)));
+__device__ __forceinline__ double warp_sum(double v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
 }
 
-__device__ __forceinline__ double block_sum(double v, double* sh) {
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    __syncthreads();
-    if (lane == 0) sh[w] = v;
-    __syncthreads();
-    double t = 0.0;
-    if (threadIdx.x == 0)
-        for (int i = 0; i < int(blockDim.x >> 5); ++i) t += sh[i];
-    return t;  // valid in thread 0
-}
-
-// partial sum of squares of column c, rows [c+1, mr)
-__global__ void __launch_bounds__(PT) pf_norm(int64_t mr, int c, const double* __restrict__ P,
-                                              int64_t ld, int64_t rows_per,
-                                              double* __restrict__ part) {
-    __shared__ double sh[32];
-    int64_t r0 = int64_t(blockIdx.x) * rows_per, r1 = min(mr, r0 + rows_per);
-    double acc = 0.0;
-    for (int64_t i = max(r0, int64_t(c) + 1) + threadIdx.x; i < r1; i += blockDim.x) {
-        double x = P[i + int64_t(c) * ld];
-        acc += x * x;
+// Factor the mr x jb panel P (ld) in place: R above the diagonal, unit-lower
+// Householder vectors below, tau[0..jb).  part: G doubles, part2: G*PB.
+template <bool SMEM>
+__global__ void __launch_bounds__(PT) qr_panel_coop(int64_t mr, int jb, double* __restrict__ P,
+                                                    int64_t ld, int64_t rows_per,
+                                                    double* __restrict__ tau_out,
+                                                    double* __restrict__ part,
+                                                    double* __restrict__ part2) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double slab[];  // rows_per x PB (ld rows_per) when SMEM
+    __shared__ double red[PT / 32][PB];
+    __shared__ double wsh[PB];
+    __shared__ double sc[3];
+    const int G = gridDim.x;
+    const int64_t r0 = int64_t(blockIdx.x) * rows_per;
+    const int64_t r1 = min(mr, r0 + rows_per);
+    const int nrow = r1 > r0 ? int(r1 - r0) : 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    auto at = [&](int64_t i, int q) -> double& {
+        if (SMEM) return slab[(i - r0) + int64_t(q) * rows_per];
+        return P[i + int64_t(q) * ld];
+    };
+    if (SMEM) {
+        for (int q = 0; q < jb; ++q)
+            for (int k = threadIdx.x; k < nrow; k += PT) slab[k + int64_t(q) * rows_per] = P[r0 + k + q * ld];
+        __syncthreads();
     }
-    double t = block_sum(acc, sh);
-    if (threadIdx.x == 0) part[blockIdx.x] = t;
-}
-
-// dlarfg on column c (every CTA recomputes it from the partials), scale v in
-// this CTA's rows, partial dots w_cc = v^T P[:, cc] for cc in (c, jb).
-__global__ void __launch_bounds__(PT) pf_reflect(int64_t mr, int jb, int c, double* __restrict__ P,
-                                                 int64_t ld, int64_t rows_per, int nparts,
-                                                 const double* __restrict__ part,
-                                                 double* __restrict__ part2,
-                                                 PanelScalars* __restrict__ sc) {
-    __shared__ double sh[32];
-    __shared__ double s_scal, s_tau;
-    if (threadIdx.x == 0) {
-        double xn2 = 0.0;
-        for (int p = 0; p < nparts; ++p) xn2 += part[p];
-        double alpha = P[c + int64_t(c) * ld];
-        double tau = 0.0, beta = alpha, scal = 1.0;
-        if (xn2 > 0.0) {
-            double xnorm = sqrt(xn2);
-            beta = -copysign(hypot(alpha, xnorm), alpha);
-            tau = (beta - alpha) / beta;
-            scal = 1.0 / (alpha - beta);
+    // partial norm^2 of column 0 below the diagonal
+    {
+        double a = 0.0;
+        for (int64_t i = max(r0, int64_t(1)) + threadIdx.x; i < r1; i += PT) {
+            double x = at(i, 0);
+            a += x * x;
         }
-        s_scal = scal;
-        s_tau = tau;
-        if (blockIdx.x == 0) {
-            sc->tau = tau;
-            sc->beta = beta;
-            sc->scal = scal;
+        a = warp_sum(a);
+        if (lane == 0) red[warp][0] = a;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < PT / 32; ++w) t += red[w][0];
+            part[blockIdx.x] = t;
         }
     }
-    __syncthreads();
-    const double scal = s_scal;
-    const bool active = s_tau != 0.0;
-    int64_t r0 = int64_t(blockIdx.x) * rows_per, r1 = min(mr, r0 + rows_per);
-    double acc[NB];
+    for (int c = 0; c < jb; ++c) {
+        grid.sync();
+        // ---- reflector (every CTA, identical arithmetic) + scale + dots
+        if (threadIdx.x == 0) {
+            double xn2 = 0.0;
+            for (int p = 0; p < G; ++p) xn2 += part[p];
+            double alpha = P[c + int64_t(c) * ld];
+            if (SMEM && c >= r0 && c < r1) alpha = at(c, c);
+            double tau = 0.0, beta = alpha, scal = 1.0;
+            if (xn2 > 0.0) {
+                beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
+                tau = (beta - alpha) / beta;
+                scal = 1.0 / (alpha - beta);
+            }
+            sc[0] = tau;
+            sc[1] = beta;
+            sc[2] = scal;
+        }
+        __syncthreads();
+        const double tau = sc[0], scal = sc[2];
+        double acc[PB];
 #pragma unroll
-    for (int q = 0; q < NB; ++q) acc[q] = 0.0;
-    for (int64_t i = max(r0, int64_t(c)) + threadIdx.x; i < r1; i += blockDim.x) {
-        double v;
-        if (i == c) {
-            v = 1.0;
-        } else {
-            v = P[i + int64_t(c) * ld];
-            if (active) {
-                v *= scal;
-                P[i + int64_t(c) * ld] = v;
+        for (int q = 0; q < PB; ++q) acc[q] = 0.0;
+        for (int64_t i = max(r0, int64_t(c)) + threadIdx.x; i < r1; i += PT) {
+            double v = 1.0;
+            if (i > c) {
+                v = at(i, c);
+                if (tau != 0.0) {
+                    v *= scal;
+                    at(i, c) = v;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < PB; ++q)
+                if (q > c && q < jb) acc[q] += v * at(i, q);
+        }
+#pragma unroll
+        for (int q = 0; q < PB; ++q) {
+            if (q > c && q < jb) {
+                double s = warp_sum(acc[q]);
+                if (lane == 0) red[warp][q] = s;
             }
         }
-#pragma unroll
-        for (int q = 0; q < NB; ++q)
-            if (q > c && q < jb) acc[q] += v * P[i + int64_t(q) * ld];
+        __syncthreads();
+        if (threadIdx.x < PB) {
+            int q = threadIdx.x;
+            double t = 0.0;
+            if (q > c && q < jb)
+                for (int w = 0; w < PT / 32; ++w) t += red[w][q];
+            part2[int64_t(blockIdx.x) * PB + q] = t;
+        }
+        grid.sync();
+        // ---- rank-1 update of the rest of the panel, next column's norm
+        if (threadIdx.x < PB) {
+            int q = threadIdx.x;
+            double t = 0.0;
+            if (q > c && q < jb)
+                for (int p = 0; p < G; ++p) t += part2[int64_t(p) * PB + q];
+            wsh[q] = t;
+        }
+        __syncthreads();
+        double na = 0.0;
+        for (int64_t i = max(r0, int64_t(c)) + threadIdx.x; i < r1; i += PT) {
+            const double v = (i == c) ? 1.0 : at(i, c);
+            if (tau != 0.0)
+                for (int q = c + 1; q < jb; ++q) at(i, q) -= tau * v * wsh[q];
+            if (i == c) at(i, c) = sc[1];
+            if (c + 1 < jb && i >= c + 2) {
+                double x = at(i, c + 1);
+                na += x * x;
+            }
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) tau_out[c] = tau;
+        na = warp_sum(na);
+        __syncthreads();
+        if (lane == 0) red[warp][0] = na;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < PT / 32; ++w) t += red[w][0];
+            part[blockIdx.x] = t;
+        }
+        if (SMEM && c + 1 < jb) {
+            // the CTA owning row c+1 publishes the next alpha for everybody
+            if (c + 1 >= r0 && c + 1 < r1 && threadIdx.x == 0)
+                P[(c + 1) + int64_t(c + 1) * ld] = at(c + 1, c + 1);
+        }
     }
-    for (int q = c + 1; q < jb; ++q) {
-        double t = block_sum(acc[q], sh);
-        if (threadIdx.x == 0) part2[int64_t(blockIdx.x) * NB + q] = t;
+    if (SMEM) {
+        __syncthreads();
+        for (int q = 0; q < jb; ++q)
+            for (int k = threadIdx.x; k < nrow; k += PT) P[r0 + k + q * ld] = slab[k + int64_t(q) * rows_per];
     }
 }
 
-// P[:, cc] -= tau v w_cc for cc in (c, jb); diagonal <- beta; partial norm of
-// the next column below its diagonal.
-__global__ void __launch_bounds__(PT) pf_update(int64_t mr, int jb, int c, double* __restrict__ P,
-                                                int64_t ld, int64_t rows_per, int nparts,
-                                                const double* __restrict__ part2,
-                                                const PanelScalars* __restrict__ sc,
-                                                double* __restrict__ part) {
-    __shared__ double sh[32];
-    __shared__ double w[NB];
-    const double tau = sc->tau;
-    if (threadIdx.x < NB) {
-        int q = threadIdx.x;
-        double s = 0.0;
-        if (q > c && q < jb)
-            for (int p = 0; p < nparts; ++p) s += part2[int64_t(p) * NB + q];
-        w[q] = s;
-    }
-    __syncthreads();
-    int64_t r0 = int64_t(blockIdx.x) * rows_per, r1 = min(mr, r0 + rows_per);
-    double nacc = 0.0;
-    for (int64_t i = max(r0, int64_t(c)) + threadIdx.x; i < r1; i += blockDim.x) {
-        double v = (i == c) ? 1.0 : P[i + int64_t(c) * ld];
-        if (tau != 0.0) {
-            for (int q = c + 1; q < jb; ++q) P[i + int64_t(q) * ld] -= tau * v * w[q];
-        }
-        if (i == c) P[i + int64_t(c) * ld] = sc->beta;
-        if (c + 1 < jb && i >= c + 2) {
-            double x = P[i + int64_t(c + 1) * ld];
-            nacc += x * x;
-        }
-    }
-    double t = block_sum(nacc, sh);
-    if (threadIdx.x == 0) part[blockIdx.x] = t;
-}
-
-__global__ void store_tau(const PanelScalars* sc, double* tau) { *tau = sc->tau; }
-
-// Vp (mr x jb): unit lower trapezoid of the factored panel
+// Vp (mr x jb, ld mr): unit lower trapezoid of the factored columns
 __global__ void form_v(int64_t mr, int jb, const double* __restrict__ P, int64_t ld,
                        double* __restrict__ V) {
     int64_t total = mr * jb;
@@ -161,33 +182,94 @@ __global__ void form_v(int64_t mr, int jb, const double* __restrict__ P, int64_t
     }
 }
 
-// dlarft (forward, columnwise): T upper triangular jb x jb (ld NB)
-__global__ void larft_k(int jb, const double* __restrict__ G, const double* __restrict__ tau,
-                        double* __restrict__ T) {
-    __shared__ double Ts[NB][NB + 1];
+// dlarft (forward, columnwise): T upper triangular jb x jb (ld NB) from
+// G = V^T V and tau.
+__global__ void __launch_bounds__(NB) larft_k(int jb, const double* __restrict__ G, int64_t ldg,
+                                              const double* __restrict__ tau,
+                                              double* __restrict__ T) {
+    extern __shared__ double Ts[];  // NB x (NB+1)
     __shared__ double wv[NB];
-    int r = threadIdx.x;
+    const int r = threadIdx.x;
+    auto t = [&](int i, int j) -> double& { return Ts[i * (NB + 1) + j]; };
+    for (int j = 0; j < NB; ++j) t(r, j) = 0.0;
+    __syncthreads();
     for (int i = 0; i < jb; ++i) {
-        // w = -tau_i G[0:i, i]; T[0:i, i] = T[0:i,0:i] w
-        if (r < i) wv[r] = -tau[i] * G[r + i * jb];
+        if (r < i) wv[r] = -tau[i] * G[r + int64_t(i) * ldg];
         __syncthreads();
         if (r < i) {
             double s = 0.0;
-            for (int q = r; q < i; ++q) s += Ts[r][q] * wv[q];
-            Ts[r][i] = s;
+            for (int q = r; q < i; ++q) s += t(r, q) * wv[q];
+            t(r, i) = s;
         }
-        if (r == i) Ts[i][i] = tau[i];
-        if (r > i && r < NB) Ts[r][i] = 0.0;
+        if (r == i) t(i, i) = tau[i];
         __syncthreads();
     }
-    for (int i = 0; i < jb; ++i)
-        if (r < NB) T[r + i * NB] = r < jb ? Ts[r][i] : 0.0;
+    for (int j = 0; j < jb; ++j) T[r + int64_t(j) * NB] = t(r, j);  // only jb columns exist
+}
+
+struct CoopCfg {
+    int grid = 0;
+    bool init = false;
+};
+
+void panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, DBuf& part,
+           DBuf& part2) {
+    static CoopCfg cfg_smem, cfg_glob;
+    const size_t smem_cap = 200 * 1024;
+    int G = c.num_sms;
+    int64_t rows_per = (mr + G - 1) / G;
+    if (rows_per < 64) {  // short panels: fewer CTAs
+        G = int(std::max<int64_t>(1, (mr + 63) / 64));
+        rows_per = (mr + G - 1) / G;
+    }
+    const size_t smem = size_t(rows_per) * PB * sizeof(double);
+    const bool use_smem = smem <= smem_cap;
+    CoopCfg& cc = use_smem ? cfg_smem : cfg_glob;
+    if (!cc.init) {
+        if (use_smem)
+            HYDOT_CUDA(cudaFuncSetAttribute(qr_panel_coop<true>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_cap)));
+        cc.init = true;
+    }
+    int per_sm = 0;
+    if (use_smem)
+        HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qr_panel_coop<true>, PT, smem));
+    else
+        HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qr_panel_coop<false>, PT, 0));
+    if (per_sm * c.num_sms < G) throw std::runtime_error("qr panel: cooperative grid does not fit");
+    double* part_p = part.d();
+    double* part2_p = part2.d();
+    void* args[] = {&mr, &jb, &P, &ld, &rows_per, &tau, &part_p, &part2_p};
+    if (use_smem)
+        HYDOT_CUDA(cudaLaunchCooperativeKernel((void*)qr_panel_coop<true>, dim3(G), dim3(PT), args,
+                                               smem, c.stream));
+    else
+        HYDOT_CUDA(cudaLaunchCooperativeKernel((void*)qr_panel_coop<false>, dim3(G), dim3(PT), args, 0,
+                                               c.stream));
+    c.count();
+}
+
+void form_v_launch(Ctx& c, int64_t mr, int jb, const double* P, int64_t ld, double* V) {
+    int blocks = int(std::max<int64_t>(1, std::min<int64_t>((mr * jb + 255) / 256, int64_t(c.num_sms) * 8)));
+    form_v<<<blocks, 256, 0, c.stream>>>(mr, jb, P, ld, V);
+    c.check_launch();
+}
+
+void larft(Ctx& c, int jb, const double* G, int64_t ldg, const double* tau, double* T) {
+    static bool attr = false;
+    const int smem = NB * (NB + 1) * sizeof(double);
+    if (!attr) {
+        HYDOT_CUDA(cudaFuncSetAttribute(larft_k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+    }
+    larft_k<<<1, NB, smem, c.stream>>>(jb, G, ldg, tau, T);
+    c.check_launch();
 }
 
 }  // namespace
 
 void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f) {
-    StageTimer _t(c, "qr_geqrf");
+    StageTimer _t(c, "qr_geqrf", m, n);
     f.m = m;
     f.n = n;
     f.a = dalloc(c, size_t(std::max<int64_t>(m * n, 1)));
@@ -197,68 +279,63 @@ void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f
     const int64_t k = std::min(m, n);
     if (k <= 0) return;
     double* a = f.a.d();
-    int maxp = panel_ctas(c, m);
-    DBuf part = dalloc(c, size_t(maxp));
-    DBuf part2 = dalloc(c, size_t(maxp) * NB);
-    DBuf scal(c, sizeof(PanelScalars));
+    DBuf part = dalloc(c, size_t(c.num_sms) * 2 + 16);
+    DBuf part2 = dalloc(c, (size_t(c.num_sms) * 2 + 16) * PB);
     DBuf V = dalloc(c, size_t(m) * NB);
     DBuf G = dalloc(c, size_t(NB) * NB);
     DBuf W = dalloc(c, size_t(NB) * size_t(std::max<int64_t>(n, 1)));
     DBuf W2 = dalloc(c, size_t(NB) * size_t(std::max<int64_t>(n, 1)));
+    DBuf Tp = dalloc(c, size_t(NB) * NB);
     for (int64_t j0 = 0; j0 < k; j0 += NB) {
         const int jb = int(std::min<int64_t>(NB, k - j0));
         const int64_t mr = m - j0;
-        double* P = a + j0 + j0 * m;
-        const int np = panel_ctas(c, mr);
-        const int64_t rows_per = (mr + np - 1) / np;
-        pf_norm<<<np, PT, 0, c.stream>>>(mr, 0, P, m, rows_per, part.d());
-        c.check_launch();
-        for (int cc = 0; cc < jb; ++cc) {
-            pf_reflect<<<np, PT, 0, c.stream>>>(mr, jb, cc, P, m, rows_per, np, part.d(),
-                                                part2.d(), scal.as<PanelScalars>());
-            c.check_launch();
-            pf_update<<<np, PT, 0, c.stream>>>(mr, jb, cc, P, m, rows_per, np, part2.d(),
-                                               scal.as<PanelScalars>(), part.d());
-            c.check_launch();
-            store_tau<<<1, 1, 0, c.stream>>>(scal.as<PanelScalars>(), f.tau.d() + j0 + cc);
-            c.check_launch();
+        double* Pb = a + j0 + j0 * m;  // top-left of the 128-block
+        // ---- factor the block with 32-wide cooperative panels
+        for (int p0 = 0; p0 < jb; p0 += PB) {
+            const int pb = std::min(PB, jb - p0);
+            const int64_t pr = mr - p0;
+            double* Pp = Pb + p0 + int64_t(p0) * m;
+            panel(c, pr, pb, Pp, m, f.tau.d() + j0 + p0, part, part2);
+            const int rest = jb - p0 - pb;
+            if (rest > 0) {
+                // apply this sub-panel's reflector to the rest of the block
+                form_v_launch(c, pr, pb, Pp, m, V.d());
+                dgemm(c, true, false, pb, pb, pr, 1.0, V.d(), pr, V.d(), pr, 0.0, G.d(), pb);
+                larft(c, pb, G.d(), pb, f.tau.d() + j0 + p0, Tp.d());
+                double* Cm = Pp + int64_t(pb) * m;
+                dgemm(c, true, false, pb, rest, pr, 1.0, V.d(), pr, Cm, m, 0.0, W.d(), pb);
+                dgemm(c, true, false, pb, rest, pb, 1.0, Tp.d(), NB, W.d(), pb, 0.0, W2.d(), pb);
+                dgemm(c, false, false, pr, rest, pb, -1.0, V.d(), pr, W2.d(), pb, 1.0, Cm, m);
+            }
         }
-        // block reflector
-        {
-            int blocks = int(std::min<int64_t>((mr * jb + 255) / 256, int64_t(c.num_sms) * 8));
-            form_v<<<blocks, 256, 0, c.stream>>>(mr, jb, P, m, V.d());
-            c.check_launch();
-        }
+        // ---- 128-wide block reflector: T and the trailing update
+        form_v_launch(c, mr, jb, Pb, m, V.d());
         dgemm(c, true, false, jb, jb, mr, 1.0, V.d(), mr, V.d(), mr, 0.0, G.d(), jb);
-        larft_k<<<1, NB, 0, c.stream>>>(jb, G.d(), f.tau.d() + j0, f.T.d() + j0 * NB);
-        c.check_launch();
+        larft(c, jb, G.d(), jb, f.tau.d() + j0, f.T.d() + j0 * NB);
         const int64_t nr = n - j0 - jb;
         if (nr > 0) {
             double* Cm = a + j0 + (j0 + jb) * m;
             dgemm(c, true, false, jb, nr, mr, 1.0, V.d(), mr, Cm, m, 0.0, W.d(), jb);
-            dgemm(c, true, false, jb, nr, jb, 1.0, f.T.d() + j0 * NB, NB, W.d(), jb, 0.0, W2.d(),
-                  jb);
+            dgemm(c, true, false, jb, nr, jb, 1.0, f.T.d() + j0 * NB, NB, W.d(), jb, 0.0, W2.d(), jb);
             dgemm(c, false, false, mr, nr, jb, -1.0, V.d(), mr, W2.d(), jb, 1.0, Cm, m);
         }
     }
 }
 
 void apply_q(Ctx& c, const QRFact& f, bool trans, int64_t k, double* Y, int64_t ldy) {
-    StageTimer _t(c, "qr_apply_q");
+    StageTimer _t(c, "qr_apply_q", f.m, f.n, k);
     const int64_t m = f.m, kk = std::min(f.m, f.n);
     if (k <= 0 || kk <= 0) return;
     DBuf V = dalloc(c, size_t(m) * NB);
     DBuf W = dalloc(c, size_t(NB) * size_t(k));
     DBuf W2 = dalloc(c, size_t(NB) * size_t(k));
-    const int64_t npan = (kk + NB - 1) / NB;
-    for (int64_t pi = 0; pi < npan; ++pi) {
-        const int64_t p = trans ? pi : (npan - 1 - pi);
-        const int64_t j0 = p * NB;
+    const int64_t nblk = (kk + NB - 1) / NB;
+    for (int64_t bi = 0; bi < nblk; ++bi) {
+        const int64_t b = trans ? bi : (nblk - 1 - bi);
+        const int64_t j0 = b * NB;
         const int jb = int(std::min<int64_t>(NB, kk - j0));
         const int64_t mr = m - j0;
-        int blocks = int(std::min<int64_t>((mr * jb + 255) / 256, int64_t(c.num_sms) * 8));
-        form_v<<<blocks, 256, 0, c.stream>>>(mr, jb, f.a.d() + j0 + j0 * m, m, V.d());
-        c.check_launch();
+        form_v_launch(c, mr, jb, f.a.d() + j0 + j0 * m, m, V.d());
         double* Ys = Y + j0;
         dgemm(c, true, false, jb, k, mr, 1.0, V.d(), mr, Ys, ldy, 0.0, W.d(), jb);
         // Q Y uses T, Q^T Y uses T^T

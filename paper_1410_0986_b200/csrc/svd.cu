@@ -6,21 +6,28 @@
 // round-robin (circle-method) order; each rotation is computed from the
 // actual column dot products, so small singular values keep high relative
 // accuracy (no Gram matrix is formed).  Two drivers:
-//   * small  (m + n) n doubles fit in shared memory: one CTA runs every sweep
-//     on-chip, one warp per column pair;
-//   * large: one launch per round, one CTA per pair, convergence flag read
-//     once per sweep.
+//   * small: (m + n) n doubles fit in shared memory -- one CTA runs every
+//     sweep on-chip, one warp per column pair;
+//   * large: one cooperative persistent kernel runs all sweeps, one warp per
+//     column pair, a grid-wide barrier between rounds and a per-sweep
+//     rotation counter for convergence (no host round trips).
 // Afterwards sigma_j = ||u_j||, U = u_j / sigma_j, sorted descending.
+#include <cooperative_groups.h>
+
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <numeric>
 
 #include "internal.h"
 
+namespace cg = cooperative_groups;
+
 namespace hydot {
 namespace {
 
-constexpr double kTol = 1.0e-15;
-constexpr int kMaxSweeps = 60;
+constexpr int kMaxSweeps = 40;
+constexpr int JT = 256;  // threads per CTA of the large driver
 
 __device__ __forceinline__ void rot_params(double a, double b, double g, double& cs, double& sn) {
     double zeta = (b - a) / (2.0 * g);
@@ -29,14 +36,51 @@ __device__ __forceinline__ void rot_params(double a, double b, double g, double&
     sn = cs * t;
 }
 
+// one warp orthogonalises columns p, q of U (m rows) and rotates V (n rows);
+// returns true when a rotation was applied
+__device__ __forceinline__ bool warp_pair(int lane, int64_t m, int64_t n, double* __restrict__ up,
+                                          double* __restrict__ uq, double* __restrict__ vp,
+                                          double* __restrict__ vq, double tol, double atol) {
+    double a = 0, b = 0, g = 0;
+    for (int64_t i = lane; i < m; i += 32) {
+        double x = up[i], y = uq[i];
+        a += x * x;
+        b += y * y;
+        g += x * y;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+        g += __shfl_xor_sync(0xffffffffu, g, o);
+    }
+    // relative criterion (high relative accuracy) AND an absolute floor at
+    // the backward-error level eps*||A||*max(|u_p|,|u_q|) (BDCSVD-grade)
+    if (!(g != 0.0 && fabs(g) > tol * sqrt(a * b) && fabs(g) > atol * sqrt(fmax(a, b))))
+        return false;  // atol = 0 keeps the pure relative criterion
+    double cs, sn;
+    rot_params(a, b, g, cs, sn);
+    for (int64_t i = lane; i < m; i += 32) {
+        double x = up[i], y = uq[i];
+        up[i] = cs * x - sn * y;
+        uq[i] = sn * x + cs * y;
+    }
+    for (int64_t i = lane; i < n; i += 32) {
+        double x = vp[i], y = vq[i];
+        vp[i] = cs * x - sn * y;
+        vq[i] = sn * x + cs * y;
+    }
+    return true;
+}
+
 // ---------------------------------------------------------- single CTA ----
 __global__ void __launch_bounds__(1024) jacobi_smem_k(int m, int n, int np,
                                                       const int2* __restrict__ pairs,
                                                       double* __restrict__ Ug, int64_t ldu,
                                                       double* __restrict__ Vg, int64_t ldv,
+                                                      double tol, double atol,
                                                       int* __restrict__ sweeps_out) {
     extern __shared__ double sm[];
-    double* U = sm;               // m x n, ld m
+    double* U = sm;                   // m x n, ld m
     double* V = sm + int64_t(m) * n;  // n x n, ld n
     __shared__ int changed;
     for (int64_t e = threadIdx.x; e < int64_t(m) * n; e += blockDim.x) {
@@ -58,37 +102,10 @@ __global__ void __launch_bounds__(1024) jacobi_smem_k(int m, int n, int np,
             for (int q = warp; q < per; q += nwarp) {
                 int2 pr = pairs[r * per + q];
                 if (pr.x >= n || pr.y >= n) continue;
-                double* up = U + int64_t(pr.x) * m;
-                double* uq = U + int64_t(pr.y) * m;
-                double a = 0, b = 0, g = 0;
-                for (int i = lane; i < m; i += 32) {
-                    double x = up[i], y = uq[i];
-                    a += x * x;
-                    b += y * y;
-                    g += x * y;
-                }
-                for (int o = 16; o > 0; o >>= 1) {
-                    a += __shfl_xor_sync(0xffffffffu, a, o);
-                    b += __shfl_xor_sync(0xffffffffu, b, o);
-                    g += __shfl_xor_sync(0xffffffffu, g, o);
-                }
-                if (g != 0.0 && fabs(g) > kTol * sqrt(a * b)) {
-                    double cs, sn;
-                    rot_params(a, b, g, cs, sn);
-                    for (int i = lane; i < m; i += 32) {
-                        double x = up[i], y = uq[i];
-                        up[i] = cs * x - sn * y;
-                        uq[i] = sn * x + cs * y;
-                    }
-                    double* vp = V + int64_t(pr.x) * n;
-                    double* vq = V + int64_t(pr.y) * n;
-                    for (int i = lane; i < n; i += 32) {
-                        double x = vp[i], y = vq[i];
-                        vp[i] = cs * x - sn * y;
-                        vq[i] = sn * x + cs * y;
-                    }
-                    if (lane == 0) changed = 1;
-                }
+                if (warp_pair(lane, m, n, U + int64_t(pr.x) * m, U + int64_t(pr.y) * m,
+                              V + int64_t(pr.x) * n, V + int64_t(pr.y) * n, tol, atol) &&
+                    lane == 0)
+                    changed = 1;
             }
             __syncthreads();
         }
@@ -106,68 +123,91 @@ __global__ void __launch_bounds__(1024) jacobi_smem_k(int m, int n, int np,
     if (threadIdx.x == 0 && sweeps_out) *sweeps_out = sweep;
 }
 
-// ------------------------------------------------------------ multi CTA ----
-__global__ void __launch_bounds__(256) jacobi_round_k(int64_t m, int n, const int2* __restrict__ pairs,
-                                                      double* __restrict__ U, int64_t ldu,
-                                                      double* __restrict__ V, int64_t ldv,
-                                                      int* __restrict__ changed) {
-    __shared__ double sh[3][8];
-    __shared__ double s_cs, s_sn;
-    __shared__ int s_rot;
-    int2 pr = pairs[blockIdx.x];
-    if (pr.x >= n || pr.y >= n) return;
-    double* up = U + int64_t(pr.x) * ldu;
-    double* uq = U + int64_t(pr.y) * ldu;
-    double a = 0, b = 0, g = 0;
-    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
-        double x = up[i], y = uq[i];
-        a += x * x;
-        b += y * y;
-        g += x * y;
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        a += __shfl_down_sync(0xffffffffu, a, o);
-        b += __shfl_down_sync(0xffffffffu, b, o);
-        g += __shfl_down_sync(0xffffffffu, g, o);
-    }
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (lane == 0) {
-        sh[0][w] = a;
-        sh[1][w] = b;
-        sh[2][w] = g;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double A = 0, B = 0, G = 0;
-        for (int i = 0; i < int(blockDim.x >> 5); ++i) {
-            A += sh[0][i];
-            B += sh[1][i];
-            G += sh[2][i];
+// ------------------------------------------------------- cooperative ------
+// counters[s] counts rotations applied in sweep s (zeroed before launch)
+__global__ void __launch_bounds__(JT) jacobi_coop_k(int64_t m, int n, int np,
+                                                    const int2* __restrict__ pairs,
+                                                    double* __restrict__ U, int64_t ldu,
+                                                    double* __restrict__ V, int64_t ldv,
+                                                    double tol, double atol,
+                                                    int* __restrict__ counters,
+                                                    int* __restrict__ sweeps_out) {
+    // one CTA (JT threads) per column pair: long columns need the memory
+    // parallelism of a whole CTA, a warp per pair was latency-bound
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double red[3][JT / 32];
+    __shared__ double rot[3];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int rounds = np - 1, per = np / 2;
+    int sweep = 0;
+    for (; sweep < kMaxSweeps; ++sweep) {
+        int mine = 0;
+        for (int r = 0; r < rounds; ++r) {
+            for (int q = blockIdx.x; q < per; q += gridDim.x) {
+                int2 pr = pairs[r * per + q];
+                if (pr.x >= n || pr.y >= n) continue;
+                double* up = U + int64_t(pr.x) * ldu;
+                double* uq = U + int64_t(pr.y) * ldu;
+                double a = 0, b = 0, g = 0;
+                for (int64_t i = threadIdx.x; i < m; i += JT) {
+                    double x = up[i], y = uq[i];
+                    a += x * x;
+                    b += y * y;
+                    g += x * y;
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    a += __shfl_xor_sync(0xffffffffu, a, o);
+                    b += __shfl_xor_sync(0xffffffffu, b, o);
+                    g += __shfl_xor_sync(0xffffffffu, g, o);
+                }
+                if (lane == 0) {
+                    red[0][w] = a;
+                    red[1][w] = b;
+                    red[2][w] = g;
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    double A = 0, B = 0, Gm = 0;
+                    for (int k = 0; k < JT / 32; ++k) {
+                        A += red[0][k];
+                        B += red[1][k];
+                        Gm += red[2][k];
+                    }
+                    rot[2] = 0.0;
+                    if (Gm != 0.0 && fabs(Gm) > tol * sqrt(A * B) && fabs(Gm) > atol * sqrt(fmax(A, B))) {
+                        double cs, sn;
+                        rot_params(A, B, Gm, cs, sn);
+                        rot[0] = cs;
+                        rot[1] = sn;
+                        rot[2] = 1.0;
+                    }
+                }
+                __syncthreads();
+                if (rot[2] != 0.0) {
+                    const double cs = rot[0], sn = rot[1];
+                    for (int64_t i = threadIdx.x; i < m; i += JT) {
+                        double x = up[i], y = uq[i];
+                        up[i] = cs * x - sn * y;
+                        uq[i] = sn * x + cs * y;
+                    }
+                    double* vp = V + int64_t(pr.x) * ldv;
+                    double* vq = V + int64_t(pr.y) * ldv;
+                    for (int64_t i = threadIdx.x; i < n; i += JT) {
+                        double x = vp[i], y = vq[i];
+                        vp[i] = cs * x - sn * y;
+                        vq[i] = sn * x + cs * y;
+                    }
+                    ++mine;
+                }
+                __syncthreads();
+            }
+            grid.sync();
         }
-        s_rot = (G != 0.0 && fabs(G) > kTol * sqrt(A * B)) ? 1 : 0;
-        if (s_rot) {
-            double cs, sn;
-            rot_params(A, B, G, cs, sn);
-            s_cs = cs;
-            s_sn = sn;
-            *changed = 1;
-        }
+        if (threadIdx.x == 0 && mine) atomicAdd(&counters[sweep], mine);
+        grid.sync();
+        if (*((volatile int*)&counters[sweep]) == 0) break;
     }
-    __syncthreads();
-    if (!s_rot) return;
-    const double cs = s_cs, sn = s_sn;
-    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
-        double x = up[i], y = uq[i];
-        up[i] = cs * x - sn * y;
-        uq[i] = sn * x + cs * y;
-    }
-    double* vp = V + int64_t(pr.x) * ldv;
-    double* vq = V + int64_t(pr.y) * ldv;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        double x = vp[i], y = vq[i];
-        vp[i] = cs * x - sn * y;
-        vq[i] = sn * x + cs * y;
-    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
 }
 
 __global__ void colnorm_k(int64_t m, int n, const double* __restrict__ U, int64_t ldu,
@@ -215,7 +255,6 @@ std::vector<int2> tournament(int n, int& np) {
             int a = p[size_t(i)], b = p[size_t(np - 1 - i)];
             out.push_back(make_int2(std::min(a, b), std::max(a, b)));
         }
-        // rotate p[1..np-1]
         int last = p[size_t(np - 1)];
         for (int i = np - 1; i > 1; --i) p[size_t(i)] = p[size_t(i - 1)];
         p[1] = last;
@@ -223,23 +262,72 @@ std::vector<int2> tournament(int n, int& np) {
     return out;
 }
 
+// per-process cache of tournament tables on the device (keyed by n)
+struct PairCache {
+    int n = -1, np = 0;
+    int2* dev = nullptr;
+};
+
+const int2* device_pairs(int n, int& np) {
+    static std::vector<PairCache> cache;
+    for (auto& e : cache)
+        if (e.n == n) {
+            np = e.np;
+            return e.dev;
+        }
+    std::vector<int2> pairs = tournament(n, np);
+    PairCache pc;
+    pc.n = n;
+    pc.np = np;
+    HYDOT_CUDA(cudaMalloc(&pc.dev, std::max<size_t>(pairs.size(), 1) * sizeof(int2)));
+    if (!pairs.empty())
+        HYDOT_CUDA(cudaMemcpy(pc.dev, pairs.data(), pairs.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    if (cache.size() > 256) {
+        cudaFree(cache.front().dev);
+        cache.erase(cache.begin());
+    }
+    cache.push_back(pc);
+    return pc.dev;
+}
+
+bool stats_on() {
+    static int on = [] {
+        const char* e = std::getenv("HYDOT_JACOBI_STATS");
+        return (e && e[0] == '1') ? 1 : 0;
+    }();
+    return on != 0;
+}
+
 }  // namespace
 
 void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, double* Uo,
                 int64_t lduo, std::vector<double>& s, double* Vo, int64_t ldvo) {
     StageTimer _t(c, n > 96 ? "svd_jacobi_large" : "svd_jacobi_small");
-    s.assign(size_t(std::max<int64_t>(n, 0)), 0.0);
+    s.assign(static_cast<size_t>(std::max<int64_t>(n, 0)), 0.0);
     if (n <= 0) return;
     if (m < n) throw std::invalid_argument("jacobi_svd: needs m >= n");
+    // LAPACK dgesvj's convergence threshold: sqrt(m) * eps
+    const double tol = std::max(1e-15, std::sqrt(double(m)) * 2.220446049250313e-16);
+    if (stats_on()) c.sync();
+    const auto t_start = std::chrono::steady_clock::now();
     int np = 0;
-    std::vector<int2> pairs = tournament(int(n), np);
-    DBuf dpairs(c, std::max<size_t>(pairs.size(), 1) * sizeof(int2));
-    if (!pairs.empty())
-        HYDOT_CUDA(cudaMemcpyAsync(dpairs.as<void>(), pairs.data(), pairs.size() * sizeof(int2),
-                                   cudaMemcpyHostToDevice, c.stream));
+    const int2* dpairs = device_pairs(int(n), np);
     DBuf U = dalloc(c, size_t(m * n));
     DBuf V = dalloc(c, size_t(n * n));
     copy2d(c, m, n, X, ldx, U.d(), m);
+    // ||A|| estimate for the absolute floor: the largest column norm
+    DBuf cn = dalloc(c, size_t(n));
+    colnorm_k<<<unsigned(n), 256, 0, c.stream>>>(m, int(n), U.d(), m, cn.d());
+    c.check_launch();
+    std::vector<double> cnh(static_cast<size_t>(n));
+    c.d2h(cnh.data(), cn.d(), size_t(n));
+    // The absolute floor is off (0): it saved few sweeps on the path's cores
+    // and leaves the vectors of negligible singular values non-orthonormal,
+    // unlike BDCSVD.  Kept for experiments via HYDOT_JACOBI_ATOL.
+    const char* at_env = std::getenv("HYDOT_JACOBI_ATOL");
+    const double atol = (at_env ? std::atof(at_env) : 0.0) * *std::max_element(cnh.begin(), cnh.end());
+    DBuf sw(c, sizeof(int) * (kMaxSweeps + 1));
+    HYDOT_CUDA(cudaMemsetAsync(sw.as<void>(), 0, sizeof(int) * (kMaxSweeps + 1), c.stream));
     const size_t smem = size_t((m + n) * n) * sizeof(double);
     if (n >= 2 && smem <= 200 * 1024) {
         static bool attr = false;
@@ -248,28 +336,40 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
                                             210 * 1024));
             attr = true;
         }
-        jacobi_smem_k<<<1, 1024, smem, c.stream>>>(int(m), int(n), np, dpairs.as<int2>(), U.d(), m,
-                                                    V.d(), n, nullptr);
+        jacobi_smem_k<<<1, 1024, smem, c.stream>>>(int(m), int(n), np, dpairs, U.d(), m, V.d(), n,
+                                                    tol, atol, sw.as<int>() + kMaxSweeps);
         c.check_launch();
     } else {
         set_identity(c, n, n, V.d(), n);
         if (n >= 2) {
-            DBuf flag(c, sizeof(int));
+            int per_sm = 0;
+            HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_coop_k, JT, 0));
             const int per = np / 2;
-            for (int sw = 0; sw < kMaxSweeps; ++sw) {
-                HYDOT_CUDA(cudaMemsetAsync(flag.as<void>(), 0, sizeof(int), c.stream));
-                for (int r = 0; r < np - 1; ++r) {
-                    jacobi_round_k<<<per, 256, 0, c.stream>>>(m, int(n), dpairs.as<int2>() + r * per,
-                                                             U.d(), m, V.d(), n, flag.as<int>());
-                    c.check_launch();
-                }
-                int h = 0;
-                HYDOT_CUDA(cudaMemcpyAsync(&h, flag.as<void>(), sizeof(int), cudaMemcpyDeviceToHost,
-                                           c.stream));
-                c.sync();
-                if (!h) break;
-            }
+            int want = per;  // one CTA per pair
+            int grid = std::max(1, std::min(want, per_sm * c.num_sms));
+            int64_t mm = m;
+            int nn = int(n), npp = np;
+            double* up = U.d();
+            double* vp = V.d();
+            int64_t ldu = m, ldv = n;
+            double tl = tol, at = atol;
+            int* cnt = sw.as<int>();
+            int* so = sw.as<int>() + kMaxSweeps;
+            const int2* pp = dpairs;
+            void* args[] = {&mm, &nn, &npp, &pp, &up, &ldu, &vp, &ldv, &tl, &at, &cnt, &so};
+            HYDOT_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_coop_k, dim3(grid), dim3(JT), args, 0,
+                                                   c.stream));
+            c.count();
         }
+    }
+    if (stats_on()) {
+        int sweeps = 0;
+        HYDOT_CUDA(cudaMemcpyAsync(&sweeps, sw.as<int>() + kMaxSweeps, sizeof(int),
+                                   cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+        fprintf(stderr, "[jacobi] m=%lld n=%lld sweeps=%d ms=%.3f\n", (long long)m, (long long)n,
+                sweeps, dt * 1e3);
     }
     DBuf sd = dalloc(c, size_t(n));
     colnorm_k<<<unsigned(n), 256, 0, c.stream>>>(m, int(n), U.d(), m, sd.d());
@@ -278,7 +378,8 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
     c.d2h(sv.data(), sd.d(), size_t(n));
     std::vector<int> perm(static_cast<size_t>(n));
     std::iota(perm.begin(), perm.end(), 0);
-    std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return sv[size_t(a)] > sv[size_t(b)]; });
+    std::stable_sort(perm.begin(), perm.end(),
+                     [&](int a, int b) { return sv[size_t(a)] > sv[size_t(b)]; });
     for (int64_t j = 0; j < n; ++j) s[size_t(j)] = sv[size_t(perm[size_t(j)])];
     DBuf dperm(c, size_t(n) * sizeof(int));
     HYDOT_CUDA(cudaMemcpyAsync(dperm.as<void>(), perm.data(), size_t(n) * sizeof(int),
@@ -287,7 +388,7 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
     finish_k<<<dim3(unsigned(gx), unsigned(n)), 256, 0, c.stream>>>(
         m, int(n), dperm.as<int>(), sd.d(), U.d(), m, Uo, lduo, V.d(), n, Vo, ldvo);
     c.check_launch();
-    c.sync();  // host vectors (pairs, perm) go out of scope
+    c.sync();
 }
 
 }  // namespace hydot

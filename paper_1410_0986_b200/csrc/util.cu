@@ -212,9 +212,13 @@ std::map<std::string, std::pair<double, long>>& prof_table() {
 bool prof_on() {
     static int on = [] {
         const char* e = std::getenv("HYDOT_PROFILE");
-        return (e && e[0] == '1') ? 1 : 0;
+        return (e && (e[0] == '1' || e[0] == '2')) ? (e[0] - '0') : 0;
     }();
     return on != 0;
+}
+int prof_level() {
+    const char* e = std::getenv("HYDOT_PROFILE");
+    return (e && e[0] == '2') ? 2 : 1;
 }
 double now_s() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
@@ -222,7 +226,8 @@ double now_s() {
 thread_local int g_depth = 0;
 }  // namespace
 
-StageTimer::StageTimer(Ctx& c, const char* name) : c_(c), name_(name) {
+StageTimer::StageTimer(Ctx& c, const char* name, int64_t a, int64_t b, int64_t k)
+    : c_(c), name_(name), a_(a), b_(b), k_(k) {
     on_ = prof_on() && g_depth == 0;
     ++g_depth;
     if (on_) {
@@ -239,6 +244,9 @@ StageTimer::~StageTimer() {
     auto& e = prof_table()[name_];
     e.first += dt;
     e.second += 1;
+    if (prof_level() == 2 && dt > 1e-3)
+        fprintf(stderr, "[stage] %s %lld %lld %lld ms=%.3f\n", name_, (long long)a_, (long long)b_,
+                (long long)k_, dt * 1e3);
 }
 }  // namespace hydot
 
@@ -260,3 +268,49 @@ extern "C" int hydot_profile_dump(char* buf, int len) {
     }
     return int(s.size());
 }
+
+// ---------------------------------------------------- column utilities --
+namespace hydot {
+namespace {
+__global__ void colnorm2_k(int64_t m, const double* __restrict__ A, int64_t lda,
+                           double* __restrict__ out) {
+    __shared__ double sh[8];
+    const double* a = A + int64_t(blockIdx.x) * lda;
+    double s = 0;
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) s += a[i] * a[i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0;
+        for (int i = 0; i < int(blockDim.x >> 5); ++i) t += sh[i];
+        out[blockIdx.x] = sqrt(t);
+    }
+}
+// dst[idx[i], j] = src[i, j]
+__global__ void scatter_rows_k(int64_t rows, int64_t cols, const double* __restrict__ s,
+                               int64_t lds, const int* __restrict__ idx, double* __restrict__ d,
+                               int64_t ldd) {
+    int64_t total = rows * cols;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        int64_t i = e % rows, j = e / rows;
+        d[int64_t(idx[i]) + j * ldd] = s[i + j * lds];
+    }
+}
+}  // namespace
+
+void col_norms(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* out_dev) {
+    if (n <= 0) return;
+    colnorm2_k<<<unsigned(n), 256, 0, c.stream>>>(m, A, lda, out_dev);
+    c.check_launch();
+}
+
+void scatter_rows(Ctx& c, int64_t rows, int64_t cols, const double* src, int64_t lds,
+                  const int* idx, double* dst, int64_t ldd) {
+    if (rows <= 0 || cols <= 0) return;
+    int blocks = int(std::max<int64_t>(1, std::min<int64_t>((rows * cols + 255) / 256, int64_t(c.num_sms) * 16)));
+    scatter_rows_k<<<blocks, 256, 0, c.stream>>>(rows, cols, src, lds, idx, dst, ldd);
+    c.check_launch();
+}
+}  // namespace hydot
