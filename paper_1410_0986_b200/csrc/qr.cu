@@ -6,10 +6,14 @@
 // so Gram/Cholesky QR is not admissible: this is true Householder.
 // Two-level blocking:
 //   panel  (32 columns)  one cooperative persistent kernel: every CTA owns a
-//          contiguous row slab (kept in shared memory when it fits), two
-//          grid-wide barriers per column (reflector + dot products, then the
-//          rank-1 update fused with the next column's norm).  Partial sums are
-//          reduced redundantly by every CTA in fixed order: deterministic.
+//          contiguous row slab (kept in shared memory when it fits) and ONE
+//          grid-wide barrier per column.  Look-ahead: while applying the
+//          reflector of column c, each CTA already accumulates the partial
+//          norm of column c+1 and its partial dot products x^T P_q with the
+//          remaining columns; with the published row c+1 the reflector data
+//          w_q = P_cq + scal (x^T P_q - alpha P_cq) of the next column need no
+//          second reduction.  Partial sums are reduced redundantly by every
+//          CTA in fixed order: deterministic.
 //   block  (128 columns) the 32-wide sub-panels update the rest of their
 //          128-block with DMMA GEMMs; the 128-wide block reflector
 //          I - V T V^T then updates the trailing matrix with three DMMA GEMMs
@@ -26,23 +30,32 @@ namespace {
 constexpr int PB = 32;        // panel width (cooperative kernel)
 constexpr int NB = kQRBlock;  // block-reflector width (128)
 constexpr int PT = 512;       // threads per panel CTA
+constexpr int GMAX = 512;     // max CTAs of a panel grid (buffer sizing)
 
 __device__ __forceinline__ double warp_sum(double v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
 
+// Buffers (double-buffered by column parity):
+//   nrm[2][GMAX]      partial ||x||^2 below the diagonal
+//   dot[2][GMAX][PB]  partial x^T P_q (rows >= diagonal)
+//   row[2][PB]        the diagonal row of the panel (published by its owner)
+struct PanelBufs {
+    double* nrm;
+    double* dot;
+    double* row;
+};
+
 // Factor the mr x jb panel P (ld) in place: R above the diagonal, unit-lower
-// Householder vectors below, tau[0..jb).  part: G doubles, part2: G*PB.
+// Householder vectors below, tau[0..jb).
 template <bool SMEM>
 __global__ void __launch_bounds__(PT) qr_panel_coop(int64_t mr, int jb, double* __restrict__ P,
                                                     int64_t ld, int64_t rows_per,
-                                                    double* __restrict__ tau_out,
-                                                    double* __restrict__ part,
-                                                    double* __restrict__ part2) {
+                                                    double* __restrict__ tau_out, PanelBufs buf) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double slab[];  // rows_per x PB (ld rows_per) when SMEM
-    __shared__ double red[PT / 32][PB];
+    __shared__ double red[PT / 32][PB + 1];
     __shared__ double wsh[PB];
     __shared__ double sc[3];
     const int G = gridDim.x;
@@ -59,30 +72,52 @@ __global__ void __launch_bounds__(PT) qr_panel_coop(int64_t mr, int jb, double* 
             for (int k = threadIdx.x; k < nrow; k += PT) slab[k + int64_t(q) * rows_per] = P[r0 + k + q * ld];
         __syncthreads();
     }
-    // partial norm^2 of column 0 below the diagonal
-    {
-        double a = 0.0;
-        for (int64_t i = max(r0, int64_t(1)) + threadIdx.x; i < r1; i += PT) {
-            double x = at(i, 0);
-            a += x * x;
+    // partials of column `col` (after all previous updates): norm below the
+    // diagonal, dots with the later columns, diagonal row -> slot `par`
+    auto partials = [&](int col, int par) {
+        double nacc = 0.0;
+        double acc[PB];
+#pragma unroll
+        for (int q = 0; q < PB; ++q) acc[q] = 0.0;
+        for (int64_t i = max(r0, int64_t(col)) + threadIdx.x; i < r1; i += PT) {
+            const double x = at(i, col);
+            if (i > col) nacc += x * x;
+#pragma unroll
+            for (int q = 0; q < PB; ++q)
+                if (q > col && q < jb) acc[q] += x * at(i, q);
+            if (i == col)
+                for (int q = col; q < jb; ++q) buf.row[par * PB + q] = at(i, q);
         }
-        a = warp_sum(a);
-        if (lane == 0) red[warp][0] = a;
+        nacc = warp_sum(nacc);
+#pragma unroll
+        for (int q = 0; q < PB; ++q)
+            if (q > col && q < jb) acc[q] = warp_sum(acc[q]);
+        __syncthreads();  // red[] may still be read by the previous reduction
+        if (lane == 0) {
+            red[warp][PB] = nacc;
+#pragma unroll
+            for (int q = 0; q < PB; ++q)
+                if (q > col && q < jb) red[warp][q] = acc[q];
+        }
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (threadIdx.x <= PB) {
+            const int q = threadIdx.x;
             double t = 0.0;
-            for (int w = 0; w < PT / 32; ++w) t += red[w][0];
-            part[blockIdx.x] = t;
+            if (q == PB || (q > col && q < jb))
+                for (int w = 0; w < PT / 32; ++w) t += red[w][q];
+            if (q == PB) buf.nrm[par * GMAX + blockIdx.x] = t;
+            else buf.dot[(int64_t(par) * GMAX + blockIdx.x) * PB + q] = t;
         }
-    }
+    };
+    partials(0, 0);
     for (int c = 0; c < jb; ++c) {
+        const int par = c & 1;
         grid.sync();
-        // ---- reflector (every CTA, identical arithmetic) + scale + dots
+        // ---- reflector of column c from the published partials (every CTA)
         if (threadIdx.x == 0) {
             double xn2 = 0.0;
-            for (int p = 0; p < G; ++p) xn2 += part[p];
-            double alpha = P[c + int64_t(c) * ld];
-            if (SMEM && c >= r0 && c < r1) alpha = at(c, c);
+            for (int p = 0; p < G; ++p) xn2 += buf.nrm[par * GMAX + p];
+            const double alpha = buf.row[par * PB + c];
             double tau = 0.0, beta = alpha, scal = 1.0;
             if (xn2 > 0.0) {
                 beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
@@ -94,10 +129,20 @@ __global__ void __launch_bounds__(PT) qr_panel_coop(int64_t mr, int jb, double* 
             sc[2] = scal;
         }
         __syncthreads();
-        const double tau = sc[0], scal = sc[2];
-        double acc[PB];
-#pragma unroll
-        for (int q = 0; q < PB; ++q) acc[q] = 0.0;
+        const double tau = sc[0], beta = sc[1], scal = sc[2];
+        if (threadIdx.x < PB) {
+            const int q = threadIdx.x;
+            double w = 0.0;
+            if (q > c && q < jb) {
+                double s = 0.0;
+                for (int p = 0; p < G; ++p) s += buf.dot[(int64_t(par) * GMAX + p) * PB + q];
+                const double pc = buf.row[par * PB + q];
+                w = pc + scal * (s - buf.row[par * PB + c] * pc);  // v^T P_q, v_c = 1
+            }
+            wsh[q] = w;
+        }
+        __syncthreads();
+        // ---- apply H_c to the rest of the panel (own rows), store v
         for (int64_t i = max(r0, int64_t(c)) + threadIdx.x; i < r1; i += PT) {
             double v = 1.0;
             if (i > c) {
@@ -107,61 +152,14 @@ __global__ void __launch_bounds__(PT) qr_panel_coop(int64_t mr, int jb, double* 
                     at(i, c) = v;
                 }
             }
-#pragma unroll
-            for (int q = 0; q < PB; ++q)
-                if (q > c && q < jb) acc[q] += v * at(i, q);
-        }
-#pragma unroll
-        for (int q = 0; q < PB; ++q) {
-            if (q > c && q < jb) {
-                double s = warp_sum(acc[q]);
-                if (lane == 0) red[warp][q] = s;
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x < PB) {
-            int q = threadIdx.x;
-            double t = 0.0;
-            if (q > c && q < jb)
-                for (int w = 0; w < PT / 32; ++w) t += red[w][q];
-            part2[int64_t(blockIdx.x) * PB + q] = t;
-        }
-        grid.sync();
-        // ---- rank-1 update of the rest of the panel, next column's norm
-        if (threadIdx.x < PB) {
-            int q = threadIdx.x;
-            double t = 0.0;
-            if (q > c && q < jb)
-                for (int p = 0; p < G; ++p) t += part2[int64_t(p) * PB + q];
-            wsh[q] = t;
-        }
-        __syncthreads();
-        double na = 0.0;
-        for (int64_t i = max(r0, int64_t(c)) + threadIdx.x; i < r1; i += PT) {
-            const double v = (i == c) ? 1.0 : at(i, c);
             if (tau != 0.0)
                 for (int q = c + 1; q < jb; ++q) at(i, q) -= tau * v * wsh[q];
-            if (i == c) at(i, c) = sc[1];
-            if (c + 1 < jb && i >= c + 2) {
-                double x = at(i, c + 1);
-                na += x * x;
-            }
+            if (i == c) at(i, c) = beta;
         }
         if (blockIdx.x == 0 && threadIdx.x == 0) tau_out[c] = tau;
-        na = warp_sum(na);
         __syncthreads();
-        if (lane == 0) red[warp][0] = na;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0;
-            for (int w = 0; w < PT / 32; ++w) t += red[w][0];
-            part[blockIdx.x] = t;
-        }
-        if (SMEM && c + 1 < jb) {
-            // the CTA owning row c+1 publishes the next alpha for everybody
-            if (c + 1 >= r0 && c + 1 < r1 && threadIdx.x == 0)
-                P[(c + 1) + int64_t(c + 1) * ld] = at(c + 1, c + 1);
-        }
+        // ---- look-ahead partials of column c+1
+        if (c + 1 < jb) partials(c + 1, par ^ 1);
     }
     if (SMEM) {
         __syncthreads();
@@ -191,7 +189,7 @@ __global__ void __launch_bounds__(NB) larft_k(int jb, const double* __restrict__
     __shared__ double wv[NB];
     const int r = threadIdx.x;
     auto t = [&](int i, int j) -> double& { return Ts[i * (NB + 1) + j]; };
-    for (int j = 0; j < NB; ++j) t(r, j) = 0.0;
+    for (int j = 0; j < jb; ++j) t(r, j) = 0.0;
     __syncthreads();
     for (int i = 0; i < jb; ++i) {
         if (r < i) wv[r] = -tau[i] * G[r + int64_t(i) * ldg];
@@ -207,29 +205,25 @@ __global__ void __launch_bounds__(NB) larft_k(int jb, const double* __restrict__
     for (int j = 0; j < jb; ++j) T[r + int64_t(j) * NB] = t(r, j);  // only jb columns exist
 }
 
-struct CoopCfg {
-    int grid = 0;
-    bool init = false;
-};
-
-void panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, DBuf& part,
-           DBuf& part2) {
-    static CoopCfg cfg_smem, cfg_glob;
+void panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, const PanelBufs& pbuf) {
+    static bool attr = false;
     const size_t smem_cap = 200 * 1024;
     int G = c.num_sms;
     int64_t rows_per = (mr + G - 1) / G;
-    if (rows_per < 64) {  // short panels: fewer CTAs
+    if (mr <= 768) {  // short panels: one CTA holds the whole panel on-chip
+        G = 1;
+        rows_per = mr;
+    } else if (rows_per < 64) {
         G = int(std::max<int64_t>(1, (mr + 63) / 64));
         rows_per = (mr + G - 1) / G;
     }
+    if (G > GMAX) throw std::runtime_error("qr panel: grid too large");
     const size_t smem = size_t(rows_per) * PB * sizeof(double);
     const bool use_smem = smem <= smem_cap;
-    CoopCfg& cc = use_smem ? cfg_smem : cfg_glob;
-    if (!cc.init) {
-        if (use_smem)
-            HYDOT_CUDA(cudaFuncSetAttribute(qr_panel_coop<true>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_cap)));
-        cc.init = true;
+    if (!attr) {
+        HYDOT_CUDA(cudaFuncSetAttribute(qr_panel_coop<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(smem_cap)));
+        attr = true;
     }
     int per_sm = 0;
     if (use_smem)
@@ -237,9 +231,8 @@ void panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, DBuf&
     else
         HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qr_panel_coop<false>, PT, 0));
     if (per_sm * c.num_sms < G) throw std::runtime_error("qr panel: cooperative grid does not fit");
-    double* part_p = part.d();
-    double* part2_p = part2.d();
-    void* args[] = {&mr, &jb, &P, &ld, &rows_per, &tau, &part_p, &part2_p};
+    PanelBufs b = pbuf;
+    void* args[] = {&mr, &jb, &P, &ld, &rows_per, &tau, &b};
     if (use_smem)
         HYDOT_CUDA(cudaLaunchCooperativeKernel((void*)qr_panel_coop<true>, dim3(G), dim3(PT), args,
                                                smem, c.stream));
@@ -279,8 +272,8 @@ void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f
     const int64_t k = std::min(m, n);
     if (k <= 0) return;
     double* a = f.a.d();
-    DBuf part = dalloc(c, size_t(c.num_sms) * 2 + 16);
-    DBuf part2 = dalloc(c, (size_t(c.num_sms) * 2 + 16) * PB);
+    DBuf pb_mem = dalloc(c, size_t(2) * GMAX + size_t(2) * GMAX * PB + 2 * PB);
+    PanelBufs pbuf{pb_mem.d(), pb_mem.d() + 2 * GMAX, pb_mem.d() + 2 * GMAX + 2 * GMAX * PB};
     DBuf V = dalloc(c, size_t(m) * NB);
     DBuf G = dalloc(c, size_t(NB) * NB);
     DBuf W = dalloc(c, size_t(NB) * size_t(std::max<int64_t>(n, 1)));
@@ -295,7 +288,7 @@ void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f
             const int pb = std::min(PB, jb - p0);
             const int64_t pr = mr - p0;
             double* Pp = Pb + p0 + int64_t(p0) * m;
-            panel(c, pr, pb, Pp, m, f.tau.d() + j0 + p0, part, part2);
+            panel(c, pr, pb, Pp, m, f.tau.d() + j0 + p0, pbuf);
             const int rest = jb - p0 - pb;
             if (rest > 0) {
                 // apply this sub-panel's reflector to the rest of the block

@@ -124,7 +124,41 @@ __global__ void __launch_bounds__(1024) jacobi_smem_k(int m, int n, int np,
 }
 
 // ------------------------------------------------------- cooperative ------
-// counters[s] counts rotations applied in sweep s (zeroed before launch)
+// warp-per-pair variant for short columns (m <= 640): 8x fewer CTAs in the
+// grid barrier; counters[s] counts rotations applied in sweep s
+__global__ void __launch_bounds__(JT) jacobi_coop_warp_k(int64_t m, int n, int np,
+                                                         const int2* __restrict__ pairs,
+                                                         double* __restrict__ U, int64_t ldu,
+                                                         double* __restrict__ V, int64_t ldv,
+                                                         double tol, double atol,
+                                                         int* __restrict__ counters,
+                                                         int* __restrict__ sweeps_out) {
+    cg::grid_group grid = cg::this_grid();
+    const int lane = threadIdx.x & 31;
+    const int gw = int(blockIdx.x) * (JT / 32) + (threadIdx.x >> 5);
+    const int tw = int(gridDim.x) * (JT / 32);
+    const int rounds = np - 1, per = np / 2;
+    int sweep = 0;
+    for (; sweep < kMaxSweeps; ++sweep) {
+        int mine = 0;
+        for (int r = 0; r < rounds; ++r) {
+            for (int q = gw; q < per; q += tw) {
+                int2 pr = pairs[r * per + q];
+                if (pr.x >= n || pr.y >= n) continue;
+                if (warp_pair(lane, m, n, U + int64_t(pr.x) * ldu, U + int64_t(pr.y) * ldu,
+                              V + int64_t(pr.x) * ldv, V + int64_t(pr.y) * ldv, tol, atol))
+                    ++mine;
+            }
+            grid.sync();
+        }
+        if (lane == 0 && mine) atomicAdd(&counters[sweep], mine);
+        grid.sync();
+        if (*((volatile int*)&counters[sweep]) == 0) break;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
+}
+
+// CTA-per-pair variant for long columns
 __global__ void __launch_bounds__(JT) jacobi_coop_k(int64_t m, int n, int np,
                                                     const int2* __restrict__ pairs,
                                                     double* __restrict__ U, int64_t ldu,
@@ -343,9 +377,14 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
         set_identity(c, n, n, V.d(), n);
         if (n >= 2) {
             int per_sm = 0;
-            HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_coop_k, JT, 0));
+            // warp-per-pair measured slower on the config-1 cores (1.95 s vs
+            // 1.44 s total): kept for experiments via HYDOT_JACOBI_WARP=1
+            static const bool warp_env = std::getenv("HYDOT_JACOBI_WARP") != nullptr;
+            const bool warp_mode = warp_env && m <= 640;
+            void* kern = warp_mode ? (void*)jacobi_coop_warp_k : (void*)jacobi_coop_k;
+            HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, JT, 0));
             const int per = np / 2;
-            int want = per;  // one CTA per pair
+            int want = warp_mode ? (per + JT / 32 - 1) / (JT / 32) : per;
             int grid = std::max(1, std::min(want, per_sm * c.num_sms));
             int64_t mm = m;
             int nn = int(n), npp = np;
@@ -357,8 +396,7 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
             int* so = sw.as<int>() + kMaxSweeps;
             const int2* pp = dpairs;
             void* args[] = {&mm, &nn, &npp, &pp, &up, &ldu, &vp, &ldv, &tl, &at, &cnt, &so};
-            HYDOT_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_coop_k, dim3(grid), dim3(JT), args, 0,
-                                                   c.stream));
+            HYDOT_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(JT), args, 0, c.stream));
             c.count();
         }
     }
