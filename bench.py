@@ -70,6 +70,8 @@ class ClockSampler:
         self.lines = []
 
     def start(self):
+        if os.environ.get("BENCH_NO_CLOCKS"):
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
@@ -115,171 +117,231 @@ def run_b200(args):
     import torch
     import paper_1410_0986_b200 as h
     from paper_1410_0986_b200 import born, configs, lowrank as lr
+    from paper_1410_0986_b200.parallel import GpuEngine, make_plan, reduce_tree
 
     rank, world, local = dist_info()
+    dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
     ctx = h.Context(local)
     cfg = configs.CONFIGS[args.config]
     st = configs.make_setup(cfg)
     g = st.grid()
-    # ---- setup (untimed): fields on the GPU, resident in HBM
-    F, fstats = born.compute_fields(ctx, g, st.sigma, st.sigma_prime, st.inv_D, st.points, tol=1e-10)
-    torch.cuda.synchronize()
-    w = torch.full((g.N,), cfg.h ** 3, dtype=torch.float64, device="cuda")
     tree = lr.ClusterTree(st.source_xy, st.box_lo, st.box_hi)
     eps = configs.compression_tolerance(st, tree.depth())
-    opts = lr.RecursiveOptions(seed=cfg.seed)
+    # ---- shard plan: this rank owns one subtree at depth log2(world)
+    plan = make_plan(tree.nodes, tree.root, world)
+    root_v = plan.shard_roots[rank]
+    srcs = plan.shard_sources[rank]
+    lo, hi = tree.node_box(root_v)
+    pts = sorted({int(st.source_point[s]) for s in srcs} |
+                 {int(st.detector_point[s, d]) for s in srcs for d in range(cfg.n_det)})
+    loc = {p: i for i, p in enumerate(pts)}
+    # ---- setup (untimed): this shard's fields on its GPU, resident in HBM
+    F, fstats = born.compute_fields(ctx, g, st.sigma, st.sigma_prime, st.inv_D,
+                                    st.points[pts], tol=1e-10)
+    torch.cuda.synchronize()
+    w = torch.full((g.N,), cfg.h ** 3, dtype=torch.float64, device=dev)
 
     def provider_for(Fdev):
-        inc = [Fdev[st.source_point[s]] for s in range(cfg.n_sources)]
-        adj = [[Fdev[st.detector_point[s, d]] for d in range(cfg.n_det)] for s in range(cfg.n_sources)]
+        inc = [Fdev[loc[int(st.source_point[s])]] for s in srcs]
+        adj = [[Fdev[loc[int(st.detector_point[s, d])]] for d in range(cfg.n_det)] for s in srcs]
         return lr.BornFieldsProvider(inc, adj, w, 1.0)
 
-    prov = provider_for(F)
-    units = cfg.n_sources * cfg.n_det  # (s,d) blocks per step (whole job = world * units)
+    eng = GpuEngine(ctx)
+    units = cfg.n_sources * cfg.n_det  # (s,d) blocks of the whole job per step
     stream = torch.cuda.current_stream()
 
-    def step():
-        rec = lr.recursive_lowrank(ctx, tree, eps, prov, opts)
-        fr = lr.recompress(ctx, rec.factor, eps, -1, rec.ledger)
+    def step(prov):
+        rec = eng.compress_subtree(st.source_xy[srcs], lo, hi, srcs, root_v, eps, prov, cfg.seed,
+                                   20, 10)
+        root = reduce_tree(plan, rank, rec.factor, eng, eps, cfg.seed, 20, 10, dist, dev)
+        fr = lr.recompress(ctx, root, eps, -1, rec.ledger) if rank == 0 else None
         return rec, fr
 
+    prov = provider_for(F)
     for _ in range(args.warmup):
-        rec, fr = step()
+        rec, fr = step(prov)
     torch.cuda.synchronize()
-    ledger_flops = rec.ledger.kernel_tally
+    ledger = torch.tensor([rec.ledger.kernel_tally], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ledger)
+    ledger_flops = float(ledger.item())
 
-    # ---- timed region (value): fields resident, K steps
+    # ---- timed region (value): fields resident, K steps, max over ranks
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = ctx.launch_count()
     if world > 1:
-        torch.distributed.barrier()
+        dist.barrier()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        rec, fr = step()
+        rec, fr = step(prov)
     e1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
-        torch.distributed.barrier()
+        dist.barrier()
     ms = e0.elapsed_time(e1)
     launches = ctx.launch_count() - launches0
     clk = clocks.stop()
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+        lt = torch.tensor([launches], dtype=torch.int64, device=dev)
+        dist.all_reduce(lt)
+        launches = int(lt.item())
     ms_per_step = ms / args.steps
-    value = world * units * args.steps / (ms / 1e3)
+    value = units * args.steps / (ms / 1e3)
     achieved_tflops = ledger_flops / (ms_per_step / 1e3) / 1e12
 
-    # ---- per-stage breakdown (one extra step, synchronised stage timers)
-    os.environ.setdefault("HYDOT_PROFILE", "0")
-
-    # ---- e2e through the reference-facing call with HOST buffers
+    # ---- e2e through the reference-facing call with HOST buffers: the
+    # shard's fields are copied from pinned host memory every step and the
+    # final factor is copied back to the host
     Fh = torch.empty(F.shape, dtype=torch.float64, pin_memory=True)
     Fh.copy_(F)
     Fd = torch.empty_like(F)
     e2e_ms = []
     d2h_bytes = 0
-    for _ in range(max(1, args.e2e_steps)):
+    # one untimed pass allocates the pinned result buffers (cudaHostAlloc of
+    # GBs is not part of a step); the timed passes reuse the cached blocks
+    for it in range(max(1, args.e2e_steps) + 1):
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
         Fd.copy_(Fh, non_blocking=True)                      # H2D of the step's inputs
-        rec2 = lr.recursive_lowrank(ctx, tree, eps, provider_for(Fd), opts)
-        fr2 = lr.recompress(ctx, rec2.factor, eps)
-        Uh = torch.empty((fr2.rank(), fr2.rows()), dtype=torch.float64, pin_memory=True)
-        Vh = torch.empty((fr2.rank(), fr2.cols()), dtype=torch.float64, pin_memory=True)
-        Ud, Vd = fr2.U, fr2.V                                 # device views (col-major)
-        Uh.copy_(Ud.T, non_blocking=True)                     # D2H of the result
-        Vh.copy_(Vd.T, non_blocking=True)
+        rec2, fr2 = step(provider_for(Fd))
+        if rank == 0:
+            Uh = torch.empty((fr2.rank(), fr2.rows()), dtype=torch.float64, pin_memory=True)
+            Vh = torch.empty((fr2.rank(), fr2.cols()), dtype=torch.float64, pin_memory=True)
+            Uh.copy_(fr2.U.T, non_blocking=True)              # D2H of the result
+            Vh.copy_(fr2.V.T, non_blocking=True)
+            d2h_bytes = (Uh.numel() + Vh.numel()) * 8
         b.record(stream)
         torch.cuda.synchronize()
-        e2e_ms.append(a.elapsed_time(b))
-        d2h_bytes = (Uh.numel() + Vh.numel()) * 8
+        t = a.elapsed_time(b)
+        if world > 1:
+            tt = torch.tensor([t], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        if it > 0:
+            e2e_ms.append(t)
     e2e_step_ms = statistics.median(e2e_ms)
-    e2e_value = world * units / (e2e_step_ms / 1e3)
-    h2d_bytes = F.numel() * 8
+    e2e_value = units / (e2e_step_ms / 1e3)
+    hb = torch.tensor([F.numel() * 8], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(hb)
+    h2d_bytes = int(hb.item())
 
-    # ---- J~ products on the compressed operator (config-4 style blocks)
-    J = lr.JOperator(ctx, fr, rec.row_perm, st.eps_c)
-    R = fr.rank()
-    matvec = {}
-    for b in (1, 64):
-        X = torch.randn(b, g.N * cfg.n_chrom, dtype=torch.float64, device="cuda")
-        Y = torch.empty(b, cfg.M, dtype=torch.float64, device="cuda")
-        for _ in range(3):
-            J.matmat_cm(X, Y, b)
-        torch.cuda.synchronize()
-        reps = 20
-        a = torch.cuda.Event(enable_timing=True)
-        bb = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(reps):
-            J.matmat_cm(X, Y, b)
-        bb.record(stream)
-        torch.cuda.synchronize()
-        t = a.elapsed_time(bb) / reps / 1e3
-        nbytes = 8.0 * (g.N * R + cfg.M * R + b * cfg.n_chrom * g.N + b * cfg.M)
-        flops = 2.0 * R * b * cfg.n_chrom * (g.N + cfg.M)
-        matvec[f"b{b}"] = {"ms": t * 1e3, "GB/s": nbytes / t / 1e9, "TFLOP/s": flops / t / 1e12,
-                           "hbm_frac": nbytes / t / 1e9 / 6554.9,
-                           "fp64_frac": flops / t / 1e12 / FP64_PEAK_TFLOPS}
-
-    # ---- CPU baseline (rank 0, N=1 only): the oracle on a bounded sample
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_sample(st, tree, eps, F.cpu().numpy(), threads=1, leaves=args.cpu_sample)
-
-    out = {
-        "metric": "(s,d) Born blocks compressed/s",
-        "value": value,
-        "unit": "blocks/s",
-        "n_gpus": world,
-        "steps": args.steps,
-        "warmup": args.warmup,
-        "ms_per_step": ms_per_step,
-        "higher_is_better": True,
-        "scaling": "weak",
-        "vs_baseline": None,
-        "dtype": "f64",
-        "data": "synthetic (seeded BASELINE config-1 physics, configs.py; fields from the GPU CG)",
-        "config": {"workload": f"{cfg.name}: compress_H = Born assembly + recursive randSVD + merges + recompress",
-                   "n": cfg.n, "N": g.N, "n_sources": cfg.n_sources, "n_det": cfg.n_det,
-                   "n_lambda": cfg.n_lambda, "n_chrom": cfg.n_chrom, "M": cfg.M,
-                   "tolerance": f"reference schedule eps_d=1e-6 -> eps={eps:.3e} (L={tree.depth()}), p=20, kprobe=10",
-                   "l2": "inputs larger than L2 (fields %.2f GB resident)" % (F.numel() * 8 / 1e9),
-                   "parallelism": f"sources sharded x{world}" if world > 1 else "single GPU",
-                   "final_rank": fr.rank(), "rank_before_recompress": rec.factor.rank()},
-        "e2e": {"value": e2e_value, "unit": "blocks/s", "h2d_bytes_per_step": int(h2d_bytes),
-                "d2h_bytes_per_step": int(d2h_bytes), "ms_per_step": e2e_step_ms},
-        "gpu_launches": int(launches),
-        "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": FP64_PEAK_TFLOPS,
-                     "unit": "TFLOP/s", "frac": achieved_tflops / FP64_PEAK_TFLOPS,
-                     "traffic": None,
-                     "what": "compression stage: reference FlopLedger flops per step "
-                             "(lowrank.cpp:31-51, %.3e) / CUDA-event step time" % ledger_flops,
-                     "peak_source": PEAK_SOURCE},
-        "clocks": clk,
-        "matvec": matvec,
-        "fields_setup": {"systems": int(len(st.points) * cfg.n_lambda),
-                         "iters_max": int(fstats.iters.max()),
-                         "relres_max": float(fstats.relres.max())},
-    }
-    if cpu is not None:
-        out["cpu_baseline"] = cpu
+    out = None
     if rank == 0:
+        # ---- J~ products on the compressed operator (config-4 style blocks)
+        # shard leaf orders: the global row order of the reduced factor
+        perm = global_perm(tree, plan, cfg.rows_per_source, st)
+        J = lr.JOperator(ctx, fr, perm, st.eps_c)
+        R = fr.rank()
+        matvec = {}
+        for b in (1, 64):
+            X = torch.randn(b, g.N * cfg.n_chrom, dtype=torch.float64, device=dev)
+            Y = torch.empty(b, cfg.M, dtype=torch.float64, device=dev)
+            for _ in range(3):
+                J.matmat_cm(X, Y, b)
+            torch.cuda.synchronize()
+            reps = 20
+            a = torch.cuda.Event(enable_timing=True)
+            bb = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                J.matmat_cm(X, Y, b)
+            bb.record(stream)
+            torch.cuda.synchronize()
+            t = a.elapsed_time(bb) / reps / 1e3
+            nbytes = 8.0 * (g.N * R + cfg.M * R + b * cfg.n_chrom * g.N + b * cfg.M)
+            flops = 2.0 * R * b * cfg.n_chrom * (g.N + cfg.M)
+            matvec[f"b{b}"] = {"ms": t * 1e3, "GB/s": nbytes / t / 1e9, "TFLOP/s": flops / t / 1e12,
+                               "hbm_frac": nbytes / t / 1e9 / 6554.9,
+                               "fp64_frac": flops / t / 1e12 / FP64_PEAK_TFLOPS}
+
+        # ---- CPU baseline (rank 0, N=1 only): the oracle on a bounded sample
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            Fg = np.zeros((len(st.points), cfg.n_lambda, g.N))
+            Fg[pts] = F.cpu().numpy()
+            cpu = cpu_sample(st, tree, eps, Fg, threads=1, leaves=args.cpu_sample)
+
+        out = {
+            "metric": "(s,d) Born blocks compressed/s",
+            "value": value,
+            "unit": "blocks/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (seeded BASELINE config-1 physics, configs.py; fields from the GPU CG)",
+            "config": {"workload": f"{cfg.name}: compress_H = Born assembly + recursive randSVD + merges + recompress",
+                       "n": cfg.n, "N": g.N, "n_sources": cfg.n_sources, "n_det": cfg.n_det,
+                       "n_lambda": cfg.n_lambda, "n_chrom": cfg.n_chrom, "M": cfg.M,
+                       "tolerance": f"reference schedule eps_d=1e-6 -> eps={eps:.3e} (L={tree.depth()}), p=20, kprobe=10",
+                       "l2": "inputs larger than L2 (fields %.2f GB resident per GPU)" % (F.numel() * 8 / 1e9),
+                       "parallelism": (f"sources sharded over {world} GPUs (subtrees at depth "
+                                       f"{plan.depth}), NCCL reduction tree for the top merges")
+                                      if world > 1 else "single GPU",
+                       "final_rank": fr.rank()},
+            "e2e": {"value": e2e_value, "unit": "blocks/s", "h2d_bytes_per_step": h2d_bytes,
+                    "d2h_bytes_per_step": int(d2h_bytes), "ms_per_step": e2e_step_ms},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": FP64_PEAK_TFLOPS,
+                         "unit": "TFLOP/s", "frac": achieved_tflops / FP64_PEAK_TFLOPS,
+                         "traffic": None,
+                         "what": "compression stage: reference FlopLedger flops per step "
+                                 "(lowrank.cpp:31-51, %.3e) / CUDA-event step time" % ledger_flops,
+                         "peak_source": PEAK_SOURCE},
+            "clocks": clk,
+            "matvec": matvec,
+            "fields_setup": {"systems": int(len(pts) * cfg.n_lambda),
+                             "iters_max": int(fstats.iters.max()),
+                             "relres_max": float(fstats.relres.max())},
+        }
+        if cpu is not None:
+            out["cpu_baseline"] = cpu
         print(json.dumps(out), flush=True)
     if world > 1:
-        torch.distributed.destroy_process_group()
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def global_perm(tree, plan, rows_per, st):
+    """Row order of the reduced factor: shard subtrees left to right, each in
+    its own leaf order (lowrank.cpp:515-519)."""
+    out = []
+    for v in plan.shard_roots:
+        order = []
+
+        def walk(u):
+            nd = tree.nodes[u]
+            if nd["left"] < 0:
+                order.extend(nd["idx"])
+            else:
+                walk(nd["left"])
+                walk(nd["right"])
+
+        walk(v)
+        for s in order:
+            out.extend(s * rows_per + q for q in range(rows_per))
+    return np.asarray(out, dtype=np.int32)
 
 
 def cpu_sample(st, tree, eps, Fh, threads: int, leaves: int = 1):

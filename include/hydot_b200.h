@@ -170,6 +170,8 @@ int hydot_tree_depth(hydot_tree t);
 /* node v: children (-1 for a leaf) and source count; idx_h may be NULL */
 hydot_status hydot_tree_node(hydot_tree t, int v, int* left, int* right, int* n_idx, int* idx_h);
 hydot_status hydot_tree_leaf_order(hydot_tree t, int* order_h);
+/* bounding box of node v (ClusterTree::Node::lo / hi, d values each) */
+hydot_status hydot_tree_node_box(hydot_tree t, int v, double* lo_h, double* hi_h);
 void hydot_tree_free(hydot_tree t);
 
 /* lowrank::BlockProvider (lowrank.hpp:122-126): fills the rows_per_source x
@@ -203,6 +205,13 @@ typedef struct {
     int p;
     int kprobe;
     int hint_mode;
+    /* Sharded execution (multi-GPU): the tree is a subtree of a global tree
+     * whose pre-order node ids start at node_offset, and local source i is
+     * global source source_ids[i].  Seeds (lowrank.cpp:485,494,500) and
+     * row_perm use the global ids, so a shard reproduces the global run's
+     * per-node seeds.  source_ids NULL / node_offset 0 = unsharded. */
+    const int* source_ids;
+    int node_offset;
 } hydot_rec_opts;
 
 /* lowrank::recursive_lowrank (lowrank.hpp:142-144, lowrank.cpp:459-521).

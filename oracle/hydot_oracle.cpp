@@ -469,10 +469,15 @@ struct RecResult {
 
 // recursive_lowrank + leaf_compress + node_hint (lowrank.cpp:442-521).
 // block(s) returns the rows_per_source x cols block of source s.
+// Sharded replay (the multi-GPU schedule): source_ids maps local source i
+// to its global id and node_offset is the subtree root's global pre-order id,
+// so seeds and row_perm use global ids (identity when unsharded).
 static RecResult recursive_lowrank(const Tree& tree, double eps, int rows_per, int64_t cols,
                                    const std::function<Mat(int)>& block, uint64_t seed, int p,
-                                   int kprobe) {
+                                   int kprobe, const int* source_ids = nullptr,
+                                   int node_offset = 0) {
     (void)cols;
+    auto gs = [&](int s) { return source_ids ? source_ids[s] : s; };
     RecResult res;
     res.node_rank.assign(tree.nodes.size(), -1);
     res.node_depth.assign(tree.nodes.size(), 0);
@@ -492,19 +497,20 @@ static RecResult recursive_lowrank(const Tree& tree, double eps, int rows_per, i
                 for (int s : nd.idx) {
                     Mat blk = block(s);
                     parts.push_back(randsvd(blk, eps, p, kprobe,
-                                            seed + 0x9e3779b97f4a7c15ULL * uint64_t(s + 1),
+                                            seed + 0x9e3779b97f4a7c15ULL * uint64_t(gs(s) + 1),
                                             &res.ledger, LEAF, std::max(1, leaf_hint + 2)));
                     leaf_hint = int(parts.back().rank());
                 }
                 if (parts.empty()) throw std::runtime_error("empty leaf cluster");
                 f = parts[0];
                 for (size_t i = 1; i < parts.size(); ++i)
-                    f = agglomerate(f, parts[i], eps, seed + 0x517cc1b727220a95ULL * uint64_t(v + 1),
+                    f = agglomerate(f, parts[i], eps,
+                                    seed + 0x517cc1b727220a95ULL * uint64_t(node_offset + v + 1),
                                     &res.ledger, node_hint(depth), p, kprobe);
             } else {
                 Factor fl = go(nd.left, depth + 1);
                 Factor fr = go(nd.right, depth + 1);
-                f = agglomerate(fl, fr, eps, seed + 0x2545f4914f6cdd1dULL * uint64_t(v + 1),
+                f = agglomerate(fl, fr, eps, seed + 0x2545f4914f6cdd1dULL * uint64_t(node_offset + v + 1),
                                 &res.ledger, node_hint(depth), p, kprobe);
             }
         } catch (const std::exception& e) {
@@ -520,7 +526,7 @@ static RecResult recursive_lowrank(const Tree& tree, double eps, int rows_per, i
     res.factor.tol = eps;
     res.source_order = tree.leaf_order();
     for (int s : res.source_order)
-        for (int q = 0; q < rows_per; ++q) res.row_perm.push_back(s * rows_per + q);
+        for (int q = 0; q < rows_per; ++q) res.row_perm.push_back(gs(s) * rows_per + q);
     return res;
 }
 
@@ -920,7 +926,7 @@ int oracle_recursive_lowrank(const oracle_tree* t, double eps, const double* H, 
 int oracle_recursive_lowrank_born(const oracle_tree* t, double eps, int64_t N, int nl, int nd,
                                   const double* const* incident, const double* const* adjoint,
                                   const double* w, double nu, uint64_t seed, int p, int kprobe,
-                                  oracle_factor** out) {
+                                  const int* source_ids, int node_offset, oracle_factor** out) {
     return guard([&] {
         int rows_per = nd * nl;
         auto block = [&](int s) {
@@ -934,7 +940,8 @@ int oracle_recursive_lowrank_born(const oracle_tree* t, double eps, int64_t N, i
                 }
             return b;
         };
-        RecResult r = recursive_lowrank(t->t, eps, rows_per, N, block, seed, p, kprobe);
+        RecResult r = recursive_lowrank(t->t, eps, rows_per, N, block, seed, p, kprobe, source_ids,
+                                        node_offset);
         std::unique_ptr<oracle_factor> f(new oracle_factor);
         f->f = std::move(r.factor);
         f->row_perm = r.row_perm;

@@ -75,8 +75,8 @@ def lib():
                                                C.POINTER(C.c_void_p)]
         L.oracle_recursive_lowrank_born.argtypes = [C.c_void_p, C.c_double, C.c_int64, C.c_int,
                                                     C.c_int, C.POINTER(_dp), C.POINTER(_dp), _dp,
-                                                    C.c_double, C.c_uint64, C.c_int, C.c_int,
-                                                    C.POINTER(C.c_void_p)]
+                                                    C.c_double, C.c_uint64, C.c_int, C.c_int, _ip,
+                                                    C.c_int, C.POINTER(C.c_void_p)]
         L.oracle_lr_matmat.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, _dp]
         L.oracle_j_matmat.argtypes = [C.c_void_p, C.c_int, C.c_int, _ip, _dp, C.c_int, C.c_int,
                                       _dp, _dp]
@@ -283,8 +283,10 @@ def recursive_lowrank(tree, eps, H, rows_per, seed=0, p=20, kprobe=10):
     return RecResult(h.value, len(tree.nodes))
 
 
-def recursive_lowrank_born(tree, eps, incident, adjoint, w, nu, seed=0, p=20, kprobe=10):
-    """incident[s]: N x nl; adjoint[s][d]: N x nl (F-order arrays)."""
+def recursive_lowrank_born(tree, eps, incident, adjoint, w, nu, seed=0, p=20, kprobe=10,
+                           source_ids=None, node_offset=0):
+    """incident[s]: N x nl; adjoint[s][d]: N x nl (F-order arrays).  source_ids /
+    node_offset: sharded replay (global seeds and row ids)."""
     ns = len(incident)
     nd = len(adjoint[0])
     N, nl = incident[0].shape
@@ -293,9 +295,13 @@ def recursive_lowrank_born(tree, eps, incident, adjoint, w, nu, seed=0, p=20, kp
     ia = (_dp * ns)(*[_d(a) for a in inc])
     aa = (_dp * len(adj))(*[_d(a) for a in adj])
     h = C.c_void_p()
+    sid = None
+    if source_ids is not None:
+        sid_arr = np.ascontiguousarray(source_ids, dtype=np.int32)
+        sid = sid_arr.ctypes.data_as(_ip)
     _check(lib().oracle_recursive_lowrank_born(tree.h, eps, N, nl, nd, ia, aa, _d(_f64(w)), nu,
-                                               C.c_uint64(seed & (2**64 - 1)), p, kprobe,
-                                               C.byref(h)))
+                                               C.c_uint64(seed & (2**64 - 1)), p, kprobe, sid,
+                                               int(node_offset), C.byref(h)))
     return RecResult(h.value, len(tree.nodes))
 
 

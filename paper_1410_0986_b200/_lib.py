@@ -48,7 +48,8 @@ class BornFields(C.Structure):
 
 class RecOpts(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("p", C.c_int), ("kprobe", C.c_int),
-                ("hint_mode", C.c_int)]
+                ("hint_mode", C.c_int), ("source_ids", C.POINTER(C.c_int)),
+                ("node_offset", C.c_int)]
 
 
 # name -> (restype, argtypes); exactly the declarations of include/hydot_b200.h
@@ -88,6 +89,7 @@ SIGNATURES = {
     "hydot_tree_depth": (C.c_int, [_vp]),
     "hydot_tree_node": (C.c_int, [_vp, C.c_int, _ip, _ip, _ip, _ip]),
     "hydot_tree_leaf_order": (C.c_int, [_vp, _ip]),
+    "hydot_tree_node_box": (C.c_int, [_vp, C.c_int, _dp, _dp]),
     "hydot_tree_free": (None, [_vp]),
     "hydot_recursive_lowrank": (C.c_int, [_vp, _vp, C.c_double, C.POINTER(Provider),
                                           C.POINTER(BornFields), C.POINTER(RecOpts),

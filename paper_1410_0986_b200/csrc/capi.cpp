@@ -355,6 +355,13 @@ hydot_status hydot_tree_leaf_order(hydot_tree t, int* order_h) {
     std::memcpy(order_h, o.data(), o.size() * sizeof(int));
     return HYDOT_OK;
 }
+hydot_status hydot_tree_node_box(hydot_tree t, int v, double* lo_h, double* hi_h) {
+    if (!t || v < 0 || v >= int(t->t.nodes.size())) return HYDOT_EINVAL;
+    const TreeNode& nd = t->t.nodes[size_t(v)];
+    if (lo_h) std::memcpy(lo_h, nd.lo.data(), nd.lo.size() * sizeof(double));
+    if (hi_h) std::memcpy(hi_h, nd.hi.data(), nd.hi.size() * sizeof(double));
+    return HYDOT_OK;
+}
 void hydot_tree_free(hydot_tree t) { delete t; }
 
 hydot_status hydot_recursive_lowrank(hydot_ctx ctx, hydot_tree tree, double eps,
@@ -366,9 +373,15 @@ hydot_status hydot_recursive_lowrank(hydot_ctx ctx, hydot_tree tree, double eps,
         Ctx& c = ctx_of(ctx);
         if (!tree || !out || (!provider == !born))
             throw std::invalid_argument("recursive_lowrank: need a tree and exactly one provider");
-        hydot_rec_opts o{0, 20, 10, 0};
+        hydot_rec_opts o{0, 20, 10, 0, nullptr, 0};
         if (opts) o = *opts;
         if (o.hint_mode != 0) throw std::invalid_argument("recursive_lowrank: unknown hint_mode");
+        std::vector<int> src_ids;
+        int nsrc = 0;
+        for (const auto& nd : tree->t.nodes)
+            for (int s : nd.idx) nsrc = std::max(nsrc, s + 1);
+        src_ids.resize(size_t(nsrc));
+        for (int s = 0; s < nsrc; ++s) src_ids[size_t(s)] = o.source_ids ? o.source_ids[s] : s;
         int rows_per;
         int64_t cols;
         BlockFn fn;
@@ -390,7 +403,8 @@ hydot_status hydot_recursive_lowrank(hydot_ctx ctx, hydot_tree tree, double eps,
                            born->nu, dst, ld);
             };
         }
-        RecOut r = recursive_lowrank(c, tree->t, eps, rows_per, cols, fn, o.seed, o.p, o.kprobe);
+        RecOut r = recursive_lowrank(c, tree->t, eps, rows_per, cols, fn, o.seed, o.p, o.kprobe,
+                                     src_ids, o.node_offset);
         c.sync();
         if (row_perm_h) std::memcpy(row_perm_h, r.row_perm.data(), r.row_perm.size() * sizeof(int));
         if (node_rank_h) std::memcpy(node_rank_h, r.node_rank.data(), r.node_rank.size() * sizeof(int));

@@ -435,7 +435,9 @@ double tolerance_schedule(double eps_d, int L, int N_r) {  // lowrank.cpp:540-54
 // recursive_lowrank (lowrank.cpp:459-521) with the reference's warm-start
 // chains (leaf_hint across leaves in DFS order, depth_hint per depth).
 RecOut recursive_lowrank(Ctx& c, const Tree& t, double eps, int rows_per, int64_t cols,
-                         const BlockFn& block, uint64_t seed, int p, int kprobe) {
+                         const BlockFn& block, uint64_t seed, int p, int kprobe,
+                         const std::vector<int>& source_ids, int node_offset) {
+    auto gsrc = [&](int s) { return source_ids.empty() ? s : source_ids[size_t(s)]; };
     RecOut res;
     res.node_rank.assign(t.nodes.size(), -1);
     res.node_depth.assign(t.nodes.size(), 0);
@@ -456,7 +458,7 @@ RecOut recursive_lowrank(Ctx& c, const Tree& t, double eps, int rows_per, int64_
                 for (int s : nd.idx) {
                     block(s, blk.d(), cols);
                     parts.push_back(randsvd(c, rows_per, cols, blk.d(), cols, eps, p, kprobe,
-                                            seed + 0x9e3779b97f4a7c15ULL * uint64_t(s + 1),
+                                            seed + 0x9e3779b97f4a7c15ULL * uint64_t(gsrc(s) + 1),
                                             &res.ledger, HYDOT_CAT_LEAF,
                                             std::max(1, leaf_hint + 2)));
                     leaf_hint = int(parts.back().rank);
@@ -465,12 +467,12 @@ RecOut recursive_lowrank(Ctx& c, const Tree& t, double eps, int rows_per, int64_
                 f = std::move(parts[0]);
                 for (size_t i = 1; i < parts.size(); ++i)
                     f = agglomerate(c, f, parts[i], eps,
-                                    seed + 0x517cc1b727220a95ULL * uint64_t(v + 1), &res.ledger,
+                                    seed + 0x517cc1b727220a95ULL * uint64_t(node_offset + v + 1), &res.ledger,
                                     node_hint(depth), p, kprobe);
             } else {
                 Factor fl = go(nd.left, depth + 1);
                 Factor fr = go(nd.right, depth + 1);
-                f = agglomerate(c, fl, fr, eps, seed + 0x2545f4914f6cdd1dULL * uint64_t(v + 1),
+                f = agglomerate(c, fl, fr, eps, seed + 0x2545f4914f6cdd1dULL * uint64_t(node_offset + v + 1),
                                 &res.ledger, node_hint(depth), p, kprobe);
             }
         } catch (const CudaError&) {
@@ -490,7 +492,7 @@ RecOut recursive_lowrank(Ctx& c, const Tree& t, double eps, int rows_per, int64_
     res.factor.tol = eps;
     res.source_order = t.leaf_order();
     for (int s : res.source_order)
-        for (int q = 0; q < rows_per; ++q) res.row_perm.push_back(s * rows_per + q);
+        for (int q = 0; q < rows_per; ++q) res.row_perm.push_back(gsrc(s) * rows_per + q);
     return res;
 }
 

@@ -65,6 +65,7 @@ struct RecOut {
 // block(s, out, ld): fill rows_per x cols block of source s row-major
 using BlockFn = std::function<void(int, double*, int64_t)>;
 RecOut recursive_lowrank(Ctx& c, const Tree& t, double eps, int rows_per, int64_t cols,
-                         const BlockFn& block, uint64_t seed, int p, int kprobe);
+                         const BlockFn& block, uint64_t seed, int p, int kprobe,
+                         const std::vector<int>& source_ids = {}, int node_offset = 0);
 
 }  // namespace hydot

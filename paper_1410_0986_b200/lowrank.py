@@ -182,6 +182,8 @@ class ClusterTree:
         check(lib().hydot_tree_build(dp(P), n, d, dp(lo), dp(hi), C.byref(h)))
         self.h = h
         self.n_sources = n
+        self.dim = d
+        self.positions = P
         L = lib()
         self.root = L.hydot_tree_root(h)
         self.nodes = []
@@ -194,6 +196,14 @@ class ClusterTree:
 
     def depth(self) -> int:
         return lib().hydot_tree_depth(self.h)
+
+    def node_box(self, v: int):
+        """(lo, hi) bounding box of node v (ClusterTree::Node::lo / hi)."""
+        d = self.dim
+        lo, hi = np.zeros(d), np.zeros(d)
+        check(lib().hydot_tree_node_box(self.h, v, lo.ctypes.data_as(C.POINTER(C.c_double)),
+                                        hi.ctypes.data_as(C.POINTER(C.c_double))))
+        return lo, hi
 
     def leaf_order(self) -> List[int]:
         out = np.zeros(self.n_sources, dtype=np.int32)
@@ -219,6 +229,9 @@ class RecursiveOptions:
     p: int = 20
     kprobe: int = 10
     hint_mode: int = 0
+    # sharded execution: global ids of the local sources / pre-order offset
+    source_ids: Optional[List[int]] = None
+    node_offset: int = 0
 
 
 @dataclass
@@ -256,8 +269,15 @@ def recursive_lowrank(ctx: Context, tree: ClusterTree, eps: float, provider,
     node_depth = np.zeros(nn, dtype=np.int32)
     h = C.c_void_p()
     led = Ledger()
-    o = _lib.RecOpts(int(opts.seed) & (2**64 - 1), opts.p, opts.kprobe, opts.hint_mode)
     keep = []
+    sid = None
+    if opts.source_ids is not None:
+        sid_arr = np.ascontiguousarray(opts.source_ids, dtype=np.int32)
+        keep.append(sid_arr)
+        sid = sid_arr.ctypes.data_as(C.POINTER(C.c_int))
+    o = _lib.RecOpts(int(opts.seed) & (2**64 - 1), opts.p, opts.kprobe, opts.hint_mode, sid,
+                     int(opts.node_offset))
+    n_global = (max(opts.source_ids) + 1) if opts.source_ids is not None else tree.n_sources
     if isinstance(provider, BornFieldsProvider):
         ns = len(provider.incident)
         nd = len(provider.adjoint[0])
