@@ -447,8 +447,13 @@ hydot_status hydot_lr_matmat(hydot_ctx ctx, hydot_factor f, int trans, int b, co
         DBuf Z = dalloc(c, size_t(F.rank) * size_t(b));
         const double* A1 = trans ? F.U.d() : F.V.d();  // contract against X
         const double* A2 = trans ? F.V.d() : F.U.d();
-        dgemm(c, true, false, F.rank, b, in_rows, 1.0, A1, in_rows, X_dev, ldx, 0.0, Z.d(), F.rank);
-        dgemm(c, false, false, out_rows, b, F.rank, 1.0, A2, out_rows, Z.d(), F.rank, 0.0, Y_dev, ldy);
+        if (skinny_ok(b)) {
+            skinny_tn(c, in_rows, F.rank, b, A1, in_rows, X_dev, ldx, Z.d(), F.rank);
+            skinny_nn(c, out_rows, F.rank, b, A2, out_rows, Z.d(), F.rank, Y_dev, ldy);
+        } else {
+            dgemm(c, true, false, F.rank, b, in_rows, 1.0, A1, in_rows, X_dev, ldx, 0.0, Z.d(), F.rank);
+            dgemm(c, false, false, out_rows, b, F.rank, 1.0, A2, out_rows, Z.d(), F.rank, 0.0, Y_dev, ldy);
+        }
         c.sync();
     });
 }
@@ -472,8 +477,13 @@ hydot_status hydot_j_matmat(hydot_ctx ctx, hydot_factor f, int trans, int b, con
                 return;
             }
             DBuf Z = dalloc(c, size_t(R * q)), T = dalloc(c, size_t(M * q));
-            dgemm(c, true, false, R, q, N, 1.0, F.V.d(), N, X_dev, N, 0.0, Z.d(), R);
-            dgemm(c, false, false, M, q, R, 1.0, F.U.d(), M, Z.d(), R, 0.0, T.d(), M);
+            if (skinny_ok(int(q))) {
+                skinny_tn(c, N, R, int(q), F.V.d(), N, X_dev, N, Z.d(), R);
+                skinny_nn(c, M, R, int(q), F.U.d(), M, Z.d(), R, T.d(), M);
+            } else {
+                dgemm(c, true, false, R, q, N, 1.0, F.V.d(), N, X_dev, N, 0.0, Z.d(), R);
+                dgemm(c, false, false, M, q, R, 1.0, F.U.d(), M, Z.d(), R, 0.0, T.d(), M);
+            }
             j_combine(c, M, b, n_c, n_lambda, T.d(), M, row_perm_dev, eps_c_dev, Y_dev, ldy);
         } else {
             if (ldx < M || ldy != N * n_c) throw std::invalid_argument("J rmatvec: dimension mismatch");
@@ -484,8 +494,13 @@ hydot_status hydot_j_matmat(hydot_ctx ctx, hydot_factor f, int trans, int b, con
             }
             DBuf G = dalloc(c, size_t(M * q)), W = dalloc(c, size_t(R * q));
             j_gather_scale(c, M, b, n_c, n_lambda, X_dev, ldx, row_perm_dev, eps_c_dev, G.d(), M);
-            dgemm(c, true, false, R, q, M, 1.0, F.U.d(), M, G.d(), M, 0.0, W.d(), R);
-            dgemm(c, false, false, N, q, R, 1.0, F.V.d(), N, W.d(), R, 0.0, Y_dev, N);
+            if (skinny_ok(int(q))) {
+                skinny_tn(c, M, R, int(q), F.U.d(), M, G.d(), M, W.d(), R);
+                skinny_nn(c, N, R, int(q), F.V.d(), N, W.d(), R, Y_dev, N);
+            } else {
+                dgemm(c, true, false, R, q, M, 1.0, F.U.d(), M, G.d(), M, 0.0, W.d(), R);
+                dgemm(c, false, false, N, q, R, 1.0, F.V.d(), N, W.d(), R, 0.0, Y_dev, N);
+            }
         }
         c.sync();
     });

@@ -189,6 +189,13 @@ void j_combine(Ctx& c, int64_t M, int b, int nc, int nl, const double* T, int64_
                const int* row_perm, const double* eps_c, double* Y, int64_t ldy);
 void j_gather_scale(Ctx& c, int64_t M, int b, int nc, int nl, const double* X, int64_t ldx,
                     const int* row_perm, const double* eps_c, double* G, int64_t ldg);
+// tall-skinny products for q <= 16 right-hand sides (HBM streams):
+// Z (R x q) = A^T X with A K x R;  Y (M x q) = A Z with A M x R
+bool skinny_ok(int q);
+void skinny_tn(Ctx& c, int64_t K, int64_t R, int q, const double* A, int64_t lda, const double* X,
+               int64_t ldx, double* Z, int64_t ldz);
+void skinny_nn(Ctx& c, int64_t M, int64_t R, int q, const double* A, int64_t lda, const double* Z,
+               int64_t ldz, double* Y, int64_t ldy);
 
 // rng.cu
 class RngStream {

@@ -61,3 +61,194 @@ void j_gather_scale(Ctx& c, int64_t M, int b, int nc, int nl, const double* X, i
 }
 
 }  // namespace hydot
+
+// --------------------------------------------------------- skinny GEMMs --
+// The b = 1 J~ products are two tall-skinny matrix products (R x q and
+// M x q with q = b * n_c <= 16): HBM-bound streams of V (N x R) and U
+// (M x R).  The DMMA tile kernel wastes its 64-wide N tile there, so these
+// kernels read every factor element exactly once with coalesced loads,
+// keep the skinny operand in shared memory and reduce split partials in a
+// fixed order (deterministic).
+namespace hydot {
+namespace {
+
+constexpr int SK_T = 256;  // threads per CTA
+
+// partial Z_chunk[j, c] = sum_{i in chunk} A[i, j] X[i, c]
+template <int Q>
+__global__ void __launch_bounds__(SK_T) skinny_tn_k(int64_t K, int64_t R, int64_t T,
+                                                    const double* __restrict__ A, int64_t lda,
+                                                    const double* __restrict__ X, int64_t ldx,
+                                                    double* __restrict__ part, int64_t jgroup,
+                                                    int q) {
+    extern __shared__ double xs[];  // T x Q (columns >= q are zero)
+    const int64_t i0 = int64_t(blockIdx.x) * T;
+    const int64_t rows = min(T, K - i0);
+    for (int64_t e = threadIdx.x; e < rows * Q; e += SK_T) {
+        const int64_t i = e % rows;
+        const int c = int(e / rows);
+        xs[i + c * T] = c < q ? X[i0 + i + int64_t(c) * ldx] : 0.0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t j0 = int64_t(blockIdx.y) * jgroup;
+    const int64_t j1 = min(R, j0 + jgroup);
+    for (int64_t j = j0 + warp; j < j1; j += SK_T / 32) {
+        const double* a = A + i0 + j * lda;
+        double acc[Q];
+#pragma unroll
+        for (int c = 0; c < Q; ++c) acc[c] = 0.0;
+        for (int64_t i = lane; i < rows; i += 32) {
+            const double v = __ldcs(a + i);
+#pragma unroll
+            for (int c = 0; c < Q; ++c) acc[c] += v * xs[i + c * T];
+        }
+#pragma unroll
+        for (int c = 0; c < Q; ++c)
+            for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+        if (lane < q) {
+            double v = 0.0;
+#pragma unroll
+            for (int c = 0; c < Q; ++c)
+                if (c == lane) v = acc[c];
+            part[(int64_t(blockIdx.x) * R + j) * q + lane] = v;
+        }
+    }
+}
+
+// Z[j, c] = sum_chunks part[chunk][j][c] (fixed order)
+__global__ void skinny_reduce_k(int64_t nchunks, int64_t R, int Q, const double* __restrict__ part,
+                                double* __restrict__ Z, int64_t ldz) {
+    const int64_t total = R * Q;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t j = e / Q;
+        const int c = int(e % Q);
+        double s = 0.0;
+        for (int64_t k = 0; k < nchunks; ++k) s += part[(k * R + j) * Q + c];
+        Z[j + int64_t(c) * ldz] = s;
+    }
+}
+
+// partial Y_chunk[i, c] = sum_{j in chunk} A[i, j] Z[j, c]
+template <int Q>
+__global__ void __launch_bounds__(SK_T) skinny_nn_k(int64_t M, int64_t R, int64_t RC,
+                                                    const double* __restrict__ A, int64_t lda,
+                                                    const double* __restrict__ Z, int64_t ldz,
+                                                    double* __restrict__ part, int q) {
+    extern __shared__ double zs[];  // RC x Q (columns >= q are zero)
+    const int64_t j0 = int64_t(blockIdx.y) * RC;
+    const int64_t cols = min(RC, R - j0);
+    for (int64_t e = threadIdx.x; e < cols * Q; e += SK_T) {
+        const int64_t j = e / Q;
+        const int c = int(e % Q);
+        zs[j * Q + c] = c < q ? Z[j0 + j + int64_t(c) * ldz] : 0.0;
+    }
+    __syncthreads();
+    const int64_t i = int64_t(blockIdx.x) * SK_T + threadIdx.x;
+    if (i >= M) return;
+    double acc[Q];
+#pragma unroll
+    for (int c = 0; c < Q; ++c) acc[c] = 0.0;
+    const double* a = A + i + j0 * lda;
+    for (int64_t j = 0; j < cols; ++j) {
+        const double v = __ldcs(a + j * lda);
+#pragma unroll
+        for (int c = 0; c < Q; ++c) acc[c] += v * zs[j * Q + c];
+    }
+#pragma unroll
+    for (int c = 0; c < Q; ++c)
+        if (c < q) part[(int64_t(blockIdx.y) * q + c) * M + i] = acc[c];
+}
+
+__global__ void skinny_nn_reduce_k(int64_t M, int64_t nchunks, int Q, const double* __restrict__ part,
+                                   double* __restrict__ Y, int64_t ldy) {
+    const int64_t total = M * Q;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = e % M;
+        const int c = int(e / M);
+        double s = 0.0;
+        for (int64_t k = 0; k < nchunks; ++k) s += part[(k * Q + c) * M + i];
+        Y[i + int64_t(c) * ldy] = s;
+    }
+}
+
+template <int Q>
+void skinny_tn_t(Ctx& c, int64_t K, int64_t R, int q, const double* A, int64_t lda, const double* X,
+                 int64_t ldx, double* Z, int64_t ldz) {
+    const int64_t T = (16384 / Q);  // 128 KB of X per CTA
+    const int64_t nchunks = (K + T - 1) / T;
+    const int64_t want = int64_t(c.num_sms) * 4;
+    int64_t groups = std::max<int64_t>(1, (want + nchunks - 1) / nchunks);
+    int64_t jgroup = std::max<int64_t>(8, (R + groups - 1) / groups);
+    groups = (R + jgroup - 1) / jgroup;
+    DBuf part = dalloc(c, size_t(nchunks * R * q));
+    static bool attr = false;
+    if (!attr) {
+        HYDOT_CUDA(cudaFuncSetAttribute(skinny_tn_k<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        int(T * Q * 8)));
+        attr = true;
+    }
+    skinny_tn_k<Q><<<dim3(unsigned(nchunks), unsigned(groups)), SK_T, size_t(T * Q * 8), c.stream>>>(
+        K, R, T, A, lda, X, ldx, part.d(), jgroup, q);
+    c.check_launch();
+    int blocks = int(std::max<int64_t>(1, std::min<int64_t>((R * q + 255) / 256, int64_t(c.num_sms) * 4)));
+    skinny_reduce_k<<<blocks, 256, 0, c.stream>>>(nchunks, R, q, part.d(), Z, ldz);
+    c.check_launch();
+}
+
+template <int Q>
+void skinny_nn_t(Ctx& c, int64_t M, int64_t R, int q, const double* A, int64_t lda, const double* Z,
+                 int64_t ldz, double* Y, int64_t ldy) {
+    const int64_t rb = (M + SK_T - 1) / SK_T;
+    const int64_t want = int64_t(c.num_sms) * 8;
+    int64_t nch = std::max<int64_t>(1, std::min<int64_t>((want + rb - 1) / rb, (R + 63) / 64));
+    int64_t RC = (R + nch - 1) / nch;
+    RC = std::min<int64_t>(RC, 16384 / Q);
+    nch = (R + RC - 1) / RC;
+    DBuf part = dalloc(c, size_t(nch * q * M));
+    static bool attr = false;
+    if (!attr) {
+        HYDOT_CUDA(cudaFuncSetAttribute(skinny_nn_k<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        16384 * 8));
+        attr = true;
+    }
+    skinny_nn_k<Q><<<dim3(unsigned(rb), unsigned(nch)), SK_T, size_t(RC * Q * 8), c.stream>>>(
+        M, R, RC, A, lda, Z, ldz, part.d(), q);
+    c.check_launch();
+    int blocks = int(std::max<int64_t>(1, std::min<int64_t>((M * q + 255) / 256, int64_t(c.num_sms) * 8)));
+    skinny_nn_reduce_k<<<blocks, 256, 0, c.stream>>>(M, nch, q, part.d(), Y, ldy);
+    c.check_launch();
+}
+
+}  // namespace
+
+bool skinny_ok(int q) { return q >= 1 && q <= 16; }
+
+void skinny_tn(Ctx& c, int64_t K, int64_t R, int q, const double* A, int64_t lda, const double* X,
+               int64_t ldx, double* Z, int64_t ldz) {
+    StageTimer _t(c, "skinny_tn", K, R, q);
+    switch (q) {
+        case 1: skinny_tn_t<1>(c, K, R, q, A, lda, X, ldx, Z, ldz); break;
+        case 2: skinny_tn_t<2>(c, K, R, q, A, lda, X, ldx, Z, ldz); break;
+        case 3: case 4: skinny_tn_t<4>(c, K, R, q, A, lda, X, ldx, Z, ldz); break;
+        case 5: case 6: case 7: case 8: skinny_tn_t<8>(c, K, R, q, A, lda, X, ldx, Z, ldz); break;
+        default: skinny_tn_t<16>(c, K, R, q, A, lda, X, ldx, Z, ldz); break;
+    }
+    (void)q;
+}
+
+void skinny_nn(Ctx& c, int64_t M, int64_t R, int q, const double* A, int64_t lda, const double* Z,
+               int64_t ldz, double* Y, int64_t ldy) {
+    StageTimer _t(c, "skinny_nn", M, R, q);
+    switch (q) {
+        case 1: skinny_nn_t<1>(c, M, R, q, A, lda, Z, ldz, Y, ldy); break;
+        case 2: skinny_nn_t<2>(c, M, R, q, A, lda, Z, ldz, Y, ldy); break;
+        case 3: case 4: skinny_nn_t<4>(c, M, R, q, A, lda, Z, ldz, Y, ldy); break;
+        case 5: case 6: case 7: case 8: skinny_nn_t<8>(c, M, R, q, A, lda, Z, ldz, Y, ldy); break;
+        default: skinny_nn_t<16>(c, M, R, q, A, lda, Z, ldz, Y, ldy); break;
+    }
+}
+
+}  // namespace hydot

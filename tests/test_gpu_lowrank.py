@@ -204,3 +204,22 @@ def test_lr_matvec_adjoint(ctx):
         assert fro(lr.lr_matvec(ctx, f, torch.as_tensor(x)).cpu().numpy() - A @ x) <= 1e-10 * fro(A @ x)
     with pytest.raises(ValueError):
         lr.lr_matvec(ctx, f, torch.zeros(30, dtype=torch.float64))
+
+
+@pytest.mark.parametrize("b", [1, 2, 3, 5, 8, 13, 16, 17, 64])
+def test_lr_matmat_widths(ctx, b):
+    """skinny (b <= 16) and DMMA (b > 16) paths of U (V^T X) / V (U^T Y)."""
+    from paper_1410_0986_b200 import lowrank as lr
+    rng = np.random.default_rng(b)
+    M, N, R = 700, 40000, 123
+    U = rng.standard_normal((M, R))
+    V = rng.standard_normal((N, R))
+    f = lr.LowRankFactor.from_tensors(ctx, torch.as_tensor(U), torch.as_tensor(V))
+    X = rng.standard_normal((N, b))
+    Y = rng.standard_normal((M, b))
+    want = U @ (V.T @ X)
+    got = lr.lr_matmat if False else lr.lr_matvec(ctx, f, torch.as_tensor(X)).cpu().numpy()
+    assert fro(got - want) <= 1e-13 * fro(want)
+    want2 = V @ (U.T @ Y)
+    got2 = lr.lr_rmatvec(ctx, f, torch.as_tensor(Y)).cpu().numpy()
+    assert fro(got2 - want2) <= 1e-13 * fro(want2)
