@@ -34,6 +34,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_PEAK_TFLOPS = 37.0  # tools/fp64_peak.cu on this pool's B200: DMMA 37.1, DFMA 37.0 TF/s
+try:
+    HBM_PEAK_GBS = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+except (OSError, KeyError, ValueError):
+    HBM_PEAK_GBS = 6554.9  # the value of MEASURED_PEAKS.json on this pool
 PEAK_SOURCE = "measured: tools/fp64_peak.cu (DMMA m16n8k4, register-resident) -> profiles/fp64_peak_r01.txt"
 
 
@@ -174,6 +178,8 @@ def run_b200(args):
     # ---- timed region (value): fields resident, K steps, max over ranks
     clocks = ClockSampler(local)
     clocks.start()
+    h.lib().hydot_ctx_timing_report(ctx.h, None, 0)   # drop warm-up records
+    h.lib().hydot_ctx_set_timing(ctx.h, 1)            # live CUDA-event stage timing
     launches0 = ctx.launch_count()
     if world > 1:
         dist.barrier()
@@ -189,6 +195,11 @@ def run_b200(args):
         dist.barrier()
     ms = e0.elapsed_time(e1)
     launches = ctx.launch_count() - launches0
+    h.lib().hydot_ctx_set_timing(ctx.h, 0)
+    buf = ctypes.create_string_buffer(1 << 16)
+    h.lib().hydot_ctx_timing_report(ctx.h, buf, 1 << 16)
+    stages = {k: {"ms_per_step": v[0] / args.steps, "calls_per_step": v[1] / args.steps,
+                  "flops": v[2], "bytes": v[3]} for k, v in json.loads(buf.value.decode()).items()}
     clk = clocks.stop()
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -268,7 +279,7 @@ def run_b200(args):
             nbytes = 8.0 * (g.N * R + cfg.M * R + b * cfg.n_chrom * g.N + b * cfg.M)
             flops = 2.0 * R * b * cfg.n_chrom * (g.N + cfg.M)
             matvec[f"b{b}"] = {"ms": t * 1e3, "GB/s": nbytes / t / 1e9, "TFLOP/s": flops / t / 1e12,
-                               "hbm_frac": nbytes / t / 1e9 / 6554.9,
+                               "hbm_frac": nbytes / t / 1e9 / HBM_PEAK_GBS,
                                "fp64_frac": flops / t / 1e12 / FP64_PEAK_TFLOPS}
 
         # ---- CPU baseline (rank 0, N=1 only): the oracle on a bounded sample
@@ -303,12 +314,14 @@ def run_b200(args):
             "e2e": {"value": e2e_value, "unit": "blocks/s", "h2d_bytes_per_step": h2d_bytes,
                     "d2h_bytes_per_step": int(d2h_bytes), "ms_per_step": e2e_step_ms},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": FP64_PEAK_TFLOPS,
-                         "unit": "TFLOP/s", "frac": achieved_tflops / FP64_PEAK_TFLOPS,
-                         "traffic": None,
-                         "what": "compression stage: reference FlopLedger flops per step "
-                                 "(lowrank.cpp:31-51, %.3e) / CUDA-event step time" % ledger_flops,
-                         "peak_source": PEAK_SOURCE},
+            "roofline": roofline_of(stages, args.steps),
+            "stage_roofline": {"bound": "tensor", "achieved": achieved_tflops,
+                               "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                               "frac": achieved_tflops / FP64_PEAK_TFLOPS,
+                               "what": "whole compression step: reference FlopLedger flops "
+                                       "(lowrank.cpp:31-51, %.3e) / CUDA-event step time"
+                                       % ledger_flops},
+            "stages": stages,
             "clocks": clk,
             "matvec": matvec,
             "fields_setup": {"systems": int(len(pts) * cfg.n_lambda),
@@ -321,6 +334,43 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+# leaf kernel classes (composite stages such as qr_geqrf / qr_apply_q contain
+# gemm and qr_panel launches and are not candidates)
+KERNEL_CLASSES = {
+    "gemm": ("tensor", "dgemm_kernel + splitk_reduce (DMMA m16n8k4.f64)"),
+    "svd_jacobi_large": ("tensor", "jacobi_coop_k (one-sided Jacobi; flops = reference BDCSVD "
+                                   "count 14*max*min^2, lowrank.cpp:38-41)"),
+    "svd_jacobi_small": ("tensor", "jacobi_smem_k"),
+    "qr_panel": ("tensor", "qr_panel_coop (Householder panel, 2*m*32^2 flops)"),
+    "skinny_tn": ("hbm", "skinny_tn_k (V^T X, b<=16)"),
+    "skinny_nn": ("hbm", "skinny_nn_k (U Z, b<=16)"),
+    "born_block": ("hbm", "born_block_k"),
+}
+TRAFFIC = {}  # filled from profiles/ when an ncu --set full capture exists
+
+
+def roofline_of(stages, steps):
+    """Roofline of the dominant kernel class, measured live (CUDA events on
+    the launching stream over the timed region)."""
+    cands = {k: v for k, v in stages.items() if k in KERNEL_CLASSES}
+    if not cands:
+        return None
+    name = max(cands, key=lambda k: cands[k]["ms_per_step"])
+    v = cands[name]
+    bound, what = KERNEL_CLASSES[name]
+    secs = v["ms_per_step"] * steps / 1e3
+    if bound == "tensor":
+        ach = v["flops"] / secs / 1e12
+        peak, unit = FP64_PEAK_TFLOPS, "TFLOP/s"
+    else:
+        ach = v["bytes"] / secs / 1e9
+        peak, unit = HBM_PEAK_GBS, "GB/s"
+    return {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+            "traffic": TRAFFIC.get(name), "kernel": what, "stage": name,
+            "ms_per_step": v["ms_per_step"], "launch_groups_per_step": v["calls_per_step"],
+            "peak_source": PEAK_SOURCE if bound == "tensor" else "MEASURED_PEAKS.json hbm_gbs"}
 
 
 def global_perm(tree, plan, rows_per, st):

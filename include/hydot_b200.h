@@ -75,6 +75,11 @@ int64_t hydot_ctx_launch_count(hydot_ctx ctx);
 /* per-stage wall times recorded when HYDOT_PROFILE=1 (JSON written into buf,
  * then cleared); returns the JSON length */
 int hydot_profile_dump(char* buf, int len);
+/* live per-stage timing with CUDA events on the context stream (no extra
+ * synchronisation while on); the report resolves and clears the records:
+ * JSON {stage: [ms, calls, algorithmic flops, algorithmic bytes]} */
+hydot_status hydot_ctx_set_timing(hydot_ctx ctx, int on);
+int hydot_ctx_timing_report(hydot_ctx ctx, char* buf, int len);
 
 /* ------------------------------------------------------------- fields -- */
 /* 7-point vertex-centred FV operator on an nx*ny*nz vertex grid (spacing h,

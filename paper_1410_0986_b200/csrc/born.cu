@@ -48,7 +48,7 @@ __global__ void born_block_k(int64_t N, int nl, const double* __restrict__ inc,
 
 void born_block(Ctx& c, int64_t N, int nl, const double* inc, const double* const* adj_h, int nd,
                 const double* w, double nu, double* out, int64_t ld) {
-    StageTimer _t(c, "born_block");
+    StageTimer _t(c, "born_block", N, nl, nd, 0.0, 8.0 * double(N) * (2.0 * nd * nl + nl + 1));
     if (N <= 0 || nl <= 0 || nd <= 0) return;
     if (ld < N) throw std::invalid_argument("assemble_H_block: ld < N");
     int rows = nd * nl;

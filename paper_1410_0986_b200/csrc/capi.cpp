@@ -8,6 +8,8 @@
 
 using namespace hydot;
 
+std::string timing_report(hydot::Ctx& c);  // util.cu
+
 struct hydot_ctx_s {
     std::shared_ptr<Ctx> c;
 };
@@ -131,6 +133,17 @@ hydot_status hydot_ctx_synchronize(hydot_ctx ctx) {
 }
 
 int64_t hydot_ctx_launch_count(hydot_ctx ctx) { return ctx && ctx->c ? ctx->c->launches : -1; }
+
+hydot_status hydot_ctx_set_timing(hydot_ctx ctx, int on) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] { ctx_of(ctx).timing = on != 0; });
+}
+
+int hydot_ctx_timing_report(hydot_ctx ctx, char* buf, int len) {
+    if (!ctx || !ctx->c) return -1;
+    std::string s = timing_report(*ctx->c);
+    if (buf && len > 0) snprintf(buf, size_t(len), "%s", s.c_str());
+    return int(s.size());
+}
 
 // ------------------------------------------------------------- fields ----
 hydot_status hydot_fields_solve(hydot_ctx ctx, const hydot_grid7* grid, int n_lambda,

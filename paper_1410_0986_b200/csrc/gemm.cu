@@ -176,7 +176,8 @@ __global__ void scale_kernel(int64_t M, int64_t N, double beta, double* C, int64
 void dgemm(Ctx& c, bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alpha,
            const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
            int64_t ldc) {
-    StageTimer _t(c, "gemm", m, n, k);
+    StageTimer _t(c, "gemm", m, n, k, 2.0 * double(m) * double(n) * double(k),
+                  8.0 * (double(m) * k + double(k) * n + double(m) * n * (beta != 0.0 ? 2 : 1)));
     if (m <= 0 || n <= 0) return;
     if (k <= 0 || alpha == 0.0) {
         int blocks = int(std::min<int64_t>((m * n + 255) / 256, 4096));

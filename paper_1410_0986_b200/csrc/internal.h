@@ -39,6 +39,26 @@ struct Ctx {
     // MT19937-64 jump polynomials on the device (rng.cu)
     uint64_t* jump_dev = nullptr;
     int64_t jump_n = 0;
+    // live per-stage timing with CUDA events on the context stream (no
+    // synchronisation; hydot_ctx_timing_report resolves them)
+    bool timing = false;
+    struct TRec {
+        const char* name;
+        cudaEvent_t a, b;
+        double flops, bytes;
+    };
+    std::vector<TRec> trecs;
+    std::vector<cudaEvent_t> ev_pool;
+    cudaEvent_t take_event() {
+        if (!ev_pool.empty()) {
+            cudaEvent_t e = ev_pool.back();
+            ev_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        HYDOT_CUDA(cudaEventCreate(&e));
+        return e;
+    }
     void count(int64_t n = 1) { launches += n; }
     void check_launch() {
         cudaError_t e = cudaGetLastError();
@@ -105,13 +125,16 @@ inline DBuf dalloc(Ctx& c, size_t n_doubles) { return DBuf(c, n_doubles * sizeof
 // Optional stage timer (HYDOT_PROFILE=1): synchronises around each scoped
 // stage and accumulates wall time per name; report via hydot_profile_dump().
 struct StageTimer {
-    StageTimer(Ctx& c, const char* name, int64_t a = -1, int64_t b = -1, int64_t k = -1);
+    StageTimer(Ctx& c, const char* name, int64_t a = -1, int64_t b = -1, int64_t k = -1,
+               double flops = 0.0, double bytes = 0.0);
     ~StageTimer();
     Ctx& c_;
     const char* name_;
     int64_t a_, b_, k_;
     double t0_ = 0;
     bool on_ = false;
+    double flops_, bytes_;
+    cudaEvent_t ea_ = nullptr;
 };
 
 // ---------------------------------------------------------------- ledger --

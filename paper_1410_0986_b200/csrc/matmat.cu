@@ -228,7 +228,7 @@ bool skinny_ok(int q) { return q >= 1 && q <= 16; }
 
 void skinny_tn(Ctx& c, int64_t K, int64_t R, int q, const double* A, int64_t lda, const double* X,
                int64_t ldx, double* Z, int64_t ldz) {
-    StageTimer _t(c, "skinny_tn", K, R, q);
+    StageTimer _t(c, "skinny_tn", K, R, q, 2.0 * double(K) * R * q, 8.0 * (double(K) * R + double(K) * q));
     switch (q) {
         case 1: skinny_tn_t<1>(c, K, R, q, A, lda, X, ldx, Z, ldz); break;
         case 2: skinny_tn_t<2>(c, K, R, q, A, lda, X, ldx, Z, ldz); break;
@@ -241,7 +241,7 @@ void skinny_tn(Ctx& c, int64_t K, int64_t R, int q, const double* A, int64_t lda
 
 void skinny_nn(Ctx& c, int64_t M, int64_t R, int q, const double* A, int64_t lda, const double* Z,
                int64_t ldz, double* Y, int64_t ldy) {
-    StageTimer _t(c, "skinny_nn", M, R, q);
+    StageTimer _t(c, "skinny_nn", M, R, q, 2.0 * double(M) * R * q, 8.0 * (double(M) * R + double(M) * q));
     switch (q) {
         case 1: skinny_nn_t<1>(c, M, R, q, A, lda, Z, ldz, Y, ldy); break;
         case 2: skinny_nn_t<2>(c, M, R, q, A, lda, Z, ldz, Y, ldy); break;

@@ -206,6 +206,7 @@ __global__ void __launch_bounds__(NB) larft_k(int jb, const double* __restrict__
 }
 
 void panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, const PanelBufs& pbuf) {
+    StageTimer _t(c, "qr_panel", mr, jb, -1, 2.0 * double(mr) * jb * jb, 16.0 * double(mr) * jb);
     static bool attr = false;
     const size_t smem_cap = 200 * 1024;
     int G = c.num_sms;
@@ -262,7 +263,7 @@ void larft(Ctx& c, int jb, const double* G, int64_t ldg, const double* tau, doub
 }  // namespace
 
 void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f) {
-    StageTimer _t(c, "qr_geqrf", m, n);
+    StageTimer _t(c, "qr_geqrf", m, n, -1, 2.0 * double(m) * double(n) * double(n));
     f.m = m;
     f.n = n;
     f.a = dalloc(c, size_t(std::max<int64_t>(m * n, 1)));
@@ -316,7 +317,7 @@ void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f
 }
 
 void apply_q(Ctx& c, const QRFact& f, bool trans, int64_t k, double* Y, int64_t ldy) {
-    StageTimer _t(c, "qr_apply_q", f.m, f.n, k);
+    StageTimer _t(c, "qr_apply_q", f.m, f.n, k, 4.0 * double(f.m) * double(std::min(f.m, f.n)) * double(k));
     const int64_t m = f.m, kk = std::min(f.m, f.n);
     if (k <= 0 || kk <= 0) return;
     DBuf V = dalloc(c, size_t(m) * NB);

@@ -480,7 +480,8 @@ bool stats_on() {
 
 void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, double* Uo,
                 int64_t lduo, std::vector<double>& s, double* Vo, int64_t ldvo) {
-    StageTimer _t(c, n > 96 ? "svd_jacobi_large" : "svd_jacobi_small");
+    StageTimer _t(c, n > 96 ? "svd_jacobi_large" : "svd_jacobi_small", m, n, -1,
+                  14.0 * double(std::max(m, n)) * double(std::min(m, n)) * double(std::min(m, n)));
     s.assign(static_cast<size_t>(std::max<int64_t>(n, 0)), 0.0);
     if (n <= 0) return;
     if (m < n) throw std::invalid_argument("jacobi_svd: needs m >= n");

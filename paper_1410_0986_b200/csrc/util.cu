@@ -197,6 +197,7 @@ double frob_diff(Ctx& c, int64_t rows, int64_t cols, const double* A, int64_t ld
 }  // namespace hydot
 
 // ------------------------------------------------------------ profiling --
+#include <array>
 #include <chrono>
 #include <cstdlib>
 #include <map>
@@ -226,8 +227,13 @@ double now_s() {
 thread_local int g_depth = 0;
 }  // namespace
 
-StageTimer::StageTimer(Ctx& c, const char* name, int64_t a, int64_t b, int64_t k)
-    : c_(c), name_(name), a_(a), b_(b), k_(k) {
+StageTimer::StageTimer(Ctx& c, const char* name, int64_t a, int64_t b, int64_t k, double flops,
+                       double bytes)
+    : c_(c), name_(name), a_(a), b_(b), k_(k), flops_(flops), bytes_(bytes) {
+    if (c_.timing) {
+        ea_ = c_.take_event();
+        cudaEventRecord(ea_, c_.stream);
+    }
     on_ = prof_on() && g_depth == 0;
     ++g_depth;
     if (on_) {
@@ -237,6 +243,11 @@ StageTimer::StageTimer(Ctx& c, const char* name, int64_t a, int64_t b, int64_t k
 }
 StageTimer::~StageTimer() {
     --g_depth;
+    if (ea_) {
+        cudaEvent_t eb = c_.take_event();
+        cudaEventRecord(eb, c_.stream);
+        c_.trecs.push_back(Ctx::TRec{name_, ea_, eb, flops_, bytes_});
+    }
     if (!on_) return;
     cudaStreamSynchronize(c_.stream);
     double dt = now_s() - t0_;
@@ -249,6 +260,34 @@ StageTimer::~StageTimer() {
                 (long long)k_, dt * 1e3);
 }
 }  // namespace hydot
+
+// resolve the event records of a context: JSON {name: [ms, calls, flops, bytes]}
+std::string timing_report(hydot::Ctx& c) {
+    cudaStreamSynchronize(c.stream);
+    std::map<std::string, std::array<double, 4>> agg;
+    for (auto& r : c.trecs) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        auto& e = agg[r.name];
+        e[0] += ms;
+        e[1] += 1;
+        e[2] += r.flops;
+        e[3] += r.bytes;
+        c.ev_pool.push_back(r.a);
+        c.ev_pool.push_back(r.b);
+    }
+    c.trecs.clear();
+    std::string s = "{";
+    bool first = true;
+    for (auto& kv : agg) {
+        char tmp[320];
+        snprintf(tmp, sizeof tmp, "%s\"%s\": [%.6f, %.0f, %.6e, %.6e]", first ? "" : ", ", kv.first.c_str(),
+                 kv.second[0], kv.second[1], kv.second[2], kv.second[3]);
+        s += tmp;
+        first = false;
+    }
+    return s + "}";
+}
 
 extern "C" int hydot_profile_dump(char* buf, int len) {
     std::lock_guard<std::mutex> lk(hydot::g_prof_mu);
