@@ -145,9 +145,17 @@ def run_b200(args):
                  {int(st.detector_point[s, d]) for s in srcs for d in range(cfg.n_det)})
     loc = {p: i for i, p in enumerate(pts)}
     # ---- setup (untimed): this shard's fields on its GPU, resident in HBM
+    # (timed with CUDA events: the CG roofline is reported separately)
+    fe0, fe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    fe0.record(torch.cuda.current_stream())
     F, fstats = born.compute_fields(ctx, g, st.sigma, st.sigma_prime, st.inv_D,
                                     st.points[pts], tol=1e-10)
+    fe1.record(torch.cuda.current_stream())
     torch.cuda.synchronize()
+    fields_s = fe0.elapsed_time(fe1) / 1e3
+    cg_iters = float(fstats.iters.sum())
+    fields_gbs = 48.0 * g.N * cg_iters / fields_s / 1e9  # 48 N B per system-iteration
     w = torch.full((g.N,), cfg.h ** 3, dtype=torch.float64, device=dev)
 
     def provider_for(Fdev):
@@ -326,7 +334,15 @@ def run_b200(args):
             "matvec": matvec,
             "fields_setup": {"systems": int(len(pts) * cfg.n_lambda),
                              "iters_max": int(fstats.iters.max()),
-                             "relres_max": float(fstats.relres.max())},
+                             "iters_total": int(cg_iters),
+                             "relres_max": float(fstats.relres.max()),
+                             "seconds": fields_s,
+                             "roofline": {"bound": "hbm", "achieved": fields_gbs,
+                                          "peak": HBM_PEAK_GBS, "unit": "GB/s",
+                                          "frac": fields_gbs / HBM_PEAK_GBS,
+                                          "what": "batched CG (cg_pa + cg_xr): 48 N bytes per "
+                                                  "system-iteration (SURVEY 8d)"},
+                             "e2e_with_fields_blocks_per_s": units / (ms_per_step / 1e3 + fields_s)},
         }
         if cpu is not None:
             out["cpu_baseline"] = cpu

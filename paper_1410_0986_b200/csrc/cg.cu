@@ -21,22 +21,44 @@ namespace hydot {
 namespace {
 
 constexpr int CT = 256;       // threads per CTA
-constexpr int VPT = 4;        // vertices per thread
+constexpr int VPT = 16;       // vertices per thread (amortises the scalar prologue)
 constexpr int CV = CT * VPT;  // vertices per CTA
 
 struct Stencil {
     int nx, ny, nz;
     double h;
+    float inv_nx, inv_ny;  // for the division-free vertex decode
 };
+
+inline Stencil make_stencil(const hydot_grid7& g) {
+    return Stencil{g.nx, g.ny, g.nz, g.h, 1.0f / float(g.nx), 1.0f / float(g.ny)};
+}
+
+// q = i / d, r = i % d for i < 2^24 without an integer division: a float
+// estimate corrected by one step (64-bit div/mod dominated the CG kernels)
+__device__ __forceinline__ void fdivmod(unsigned i, unsigned d, float inv_d, unsigned& q,
+                                        unsigned& r) {
+    q = __float2uint_rz(__uint2float_rn(i) * inv_d);
+    int rr = int(i) - int(q * d);
+    if (rr < 0) {
+        --q;
+        rr += int(d);
+    } else if (rr >= int(d)) {
+        ++q;
+        rr -= int(d);
+    }
+    r = unsigned(rr);
+}
 
 // y_i = (A x)_i with x(j) supplied by a functor; reference operation order
 template <class Get>
 __device__ __forceinline__ double stencil_at(const Stencil& g, double sigma, double sigmap,
                                              int64_t i, Get get) {
     const int64_t plane = int64_t(g.nx) * g.ny;
-    const int ix = int(i % g.nx);
-    const int iy = int((i / g.nx) % g.ny);
-    const int iz = int(i / plane);
+    unsigned q1, ux, uy, uz;
+    fdivmod(unsigned(i), unsigned(g.nx), g.inv_nx, q1, ux);
+    fdivmod(q1, unsigned(g.ny), g.inv_ny, uz, uy);
+    const int ix = int(ux), iy = int(uy), iz = int(uz);
     const double xi = get(i);
     if (ix == 0 || ix == g.nx - 1 || iy == 0 || iy == g.ny - 1) return xi;
     const double h = g.h;
@@ -128,10 +150,11 @@ __global__ void __launch_bounds__(CT) cg_pa(Stencil g, int64_t N, int nl, int k0
                                             const double* __restrict__ Pold,
                                             double* __restrict__ Pnew, double* __restrict__ partA,
                                             const double* __restrict__ partB, int nparts,
-                                            SysState* __restrict__ st, double tol, int fixed) {
+                                            SysState* __restrict__ st, double tol, int fixed,
+                                            const int* __restrict__ act) {
     __shared__ double sh[CT / 32];
     __shared__ double bc;
-    const int sys = blockIdx.y;
+    const int sys = act[blockIdx.y];  // compacted list of unconverged systems
     SysState& S = st[sys];
     if (S.done) return;
     const int l = (k0 + sys) % nl;
@@ -186,10 +209,11 @@ __global__ void __launch_bounds__(CT) cg_xr(Stencil g, int64_t N, int nl, int k0
                                             const double* __restrict__ P,
                                             const double* __restrict__ partA,
                                             double* __restrict__ partB, int nparts,
-                                            SysState* __restrict__ st) {
+                                            SysState* __restrict__ st,
+                                            const int* __restrict__ act) {
     __shared__ double sh[CT / 32];
     __shared__ double bc;
-    const int sys = blockIdx.y;
+    const int sys = act[blockIdx.y];
     SysState& S = st[sys];
     if (S.done) return;
     const int l = (k0 + sys) % nl;
@@ -267,7 +291,7 @@ __global__ void count_active(int n, const SysState* __restrict__ st, int* __rest
 void apply7(Ctx& c, const hydot_grid7& g, double sigma, double sigmap, const double* x,
             double* y) {
     const int64_t N = int64_t(g.nx) * g.ny * g.nz;
-    Stencil s{g.nx, g.ny, g.nz, g.h};
+    Stencil s = make_stencil(g);
     int blocks = int(std::min<int64_t>((N + 255) / 256, int64_t(c.num_sms) * 16));
     apply7_k<<<blocks, 256, 0, c.stream>>>(s, N, sigma, sigmap, x, y);
     c.check_launch();
@@ -287,7 +311,9 @@ void fields_solve(Ctx& c, const hydot_grid7& g, int nl, const double* sigma,
         if (ix == 0 || ix == g.nx - 1 || iy == 0 || iy == g.ny - 1)
             throw std::invalid_argument("source support falls entirely on the Dirichlet boundary");
     }
-    Stencil st{g.nx, g.ny, g.nz, g.h};
+    Stencil st = make_stencil(g);
+    if (int64_t(g.nx) * g.ny * g.nz >= (int64_t(1) << 24))
+        throw std::invalid_argument("fields_solve: grid too large for the 24-bit vertex decode");
     const int total = n_rhs * nl;
     const int nparts = int((N + CV - 1) / CV);
     // batch so that r and p stay under ~24 GB
@@ -306,7 +332,7 @@ void fields_solve(Ctx& c, const hydot_grid7& g, int nl, const double* sigma,
     DBuf pA = dalloc(c, size_t(batch) * size_t(nparts));
     DBuf pB = dalloc(c, size_t(batch) * size_t(nparts));
     DBuf S(c, size_t(batch) * sizeof(SysState));
-    DBuf act(c, sizeof(int));
+    DBuf dact(c, sizeof(int) * size_t(batch));
     if (stats) {
         stats->iters.assign(size_t(total), 0);
         stats->relres.assign(size_t(total), 0.0);
@@ -323,35 +349,50 @@ void fields_solve(Ctx& c, const hydot_grid7& g, int nl, const double* sigma,
                                               P.d() + size_t(batch) * size_t(N), ss);
             c.check_launch();
         }
-        dim3 grid = dim3(unsigned(nparts), unsigned(nb));
         auto pbuf = [&](int i) { return P.d() + size_t(i & 1) * size_t(batch) * size_t(N); };
+        // active-system list: converged systems are dropped from the grid
+        // every 8 iterations (systems converge between ~70 and ~135 iterations)
+        std::vector<int> active(static_cast<size_t>(nb));
+        for (int k = 0; k < nb; ++k) active[size_t(k)] = k;
+        std::vector<SysState> hst(static_cast<size_t>(nb));
+        HYDOT_CUDA(cudaMemcpyAsync(dact.as<void>(), active.data(), active.size() * sizeof(int),
+                                   cudaMemcpyHostToDevice, c.stream));
         int it = 0;
         for (; it < limit; ++it) {
+            dim3 grid = dim3(unsigned(nparts), unsigned(active.size()));
             cg_pa<<<grid, CT, 0, c.stream>>>(st, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
                                             pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
-                                            tol, fixed_iters > 0);
+                                            tol, fixed_iters > 0, dact.as<int>());
             c.check_launch();
             cg_xr<<<grid, CT, 0, c.stream>>>(st, N, nl, k0, it, dsig.d(), dsigp.d(), X, R.d(),
-                                            pbuf(it), pA.d(), pB.d(), nparts, ss);
+                                            pbuf(it), pA.d(), pB.d(), nparts, ss, dact.as<int>());
             c.check_launch();
-            if (fixed_iters <= 0 && (it % 16) == 15) {
-                count_active<<<1, 1024, 0, c.stream>>>(nb, ss, act.as<int>());
-                c.check_launch();
-                int h = 0;
-                HYDOT_CUDA(cudaMemcpyAsync(&h, act.as<void>(), sizeof(int), cudaMemcpyDeviceToHost,
-                                           c.stream));
+            if (fixed_iters <= 0 && (it % 8) == 7) {
+                HYDOT_CUDA(cudaMemcpyAsync(hst.data(), ss, size_t(nb) * sizeof(SysState),
+                                           cudaMemcpyDeviceToHost, c.stream));
                 c.sync();
-                if (h == 0) {
+                std::vector<int> still;
+                for (int k : active)
+                    if (!hst[size_t(k)].done) still.push_back(k);
+                if (still.empty()) {
                     ++it;
                     break;
+                }
+                if (still.size() < active.size()) {
+                    active.swap(still);
+                    HYDOT_CUDA(cudaMemcpyAsync(dact.as<void>(), active.data(),
+                                               active.size() * sizeof(int), cudaMemcpyHostToDevice,
+                                               c.stream));
+                    c.sync();  // host vector is reused
                 }
             }
         }
         if (fixed_iters <= 0 && it >= limit) {
             // one more convergence check for systems finishing on the last step
+            dim3 grid = dim3(unsigned(nparts), unsigned(active.size()));
             cg_pa<<<grid, CT, 0, c.stream>>>(st, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
                                             pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
-                                            tol, 0);
+                                            tol, 0, dact.as<int>());
             c.check_launch();
         }
         {

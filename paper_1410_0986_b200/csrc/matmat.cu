@@ -98,10 +98,25 @@ __global__ void __launch_bounds__(SK_T) skinny_tn_k(int64_t K, int64_t R, int64_
         double acc[Q];
 #pragma unroll
         for (int c = 0; c < Q; ++c) acc[c] = 0.0;
-        for (int64_t i = lane; i < rows; i += 32) {
-            const double v = __ldcs(a + i);
+        if ((reinterpret_cast<uintptr_t>(a) & 15) == 0) {
+            // 128-bit streaming loads: two rows per lane per step
+            const int64_t rows2 = rows & ~int64_t(1);
+            for (int64_t i = 2 * lane; i < rows2; i += 64) {
+                const double2 v = __ldcs(reinterpret_cast<const double2*>(a + i));
 #pragma unroll
-            for (int c = 0; c < Q; ++c) acc[c] += v * xs[i + c * T];
+                for (int c = 0; c < Q; ++c) acc[c] += v.x * xs[i + c * T] + v.y * xs[i + 1 + c * T];
+            }
+            if ((rows & 1) && lane == 0) {
+                const double v = a[rows - 1];
+#pragma unroll
+                for (int c = 0; c < Q; ++c) acc[c] += v * xs[rows - 1 + c * T];
+            }
+        } else {
+            for (int64_t i = lane; i < rows; i += 32) {
+                const double v = __ldcs(a + i);
+#pragma unroll
+                for (int c = 0; c < Q; ++c) acc[c] += v * xs[i + c * T];
+            }
         }
 #pragma unroll
         for (int c = 0; c < Q; ++c)
