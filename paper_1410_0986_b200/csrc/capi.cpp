@@ -524,6 +524,7 @@ hydot_status hydot_thin_svd(hydot_ctx ctx, int64_t m, int64_t n, const double* a
     return guard(ctx ? ctx->c.get() : nullptr, [&] {
         Ctx& c = ctx_of(ctx);
         if (m < 0 || n < 0 || lda < m) throw std::invalid_argument("thin_svd: bad dimensions");
+        StrictSVD strict;  // full orthonormal U, V like Eigen::BDCSVD
         SVDd s = fast_thin_svd(c, a_dev, lda, false, m, n, nullptr, HYDOT_CAT_OTHER);
         const int64_t k = s.k;
         if (k > 0) {

@@ -192,6 +192,14 @@ void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f
 // Y (m x k) := Q Y (trans=false) or Q^T Y
 void apply_q(Ctx& c, const QRFact& f, bool trans, int64_t k, double* Y, int64_t ldy);
 
+// While alive, Jacobi SVDs accumulate V for every column (full BDCSVD
+// contract, e.g. hydot_thin_svd); otherwise the large driver recovers V
+// from one GEMM, exact for every singular triple the path can keep.
+struct StrictSVD {
+    StrictSVD();
+    ~StrictSVD();
+    bool prev_;
+};
 // svd.cu : one-sided Jacobi thin SVD of X (m x n, m >= n); s descending.
 void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, double* U,
                 int64_t ldu, std::vector<double>& s, double* V, int64_t ldv);

@@ -224,12 +224,14 @@ __global__ void __launch_bounds__(JT) jacobi_coop_k(int64_t m, int n, int np,
                         up[i] = cs * x - sn * y;
                         uq[i] = sn * x + cs * y;
                     }
-                    double* vp = V + int64_t(pr.x) * ldv;
-                    double* vq = V + int64_t(pr.y) * ldv;
-                    for (int64_t i = threadIdx.x; i < n; i += JT) {
-                        double x = vp[i], y = vq[i];
-                        vp[i] = cs * x - sn * y;
-                        vq[i] = sn * x + cs * y;
+                    if (V) {  // V == nullptr: right vectors recovered after the sweeps
+                        double* vp = V + int64_t(pr.x) * ldv;
+                        double* vq = V + int64_t(pr.y) * ldv;
+                        for (int64_t i = threadIdx.x; i < n; i += JT) {
+                            double x = vp[i], y = vq[i];
+                            vp[i] = cs * x - sn * y;
+                            vq[i] = sn * x + cs * y;
+                        }
                     }
                     ++mine;
                 }
@@ -468,6 +470,16 @@ void launch_block_jacobi(Ctx& c, int64_t m, int64_t n, double* U, int64_t ldu, d
     }
 }
 
+thread_local bool g_strict_svd = false;
+bool strict_svd_flag() { return g_strict_svd; }
+bool lazy_v_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("HYDOT_JACOBI_LAZYV");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 bool stats_on() {
     static int on = [] {
         const char* e = std::getenv("HYDOT_JACOBI_STATS");
@@ -477,6 +489,9 @@ bool stats_on() {
 }
 
 }  // namespace
+
+StrictSVD::StrictSVD() : prev_(g_strict_svd) { g_strict_svd = true; }
+StrictSVD::~StrictSVD() { g_strict_svd = prev_; }
 
 void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, double* Uo,
                 int64_t lduo, std::vector<double>& s, double* Vo, int64_t ldvo) {
@@ -507,6 +522,7 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
     const double atol = (at_env ? std::atof(at_env) : 0.0) * *std::max_element(cnh.begin(), cnh.end());
     DBuf sw(c, sizeof(int) * (kMaxSweeps + 1));
     HYDOT_CUDA(cudaMemsetAsync(sw.as<void>(), 0, sizeof(int) * (kMaxSweeps + 1), c.stream));
+    bool lazy_v = false;
     const size_t smem = size_t((m + n) * n) * sizeof(double);
     if (n >= 2 && smem <= 200 * 1024) {
         static bool attr = false;
@@ -538,7 +554,8 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
             int64_t mm = m;
             int nn = int(n), npp = np;
             double* up = U.d();
-            double* vp = V.d();
+            lazy_v = !warp_mode && !strict_svd_flag() && lazy_v_enabled();
+            double* vp = lazy_v ? nullptr : V.d();
             int64_t ldu = m, ldv = n;
             double tl = tol, at = atol;
             int* cnt = sw.as<int>();
@@ -563,6 +580,25 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
     c.check_launch();
     std::vector<double> sv(static_cast<size_t>(n));
     c.d2h(sv.data(), sd.d(), size_t(n));
+    if (lazy_v) {
+        // right vectors from X = U S V^T:  V = X^T W S^-2 with W = U S the
+        // rotated columns (one DMMA GEMM instead of rotating V every round);
+        // column j carries an error eps ||X|| / s_j, i.e. backward-stable
+        // for every kept triple (s_j > eps_tol s_1 >> eps s_1); columns
+        // with s_j below 1e-14 s_1 are set to zero (never kept).
+        dgemm(c, true, false, n, n, m, 1.0, X, ldx, U.d(), m, 0.0, V.d(), n);
+        const double smax = *std::max_element(sv.begin(), sv.end());
+        std::vector<double> inv(static_cast<size_t>(n));
+        for (int64_t j = 0; j < n; ++j) {
+            const double sj = sv[size_t(j)];
+            inv[size_t(j)] = (sj > 1e-14 * smax && sj > 0.0) ? 1.0 / (sj * sj) : 0.0;
+        }
+        DBuf dinv = dalloc(c, size_t(n));
+        HYDOT_CUDA(cudaMemcpyAsync(dinv.d(), inv.data(), size_t(n) * 8, cudaMemcpyHostToDevice,
+                                   c.stream));
+        scale_cols(c, n, n, V.d(), n, dinv.d());
+        c.sync();
+    }
     std::vector<int> perm(static_cast<size_t>(n));
     std::iota(perm.begin(), perm.end(), 0);
     std::stable_sort(perm.begin(), perm.end(),
