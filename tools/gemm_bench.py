@@ -19,6 +19,10 @@ shapes = [
     ("matvec VtX TN 2131x256x110592", True, False, 2131, 256, 110592, 0.0),
     ("matvec UZ NN 4800x256x2131", False, False, 4800, 256, 2131, 0.0),
 ]
+sel = os.environ.get("GEMM_SHAPES")
+if sel:
+    shapes = [shapes[int(i)] for i in sel.split(",")]
+reps = int(os.environ.get("GEMM_REPS", "10"))
 for name, ta, tb, m, n, k, beta in shapes:
     A = torch.randn((m * k,), dtype=torch.float64, device="cuda")
     B = torch.randn((k * n,), dtype=torch.float64, device="cuda")
@@ -28,7 +32,6 @@ for name, ta, tb, m, n, k, beta in shapes:
     for _ in range(3):
         h.dgemm(ctx, ta, tb, m, n, k, 1.0, A, lda, B, ldb, beta, C, m)
     torch.cuda.synchronize()
-    reps = 10
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
@@ -36,4 +39,4 @@ for name, ta, tb, m, n, k, beta in shapes:
     e1.record()
     torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / reps / 1e3
-    print(json.dumps({"shape": name, "ms": t * 1e3, "tflops": 2.0 * m * n * k / t / 1e12}), flush=True)
+    print(json.dumps({"shape": name, "tile": os.environ.get("HYDOT_GEMM_TILE", "auto"), "ms": t * 1e3, "tflops": 2.0 * m * n * k / t / 1e12}), flush=True)
