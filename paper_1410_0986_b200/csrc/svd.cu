@@ -8,9 +8,12 @@
 // accuracy (no Gram matrix is formed).  Two drivers:
 //   * small: (m + n) n doubles fit in shared memory -- one CTA runs every
 //     sweep on-chip, one warp per column pair;
-//   * large: one cooperative persistent kernel runs all sweeps, one warp per
-//     column pair, a grid-wide barrier between rounds and a per-sweep
-//     rotation counter for convergence (no host round trips).
+//   * large: one cooperative persistent kernel runs all sweeps, one CTA per
+//     column pair (the pair held in registers when V is recovered lazily),
+//     a grid-wide barrier between rounds and a per-sweep rotation counter
+//     for convergence (no host round trips).  A dataflow variant with
+//     per-column completion flags instead of round barriers measured 1.75x
+//     slower (a release fence per pair serialises each CTA).
 // Afterwards sigma_j = ||u_j||, U = u_j / sigma_j, sorted descending.
 #include <cooperative_groups.h>
 
@@ -236,6 +239,86 @@ __global__ void __launch_bounds__(JT) jacobi_coop_k(int64_t m, int n, int np,
                     ++mine;
                 }
                 __syncthreads();
+            }
+            grid.sync();
+        }
+        if (threadIdx.x == 0 && mine) atomicAdd(&counters[sweep], mine);
+        grid.sync();
+        if (*((volatile int*)&counters[sweep]) == 0) break;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
+}
+
+// CTA-per-pair variant with the column pair held in registers (m <= EPT*JT):
+// one read and (when rotated) one write of each column per round instead
+// of read / re-read / write; every thread derives the rotation from the
+// shared partial sums (no second block barrier).  V is never rotated here
+// (lazy V only).
+template <int EPT>
+__global__ void __launch_bounds__(JT, EPT <= 4 ? 4 : (EPT <= 8 ? 3 : 2)) jacobi_coop_reg_k(int64_t m, int n, int np,
+                                                        const int2* __restrict__ pairs,
+                                                        double* __restrict__ U, int64_t ldu,
+                                                        double tol, int* __restrict__ counters,
+                                                        int* __restrict__ sweeps_out) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double red[2][3][JT / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int rounds = np - 1, per = np / 2;
+    int sweep = 0, parity = 0;
+    for (; sweep < kMaxSweeps; ++sweep) {
+        int mine = 0;
+        for (int r = 0; r < rounds; ++r) {
+            for (int q = blockIdx.x; q < per; q += gridDim.x) {
+                int2 pr = pairs[r * per + q];
+                if (pr.x >= n || pr.y >= n) continue;
+                double* up = U + int64_t(pr.x) * ldu;
+                double* uq = U + int64_t(pr.y) * ldu;
+                double x[EPT], y[EPT];
+                double a = 0, b = 0, g = 0;
+#pragma unroll
+                for (int e = 0; e < EPT; ++e) {
+                    const int64_t i = threadIdx.x + int64_t(e) * JT;
+                    x[e] = i < m ? up[i] : 0.0;
+                    y[e] = i < m ? uq[i] : 0.0;
+                }
+#pragma unroll
+                for (int e = 0; e < EPT; ++e) {
+                    a += x[e] * x[e];
+                    b += y[e] * y[e];
+                    g += x[e] * y[e];
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    a += __shfl_xor_sync(0xffffffffu, a, o);
+                    b += __shfl_xor_sync(0xffffffffu, b, o);
+                    g += __shfl_xor_sync(0xffffffffu, g, o);
+                }
+                if (lane == 0) {
+                    red[parity][0][w] = a;
+                    red[parity][1][w] = b;
+                    red[parity][2][w] = g;
+                }
+                __syncthreads();
+                double A = 0, B = 0, Gm = 0;
+#pragma unroll
+                for (int k = 0; k < JT / 32; ++k) {
+                    A += red[parity][0][k];
+                    B += red[parity][1][k];
+                    Gm += red[parity][2][k];
+                }
+                parity ^= 1;  // the next pair writes the other buffer: no trailing barrier
+                if (Gm != 0.0 && fabs(Gm) > tol * sqrt(A * B)) {
+                    double cs, sn;
+                    rot_params(A, B, Gm, cs, sn);
+#pragma unroll
+                    for (int e = 0; e < EPT; ++e) {
+                        const int64_t i = threadIdx.x + int64_t(e) * JT;
+                        if (i < m) {
+                            up[i] = cs * x[e] - sn * y[e];
+                            uq[i] = sn * x[e] + cs * y[e];
+                        }
+                    }
+                    ++mine;
+                }
             }
             grid.sync();
         }
@@ -545,8 +628,19 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
             // warp-per-pair measured slower on the config-1 cores (1.95 s vs
             // 1.44 s total): kept for experiments via HYDOT_JACOBI_WARP=1
             static const bool warp_env = std::getenv("HYDOT_JACOBI_WARP") != nullptr;
+            static const bool reg_env = [] {
+                const char* e = std::getenv("HYDOT_JACOBI_REG");
+                return !(e && e[0] == '0');
+            }();
             const bool warp_mode = warp_env && m <= 640;
+            lazy_v = !warp_mode && !strict_svd_flag() && lazy_v_enabled();
+            const bool reg_mode = lazy_v && atol == 0.0 && reg_env && m <= 16 * JT;
             void* kern = warp_mode ? (void*)jacobi_coop_warp_k : (void*)jacobi_coop_k;
+            if (reg_mode) {
+                kern = m <= 4 * JT   ? (void*)jacobi_coop_reg_k<4>
+                       : m <= 8 * JT ? (void*)jacobi_coop_reg_k<8>
+                                     : (void*)jacobi_coop_reg_k<16>;
+            }
             HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, JT, 0));
             const int per = np / 2;
             int want = warp_mode ? (per + JT / 32 - 1) / (JT / 32) : per;
@@ -554,7 +648,6 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
             int64_t mm = m;
             int nn = int(n), npp = np;
             double* up = U.d();
-            lazy_v = !warp_mode && !strict_svd_flag() && lazy_v_enabled();
             double* vp = lazy_v ? nullptr : V.d();
             int64_t ldu = m, ldv = n;
             double tl = tol, at = atol;
@@ -562,7 +655,9 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
             int* so = sw.as<int>() + kMaxSweeps;
             const int2* pp = dpairs;
             void* args[] = {&mm, &nn, &npp, &pp, &up, &ldu, &vp, &ldv, &tl, &at, &cnt, &so};
-            HYDOT_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(JT), args, 0, c.stream));
+            void* rargs[] = {&mm, &nn, &npp, &pp, &up, &ldu, &tl, &cnt, &so};
+            HYDOT_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(JT), reg_mode ? rargs : args,
+                                                   0, c.stream));
             c.count();
         }
     }
