@@ -268,6 +268,104 @@ hydot_status hydot_dgemm(hydot_ctx ctx, int transa, int transb, int64_t m, int64
                          double alpha, const double* A_dev, int64_t lda, const double* B_dev,
                          int64_t ldb, double beta, double* C_dev, int64_t ldc);
 
+/* ---------------------------------------------------------------- pals -- */
+/* Parametric level-set reconstruction, the caller of the compressed
+ * operator: proj/include/hydot/pals.hpp, src/pals.cpp.
+ * N- and M-length arrays are device pointers; parameters, spectra and
+ * concentrations are host arrays. */
+
+/* grid::build_grid (grid.cpp:94-110): vertices on [-Lx,Lx]x[-Ly,Ly]x[0,Lz],
+ * x-fastest, h = 2L/(n-1) laterally and Lz/(nz-1) vertically. */
+typedef struct hydot_grid_geom {
+    int nx, ny, nz;
+    double Lx, Ly, Lz;
+} hydot_grid_geom;
+
+/* PaLSParams (pals.hpp:16-32): n_p RBF weights, widths, centres. */
+typedef struct hydot_pals_params {
+    int np;
+    double* alpha;    /* n_p */
+    double* beta;     /* n_p, > 0 */
+    double* centers;  /* n_p x 3, column-major */
+    double tau_level, eps_H, nu_norm;
+} hydot_pals_params;
+
+/* The measurement operator handed to the loop (the reference's Hmv,
+ * experiments.cpp:255-262): y[row_perm[i]] = (U V^T x)[i]. */
+typedef struct hydot_hop {
+    hydot_factor H;
+    const int* row_perm_dev; /* M ints; NULL = identity order */
+} hydot_hop;
+
+enum { HYDOT_PALS_LEVEL_SET = 0, HYDOT_PALS_SHAPE = 1, HYDOT_PALS_JACOBIAN = 2 };
+
+/* level_set / shape / shape_jacobian (pals.cpp:74-119): which selects phi
+ * (N), mu = H_eps(phi - tau) (N) or dmu/dp (N x 5 n_p, columns
+ * [d/dalpha | d/dbeta | d/dcx | d/dcy | d/dcz], ld ldo). */
+hydot_status hydot_pals_eval(hydot_ctx ctx, int which, const hydot_grid_geom* geom,
+                             const hydot_pals_params* p, double* out_dev, int64_t ldo);
+
+/* Hmv on b columns: Y (M x b) = P U V^T X, X N x b. */
+hydot_status hydot_pals_hmv(hydot_ctx ctx, const hydot_hop* op, int b, const double* X_dev,
+                            int64_t ldx, double* Y_dev, int64_t ldy);
+
+/* solve_concentrations (pals.cpp:139-156): c = (W D(p))^+ (W y), D columns
+ * E_i H mu; ext_h n_lambda x n_species (extinction at the setup
+ * wavelengths, column-major); flagged = rank-deficient system. */
+hydot_status hydot_pals_solve_concentrations(hydot_ctx ctx, const hydot_hop* op, const double* mu_dev,
+                                             const double* w_dev, const double* y_dev,
+                                             const double* ext_h, int n_lambda, int n_species,
+                                             double* c_h, int* flagged_h);
+
+/* lm_step (pals.cpp:158-169): dp minimising ||[J; sqrt(nu) I] dp + [eps; 0]||
+ * (J M x n on the device, dp n on the host). */
+hydot_status hydot_pals_lm_step(hydot_ctx ctx, int64_t M, int n, const double* J_dev, int64_t ldj,
+                                const double* eps_dev, double nu, double* dp_h);
+
+/* metrics (pals.cpp:307-329). */
+hydot_status hydot_pals_metrics(hydot_ctx ctx, int64_t n, const double* mu_true_dev,
+                                const double* mu_hat_dev, double threshold, double* l2_rel_h,
+                                double* dice_h, int* flagged_h);
+
+/* ReconConfig (pals.hpp:67-75). */
+typedef struct hydot_recon_config {
+    int max_outer, max_inner, max_retries;
+    double gamma, nu0, stagnation_tol;
+    const double* fixed_c_h; /* n_species, or NULL to solve for c */
+} hydot_recon_config;
+
+/* TraceRow (pals.hpp:77-84). */
+typedef struct hydot_trace_row {
+    int outer, inner;
+    double resnorm, nu;
+    int accepted;
+    double dice;
+} hydot_trace_row;
+
+/* ReconResult (pals.hpp:86-93); arrays are caller-allocated: p.alpha /
+ * p.beta (n_p), p.centers (3 n_p), c_h (n_species), trace_h (trace_cap).
+ * trace_len is the full trace length (rows beyond trace_cap dropped);
+ * hmv_calls / hmv_columns count the operator products issued. */
+typedef struct hydot_recon_result {
+    hydot_pals_params p;
+    double* c_h;
+    hydot_trace_row* trace_h;
+    int trace_cap, trace_len;
+    double resnorm;
+    int converged, flagged;
+    int64_t hmv_calls, hmv_columns;
+} hydot_recon_result;
+
+/* reconstruct (pals.cpp:193-295): alternating concentration / shape
+ * reconstruction with Levenberg-Marquardt shape updates on the device;
+ * mu_truth_dev (N) optional, for the dice column of the trace. */
+hydot_status hydot_pals_reconstruct(hydot_ctx ctx, const hydot_hop* op, const hydot_grid_geom* geom,
+                                    const double* ext_h, int n_lambda, int n_species,
+                                    const double* y_dev, const double* w_dev,
+                                    const hydot_pals_params* init, double noise_norm,
+                                    const hydot_recon_config* cfg, const double* mu_truth_dev,
+                                    hydot_recon_result* out);
+
 #ifdef __cplusplus
 }
 #endif

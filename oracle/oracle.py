@@ -339,3 +339,129 @@ def fast_thin_svd(A):
     V = np.empty((n, k), order="F")
     _check(lib().oracle_fast_thin_svd(_d(A), m, n, _d(U), _d(s), _d(V)))
     return U, s, V
+
+
+# --------------------------------------------------------------- PaLS -----
+# Restatement of proj/src/pals.cpp (pals_oracle.cpp).  `geom` is
+# (nx, ny, nz, Lx, Ly, Lz) as grid::build_grid; `p` any object with
+# alpha, beta (n_p), centers (n_p x 3), tau_level, eps_H, nu_norm.
+_pals_ready = False
+
+
+def _pals_lib():
+    global _pals_ready
+    L = lib()
+    if not _pals_ready:
+        L.oracle_pals_last_error.restype = C.c_char_p
+        L.oracle_pals_scalar.argtypes = [C.c_int, C.c_double, C.c_double, _dp]
+        L.oracle_pals_eval.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                       C.c_double, C.c_int, _dp, _dp, _dp, C.c_double, C.c_double,
+                                       C.c_double, _dp]
+        L.oracle_pals_solve_concentrations.argtypes = [_dp, _dp, C.c_int64, C.c_int64, C.c_int64,
+                                                       _ip, _dp, _dp, _dp, _dp, C.c_int, C.c_int,
+                                                       _dp, _ip]
+        L.oracle_pals_lm_step.argtypes = [_dp, C.c_int64, C.c_int, _dp, C.c_double, _dp]
+        L.oracle_pals_metrics.argtypes = [C.c_int64, _dp, _dp, C.c_double, _dp, _dp, _ip]
+        L.oracle_pals_reconstruct.argtypes = (
+            [_dp, _dp, C.c_int64, C.c_int64, C.c_int64, _ip, C.c_int, C.c_int, C.c_int, C.c_double,
+             C.c_double, C.c_double, _dp, C.c_int, C.c_int, _dp, _dp, C.c_int, _dp, _dp, _dp,
+             C.c_double, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
+             C.c_double, C.c_double, C.c_double, _dp, _dp, _dp, _dp, _dp, _dp, _dp, C.c_int, _dp])
+        _pals_ready = True
+    return L
+
+
+def _pcheck(rc):
+    if rc != 0:
+        msg = _pals_lib().oracle_pals_last_error().decode()
+        raise (ValueError if rc == 1 else RuntimeError)(msg)
+
+
+def pals_scalar(name, t, eps=1.0):
+    which = {"wendland": 0, "wendland_deriv": 1, "smooth_heaviside": 2, "smooth_delta": 3}[name]
+    out = C.c_double()
+    _pcheck(_pals_lib().oracle_pals_scalar(which, float(t), float(eps), C.byref(out)))
+    return out.value
+
+
+def _pargs(p):
+    a = _f64(p.alpha)
+    b = _f64(p.beta)
+    c = np.asfortranarray(p.centers, dtype=np.float64)
+    return a, b, c
+
+
+def pals_eval(which, geom, p):
+    """which: 'level_set' | 'shape' | 'shape_jacobian' (N x 5 n_p, F-order)."""
+    nx, ny, nz, Lx, Ly, Lz = geom
+    N = nx * ny * nz
+    a, b, c = _pargs(p)
+    k = {"level_set": 0, "shape": 1, "shape_jacobian": 2}[which]
+    out = np.zeros((N, 5 * len(a)) if k == 2 else N, order="F")
+    _pcheck(_pals_lib().oracle_pals_eval(k, nx, ny, nz, Lx, Ly, Lz, len(a), _d(a), _d(b), _d(c),
+                                         p.tau_level, p.eps_H, p.nu_norm, _d(out)))
+    return out
+
+
+def _hop_args(U, V, perm):
+    U = np.asfortranarray(U, dtype=np.float64)
+    V = np.asfortranarray(V, dtype=np.float64)
+    pp = None if perm is None else np.ascontiguousarray(perm, dtype=np.int32)
+    return U, V, pp
+
+
+def pals_solve_concentrations(U, V, perm, mu, w, y, ext):
+    """ext: n_lambda x n_species extinction at the setup wavelengths."""
+    U, V, pp = _hop_args(U, V, perm)
+    ext = np.asfortranarray(ext, dtype=np.float64)
+    nl, nsp = ext.shape
+    c = np.zeros(nsp)
+    fl = C.c_int()
+    _pcheck(_pals_lib().oracle_pals_solve_concentrations(
+        _d(U), _d(V), U.shape[0], V.shape[0], U.shape[1],
+        None if pp is None else pp.ctypes.data_as(_ip), _d(_f64(mu)), _d(_f64(w)), _d(_f64(y)),
+        _d(ext), nl, nsp, _d(c), C.byref(fl)))
+    return c, bool(fl.value)
+
+
+def pals_lm_step(J, eps, nu):
+    J = np.asfortranarray(J, dtype=np.float64)
+    dp = np.zeros(J.shape[1])
+    _pcheck(_pals_lib().oracle_pals_lm_step(_d(J), J.shape[0], J.shape[1], _d(_f64(eps)), nu,
+                                            _d(dp)))
+    return dp
+
+
+def pals_metrics(a, b, threshold=0.5):
+    l2, dice, fl = C.c_double(), C.c_double(), C.c_int()
+    a, b = _f64(a), _f64(b)
+    _pcheck(_pals_lib().oracle_pals_metrics(len(a), _d(a), _d(b), threshold, C.byref(l2),
+                                            C.byref(dice), C.byref(fl)))
+    return l2.value, dice.value, bool(fl.value)
+
+
+def pals_reconstruct(U, V, perm, geom, ext, y, w, init, noise_norm, max_outer=30, max_inner=5,
+                     max_retries=8, gamma=1.2, nu0=1.0, stagnation_tol=1e-6, fixed_c=None,
+                     mu_truth=None, trace_cap=4096):
+    """Returns dict(alpha, beta, centers, c, trace (rows x 6), resnorm, converged, flagged)."""
+    U, V, pp = _hop_args(U, V, perm)
+    nx, ny, nz, Lx, Ly, Lz = geom
+    ext = np.asfortranarray(ext, dtype=np.float64)
+    nl, nsp = ext.shape
+    a, b, c = _pargs(init)
+    n = len(a)
+    ao, bo, co = np.zeros(n), np.zeros(n), np.zeros((n, 3), order="F")
+    cc = np.zeros(nsp)
+    tr = np.zeros((trace_cap, 6))
+    sc = np.zeros(4)
+    fc = None if fixed_c is None else _d(_f64(fixed_c))
+    mt = None if mu_truth is None else _d(_f64(mu_truth))
+    _pcheck(_pals_lib().oracle_pals_reconstruct(
+        _d(U), _d(V), U.shape[0], V.shape[0], U.shape[1],
+        None if pp is None else pp.ctypes.data_as(_ip), nx, ny, nz, Lx, Ly, Lz, _d(ext), nl, nsp,
+        _d(_f64(y)), _d(_f64(w)), n, _d(a), _d(b), _d(c), init.tau_level, init.eps_H,
+        init.nu_norm, noise_norm, max_outer, max_inner, max_retries, gamma, nu0, stagnation_tol,
+        fc, mt, _d(ao), _d(bo), _d(co), _d(cc), _d(tr), trace_cap, _d(sc)))
+    ln = int(sc[3])
+    return dict(alpha=ao, beta=bo, centers=co, c=cc, trace=tr[:min(ln, trace_cap)].copy(),
+                resnorm=sc[0], converged=bool(sc[1]), flagged=bool(sc[2]))

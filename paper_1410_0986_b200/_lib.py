@@ -52,6 +52,38 @@ class RecOpts(C.Structure):
                 ("node_offset", C.c_int)]
 
 
+class GridGeom(C.Structure):
+    _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int), ("Lx", C.c_double),
+                ("Ly", C.c_double), ("Lz", C.c_double)]
+
+
+class PalsParams(C.Structure):
+    _fields_ = [("np", C.c_int), ("alpha", _dp), ("beta", _dp), ("centers", _dp),
+                ("tau_level", C.c_double), ("eps_H", C.c_double), ("nu_norm", C.c_double)]
+
+
+class Hop(C.Structure):
+    _fields_ = [("H", _vp), ("row_perm_dev", _ip)]
+
+
+class ReconConfig(C.Structure):
+    _fields_ = [("max_outer", C.c_int), ("max_inner", C.c_int), ("max_retries", C.c_int),
+                ("gamma", C.c_double), ("nu0", C.c_double), ("stagnation_tol", C.c_double),
+                ("fixed_c_h", _dp)]
+
+
+class TraceRowC(C.Structure):
+    _fields_ = [("outer", C.c_int), ("inner", C.c_int), ("resnorm", C.c_double),
+                ("nu", C.c_double), ("accepted", C.c_int), ("dice", C.c_double)]
+
+
+class ReconResultC(C.Structure):
+    _fields_ = [("p", PalsParams), ("c_h", _dp), ("trace_h", C.POINTER(TraceRowC)),
+                ("trace_cap", C.c_int), ("trace_len", C.c_int), ("resnorm", C.c_double),
+                ("converged", C.c_int), ("flagged", C.c_int), ("hmv_calls", C.c_int64),
+                ("hmv_columns", C.c_int64)]
+
+
 # name -> (restype, argtypes); exactly the declarations of include/hydot_b200.h
 SIGNATURES = {
     "hydot_version": (C.c_int, []),
@@ -105,6 +137,17 @@ SIGNATURES = {
     "hydot_householder_qr": (C.c_int, [_vp, C.c_int64, C.c_int64, _dp, C.c_int64, _dp, _dp]),
     "hydot_dgemm": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_double,
                               _dp, C.c_int64, _dp, C.c_int64, C.c_double, _dp, C.c_int64]),
+    "hydot_pals_eval": (C.c_int, [_vp, C.c_int, C.POINTER(GridGeom), C.POINTER(PalsParams), _dp,
+                                  C.c_int64]),
+    "hydot_pals_hmv": (C.c_int, [_vp, C.POINTER(Hop), C.c_int, _dp, C.c_int64, _dp, C.c_int64]),
+    "hydot_pals_solve_concentrations": (C.c_int, [_vp, C.POINTER(Hop), _dp, _dp, _dp, _dp, C.c_int,
+                                                  C.c_int, _dp, _ip]),
+    "hydot_pals_lm_step": (C.c_int, [_vp, C.c_int64, C.c_int, _dp, C.c_int64, _dp, C.c_double,
+                                     _dp]),
+    "hydot_pals_metrics": (C.c_int, [_vp, C.c_int64, _dp, _dp, C.c_double, _dp, _dp, _ip]),
+    "hydot_pals_reconstruct": (C.c_int, [_vp, C.POINTER(Hop), C.POINTER(GridGeom), _dp, C.c_int,
+                                         C.c_int, _dp, _dp, C.POINTER(PalsParams), C.c_double,
+                                         C.POINTER(ReconConfig), _dp, C.POINTER(ReconResultC)]),
 }
 
 _LIB = None

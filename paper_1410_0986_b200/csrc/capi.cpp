@@ -5,6 +5,7 @@
 #include <mutex>
 
 #include "lowrank.h"
+#include "pals.h"
 
 using namespace hydot;
 
@@ -561,6 +562,124 @@ hydot_status hydot_dgemm(hydot_ctx ctx, int transa, int transb, int64_t m, int64
         if (m < 0 || n < 0 || k < 0 || ldc < m) throw std::invalid_argument("dgemm: bad dimensions");
         dgemm(c, transa != 0, transb != 0, m, n, k, alpha, A_dev, lda, B_dev, ldb, beta, C_dev, ldc);
         c.sync();
+    });
+}
+
+// ------------------------------------------------------------------ pals --
+namespace {
+hydot::pals::Hop hop_of(const hydot_hop* op) {
+    if (!op || !op->H) throw std::invalid_argument("PaLS: null operator");
+    hydot::pals::Hop h;
+    h.f = &op->H->f;
+    h.perm = op->row_perm_dev;
+    return h;
+}
+hydot::pals::Geom geom_of(const hydot_grid_geom* g) {
+    if (!g) throw std::invalid_argument("PaLS: null grid");
+    return hydot::pals::Geom::make(*g);
+}
+hydot::pals::Params params_of(const hydot_pals_params* p) {
+    if (!p) throw std::invalid_argument("PaLS: null parameters");
+    return hydot::pals::Params::from(*p);
+}
+}  // namespace
+
+hydot_status hydot_pals_eval(hydot_ctx ctx, int which, const hydot_grid_geom* geom,
+                             const hydot_pals_params* p, double* out_dev, int64_t ldo) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        hydot::pals::Geom g = geom_of(geom);
+        if (which < 0 || which > 2 || !out_dev || ldo < g.N()) throw std::invalid_argument("pals_eval: bad arguments");
+        hydot::pals::eval(c, which, g, params_of(p), out_dev, ldo);
+        c.sync();
+    });
+}
+
+hydot_status hydot_pals_hmv(hydot_ctx ctx, const hydot_hop* op, int b, const double* X_dev, int64_t ldx,
+                            double* Y_dev, int64_t ldy) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (b < 0) throw std::invalid_argument("Hmv: negative column count");
+        hydot::pals::hmv(c, hop_of(op), b, X_dev, ldx, Y_dev, ldy);
+        c.sync();
+    });
+}
+
+hydot_status hydot_pals_solve_concentrations(hydot_ctx ctx, const hydot_hop* op, const double* mu_dev,
+                                             const double* w_dev, const double* y_dev, const double* ext_h,
+                                             int n_lambda, int n_species, double* c_h, int* flagged_h) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!mu_dev || !w_dev || !y_dev || !ext_h || !c_h) throw std::invalid_argument("solve_concentrations: null argument");
+        hydot::pals::Conc r =
+            hydot::pals::solve_concentrations(c, hop_of(op), mu_dev, w_dev, y_dev, ext_h, n_lambda, n_species);
+        std::copy(r.c.begin(), r.c.end(), c_h);
+        if (flagged_h) *flagged_h = r.flagged ? 1 : 0;
+    });
+}
+
+hydot_status hydot_pals_lm_step(hydot_ctx ctx, int64_t M, int n, const double* J_dev, int64_t ldj,
+                                const double* eps_dev, double nu, double* dp_h) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (M < 0 || n < 0 || !dp_h) throw std::invalid_argument("lm_step: bad arguments");
+        std::vector<double> dp = hydot::pals::lm_step(c, M, n, J_dev, ldj, eps_dev, nu);
+        std::copy(dp.begin(), dp.end(), dp_h);
+    });
+}
+
+hydot_status hydot_pals_metrics(hydot_ctx ctx, int64_t n, const double* mu_true_dev, const double* mu_hat_dev,
+                                double threshold, double* l2_rel_h, double* dice_h, int* flagged_h) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (n < 0) throw std::invalid_argument("metrics: length mismatch");
+        hydot::pals::Metrics m = hydot::pals::metrics(c, n, mu_true_dev, mu_hat_dev, threshold);
+        if (l2_rel_h) *l2_rel_h = m.l2_rel;
+        if (dice_h) *dice_h = m.dice;
+        if (flagged_h) *flagged_h = m.flagged ? 1 : 0;
+    });
+}
+
+hydot_status hydot_pals_reconstruct(hydot_ctx ctx, const hydot_hop* op, const hydot_grid_geom* geom,
+                                    const double* ext_h, int n_lambda, int n_species, const double* y_dev,
+                                    const double* w_dev, const hydot_pals_params* init, double noise_norm,
+                                    const hydot_recon_config* cfg, const double* mu_truth_dev,
+                                    hydot_recon_result* out) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!ext_h || !y_dev || !w_dev || !cfg || !out || n_lambda < 1 || n_species < 0)
+            throw std::invalid_argument("reconstruct: bad arguments");
+        hydot::pals::Params p0 = params_of(init);
+        if (out->p.np != p0.np() || (p0.np() > 0 && (!out->p.alpha || !out->p.beta || !out->p.centers)) ||
+            (n_species > 0 && !out->c_h) || (out->trace_cap > 0 && !out->trace_h))
+            throw std::invalid_argument("reconstruct: result arrays");
+        hydot::pals::ReconCfg rc;
+        rc.max_outer = cfg->max_outer;
+        rc.max_inner = cfg->max_inner;
+        rc.max_retries = cfg->max_retries;
+        rc.gamma = cfg->gamma;
+        rc.nu0 = cfg->nu0;
+        rc.stagnation_tol = cfg->stagnation_tol;
+        if (cfg->fixed_c_h) rc.fixed_c.assign(cfg->fixed_c_h, cfg->fixed_c_h + n_species);
+        hydot::pals::Recon r = hydot::pals::reconstruct(c, hop_of(op), geom_of(geom), ext_h, n_lambda, n_species,
+                                                        y_dev, w_dev, p0, noise_norm, rc, mu_truth_dev);
+        std::copy(r.p.alpha.begin(), r.p.alpha.end(), out->p.alpha);
+        std::copy(r.p.beta.begin(), r.p.beta.end(), out->p.beta);
+        std::copy(r.p.centers.begin(), r.p.centers.end(), out->p.centers);
+        out->p.tau_level = r.p.tau_level;
+        out->p.eps_H = r.p.eps_H;
+        out->p.nu_norm = r.p.nu_norm;
+        std::copy(r.c.begin(), r.c.end(), out->c_h);
+        out->trace_len = int(r.trace.size());
+        for (int i = 0; i < std::min(out->trace_len, out->trace_cap); ++i) {
+            const auto& t = r.trace[size_t(i)];
+            out->trace_h[i] = hydot_trace_row{t.outer, t.inner, t.resnorm, t.nu, t.accepted ? 1 : 0, t.dice};
+        }
+        out->resnorm = r.resnorm;
+        out->converged = r.converged ? 1 : 0;
+        out->flagged = r.flagged ? 1 : 0;
+        out->hmv_calls = r.hmv_calls;
+        out->hmv_columns = r.hmv_columns;
     });
 }
 

@@ -505,7 +505,7 @@ void RngStream::ensure_normals(int64_t upto) {
 }
 
 const double* RngStream::take(int64_t count) {
-    StageTimer _t(c_, "rng");
+    StageTimer _t(c_, "rng", count, n_chunks_, int64_t(seed_ & 0xffff));
     ensure_normals(consumed_ + count);
     const double* p = normals_.d() + consumed_;
     consumed_ += count;

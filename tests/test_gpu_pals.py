@@ -1,0 +1,188 @@
+"""GPU parity of the device PaLS loop (csrc/pals.cu,
+csrc/pals_loop.cpp) against the CPU oracle restatement of
+proj/src/pals.cpp.  Tolerances: shape / level set 1e-13 relative, Jacobian
+1e-12 of the column norm (the kernels follow the reference expressions with
+explicit rounding; only sin/cos differ by ulps), operator products 1e-12,
+concentrations 1e-10, LM steps 1e-9 (the reference's own bound), full
+reconstruction: identical accept/reject trace and final state to 1e-8."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as orc
+
+import pals_fixture as pf
+
+pytestmark = pytest.mark.gpu
+
+GEOM = (7, 7, 6, 3.0, 3.0, 2.0)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_1410_0986_b200 as h
+    return h.Context(0)
+
+
+def _params(p):
+    from paper_1410_0986_b200 import pals
+    return pals.PaLSParams(p.alpha, p.beta, p.centers, p.tau_level, p.eps_H, p.nu_norm)
+
+
+def _geom(g):
+    from paper_1410_0986_b200 import pals
+    return pals.GridGeom(*g)
+
+
+def _hop(ctx, U, V, perm=None):
+    from paper_1410_0986_b200 import lowrank as lr, pals
+    f = lr.LowRankFactor.from_tensors(ctx, torch.as_tensor(np.ascontiguousarray(U)),
+                                      torch.as_tensor(np.ascontiguousarray(V)))
+    return pals.HOperator(ctx, f, perm), f
+
+
+def test_level_set_shape_jacobian_match_oracle(ctx):
+    from paper_1410_0986_b200 import pals
+    rng = np.random.default_rng(7)
+    for n_p in (1, 3, 16):
+        p = pf.random_params(rng, GEOM, n_p)
+        g, q = _geom(GEOM), _params(p)
+        for which, fn in (("level_set", pals.level_set), ("shape", pals.shape)):
+            want = orc.pals_eval(which, GEOM, p)
+            got = fn(ctx, q, g).cpu().numpy()
+            np.testing.assert_allclose(got, want, rtol=1e-13, atol=1e-15 * max(1.0, np.abs(want).max()))
+        want = orc.pals_eval("shape_jacobian", GEOM, p)
+        got = pals.shape_jacobian(ctx, q, g).cpu().numpy()
+        assert got.shape == want.shape == (7 * 7 * 6, 5 * n_p)
+        for j in range(want.shape[1]):
+            assert np.linalg.norm(got[:, j] - want[:, j]) <= 1e-12 * max(np.linalg.norm(want[:, j]), 1e-300)
+
+
+def test_hmv_with_row_permutation(ctx):
+    rng = np.random.default_rng(8)
+    M, N, R = 37, 210, 9
+    U, V = rng.standard_normal((M, R)), rng.standard_normal((N, R))
+    perm = rng.permutation(M).astype(np.int32)
+    H, _ = _hop(ctx, U, V, perm)
+    for b in (1, 5, 80):
+        X = rng.standard_normal((N, b))
+        T = U @ (V.T @ X)
+        want = np.empty_like(T)
+        want[perm] = T
+        got = H(torch.as_tensor(X).cuda()).cpu().numpy()
+        np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12 * np.abs(want).max())
+
+
+def test_solve_concentrations_matches_oracle(ctx):
+    from paper_1410_0986_b200 import pals
+    geom = (6, 6, 5, 3.0, 3.0, 2.0)
+    N, nl = 180, 9
+    M = 3 * nl
+    ext = np.abs(orc.gaussian(11, nl * 4).reshape(4, nl).T) + 0.1
+    H = orc.gaussian(5, M * N).reshape(N, M).T
+    p = pf.random_params(np.random.default_rng(5), geom, 2)
+    mu = orc.pals_eval("shape", geom, p)
+    c_true = np.array([8.0, 8.0, 0.1, -0.1])
+    y = (ext @ c_true)[np.arange(M) % nl] * (H @ mu)
+    w = np.ones(M)
+    op, _ = _hop(ctx, np.eye(M), H.T)  # dense H as the factor I (H^T)^T
+    r = pals.solve_concentrations(ctx, op, mu, w, y, ext)
+    c_o, fl_o = orc.pals_solve_concentrations(np.eye(M), H.T, None, mu, w, y, ext)
+    assert r.flagged == fl_o is False
+    np.testing.assert_allclose(r.c, c_o, rtol=1e-10)
+    np.testing.assert_allclose(r.c, c_true, rtol=1e-8)
+    bad = pals.solve_concentrations(ctx, op, np.zeros(N), w, y, ext)
+    assert bad.flagged and all(v == 0 for v in bad.c)
+
+
+def test_lm_step_matches_oracle_and_normal_equations(ctx):
+    from paper_1410_0986_b200 import pals
+    rng = np.random.default_rng(9)
+    for M, n in ((30, 8), (500, 80), (2000, 5)):
+        J, r = rng.standard_normal((M, n)), rng.standard_normal(M)
+        for nu in (1e-6, 1.0, 50.0):
+            dp = pals.lm_step(ctx, J, r, nu)
+            want = np.linalg.solve(J.T @ J + nu * np.eye(n), -J.T @ r)
+            assert np.linalg.norm(dp - want) <= 1e-9 * np.linalg.norm(want)
+            dpo = orc.pals_lm_step(J, r, nu)
+            assert np.linalg.norm(dp - dpo) <= 1e-9 * np.linalg.norm(dpo)
+    with pytest.raises(Exception):
+        pals.lm_step(ctx, J, r, -1.0)
+
+
+def test_metrics_match_oracle(ctx):
+    from paper_1410_0986_b200 import pals
+    rng = np.random.default_rng(10)
+    for a, b in ((np.array([1, 1, 0, 0, 1, 0.0]), np.array([1, 0, 0, 0, 1, 1.0])),
+                 (rng.uniform(size=5000), rng.uniform(size=5000)),
+                 (np.zeros(6), np.zeros(6))):
+        m = pals.metrics(ctx, a, b)
+        l2, dice, fl = orc.pals_metrics(a, b)
+        assert m.dice == pytest.approx(dice, rel=1e-14) and m.flagged == fl
+        assert m.l2_rel == pytest.approx(l2, rel=1e-12, abs=1e-15)
+
+
+def _compare_recon(r, o):
+    assert r.converged == o["converged"] and r.flagged == o["flagged"]
+    tr = np.array([[t.outer, t.inner, t.resnorm, t.nu, t.accepted, t.dice] for t in r.trace])
+    assert tr.shape == o["trace"].shape
+    np.testing.assert_array_equal(tr[:, [0, 1, 4]], o["trace"][:, [0, 1, 4]])
+    np.testing.assert_allclose(tr[:, 3], o["trace"][:, 3], rtol=1e-12)
+    np.testing.assert_allclose(tr[:, 2], o["trace"][:, 2], rtol=1e-8)
+    np.testing.assert_allclose(tr[:, 5], o["trace"][:, 5], rtol=1e-12)
+    assert r.resnorm == pytest.approx(o["resnorm"], rel=1e-8)
+    np.testing.assert_allclose(r.c, o["c"], rtol=1e-8, atol=1e-12)
+    v_o = np.concatenate([o["alpha"], o["beta"], o["centers"][:, 0], o["centers"][:, 1],
+                          o["centers"][:, 2]])
+    np.testing.assert_allclose(r.p.to_vector(), v_o, rtol=1e-8, atol=1e-10)
+
+
+def test_reconstruct_matches_oracle_dense_operator(ctx):
+    from paper_1410_0986_b200 import pals
+    P = pf.recon_problem(9)
+    M = P["H"].shape[0]
+    op, _ = _hop(ctx, np.eye(M), P["H"].T)
+    cfg = pals.ReconConfig(max_outer=25)
+    r = pals.reconstruct(ctx, P["y"], op, _geom(P["geom"]), P["ext"], _params(P["init"]), P["w"],
+                         P["noise_norm"], cfg, mu_truth=P["mu_true"])
+    o = orc.pals_reconstruct(np.eye(M), P["H"].T, None, P["geom"], P["ext"], P["y"], P["w"],
+                             P["init"], P["noise_norm"], max_outer=25, mu_truth=P["mu_true"])
+    assert r.converged and r.resnorm <= 1.2 * P["noise_norm"] * (1 + 1e-9)
+    _compare_recon(r, o)
+    assert r.hmv_calls > 0 and r.hmv_columns >= r.hmv_calls
+    m = pals.metrics(ctx, P["mu_true"], pals.shape(ctx, r.p, _geom(P["geom"])))
+    assert m.dice >= 0.6
+
+
+def test_reconstruct_compressed_permuted_operator(ctx):
+    """The loop over a low-rank factor with a row permutation (the shape the
+    compress path hands to PaLS), fixed concentrations, vs the oracle."""
+    from paper_1410_0986_b200 import pals
+    P = pf.recon_problem(9)
+    H = P["H"]
+    Uh, s, Vt = np.linalg.svd(H, full_matrices=False)
+    k = int((s > 1e-9 * s[0]).sum())
+    U, V = Uh[:, :k], (Vt[:k].T * s[:k])
+    perm = np.random.default_rng(12).permutation(H.shape[0]).astype(np.int32)
+    Up = np.empty_like(U)
+    Up[np.arange(len(perm))] = U[perm]  # factor row i is H row perm[i]
+    op, _ = _hop(ctx, Up, V, perm)
+    cfg = pals.ReconConfig(max_outer=6, fixed_c=list(P["c_true"]))
+    r = pals.reconstruct(ctx, P["y"], op, _geom(P["geom"]), P["ext"], _params(P["init"]), P["w"],
+                         P["noise_norm"], cfg)
+    o = orc.pals_reconstruct(Up, V, perm, P["geom"], P["ext"], P["y"], P["w"], P["init"],
+                             P["noise_norm"], max_outer=6, fixed_c=P["c_true"])
+    _compare_recon(r, o)
+
+
+def test_reconstruct_argument_errors(ctx):
+    from paper_1410_0986_b200 import pals
+    P = pf.recon_problem(9)
+    M = P["H"].shape[0]
+    op, _ = _hop(ctx, np.eye(M), P["H"].T)
+    with pytest.raises(ValueError):
+        pals.reconstruct(ctx, P["y"], op, _geom(P["geom"]), P["ext"], _params(P["init"]), P["w"],
+                         P["noise_norm"], pals.ReconConfig(gamma=1.0))
+    with pytest.raises(Exception):  # grid / operator mismatch
+        pals.reconstruct(ctx, P["y"], op, pals.GridGeom(8, 8, 8, 7.0, 7.0, 14.0), P["ext"],
+                         _params(P["init"]), P["w"], P["noise_norm"])
