@@ -10,6 +10,7 @@ room for the factors.  Synthetic seeded inputs (configs.py); the fields
 (4.95 GB) are larger than L2, so no flush is needed between steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+  python bench.py --config 4 --steps 20   # PaLS loop on the compressed cfg2 operator
 
 --impl reference times the CPU oracle restatement of the reference
 (oracle/, "port": the reference itself needs Eigen and cannot be built here)
@@ -436,6 +437,150 @@ def cpu_sample(st, tree, eps, Fh, threads: int, leaves: int = 1):
             "seconds": dt}
 
 
+# ------------------------------------------------------------- config 4 --
+def run_pals(args):
+    """BASELINE config 4: the PaLS reconstruction loop (pals.cpp:193-295, run
+    on the device) over config 2's compressed operator.  Setup (untimed):
+    config-2 fields + compress_H on this GPU.  Timed: `--steps` Gauss-Newton
+    steps of reconstruct (max_inner = 1: one LM step with its retries per
+    outer iteration, after the concentration solve), plus the BASELINE's
+    literal blocks of 64 J~x and 64 J~^T y products per step."""
+    import torch
+    import paper_1410_0986_b200 as h
+    from paper_1410_0986_b200 import born, configs, lowrank as lr, pals
+    from paper_1410_0986_b200.parallel import GpuEngine, make_plan
+
+    rank, world, local = dist_info()
+    if rank != 0:
+        return  # config 4 is a single-operator loop: replicas only
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    ctx = h.Context(local)
+    cfg = configs.CONFIGS[2]
+    st = configs.make_setup(cfg)
+    g = st.grid()
+    tree = lr.ClusterTree(st.source_xy, st.box_lo, st.box_hi)
+    eps = configs.compression_tolerance(st, tree.depth())
+    plan = make_plan(tree.nodes, tree.root, 1)
+    t0 = time.perf_counter()
+    F, _ = born.compute_fields(ctx, g, st.sigma, st.sigma_prime, st.inv_D, st.points, tol=1e-10)
+    w = torch.full((g.N,), cfg.h ** 3, dtype=torch.float64, device=dev)
+    srcs = list(range(cfg.n_sources))
+    prov = lr.BornFieldsProvider([F[int(st.source_point[s])] for s in srcs],
+                                 [[F[int(st.detector_point[s, d])] for d in range(cfg.n_det)]
+                                  for s in srcs], w, 1.0)
+    eng = GpuEngine(ctx)
+    rec = eng.compress_subtree(st.source_xy, st.box_lo, st.box_hi, srcs, tree.root, eps, prov,
+                               cfg.seed, 20, 10)
+    fr = lr.recompress(ctx, rec.factor, eps, -1, rec.ledger)
+    del prov, F, rec
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    setup_s = time.perf_counter() - t0
+    perm = global_perm(tree, plan, cfg.rows_per_source, st)
+    Hop = pals.HOperator(ctx, fr, perm)
+    geom = pals.GridGeom.for_grid7(cfg.n, cfg.h)
+    tr = configs.pals_truth(st)
+    truth = pals.PaLSParams(tr.alpha, tr.beta, tr.centers, tr.tau_level, tr.eps_H, tr.nu_norm)
+    init = pals.PaLSParams(tr.init_alpha, tr.init_beta, tr.init_centers, tr.tau_level, tr.eps_H,
+                           tr.nu_norm)
+    mu_true = pals.shape(ctx, truth, geom)
+    hm = Hop(mu_true)
+    scale = torch.as_tensor(st.eps_c @ tr.conc, device=dev)
+    y_clean = scale[torch.arange(cfg.M, device=dev) % cfg.n_lambda] * hm  # forward_measure
+    eta = h.gaussian(ctx, configs.PALS_SEED, 0, cfg.M)                      # add_noise, 40 dB
+    target = torch.linalg.norm(y_clean) * 10.0 ** (-40.0 / 20.0)
+    eta = eta * (target / torch.linalg.norm(eta))
+    y = y_clean + eta
+    wdiag = torch.full((cfg.M,), float(np.sqrt(cfg.M) / target), dtype=torch.float64, device=dev)
+    noise_norm = float(torch.linalg.norm(wdiag * eta))
+    # the loop is run to a fixed step count: the discrepancy target is not
+    # used as a stop (noise_norm = 0), the stagnation test still applies
+    rc = pals.ReconConfig(max_outer=args.steps, max_inner=1)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        pals.reconstruct(ctx, y, Hop, geom, st.eps_c, init, wdiag, 0.0,
+                         pals.ReconConfig(max_outer=2, max_inner=1))
+    J = lr.JOperator(ctx, fr, perm, st.eps_c)
+    X64 = torch.randn(64, g.N * cfg.n_chrom, dtype=torch.float64, device=dev)
+    Y64 = torch.empty(64, cfg.M, dtype=torch.float64, device=dev)
+    for _ in range(2):
+        J.matmat_cm(X64, Y64, 64)
+        J.rmatmat_cm(Y64, X64, 64)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    h.lib().hydot_ctx_timing_report(ctx.h, None, 0)
+    h.lib().hydot_ctx_set_timing(ctx.h, 1)
+    launches0 = ctx.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    res = pals.reconstruct(ctx, y, Hop, geom, st.eps_c, init, wdiag, 0.0, rc, mu_truth=mu_true)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    loop_ms = e0.elapsed_time(e1)
+    h.lib().hydot_ctx_set_timing(ctx.h, 0)
+    buf = ctypes.create_string_buffer(1 << 16)
+    h.lib().hydot_ctx_timing_report(ctx.h, buf, 1 << 16)
+    gn_steps = max(1, len({(t.outer, t.inner) for t in res.trace if t.inner >= 0}))
+    stages = {k: {"ms_per_step": v[0] / gn_steps, "calls_per_step": v[1] / gn_steps,
+                  "flops": v[2], "bytes": v[3]} for k, v in json.loads(buf.value.decode()).items()}
+    # BASELINE's literal per-step blocks: 64 J~x + 64 J~^T y per step
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(args.steps):
+        J.matmat_cm(X64, Y64, 64)
+        J.rmatmat_cm(Y64, X64, 64)
+    b.record(stream)
+    torch.cuda.synchronize()
+    launches = ctx.launch_count() - launches0
+    clk = clocks.stop()
+    blk_s = a.elapsed_time(b) / 1e3 / args.steps
+    R = fr.rank()
+    nbytes = 2 * 8.0 * (g.N * R + cfg.M * R + 64 * cfg.n_chrom * g.N + 64 * cfg.M)
+    flops = 2 * 2.0 * R * 64 * cfg.n_chrom * (g.N + cfg.M)
+    # e2e: the loop through the public call with host-resident y and w
+    yh, wh = y.cpu().numpy(), wdiag.cpu().numpy()
+    a2, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a2.record(stream)
+    res2 = pals.reconstruct(ctx, yh, Hop, geom, st.eps_c, init, wh, 0.0, rc)
+    b2.record(stream)
+    torch.cuda.synchronize()
+    steps2 = max(1, len({(t.outer, t.inner) for t in res2.trace if t.inner >= 0}))
+    e2e_s = a2.elapsed_time(b2) / 1e3 / steps2
+    step_s = loop_ms / 1e3 / gn_steps
+    jac = stages.get("pals_jacobian")
+    roof = None
+    if jac:
+        ach = jac["bytes"] / (jac["ms_per_step"] * gn_steps / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": HBM_PEAK_GBS, "unit": "GB/s",
+                "frac": ach / HBM_PEAK_GBS, "traffic": None, "stage": "pals_jacobian",
+                "kernel": "pals_eval_k<JACOBIAN> (N x 5 n_p write, 8*5*n_p B per vertex)"}
+    m = pals.metrics(ctx, mu_true, pals.shape(ctx, res.p, geom))
+    out = {"metric": "PaLS Gauss-Newton time per step", "value": step_s, "unit": "s/step",
+           "n_gpus": 1, "steps": gn_steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+           "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded BASELINE config-4 anomaly over the config-2 operator)",
+           "config": {"workload": "cfg4: PaLS reconstruct (pals.cpp:193-295) on the compressed cfg2 operator",
+                      "n": cfg.n, "N": g.N, "M": cfg.M, "n_rbf": len(tr.alpha),
+                      "num_params": 5 * len(tr.alpha), "operator_rank": R,
+                      "max_inner": 1, "setup_s": setup_s,
+                      "l2": "operator (V: %.2f GB) larger than L2" % (g.N * R * 8 / 1e9)},
+           "gpu_launches": int(launches),
+           "e2e": {"value": e2e_s, "unit": "s/step", "h2d_bytes_per_step": int(2 * cfg.M * 8 / steps2),
+                   "d2h_bytes_per_step": int(8 * (5 * len(tr.alpha) + cfg.n_chrom) / 1)},
+           "roofline": roof,
+           "stages": stages, "clocks": clk,
+           "loop": {"gn_steps": gn_steps, "hmv_calls": res.hmv_calls, "hmv_columns": res.hmv_columns,
+                    "resnorm0": res.trace[0].resnorm if res.trace else None,
+                    "resnorm": res.resnorm, "flagged": res.flagged, "dice_vs_truth": m.dice},
+           "matvec_blocks": {"b": 64, "ms_per_step": blk_s * 1e3, "GB/s": nbytes / blk_s / 1e9,
+                             "TFLOP/s": flops / blk_s / 1e12, "hbm_frac": nbytes / blk_s / 1e9 / HBM_PEAK_GBS,
+                             "fp64_frac": flops / blk_s / 1e12 / FP64_PEAK_TFLOPS,
+                             "what": "64 J~x + 64 J~^T y per step (hydot_j_matmat, 4 chromophores)"}}
+    print(json.dumps(out), flush=True)
+
+
 # ---------------------------------------------------------- reference arm --
 def run_reference(args):
     rank, world, local = dist_info()
@@ -492,6 +637,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == 4:
+        run_pals(args)
     else:
         run_b200(args)
 

@@ -152,3 +152,44 @@ def compression_tolerance(setup: Setup, tree_depth: int) -> float:
     cfg = setup.cfg
     Nr = min(cfg.M, cfg.N)
     return cfg.eps_d / (2.0 ** (tree_depth / 2.0) * (tree_depth + 1) * np.sqrt(Nr))
+
+
+# ------------------------------------------------------------- config 4 --
+# BASELINE config 4: the PaLS loop on config 2's compressed operator.  The
+# anomaly is a level set of 16 compactly supported RBFs (Wendland, the
+# reference's basis, pals.cpp:38-43) with centres uniform in the interior,
+# widths U[3,8] mm (beta = 1/width), weights N(0,1); chromophore contrasts
+# U[0.5,2] x background; 1 % noise = add_noise(y, 40 dB) (born.cpp:131-154).
+PALS_N_RBF = 16
+PALS_SEED = SEED + 4
+
+
+@dataclass
+class PalsTruth:
+    alpha: np.ndarray
+    beta: np.ndarray
+    centers: np.ndarray   # n_p x 3 (mm, grid frame: x,y in [-L, L], z in [0, 2L])
+    conc: np.ndarray      # perturbed concentrations (n_chrom)
+    init_alpha: np.ndarray
+    init_beta: np.ndarray
+    init_centers: np.ndarray
+    tau_level: float = 0.1
+    eps_H: float = 0.05
+    nu_norm: float = 1e-3
+
+
+def pals_truth(setup: Setup, seed: int = PALS_SEED, n_rbf: int = PALS_N_RBF) -> PalsTruth:
+    cfg = setup.cfg
+    rng = np.random.default_rng(seed)
+    L = (cfg.n - 1) * cfg.h / 2
+    centers = np.stack([rng.uniform(-0.6 * L, 0.6 * L, n_rbf), rng.uniform(-0.6 * L, 0.6 * L, n_rbf),
+                        rng.uniform(0.3 * 2 * L, 0.7 * 2 * L, n_rbf)], axis=1)
+    width = rng.uniform(3.0, 8.0, n_rbf)
+    alpha = rng.standard_normal(n_rbf)
+    conc = setup.conc * rng.uniform(0.5, 2.0, cfg.n_chrom)
+    # start of the reconstruction: weights damped, widths and centres perturbed
+    init_alpha = 0.8 * alpha
+    init_beta = 1.0 / (width * rng.uniform(0.85, 1.15, n_rbf))
+    init_centers = centers + rng.uniform(-cfg.h, cfg.h, centers.shape)
+    return PalsTruth(alpha, 1.0 / width, centers, conc, init_alpha, init_beta, init_centers,
+                     nu_norm=1e-3 * cfg.h)
