@@ -168,6 +168,78 @@ __global__ void __launch_bounds__(PT) qr_panel_coop(int64_t mr, int jb, double* 
     }
 }
 
+// Single-CTA panel for short panels (mr <= kCtaRows): the mr x jb slab lives
+// in shared memory and each column costs two block barriers.  Phase 1: warp
+// w computes s_q = x^T P[c+1:, q] for its columns q > c (x the unscaled
+// sub-column below the diagonal) and the last warps the norm ||x||^2; phase
+// 2: every thread forms (beta, tau, scal) redundantly, w_q = P_cq + scal
+// s_q, and applies H_c = I - tau v v^T (v = [1; scal x]) to its (row, q)
+// entries, storing v and beta.
+constexpr int kCtaRows = 768;
+constexpr int CT = 512;
+__global__ void __launch_bounds__(CT) qr_panel_cta(int mr, int jb, double* __restrict__ P, int64_t ld,
+                                                   double* __restrict__ tau_out) {
+    extern __shared__ double slab[];  // mr x jb, ld mr
+    __shared__ double s_dot[PB], s_pc[PB];
+    __shared__ double s_nrm[CT / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = CT / 32;
+    for (int q = 0; q < jb; ++q)
+        for (int i = threadIdx.x; i < mr; i += CT) slab[i + q * mr] = P[i + int64_t(q) * ld];
+    __syncthreads();
+    for (int c = 0; c < jb; ++c) {
+        const double* x = slab + int64_t(c) * mr;
+        // ---- phase 1: dots with the later columns (warp per column) + norm
+        const int nq = jb - c - 1;
+        for (int t = warp; t < nq; t += NW) {
+            const double* pq = slab + int64_t(c + 1 + t) * mr;
+            double s = 0.0;
+            for (int i = c + 1 + lane; i < mr; i += 32) s += x[i] * pq[i];
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) {
+                s_dot[c + 1 + t] = s;
+                s_pc[c + 1 + t] = pq[c];  // P_cq before the update (phase 2 rewrites it)
+            }
+        }
+        double nacc = 0.0;
+        for (int i = c + 1 + threadIdx.x; i < mr; i += CT) nacc += x[i] * x[i];
+        for (int o = 16; o > 0; o >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, o);
+        if (lane == 0) s_nrm[warp] = nacc;
+        __syncthreads();
+        // ---- phase 2: reflector (redundantly per thread) and update
+        double xn2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < NW; ++k) xn2 += s_nrm[k];
+        const double alpha = x[c];
+        double tau = 0.0, beta = alpha, scal = 1.0;
+        if (xn2 > 0.0) {
+            beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
+            tau = (beta - alpha) / beta;
+            scal = 1.0 / (alpha - beta);
+        }
+        if (tau != 0.0) {
+            for (int q = c + 1 + warp; q < jb; q += NW) {  // warp per column, lanes over rows
+                const double wq = s_pc[q] + scal * s_dot[q];
+                double* pq = slab + int64_t(q) * mr;
+                if (lane == 0) pq[c] -= tau * wq;  // v_c = 1
+                for (int i = c + 1 + lane; i < mr; i += 32) pq[i] -= tau * (x[i] * scal) * wq;
+            }
+        }
+        __syncthreads();  // column c, s_dot, s_pc and s_nrm fully consumed
+        // scale column c into v; the next column's phase 1 touches only
+        // columns > c, so no barrier is needed before it
+        if (tau != 0.0)
+            for (int i = c + 1 + threadIdx.x; i < mr; i += CT) slab[i + int64_t(c) * mr] *= scal;
+        if (threadIdx.x == 0) {
+            slab[c + int64_t(c) * mr] = beta;
+            tau_out[c] = tau;
+        }
+    }
+    __syncthreads();
+    for (int q = 0; q < jb; ++q)
+        for (int i = threadIdx.x; i < mr; i += CT) P[i + int64_t(q) * ld] = slab[i + q * mr];
+}
+
 // Vp (mr x jb, ld mr): unit lower trapezoid of the factored columns
 __global__ void form_v(int64_t mr, int jb, const double* __restrict__ P, int64_t ld,
                        double* __restrict__ V) {
@@ -209,12 +281,20 @@ void panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, const
     StageTimer _t(c, "qr_panel", mr, jb, -1, 2.0 * double(mr) * jb * jb, 16.0 * double(mr) * jb);
     static bool attr = false;
     const size_t smem_cap = 200 * 1024;
+    if (mr <= kCtaRows) {  // short panels: one CTA, the whole panel on-chip
+        static bool cattr = false;
+        if (!cattr) {
+            HYDOT_CUDA(cudaFuncSetAttribute(qr_panel_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            int(smem_cap)));
+            cattr = true;
+        }
+        qr_panel_cta<<<1, CT, size_t(mr) * jb * sizeof(double), c.stream>>>(int(mr), jb, P, ld, tau);
+        c.check_launch();
+        return;
+    }
     int G = c.num_sms;
     int64_t rows_per = (mr + G - 1) / G;
-    if (mr <= 768) {  // short panels: one CTA holds the whole panel on-chip
-        G = 1;
-        rows_per = mr;
-    } else if (rows_per < 64) {
+    if (rows_per < 64) {
         G = int(std::max<int64_t>(1, (mr + 63) / 64));
         rows_per = (mr + G - 1) / G;
     }
