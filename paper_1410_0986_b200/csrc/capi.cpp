@@ -1,6 +1,7 @@
 // capi.cpp -- the C ABI (include/hydot_b200.h) over the device drivers.
 // Status mapping keeps the reference's exception classes:
 // std::invalid_argument -> HYDOT_EINVAL, std::runtime_error -> HYDOT_ERUNTIME.
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -95,6 +96,25 @@ hydot_status hydot_ctx_create(int device, hydot_ctx* out) {
         if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
             uint64_t thr = UINT64_MAX;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            // map a working reserve once per device so the GB-sized per-node
+            // buffers of the merges never wait for the pool to grow
+            // (HYDOT_POOL_RESERVE_GB, default 16; 0 disables)
+            static bool reserved[64] = {};
+            const char* e = std::getenv("HYDOT_POOL_RESERVE_GB");
+            const double gb = e ? std::atof(e) : 16.0;
+            if (gb > 0 && device >= 0 && device < 64 && !reserved[device]) {
+                reserved[device] = true;
+                size_t fr = 0, tot = 0;
+                HYDOT_CUDA(cudaMemGetInfo(&fr, &tot));
+                const size_t want = std::min(size_t(gb * double(1ull << 30)), fr / 4);
+                void* p = nullptr;
+                if (want > 0 && cudaMallocAsync(&p, want, c->stream) == cudaSuccess) {
+                    HYDOT_CUDA(cudaFreeAsync(p, c->stream));
+                    HYDOT_CUDA(cudaStreamSynchronize(c->stream));
+                } else {
+                    cudaGetLastError();
+                }
+            }
         }
         auto* h = new hydot_ctx_s;
         h->c = c;
