@@ -89,16 +89,21 @@ __global__ void __launch_bounds__(PT) qr_panel_coop(int64_t mr, int jb, double* 
                 for (int q = col; q < jb; ++q) buf.row[par * PB + q] = at(i, q);
         }
         nacc = warp_sum(nacc);
+        // transpose-reduce: afterwards lane q holds sum over lanes of acc[q]
+        // (31 shuffles instead of 32 full butterflies)
 #pragma unroll
-        for (int q = 0; q < PB; ++q)
-            if (q > col && q < jb) acc[q] = warp_sum(acc[q]);
-        __syncthreads();  // red[] may still be read by the previous reduction
-        if (lane == 0) {
-            red[warp][PB] = nacc;
+        for (int sft = PB / 2; sft >= 1; sft >>= 1) {
+            const bool upper = (lane & sft) != 0;
 #pragma unroll
-            for (int q = 0; q < PB; ++q)
-                if (q > col && q < jb) red[warp][q] = acc[q];
+            for (int j = 0; j < sft; ++j) {
+                const double send = upper ? acc[j] : acc[j + sft];
+                const double keep = upper ? acc[j + sft] : acc[j];
+                acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+            }
         }
+        __syncthreads();  // red[] may still be read by the previous reduction
+        red[warp][lane] = acc[0];
+        if (lane == 0) red[warp][PB] = nacc;
         __syncthreads();
         if (threadIdx.x <= PB) {
             const int q = threadIdx.x;
@@ -113,34 +118,47 @@ __global__ void __launch_bounds__(PT) qr_panel_coop(int64_t mr, int jb, double* 
     for (int c = 0; c < jb; ++c) {
         const int par = c & 1;
         grid.sync();
-        // ---- reflector of column c from the published partials (every CTA)
-        if (threadIdx.x == 0) {
+        // ---- reflector of column c from the published partials (every CTA,
+        // identical fixed-order warp reductions -> identical results).  Warp 0
+        // reduces the G norm partials, the other warps the dot partials of
+        // their columns; lanes stride over the partials so the L2 loads are
+        // issued together instead of as one dependent chain.
+        if (warp == 0) {
             double xn2 = 0.0;
-            for (int p = 0; p < G; ++p) xn2 += buf.nrm[par * GMAX + p];
-            const double alpha = buf.row[par * PB + c];
-            double tau = 0.0, beta = alpha, scal = 1.0;
-            if (xn2 > 0.0) {
-                beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
-                tau = (beta - alpha) / beta;
-                scal = 1.0 / (alpha - beta);
+            for (int p = lane; p < G; p += 32) xn2 += buf.nrm[par * GMAX + p];
+            xn2 = warp_sum(xn2);
+            if (lane == 0) {
+                const double alpha = buf.row[par * PB + c];
+                double tau = 0.0, beta = alpha, scal = 1.0;
+                if (xn2 > 0.0) {
+                    beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
+                    tau = (beta - alpha) / beta;
+                    scal = 1.0 / (alpha - beta);
+                }
+                sc[0] = tau;
+                sc[1] = beta;
+                sc[2] = scal;
             }
-            sc[0] = tau;
-            sc[1] = beta;
-            sc[2] = scal;
+        } else {
+            for (int q = c + warp; q < jb; q += PT / 32 - 1) {  // q = c+1, c+2, ...
+                double s = 0.0;
+                for (int p = lane; p < G; p += 32) s += buf.dot[(int64_t(par) * GMAX + p) * PB + q];
+                s = warp_sum(s);
+                if (lane == 0) wsh[q] = s;  // raw x^T P_q; scaled below
+            }
         }
         __syncthreads();
         const double tau = sc[0], beta = sc[1], scal = sc[2];
+        double wq_own = 0.0;
         if (threadIdx.x < PB) {
             const int q = threadIdx.x;
-            double w = 0.0;
             if (q > c && q < jb) {
-                double s = 0.0;
-                for (int p = 0; p < G; ++p) s += buf.dot[(int64_t(par) * GMAX + p) * PB + q];
                 const double pc = buf.row[par * PB + q];
-                w = pc + scal * (s - buf.row[par * PB + c] * pc);  // v^T P_q, v_c = 1
+                wq_own = pc + scal * (wsh[q] - buf.row[par * PB + c] * pc);  // v^T P_q, v_c = 1
             }
-            wsh[q] = w;
         }
+        __syncthreads();
+        if (threadIdx.x < PB) wsh[threadIdx.x] = wq_own;
         __syncthreads();
         // ---- apply H_c to the rest of the panel (own rows), store v
         for (int64_t i = max(r0, int64_t(c)) + threadIdx.x; i < r1; i += PT) {
