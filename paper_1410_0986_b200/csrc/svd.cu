@@ -8,12 +8,16 @@
 // accuracy (no Gram matrix is formed).  Two drivers:
 //   * small: (m + n) n doubles fit in shared memory -- one CTA runs every
 //     sweep on-chip, one warp per column pair;
-//   * large: one cooperative persistent kernel runs all sweeps, one CTA per
-//     column pair (the pair held in registers when V is recovered lazily),
-//     a grid-wide barrier between rounds and a per-sweep rotation counter
-//     for convergence (no host round trips).  A dataflow variant with
-//     per-column completion flags instead of round barriers measured 1.75x
-//     slower (a release fence per pair serialises each CTA).
+//   * large: one cooperative persistent kernel runs all sweeps with a
+//     grid-wide barrier between rounds and a per-sweep rotation counter for
+//     convergence (no host round trips).  With lazy V (the path's default)
+//     and m <= 2560 it is the register block-Jacobi jacobi_rblk_k (blocks of
+//     4 columns, a 28-pair mini-sweep per block pair in registers: 4x fewer
+//     barriers and passes over U; 1.24x faster over config 1's cores than the
+//     point driver); otherwise one CTA per column pair.  Measured slower and
+//     kept out of the default: a dataflow variant with per-column completion
+//     flags (a release fence per pair serialises each CTA, 1.75x) and a
+//     shared-memory block variant (bound by per-SM shared-memory bandwidth).
 // Afterwards sigma_j = ||u_j||, U = u_j / sigma_j, sorted descending.
 #include <cooperative_groups.h>
 
@@ -329,6 +333,144 @@ __global__ void __launch_bounds__(JT, EPT <= 4 ? 4 : (EPT <= 8 ? 3 : 2)) jacobi_
     if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
 }
 
+// Block one-sided Jacobi for the lazy-V driver, register resident.  Columns
+// are grouped in blocks of RB = 4; a global round pairs the blocks (circle
+// method over nb blocks) and each CTA loads its block pair into registers --
+// thread t holds rows t, t + 512, ... of all 8 columns -- and runs one full
+// mini-sweep over the 28 column pairs: 7 sub-rounds of 4 disjoint pairs whose
+// indices are compile-time constants (unrolled circle method), each sub-round
+// one block reduction of the 12 dot products, rotations computed from the
+// actual column dots (the point driver's accuracy) and applied in registers.
+// Per sweep: nb-1 grid barriers and passes over U instead of n-1.
+constexpr int RB = 4;            // block width
+constexpr int RC = 2 * RB;       // columns per block pair
+constexpr int RT = 512;          // threads
+constexpr int RNV = 3 * RB;      // dot products per sub-round
+
+__host__ __device__ constexpr int circ_col(int pos, int r, int np) {
+    return pos == 0 ? 0 : ((pos - 1 + r) % (np - 1)) + 1;
+}
+
+template <int R>
+__global__ void __launch_bounds__(RT, 1) jacobi_rblk_k(int64_t m, int n, int nb, const int2* __restrict__ bpairs,
+                                                      double* __restrict__ U, int64_t ldu, double tol,
+                                                      int* __restrict__ counters, int* __restrict__ sweeps_out) {
+    constexpr int NW = RT / 32;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double red[RNV][NW];
+    __shared__ double tot[RNV];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nbp = nb + (nb & 1);
+    const int rounds = nbp - 1, per = nbp / 2;
+    int sweep = 0;
+    double x[R][RC];
+    for (; sweep < kMaxSweeps; ++sweep) {
+        int mine = 0;
+        for (int r = 0; r < rounds; ++r) {
+            for (int q = blockIdx.x; q < per; q += gridDim.x) {
+                const int2 bp = bpairs[r * per + q];
+                int col[RC];
+#pragma unroll
+                for (int j = 0; j < RC; ++j) {
+                    const int blk = j < RB ? bp.x : bp.y;
+                    const int cj = blk * RB + (j % RB);
+                    col[j] = (blk < nb && cj < n) ? cj : -1;
+                }
+#pragma unroll
+                for (int j = 0; j < RC; ++j)
+#pragma unroll
+                    for (int rr = 0; rr < R; ++rr) {
+                        const int64_t i = threadIdx.x + int64_t(rr) * RT;
+                        x[rr][j] = (col[j] >= 0 && i < m) ? __ldcg(U + i + int64_t(col[j]) * ldu) : 0.0;
+                    }
+#pragma unroll
+                for (int sr = 0; sr < RC - 1; ++sr) {
+                    double part[16];  // 12 dot products of this sub-round, padded
+#pragma unroll
+                    for (int k = 0; k < RB; ++k) {
+                        const int p = circ_col(k, sr, RC), o = circ_col(RC - 1 - k, sr, RC);
+                        double a = 0.0, b = 0.0, g = 0.0;
+#pragma unroll
+                        for (int rr = 0; rr < R; ++rr) {
+                            a += x[rr][p] * x[rr][p];
+                            b += x[rr][o] * x[rr][o];
+                            g += x[rr][p] * x[rr][o];
+                        }
+                        part[3 * k] = a;
+                        part[3 * k + 1] = b;
+                        part[3 * k + 2] = g;
+                    }
+#pragma unroll
+                    for (int v = RNV; v < 16; ++v) part[v] = 0.0;
+                    // warp transpose-reduce: lane l ends with the warp total of
+                    // quantity (l & 15) -- 12 + 15 shuffles
+#pragma unroll
+                    for (int v = 0; v < RNV; ++v) part[v] += __shfl_xor_sync(0xffffffffu, part[v], 16);
+#pragma unroll
+                    for (int sft = 8; sft >= 1; sft >>= 1) {
+                        const bool upper = (lane & sft) != 0;
+#pragma unroll
+                        for (int j = 0; j < sft; ++j) {
+                            const double send = upper ? part[j] : part[j + sft];
+                            const double keep = upper ? part[j + sft] : part[j];
+                            part[j] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+                        }
+                    }
+                    if (lane < RNV) red[lane][warp] = part[0];
+                    __syncthreads();
+                    if (warp < RB) {  // warp k finishes pair k and forms its rotation once
+                        double A = lane < NW ? red[3 * warp][lane] : 0.0;
+                        double Bv = lane < NW ? red[3 * warp + 1][lane] : 0.0;
+                        double G = lane < NW ? red[3 * warp + 2][lane] : 0.0;
+                        for (int sft = NW / 2; sft > 0; sft >>= 1) {
+                            A += __shfl_xor_sync(0xffffffffu, A, sft);
+                            Bv += __shfl_xor_sync(0xffffffffu, Bv, sft);
+                            G += __shfl_xor_sync(0xffffffffu, G, sft);
+                        }
+                        if (lane == 0) {
+                            double cs = 1.0, sn = 0.0, on = 0.0;
+                            if (G != 0.0 && fabs(G) > tol * sqrt(A * Bv)) {
+                                rot_params(A, Bv, G, cs, sn);
+                                on = 1.0;
+                            }
+                            tot[3 * warp] = cs;
+                            tot[3 * warp + 1] = sn;
+                            tot[3 * warp + 2] = on;
+                        }
+                    }
+                    __syncthreads();
+#pragma unroll
+                    for (int k = 0; k < RB; ++k) {
+                        const int p = circ_col(k, sr, RC), o = circ_col(RC - 1 - k, sr, RC);
+                        if (tot[3 * k + 2] != 0.0) {
+                            const double cs = tot[3 * k], sn = tot[3 * k + 1];
+#pragma unroll
+                            for (int rr = 0; rr < R; ++rr) {
+                                const double xp = x[rr][p], xo = x[rr][o];
+                                x[rr][p] = cs * xp - sn * xo;
+                                x[rr][o] = sn * xp + cs * xo;
+                            }
+                            if (threadIdx.x == 0) ++mine;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < RC; ++j)
+#pragma unroll
+                    for (int rr = 0; rr < R; ++rr) {
+                        const int64_t i = threadIdx.x + int64_t(rr) * RT;
+                        if (col[j] >= 0 && i < m) __stcg(U + i + int64_t(col[j]) * ldu, x[rr][j]);
+                    }
+            }
+            grid.sync();
+        }
+        if (threadIdx.x == 0 && mine) atomicAdd(&counters[sweep], mine);
+        grid.sync();
+        if (*((volatile int*)&counters[sweep]) == 0) break;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
+}
+
 // ----------------------------------------------------- block Jacobi -------
 // One-sided block Jacobi: columns are grouped in blocks of B; a round pairs
 // the blocks (circle method over nb blocks), each CTA loads its block pair
@@ -553,6 +695,45 @@ void launch_block_jacobi(Ctx& c, int64_t m, int64_t n, double* U, int64_t ldu, d
     }
 }
 
+// register block-Jacobi for the lazy-V driver: rows per thread R = m / 512
+// (<= 5); 0 = not used
+int rblk_rows(int64_t m, int64_t n) {
+    static const int mode = [] {
+        const char* e = std::getenv("HYDOT_JACOBI_BLK");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (mode == 0 || (n + RB - 1) / RB < 4) return 0;
+    const int64_t R = (m + RT - 1) / RT;
+    return R <= 5 ? int(R) : 0;
+}
+
+template <int R>
+void launch_rblk_t(Ctx& c, int64_t m, int64_t n, double* U, int64_t ldu, double tol, int* counters,
+                   int* sweeps_out) {
+    int nb = int((n + RB - 1) / RB);
+    int npb = 0;
+    const int2* bp = device_pairs(nb, npb);
+    int per_sm = 0;
+    HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_rblk_k<R>, RT, 0));
+    int grid = std::max(1, std::min(npb / 2, per_sm * c.num_sms));
+    int64_t mm = m;
+    int nn = int(n), nbb = nb;
+    void* args[] = {&mm, &nn, &nbb, &bp, &U, &ldu, &tol, &counters, &sweeps_out};
+    HYDOT_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_rblk_k<R>, dim3(grid), dim3(RT), args, 0, c.stream));
+    c.count();
+}
+
+void launch_rblk(Ctx& c, int R, int64_t m, int64_t n, double* U, int64_t ldu, double tol, int* counters,
+                 int* sweeps_out) {
+    switch (R) {
+        case 1: launch_rblk_t<1>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
+        case 2: launch_rblk_t<2>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
+        case 3: launch_rblk_t<3>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
+        case 4: launch_rblk_t<4>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
+        default: launch_rblk_t<5>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
+    }
+}
+
 thread_local bool g_strict_svd = false;
 bool strict_svd_flag() { return g_strict_svd; }
 bool lazy_v_enabled() {
@@ -617,6 +798,9 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
         jacobi_smem_k<<<1, 1024, smem, c.stream>>>(int(m), int(n), np, dpairs, U.d(), m, V.d(), n,
                                                     tol, atol, sw.as<int>() + kMaxSweeps);
         c.check_launch();
+    } else if (n >= 2 && !strict_svd_flag() && lazy_v_enabled() && atol == 0.0 && rblk_rows(m, n) > 0) {
+        lazy_v = true;
+        launch_rblk(c, rblk_rows(m, n), m, n, U.d(), m, tol, sw.as<int>(), sw.as<int>() + kMaxSweeps);
     } else if (use_block_jacobi(m, n)) {
         set_identity(c, n, n, V.d(), n);
         launch_block_jacobi(c, m, n, U.d(), m, V.d(), n, tol, atol, sw.as<int>(),
