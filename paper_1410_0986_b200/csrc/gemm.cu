@@ -52,7 +52,15 @@ template <int RC, int SC, int L, int NT>
 __device__ __forceinline__ void load_block(double* dst, const double* __restrict__ g, int64_t ld,
                                            int64_t r0, int64_t rmax, int64_t s0, int64_t smax,
                                            bool vec, int tid) {
-    if (vec) {
+    if (vec && r0 + RC <= rmax && s0 + SC <= smax) {  // interior block: no predicates
+        const double* base = g + r0 + s0 * ld;
+#pragma unroll
+        for (int e = 0; e < (RC * SC) / (2 * NT); ++e) {
+            const int idx = tid + e * NT;
+            const int r = (idx % (RC / 2)) * 2, sidx = idx / (RC / 2);
+            cp_async16(dst + sidx * L + r, base + r + int64_t(sidx) * ld, 16);
+        }
+    } else if (vec) {
 #pragma unroll
         for (int e = 0; e < (RC * SC) / (2 * NT); ++e) {
             int idx = tid + e * NT;
