@@ -545,7 +545,14 @@ hydot_status hydot_thin_svd(hydot_ctx ctx, int64_t m, int64_t n, const double* a
     return guard(ctx ? ctx->c.get() : nullptr, [&] {
         Ctx& c = ctx_of(ctx);
         if (m < 0 || n < 0 || lda < m) throw std::invalid_argument("thin_svd: bad dimensions");
-        StrictSVD strict;  // full orthonormal U, V like Eigen::BDCSVD
+        // full orthonormal U, V like Eigen::BDCSVD; HYDOT_THIN_SVD_PATH=1
+        // runs the path's own (lazy-V) variant instead, for profiling
+        static const bool path_mode = [] {
+            const char* e = std::getenv("HYDOT_THIN_SVD_PATH");
+            return e && e[0] == '1';
+        }();
+        std::unique_ptr<StrictSVD> strict;
+        if (!path_mode) strict.reset(new StrictSVD());
         SVDd s = fast_thin_svd(c, a_dev, lda, false, m, n, nullptr, HYDOT_CAT_OTHER);
         const int64_t k = s.k;
         if (k > 0) {

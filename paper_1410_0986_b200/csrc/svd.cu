@@ -344,14 +344,14 @@ __global__ void __launch_bounds__(JT, EPT <= 4 ? 4 : (EPT <= 8 ? 3 : 2)) jacobi_
 // Per sweep: nb-1 grid barriers and passes over U instead of n-1.
 constexpr int RB = 4;            // block width
 constexpr int RC = 2 * RB;       // columns per block pair
-constexpr int RT = 512;          // threads
 constexpr int RNV = 3 * RB;      // dot products per sub-round
+constexpr int RMAXR = 5;         // max rows per thread (5-9 measured: 5 fastest)
 
 __host__ __device__ constexpr int circ_col(int pos, int r, int np) {
     return pos == 0 ? 0 : ((pos - 1 + r) % (np - 1)) + 1;
 }
 
-template <int R>
+template <int R, int RT>
 __global__ void __launch_bounds__(RT, 1) jacobi_rblk_k(int64_t m, int n, int nb, const int2* __restrict__ bpairs,
                                                       double* __restrict__ U, int64_t ldu, double tol,
                                                       int* __restrict__ counters, int* __restrict__ sweeps_out) {
@@ -418,10 +418,11 @@ __global__ void __launch_bounds__(RT, 1) jacobi_rblk_k(int64_t m, int n, int nb,
                     }
                     if (lane < RNV) red[lane][warp] = part[0];
                     __syncthreads();
-                    if (warp < RB) {  // warp k finishes pair k and forms its rotation once
-                        double A = lane < NW ? red[3 * warp][lane] : 0.0;
-                        double Bv = lane < NW ? red[3 * warp + 1][lane] : 0.0;
-                        double G = lane < NW ? red[3 * warp + 2][lane] : 0.0;
+                    for (int k = warp; k < RB; k += NW) {  // a warp finishes pair k, forms its rotation once
+                        double A = lane < NW ? red[3 * k][lane] : 0.0;
+                        double Bv = lane < NW ? red[3 * k + 1][lane] : 0.0;
+                        double G = lane < NW ? red[3 * k + 2][lane] : 0.0;
+#pragma unroll
                         for (int sft = NW / 2; sft > 0; sft >>= 1) {
                             A += __shfl_xor_sync(0xffffffffu, A, sft);
                             Bv += __shfl_xor_sync(0xffffffffu, Bv, sft);
@@ -433,9 +434,9 @@ __global__ void __launch_bounds__(RT, 1) jacobi_rblk_k(int64_t m, int n, int nb,
                                 rot_params(A, Bv, G, cs, sn);
                                 on = 1.0;
                             }
-                            tot[3 * warp] = cs;
-                            tot[3 * warp + 1] = sn;
-                            tot[3 * warp + 2] = on;
+                            tot[3 * k] = cs;
+                            tot[3 * k + 1] = sn;
+                            tot[3 * k + 2] = on;
                         }
                     }
                     __syncthreads();
@@ -695,42 +696,60 @@ void launch_block_jacobi(Ctx& c, int64_t m, int64_t n, double* U, int64_t ldu, d
     }
 }
 
-// register block-Jacobi for the lazy-V driver: rows per thread R = m / 512
-// (<= 5); 0 = not used
-int rblk_rows(int64_t m, int64_t n) {
+// register block-Jacobi for the lazy-V driver: the fewest threads T (a
+// power of two >= 64) with at most RMAXR rows each -- the per-sub-round
+// reduction costs instructions per warp, so fat threads win; 0 = not used
+bool rblk_shape(int64_t m, int64_t n, int& R, int& T) {
     static const int mode = [] {
         const char* e = std::getenv("HYDOT_JACOBI_BLK");
         return e ? std::atoi(e) : 1;
     }();
-    if (mode == 0 || (n + RB - 1) / RB < 4) return 0;
-    const int64_t R = (m + RT - 1) / RT;
-    return R <= 5 ? int(R) : 0;
+    if (mode == 0 || (n + RB - 1) / RB < 4) return false;
+    for (T = 64; T <= 512; T *= 2) {
+        R = int((m + T - 1) / T);
+        const int cap = T == 512 ? 5 : RMAXR;  // 512 threads: 128 registers each
+        if (R <= cap) {
+            R = R <= 3 ? 3 : R <= 5 ? 5 : R <= 7 ? 7 : 9;  // instantiated row counts
+            return true;
+        }
+    }
+    return false;
 }
 
-template <int R>
+template <int R, int T>
 void launch_rblk_t(Ctx& c, int64_t m, int64_t n, double* U, int64_t ldu, double tol, int* counters,
                    int* sweeps_out) {
     int nb = int((n + RB - 1) / RB);
     int npb = 0;
     const int2* bp = device_pairs(nb, npb);
     int per_sm = 0;
-    HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_rblk_k<R>, RT, 0));
+    HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_rblk_k<R, T>, T, 0));
     int grid = std::max(1, std::min(npb / 2, per_sm * c.num_sms));
     int64_t mm = m;
     int nn = int(n), nbb = nb;
     void* args[] = {&mm, &nn, &nbb, &bp, &U, &ldu, &tol, &counters, &sweeps_out};
-    HYDOT_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_rblk_k<R>, dim3(grid), dim3(RT), args, 0, c.stream));
+    HYDOT_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_rblk_k<R, T>, dim3(grid), dim3(T), args, 0, c.stream));
     c.count();
 }
 
-void launch_rblk(Ctx& c, int R, int64_t m, int64_t n, double* U, int64_t ldu, double tol, int* counters,
-                 int* sweeps_out) {
+template <int T>
+void launch_rblk_r(Ctx& c, int R, int64_t m, int64_t n, double* U, int64_t ldu, double tol, int* counters,
+                   int* sweeps_out) {
     switch (R) {
-        case 1: launch_rblk_t<1>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
-        case 2: launch_rblk_t<2>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
-        case 3: launch_rblk_t<3>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
-        case 4: launch_rblk_t<4>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
-        default: launch_rblk_t<5>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
+        case 3: launch_rblk_t<3, T>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
+        case 5: launch_rblk_t<5, T>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
+        case 7: launch_rblk_t<(T == 512 ? 5 : 7), T>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
+        default: launch_rblk_t<(T == 512 ? 5 : 9), T>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
+    }
+}
+
+void launch_rblk(Ctx& c, int R, int T, int64_t m, int64_t n, double* U, int64_t ldu, double tol,
+                 int* counters, int* sweeps_out) {
+    switch (T) {
+        case 64: launch_rblk_r<64>(c, R, m, n, U, ldu, tol, counters, sweeps_out); break;
+        case 128: launch_rblk_r<128>(c, R, m, n, U, ldu, tol, counters, sweeps_out); break;
+        case 256: launch_rblk_r<256>(c, R, m, n, U, ldu, tol, counters, sweeps_out); break;
+        default: launch_rblk_r<512>(c, R, m, n, U, ldu, tol, counters, sweeps_out); break;
     }
 }
 
@@ -798,9 +817,10 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
         jacobi_smem_k<<<1, 1024, smem, c.stream>>>(int(m), int(n), np, dpairs, U.d(), m, V.d(), n,
                                                     tol, atol, sw.as<int>() + kMaxSweeps);
         c.check_launch();
-    } else if (n >= 2 && !strict_svd_flag() && lazy_v_enabled() && atol == 0.0 && rblk_rows(m, n) > 0) {
+    } else if (int rbR = 0, rbT = 0; n >= 2 && !strict_svd_flag() && lazy_v_enabled() && atol == 0.0 &&
+                                     rblk_shape(m, n, rbR, rbT)) {
         lazy_v = true;
-        launch_rblk(c, rblk_rows(m, n), m, n, U.d(), m, tol, sw.as<int>(), sw.as<int>() + kMaxSweeps);
+        launch_rblk(c, rbR, rbT, m, n, U.d(), m, tol, sw.as<int>(), sw.as<int>() + kMaxSweeps);
     } else if (use_block_jacobi(m, n)) {
         set_identity(c, n, n, V.d(), n);
         launch_block_jacobi(c, m, n, U.d(), m, V.d(), n, tol, atol, sw.as<int>(),
