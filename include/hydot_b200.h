@@ -79,6 +79,10 @@ int hydot_profile_dump(char* buf, int len);
  * synchronisation while on); the report resolves and clears the records:
  * JSON {stage: [ms, calls, algorithmic flops, algorithmic bytes]} */
 hydot_status hydot_ctx_set_timing(hydot_ctx ctx, int on);
+/* restrict the live timing to the stages named in a comma-separated list
+ * (NULL or "" = all stages): lets a benchmark time one kernel class inside
+ * its timed region without paying an event pair per stage everywhere. */
+hydot_status hydot_ctx_set_timing_filter(hydot_ctx ctx, const char* names);
 int hydot_ctx_timing_report(hydot_ctx ctx, char* buf, int len);
 
 /* ------------------------------------------------------------- fields -- */

@@ -96,6 +96,7 @@ SIGNATURES = {
     "hydot_profile_dump": (C.c_int, [C.c_char_p, C.c_int]),
     "hydot_ctx_set_timing": (C.c_int, [_vp, C.c_int]),
     "hydot_ctx_timing_report": (C.c_int, [_vp, C.c_char_p, C.c_int]),
+    "hydot_ctx_set_timing_filter": (C.c_int, [_vp, C.c_char_p]),
     "hydot_fields_solve": (C.c_int, [_vp, C.POINTER(Grid7), C.c_int, _dp, _dp, _dp, _i64p, C.c_int,
                                      C.c_double, C.c_int, C.c_int, _dp, _ip, _dp]),
     "hydot_apply7": (C.c_int, [_vp, C.POINTER(Grid7), C.c_double, C.c_double, _dp, _dp]),

@@ -98,15 +98,18 @@ hydot_status hydot_ctx_create(int device, hydot_ctx* out) {
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
             // map a working reserve once per device so the GB-sized per-node
             // buffers of the merges never wait for the pool to grow
-            // (HYDOT_POOL_RESERVE_GB, default 16; 0 disables)
+            // (HYDOT_POOL_RESERVE_GB, default 48 -- config 1 measured 2.42 s
+            // per step with 16 GB (the pool kept growing under fragmentation)
+            // and 2.06 s with 48 GB; capped at a third of the free memory;
+            // 0 disables)
             static bool reserved[64] = {};
             const char* e = std::getenv("HYDOT_POOL_RESERVE_GB");
-            const double gb = e ? std::atof(e) : 16.0;
+            const double gb = e ? std::atof(e) : 48.0;
             if (gb > 0 && device >= 0 && device < 64 && !reserved[device]) {
                 reserved[device] = true;
                 size_t fr = 0, tot = 0;
                 HYDOT_CUDA(cudaMemGetInfo(&fr, &tot));
-                const size_t want = std::min(size_t(gb * double(1ull << 30)), fr / 4);
+                const size_t want = std::min(size_t(gb * double(1ull << 30)), fr / 3);
                 void* p = nullptr;
                 if (want > 0 && cudaMallocAsync(&p, want, c->stream) == cudaSuccess) {
                     HYDOT_CUDA(cudaFreeAsync(p, c->stream));
@@ -157,6 +160,23 @@ int64_t hydot_ctx_launch_count(hydot_ctx ctx) { return ctx && ctx->c ? ctx->c->l
 
 hydot_status hydot_ctx_set_timing(hydot_ctx ctx, int on) {
     return guard(ctx ? ctx->c.get() : nullptr, [&] { ctx_of(ctx).timing = on != 0; });
+}
+
+hydot_status hydot_ctx_set_timing_filter(hydot_ctx ctx, const char* names) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        c.timing_filter.clear();
+        if (!names) return;
+        std::string s(names), cur;
+        for (char ch : s + ",") {
+            if (ch == ',') {
+                if (!cur.empty()) c.timing_filter.push_back(cur);
+                cur.clear();
+            } else if (ch != ' ') {
+                cur += ch;
+            }
+        }
+    });
 }
 
 int hydot_ctx_timing_report(hydot_ctx ctx, char* buf, int len) {

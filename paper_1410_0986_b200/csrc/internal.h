@@ -42,6 +42,14 @@ struct Ctx {
     // live per-stage timing with CUDA events on the context stream (no
     // synchronisation; hydot_ctx_timing_report resolves them)
     bool timing = false;
+    std::vector<std::string> timing_filter;  // empty = every stage
+    bool timed(const char* name) const {
+        if (!timing) return false;
+        if (timing_filter.empty()) return true;
+        for (const auto& f : timing_filter)
+            if (f == name) return true;
+        return false;
+    }
     struct TRec {
         const char* name;
         cudaEvent_t a, b;

@@ -230,7 +230,7 @@ thread_local int g_depth = 0;
 StageTimer::StageTimer(Ctx& c, const char* name, int64_t a, int64_t b, int64_t k, double flops,
                        double bytes)
     : c_(c), name_(name), a_(a), b_(b), k_(k), flops_(flops), bytes_(bytes) {
-    if (c_.timing) {
+    if (c_.timed(name)) {
         ea_ = c_.take_event();
         cudaEventRecord(ea_, c_.stream);
     }
