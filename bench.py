@@ -212,11 +212,13 @@ def run_b200(args):
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("hydot_timed")  # ncu --nvtx-include hydot_timed/ captures this region
     e0.record(stream)
     for _ in range(args.steps):
         rec, fr = step(prov)
     e1.record(stream)
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
