@@ -216,14 +216,45 @@ __global__ void __launch_bounds__(Tile<BM, BN, WM, WN>::NT, Tile<BM, BN, WM, WN>
             }
 }
 
-__global__ void splitk_reduce(int64_t M, int64_t N, int splits, const double* __restrict__ ws,
-                              double* __restrict__ C, int64_t ldc, double alpha, double beta) {
-    int64_t total = M * N;
+// sum the split-K slices in a fixed order: threadIdx.x over 32 consecutive
+// elements (coalesced), threadIdx.y over z-slices, then a fixed-order
+// shared-memory combine -- a long serial load chain per element was the
+// reduce's cost when one GEMM had hundreds of slices
+constexpr int RZ = 8;
+__global__ void __launch_bounds__(32 * RZ) splitk_reduce(int64_t M, int64_t N, int splits,
+                                                         const double* __restrict__ ws,
+                                                         double* __restrict__ C, int64_t ldc,
+                                                         double alpha, double beta) {
+    __shared__ double part[RZ][33];
+    const int64_t total = M * N;
+    for (int64_t e0 = blockIdx.x * int64_t(32); e0 < total; e0 += int64_t(gridDim.x) * 32) {
+        const int64_t e = e0 + threadIdx.x;
+        double s = 0.0;
+        if (e < total)
+            for (int z = threadIdx.y; z < splits; z += RZ) s += ws[int64_t(z) * total + e];
+        part[threadIdx.y][threadIdx.x] = s;
+        __syncthreads();
+        if (threadIdx.y == 0 && e < total) {
+            double t = 0.0;
+#pragma unroll
+            for (int y = 0; y < RZ; ++y) t += part[y][threadIdx.x];
+            const int64_t r = e % M, cc = e / M;
+            double* cp = C + r + cc * ldc;
+            *cp = beta == 0.0 ? alpha * t : alpha * t + beta * *cp;
+        }
+        __syncthreads();
+    }
+}
+
+// few slices: one thread per element
+__global__ void splitk_reduce_1d(int64_t M, int64_t N, int splits, const double* __restrict__ ws,
+                                 double* __restrict__ C, int64_t ldc, double alpha, double beta) {
+    const int64_t total = M * N;
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
          e += int64_t(gridDim.x) * blockDim.x) {
         double s = 0.0;
         for (int z = 0; z < splits; ++z) s += ws[int64_t(z) * total + e];
-        int64_t r = e % M, cc = e / M;
+        const int64_t r = e % M, cc = e / M;
         double* cp = C + r + cc * ldc;
         *cp = beta == 0.0 ? alpha * s : alpha * s + beta * *cp;
     }
@@ -250,6 +281,7 @@ void run_tiles(Ctx& c, bool ta, bool tb, int64_t m, int64_t n, int64_t k, double
     if (tiles < target) {
         splits = (target + tiles - 1) / tiles;
         splits = std::min<int64_t>(splits, (k + 255) / 256);  // >= 256 k per slice
+        splits = std::min<int64_t>(splits, 128);
         int64_t cap = (int64_t(512) << 20) / (8 * m * n);     // workspace <= 512 MB
         splits = std::max<int64_t>(1, std::min(splits, std::max<int64_t>(cap, 1)));
     }
@@ -284,10 +316,14 @@ void run_tiles(Ctx& c, bool ta, bool tb, int64_t m, int64_t n, int64_t k, double
     else if (ta && !tb) launch(dgemm_kernel<true, false, BM, BN, WM, WN>);
     else launch(dgemm_kernel<true, true, BM, BN, WM, WN>);
     c.check_launch();
-    if (splits > 1) {
+    if (splits > 8) {
+        int blocks = int(std::min<int64_t>((m * n + 31) / 32, int64_t(c.num_sms) * 16));
+        splitk_reduce<<<blocks, dim3(32, RZ), 0, c.stream>>>(m, n, int(splits), ws.d(), C, ldc, alpha,
+                                                             beta);
+        c.check_launch();
+    } else if (splits > 1) {
         int blocks = int(std::min<int64_t>((m * n + 255) / 256, int64_t(c.num_sms) * 8));
-        splitk_reduce<<<blocks, 256, 0, c.stream>>>(m, n, int(splits), ws.d(), C, ldc, alpha,
-                                                    beta);
+        splitk_reduce_1d<<<blocks, 256, 0, c.stream>>>(m, n, int(splits), ws.d(), C, ldc, alpha, beta);
         c.check_launch();
     }
 }

@@ -270,29 +270,71 @@ __global__ void form_v(int64_t mr, int jb, const double* __restrict__ P, int64_t
     }
 }
 
-// dlarft (forward, columnwise): T upper triangular jb x jb (ld NB) from
-// G = V^T V and tau.
-__global__ void __launch_bounds__(NB) larft_k(int jb, const double* __restrict__ G, int64_t ldg,
-                                              const double* __restrict__ tau,
-                                              double* __restrict__ T) {
-    extern __shared__ double Ts[];  // NB x (NB+1)
-    __shared__ double wv[NB];
-    const int r = threadIdx.x;
+// dlarft (forward, columnwise): T upper triangular jb x jb (ld NB) with
+// H_0 ... H_{jb-1} = I - V T V^T, from G = V^T V and tau.  The 32 x 32
+// diagonal blocks follow LAPACK's column recurrence (one warp per block, in
+// parallel); they are then joined by the compact-WY merge
+//   T = [[T1, -T1 (V1^T V2) T2], [0, T2]]
+// at widths 32 -> 64 -> 128 with small shared-memory products.
+constexpr int LT = 512;
+__global__ void __launch_bounds__(LT) larft_k(int jb, const double* __restrict__ G, int64_t ldg,
+                                              const double* __restrict__ tau, double* __restrict__ T) {
+    extern __shared__ double Ts[];  // NB x (NB+1): T
+    double* X = Ts + NB * (NB + 1);  // (NB/2) x (NB/2 + 1): merge scratch
     auto t = [&](int i, int j) -> double& { return Ts[i * (NB + 1) + j]; };
-    for (int j = 0; j < jb; ++j) t(r, j) = 0.0;
+    constexpr int XL = NB / 2 + 1;
+    for (int e = threadIdx.x; e < NB * (NB + 1); e += LT) Ts[e] = 0.0;
     __syncthreads();
-    for (int i = 0; i < jb; ++i) {
-        if (r < i) wv[r] = -tau[i] * G[r + int64_t(i) * ldg];
-        __syncthreads();
-        if (r < i) {
-            double s = 0.0;
-            for (int q = r; q < i; ++q) s += t(r, q) * wv[q];
-            t(r, i) = s;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // ---- diagonal 32-blocks: warp w owns columns [32w, 32w+32)
+    {
+        const int b0 = warp * 32;
+        if (b0 < jb) {
+            const int bn = min(32, jb - b0);
+            const int r = b0 + lane;  // this lane's row
+            for (int ii = 0; ii < bn; ++ii) {
+                const int i = b0 + ii;
+                // t(r, i) = sum_{q=r}^{i-1} t(r, q) * (-tau_i G(q, i)),  r < i in the block
+                double s = 0.0;
+                if (lane < ii) {
+                    const double ti = -tau[i];
+                    for (int q = r; q < i; ++q) s += t(r, q) * (ti * G[q + int64_t(i) * ldg]);
+                }
+                __syncwarp();
+                if (lane < ii) t(r, i) = s;
+                if (lane == ii) t(i, i) = tau[i];
+                __syncwarp();
+            }
         }
-        if (r == i) t(i, i) = tau[i];
-        __syncthreads();
     }
-    for (int j = 0; j < jb; ++j) T[r + int64_t(j) * NB] = t(r, j);  // only jb columns exist
+    __syncthreads();
+    // ---- merges: width w blocks (w = 32, 64) pairwise into 2w
+    for (int w = 32; w < jb; w *= 2) {
+        for (int a0 = 0; a0 + w < jb; a0 += 2 * w) {
+            const int b0 = a0 + w;
+            const int na = w, nb = min(w, jb - b0);
+            // X = G(a-block, b-block) * T2   (na x nb)
+            for (int e = threadIdx.x; e < na * nb; e += LT) {
+                const int i = e % na, j = e / na;
+                double s = 0.0;
+                for (int q = 0; q <= j; ++q) s += G[(a0 + i) + int64_t(b0 + q) * ldg] * t(b0 + q, b0 + j);
+                X[i * XL + j] = s;
+            }
+            __syncthreads();
+            // T12 = -T1 * X   (T1 upper triangular na x na)
+            for (int e = threadIdx.x; e < na * nb; e += LT) {
+                const int i = e % na, j = e / na;
+                double s = 0.0;
+                for (int q = i; q < na; ++q) s += t(a0 + i, a0 + q) * X[q * XL + j];
+                t(a0 + i, b0 + j) = -s;
+            }
+            __syncthreads();
+        }
+    }
+    for (int e = threadIdx.x; e < NB * jb; e += LT) {
+        const int r = e % NB, j = e / NB;
+        T[r + int64_t(j) * NB] = t(r, j);  // only jb columns exist
+    }
 }
 
 void panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, const PanelBufs& pbuf) {
@@ -349,12 +391,12 @@ void form_v_launch(Ctx& c, int64_t mr, int jb, const double* P, int64_t ld, doub
 
 void larft(Ctx& c, int jb, const double* G, int64_t ldg, const double* tau, double* T) {
     static bool attr = false;
-    const int smem = NB * (NB + 1) * sizeof(double);
+    const int smem = (NB * (NB + 1) + (NB / 2) * (NB / 2 + 1)) * sizeof(double);
     if (!attr) {
         HYDOT_CUDA(cudaFuncSetAttribute(larft_k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;
     }
-    larft_k<<<1, NB, smem, c.stream>>>(jb, G, ldg, tau, T);
+    larft_k<<<1, LT, smem, c.stream>>>(jb, G, ldg, tau, T);
     c.check_launch();
 }
 
