@@ -300,27 +300,39 @@ __global__ void rng_prefix_k(uint64_t seed, uint64_t* __restrict__ zout) {
     for (int i = threadIdx.x; i < mt::PREFIX; i += blockDim.x) zout[i] = z[i];
 }
 
-// window of chunk c: w[j] = xor_{i : g_c[i]} z[i+j]
-__global__ void rng_jump_k(const uint64_t* __restrict__ zpre, const uint64_t* __restrict__ gtab,
-                           int64_t c0, uint64_t* __restrict__ windows) {
+// window of chunk c: w[j] = xor_{i : g_c[i]} z[i+j].  Branch-free GF(2)
+// product: thread (chunk, jj) owns w[4jj .. 4jj+3]; for every 64-bit word of
+// g_c it walks the 67 words z[64w + 4jj + b] once and applies all 64 bits as
+// masks to the 4 accumulators (no data-dependent loop, 4x reuse of each
+// shared-memory load).  One CTA serves JCH chunks from the same prefix.
+constexpr int JK = 4;                 // window words per thread
+constexpr int JPC = mt::NW / JK;      // threads per chunk (78)
+constexpr int JCH = 4;                // chunks per CTA
+__global__ void __launch_bounds__(JPC * JCH) rng_jump_k(const uint64_t* __restrict__ zpre,
+                                                        const uint64_t* __restrict__ gtab, int64_t c0,
+                                                        int64_t nc, uint64_t* __restrict__ windows) {
     extern __shared__ uint64_t z[];
     for (int i = threadIdx.x; i < mt::PREFIX; i += blockDim.x) z[i] = zpre[i];
     __syncthreads();
-    const int64_t c = c0 + blockIdx.x;
-    const int j = threadIdx.x;
-    if (j >= mt::NW) return;
-    const uint64_t* g = gtab + c * mt::PW;
-    uint64_t acc = 0;
+    const int lc = threadIdx.x / JPC, jj = threadIdx.x % JPC;
+    const int64_t ci = int64_t(blockIdx.x) * JCH + lc;  // chunk index within this call
+    if (ci >= nc) return;
+    const uint64_t* g = gtab + (c0 + ci) * mt::PW;
+    const int j0 = jj * JK;
+    uint64_t acc[JK] = {0, 0, 0, 0};
     for (int w = 0; w < mt::PW; ++w) {
-        uint64_t bits = g[w];
-        const uint64_t* zp = z + 64 * w + j;
-        while (bits) {
-            int b = __ffsll(static_cast<long long>(bits)) - 1;
-            acc ^= zp[b];
-            bits &= bits - 1;
+        const uint64_t bits = __ldg(g + w);
+        if (bits == 0) continue;
+        const uint64_t* zp = z + 64 * w + j0;
+#pragma unroll 16
+        for (int b = 0; b < 64; ++b) {
+            const uint64_t m = 0ULL - ((bits >> b) & 1ULL);
+#pragma unroll
+            for (int t = 0; t < JK; ++t) acc[t] ^= zp[b + t] & m;
         }
     }
-    windows[int64_t(blockIdx.x) * mt::NW + j] = acc;
+#pragma unroll
+    for (int t = 0; t < JK; ++t) windows[ci * mt::NW + j0 + t] = acc[t];
 }
 
 __device__ __forceinline__ bool polar_accept(uint64_t r1, uint64_t r2, double& x, double& y,
@@ -462,8 +474,8 @@ void RngStream::generate_chunks(int64_t c_end) {
     DBuf raw(c_, size_t(nc) * size_t(mt::S) * 8);
     DBuf counts(c_, size_t(nc) * sizeof(int));
     DBuf offs(c_, size_t(nc) * sizeof(int64_t));
-    rng_jump_k<<<unsigned(nc), 320, size_t(mt::PREFIX) * 8, c_.stream>>>(
-        prefix_.as<uint64_t>(), jumps, c0, windows.as<uint64_t>());
+    rng_jump_k<<<unsigned((nc + JCH - 1) / JCH), JPC * JCH, size_t(mt::PREFIX) * 8, c_.stream>>>(
+        prefix_.as<uint64_t>(), jumps, c0, nc, windows.as<uint64_t>());
     c_.check_launch();
     rng_generate_k<<<unsigned(nc), 160, 0, c_.stream>>>(windows.as<uint64_t>(), raw.as<uint64_t>(),
                                                         counts.as<int>());
@@ -526,8 +538,8 @@ void RngStream::raw(int64_t offset, int64_t count, uint64_t* out) {
     DBuf windows(c_, size_t(nc) * mt::NW * 8);
     DBuf rawb(c_, size_t(nc) * size_t(mt::S) * 8);
     DBuf counts(c_, size_t(nc) * sizeof(int));
-    rng_jump_k<<<unsigned(nc), 320, size_t(mt::PREFIX) * 8, c_.stream>>>(
-        prefix_.as<uint64_t>(), jumps, cb, windows.as<uint64_t>());
+    rng_jump_k<<<unsigned((nc + JCH - 1) / JCH), JPC * JCH, size_t(mt::PREFIX) * 8, c_.stream>>>(
+        prefix_.as<uint64_t>(), jumps, cb, nc, windows.as<uint64_t>());
     c_.check_launch();
     rng_generate_k<<<unsigned(nc), 160, 0, c_.stream>>>(windows.as<uint64_t>(),
                                                         rawb.as<uint64_t>(), counts.as<int>());
