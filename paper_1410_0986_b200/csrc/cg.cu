@@ -15,6 +15,8 @@
 // stencil and the vector updates use explicit _rn intrinsics in the oracle's
 // operation order (no FMA contraction), so only the dot-product summation
 // order differs from the CPU restatement.
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace hydot {
@@ -50,41 +52,55 @@ __device__ __forceinline__ void fdivmod(unsigned i, unsigned d, float inv_d, uns
     r = unsigned(rr);
 }
 
-// y_i = (A x)_i with x(j) supplied by a functor; reference operation order
+// y_i = (A x)_i with x(j) supplied by a functor; reference operation order.
+// Branch-free: every neighbour is loaded from a clamped in-range index and
+// masked by a select, so the compiler can issue all loads of the unrolled
+// vertices before their first use (the branchy form stalled on each load).
+// The masked terms add +0.0, leaving every sum as in the reference order.
 template <class Get>
 __device__ __forceinline__ double stencil_at(const Stencil& g, double sigma, double sigmap,
                                              int64_t i, Get get) {
     const int64_t plane = int64_t(g.nx) * g.ny;
+    const int64_t N = plane * g.nz;
     unsigned q1, ux, uy, uz;
     fdivmod(unsigned(i), unsigned(g.nx), g.inv_nx, q1, ux);
     fdivmod(q1, unsigned(g.ny), g.inv_ny, uz, uy);
     const int ix = int(ux), iy = int(uy), iz = int(uz);
     const double xi = get(i);
-    if (ix == 0 || ix == g.nx - 1 || iy == 0 || iy == g.ny - 1) return xi;
+    const bool dir = (ix == 0 || ix == g.nx - 1 || iy == 0 || iy == g.ny - 1);
+    const bool bxm = ix - 1 > 0, bxp = ix + 1 < g.nx - 1, bym = iy - 1 > 0, byp = iy + 1 < g.ny - 1;
+    const bool bzm = iz > 0, bzp = iz < g.nz - 1;
+    const double vxm = get(i > 0 ? i - 1 : i);
+    const double vxp = get(i + 1 < N ? i + 1 : i);
+    const double vym = get(i >= g.nx ? i - g.nx : i);
+    const double vyp = get(i + g.nx < N ? i + g.nx : i);
+    const double vzm = get(i >= plane ? i - plane : i);
+    const double vzp = get(i + plane < N ? i + plane : i);
     const double h = g.h;
     const bool zb = (iz == 0 || iz == g.nz - 1);
     const double zext = zb ? 0.5 * h : h;
     const double V = __dmul_rn(__dmul_rn(h, h), zext);
     const double S = zb ? __dmul_rn(h, h) : 0.0;
-    const double xm = ix - 1 > 0 ? get(i - 1) : 0.0;
-    const double xp = ix + 1 < g.nx - 1 ? get(i + 1) : 0.0;
-    const double ym = iy - 1 > 0 ? get(i - g.nx) : 0.0;
-    const double yp = iy + 1 < g.ny - 1 ? get(i + g.nx) : 0.0;
+    const double xm = bxm ? vxm : 0.0;
+    const double xp = bxp ? vxp : 0.0;
+    const double ym = bym ? vym : 0.0;
+    const double yp = byp ? vyp : 0.0;
     double wsum = 4.0 * zext;
     double nb = __dmul_rn(zext, xm);
     nb = __dadd_rn(nb, __dmul_rn(zext, xp));
     nb = __dadd_rn(nb, __dmul_rn(zext, ym));
     nb = __dadd_rn(nb, __dmul_rn(zext, yp));
-    if (iz > 0) {
+    if (bzm) {
         wsum = __dadd_rn(wsum, h);
-        nb = __dadd_rn(nb, __dmul_rn(h, get(i - plane)));
+        nb = __dadd_rn(nb, __dmul_rn(h, vzm));
     }
-    if (iz < g.nz - 1) {
+    if (bzp) {
         wsum = __dadd_rn(wsum, h);
-        nb = __dadd_rn(nb, __dmul_rn(h, get(i + plane)));
+        nb = __dadd_rn(nb, __dmul_rn(h, vzp));
     }
     const double diag = __dadd_rn(__dadd_rn(wsum, __dmul_rn(sigma, V)), __dmul_rn(sigmap, S));
-    return __dsub_rn(__dmul_rn(diag, xi), nb);
+    const double y = __dsub_rn(__dmul_rn(diag, xi), nb);
+    return dir ? xi : y;
 }
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
@@ -143,7 +159,7 @@ __global__ void cg_init(int64_t N, int nl, const int64_t* __restrict__ rhs_verte
     }
 }
 
-__global__ void __launch_bounds__(CT) cg_pa(Stencil g, int64_t N, int nl, int k0, int it,
+__global__ void __launch_bounds__(CT, 4) cg_pa(Stencil g, int64_t N, int nl, int k0, int it,
                                             const double* __restrict__ sig,
                                             const double* __restrict__ sigp,
                                             const double* __restrict__ R,
@@ -202,7 +218,7 @@ __global__ void __launch_bounds__(CT) cg_pa(Stencil g, int64_t N, int nl, int k0
     if (threadIdx.x == 0) partA[int64_t(sys) * nparts + blockIdx.x] = t;
 }
 
-__global__ void __launch_bounds__(CT) cg_xr(Stencil g, int64_t N, int nl, int k0, int it,
+__global__ void __launch_bounds__(CT, 4) cg_xr(Stencil g, int64_t N, int nl, int k0, int it,
                                             const double* __restrict__ sig,
                                             const double* __restrict__ sigp,
                                             double* __restrict__ X, double* __restrict__ R,
@@ -316,9 +332,20 @@ void fields_solve(Ctx& c, const hydot_grid7& g, int nl, const double* sigma,
         throw std::invalid_argument("fields_solve: grid too large for the 24-bit vertex decode");
     const int total = n_rhs * nl;
     const int nparts = int((N + CV - 1) / CV);
-    // batch so that r and p stay under ~24 GB
+    // One batch of up to 24 GB (all systems iterate together, HBM-bound).
+    // HYDOT_CG_L2_MB > 0 instead iterates L2-sized groups (32 N bytes per
+    // system): measured slower on config 1 (1.4-2.8 s vs 0.96 s -- small
+    // groups make the iterations launch- and sync-bound), kept for experiments.
+    // A z-marching shared-memory stencil (one CTA per x-y tile walking z)
+    // also measured slower (1.35 s: one plane of loads in flight per CTA).
+    static const int l2_mb = [] {
+        const char* e = std::getenv("HYDOT_CG_L2_MB");
+        return e ? std::atoi(e) : 0;
+    }();
     int64_t per_sys = 2 * N * 8;
     int batch = int(std::max<int64_t>(1, std::min<int64_t>(total, (int64_t(24) << 30) / per_sys)));
+    if (l2_mb > 0)
+        batch = int(std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t(l2_mb) << 20) / (4 * per_sys))));
     batch = std::min(batch, 65535);
     DBuf dsig = dalloc(c, size_t(nl)), dsigp = dalloc(c, size_t(nl)), dinv = dalloc(c, size_t(nl));
     HYDOT_CUDA(cudaMemcpyAsync(dsig.d(), sigma, size_t(nl) * 8, cudaMemcpyHostToDevice, c.stream));
