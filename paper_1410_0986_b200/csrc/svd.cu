@@ -86,16 +86,20 @@ __global__ void __launch_bounds__(1024) jacobi_smem_k(int m, int n, int np,
                                                       double* __restrict__ Vg, int64_t ldv,
                                                       double tol, double atol,
                                                       int* __restrict__ sweeps_out) {
+    // Vg == nullptr: lazy V (only U lives in shared memory, V is recovered
+    // by the caller's GEMM) -- lets n up to ~160 run on one SM
     extern __shared__ double sm[];
+    const bool withV = Vg != nullptr;
+    const int vn = withV ? n : 0;
     double* U = sm;                   // m x n, ld m
-    double* V = sm + int64_t(m) * n;  // n x n, ld n
+    double* V = sm + int64_t(m) * n;  // n x n, ld n (withV)
     __shared__ int changed;
     for (int64_t e = threadIdx.x; e < int64_t(m) * n; e += blockDim.x) {
         int64_t i = e % m, j = e / m;
         U[e] = Ug[i + j * ldu];
     }
-    for (int64_t e = threadIdx.x; e < int64_t(n) * n; e += blockDim.x) {
-        int64_t i = e % n, j = e / n;
+    for (int64_t e = threadIdx.x; e < int64_t(vn) * vn; e += blockDim.x) {
+        int64_t i = e % vn, j = e / vn;
         V[e] = (i == j) ? 1.0 : 0.0;
     }
     __syncthreads();
@@ -109,8 +113,8 @@ __global__ void __launch_bounds__(1024) jacobi_smem_k(int m, int n, int np,
             for (int q = warp; q < per; q += nwarp) {
                 int2 pr = pairs[r * per + q];
                 if (pr.x >= n || pr.y >= n) continue;
-                if (warp_pair(lane, m, n, U + int64_t(pr.x) * m, U + int64_t(pr.y) * m,
-                              V + int64_t(pr.x) * n, V + int64_t(pr.y) * n, tol, atol) &&
+                if (warp_pair(lane, m, vn, U + int64_t(pr.x) * m, U + int64_t(pr.y) * m,
+                              V + int64_t(pr.x) * vn, V + int64_t(pr.y) * vn, tol, atol) &&
                     lane == 0)
                     changed = 1;
             }
@@ -123,8 +127,8 @@ __global__ void __launch_bounds__(1024) jacobi_smem_k(int m, int n, int np,
         int64_t i = e % m, j = e / m;
         Ug[i + j * ldu] = U[e];
     }
-    for (int64_t e = threadIdx.x; e < int64_t(n) * n; e += blockDim.x) {
-        int64_t i = e % n, j = e / n;
+    for (int64_t e = threadIdx.x; e < int64_t(vn) * vn; e += blockDim.x) {
+        int64_t i = e % vn, j = e / vn;
         Vg[i + j * ldv] = V[e];
     }
     if (threadIdx.x == 0 && sweeps_out) *sweeps_out = sweep;
@@ -807,6 +811,8 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
     HYDOT_CUDA(cudaMemsetAsync(sw.as<void>(), 0, sizeof(int) * (kMaxSweeps + 1), c.stream));
     bool lazy_v = false;
     const size_t smem = size_t((m + n) * n) * sizeof(double);
+    // (a U-only single-CTA variant for 110 < n <= 160 measured 2x slower
+    // than the multi-SM block driver: one SM's FP64 rate bounds each round)
     if (n >= 2 && smem <= 200 * 1024) {
         static bool attr = false;
         if (!attr) {
