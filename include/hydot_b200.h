@@ -272,6 +272,28 @@ hydot_status hydot_dgemm(hydot_ctx ctx, int transa, int transb, int64_t m, int64
                          double alpha, const double* A_dev, int64_t lda, const double* B_dev,
                          int64_t ldb, double beta, double* C_dev, int64_t ldc);
 
+/* ------------------------------------------------------------ file I/O -- */
+/* save_factor / load_factor (lowrank.hpp:165-167, lowrank.cpp:601-655): the
+ * reference's binary factor file -- int64 rows, cols, rank; float64 tol;
+ * int64 method; int64 plen and plen int64 row_perm; U then V row-major.
+ * Errors: HYDOT_ERUNTIME with "cannot write factor: ", "cannot read
+ * factor: ", "corrupt factor file: ", "truncated factor file: " + path. */
+hydot_status hydot_factor_save(hydot_ctx ctx, hydot_factor f, const int* row_perm_h, int64_t plen,
+                               const char* path);
+hydot_status hydot_factor_file_info(const char* path, int64_t* rows, int64_t* cols, int64_t* rank,
+                                    int64_t* plen);
+/* row_perm_h (perm_cap ints, may be NULL) receives the stored permutation */
+hydot_status hydot_factor_load(hydot_ctx ctx, const char* path, hydot_factor* out, int* row_perm_h,
+                               int64_t perm_cap);
+/* save_block / load_block (born.hpp:85-86, born.cpp:156-185): float64 rows,
+ * cols, then the block row-major.  The device block is row-major with row
+ * stride ld (the layout hydot_born_block writes). */
+hydot_status hydot_block_save(hydot_ctx ctx, const double* block_dev, int64_t rows, int64_t cols,
+                              int64_t ld, const char* path);
+hydot_status hydot_block_file_info(const char* path, int64_t* rows, int64_t* cols);
+hydot_status hydot_block_load(hydot_ctx ctx, const char* path, double* block_dev, int64_t ld,
+                              int64_t* rows, int64_t* cols);
+
 /* ---------------------------------------------------------------- pals -- */
 /* Parametric level-set reconstruction, the caller of the compressed
  * operator: proj/include/hydot/pals.hpp, src/pals.cpp.

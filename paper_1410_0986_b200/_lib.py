@@ -149,6 +149,12 @@ SIGNATURES = {
     "hydot_pals_reconstruct": (C.c_int, [_vp, C.POINTER(Hop), C.POINTER(GridGeom), _dp, C.c_int,
                                          C.c_int, _dp, _dp, C.POINTER(PalsParams), C.c_double,
                                          C.POINTER(ReconConfig), _dp, C.POINTER(ReconResultC)]),
+    "hydot_factor_save": (C.c_int, [_vp, _vp, _ip, C.c_int64, C.c_char_p]),
+    "hydot_factor_file_info": (C.c_int, [C.c_char_p, _i64p, _i64p, _i64p, _i64p]),
+    "hydot_factor_load": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp), _ip, C.c_int64]),
+    "hydot_block_save": (C.c_int, [_vp, _dp, C.c_int64, C.c_int64, C.c_int64, C.c_char_p]),
+    "hydot_block_file_info": (C.c_int, [C.c_char_p, _i64p, _i64p]),
+    "hydot_block_load": (C.c_int, [_vp, C.c_char_p, _dp, C.c_int64, _i64p, _i64p]),
 }
 
 _LIB = None

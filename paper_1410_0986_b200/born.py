@@ -9,6 +9,7 @@ column-major Mat), a Born block is (n_det*n_lambda, N).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from typing import List, Sequence
 
@@ -111,3 +112,24 @@ def assemble_H_dense(ctx: Context, incident: List[torch.Tensor], adjoint: List[L
         assemble_H_block(ctx, incident[s], adjoint[s], lumped_w, nu,
                          out=H[s * nd * nl:(s + 1) * nd * nl])
     return H
+
+
+def save_block(ctx: Context, path: str, block: torch.Tensor) -> None:
+    """save_block (born.hpp:85, born.cpp:156-167) from a device block
+    (rows, cols) -- the (n_det*n_lambda) x N layout of assemble_H_block."""
+    if block.dim() != 2 or block.stride(1) != 1:
+        raise ValueError("save_block: expected a row-major 2-D tensor")
+    rows, cols = block.shape
+    check(lib().hydot_block_save(ctx.h, dptr(block), rows, cols, block.stride(0),
+                                 os.fsencode(path)), ctx.h)
+
+
+def load_block(ctx: Context, path: str) -> torch.Tensor:
+    """load_block (born.hpp:86, born.cpp:169-185) into device memory."""
+    rows, cols = C.c_int64(), C.c_int64()
+    check(lib().hydot_block_file_info(os.fsencode(path), C.byref(rows), C.byref(cols)), None)
+    out = ctx.empty(max(rows.value, 1), max(cols.value, 1))[:rows.value, :cols.value]
+    r2, c2 = C.c_int64(), C.c_int64()
+    check(lib().hydot_block_load(ctx.h, os.fsencode(path), dptr(out), max(cols.value, 1),
+                                 C.byref(r2), C.byref(c2)), ctx.h)
+    return out

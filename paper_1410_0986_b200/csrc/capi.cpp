@@ -730,4 +730,76 @@ hydot_status hydot_pals_reconstruct(hydot_ctx ctx, const hydot_hop* op, const hy
     });
 }
 
+// --------------------------------------------------------------- file I/O --
+hydot_status hydot_factor_save(hydot_ctx ctx, hydot_factor f, const int* row_perm_h, int64_t plen,
+                               const char* path) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!f || !path || plen < 0 || (plen > 0 && !row_perm_h))
+            throw std::invalid_argument("save_factor: bad arguments");
+        save_factor_file(c, path, f->f, row_perm_h, plen);
+    });
+}
+
+hydot_status hydot_factor_file_info(const char* path, int64_t* rows, int64_t* cols, int64_t* rank,
+                                    int64_t* plen) {
+    return guard(nullptr, [&] {
+        if (!path) throw std::invalid_argument("load_factor: null path");
+        int64_t m, n, r, p;
+        factor_file_info(path, m, n, r, p);
+        if (rows) *rows = m;
+        if (cols) *cols = n;
+        if (rank) *rank = r;
+        if (plen) *plen = p;
+    });
+}
+
+hydot_status hydot_factor_load(hydot_ctx ctx, const char* path, hydot_factor* out, int* row_perm_h,
+                               int64_t perm_cap) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!out || !path) throw std::invalid_argument("load_factor: bad arguments");
+        std::vector<int> perm;
+        Factor f = load_factor_file(c, path, perm);
+        if (row_perm_h) {
+            if (perm_cap < int64_t(perm.size())) throw std::invalid_argument("load_factor: row_perm buffer too small");
+            std::copy(perm.begin(), perm.end(), row_perm_h);
+        }
+        c.sync();
+        *out = wrap(ctx->c, std::move(f));
+    });
+}
+
+hydot_status hydot_block_save(hydot_ctx ctx, const double* block_dev, int64_t rows, int64_t cols,
+                              int64_t ld, const char* path) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!path || rows < 0 || cols < 0 || (rows > 0 && (!block_dev || ld < cols)))
+            throw std::invalid_argument("save_block: bad arguments");
+        save_block_file(c, path, block_dev, rows, cols, ld);
+    });
+}
+
+hydot_status hydot_block_file_info(const char* path, int64_t* rows, int64_t* cols) {
+    return guard(nullptr, [&] {
+        if (!path) throw std::invalid_argument("load_block: null path");
+        int64_t r, k;
+        block_file_info(path, r, k);
+        if (rows) *rows = r;
+        if (cols) *cols = k;
+    });
+}
+
+hydot_status hydot_block_load(hydot_ctx ctx, const char* path, double* block_dev, int64_t ld, int64_t* rows,
+                              int64_t* cols) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!path || !block_dev) throw std::invalid_argument("load_block: bad arguments");
+        int64_t r = 0, k = 0;
+        load_block_file(c, path, block_dev, ld, r, k);
+        if (rows) *rows = r;
+        if (cols) *cols = k;
+    });
+}
+
 }  // extern "C"

@@ -68,4 +68,13 @@ RecOut recursive_lowrank(Ctx& c, const Tree& t, double eps, int rows_per, int64_
                          const BlockFn& block, uint64_t seed, int p, int kprobe,
                          const std::vector<int>& source_ids = {}, int node_offset = 0);
 
+// fileio.cpp: the reference's factor / block file formats
+void save_factor_file(Ctx& c, const std::string& path, const Factor& f, const int* perm, int64_t plen);
+bool factor_file_info(const std::string& path, int64_t& rows, int64_t& cols, int64_t& rank, int64_t& plen);
+Factor load_factor_file(Ctx& c, const std::string& path, std::vector<int>& perm);
+void save_block_file(Ctx& c, const std::string& path, const double* block, int64_t rows, int64_t cols,
+                     int64_t ld);
+void block_file_info(const std::string& path, int64_t& rows, int64_t& cols);
+void load_block_file(Ctx& c, const std::string& path, double* block, int64_t ld, int64_t& rows, int64_t& cols);
+
 }  // namespace hydot

@@ -8,6 +8,7 @@ are read.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import Callable, List, Optional
 
@@ -434,3 +435,24 @@ def householder_qr(ctx: Context, A: torch.Tensor):
     Q = ctx.empty(n, m)
     check(lib().hydot_householder_qr(ctx.h, m, n, dptr(Acm), m, dptr(R), dptr(Q)), ctx.h)
     return Q.T, R.T
+
+
+def save_factor(path: str, f: LowRankFactor, row_perm=None) -> None:
+    """save_factor (lowrank.hpp:165-166, lowrank.cpp:601-621): the reference's
+    binary factor file, written from device memory."""
+    perm = np.ascontiguousarray([] if row_perm is None else row_perm, dtype=np.int32)
+    check(lib().hydot_factor_save(f.ctx.h, f.h, perm.ctypes.data_as(C.POINTER(C.c_int)),
+                                  len(perm), os.fsencode(path)), f.ctx.h)
+
+
+def load_factor(ctx: Context, path: str):
+    """load_factor (lowrank.hpp:167, lowrank.cpp:623-655) into device memory:
+    returns (LowRankFactor, row_perm int32 array)."""
+    rows, cols, rank, plen = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+    check(lib().hydot_factor_file_info(os.fsencode(path), C.byref(rows), C.byref(cols),
+                                       C.byref(rank), C.byref(plen)), None)
+    perm = np.zeros(max(plen.value, 1), dtype=np.int32)
+    h = C.c_void_p()
+    check(lib().hydot_factor_load(ctx.h, os.fsencode(path), C.byref(h),
+                                  perm.ctypes.data_as(C.POINTER(C.c_int)), len(perm)), ctx.h)
+    return LowRankFactor(ctx, h), perm[:plen.value].copy()

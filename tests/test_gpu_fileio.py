@@ -1,0 +1,79 @@
+"""The reference's factor / block file formats (lowrank.cpp:601-655,
+born.cpp:156-185) written and read from device memory; the expected bytes
+are built with numpy directly from the reference's layout."""
+import os
+import struct
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import paper_1410_0986_b200 as h
+    return h.Context(0)
+
+
+def ref_factor_bytes(U, V, tol, method, perm):
+    m, r = U.shape
+    n = V.shape[0]
+    b = struct.pack("<qqqdqq", m, n, r, tol, method, len(perm))
+    b += np.asarray(perm, dtype="<i8").tobytes()
+    b += np.ascontiguousarray(U, dtype="<f8").tobytes()  # row-major
+    b += np.ascontiguousarray(V, dtype="<f8").tobytes()
+    return b
+
+
+@pytest.mark.parametrize("m,n,r", [(37, 53, 5), (300, 1000, 31), (4, 3, 0), (2000, 9000, 64)])
+def test_factor_save_matches_reference_bytes_and_round_trips(ctx, tmp_path, m, n, r):
+    from paper_1410_0986_b200 import lowrank as lr
+    rng = np.random.default_rng(m + n + r)
+    U, V = rng.standard_normal((m, r)), rng.standard_normal((n, r))
+    perm = rng.permutation(m).astype(np.int32)
+    f = lr.LowRankFactor.from_tensors(ctx, torch.as_tensor(U), torch.as_tensor(V), tol=1e-7,
+                                      method=lr.RECURSIVE)
+    path = str(tmp_path / "f.bin")
+    lr.save_factor(path, f, perm)
+    assert open(path, "rb").read() == ref_factor_bytes(U, V, 1e-7, lr.RECURSIVE, perm)
+    g, p2 = lr.load_factor(ctx, path)
+    assert (g.rows(), g.cols(), g.rank()) == (m, n, r) and g.tol == 1e-7 and g.method == lr.RECURSIVE
+    np.testing.assert_array_equal(p2, perm)
+    np.testing.assert_array_equal(g.U.cpu().numpy(), U)
+    np.testing.assert_array_equal(g.V.cpu().numpy(), V)
+
+
+def test_factor_load_errors(ctx, tmp_path):
+    from paper_1410_0986_b200 import lowrank as lr
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(struct.pack("<qqqdqq", 3, 2, 5, 0.0, 0, 0))  # rank > min(m, n)
+    with pytest.raises(Exception, match="corrupt factor file"):
+        lr.load_factor(ctx, str(bad))
+    short = tmp_path / "short.bin"
+    short.write_bytes(ref_factor_bytes(np.ones((4, 2)), np.ones((5, 2)), 0.0, 0, [0, 1, 2, 3])[:-16])
+    with pytest.raises(Exception, match="truncated factor file"):
+        lr.load_factor(ctx, str(short))
+    with pytest.raises(Exception, match="cannot read factor"):
+        lr.load_factor(ctx, str(tmp_path / "missing.bin"))
+
+
+def test_block_save_load(ctx, tmp_path):
+    from paper_1410_0986_b200 import born
+    rng = np.random.default_rng(3)
+    B = rng.standard_normal((60, 2049))
+    dev = torch.as_tensor(B).cuda()
+    path = str(tmp_path / "b.bin")
+    born.save_block(ctx, path, dev)
+    want = struct.pack("<dd", 60.0, 2049.0) + np.ascontiguousarray(B, dtype="<f8").tobytes()
+    assert open(path, "rb").read() == want
+    back = born.load_block(ctx, path)
+    np.testing.assert_array_equal(back.cpu().numpy(), B)
+    # a strided (sub-)block is written as its logical rows
+    born.save_block(ctx, path, dev[:, :100])
+    np.testing.assert_array_equal(born.load_block(ctx, path).cpu().numpy(), B[:, :100])
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(struct.pack("<dd", -1.0, 2.0))
+    with pytest.raises(Exception, match="corrupt block file"):
+        born.load_block(ctx, str(bad))
