@@ -135,40 +135,6 @@ __global__ void __launch_bounds__(1024) jacobi_smem_k(int m, int n, int np,
 }
 
 // ------------------------------------------------------- cooperative ------
-// warp-per-pair variant for short columns (m <= 640): 8x fewer CTAs in the
-// grid barrier; counters[s] counts rotations applied in sweep s
-__global__ void __launch_bounds__(JT) jacobi_coop_warp_k(int64_t m, int n, int np,
-                                                         const int2* __restrict__ pairs,
-                                                         double* __restrict__ U, int64_t ldu,
-                                                         double* __restrict__ V, int64_t ldv,
-                                                         double tol, double atol,
-                                                         int* __restrict__ counters,
-                                                         int* __restrict__ sweeps_out) {
-    cg::grid_group grid = cg::this_grid();
-    const int lane = threadIdx.x & 31;
-    const int gw = int(blockIdx.x) * (JT / 32) + (threadIdx.x >> 5);
-    const int tw = int(gridDim.x) * (JT / 32);
-    const int rounds = np - 1, per = np / 2;
-    int sweep = 0;
-    for (; sweep < kMaxSweeps; ++sweep) {
-        int mine = 0;
-        for (int r = 0; r < rounds; ++r) {
-            for (int q = gw; q < per; q += tw) {
-                int2 pr = pairs[r * per + q];
-                if (pr.x >= n || pr.y >= n) continue;
-                if (warp_pair(lane, m, n, U + int64_t(pr.x) * ldu, U + int64_t(pr.y) * ldu,
-                              V + int64_t(pr.x) * ldv, V + int64_t(pr.y) * ldv, tol, atol))
-                    ++mine;
-            }
-            grid.sync();
-        }
-        if (lane == 0 && mine) atomicAdd(&counters[sweep], mine);
-        grid.sync();
-        if (*((volatile int*)&counters[sweep]) == 0) break;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
-}
-
 // CTA-per-pair variant for long columns
 __global__ void __launch_bounds__(JT) jacobi_coop_k(int64_t m, int n, int np,
                                                     const int2* __restrict__ pairs,
@@ -476,99 +442,6 @@ __global__ void __launch_bounds__(RT, 1) jacobi_rblk_k(int64_t m, int n, int nb,
     if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
 }
 
-// ----------------------------------------------------- block Jacobi -------
-// One-sided block Jacobi: columns are grouped in blocks of B; a round pairs
-// the blocks (circle method over nb blocks), each CTA loads its block pair
-// (2B columns of U, m rows) into shared memory and runs one full mini-sweep
-// over all (2B choose 2) column pairs there (rotations computed from the
-// actual columns, same criterion as the point driver), accumulating the
-// 2B x 2B rotation product, which is then applied to the 2B columns of V.
-// Per sweep this touches U and V (nb-1) times instead of (n-1) times and
-// needs (nb-1) grid barriers instead of (n-1).
-template <int B>
-__global__ void __launch_bounds__(512) jacobi_block_k(int64_t m, int n, int nb,
-                                                         const int2* __restrict__ bpairs,
-                                                         const int2* __restrict__ ipairs,
-                                                         double* __restrict__ U, int64_t ldu,
-                                                         double* __restrict__ V, int64_t ldv,
-                                                         double tol, double atol,
-                                                         int* __restrict__ counters,
-                                                         int* __restrict__ sweeps_out) {
-    constexpr int C2 = 2 * B;  // columns per block pair
-    cg::grid_group grid = cg::this_grid();
-    extern __shared__ double sm[];
-    double* Us = sm;                       // m x C2
-    double* rot = sm + int64_t(m) * C2;    // C2 x C2 (column-major)
-    __shared__ int colid[C2];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int rounds = nb - 1, per = nb / 2;
-    int sweep = 0;
-    for (; sweep < kMaxSweeps; ++sweep) {
-        int mine = 0;
-        for (int r = 0; r < rounds; ++r) {
-            for (int q = blockIdx.x; q < per; q += gridDim.x) {
-                const int2 bp = bpairs[r * per + q];
-                if (threadIdx.x < C2) {
-                    const int blk = threadIdx.x < B ? bp.x : bp.y;
-                    const int col = blk * B + (threadIdx.x % B);
-                    colid[threadIdx.x] = col < n ? col : -1;
-                }
-                for (int e = threadIdx.x; e < C2 * C2; e += blockDim.x)
-                    rot[e] = (e % C2 == e / C2) ? 1.0 : 0.0;
-                __syncthreads();
-                for (int k = 0; k < C2; ++k) {
-                    const int col = colid[k];
-                    double* dst = Us + int64_t(k) * m;
-                    if (col >= 0) {
-                        const double* src = U + int64_t(col) * ldu;
-                        for (int64_t i = threadIdx.x; i < m; i += blockDim.x) dst[i] = src[i];
-                    } else {
-                        for (int64_t i = threadIdx.x; i < m; i += blockDim.x) dst[i] = 0.0;
-                    }
-                }
-                __syncthreads();
-                // mini-sweep: C2-1 sub-rounds of B disjoint pairs, one warp each
-                for (int sr = 0; sr < C2 - 1; ++sr) {
-                    const int2 pr = warp < B ? ipairs[sr * B + warp] : make_int2(0, 0);
-                    if (warp < B && colid[pr.x] >= 0 && colid[pr.y] >= 0 &&
-                        warp_pair(lane, m, C2, Us + int64_t(pr.x) * m, Us + int64_t(pr.y) * m,
-                                  rot + pr.x * C2, rot + pr.y * C2, tol, atol) &&
-                        lane == 0)
-                        ++mine;
-                    __syncthreads();
-                }
-                // write back U; V[:, cols] <- V[:, cols] * rot
-                for (int k = 0; k < C2; ++k) {
-                    const int col = colid[k];
-                    if (col < 0) continue;
-                    double* dst = U + int64_t(col) * ldu;
-                    const double* src = Us + int64_t(k) * m;
-                    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) dst[i] = src[i];
-                }
-                for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-                    double v[C2];
-#pragma unroll
-                    for (int k = 0; k < C2; ++k) v[k] = colid[k] >= 0 ? V[i + int64_t(colid[k]) * ldv] : 0.0;
-#pragma unroll
-                    for (int j = 0; j < C2; ++j) {
-                        if (colid[j] < 0) continue;
-                        double s = 0.0;
-#pragma unroll
-                        for (int k = 0; k < C2; ++k) s += v[k] * rot[k + j * C2];
-                        V[i + int64_t(colid[j]) * ldv] = s;
-                    }
-                }
-                __syncthreads();
-            }
-            grid.sync();
-        }
-        if (lane == 0 && mine) atomicAdd(&counters[sweep], mine);
-        grid.sync();
-        if (*((volatile int*)&counters[sweep]) == 0) break;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
-}
-
 __global__ void colnorm_k(int64_t m, int n, const double* __restrict__ U, int64_t ldu,
                           double* __restrict__ s) {
     __shared__ double sh[8];
@@ -647,57 +520,6 @@ const int2* device_pairs(int n, int& np) {
     }
     cache.push_back(pc);
     return pc.dev;
-}
-
-int block_width(int64_t m) {
-    // largest B in {16, 8, 4, 2} whose block pair (m x 2B) + rotation fits
-    for (int b = 16; b >= 2; b /= 2)
-        if (size_t(m) * 2 * b * 8 + size_t(4 * b * b) * 8 <= 200 * 1024) return b;
-    return 0;
-}
-
-bool use_block_jacobi(int64_t m, int64_t n) {
-    static const int mode = [] {
-        const char* e = std::getenv("HYDOT_JACOBI_BLOCK");
-        // off by default: on the config-1 pipeline the point driver with the
-        // QR-QR preconditioner is faster (1.44 s vs 1.56 s Jacobi per step)
-        return e ? std::atoi(e) : 0;
-    }();
-    return mode != 0 && n >= 256 && block_width(m) >= 4;
-}
-
-template <int B>
-void launch_block_t(Ctx& c, int64_t m, int64_t n, double* U, int64_t ldu, double* V, int64_t ldv,
-                    double tol, double atol, int* counters, int* sweeps_out) {
-    int nb = int((n + B - 1) / B);
-    int npb = 0, npi = 0;
-    const int2* bp = device_pairs(nb, npb);     // tournament over blocks (padded to even)
-    const int2* ip = device_pairs(2 * B, npi);  // mini-sweep pairs
-    const size_t smem = size_t(m) * 2 * B * 8 + size_t(4 * B * B) * 8;
-    static bool attr = false;
-    if (!attr) {
-        HYDOT_CUDA(cudaFuncSetAttribute(jacobi_block_k<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        210 * 1024));
-        attr = true;
-    }
-    int per_sm = 0;
-    HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_block_k<B>, 512, smem));
-    int grid = std::max(1, std::min(npb / 2, per_sm * c.num_sms));
-    int64_t mm = m;
-    int nn = int(n), nbb = npb;
-    void* args[] = {&mm, &nn, &nbb, &bp, &ip, &U, &ldu, &V, &ldv, &tol, &atol, &counters, &sweeps_out};
-    HYDOT_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_block_k<B>, dim3(grid), dim3(512), args,
-                                           smem, c.stream));
-    c.count();
-}
-
-void launch_block_jacobi(Ctx& c, int64_t m, int64_t n, double* U, int64_t ldu, double* V,
-                         int64_t ldv, double tol, double atol, int* counters, int* sweeps_out) {
-    switch (block_width(m)) {
-        case 16: launch_block_t<16>(c, m, n, U, ldu, V, ldv, tol, atol, counters, sweeps_out); break;
-        case 8: launch_block_t<8>(c, m, n, U, ldu, V, ldv, tol, atol, counters, sweeps_out); break;
-        default: launch_block_t<4>(c, m, n, U, ldu, V, ldv, tol, atol, counters, sweeps_out); break;
-    }
 }
 
 // register block-Jacobi for the lazy-V driver: the fewest threads T (a
@@ -827,25 +649,17 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
                                      rblk_shape(m, n, rbR, rbT)) {
         lazy_v = true;
         launch_rblk(c, rbR, rbT, m, n, U.d(), m, tol, sw.as<int>(), sw.as<int>() + kMaxSweeps);
-    } else if (use_block_jacobi(m, n)) {
-        set_identity(c, n, n, V.d(), n);
-        launch_block_jacobi(c, m, n, U.d(), m, V.d(), n, tol, atol, sw.as<int>(),
-                            sw.as<int>() + kMaxSweeps);
     } else {
         set_identity(c, n, n, V.d(), n);
         if (n >= 2) {
             int per_sm = 0;
-            // warp-per-pair measured slower on the config-1 cores (1.95 s vs
-            // 1.44 s total): kept for experiments via HYDOT_JACOBI_WARP=1
-            static const bool warp_env = std::getenv("HYDOT_JACOBI_WARP") != nullptr;
             static const bool reg_env = [] {
                 const char* e = std::getenv("HYDOT_JACOBI_REG");
                 return !(e && e[0] == '0');
             }();
-            const bool warp_mode = warp_env && m <= 640;
-            lazy_v = !warp_mode && !strict_svd_flag() && lazy_v_enabled();
+            lazy_v = !strict_svd_flag() && lazy_v_enabled();
             const bool reg_mode = lazy_v && atol == 0.0 && reg_env && m <= 16 * JT;
-            void* kern = warp_mode ? (void*)jacobi_coop_warp_k : (void*)jacobi_coop_k;
+            void* kern = (void*)jacobi_coop_k;
             if (reg_mode) {
                 kern = m <= 4 * JT   ? (void*)jacobi_coop_reg_k<4>
                        : m <= 8 * JT ? (void*)jacobi_coop_reg_k<8>
@@ -853,7 +667,7 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
             }
             HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, JT, 0));
             const int per = np / 2;
-            int want = warp_mode ? (per + JT / 32 - 1) / (JT / 32) : per;
+            int want = per;
             int grid = std::max(1, std::min(want, per_sm * c.num_sms));
             int64_t mm = m;
             int nn = int(n), npp = np;
