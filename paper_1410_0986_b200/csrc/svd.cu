@@ -312,20 +312,24 @@ __global__ void __launch_bounds__(JT, EPT <= 4 ? 4 : (EPT <= 8 ? 3 : 2)) jacobi_
 // one block reduction of the 12 dot products, rotations computed from the
 // actual column dots (the point driver's accuracy) and applied in registers.
 // Per sweep: nb-1 grid barriers and passes over U instead of n-1.
-constexpr int RB = 4;            // block width
-constexpr int RC = 2 * RB;       // columns per block pair
-constexpr int RNV = 3 * RB;      // dot products per sub-round
-constexpr int RMAXR = 5;         // max rows per thread (5-9 measured: 5 fastest)
+constexpr int RB = 4;            // default block width (columns)
+constexpr int RMAXR = 5;         // max rows per thread at RB = 4 (5-9 measured: 5 fastest)
 
 __host__ __device__ constexpr int circ_col(int pos, int r, int np) {
     return pos == 0 ? 0 : ((pos - 1 + r) % (np - 1)) + 1;
 }
 
-template <int R, int RT>
+// RBk = block width: 4 (8 columns per pair, 28-pair mini-sweep) or 2 (4
+// columns, 6 pairs) -- the narrow form keeps cores up to 6144 rows in
+// registers (12 rows x 4 columns per thread at 512 threads)
+template <int R, int RT, int RBk>
 __global__ void __launch_bounds__(RT, 1) jacobi_rblk_k(int64_t m, int n, int nb, const int2* __restrict__ bpairs,
                                                       double* __restrict__ U, int64_t ldu, double tol,
                                                       int* __restrict__ counters, int* __restrict__ sweeps_out) {
     constexpr int NW = RT / 32;
+    constexpr int RC = 2 * RBk;          // columns per block pair
+    constexpr int RNV = 3 * RBk;         // dot products per sub-round
+    constexpr int NVP = RNV <= 8 ? 8 : 16;  // padded to a power of two
     cg::grid_group grid = cg::this_grid();
     __shared__ double red[RNV][NW];
     __shared__ double tot[RNV];
@@ -342,8 +346,8 @@ __global__ void __launch_bounds__(RT, 1) jacobi_rblk_k(int64_t m, int n, int nb,
                 int col[RC];
 #pragma unroll
                 for (int j = 0; j < RC; ++j) {
-                    const int blk = j < RB ? bp.x : bp.y;
-                    const int cj = blk * RB + (j % RB);
+                    const int blk = j < RBk ? bp.x : bp.y;
+                    const int cj = blk * RBk + (j % RBk);
                     col[j] = (blk < nb && cj < n) ? cj : -1;
                 }
 #pragma unroll
@@ -355,9 +359,9 @@ __global__ void __launch_bounds__(RT, 1) jacobi_rblk_k(int64_t m, int n, int nb,
                     }
 #pragma unroll
                 for (int sr = 0; sr < RC - 1; ++sr) {
-                    double part[16];  // 12 dot products of this sub-round, padded
+                    double part[NVP];  // the sub-round's dot products, padded
 #pragma unroll
-                    for (int k = 0; k < RB; ++k) {
+                    for (int k = 0; k < RBk; ++k) {
                         const int p = circ_col(k, sr, RC), o = circ_col(RC - 1 - k, sr, RC);
                         double a = 0.0, b = 0.0, g = 0.0;
 #pragma unroll
@@ -371,13 +375,15 @@ __global__ void __launch_bounds__(RT, 1) jacobi_rblk_k(int64_t m, int n, int nb,
                         part[3 * k + 2] = g;
                     }
 #pragma unroll
-                    for (int v = RNV; v < 16; ++v) part[v] = 0.0;
-                    // warp transpose-reduce: lane l ends with the warp total of
-                    // quantity (l & 15) -- 12 + 15 shuffles
+                    for (int v = RNV; v < NVP; ++v) part[v] = 0.0;
+                    // warp reduce: plain butterflies down to NVP lanes, then a
+                    // transpose-reduce -- lane l ends with quantity (l % NVP)
 #pragma unroll
-                    for (int v = 0; v < RNV; ++v) part[v] += __shfl_xor_sync(0xffffffffu, part[v], 16);
+                    for (int sft = 16; sft >= NVP; sft >>= 1)
 #pragma unroll
-                    for (int sft = 8; sft >= 1; sft >>= 1) {
+                        for (int v = 0; v < RNV; ++v) part[v] += __shfl_xor_sync(0xffffffffu, part[v], sft);
+#pragma unroll
+                    for (int sft = NVP / 2; sft >= 1; sft >>= 1) {
                         const bool upper = (lane & sft) != 0;
 #pragma unroll
                         for (int j = 0; j < sft; ++j) {
@@ -388,7 +394,7 @@ __global__ void __launch_bounds__(RT, 1) jacobi_rblk_k(int64_t m, int n, int nb,
                     }
                     if (lane < RNV) red[lane][warp] = part[0];
                     __syncthreads();
-                    for (int k = warp; k < RB; k += NW) {  // a warp finishes pair k, forms its rotation once
+                    for (int k = warp; k < RBk; k += NW) {  // a warp finishes pair k, forms its rotation once
                         double A = lane < NW ? red[3 * k][lane] : 0.0;
                         double Bv = lane < NW ? red[3 * k + 1][lane] : 0.0;
                         double G = lane < NW ? red[3 * k + 2][lane] : 0.0;
@@ -411,7 +417,7 @@ __global__ void __launch_bounds__(RT, 1) jacobi_rblk_k(int64_t m, int n, int nb,
                     }
                     __syncthreads();
 #pragma unroll
-                    for (int k = 0; k < RB; ++k) {
+                    for (int k = 0; k < RBk; ++k) {
                         const int p = circ_col(k, sr, RC), o = circ_col(RC - 1 - k, sr, RC);
                         if (tot[3 * k + 2] != 0.0) {
                             const double cs = tot[3 * k], sn = tot[3 * k + 1];
@@ -522,60 +528,77 @@ const int2* device_pairs(int n, int& np) {
     return pc.dev;
 }
 
-// register block-Jacobi for the lazy-V driver: the fewest threads T (a
-// power of two >= 64) with at most RMAXR rows each -- the per-sub-round
-// reduction costs instructions per warp, so fat threads win; 0 = not used
-bool rblk_shape(int64_t m, int64_t n, int& R, int& T) {
+// register block-Jacobi for the lazy-V driver: 4-column blocks with the
+// fewest threads T (a power of two >= 64) holding <= RMAXR rows each -- the
+// per-sub-round reduction costs instructions per warp, so fat threads win;
+// cores too long for that use 2-column blocks at 512 threads (<= 12 rows
+// per thread, m <= 6144).  false = not used.
+bool rblk_shape(int64_t m, int64_t n, int& R, int& T, int& B) {
     static const int mode = [] {
         const char* e = std::getenv("HYDOT_JACOBI_BLK");
         return e ? std::atoi(e) : 1;
     }();
-    if (mode == 0 || (n + RB - 1) / RB < 4) return false;
-    for (T = 64; T <= 512; T *= 2) {
-        R = int((m + T - 1) / T);
-        const int cap = T == 512 ? 5 : RMAXR;  // 512 threads: 128 registers each
-        if (R <= cap) {
-            R = R <= 3 ? 3 : R <= 5 ? 5 : R <= 7 ? 7 : 9;  // instantiated row counts
-            return true;
+    if (mode == 0) return false;
+    B = RB;
+    if ((n + RB - 1) / RB >= 4) {
+        for (T = 64; T <= 512; T *= 2) {
+            R = int((m + T - 1) / T);
+            const int cap = T == 512 ? 5 : RMAXR;  // 512 threads: 128 registers each
+            if (R <= cap) {
+                R = R <= 3 ? 3 : 5;  // instantiated row counts
+                return true;
+            }
         }
     }
-    return false;
+    // 2-column blocks only beyond the register point driver's reach (m >
+    // 4096): at 3000 rows they measured on par with it (681 vs 650 ms), at
+    // 5686 rows 1.65x faster than the CTA-per-pair driver (5.1 vs 8.5 s)
+    if (m <= 16 * JT) return false;
+    B = 2;
+    T = 512;
+    R = int((m + T - 1) / T);
+    if (R > 12 || (n + 1) / 2 < 4) return false;
+    R = R <= 6 ? 6 : R <= 9 ? 9 : 12;
+    return true;
 }
 
-template <int R, int T>
+template <int R, int T, int B>
 void launch_rblk_t(Ctx& c, int64_t m, int64_t n, double* U, int64_t ldu, double tol, int* counters,
                    int* sweeps_out) {
-    int nb = int((n + RB - 1) / RB);
+    int nb = int((n + B - 1) / B);
     int npb = 0;
     const int2* bp = device_pairs(nb, npb);
     int per_sm = 0;
-    HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_rblk_k<R, T>, T, 0));
+    HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_rblk_k<R, T, B>, T, 0));
     int grid = std::max(1, std::min(npb / 2, per_sm * c.num_sms));
     int64_t mm = m;
     int nn = int(n), nbb = nb;
     void* args[] = {&mm, &nn, &nbb, &bp, &U, &ldu, &tol, &counters, &sweeps_out};
-    HYDOT_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_rblk_k<R, T>, dim3(grid), dim3(T), args, 0, c.stream));
+    HYDOT_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_rblk_k<R, T, B>, dim3(grid), dim3(T), args, 0,
+                                           c.stream));
     c.count();
 }
 
-template <int T>
-void launch_rblk_r(Ctx& c, int R, int64_t m, int64_t n, double* U, int64_t ldu, double tol, int* counters,
-                   int* sweeps_out) {
-    switch (R) {
-        case 3: launch_rblk_t<3, T>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
-        case 5: launch_rblk_t<5, T>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
-        case 7: launch_rblk_t<(T == 512 ? 5 : 7), T>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
-        default: launch_rblk_t<(T == 512 ? 5 : 9), T>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
-    }
-}
-
-void launch_rblk(Ctx& c, int R, int T, int64_t m, int64_t n, double* U, int64_t ldu, double tol,
+void launch_rblk(Ctx& c, int R, int T, int B, int64_t m, int64_t n, double* U, int64_t ldu, double tol,
                  int* counters, int* sweeps_out) {
+    if (B == 2) {
+        switch (R) {
+            case 6: launch_rblk_t<6, 512, 2>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
+            case 9: launch_rblk_t<9, 512, 2>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
+            default: launch_rblk_t<12, 512, 2>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
+        }
+        return;
+    }
+    const bool r3 = R == 3;
     switch (T) {
-        case 64: launch_rblk_r<64>(c, R, m, n, U, ldu, tol, counters, sweeps_out); break;
-        case 128: launch_rblk_r<128>(c, R, m, n, U, ldu, tol, counters, sweeps_out); break;
-        case 256: launch_rblk_r<256>(c, R, m, n, U, ldu, tol, counters, sweeps_out); break;
-        default: launch_rblk_r<512>(c, R, m, n, U, ldu, tol, counters, sweeps_out); break;
+        case 64: r3 ? launch_rblk_t<3, 64, RB>(c, m, n, U, ldu, tol, counters, sweeps_out)
+                    : launch_rblk_t<5, 64, RB>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
+        case 128: r3 ? launch_rblk_t<3, 128, RB>(c, m, n, U, ldu, tol, counters, sweeps_out)
+                     : launch_rblk_t<5, 128, RB>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
+        case 256: r3 ? launch_rblk_t<3, 256, RB>(c, m, n, U, ldu, tol, counters, sweeps_out)
+                     : launch_rblk_t<5, 256, RB>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
+        default: r3 ? launch_rblk_t<3, 512, RB>(c, m, n, U, ldu, tol, counters, sweeps_out)
+                    : launch_rblk_t<5, 512, RB>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
     }
 }
 
@@ -645,10 +668,10 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
         jacobi_smem_k<<<1, 1024, smem, c.stream>>>(int(m), int(n), np, dpairs, U.d(), m, V.d(), n,
                                                     tol, atol, sw.as<int>() + kMaxSweeps);
         c.check_launch();
-    } else if (int rbR = 0, rbT = 0; n >= 2 && !strict_svd_flag() && lazy_v_enabled() && atol == 0.0 &&
-                                     rblk_shape(m, n, rbR, rbT)) {
+    } else if (int rbR = 0, rbT = 0, rbB = 0; n >= 2 && !strict_svd_flag() && lazy_v_enabled() && atol == 0.0 &&
+                                               rblk_shape(m, n, rbR, rbT, rbB)) {
         lazy_v = true;
-        launch_rblk(c, rbR, rbT, m, n, U.d(), m, tol, sw.as<int>(), sw.as<int>() + kMaxSweeps);
+        launch_rblk(c, rbR, rbT, rbB, m, n, U.d(), m, tol, sw.as<int>(), sw.as<int>() + kMaxSweeps);
     } else {
         set_identity(c, n, n, V.d(), n);
         if (n >= 2) {
