@@ -112,6 +112,30 @@ hydot_status hydot_fields_solve(hydot_ctx ctx, const hydot_grid7* grid, int n_la
 hydot_status hydot_apply7(hydot_ctx ctx, const hydot_grid7* grid, double sigma,
                           double sigma_prime, const double* x_dev, double* y_dev);
 
+/* grid::build_grid (grid.cpp:94-110): vertices on [-Lx,Lx]x[-Ly,Ly]x[0,Lz],
+ * x-fastest, h = 2L/(n-1) laterally and Lz/(nz-1) vertically. */
+typedef struct hydot_grid_geom {
+    int nx, ny, nz;
+    double Lx, Ly, Lz;
+} hydot_grid_geom;
+
+/* The reference's own operator, for reference fixtures: trilinear-FEM
+ * stiffness K with the Dirichlet side vertices eliminated (unit diagonal),
+ * row-lumped mass M and the bilinear face mass R on z = 0 and z = Lz
+ * (grid.cpp:112-174; element matrices by its 2x2x2 Gauss rule), applied
+ * matrix-free: y = (K + sigma M + sigma' R) x. */
+hydot_status hydot_apply_fem(hydot_ctx ctx, const hydot_grid_geom* geom, double sigma,
+                             double sigma_prime, const double* x_dev, double* y_dev);
+/* compute_fields (born.cpp:39-80) with that operator and the reference's
+ * point sources: points_h (n_points x 3, x y z) give the trilinear
+ * point_source_vector (grid.cpp:212-237) with Dirichlet entries zeroed
+ * (born.cpp:27-35); same batched CG, output layout as hydot_fields_solve. */
+hydot_status hydot_fields_solve_fem(hydot_ctx ctx, const hydot_grid_geom* geom, int n_lambda,
+                                    const double* sigma_h, const double* sigma_prime_h,
+                                    const double* inv_D_h, const double* points_h, int n_points,
+                                    double tol, int max_iter, int fixed_iters, double* out_dev,
+                                    int* iters_h, double* relres_h);
+
 /* --------------------------------------------------------------- born -- */
 /* born::assemble_H_block (born.hpp:61-62, born.cpp:82-98):
  *   out[(d*n_lambda + l)*ld + v] = (-nu) * ((phi_d[v,l] * phi_s[v,l]) * w[v])
@@ -299,13 +323,6 @@ hydot_status hydot_block_load(hydot_ctx ctx, const char* path, double* block_dev
  * operator: proj/include/hydot/pals.hpp, src/pals.cpp.
  * N- and M-length arrays are device pointers; parameters, spectra and
  * concentrations are host arrays. */
-
-/* grid::build_grid (grid.cpp:94-110): vertices on [-Lx,Lx]x[-Ly,Ly]x[0,Lz],
- * x-fastest, h = 2L/(n-1) laterally and Lz/(nz-1) vertically. */
-typedef struct hydot_grid_geom {
-    int nx, ny, nz;
-    double Lx, Ly, Lz;
-} hydot_grid_geom;
 
 /* PaLSParams (pals.hpp:16-32): n_p RBF weights, widths, centres. */
 typedef struct hydot_pals_params {

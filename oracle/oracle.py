@@ -465,3 +465,71 @@ def pals_reconstruct(U, V, perm, geom, ext, y, w, init, noise_norm, max_outer=30
     ln = int(sc[3])
     return dict(alpha=ao, beta=bo, centers=co, c=cc, trace=tr[:min(ln, trace_cap)].copy(),
                 resnorm=sc[0], converged=bool(sc[1]), flagged=bool(sc[2]))
+
+
+# --------------------------------------------------------------- FEM -----
+# The reference's own field operator (fem_oracle.cpp; grid.cpp:12-174).
+_fem_ready = False
+
+
+def _fem_lib():
+    global _fem_ready
+    L = lib()
+    if not _fem_ready:
+        L.oracle_fem_last_error.restype = C.c_char_p
+        g6 = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double]
+        L.oracle_fem_element.argtypes = [C.c_double, C.c_double, C.c_double, _dp, _dp, _dp]
+        L.oracle_fem_apply.argtypes = g6 + [C.c_double, C.c_double, _dp, _dp]
+        L.oracle_fem_dense.argtypes = g6 + [C.c_double, C.c_double, _dp]
+        L.oracle_fem_point_source.argtypes = g6 + [_dp, _dp]
+        L.oracle_fem_fields.argtypes = g6 + [C.c_int, _dp, _dp, _dp, _dp, C.c_int, C.c_double, C.c_int,
+                                             C.c_int, C.c_int, _dp, _ip, _dp]
+        _fem_ready = True
+    return L
+
+
+def _fcheck(rc):
+    if rc != 0:
+        msg = _fem_lib().oracle_fem_last_error().decode()
+        raise (ValueError if rc == 1 else RuntimeError)(msg)
+
+
+def fem_element(hx, hy, hz):
+    Ke, Me, Re = np.zeros(64), np.zeros(64), np.zeros(16)
+    _fcheck(_fem_lib().oracle_fem_element(hx, hy, hz, _d(Ke), _d(Me), _d(Re)))
+    return Ke.reshape(8, 8), Me.reshape(8, 8), Re.reshape(4, 4)
+
+
+def fem_apply(geom, sigma, sigmap, x):
+    x = _f64(x)
+    y = np.empty_like(x)
+    _fcheck(_fem_lib().oracle_fem_apply(*geom, sigma, sigmap, _d(x), _d(y)))
+    return y
+
+
+def fem_dense(geom, sigma, sigmap):
+    N = geom[0] * geom[1] * geom[2]
+    A = np.zeros((N, N), order="F")
+    _fcheck(_fem_lib().oracle_fem_dense(*geom, sigma, sigmap, _d(A)))
+    return A
+
+
+def fem_point_source(geom, r):
+    N = geom[0] * geom[1] * geom[2]
+    b = np.zeros(N)
+    _fcheck(_fem_lib().oracle_fem_point_source(*geom, _d(_f64(r)), _d(b)))
+    return b
+
+
+def fem_fields(geom, sigma, sigmap, inv_D, points, tol=1e-10, max_iter=20000, fixed_iters=0, threads=1):
+    """(N x (n*nl), F-order) fields, iterations, relative residuals."""
+    N = geom[0] * geom[1] * geom[2]
+    nl = len(sigma)
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    out = np.empty((N, len(pts) * nl), order="F")
+    iters = np.zeros(len(pts) * nl, dtype=np.int32)
+    rel = np.zeros(len(pts) * nl)
+    _fcheck(_fem_lib().oracle_fem_fields(*geom, nl, _d(_f64(sigma)), _d(_f64(sigmap)), _d(_f64(inv_D)),
+                                         _d(pts), len(pts), tol, max_iter, fixed_iters, threads, _d(out),
+                                         iters.ctypes.data_as(_ip), _d(rel)))
+    return out, iters, rel

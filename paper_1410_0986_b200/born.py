@@ -133,3 +133,44 @@ def load_block(ctx: Context, path: str) -> torch.Tensor:
     check(lib().hydot_block_load(ctx.h, os.fsencode(path), dptr(out), max(cols.value, 1),
                                  C.byref(r2), C.byref(c2)), ctx.h)
     return out
+
+
+def _geom_c(geom):
+    """(nx, ny, nz, Lx, Ly, Lz) or any object with those attributes."""
+    if hasattr(geom, "Lx"):
+        t = (geom.nx, geom.ny, geom.nz, geom.Lx, geom.Ly, geom.Lz)
+    else:
+        t = tuple(geom)
+    return _lib.GridGeom(int(t[0]), int(t[1]), int(t[2]), float(t[3]), float(t[4]), float(t[5]))
+
+
+def apply_operator_fem(ctx: Context, geom, sigma: float, sigma_prime: float,
+                       x: torch.Tensor) -> torch.Tensor:
+    """(K + sigma M + sigma' R) x with the reference's trilinear-FEM K, lumped M
+    and z-face R (grid.cpp:112-174), matrix-free on the device."""
+    y = torch.empty_like(x)
+    g = _geom_c(geom)
+    check(lib().hydot_apply_fem(ctx.h, C.byref(g), sigma, sigma_prime, dptr(x), dptr(y)), ctx.h)
+    return y
+
+
+def compute_fields_fem(ctx: Context, geom, sigma, sigma_prime, inv_D, points_xyz,
+                       tol: float = 1e-10, max_iter: int = 20000, fixed_iters: int = 0):
+    """compute_fields (born.cpp:39-80) on the reference's own FEM operator with
+    its trilinear point sources (points_xyz: n x 3 coordinates); returns
+    (n, n_lambda, N) fields x_l / D_l and the CG statistics."""
+    sig = np.ascontiguousarray(sigma, dtype=np.float64)
+    sigp = np.ascontiguousarray(sigma_prime, dtype=np.float64)
+    invd = np.ascontiguousarray(inv_D, dtype=np.float64)
+    nl = sig.size
+    pts = np.ascontiguousarray(points_xyz, dtype=np.float64).reshape(-1, 3)
+    g = _geom_c(geom)
+    N = g.nx * g.ny * g.nz
+    out = ctx.empty(len(pts), nl, N)
+    iters = np.zeros(len(pts) * nl, dtype=np.int32)
+    rel = np.zeros(len(pts) * nl, dtype=np.float64)
+    dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+    check(lib().hydot_fields_solve_fem(ctx.h, C.byref(g), nl, dp(sig), dp(sigp), dp(invd), dp(pts),
+                                       len(pts), tol, max_iter, fixed_iters, dptr(out),
+                                       iters.ctypes.data_as(C.POINTER(C.c_int)), dp(rel)), ctx.h)
+    return out, FieldStats(iters.reshape(len(pts), nl), rel.reshape(len(pts), nl))

@@ -210,6 +210,39 @@ hydot_status hydot_fields_solve(hydot_ctx ctx, const hydot_grid7* grid, int n_la
     });
 }
 
+hydot_status hydot_apply_fem(hydot_ctx ctx, const hydot_grid_geom* geom, double sigma, double sigma_prime,
+                             const double* x_dev, double* y_dev) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!geom || !x_dev || !y_dev) throw std::invalid_argument("hydot_apply_fem: null argument");
+        apply_fem(c, *geom, sigma, sigma_prime, x_dev, y_dev);
+    });
+}
+
+hydot_status hydot_fields_solve_fem(hydot_ctx ctx, const hydot_grid_geom* geom, int n_lambda,
+                                    const double* sigma_h, const double* sigma_prime_h, const double* inv_D_h,
+                                    const double* points_h, int n_points, double tol, int max_iter,
+                                    int fixed_iters, double* out_dev, int* iters_h, double* relres_h) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!geom || !sigma_h || !sigma_prime_h || !inv_D_h || !points_h || !out_dev)
+            throw std::invalid_argument("hydot_fields_solve_fem: null argument");
+        CGStats st;
+        fields_solve_fem(c, *geom, n_lambda, sigma_h, sigma_prime_h, inv_D_h, points_h, n_points, tol, max_iter,
+                         fixed_iters, out_dev, &st);
+        const int total = n_points * n_lambda;
+        for (int k = 0; k < total; ++k) {
+            if (iters_h) iters_h[k] = st.iters[size_t(k)];
+            if (relres_h) relres_h[k] = st.relres[size_t(k)];
+        }
+        if (fixed_iters <= 0)
+            for (int k = 0; k < total; ++k)
+                if (!(st.relres[size_t(k)] <= tol))
+                    throw std::runtime_error("field solve failed at point " + std::to_string(k / n_lambda) +
+                                             ", wavelength index " + std::to_string(k % n_lambda));
+    });
+}
+
 hydot_status hydot_apply7(hydot_ctx ctx, const hydot_grid7* grid, double sigma,
                           double sigma_prime, const double* x_dev, double* y_dev) {
     return guard(ctx ? ctx->c.get() : nullptr, [&] {

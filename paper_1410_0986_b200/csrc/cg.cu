@@ -15,6 +15,7 @@
 // stencil and the vector updates use explicit _rn intrinsics in the oracle's
 // operation order (no FMA contraction), so only the dot-product summation
 // order differs from the CPU restatement.
+#include <cmath>
 #include <cstdlib>
 
 #include "internal.h"
@@ -126,6 +127,83 @@ __device__ __forceinline__ double sum_parts(const double* __restrict__ parts, in
     return *bc;
 }
 
+// ---------------------------------------------------------- operators --
+// Op7: the BASELINE 7-point vertex-centred FV operator (stencil_at).
+struct Op7 {
+    Stencil g;
+    template <class Get>
+    __device__ __forceinline__ double operator()(int64_t i, double sigma, double sigmap, Get get) const {
+        return stencil_at(g, sigma, sigmap, i, get);
+    }
+};
+
+// OpFem: the reference's operator K + sigma M + sigma' R (grid.cpp:112-174)
+// applied matrix-free: K trilinear-element stiffness with the Dirichlet
+// side vertices eliminated (unit diagonal), M row-sum-lumped element mass,
+// R bilinear face mass on the z = 0 and z = Lz faces -- not restricted to
+// non-Dirichlet vertices, as in assemble_robin (the SURVEY A1 quirk).
+// Element matrices come from the reference's 2x2x2 Gauss rule (host).
+// Row sums run cell by cell in (cz, cy, cx) order, local vertex b inner.
+struct OpFem {
+    int nx, ny, nz;
+    float inv_nx, inv_ny;
+    const double* __restrict__ em;  // Ke (64) | Me (64) | Re (16)
+    template <class Get>
+    __device__ __forceinline__ double operator()(int64_t i, double sigma, double sigmap, Get get) const {
+        unsigned q1, ux, uy, uz;
+        fdivmod(unsigned(i), unsigned(nx), inv_nx, q1, ux);
+        fdivmod(q1, unsigned(ny), inv_ny, uz, uy);
+        const int ix = int(ux), iy = int(uy), iz = int(uz);
+        auto dir = [&](int jx, int jy) { return jx == 0 || jx == nx - 1 || jy == 0 || jy == ny - 1; };
+        const bool di = dir(ix, iy);
+        const double xi = get(i);
+        double kx = 0.0, m = 0.0;
+        for (int oz = -1; oz <= 0; ++oz) {
+            const int cz = iz + oz;
+            if (cz < 0 || cz > nz - 2) continue;
+            for (int oy = -1; oy <= 0; ++oy) {
+                const int cy = iy + oy;
+                if (cy < 0 || cy > ny - 2) continue;
+                for (int ox = -1; ox <= 0; ++ox) {
+                    const int cx = ix + ox;
+                    if (cx < 0 || cx > nx - 2) continue;
+                    const int a = (ox ? 1 : 0) | (oy ? 2 : 0) | (oz ? 4 : 0);
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        const int jx = cx + (b & 1), jy = cy + ((b >> 1) & 1), jz = cz + ((b >> 2) & 1);
+                        m = __dadd_rn(m, em[64 + a * 8 + b]);
+                        if (!di && !dir(jx, jy)) {
+                            const int64_t j = (int64_t(jz) * ny + jy) * nx + jx;
+                            kx = __dadd_rn(kx, __dmul_rn(em[a * 8 + b], get(j)));
+                        }
+                    }
+                }
+            }
+        }
+        double y = di ? xi : kx;
+        y = __dadd_rn(y, __dmul_rn(sigma, __dmul_rn(m, xi)));
+        if (iz == 0 || iz == nz - 1) {
+            double rx = 0.0;
+            for (int oy = -1; oy <= 0; ++oy) {
+                const int cy = iy + oy;
+                if (cy < 0 || cy > ny - 2) continue;
+                for (int ox = -1; ox <= 0; ++ox) {
+                    const int cx = ix + ox;
+                    if (cx < 0 || cx > nx - 2) continue;
+                    const int a = (ox ? 1 : 0) | (oy ? 2 : 0);
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const int64_t j = (int64_t(iz) * ny + cy + ((b >> 1) & 1)) * nx + cx + (b & 1);
+                        rx = __dadd_rn(rx, __dmul_rn(em[128 + a * 4 + b], get(j)));
+                    }
+                }
+            }
+            y = __dadd_rn(y, __dmul_rn(sigmap, rx));
+        }
+        return y;
+    }
+};
+
 struct SysState {
     double rr[2];   // r.r published per iteration parity
     double bnorm;   // ||b||
@@ -134,32 +212,44 @@ struct SysState {
     double relres;
 };
 
-__global__ void cg_init(int64_t N, int nl, const int64_t* __restrict__ rhs_vertex, int k0,
-                        double* __restrict__ X, double* __restrict__ R, double* __restrict__ P,
-                        SysState* __restrict__ st) {
+// zero x, r, p; scalars from ||b||^2 (b set by cg_rhs)
+__global__ void cg_init(int64_t N, int nl, const double* __restrict__ rhs_b2, int k0, double* __restrict__ X,
+                        double* __restrict__ R, double* __restrict__ P, SysState* __restrict__ st) {
     const int sys = blockIdx.y;
     const int kglob = k0 + sys;
-    const int64_t v = rhs_vertex[kglob / nl];
     double* x = X + int64_t(sys) * N;  // x lives in the output (caller column)
     double* r = R + int64_t(sys) * N;
     double* p = P + int64_t(sys) * N;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < N;
          i += int64_t(gridDim.x) * blockDim.x) {
         x[i] = 0.0;
-        r[i] = (i == v) ? 1.0 : 0.0;
+        r[i] = 0.0;
         p[i] = 0.0;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        st[sys].rr[0] = 1.0;
+        const double b2 = rhs_b2[kglob / nl];
+        st[sys].rr[0] = b2;
         st[sys].rr[1] = 0.0;
-        st[sys].bnorm = 1.0;
+        st[sys].bnorm = sqrt(b2);
         st[sys].done = 0;
         st[sys].iters = 0;
         st[sys].relres = 1.0;
     }
 }
 
-__global__ void __launch_bounds__(CT, 4) cg_pa(Stencil g, int64_t N, int nl, int k0, int it,
+// r = b: up to 8 (vertex, weight) entries per right-hand side
+__global__ void cg_rhs(int64_t N, int nl, int k0, int nb, const int64_t* __restrict__ ridx,
+                       const double* __restrict__ rw, double* __restrict__ R) {
+    const int sys = blockIdx.x * blockDim.y + threadIdx.y;
+    const int e = threadIdx.x;  // 0..7
+    if (sys >= nb) return;
+    const int rhs = (k0 + sys) / nl;
+    const int64_t v = ridx[int64_t(rhs) * 8 + e];
+    if (v >= 0) R[int64_t(sys) * N + v] = rw[int64_t(rhs) * 8 + e];
+}
+
+template <class Op>
+__global__ void __launch_bounds__(CT, 4) cg_pa(Op op, int64_t N, int nl, int k0, int it,
                                             const double* __restrict__ sig,
                                             const double* __restrict__ sigp,
                                             const double* __restrict__ R,
@@ -209,7 +299,7 @@ __global__ void __launch_bounds__(CT, 4) cg_pa(Stencil g, int64_t N, int nl, int
         const int64_t i = base + int64_t(k) * CT;
         if (i < N) {
             const double pi = pnew(i);
-            const double ap = stencil_at(g, sigma, sigmap, i, pnew);
+            const double ap = op(i, sigma, sigmap, pnew);
             p[i] = pi;
             acc += pi * ap;
         }
@@ -218,7 +308,8 @@ __global__ void __launch_bounds__(CT, 4) cg_pa(Stencil g, int64_t N, int nl, int
     if (threadIdx.x == 0) partA[int64_t(sys) * nparts + blockIdx.x] = t;
 }
 
-__global__ void __launch_bounds__(CT, 4) cg_xr(Stencil g, int64_t N, int nl, int k0, int it,
+template <class Op>
+__global__ void __launch_bounds__(CT, 4) cg_xr(Op op, int64_t N, int nl, int k0, int it,
                                             const double* __restrict__ sig,
                                             const double* __restrict__ sigp,
                                             double* __restrict__ X, double* __restrict__ R,
@@ -246,7 +337,7 @@ __global__ void __launch_bounds__(CT, 4) cg_xr(Stencil g, int64_t N, int nl, int
     for (int k = 0; k < VPT; ++k) {
         const int64_t i = base + int64_t(k) * CT;
         if (i < N) {
-            const double q = stencil_at(g, sigma, sigmap, i, getp);
+            const double q = op(i, sigma, sigmap, getp);
             x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
             const double rn = __dsub_rn(r[i], __dmul_rn(alpha, q));
             r[i] = rn;
@@ -280,12 +371,13 @@ __global__ void cg_finish(int64_t N, int nl, int k0, int it_total, double* __res
         x[i] = x[i] * s;
 }
 
-__global__ void apply7_k(Stencil g, int64_t N, double sigma, double sigmap,
-                         const double* __restrict__ x, double* __restrict__ y) {
+template <class Op>
+__global__ void apply_k(Op op, int64_t N, double sigma, double sigmap, const double* __restrict__ x,
+                        double* __restrict__ y) {
     auto get = [&](int64_t j) { return x[j]; };
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < N;
          i += int64_t(gridDim.x) * blockDim.x)
-        y[i] = stencil_at(g, sigma, sigmap, i, get);
+        y[i] = op(i, sigma, sigmap, get);
 }
 
 __global__ void count_active(int n, const SysState* __restrict__ st, int* __restrict__ out) {
@@ -304,32 +396,16 @@ __global__ void count_active(int n, const SysState* __restrict__ st, int* __rest
 
 }  // namespace
 
-void apply7(Ctx& c, const hydot_grid7& g, double sigma, double sigmap, const double* x,
-            double* y) {
-    const int64_t N = int64_t(g.nx) * g.ny * g.nz;
-    Stencil s = make_stencil(g);
-    int blocks = int(std::min<int64_t>((N + 255) / 256, int64_t(c.num_sms) * 16));
-    apply7_k<<<blocks, 256, 0, c.stream>>>(s, N, sigma, sigmap, x, y);
-    c.check_launch();
-}
+namespace {
 
-void fields_solve(Ctx& c, const hydot_grid7& g, int nl, const double* sigma,
-                  const double* sigmap, const double* inv_D, const int64_t* rhs_vertex, int n_rhs,
-                  double tol, int max_iter, int fixed_iters, double* out, CGStats* stats) {
-    if (g.nx < 3 || g.ny < 3 || g.nz < 2 || g.h <= 0)
-        throw std::invalid_argument("fields_solve: bad grid");
-    if (nl <= 0 || n_rhs <= 0) throw std::invalid_argument("compute_fields: no wavelengths");
-    const int64_t N = int64_t(g.nx) * g.ny * g.nz;
-    for (int s = 0; s < n_rhs; ++s) {
-        int64_t v = rhs_vertex[s];
-        if (v < 0 || v >= N) throw std::invalid_argument("point_source_vector: point outside domain");
-        int ix = int(v % g.nx), iy = int((v / g.nx) % g.ny);
-        if (ix == 0 || ix == g.nx - 1 || iy == 0 || iy == g.ny - 1)
-            throw std::invalid_argument("source support falls entirely on the Dirichlet boundary");
-    }
-    Stencil st = make_stencil(g);
-    if (int64_t(g.nx) * g.ny * g.nz >= (int64_t(1) << 24))
-        throw std::invalid_argument("fields_solve: grid too large for the 24-bit vertex decode");
+// the batched CG over any operator: rhs n_rhs sparse vectors (ridx / rw, 8
+// entries each, -1 = unused) times n_lambda shifts
+template <class Op>
+void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, const double* sigmap,
+              const double* inv_D, const std::vector<int64_t>& ridx, const std::vector<double>& rw,
+              const std::vector<double>& b2, int n_rhs, double tol, int max_iter, int fixed_iters, double* out,
+              CGStats* stats) {
+    if (N >= (int64_t(1) << 24)) throw std::invalid_argument("fields_solve: grid too large for the 24-bit vertex decode");
     const int total = n_rhs * nl;
     const int nparts = int((N + CV - 1) / CV);
     // One batch of up to 24 GB (all systems iterate together, HBM-bound).
@@ -351,9 +427,12 @@ void fields_solve(Ctx& c, const hydot_grid7& g, int nl, const double* sigma,
     HYDOT_CUDA(cudaMemcpyAsync(dsig.d(), sigma, size_t(nl) * 8, cudaMemcpyHostToDevice, c.stream));
     HYDOT_CUDA(cudaMemcpyAsync(dsigp.d(), sigmap, size_t(nl) * 8, cudaMemcpyHostToDevice, c.stream));
     HYDOT_CUDA(cudaMemcpyAsync(dinv.d(), inv_D, size_t(nl) * 8, cudaMemcpyHostToDevice, c.stream));
-    DBuf drhs(c, size_t(n_rhs) * 8);
-    HYDOT_CUDA(cudaMemcpyAsync(drhs.as<void>(), rhs_vertex, size_t(n_rhs) * 8,
-                               cudaMemcpyHostToDevice, c.stream));
+    // sparse right-hand sides: 8 (vertex, weight) entries each, and ||b||^2
+    DBuf dridx(c, size_t(n_rhs) * 8 * sizeof(int64_t));
+    DBuf drw = dalloc(c, size_t(n_rhs) * 8), db2 = dalloc(c, size_t(n_rhs));
+    HYDOT_CUDA(cudaMemcpyAsync(dridx.as<void>(), ridx.data(), ridx.size() * 8, cudaMemcpyHostToDevice, c.stream));
+    HYDOT_CUDA(cudaMemcpyAsync(drw.d(), rw.data(), rw.size() * 8, cudaMemcpyHostToDevice, c.stream));
+    HYDOT_CUDA(cudaMemcpyAsync(db2.d(), b2.data(), b2.size() * 8, cudaMemcpyHostToDevice, c.stream));
     DBuf R = dalloc(c, size_t(batch) * size_t(N));
     DBuf P = dalloc(c, 2 * size_t(batch) * size_t(N));  // double-buffered p
     DBuf pA = dalloc(c, size_t(batch) * size_t(nparts));
@@ -372,8 +451,11 @@ void fields_solve(Ctx& c, const hydot_grid7& g, int nl, const double* sigma,
         {
             dim3 gi = dim3(unsigned(std::min<int64_t>((N + 255) / 256, 1024)), unsigned(nb));
             // p_old of iteration 0 is buffer 1 (zeroed); p_it lives in buffer it&1
-            cg_init<<<gi, 256, 0, c.stream>>>(N, nl, drhs.as<int64_t>(), k0, X, R.d(),
+            cg_init<<<gi, 256, 0, c.stream>>>(N, nl, db2.d(), k0, X, R.d(),
                                               P.d() + size_t(batch) * size_t(N), ss);
+            c.check_launch();
+            dim3 gr = dim3(unsigned((nb + 31) / 32));
+            cg_rhs<<<gr, dim3(8, 32), 0, c.stream>>>(N, nl, k0, nb, dridx.as<int64_t>(), drw.d(), R.d());
             c.check_launch();
         }
         auto pbuf = [&](int i) { return P.d() + size_t(i & 1) * size_t(batch) * size_t(N); };
@@ -387,11 +469,11 @@ void fields_solve(Ctx& c, const hydot_grid7& g, int nl, const double* sigma,
         int it = 0;
         for (; it < limit; ++it) {
             dim3 grid = dim3(unsigned(nparts), unsigned(active.size()));
-            cg_pa<<<grid, CT, 0, c.stream>>>(st, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
+            cg_pa<<<grid, CT, 0, c.stream>>>(op, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
                                             pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
                                             tol, fixed_iters > 0, dact.as<int>());
             c.check_launch();
-            cg_xr<<<grid, CT, 0, c.stream>>>(st, N, nl, k0, it, dsig.d(), dsigp.d(), X, R.d(),
+            cg_xr<<<grid, CT, 0, c.stream>>>(op, N, nl, k0, it, dsig.d(), dsigp.d(), X, R.d(),
                                             pbuf(it), pA.d(), pB.d(), nparts, ss, dact.as<int>());
             c.check_launch();
             if (fixed_iters <= 0 && (it % 8) == 7) {
@@ -417,7 +499,7 @@ void fields_solve(Ctx& c, const hydot_grid7& g, int nl, const double* sigma,
         if (fixed_iters <= 0 && it >= limit) {
             // one more convergence check for systems finishing on the last step
             dim3 grid = dim3(unsigned(nparts), unsigned(active.size()));
-            cg_pa<<<grid, CT, 0, c.stream>>>(st, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
+            cg_pa<<<grid, CT, 0, c.stream>>>(op, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
                                             pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
                                             tol, 0, dact.as<int>());
             c.check_launch();
@@ -439,6 +521,159 @@ void fields_solve(Ctx& c, const hydot_grid7& g, int nl, const double* sigma,
         }
     }
     c.sync();
+}
+
+void check_grid(int nx, int ny, int nz) {
+    if (nx < 3 || ny < 3 || nz < 2) throw std::invalid_argument("fields_solve: bad grid");
+}
+
+}  // namespace
+
+void apply7(Ctx& c, const hydot_grid7& g, double sigma, double sigmap, const double* x, double* y) {
+    const int64_t N = int64_t(g.nx) * g.ny * g.nz;
+    Op7 op{make_stencil(g)};
+    int blocks = int(std::min<int64_t>((N + 255) / 256, int64_t(c.num_sms) * 16));
+    apply_k<<<blocks, 256, 0, c.stream>>>(op, N, sigma, sigmap, x, y);
+    c.check_launch();
+}
+
+void fields_solve(Ctx& c, const hydot_grid7& g, int nl, const double* sigma, const double* sigmap,
+                  const double* inv_D, const int64_t* rhs_vertex, int n_rhs, double tol, int max_iter,
+                  int fixed_iters, double* out, CGStats* stats) {
+    check_grid(g.nx, g.ny, g.nz);
+    if (g.h <= 0) throw std::invalid_argument("fields_solve: bad grid");
+    if (nl <= 0 || n_rhs <= 0) throw std::invalid_argument("compute_fields: no wavelengths");
+    const int64_t N = int64_t(g.nx) * g.ny * g.nz;
+    std::vector<int64_t> ridx(size_t(n_rhs) * 8, -1);
+    std::vector<double> rw(size_t(n_rhs) * 8, 0.0), b2(size_t(n_rhs), 1.0);
+    for (int s = 0; s < n_rhs; ++s) {
+        int64_t v = rhs_vertex[s];
+        if (v < 0 || v >= N) throw std::invalid_argument("point_source_vector: point outside domain");
+        int ix = int(v % g.nx), iy = int((v / g.nx) % g.ny);
+        if (ix == 0 || ix == g.nx - 1 || iy == 0 || iy == g.ny - 1)
+            throw std::invalid_argument("source support falls entirely on the Dirichlet boundary");
+        ridx[size_t(s) * 8] = v;
+        rw[size_t(s) * 8] = 1.0;
+    }
+    cg_batch(c, Op7{make_stencil(g)}, N, nl, sigma, sigmap, inv_D, ridx, rw, b2, n_rhs, tol, max_iter,
+             fixed_iters, out, stats);
+}
+
+// ------------------------------------------------------------- FEM mode --
+namespace {
+
+constexpr double kGaussPt = 0.57735026918962576451;  // grid.cpp:14
+
+// element stiffness / mass (grid.cpp:39-64) and face mass (:67-88) by the
+// reference's 2x2x2 (2x2) Gauss rule, same summation order
+void fem_element_matrices(double hx, double hy, double hz, double Ke[64], double Me[64], double Re[16]) {
+    for (int e = 0; e < 64; ++e) Ke[e] = Me[e] = 0.0;
+    for (int e = 0; e < 16; ++e) Re[e] = 0.0;
+    const double detJ = hx * hy * hz / 8.0;
+    const double ih[3] = {2.0 / hx, 2.0 / hy, 2.0 / hz};
+    auto sgn = [](int a, int bit) { return (a & bit) ? 1.0 : -1.0; };
+    for (int qx = 0; qx < 2; ++qx)
+        for (int qy = 0; qy < 2; ++qy)
+            for (int qz = 0; qz < 2; ++qz) {
+                const double xi = qx ? kGaussPt : -kGaussPt, eta = qy ? kGaussPt : -kGaussPt,
+                             zeta = qz ? kGaussPt : -kGaussPt;
+                double N[8], G[8][3];
+                for (int a = 0; a < 8; ++a) {
+                    const double sx = sgn(a, 1), sy = sgn(a, 2), sz = sgn(a, 4);
+                    N[a] = 0.125 * (1 + sx * xi) * (1 + sy * eta) * (1 + sz * zeta);
+                    G[a][0] = 0.125 * sx * (1 + sy * eta) * (1 + sz * zeta) * ih[0];
+                    G[a][1] = 0.125 * sy * (1 + sx * xi) * (1 + sz * zeta) * ih[1];
+                    G[a][2] = 0.125 * sz * (1 + sx * xi) * (1 + sy * eta) * ih[2];
+                }
+                for (int a = 0; a < 8; ++a)
+                    for (int b = 0; b < 8; ++b) {
+                        const double dot = G[a][0] * G[b][0] + G[a][1] * G[b][1] + G[a][2] * G[b][2];
+                        Ke[a * 8 + b] += detJ * dot;
+                        Me[a * 8 + b] += detJ * N[a] * N[b];
+                    }
+            }
+    const double detF = hx * hy / 4.0;
+    for (int qx = 0; qx < 2; ++qx)
+        for (int qy = 0; qy < 2; ++qy) {
+            const double xi = qx ? kGaussPt : -kGaussPt, eta = qy ? kGaussPt : -kGaussPt;
+            for (int a = 0; a < 4; ++a) {
+                const double Na = 0.25 * (1 + sgn(a, 1) * xi) * (1 + sgn(a, 2) * eta);
+                for (int b = 0; b < 4; ++b) {
+                    const double Nb = 0.25 * (1 + sgn(b, 1) * xi) * (1 + sgn(b, 2) * eta);
+                    Re[a * 4 + b] += detF * Na * Nb;
+                }
+            }
+        }
+}
+
+struct FemSetup {
+    OpFem op{};
+    DBuf em;
+    int64_t N = 0;
+    double hx = 0, hy = 0, hz = 0;
+};
+
+FemSetup fem_setup(Ctx& c, const hydot_grid_geom& g) {
+    check_grid(g.nx, g.ny, g.nz);
+    if (g.Lx <= 0 || g.Ly <= 0 || g.Lz <= 0) throw std::invalid_argument("build_grid: extents must be positive");
+    FemSetup f;
+    f.hx = 2 * g.Lx / (g.nx - 1);
+    f.hy = 2 * g.Ly / (g.ny - 1);
+    f.hz = g.Lz / (g.nz - 1);
+    double h[144];
+    fem_element_matrices(f.hx, f.hy, f.hz, h, h + 64, h + 128);
+    f.em = dalloc(c, 144);
+    HYDOT_CUDA(cudaMemcpyAsync(f.em.d(), h, sizeof h, cudaMemcpyHostToDevice, c.stream));
+    c.sync();
+    f.op = OpFem{g.nx, g.ny, g.nz, 1.0f / float(g.nx), 1.0f / float(g.ny), f.em.d()};
+    f.N = int64_t(g.nx) * g.ny * g.nz;
+    return f;
+}
+
+}  // namespace
+
+void apply_fem(Ctx& c, const hydot_grid_geom& g, double sigma, double sigmap, const double* x, double* y) {
+    FemSetup f = fem_setup(c, g);
+    int blocks = int(std::min<int64_t>((f.N + 255) / 256, int64_t(c.num_sms) * 16));
+    apply_k<<<blocks, 256, 0, c.stream>>>(f.op, f.N, sigma, sigmap, x, y);
+    c.check_launch();
+    c.sync();
+}
+
+void fields_solve_fem(Ctx& c, const hydot_grid_geom& g, int nl, const double* sigma, const double* sigmap,
+                      const double* inv_D, const double* points, int n_pts, double tol, int max_iter,
+                      int fixed_iters, double* out, CGStats* stats) {
+    if (nl <= 0 || n_pts <= 0) throw std::invalid_argument("compute_fields: no wavelengths");
+    FemSetup f = fem_setup(c, g);
+    // source_rhs (born.cpp:27-35): trilinear point_source_vector
+    // (grid.cpp:212-237) with the Dirichlet vertices zeroed
+    std::vector<int64_t> ridx(size_t(n_pts) * 8, -1);
+    std::vector<double> rw(size_t(n_pts) * 8, 0.0), b2(size_t(n_pts), 0.0);
+    auto clamp_cell = [](double t, int ncells) {
+        int cc = int(std::floor(t));
+        return cc < 0 ? 0 : (cc > ncells - 1 ? ncells - 1 : cc);
+    };
+    for (int s = 0; s < n_pts; ++s) {
+        const double rx = points[3 * s], ry = points[3 * s + 1], rz = points[3 * s + 2];
+        if (!(rx >= -g.Lx && rx <= g.Lx && ry >= -g.Ly && ry <= g.Ly && rz >= 0.0 && rz <= g.Lz))
+            throw std::invalid_argument("point_source_vector: point outside domain");
+        const double tx = (rx + g.Lx) / f.hx, ty = (ry + g.Ly) / f.hy, tz = rz / f.hz;
+        const int cx = clamp_cell(tx, g.nx - 1), cy = clamp_cell(ty, g.ny - 1), cz = clamp_cell(tz, g.nz - 1);
+        const double xi = 2 * (tx - cx) - 1, eta = 2 * (ty - cy) - 1, zeta = 2 * (tz - cz) - 1;
+        double nrm2 = 0.0;
+        for (int a = 0; a < 8; ++a) {
+            const int jx = cx + (a & 1), jy = cy + ((a >> 1) & 1), jz = cz + ((a >> 2) & 1);
+            const double sx = (a & 1) ? 1.0 : -1.0, sy = (a & 2) ? 1.0 : -1.0, sz = (a & 4) ? 1.0 : -1.0;
+            double w = 0.125 * (1 + sx * xi) * (1 + sy * eta) * (1 + sz * zeta);
+            if (jx == 0 || jx == g.nx - 1 || jy == 0 || jy == g.ny - 1) w = 0.0;
+            ridx[size_t(s) * 8 + a] = w != 0.0 ? (int64_t(jz) * g.ny + jy) * g.nx + jx : -1;
+            rw[size_t(s) * 8 + a] = w;
+            nrm2 += w * w;
+        }
+        if (nrm2 == 0.0) throw std::invalid_argument("source support falls entirely on the Dirichlet boundary");
+        b2[size_t(s)] = nrm2;
+    }
+    cg_batch(c, f.op, f.N, nl, sigma, sigmap, inv_D, ridx, rw, b2, n_pts, tol, max_iter, fixed_iters, out, stats);
 }
 
 }  // namespace hydot

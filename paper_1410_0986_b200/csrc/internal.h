@@ -222,6 +222,11 @@ void fields_solve(Ctx& c, const hydot_grid7& g, int nl, const double* sigma,
                   double tol, int max_iter, int fixed_iters, double* out, CGStats* stats);
 void apply7(Ctx& c, const hydot_grid7& g, double sigma, double sigmap, const double* x,
             double* y);
+// the reference's trilinear-FEM operator K + sigma M + sigma' R (grid.cpp)
+void apply_fem(Ctx& c, const hydot_grid_geom& g, double sigma, double sigmap, const double* x, double* y);
+void fields_solve_fem(Ctx& c, const hydot_grid_geom& g, int nl, const double* sigma, const double* sigmap,
+                      const double* inv_D, const double* points, int n_pts, double tol, int max_iter,
+                      int fixed_iters, double* out, CGStats* stats);
 
 // matmat.cu
 void j_combine(Ctx& c, int64_t M, int b, int nc, int nl, const double* T, int64_t ldt,
