@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(PT) qr_panel_coop(int64_t mr, int jb, double* 
 // s_q, and applies H_c = I - tau v v^T (v = [1; scal x]) to its (row, q)
 // entries, storing v and beta.
 constexpr int kCtaRows = 768;
-constexpr int CT = 512;
+constexpr int CT = 512;  // (1024 measured slower: barriers + 32-way norm reduction)
 __global__ void __launch_bounds__(CT) qr_panel_cta(int mr, int jb, double* __restrict__ P, int64_t ld,
                                                    double* __restrict__ tau_out) {
     extern __shared__ double slab[];  // mr x jb, ld mr
