@@ -539,9 +539,16 @@ bool rblk_shape(int64_t m, int64_t n, int& R, int& T, int& B) {
         return e ? std::atoi(e) : 1;
     }();
     if (mode == 0) return false;
+    // at least 128 threads: with 64 each of the 2 warps forms two rotations
+    // per sub-round in sequence (111-320-row cores: 242 -> 174 ms per
+    // config-1 step at 128; 206 ms at 256)
+    static const int tmin = [] {
+        const char* e = std::getenv("HYDOT_JACOBI_TMIN");
+        return e ? std::max(64, std::atoi(e)) : 128;
+    }();
     B = RB;
     if ((n + RB - 1) / RB >= 4) {
-        for (T = 64; T <= 512; T *= 2) {
+        for (T = tmin; T <= 512; T *= 2) {
             R = int((m + T - 1) / T);
             const int cap = T == 512 ? 5 : RMAXR;  // 512 threads: 128 registers each
             if (R <= cap) {
