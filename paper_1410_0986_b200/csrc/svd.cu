@@ -36,10 +36,14 @@ namespace {
 constexpr int kMaxSweeps = 40;
 constexpr int JT = 256;  // threads per CTA of the large driver
 
+// Jacobi rotation annihilating g for the 2x2 Gram [[a, g], [g, b]]:
+// t = sign(d) g / (|d| + sqrt(d^2 + g^2)), d = (b - a) / 2 -- the usual
+// zeta = d / g form multiplied through by |g| (one division, one sqrt and
+// one rsqrt on the critical path instead of three divisions and two sqrts)
 __device__ __forceinline__ void rot_params(double a, double b, double g, double& cs, double& sn) {
-    double zeta = (b - a) / (2.0 * g);
-    double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-    cs = 1.0 / sqrt(1.0 + t * t);
+    const double d = 0.5 * (b - a);
+    const double t = copysign(1.0, d) * g / (fabs(d) + sqrt(fma(d, d, g * g)));
+    cs = rsqrt(fma(t, t, 1.0));
     sn = cs * t;
 }
 
