@@ -105,13 +105,19 @@ __global__ void __launch_bounds__(PT) qr_panel_coop(int64_t mr, int jb, double* 
         red[warp][lane] = acc[0];
         if (lane == 0) red[warp][PB] = nacc;
         __syncthreads();
-        if (threadIdx.x <= PB) {
-            const int q = threadIdx.x;
-            double t = 0.0;
-            if (q == PB || (q > col && q < jb))
-                for (int w = 0; w < PT / 32; ++w) t += red[w][q];
-            if (q == PB) buf.nrm[par * GMAX + blockIdx.x] = t;
-            else buf.dot[(int64_t(par) * GMAX + blockIdx.x) * PB + q] = t;
+        // the 32 dots and the norm summed over the 16 warps with shuffles,
+        // one half-warp per quantity; slot 0 (dot 0 is never needed: q > col
+        // >= 0) carries the norm
+        {
+            const int slot = 2 * warp + (lane >> 4), hl = lane & 15;
+            const int q = slot == 0 ? PB : slot;
+            double t = (q <= PB && hl < PT / 32) ? red[hl][q] : 0.0;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (hl == 0 && q <= PB) {
+                if (q == PB) buf.nrm[par * GMAX + blockIdx.x] = t;
+                else if (q > col && q < jb) buf.dot[(int64_t(par) * GMAX + blockIdx.x) * PB + q] = t;
+            }
         }
     };
     partials(0, 0);
@@ -131,7 +137,7 @@ __global__ void __launch_bounds__(PT) qr_panel_coop(int64_t mr, int jb, double* 
                 const double alpha = buf.row[par * PB + c];
                 double tau = 0.0, beta = alpha, scal = 1.0;
                 if (xn2 > 0.0) {
-                    beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
+                    beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
                     tau = (beta - alpha) / beta;
                     scal = 1.0 / (alpha - beta);
                 }
@@ -224,14 +230,15 @@ __global__ void __launch_bounds__(CT) qr_panel_cta(int mr, int jb, double* __res
         for (int o = 16; o > 0; o >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, o);
         if (lane == 0) s_nrm[warp] = nacc;
         __syncthreads();
-        // ---- phase 2: reflector (redundantly per thread) and update
-        double xn2 = 0.0;
+        // ---- phase 2: reflector (redundantly per warp) and update; the 16
+        // warp partials are summed with shuffles, not a dependent load chain
+        double xn2 = lane < NW ? s_nrm[lane] : 0.0;
 #pragma unroll
-        for (int k = 0; k < NW; ++k) xn2 += s_nrm[k];
+        for (int o = 16; o > 0; o >>= 1) xn2 += __shfl_xor_sync(0xffffffffu, xn2, o);  // all lanes get the sum
         const double alpha = x[c];
         double tau = 0.0, beta = alpha, scal = 1.0;
         if (xn2 > 0.0) {
-            beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
+            beta = -copysign(sqrt(fma(alpha, alpha, xn2)), alpha);
             tau = (beta - alpha) / beta;
             scal = 1.0 / (alpha - beta);
         }
