@@ -162,16 +162,28 @@ __global__ void __launch_bounds__(SK_T) skinny_tn_k(int64_t K, int64_t R, int64_
 }
 
 // Z[j, c] = sum_chunks part[chunk][j][c] (fixed order)
-__global__ void skinny_reduce_k(int64_t nchunks, int64_t R, int Q, const double* __restrict__ part,
-                                double* __restrict__ Z, int64_t ldz) {
+// sum the chunk partials: threadIdx.x over 32 consecutive outputs, threadIdx.y
+// over chunks, fixed-order shared-memory combine (no long dependent chain)
+constexpr int SRZ = 8;
+__global__ void __launch_bounds__(32 * SRZ) skinny_reduce_k(int64_t nchunks, int64_t R, int Q,
+                                                            const double* __restrict__ part,
+                                                            double* __restrict__ Z, int64_t ldz) {
+    __shared__ double sh[SRZ][33];
     const int64_t total = R * Q;
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
-         e += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t j = e / Q;
-        const int c = int(e % Q);
+    for (int64_t e0 = blockIdx.x * int64_t(32); e0 < total; e0 += int64_t(gridDim.x) * 32) {
+        const int64_t e = e0 + threadIdx.x;
         double s = 0.0;
-        for (int64_t k = 0; k < nchunks; ++k) s += part[(k * R + j) * Q + c];
-        Z[j + int64_t(c) * ldz] = s;
+        if (e < total)
+            for (int64_t k = threadIdx.y; k < nchunks; k += SRZ) s += part[k * total + e];
+        sh[threadIdx.y][threadIdx.x] = s;
+        __syncthreads();
+        if (threadIdx.y == 0 && e < total) {
+            double t = 0.0;
+#pragma unroll
+            for (int y = 0; y < SRZ; ++y) t += sh[y][threadIdx.x];
+            Z[e / Q + (e % Q) * ldz] = t;
+        }
+        __syncthreads();
     }
 }
 
@@ -250,8 +262,8 @@ void skinny_tn_t(Ctx& c, int64_t K, int64_t R, int q, const double* A, int64_t l
     skinny_tn_k<Q><<<dim3(unsigned(nchunks), unsigned(groups)), SK_T, size_t(T * Q * 8), c.stream>>>(
         K, R, T, A, lda, X, ldx, part.d(), jgroup, q);
     c.check_launch();
-    int blocks = int(std::max<int64_t>(1, std::min<int64_t>((R * q + 255) / 256, int64_t(c.num_sms) * 4)));
-    skinny_reduce_k<<<blocks, 256, 0, c.stream>>>(nchunks, R, q, part.d(), Z, ldz);
+    int blocks = int(std::max<int64_t>(1, std::min<int64_t>((R * q + 31) / 32, int64_t(c.num_sms) * 16)));
+    skinny_reduce_k<<<blocks, dim3(32, SRZ), 0, c.stream>>>(nchunks, R, q, part.d(), Z, ldz);
     c.check_launch();
 }
 
