@@ -220,7 +220,10 @@ typedef struct {
 
 /* Built-in device provider forming Born blocks from resident fields
  * (compress_H's provider, experiments.cpp:235-240, without a dense H):
- * incident_dev_h[s] (N x n_lambda), adjoint_dev_h[s*n_det + d]. */
+ * incident_dev_h[s] (N x n_lambda), adjoint_dev_h[s*n_det + d].
+ * ready_events_h (optional, n_sources cudaEvent_t or NULL): the context
+ * stream waits on source s's event before forming its blocks, so a caller
+ * can stream the fields in on another stream while earlier leaves compress. */
 typedef struct {
     int64_t N;
     int n_lambda, n_sources, n_det;
@@ -228,6 +231,7 @@ typedef struct {
     const double* const* adjoint_dev_h;
     const double* w_dev;
     double nu;
+    void* const* ready_events_h;
 } hydot_born_fields;
 
 /* RecursiveOptions (lowrank.hpp:128-131) + knobs the reference hard-codes

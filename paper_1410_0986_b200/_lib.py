@@ -43,7 +43,8 @@ class Provider(C.Structure):
 class BornFields(C.Structure):
     _fields_ = [("N", C.c_int64), ("n_lambda", C.c_int), ("n_sources", C.c_int),
                 ("n_det", C.c_int), ("incident_dev_h", C.POINTER(_dp)),
-                ("adjoint_dev_h", C.POINTER(_dp)), ("w_dev", _dp), ("nu", C.c_double)]
+                ("adjoint_dev_h", C.POINTER(_dp)), ("w_dev", _dp), ("nu", C.c_double),
+                ("ready_events_h", C.POINTER(C.c_void_p))]
 
 
 class RecOpts(C.Structure):

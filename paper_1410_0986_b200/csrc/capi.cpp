@@ -485,6 +485,8 @@ hydot_status hydot_recursive_lowrank(hydot_ctx ctx, hydot_tree tree, double eps,
             cols = born->N;
             fn = [&](int s, double* dst, int64_t ld) {
                 if (s < 0 || s >= born->n_sources) throw std::invalid_argument("source out of range");
+                if (born->ready_events_h && born->ready_events_h[s])
+                    HYDOT_CUDA(cudaStreamWaitEvent(c.stream, static_cast<cudaEvent_t>(born->ready_events_h[s]), 0));
                 born_block(c, born->N, born->n_lambda, born->incident_dev_h[s],
                            born->adjoint_dev_h + int64_t(s) * born->n_det, born->n_det, born->w_dev,
                            born->nu, dst, ld);

@@ -255,6 +255,9 @@ class BornFieldsProvider:
     adjoint: list
     w: torch.Tensor
     nu: float = 1.0
+    # optional torch.cuda.Event per source: the engine's stream waits on it
+    # before forming that source's blocks (stream the fields in meanwhile)
+    ready_events: Optional[list] = None
 
 
 def recursive_lowrank(ctx: Context, tree: ClusterTree, eps: float, provider,
@@ -286,7 +289,14 @@ def recursive_lowrank(ctx: Context, tree: ClusterTree, eps: float, provider,
         inc = (_lib._dp * ns)(*[dptr(t) for t in provider.incident])
         adj = (_lib._dp * (ns * nd))(*[dptr(t) for s in range(ns) for t in provider.adjoint[s]])
         keep += [inc, adj]
-        bf = _lib.BornFields(N, nl, ns, nd, inc, adj, dptr(provider.w), provider.nu)
+        evs = None
+        if provider.ready_events is not None:
+            if len(provider.ready_events) != ns:
+                raise ValueError("BornFieldsProvider: one ready event per source")
+            evs = (C.c_void_p * ns)(*[C.c_void_p(e.cuda_event) for e in provider.ready_events])
+            keep.append(evs)
+        bf = _lib.BornFields(N, nl, ns, nd, inc, adj, dptr(provider.w), provider.nu,
+                             None if evs is None else C.cast(evs, C.POINTER(C.c_void_p)))
         rows_per = nd * nl
         row_perm = np.zeros(tree.n_sources * rows_per, dtype=np.int32)
         rc = lib().hydot_recursive_lowrank(ctx.h, tree.h, eps, None, C.byref(bf), C.byref(o),
