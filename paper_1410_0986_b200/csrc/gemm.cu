@@ -14,6 +14,8 @@
 // measured slower on every path shape (1 CTA/SM at 254 registers).  K-long shapes use split-K: each z-slice writes a
 // partial tile to a workspace and a second kernel sums the slices in fixed
 // z order, so results are deterministic run to run.
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace hydot {
@@ -335,6 +337,20 @@ void dgemm(Ctx& c, bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alp
            int64_t ldc) {
     StageTimer _t(c, "gemm", m, n, k, 2.0 * double(m) * double(n) * double(k),
                   8.0 * (double(m) * k + double(k) * n + double(m) * n * (beta != 0.0 ? 2 : 1)));
+    // HYDOT_GEMM_CLASSES=1: also time by shape class (profiling aid)
+    static const bool classes = [] {
+        const char* e = std::getenv("HYDOT_GEMM_CLASSES");
+        return e && e[0] == '1';
+    }();
+    std::unique_ptr<StageTimer> t2;
+    if (classes) {
+        const char* cls = (m <= 32 || n <= 32) ? (k >= 4096 ? "gemm_c_thin_longk" : "gemm_c_thin")
+                          : k <= 32            ? "gemm_c_k32"
+                          : k <= 128           ? "gemm_c_k128"
+                          : k >= 4096          ? "gemm_c_longk"
+                                               : "gemm_c_mid";
+        t2.reset(new StageTimer(c, cls, m, n, k, 2.0 * double(m) * double(n) * double(k), 0.0));
+    }
     if (m <= 0 || n <= 0) return;
     if (k <= 0 || alpha == 0.0) {
         int blocks = int(std::min<int64_t>((m * n + 255) / 256, 4096));
