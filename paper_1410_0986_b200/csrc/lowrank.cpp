@@ -36,6 +36,29 @@ DBuf materialise_t(Ctx& c, const double* S, int64_t ld, int64_t m, int64_t n) {
 // QR-factored triangle needs ~4x fewer sweeps than on X itself (measured
 // 8-10 vs 28-41 on graded 300x300 cores).  `upper`: X is already the n x n
 // triangle R1 (Q1 = I).
+// HYDOT_SVD_PRESORT_TALL=0 restores sorting the triangle after the tall QR
+bool presort_tall() {
+    static const bool on = [] {
+        const char* e = std::getenv("HYDOT_SVD_PRESORT_TALL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// SVD of an n x n upper triangle R1 that came from the QR of norm-ordered
+// columns: R1^T = Q2 R2, Jacobi on L = R2^T = Ux S Vx^T, so R1 = Ux S (Q2 Vx)^T.
+// Ux -> U (n x n), Q2 Vx -> V (n x n).
+void svd_of_sorted_r(Ctx& c, int64_t n, const double* R1, double* U, std::vector<double>& s, double* V) {
+    QRFact q2;
+    DBuf T = dalloc(c, size_t(n * n)), R2 = dalloc(c, size_t(n * n));
+    transpose(c, n, n, R1, n, T.d(), n);  // R1^T
+    geqrf(c, n, n, T.d(), n, q2);
+    extract_upper(c, n, q2.a.d(), n, R2.d(), n);
+    transpose(c, n, n, R2.d(), n, T.d(), n);  // L = R2^T
+    jacobi_svd(c, n, n, T.d(), n, U, n, s, V, n);
+    apply_q(c, q2, false, n, V, n);  // Q2 Vx
+}
+
 void jacobi_precond(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, bool upper,
                     double* U, int64_t ldu, std::vector<double>& s, double* V, int64_t ldv) {
     if (n <= 48) {  // the single-CTA shared-memory driver is already cheap
@@ -154,18 +177,45 @@ SVDd fast_thin_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, i
             Lp = tmp.d();
             ldl = m;
         }
-        QRFact qf;
-        geqrf(c, m, n, Lp, ldl, qf);
-        tmp.release();
-        DBuf R = dalloc(c, size_t(n * n));
-        extract_upper(c, n, qf.a.d(), m, R.d(), n);
         SVDd o;
         o.m = m;
         o.n = n;
         o.k = n;
         o.V = dalloc(c, size_t(n * n));
         DBuf Ur = dalloc(c, size_t(n * n));
-        jacobi_precond(c, n, n, R.d(), n, true, Ur.d(), n, o.s, o.V.d(), n);
+        QRFact qf;
+        if (n <= 48 || !presort_tall()) {
+            geqrf(c, m, n, Lp, ldl, qf);
+            tmp.release();
+            DBuf R = dalloc(c, size_t(n * n));
+            extract_upper(c, n, qf.a.d(), m, R.d(), n);
+            jacobi_precond(c, n, n, R.d(), n, true, Ur.d(), n, o.s, o.V.d(), n);
+        } else {
+            // norm-order the tall columns first: QR(A P) = Q R1 is the
+            // preconditioner's first QR, so only R1^T's QR remains
+            // (A = (Q Ux) S (P Q2 Vx)^T) -- one n x n QR and one n x n
+            // Q-application fewer than sorting R afterwards
+            DBuf nrm = dalloc(c, size_t(n));
+            col_norms(c, m, n, Lp, ldl, nrm.d());
+            std::vector<double> hn(static_cast<size_t>(n));
+            c.d2h(hn.data(), nrm.d(), size_t(n));
+            std::vector<int> perm(static_cast<size_t>(n));
+            for (int64_t j = 0; j < n; ++j) perm[size_t(j)] = int(j);
+            std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return hn[size_t(a)] > hn[size_t(b)]; });
+            DBuf dperm(c, size_t(n) * sizeof(int));
+            HYDOT_CUDA(cudaMemcpyAsync(dperm.as<void>(), perm.data(), size_t(n) * sizeof(int),
+                                       cudaMemcpyHostToDevice, c.stream));
+            DBuf As = dalloc(c, size_t(m * n));
+            gather_cols(c, m, n, Lp, ldl, dperm.as<int>(), As.d(), m);
+            tmp.release();
+            geqrf(c, m, n, As.d(), m, qf);
+            As.release();
+            DBuf R1 = dalloc(c, size_t(n * n)), Vr = dalloc(c, size_t(n * n));
+            extract_upper(c, n, qf.a.d(), m, R1.d(), n);
+            svd_of_sorted_r(c, n, R1.d(), Ur.d(), o.s, Vr.d());
+            scatter_rows(c, n, n, Vr.d(), n, dperm.as<int>(), o.V.d(), n);  // V = P (Q2 Vx)
+            c.sync();  // host perm vector goes out of scope
+        }
         // U = Q [Ur; 0]
         o.U = dalloc(c, size_t(m * n));
         fill(c, m, n, 0.0, o.U.d(), m);
