@@ -181,6 +181,8 @@ void gather_cols(Ctx& c, int64_t rows, int64_t cols, const double* src, int64_t 
 double frob_diff(Ctx& c, int64_t rows, int64_t cols, const double* A, int64_t lda,
                  const double* B, int64_t ldb);  // ||A - B||_F (synchronises)
 void col_norms(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* out_dev);
+// ||offdiag(A)||_F / ||A||_F of an n x n matrix (synchronises)
+double offdiag_ratio(Ctx& c, int64_t n, const double* A, int64_t lda);
 void scatter_rows(Ctx& c, int64_t rows, int64_t cols, const double* src, int64_t lds,
                   const int* idx_dev, double* dst, int64_t ldd);  // dst[idx[i],:] = src[i,:]
 

@@ -374,7 +374,20 @@ Factor recompress(Ctx& c, const Factor& f, double eps, int rank, Ledger* l) {
     extract_upper(c, r, qv.a.d(), N, Rv.d(), r);
     dgemm(c, false, true, r, r, r, 1.0, Ru.d(), r, Rv.d(), r, 0.0, core.d(), r);  // :567
     charge(l, HYDOT_CAT_RECOMPRESS, 2.0 * double(r) * double(r) * double(r));
-    SVDd svd = thin_svd(c, core.d(), r, false, r, r, l, HYDOT_CAT_RECOMPRESS);  // :568
+    // The core of a factor whose U / V columns are already orthogonal (every
+    // factor the recursion produces) is diagonal to rounding: Jacobi then
+    // converges in 1-2 sweeps on it directly and the QR preconditioning
+    // (sort + two r x r QRs) is skipped.  General cores keep it.
+    SVDd svd;
+    if (r > 48 && offdiag_ratio(c, r, core.d(), r) < 1e-8) {
+        charge(l, HYDOT_CAT_RECOMPRESS, svd_flops(double(r), double(r)));  // as thin_svd
+        svd.m = svd.n = svd.k = r;
+        svd.U = dalloc(c, size_t(r * r));
+        svd.V = dalloc(c, size_t(r * r));
+        jacobi_svd(c, r, r, core.d(), r, svd.U.d(), r, svd.s, svd.V.d(), r);
+    } else {
+        svd = thin_svd(c, core.d(), r, false, r, r, l, HYDOT_CAT_RECOMPRESS);  // :568
+    }
     const std::vector<double>& s = svd.s;
     const double s1 = s.empty() ? 0.0 : s[0];
     int64_t keep;

@@ -77,6 +77,29 @@ __global__ void gather_cols_k(int64_t rows, int64_t cols, const double* __restri
 }
 
 // per-block partial sums of (A-B)^2 in fixed order; final sum on one block
+// sum of squares of the off-diagonal (off = 1) or diagonal (off = 0) part
+__global__ void part2_partial(int64_t n, const double* __restrict__ A, int64_t lda, int off,
+                              double* __restrict__ part) {
+    __shared__ double sh[256];
+    double acc = 0.0;
+    const int64_t total = n * n;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = e % n, j = e / n;
+        if ((i != j) == (off != 0)) {
+            const double v = A[i + j * lda];
+            acc += v * v;
+        }
+    }
+    sh[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
 __global__ void diff2_partial(int64_t rows, int64_t cols, const double* __restrict__ A,
                               int64_t lda, const double* __restrict__ B, int64_t ldb,
                               double* __restrict__ part) {
@@ -177,6 +200,24 @@ void gather_cols(Ctx& c, int64_t rows, int64_t cols, const double* src, int64_t 
     gather_cols_k<<<grid_for(c, rows * cols), 256, 0, c.stream>>>(rows, cols, src, lds, idx, dst,
                                                                    ldd);
     c.check_launch();
+}
+
+double offdiag_ratio(Ctx& c, int64_t n, const double* A, int64_t lda) {
+    if (n <= 1) return 0.0;
+    const int blocks = std::min(grid_for(c, n * n), 256);
+    DBuf part = dalloc(c, 2 * (size_t(blocks) + 1));
+    double v[2];
+    for (int off = 0; off < 2; ++off) {
+        double* pp = part.d() + off * (blocks + 1);
+        part2_partial<<<blocks, 256, 0, c.stream>>>(n, A, lda, off, pp);
+        c.check_launch();
+        sum_partials<<<1, 256, 0, c.stream>>>(blocks, pp, pp + blocks);
+        c.check_launch();
+    }
+    c.d2h(&v[0], part.d() + blocks, 1);
+    c.d2h(&v[1], part.d() + (blocks + 1) + blocks, 1);
+    const double tot = v[0] + v[1];
+    return tot > 0.0 ? std::sqrt(v[1] / tot) : 0.0;
 }
 
 double frob_diff(Ctx& c, int64_t rows, int64_t cols, const double* A, int64_t lda,
