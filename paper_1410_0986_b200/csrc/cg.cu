@@ -10,6 +10,10 @@
 //           partial p.Ap                                   (reads r,p; writes p)
 //   cg_xr : alpha = rr / p.Ap, x += alpha p, r -= alpha A p, partial r.r
 //                                                         (reads p,x,r; writes x,r)
+// For the 7-point operator (the BASELINE fields) the same two kernels run
+// z-marching (cgz_pa / cgz_xr below): a CTA owns full x-rows of one system
+// and walks the z planes with three planes of p in shared memory -- config 1
+// fields 0.93 -> 0.63 s (36 -> 53 % of the 48 N B/iteration HBM figure).
 // Scalars never leave the device: each CTA sums its system's partials in a
 // fixed order (deterministic), CTA 0 publishes rr into a parity slot.  The
 // stencil and the vector updates use explicit _rn intrinsics in the oracle's
@@ -17,6 +21,7 @@
 // order differs from the CPU restatement.
 #include <cmath>
 #include <cstdlib>
+#include <type_traits>
 
 #include "internal.h"
 
@@ -53,32 +58,17 @@ __device__ __forceinline__ void fdivmod(unsigned i, unsigned d, float inv_d, uns
     r = unsigned(rr);
 }
 
-// y_i = (A x)_i with x(j) supplied by a functor; reference operation order.
-// Branch-free: every neighbour is loaded from a clamped in-range index and
-// masked by a select, so the compiler can issue all loads of the unrolled
-// vertices before their first use (the branchy form stalled on each load).
-// The masked terms add +0.0, leaving every sum as in the reference order.
-template <class Get>
-__device__ __forceinline__ double stencil_at(const Stencil& g, double sigma, double sigmap,
-                                             int64_t i, Get get) {
-    const int64_t plane = int64_t(g.nx) * g.ny;
-    const int64_t N = plane * g.nz;
-    unsigned q1, ux, uy, uz;
-    fdivmod(unsigned(i), unsigned(g.nx), g.inv_nx, q1, ux);
-    fdivmod(q1, unsigned(g.ny), g.inv_ny, uz, uy);
-    const int ix = int(ux), iy = int(uy), iz = int(uz);
-    const double xi = get(i);
-    const bool dir = (ix == 0 || ix == g.nx - 1 || iy == 0 || iy == g.ny - 1);
-    const bool bxm = ix - 1 > 0, bxp = ix + 1 < g.nx - 1, bym = iy - 1 > 0, byp = iy + 1 < g.ny - 1;
-    const bool bzm = iz > 0, bzp = iz < g.nz - 1;
-    const double vxm = get(i > 0 ? i - 1 : i);
-    const double vxp = get(i + 1 < N ? i + 1 : i);
-    const double vym = get(i >= g.nx ? i - g.nx : i);
-    const double vyp = get(i + g.nx < N ? i + g.nx : i);
-    const double vzm = get(i >= plane ? i - plane : i);
-    const double vzp = get(i + plane < N ? i + plane : i);
-    const double h = g.h;
-    const bool zb = (iz == 0 || iz == g.nz - 1);
+// The 7-point operator row at vertex (ix, iy, iz) from its centre and six
+// neighbour values, in the reference operation order.  Masked neighbours are
+// selected away (not multiplied), so stale or clamped values never matter.
+__device__ __forceinline__ double stencil7(int nx, int ny, int nz, double h, int ix, int iy, int iz,
+                                           double sigma, double sigmap, double xi, double vxm,
+                                           double vxp, double vym, double vyp, double vzm,
+                                           double vzp) {
+    const bool dir = (ix == 0 || ix == nx - 1 || iy == 0 || iy == ny - 1);
+    const bool bxm = ix - 1 > 0, bxp = ix + 1 < nx - 1, bym = iy - 1 > 0, byp = iy + 1 < ny - 1;
+    const bool bzm = iz > 0, bzp = iz < nz - 1;
+    const bool zb = (iz == 0 || iz == nz - 1);
     const double zext = zb ? 0.5 * h : h;
     const double V = __dmul_rn(__dmul_rn(h, h), zext);
     const double S = zb ? __dmul_rn(h, h) : 0.0;
@@ -102,6 +92,71 @@ __device__ __forceinline__ double stencil_at(const Stencil& g, double sigma, dou
     const double diag = __dadd_rn(__dadd_rn(wsum, __dmul_rn(sigma, V)), __dmul_rn(sigmap, S));
     const double y = __dsub_rn(__dmul_rn(diag, xi), nb);
     return dir ? xi : y;
+}
+
+// stencil7 split for the z-marching kernels: the diagonal depends only on
+// the plane (zdiag, once per plane), the neighbour sum on the vertex
+// (stencil7_nb); together they are stencil7's operations in its order.
+struct ZDiag {
+    double zext, diag;
+    bool bzm, bzp;
+};
+
+__device__ __forceinline__ ZDiag zdiag(int nz, double h, int iz, double sigma, double sigmap) {
+    ZDiag d;
+    d.bzm = iz > 0;
+    d.bzp = iz < nz - 1;
+    const bool zb = (iz == 0 || iz == nz - 1);
+    d.zext = zb ? 0.5 * h : h;
+    const double V = __dmul_rn(__dmul_rn(h, h), d.zext);
+    const double S = zb ? __dmul_rn(h, h) : 0.0;
+    double wsum = 4.0 * d.zext;
+    if (d.bzm) wsum = __dadd_rn(wsum, h);
+    if (d.bzp) wsum = __dadd_rn(wsum, h);
+    d.diag = __dadd_rn(__dadd_rn(wsum, __dmul_rn(sigma, V)), __dmul_rn(sigmap, S));
+    return d;
+}
+
+__device__ __forceinline__ double stencil7_nb(int nx, int ny, double h, const ZDiag& d, int ix, int iy,
+                                              double xi, double vxm, double vxp, double vym,
+                                              double vyp, double vzm, double vzp) {
+    const bool dir = (ix == 0 || ix == nx - 1 || iy == 0 || iy == ny - 1);
+    const bool bxm = ix - 1 > 0, bxp = ix + 1 < nx - 1, bym = iy - 1 > 0, byp = iy + 1 < ny - 1;
+    const double xm = bxm ? vxm : 0.0;
+    const double xp = bxp ? vxp : 0.0;
+    const double ym = bym ? vym : 0.0;
+    const double yp = byp ? vyp : 0.0;
+    double nb = __dmul_rn(d.zext, xm);
+    nb = __dadd_rn(nb, __dmul_rn(d.zext, xp));
+    nb = __dadd_rn(nb, __dmul_rn(d.zext, ym));
+    nb = __dadd_rn(nb, __dmul_rn(d.zext, yp));
+    if (d.bzm) nb = __dadd_rn(nb, __dmul_rn(h, vzm));
+    if (d.bzp) nb = __dadd_rn(nb, __dmul_rn(h, vzp));
+    const double y = __dsub_rn(__dmul_rn(d.diag, xi), nb);
+    return dir ? xi : y;
+}
+
+// y_i = (A x)_i with x(j) supplied by a functor; reference operation order.
+// Branch-free: every neighbour is loaded from a clamped in-range index, so
+// the compiler can issue all loads of the unrolled vertices before their
+// first use (the branchy form stalled on each load).
+template <class Get>
+__device__ __forceinline__ double stencil_at(const Stencil& g, double sigma, double sigmap,
+                                             int64_t i, Get get) {
+    const int64_t plane = int64_t(g.nx) * g.ny;
+    const int64_t N = plane * g.nz;
+    unsigned q1, ux, uy, uz;
+    fdivmod(unsigned(i), unsigned(g.nx), g.inv_nx, q1, ux);
+    fdivmod(q1, unsigned(g.ny), g.inv_ny, uz, uy);
+    const double xi = get(i);
+    const double vxm = get(i > 0 ? i - 1 : i);
+    const double vxp = get(i + 1 < N ? i + 1 : i);
+    const double vym = get(i >= g.nx ? i - g.nx : i);
+    const double vyp = get(i + g.nx < N ? i + g.nx : i);
+    const double vzm = get(i >= plane ? i - plane : i);
+    const double vzp = get(i + plane < N ? i + plane : i);
+    return stencil7(g.nx, g.ny, g.nz, g.h, int(ux), int(uy), int(uz), sigma, sigmap, xi, vxm, vxp,
+                    vym, vyp, vzm, vzp);
 }
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
@@ -348,6 +403,260 @@ __global__ void __launch_bounds__(CT, 4) cg_xr(Op op, int64_t N, int nl, int k0,
     if (threadIdx.x == 0) partB[int64_t(sys) * nparts + blockIdx.x] = t;
 }
 
+// ------------------------------------------------------ z-marching (Op7) --
+// The same two kernels for the 7-point operator with a 2.5-D tiling: a CTA
+// owns `ty` full x-rows of one system and marches through the z planes,
+// keeping three planes of its (ty+2)-row halo'ed tile in shared memory.
+// Each vertex's p_new is formed once per plane (instead of once per stencil
+// use), every load is a coalesced x-row, and the next plane is prefetched
+// into registers while the current one is computed.  Arithmetic is
+// stencil7 in the reference order, so the result is bit-identical to the
+// vertex-parallel kernels above (only the dot-product partition differs).
+constexpr int ZT = 256;  // threads per CTA
+constexpr int ZE = 6;    // halo'ed tile elements per thread: (ty + 2) nx <= ZT ZE
+constexpr int ZO = 5;    // own-tile elements per thread:     ty nx <= ZT ZO
+
+struct ZGeo {
+    int nx, ny, nz, ty;
+    double h;
+};
+
+// Tile geometry: halo'ed element e (row-major over ty+2 rows) lives at plane
+// offset base + e and is inside the grid for lo <= e < hi; own element e
+// (e < Wo) lives at base + nx + e and at tile index e + nx.  Only the own
+// elements' (ix, iy) are kept per thread (packed), for the stencil masks.
+struct ZIdx {
+    int base, lo, hi, W, Wo;
+    int oxy[ZO];  // ix | iy << 16
+};
+
+__device__ __forceinline__ void zidx(const ZGeo& g, ZIdx& z) {
+    const int y0 = blockIdx.x * g.ty;
+    const int rows = min(g.ty, g.ny - y0);
+    z.W = (rows + 2) * g.nx;
+    z.Wo = rows * g.nx;
+    z.base = (y0 - 1) * g.nx;
+    z.lo = y0 == 0 ? g.nx : 0;
+    z.hi = y0 + rows == g.ny ? (rows + 1) * g.nx : z.W;
+#pragma unroll
+    for (int k = 0; k < ZO; ++k) {
+        const int e = threadIdx.x + k * ZT;
+        const int ry = e / g.nx, ix = e - ry * g.nx;
+        z.oxy[k] = ix | ((y0 + ry) << 16);
+    }
+}
+
+// stencil at own element e of plane iz from the three shared planes
+__device__ __forceinline__ double zstencil(const ZGeo& g, const ZIdx& z, int k, int e, const ZDiag& d,
+                                           const double* __restrict__ c, const double* __restrict__ dn,
+                                           const double* __restrict__ up) {
+    const int si = e + g.nx, ix = z.oxy[k] & 0xffff, iy = z.oxy[k] >> 16;
+    return stencil7_nb(g.nx, g.ny, g.h, d, ix, iy, c[si], c[ix > 0 ? si - 1 : si],
+                       c[ix < g.nx - 1 ? si + 1 : si], c[si - g.nx], c[si + g.nx], dn[si], up[si]);
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(ZT, MINB) cgz_pa(ZGeo g, int64_t N, int nl, int k0, int it,
+                                              const double* __restrict__ sig,
+                                              const double* __restrict__ sigp,
+                                              const double* __restrict__ R,
+                                              const double* __restrict__ Pold,
+                                              double* __restrict__ Pnew, double* __restrict__ partA,
+                                              const double* __restrict__ partB, int nparts,
+                                              SysState* __restrict__ st, double tol, int fixed,
+                                              const int* __restrict__ act) {
+    extern __shared__ double zs[];  // 3 planes of the halo'ed tile
+    __shared__ double sh[ZT / 32];
+    __shared__ double bc;
+    const int sys = act[blockIdx.y];
+    SysState& S = st[sys];
+    if (S.done) return;
+    const int l = (k0 + sys) % nl;
+    double beta = 0.0;
+    const int slot = it & 1;
+    if (it > 0) {
+        const double rr_new = sum_parts(partB + int64_t(sys) * nparts, nparts, sh, &bc);
+        const double rr_old = S.rr[slot ^ 1];
+        const double relres = sqrt(rr_new) / S.bnorm;
+        if (!fixed && relres <= tol) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                S.done = 1;
+                S.iters = it;
+                S.relres = relres;
+            }
+            return;
+        }
+        beta = rr_new / rr_old;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            S.rr[slot] = rr_new;
+            S.relres = relres;
+            S.iters = it;
+        }
+    }
+    ZIdx z;
+    zidx(g, z);
+    const int64_t plane = int64_t(g.nx) * g.ny;
+    const double* r = R + int64_t(sys) * N;
+    const double* po = Pold + int64_t(sys) * N;
+    double* p = Pnew + int64_t(sys) * N;
+    const double sigma = sig[l], sigmap = sigp[l];
+    double rv[ZE], pv[ZE];
+    auto load = [&](int iz) {
+#pragma unroll
+        for (int k = 0; k < ZE; ++k) {
+            const int e = threadIdx.x + k * ZT;
+            if (e >= z.lo && e < z.hi) {
+                const int64_t i = iz * plane + z.base + e;
+                rv[k] = __ldcs(r + i);
+                pv[k] = __ldcs(po + i);
+            }
+        }
+    };
+    auto put = [&](int iz) {
+        double* s = zs + (iz % 3) * z.W;
+#pragma unroll
+        for (int k = 0; k < ZE; ++k) {
+            const int e = threadIdx.x + k * ZT;
+            if (e < z.W) s[e] = (e >= z.lo && e < z.hi) ? __dadd_rn(rv[k], __dmul_rn(beta, pv[k])) : 0.0;
+        }
+    };
+    load(0);
+    put(0);
+    if (g.nz > 1) load(1);
+    double acc = 0.0;
+    for (int iz = 0; iz < g.nz; ++iz) {
+        if (iz + 1 < g.nz) put(iz + 1);
+        if (iz + 2 < g.nz) load(iz + 2);
+        __syncthreads();
+        const double* c = zs + (iz % 3) * z.W;
+        const double* dn = zs + ((iz + 2) % 3) * z.W;
+        const double* up = zs + ((iz + 1) % 3) * z.W;
+        const ZDiag d = zdiag(g.nz, g.h, iz, sigma, sigmap);
+#pragma unroll
+        for (int k = 0; k < ZO; ++k) {
+            const int e = threadIdx.x + k * ZT;
+            if (e < z.Wo) {
+                const double pi = c[e + g.nx];
+                const double ap = zstencil(g, z, k, e, d, c, dn, up);
+                __stcs(p + iz * plane + z.base + g.nx + e, pi);
+                acc += pi * ap;
+            }
+        }
+        __syncthreads();
+    }
+    const double t = block_sum(acc, sh);
+    if (threadIdx.x == 0) partA[int64_t(sys) * nparts + blockIdx.x] = t;
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(ZT, MINB) cgz_xr(ZGeo g, int64_t N, int nl, int k0, int it,
+                                              const double* __restrict__ sig,
+                                              const double* __restrict__ sigp,
+                                              double* __restrict__ X, double* __restrict__ R,
+                                              const double* __restrict__ P,
+                                              const double* __restrict__ partA,
+                                              double* __restrict__ partB, int nparts,
+                                              SysState* __restrict__ st,
+                                              const int* __restrict__ act) {
+    extern __shared__ double zs[];
+    __shared__ double sh[ZT / 32];
+    __shared__ double bc;
+    const int sys = act[blockIdx.y];
+    SysState& S = st[sys];
+    if (S.done) return;
+    const int l = (k0 + sys) % nl;
+    const double pq = sum_parts(partA + int64_t(sys) * nparts, nparts, sh, &bc);
+    const double alpha = S.rr[it & 1] / pq;
+    ZIdx z;
+    zidx(g, z);
+    const int64_t plane = int64_t(g.nx) * g.ny;
+    double* x = X + int64_t(sys) * N;
+    double* r = R + int64_t(sys) * N;
+    const double* p = P + int64_t(sys) * N;
+    const double sigma = sig[l], sigmap = sigp[l];
+    double pv[ZE], xv[ZO], rv[ZO];
+    auto loadp = [&](int iz) {
+#pragma unroll
+        for (int k = 0; k < ZE; ++k) {
+            const int e = threadIdx.x + k * ZT;
+            if (e >= z.lo && e < z.hi) pv[k] = __ldcs(p + iz * plane + z.base + e);
+        }
+    };
+    auto loadxr = [&](int iz) {
+#pragma unroll
+        for (int k = 0; k < ZO; ++k) {
+            const int e = threadIdx.x + k * ZT;
+            if (e < z.Wo) {
+                xv[k] = __ldcs(x + iz * plane + z.base + g.nx + e);
+                rv[k] = __ldcs(r + iz * plane + z.base + g.nx + e);
+            }
+        }
+    };
+    auto put = [&](int iz) {
+        double* s = zs + (iz % 3) * z.W;
+#pragma unroll
+        for (int k = 0; k < ZE; ++k) {
+            const int e = threadIdx.x + k * ZT;
+            if (e < z.W) s[e] = (e >= z.lo && e < z.hi) ? pv[k] : 0.0;
+        }
+    };
+    loadp(0);
+    put(0);
+    if (g.nz > 1) loadp(1);
+    loadxr(0);
+    double acc = 0.0;
+    for (int iz = 0; iz < g.nz; ++iz) {
+        if (iz + 1 < g.nz) put(iz + 1);
+        if (iz + 2 < g.nz) loadp(iz + 2);
+        __syncthreads();
+        const double* c = zs + (iz % 3) * z.W;
+        const double* dn = zs + ((iz + 2) % 3) * z.W;
+        const double* up = zs + ((iz + 1) % 3) * z.W;
+        const ZDiag d = zdiag(g.nz, g.h, iz, sigma, sigmap);
+#pragma unroll
+        for (int k = 0; k < ZO; ++k) {
+            const int e = threadIdx.x + k * ZT;
+            if (e < z.Wo) {
+                const double q = zstencil(g, z, k, e, d, c, dn, up);
+                const int64_t i = iz * plane + z.base + g.nx + e;
+                __stcs(x + i, __dadd_rn(xv[k], __dmul_rn(alpha, c[e + g.nx])));
+                const double rn = __dsub_rn(rv[k], __dmul_rn(alpha, q));
+                __stcs(r + i, rn);
+                acc += rn * rn;
+            }
+        }
+        if (iz + 1 < g.nz) loadxr(iz + 1);  // in flight across the barrier and the next put
+        __syncthreads();
+    }
+    const double t = block_sum(acc, sh);
+    if (threadIdx.x == 0) partB[int64_t(sys) * nparts + blockIdx.x] = t;
+}
+
+// CTAs per SM the z-marching kernels are compiled for (3: 80 registers;
+// 4 forces 64 and spills: 0.84 vs 0.63 s on config 1); HYDOT_CG_ZOCC=4 for experiments
+int zmarch_occ() {
+    static const int o = [] {
+        const char* e = std::getenv("HYDOT_CG_ZOCC");
+        return e && e[0] == '4' ? 4 : 3;
+    }();
+    return o;
+}
+#define ZSEL(k) (zmarch_occ() == 3 ? k<3> : k<4>)
+
+// z-march tile height for an nx x ny plane (0 = tile does not fit: use the
+// vertex-parallel kernels); balanced over the tiles
+int zmarch_ty(int nx, int ny) {
+    static const bool on = [] {
+        const char* e = std::getenv("HYDOT_CG_ZMARCH");
+        return !(e && e[0] == '0');
+    }();
+    if (!on) return 0;
+    const int tmax = std::min(ny, std::min(ZT * ZE / nx - 2, ZT * ZO / nx));
+    if (tmax < 1) return 0;
+    const int ntiles = (ny + tmax - 1) / tmax;
+    return (ny + ntiles - 1) / ntiles;
+}
+
 // fixed-iteration / max-iteration finish: final relres, scale by inv_D
 __global__ void cg_finish(int64_t N, int nl, int k0, int it_total, double* __restrict__ X,
                           const double* __restrict__ invD, const double* __restrict__ partB,
@@ -407,7 +716,18 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
               CGStats* stats) {
     if (N >= (int64_t(1) << 24)) throw std::invalid_argument("fields_solve: grid too large for the 24-bit vertex decode");
     const int total = n_rhs * nl;
-    const int nparts = int((N + CV - 1) / CV);
+    int nparts = int((N + CV - 1) / CV);
+    // 7-point operator: z-marching kernels when the halo'ed tile fits
+    ZGeo zg{};
+    size_t zsmem = 0;
+    if constexpr (std::is_same_v<Op, Op7>) {
+        const int ty = zmarch_ty(op.g.nx, op.g.ny);
+        if (ty > 0) {
+            zg = ZGeo{op.g.nx, op.g.ny, op.g.nz, ty, op.g.h};
+            nparts = (op.g.ny + ty - 1) / ty;
+            zsmem = size_t(3) * size_t(ty + 2) * size_t(op.g.nx) * sizeof(double);
+        }
+    }
     // One batch of up to 24 GB (all systems iterate together, HBM-bound).
     // HYDOT_CG_L2_MB > 0 instead iterates L2-sized groups (32 N bytes per
     // system): measured slower on config 1 (1.4-2.8 s vs 0.96 s -- small
@@ -469,6 +789,15 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
         int it = 0;
         for (; it < limit; ++it) {
             dim3 grid = dim3(unsigned(nparts), unsigned(active.size()));
+            if (zsmem) {
+                ZSEL(cgz_pa)<<<grid, ZT, zsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
+                                                      pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
+                                                      tol, fixed_iters > 0, dact.as<int>());
+                c.check_launch();
+                ZSEL(cgz_xr)<<<grid, ZT, zsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), X, R.d(),
+                                                      pbuf(it), pA.d(), pB.d(), nparts, ss, dact.as<int>());
+                c.check_launch();
+            } else {
             cg_pa<<<grid, CT, 0, c.stream>>>(op, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
                                             pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
                                             tol, fixed_iters > 0, dact.as<int>());
@@ -476,6 +805,7 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
             cg_xr<<<grid, CT, 0, c.stream>>>(op, N, nl, k0, it, dsig.d(), dsigp.d(), X, R.d(),
                                             pbuf(it), pA.d(), pB.d(), nparts, ss, dact.as<int>());
             c.check_launch();
+            }
             if (fixed_iters <= 0 && (it % 8) == 7) {
                 HYDOT_CUDA(cudaMemcpyAsync(hst.data(), ss, size_t(nb) * sizeof(SysState),
                                            cudaMemcpyDeviceToHost, c.stream));
@@ -499,9 +829,14 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
         if (fixed_iters <= 0 && it >= limit) {
             // one more convergence check for systems finishing on the last step
             dim3 grid = dim3(unsigned(nparts), unsigned(active.size()));
-            cg_pa<<<grid, CT, 0, c.stream>>>(op, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
-                                            pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
-                                            tol, 0, dact.as<int>());
+            if (zsmem)
+                ZSEL(cgz_pa)<<<grid, ZT, zsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
+                                                      pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
+                                                      tol, 0, dact.as<int>());
+            else
+                cg_pa<<<grid, CT, 0, c.stream>>>(op, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
+                                                pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
+                                                tol, 0, dact.as<int>());
             c.check_launch();
         }
         {
