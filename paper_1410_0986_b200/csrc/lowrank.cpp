@@ -226,6 +226,15 @@ SVDd fast_thin_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, i
     return thin_svd(c, S, ld, trans, m, n, l, cat);  // lowrank.cpp:88-92
 }
 
+// HYDOT_TRACE_RANDSVD=1: one stderr line per sketch pass / Q = I decision
+bool trace_randsvd() {
+    static const bool on = [] {
+        const char* e = std::getenv("HYDOT_TRACE_RANDSVD");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
 Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, double eps, int p,
                int kprobe, uint64_t seed, Ledger* l, int cat, int r0) {
     Factor f;
@@ -245,6 +254,9 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
     while (true) {
         const int64_t rs = std::min<int64_t>(r + p, nmax);
         if (rs >= nmax && m <= n) {  // lowrank.cpp:159-164: Q = I_m
+            if (trace_randsvd())
+                fprintf(stderr, "[randsvd] m=%lld n=%lld r=%lld identity\n", (long long)m, (long long)n,
+                        (long long)r);
             identity = true;
             break;
         }
@@ -267,6 +279,10 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
         dgemm(c, false, false, m, kprobe, qc, 1.0, Q, m, QtP.d(), qc, 0.0, QQtP.d(), m);
         charge(l, cat, 2.0 * double(m) * double(kprobe) * double(qc));
         const double er = frob_diff(c, m, kprobe, P, m, QQtP.d(), m);
+        if (trace_randsvd())
+            fprintf(stderr, "[randsvd] m=%lld n=%lld r=%lld rs=%lld er=%.3e thr=%.3e %s\n", (long long)m,
+                    (long long)n, (long long)r, (long long)rs, er, eps * sigma_top,
+                    er <= eps * sigma_top ? "accept" : "reject");
         if (er <= eps * sigma_top) break;  // lowrank.cpp:176
         if (r >= nmax) {                   // :177-180
             f.flagged = true;
