@@ -67,6 +67,22 @@ void ledger_out(const Ledger& l, hydot_ledger* out) {
     out->kernel_tally += l.kernel_tally;
 }
 
+// the factor with V materialised (a lazy root V is formed on first use)
+Factor& dense(Ctx& c, hydot_factor f) {
+    materialize_v(c, f->f);
+    return f->f;
+}
+
+// recursive_lowrank keeps the root's V implicit for recompress
+// (HYDOT_LAZY_ROOT=0 materialises it at once)
+bool lazy_root_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("HYDOT_LAZY_ROOT");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 hydot_factor wrap(const std::shared_ptr<Ctx>& owner, Factor&& f) {
     auto* h = new hydot_factor_s;
     h->owner = owner;
@@ -346,6 +362,7 @@ hydot_status hydot_factor_download(hydot_ctx ctx, hydot_factor f, double* U, dou
         Ctx& c = ctx_of(ctx);
         if (!f) throw std::invalid_argument("null factor");
         auto kind = to_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+        if (V) dense(c, f);
         if (f->f.rank > 0) {
             if (U)
                 HYDOT_CUDA(cudaMemcpyAsync(U, f->f.U.d(), size_t(f->f.rows * f->f.rank) * 8, kind,
@@ -360,6 +377,14 @@ hydot_status hydot_factor_download(hydot_ctx ctx, hydot_factor f, double* U, dou
 
 hydot_status hydot_factor_device_ptrs(hydot_factor f, const double** U_dev, const double** V_dev) {
     if (!f) return HYDOT_EINVAL;
+    if (V_dev && f->f.lazy) {
+        if (!f->owner) return HYDOT_ERUNTIME;
+        hydot_status st = guard(f->owner.get(), [&] {
+            cudaSetDevice(f->owner->device);
+            dense(*f->owner, f);
+        });
+        if (st != HYDOT_OK) return st;
+    }
     if (U_dev) *U_dev = f->f.U.d();
     if (V_dev) *V_dev = f->f.V.d();
     return HYDOT_OK;
@@ -394,7 +419,7 @@ hydot_status hydot_agglomerate(hydot_ctx ctx, hydot_factor f1, hydot_factor f2, 
         Ctx& c = ctx_of(ctx);
         if (!f1 || !f2 || !out) throw std::invalid_argument("agglomerate: null factor");
         Ledger l;
-        Factor f = agglomerate(c, f1->f, f2->f, eps, seed, &l, rank_hint, p, kprobe);
+        Factor f = agglomerate(c, dense(c, f1), dense(c, f2), eps, seed, &l, rank_hint, p, kprobe);
         c.sync();
         ledger_out(l, ledger_h);
         *out = wrap(ctx->c, std::move(f));
@@ -493,7 +518,7 @@ hydot_status hydot_recursive_lowrank(hydot_ctx ctx, hydot_tree tree, double eps,
             };
         }
         RecOut r = recursive_lowrank(c, tree->t, eps, rows_per, cols, fn, o.seed, o.p, o.kprobe,
-                                     src_ids, o.node_offset);
+                                     src_ids, o.node_offset, lazy_root_enabled());
         c.sync();
         if (row_perm_h) std::memcpy(row_perm_h, r.row_perm.data(), r.row_perm.size() * sizeof(int));
         if (node_rank_h) std::memcpy(node_rank_h, r.node_rank.data(), r.node_rank.size() * sizeof(int));
@@ -522,7 +547,7 @@ hydot_status hydot_lr_matmat(hydot_ctx ctx, hydot_factor f, int trans, int b, co
     return guard(ctx ? ctx->c.get() : nullptr, [&] {
         Ctx& c = ctx_of(ctx);
         if (!f) throw std::invalid_argument("lr_matvec: null factor");
-        const Factor& F = f->f;
+        const Factor& F = dense(c, f);
         const int64_t in_rows = trans ? F.rows : F.cols, out_rows = trans ? F.cols : F.rows;
         if (b < 0 || ldx < in_rows || ldy < out_rows)
             throw std::invalid_argument(trans ? "lr_rmatvec: dimension mismatch"
@@ -554,7 +579,7 @@ hydot_status hydot_j_matmat(hydot_ctx ctx, hydot_factor f, int trans, int b, con
         Ctx& c = ctx_of(ctx);
         if (!f || !row_perm_dev || !eps_c_dev || n_lambda < 1 || n_c < 1 || b < 0)
             throw std::invalid_argument("J matmat: bad arguments");
-        const Factor& F = f->f;
+        const Factor& F = dense(c, f);
         const int64_t M = F.rows, N = F.cols, R = F.rank;
         const int64_t q = int64_t(b) * n_c;
         if (b == 0) return;
@@ -649,10 +674,10 @@ hydot_status hydot_dgemm(hydot_ctx ctx, int transa, int transb, int64_t m, int64
 
 // ------------------------------------------------------------------ pals --
 namespace {
-hydot::pals::Hop hop_of(const hydot_hop* op) {
+hydot::pals::Hop hop_of(Ctx& c, const hydot_hop* op) {
     if (!op || !op->H) throw std::invalid_argument("PaLS: null operator");
     hydot::pals::Hop h;
-    h.f = &op->H->f;
+    h.f = &dense(c, op->H);
     h.perm = op->row_perm_dev;
     return h;
 }
@@ -682,7 +707,7 @@ hydot_status hydot_pals_hmv(hydot_ctx ctx, const hydot_hop* op, int b, const dou
     return guard(ctx ? ctx->c.get() : nullptr, [&] {
         Ctx& c = ctx_of(ctx);
         if (b < 0) throw std::invalid_argument("Hmv: negative column count");
-        hydot::pals::hmv(c, hop_of(op), b, X_dev, ldx, Y_dev, ldy);
+        hydot::pals::hmv(c, hop_of(c, op), b, X_dev, ldx, Y_dev, ldy);
         c.sync();
     });
 }
@@ -694,7 +719,7 @@ hydot_status hydot_pals_solve_concentrations(hydot_ctx ctx, const hydot_hop* op,
         Ctx& c = ctx_of(ctx);
         if (!mu_dev || !w_dev || !y_dev || !ext_h || !c_h) throw std::invalid_argument("solve_concentrations: null argument");
         hydot::pals::Conc r =
-            hydot::pals::solve_concentrations(c, hop_of(op), mu_dev, w_dev, y_dev, ext_h, n_lambda, n_species);
+            hydot::pals::solve_concentrations(c, hop_of(c, op), mu_dev, w_dev, y_dev, ext_h, n_lambda, n_species);
         std::copy(r.c.begin(), r.c.end(), c_h);
         if (flagged_h) *flagged_h = r.flagged ? 1 : 0;
     });
@@ -743,7 +768,7 @@ hydot_status hydot_pals_reconstruct(hydot_ctx ctx, const hydot_hop* op, const hy
         rc.nu0 = cfg->nu0;
         rc.stagnation_tol = cfg->stagnation_tol;
         if (cfg->fixed_c_h) rc.fixed_c.assign(cfg->fixed_c_h, cfg->fixed_c_h + n_species);
-        hydot::pals::Recon r = hydot::pals::reconstruct(c, hop_of(op), geom_of(geom), ext_h, n_lambda, n_species,
+        hydot::pals::Recon r = hydot::pals::reconstruct(c, hop_of(c, op), geom_of(geom), ext_h, n_lambda, n_species,
                                                         y_dev, w_dev, p0, noise_norm, rc, mu_truth_dev);
         std::copy(r.p.alpha.begin(), r.p.alpha.end(), out->p.alpha);
         std::copy(r.p.beta.begin(), r.p.beta.end(), out->p.beta);
@@ -772,7 +797,7 @@ hydot_status hydot_factor_save(hydot_ctx ctx, hydot_factor f, const int* row_per
         Ctx& c = ctx_of(ctx);
         if (!f || !path || plen < 0 || (plen > 0 && !row_perm_h))
             throw std::invalid_argument("save_factor: bad arguments");
-        save_factor_file(c, path, f->f, row_perm_h, plen);
+        save_factor_file(c, path, dense(c, f), row_perm_h, plen);
     });
 }
 

@@ -154,10 +154,14 @@ SVDd thin_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, int64_
     return direct_svd(c, S, ld, trans, m, n);
 }
 
-SVDd fast_thin_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, int64_t n,
-                   Ledger* l, int cat) {
+namespace {
+// lazyU / lazyV: the caller accepts U (resp. V) as Q [Ur; 0] when the tall
+// branch produces it (the request is forwarded through the transposed
+// recursion); the SVDd's U (V) is then left empty.
+SVDd fast_thin_svd_impl(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, int64_t n,
+                        Ledger* l, int cat, LazyV* lazyU, LazyV* lazyV) {
     if (n >= 2 * m && m > 0) {  // lowrank.cpp:66-72
-        SVDd t = fast_thin_svd(c, S, ld, !trans, n, m, l, cat);
+        SVDd t = fast_thin_svd_impl(c, S, ld, !trans, n, m, l, cat, lazyV, lazyU);
         SVDd o;
         o.m = m;
         o.n = n;
@@ -217,6 +221,13 @@ SVDd fast_thin_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, i
             c.sync();  // host perm vector goes out of scope
         }
         // U = Q [Ur; 0]
+        if (lazyU) {
+            lazyU->q = std::move(qf);
+            lazyU->Z = std::move(Ur);
+            lazyU->zr = n;
+            lazyU->set = true;
+            return o;
+        }
         o.U = dalloc(c, size_t(m * n));
         fill(c, m, n, 0.0, o.U.d(), m);
         copy2d(c, n, n, Ur.d(), n, o.U.d(), m);
@@ -224,6 +235,25 @@ SVDd fast_thin_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, i
         return o;
     }
     return thin_svd(c, S, ld, trans, m, n, l, cat);  // lowrank.cpp:88-92
+}
+}  // namespace
+
+SVDd fast_thin_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, int64_t n,
+                   Ledger* l, int cat) {
+    return fast_thin_svd_impl(c, S, ld, trans, m, n, l, cat, nullptr, nullptr);
+}
+
+void materialize_v(Ctx& c, Factor& f) {
+    if (!f.lazy) return;
+    const LazyV& L = *f.lazy;
+    f.V = dalloc(c, size_t(std::max<int64_t>(f.cols * f.rank, 1)));
+    if (f.rank > 0) {
+        fill(c, f.cols, f.rank, 0.0, f.V.d(), f.cols);
+        copy2d(c, L.zr, f.rank, L.Z.d(), L.zr, f.V.d(), f.cols);
+        apply_q(c, L.q, false, f.rank, f.V.d(), f.cols);
+    }
+    c.sync();
+    f.lazy.reset();
 }
 
 // HYDOT_TRACE_RANDSVD=1: one stderr line per sketch pass / Q = I decision
@@ -236,7 +266,7 @@ bool trace_randsvd() {
 }
 
 Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, double eps, int p,
-               int kprobe, uint64_t seed, Ledger* l, int cat, int r0) {
+               int kprobe, uint64_t seed, Ledger* l, int cat, int r0, bool lazy_v) {
     Factor f;
     f.rows = m;
     f.cols = n;
@@ -305,7 +335,8 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
         ldb = n;
     }
     charge(l, cat, 2.0 * double(m) * double(n) * double(qc));
-    SVDd svdB = fast_thin_svd(c, Btp, ldb, true, qc, n, l, cat);
+    auto lz = std::make_shared<LazyV>();
+    SVDd svdB = fast_thin_svd_impl(c, Btp, ldb, true, qc, n, l, cat, nullptr, lazy_v ? lz.get() : nullptr);
     const std::vector<double>& s = svdB.s;
     const double s1 = s.empty() ? 0.0 : s[0];
     int64_t keep = 0;
@@ -313,7 +344,7 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
         if (s[i] > eps * s1 && s[i] > 0) keep = int64_t(i) + 1;  // :187-190
     f.rank = keep;
     f.U = dalloc(c, size_t(std::max<int64_t>(m * keep, 1)));
-    f.V = dalloc(c, size_t(std::max<int64_t>(n * keep, 1)));
+    if (!lz->set) f.V = dalloc(c, size_t(std::max<int64_t>(n * keep, 1)));
     if (keep > 0) {
         if (identity) {
             copy2d(c, m, keep, svdB.U.d(), qc, f.U.d(), m);  // I * U (exact)
@@ -321,12 +352,22 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
             dgemm(c, false, false, m, keep, qc, 1.0, svdY.U.d(), m, svdB.U.d(), qc, 0.0, f.U.d(),
                   m);  // :191
         }
-        copy2d(c, n, keep, svdB.V.d(), n, f.V.d(), n);  // :192
         DBuf sd = dalloc(c, size_t(keep));
         HYDOT_CUDA(cudaMemcpyAsync(sd.d(), s.data(), size_t(keep) * 8, cudaMemcpyHostToDevice,
                                    c.stream));
-        scale_cols(c, n, keep, f.V.d(), n, sd.d());
+        if (lz->set) {  // V = Q [Ur[:, :keep] S; 0], kept implicit
+            DBuf Z = dalloc(c, size_t(lz->zr * keep));
+            copy2d(c, lz->zr, keep, lz->Z.d(), lz->zr, Z.d(), lz->zr);
+            scale_cols(c, lz->zr, keep, Z.d(), lz->zr, sd.d());
+            lz->Z = std::move(Z);
+            f.lazy = lz;
+        } else {
+            copy2d(c, n, keep, svdB.V.d(), n, f.V.d(), n);  // :192
+            scale_cols(c, n, keep, f.V.d(), n, sd.d());
+        }
         c.sync();
+    } else if (lz->set) {
+        f.V = dalloc(c, 1);
     }
     charge(l, cat, 2.0 * double(m) * double(keep) * double(qc));
     charge(l, cat, 1.0 * double(n) * double(keep));  // :193-197
@@ -334,7 +375,8 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
 }
 
 Factor agglomerate(Ctx& c, const Factor& f1, const Factor& f2, double eps, uint64_t seed,
-                   Ledger* l, int rank_hint, int p, int kprobe) {
+                   Ledger* l, int rank_hint, int p, int kprobe, bool lazy_v) {
+    if (f1.lazy || f2.lazy) throw std::runtime_error("agglomerate: factor V not materialised");
     if (f1.cols != f2.cols)
         throw std::invalid_argument("agglomerate: column dimension mismatch");  // :324-325
     const int64_t n = f1.cols, r1 = f1.rank, r2 = f2.rank, m1 = f1.rows, m2 = f2.rows;
@@ -353,7 +395,7 @@ Factor agglomerate(Ctx& c, const Factor& f1, const Factor& f2, double eps, uint6
     copy2d(c, n, r2, f2.V.d(), n, Wt.d() + n * r1, n);
     const int hint = int(std::max<int64_t>({r1, r2, int64_t(rank_hint)}));
     Factor inner = randsvd(c, r1 + r2, n, Wt.d(), n, eps, p, kprobe, seed, l,
-                           HYDOT_CAT_AGGLOMERATION, hint);  // :344-346
+                           HYDOT_CAT_AGGLOMERATION, hint, lazy_v);  // :344-346
     Wt.release();
     const int64_t rp = inner.rank;
     out.rank = rp;
@@ -367,6 +409,7 @@ Factor agglomerate(Ctx& c, const Factor& f1, const Factor& f2, double eps, uint6
         charge(l, HYDOT_CAT_AGGLOMERATION, 2.0 * double(m2) * double(rp) * double(r2));
     }
     out.V = std::move(inner.V);
+    out.lazy = std::move(inner.lazy);
     out.flagged = f1.flagged || f2.flagged || inner.flagged;  // :357
     return out;
 }
@@ -382,12 +425,19 @@ Factor recompress(Ctx& c, const Factor& f, double eps, int rank, Ledger* l) {
     if (r == 0) return out;  // :554-558
     if (M < r || N < r) throw std::invalid_argument("recompress: rank exceeds a factor dimension");
     charge(l, HYDOT_CAT_RECOMPRESS, qr_flops(double(M), double(r)) + qr_flops(double(N), double(r)));
+    // V = Q_W [Z; 0] (lazy root): QR(V) = Q_W blkdiag(Q_Z, I) [R_Z; 0], so
+    // only the small zr x r Z is factored and Q_W is applied once at the end
+    const LazyV* lv = f.lazy.get();
     QRFact qu, qv;
     geqrf(c, M, r, f.U.d(), M, qu);  // :564
-    geqrf(c, N, r, f.V.d(), N, qv);
+    if (lv)
+        geqrf(c, lv->zr, r, lv->Z.d(), lv->zr, qv);
+    else
+        geqrf(c, N, r, f.V.d(), N, qv);
+    const int64_t vm = lv ? lv->zr : N;
     DBuf Ru = dalloc(c, size_t(r * r)), Rv = dalloc(c, size_t(r * r)), core = dalloc(c, size_t(r * r));
     extract_upper(c, r, qu.a.d(), M, Ru.d(), r);
-    extract_upper(c, r, qv.a.d(), N, Rv.d(), r);
+    extract_upper(c, r, qv.a.d(), vm, Rv.d(), r);
     dgemm(c, false, true, r, r, r, 1.0, Ru.d(), r, Rv.d(), r, 0.0, core.d(), r);  // :567
     charge(l, HYDOT_CAT_RECOMPRESS, 2.0 * double(r) * double(r) * double(r));
     // The core of a factor whose U / V columns are already orthogonal (every
@@ -422,13 +472,24 @@ Factor recompress(Ctx& c, const Factor& f, double eps, int rank, Ledger* l) {
         fill(c, M, keep, 0.0, out.U.d(), M);
         copy2d(c, r, keep, svd.U.d(), r, out.U.d(), M);
         apply_q(c, qu, false, keep, out.U.d(), M);
-        fill(c, N, keep, 0.0, out.V.d(), N);
-        copy2d(c, r, keep, svd.V.d(), r, out.V.d(), N);
         DBuf sd = dalloc(c, size_t(keep));
         HYDOT_CUDA(cudaMemcpyAsync(sd.d(), s.data(), size_t(keep) * 8, cudaMemcpyHostToDevice,
                                    c.stream));
-        scale_cols(c, r, keep, out.V.d(), N, sd.d());
-        apply_q(c, qv, false, keep, out.V.d(), N);
+        if (lv) {
+            DBuf small = dalloc(c, size_t(vm * keep));  // Q_Z [V~_k S_k; 0]
+            fill(c, vm, keep, 0.0, small.d(), vm);
+            copy2d(c, r, keep, svd.V.d(), r, small.d(), vm);
+            scale_cols(c, r, keep, small.d(), vm, sd.d());
+            apply_q(c, qv, false, keep, small.d(), vm);
+            fill(c, N, keep, 0.0, out.V.d(), N);
+            copy2d(c, vm, keep, small.d(), vm, out.V.d(), N);
+            apply_q(c, lv->q, false, keep, out.V.d(), N);
+        } else {
+            fill(c, N, keep, 0.0, out.V.d(), N);
+            copy2d(c, r, keep, svd.V.d(), r, out.V.d(), N);
+            scale_cols(c, r, keep, out.V.d(), N, sd.d());
+            apply_q(c, qv, false, keep, out.V.d(), N);
+        }
         c.sync();
     }
     charge(l, HYDOT_CAT_RECOMPRESS, 2.0 * double(M) * double(keep) * double(r));
@@ -515,7 +576,7 @@ double tolerance_schedule(double eps_d, int L, int N_r) {  // lowrank.cpp:540-54
 // chains (leaf_hint across leaves in DFS order, depth_hint per depth).
 RecOut recursive_lowrank(Ctx& c, const Tree& t, double eps, int rows_per, int64_t cols,
                          const BlockFn& block, uint64_t seed, int p, int kprobe,
-                         const std::vector<int>& source_ids, int node_offset) {
+                         const std::vector<int>& source_ids, int node_offset, bool lazy_root) {
     auto gsrc = [&](int s) { return source_ids.empty() ? s : source_ids[size_t(s)]; };
     RecOut res;
     res.node_rank.assign(t.nodes.size(), -1);
@@ -534,12 +595,13 @@ RecOut recursive_lowrank(Ctx& c, const Tree& t, double eps, int rows_per, int64_
         try {
             if (nd.is_leaf()) {
                 std::vector<Factor> parts;
+                const bool lazy_here = lazy_root && v == t.root;
                 for (int s : nd.idx) {
                     block(s, blk.d(), cols);
                     parts.push_back(randsvd(c, rows_per, cols, blk.d(), cols, eps, p, kprobe,
                                             seed + 0x9e3779b97f4a7c15ULL * uint64_t(gsrc(s) + 1),
                                             &res.ledger, HYDOT_CAT_LEAF,
-                                            std::max(1, leaf_hint + 2)));
+                                            std::max(1, leaf_hint + 2), lazy_here && nd.idx.size() == 1));
                     leaf_hint = int(parts.back().rank);
                 }
                 if (parts.empty()) throw std::runtime_error("empty leaf cluster");
@@ -547,12 +609,12 @@ RecOut recursive_lowrank(Ctx& c, const Tree& t, double eps, int rows_per, int64_
                 for (size_t i = 1; i < parts.size(); ++i)
                     f = agglomerate(c, f, parts[i], eps,
                                     seed + 0x517cc1b727220a95ULL * uint64_t(node_offset + v + 1), &res.ledger,
-                                    node_hint(depth), p, kprobe);
+                                    node_hint(depth), p, kprobe, lazy_here && i + 1 == parts.size());
             } else {
                 Factor fl = go(nd.left, depth + 1);
                 Factor fr = go(nd.right, depth + 1);
                 f = agglomerate(c, fl, fr, eps, seed + 0x2545f4914f6cdd1dULL * uint64_t(node_offset + v + 1),
-                                &res.ledger, node_hint(depth), p, kprobe);
+                                &res.ledger, node_hint(depth), p, kprobe, lazy_root && v == t.root);
             }
         } catch (const CudaError&) {
             throw;

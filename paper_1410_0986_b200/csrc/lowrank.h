@@ -2,10 +2,23 @@
 #pragma once
 
 #include <functional>
+#include <memory>
 
 #include "internal.h"
 
 namespace hydot {
+
+// V held implicitly as Q [Z; 0]: Q the (cols x zr) Householder QR of the
+// last tall factorisation, Z zr x rank (ld zr).  The root of the recursion
+// keeps its V this way so that recompress can factor the small Z instead of
+// the tall V (one cols x r QR and one Q application fewer); any other use
+// materialises V first (materialize_v).
+struct LazyV {
+    QRFact q;
+    DBuf Z;
+    int64_t zr = 0;
+    bool set = false;
+};
 
 // lowrank::LowRankFactor (lowrank.hpp:25-36) with U, V in device memory.
 struct Factor {
@@ -14,7 +27,10 @@ struct Factor {
     double tol = 0.0;
     int method = HYDOT_METHOD_NONE;
     bool flagged = false;
+    std::shared_ptr<LazyV> lazy;  // non-null: V is Q [Z; 0] (V itself empty)
 };
+// V := Q [Z; 0] in place (no-op for a dense factor)
+void materialize_v(Ctx& c, Factor& f);
 
 // thin SVD result: U m x k, s (host), V n x k
 struct SVDd {
@@ -33,11 +49,12 @@ SVDd thin_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, int64_
 
 // randsvd (lowrank.cpp:131-199) on A (m x n) given row-major: A(i,j) =
 // At[j + i*lda].
+// lazy_v: the result may keep V as Q [Z; 0] (see LazyV)
 Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, double eps, int p,
-               int kprobe, uint64_t seed, Ledger* l, int cat, int r0);
+               int kprobe, uint64_t seed, Ledger* l, int cat, int r0, bool lazy_v = false);
 
 Factor agglomerate(Ctx& c, const Factor& f1, const Factor& f2, double eps, uint64_t seed,
-                   Ledger* l, int rank_hint, int p, int kprobe);
+                   Ledger* l, int rank_hint, int p, int kprobe, bool lazy_v = false);
 
 Factor recompress(Ctx& c, const Factor& f, double eps, int rank, Ledger* l);
 
@@ -66,7 +83,8 @@ struct RecOut {
 using BlockFn = std::function<void(int, double*, int64_t)>;
 RecOut recursive_lowrank(Ctx& c, const Tree& t, double eps, int rows_per, int64_t cols,
                          const BlockFn& block, uint64_t seed, int p, int kprobe,
-                         const std::vector<int>& source_ids = {}, int node_offset = 0);
+                         const std::vector<int>& source_ids = {}, int node_offset = 0,
+                         bool lazy_root = false);
 
 // fileio.cpp: the reference's factor / block file formats
 void save_factor_file(Ctx& c, const std::string& path, const Factor& f, const int* perm, int64_t plen);

@@ -136,6 +136,37 @@ def test_recursive_dense_provider_parity(ctx, oracle):
     assert abs(led.kernel_tally - orec.ledger[4]) <= 1e-9 * orec.ledger[4]
 
 
+def test_recompress_lazy_root_matches_dense(ctx):
+    """The recursion's root keeps V as Q [Z; 0] (LazyV); recompress factors
+    the small Z instead of the tall V.  Same singular values / rank / J~ as
+    recompressing the materialised copy of the same factor."""
+    from paper_1410_0986_b200 import lowrank as lr
+    rng = np.random.default_rng(11)
+    ns, rows_per, cols = 4, 20, 3000   # tall W^T: the root takes the Q = I / tall-QR path
+    H = random_lowrank(rng, ns * rows_per, cols, 40, 1e-7)
+    pos = np.array([[(s % 2) * 1.0, (s // 2) * 1.0] for s in range(ns)])
+    tree = lr.ClusterTree(pos, [0, 0], [1, 1])
+    Ht = torch.as_tensor(H).cuda()
+
+    class Prov:
+        rows_per_source = rows_per
+        cols = 3000
+
+        @staticmethod
+        def block(s):
+            return Ht[s * rows_per:(s + 1) * rows_per]
+
+    eps = 1e-9
+    rec = lr.recursive_lowrank(ctx, tree, eps, Prov, lr.RecursiveOptions(seed=3))
+    lazy = lr.recompress(ctx, rec.factor, eps)          # first use: the implicit V
+    U, V = rec.factor.U, rec.factor.V                    # materialises V
+    dense = lr.recompress(ctx, lr.LowRankFactor.from_tensors(ctx, U, V), eps)
+    assert lazy.rank() == dense.rank()
+    A, B = lazy.dense().cpu().numpy(), dense.dense().cpu().numpy()
+    assert fro(A - B) <= 1e-12 * fro(B)
+    assert fro(U.cpu().numpy() @ V.cpu().numpy().T - B) <= 1e-9 * fro(B)
+
+
 def test_born_pipeline_parity_small(ctx, oracle):
     """fields -> Born blocks -> recursive compression -> recompress -> J~ products,
     device vs oracle on identical (device-computed) fields."""
