@@ -14,6 +14,9 @@
 // z-marching (cgz_pa / cgz_xr below): a CTA owns full x-rows of one system
 // and walks the z planes with three planes of p in shared memory -- config 1
 // fields 0.93 -> 0.63 s (36 -> 53 % of the 48 N B/iteration HBM figure).
+// With even nx the planes are streamed by bulk copies (cp.async.bulk +
+// mbarrier rings, cgzt_pa / cgzt_xr): 0.63 -> 0.50 s on config 1 (68 %),
+// 6.96 -> 5.45 s on config 2 (69 %).
 // Scalars never leave the device: each CTA sums its system's partials in a
 // fixed order (deterministic), CTA 0 publishes rr into a parity slot.  The
 // stencil and the vector updates use explicit _rn intrinsics in the oracle's
@@ -632,6 +635,234 @@ __global__ void __launch_bounds__(ZT, MINB) cgz_xr(ZGeo g, int64_t N, int nl, in
     if (threadIdx.x == 0) partB[int64_t(sys) * nparts + blockIdx.x] = t;
 }
 
+// ------------------------------------------- z-marching with bulk copies --
+// cgzt_xr: cgz_xr with the planes streamed by the bulk-copy engine (one
+// cp.async.bulk per plane and array, mbarrier completion) into shared-memory
+// rings -- p: 5 planes (3 in use, 2 in flight), x / r: 3 planes (1 in use,
+// 2 in flight).  No load instructions or prefetch registers in the loop and
+// one block barrier per plane.  Needs 16-byte aligned rows (nx even).
+constexpr int NSP = 5, NSX = 3;
+
+__device__ __forceinline__ uint32_t su32(const void* q) { return uint32_t(__cvta_generic_to_shared(q)); }
+__device__ __forceinline__ void mb_init(uint64_t* b) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mb_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     su32(dst)),
+                 "l"(src), "r"(bytes), "r"(su32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t par) {
+    asm volatile(
+        "{\n\t.reg .pred P;\nWAIT%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t@!P bra WAIT%=;\n}" ::"r"(
+            su32(b)),
+        "r"(par)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(ZT, 2) cgzt_xr(ZGeo g, int64_t N, int nl, int k0, int it,
+                                               const double* __restrict__ sig,
+                                               const double* __restrict__ sigp,
+                                               double* __restrict__ X, double* __restrict__ R,
+                                               const double* __restrict__ P,
+                                               const double* __restrict__ partA,
+                                               double* __restrict__ partB, int nparts,
+                                               SysState* __restrict__ st,
+                                               const int* __restrict__ act) {
+    extern __shared__ __align__(16) double zs[];
+    __shared__ __align__(8) uint64_t bar[NSP + NSX];
+    __shared__ double sh[ZT / 32];
+    __shared__ double bc;
+    const int sys = act[blockIdx.y];
+    SysState& S = st[sys];
+    if (S.done) return;
+    const int l = (k0 + sys) % nl;
+    const double pq = sum_parts(partA + int64_t(sys) * nparts, nparts, sh, &bc);
+    const double alpha = S.rr[it & 1] / pq;
+    ZIdx z;
+    zidx(g, z);
+    const int64_t plane = int64_t(g.nx) * g.ny;
+    double* x = X + int64_t(sys) * N;
+    double* r = R + int64_t(sys) * N;
+    const double* p = P + int64_t(sys) * N;
+    const double sigma = sig[l], sigmap = sigp[l];
+    double* pring = zs;                   // NSP x W
+    double* xring = zs + NSP * z.W;       // NSX x (x | r) x Wo
+    const uint32_t pbytes = uint32_t(z.hi - z.lo) * 8u, xbytes = uint32_t(z.Wo) * 8u;
+    auto issue_p = [&](int j) {
+        const int sl = j % NSP;
+        mb_expect(&bar[sl], pbytes);
+        bulk_load(pring + sl * z.W + z.lo, p + j * plane + z.base + z.lo, pbytes, &bar[sl]);
+    };
+    auto issue_xr = [&](int j) {
+        const int sl = j % NSX;
+        mb_expect(&bar[NSP + sl], 2u * xbytes);
+        const int64_t o = j * plane + z.base + g.nx;
+        bulk_load(xring + (2 * sl) * z.Wo, x + o, xbytes, &bar[NSP + sl]);
+        bulk_load(xring + (2 * sl + 1) * z.Wo, r + o, xbytes, &bar[NSP + sl]);
+    };
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NSP + NSX; ++i) mb_init(&bar[i]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int j = 0; j < 3 && j < g.nz; ++j) issue_p(j);
+        for (int j = 0; j < 2 && j < g.nz; ++j) issue_xr(j);
+    }
+    double acc = 0.0;
+    for (int iz = 0; iz < g.nz; ++iz) {
+        if (iz > 0) __syncthreads();  // plane iz-1's reads are done: its slots may refill
+        if (threadIdx.x == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (iz + 3 < g.nz) issue_p(iz + 3);    // into p(iz-2)'s slot
+            if (iz + 2 < g.nz) issue_xr(iz + 2);   // into x/r(iz-1)'s slot
+        }
+        if (iz == 0) mb_wait(&bar[0], 0);
+        if (iz + 1 < g.nz) mb_wait(&bar[(iz + 1) % NSP], uint32_t(((iz + 1) / NSP) & 1));
+        mb_wait(&bar[NSP + iz % NSX], uint32_t((iz / NSX) & 1));
+        const double* c = pring + (iz % NSP) * z.W;
+        const double* dn = pring + ((iz + NSP - 1) % NSP) * z.W;
+        const double* up = pring + ((iz + 1) % NSP) * z.W;
+        const double* xs = xring + (2 * (iz % NSX)) * z.Wo;
+        const double* rs = xs + z.Wo;
+        const ZDiag d = zdiag(g.nz, g.h, iz, sigma, sigmap);
+#pragma unroll
+        for (int k = 0; k < ZO; ++k) {
+            const int e = threadIdx.x + k * ZT;
+            if (e < z.Wo) {
+                const double q = zstencil(g, z, k, e, d, c, dn, up);
+                const int64_t i = iz * plane + z.base + g.nx + e;
+                __stcs(x + i, __dadd_rn(xs[e], __dmul_rn(alpha, c[e + g.nx])));
+                const double rn = __dsub_rn(rs[e], __dmul_rn(alpha, q));
+                __stcs(r + i, rn);
+                acc += rn * rn;
+            }
+        }
+    }
+    const double t = block_sum(acc, sh);
+    if (threadIdx.x == 0) partB[int64_t(sys) * nparts + blockIdx.x] = t;
+}
+
+// cgzt_pa: cgz_pa with r and p_old streamed by bulk copies into a 3-plane
+// ring; p_new = r + beta p_old is formed once per vertex into a 4-plane ring
+// (4 slots: the plane written at step iz was last read two barriers ago, so
+// one block barrier per plane suffices).
+constexpr int NSR = 3;
+
+__global__ void __launch_bounds__(ZT, 2) cgzt_pa(ZGeo g, int64_t N, int nl, int k0, int it,
+                                               const double* __restrict__ sig,
+                                               const double* __restrict__ sigp,
+                                               const double* __restrict__ R,
+                                               const double* __restrict__ Pold,
+                                               double* __restrict__ Pnew, double* __restrict__ partA,
+                                               const double* __restrict__ partB, int nparts,
+                                               SysState* __restrict__ st, double tol, int fixed,
+                                               const int* __restrict__ act) {
+    extern __shared__ __align__(16) double zs[];
+    __shared__ __align__(8) uint64_t bar[NSR];
+    __shared__ double sh[ZT / 32];
+    __shared__ double bc;
+    const int sys = act[blockIdx.y];
+    SysState& S = st[sys];
+    if (S.done) return;
+    const int l = (k0 + sys) % nl;
+    double beta = 0.0;
+    const int slot = it & 1;
+    if (it > 0) {
+        const double rr_new = sum_parts(partB + int64_t(sys) * nparts, nparts, sh, &bc);
+        const double rr_old = S.rr[slot ^ 1];
+        const double relres = sqrt(rr_new) / S.bnorm;
+        if (!fixed && relres <= tol) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                S.done = 1;
+                S.iters = it;
+                S.relres = relres;
+            }
+            return;
+        }
+        beta = rr_new / rr_old;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            S.rr[slot] = rr_new;
+            S.relres = relres;
+            S.iters = it;
+        }
+    }
+    ZIdx z;
+    zidx(g, z);
+    const int64_t plane = int64_t(g.nx) * g.ny;
+    const double* r = R + int64_t(sys) * N;
+    const double* po = Pold + int64_t(sys) * N;
+    double* p = Pnew + int64_t(sys) * N;
+    const double sigma = sig[l], sigmap = sigp[l];
+    double* raw = zs;                 // NSR x (r | p_old) x W
+    double* pn = zs + 2 * NSR * z.W;  // 4 x W
+    const uint32_t bytes = uint32_t(z.hi - z.lo) * 8u;
+    auto issue = [&](int j) {
+        const int sl = j % NSR;
+        mb_expect(&bar[sl], 2u * bytes);
+        const int64_t o = j * plane + z.base + z.lo;
+        bulk_load(raw + (2 * sl) * z.W + z.lo, r + o, bytes, &bar[sl]);
+        bulk_load(raw + (2 * sl + 1) * z.W + z.lo, po + o, bytes, &bar[sl]);
+    };
+    auto convert = [&](int j) {  // pn[j % 4] = r + beta p_old on the in-grid rows
+        const int sl = j % NSR;
+        mb_wait(&bar[sl], uint32_t((j / NSR) & 1));
+        const double* rs = raw + (2 * sl) * z.W;
+        const double* ps = rs + z.W;
+        double* out = pn + (j & 3) * z.W;
+#pragma unroll
+        for (int k = 0; k < ZE; ++k) {
+            const int e = threadIdx.x + k * ZT;
+            if (e >= z.lo && e < z.hi) out[e] = __dadd_rn(rs[e], __dmul_rn(beta, ps[e]));
+        }
+    };
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NSR; ++i) mb_init(&bar[i]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int e = threadIdx.x; e < 4 * z.W; e += ZT) pn[e] = 0.0;  // out-of-grid halo rows
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int j = 0; j < NSR && j < g.nz; ++j) issue(j);
+    convert(0);
+    __syncthreads();
+    if (threadIdx.x == 0 && NSR < g.nz) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(NSR);
+    }
+    double acc = 0.0;
+    for (int iz = 0; iz < g.nz; ++iz) {
+        const int j = iz + 1;
+        if (j < g.nz) convert(j);
+        __syncthreads();
+        if (threadIdx.x == 0 && j + NSR < g.nz) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(j + NSR);  // into raw(j)'s slot, converted above
+        }
+        const double* c = pn + (iz & 3) * z.W;
+        const double* dn = pn + ((iz + 3) & 3) * z.W;
+        const double* up = pn + ((iz + 1) & 3) * z.W;
+        const ZDiag d = zdiag(g.nz, g.h, iz, sigma, sigmap);
+#pragma unroll
+        for (int k = 0; k < ZO; ++k) {
+            const int e = threadIdx.x + k * ZT;
+            if (e < z.Wo) {
+                const double pi = c[e + g.nx];
+                const double ap = zstencil(g, z, k, e, d, c, dn, up);
+                __stcs(p + iz * plane + z.base + g.nx + e, pi);
+                acc += pi * ap;
+            }
+        }
+    }
+    const double t = block_sum(acc, sh);
+    if (threadIdx.x == 0) partA[int64_t(sys) * nparts + blockIdx.x] = t;
+}
+
 // CTAs per SM the z-marching kernels are compiled for (3: 80 registers;
 // 4 forces 64 and spills: 0.84 vs 0.63 s on config 1); HYDOT_CG_ZOCC=4 for experiments
 int zmarch_occ() {
@@ -642,6 +873,15 @@ int zmarch_occ() {
     return o;
 }
 #define ZSEL(k) (zmarch_occ() == 3 ? k<3> : k<4>)
+
+// bulk-copy x/r kernel for even nx (HYDOT_CG_BULK=0 keeps the register one)
+bool zbulk_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("HYDOT_CG_BULK");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 // z-march tile height for an nx x ny plane (0 = tile does not fit: use the
 // vertex-parallel kernels); balanced over the tiles
@@ -719,13 +959,32 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
     int nparts = int((N + CV - 1) / CV);
     // 7-point operator: z-marching kernels when the halo'ed tile fits
     ZGeo zg{};
-    size_t zsmem = 0;
+    size_t zsmem = 0, ztsmem = 0, ztpsmem = 0;
     if constexpr (std::is_same_v<Op, Op7>) {
         const int ty = zmarch_ty(op.g.nx, op.g.ny);
         if (ty > 0) {
             zg = ZGeo{op.g.nx, op.g.ny, op.g.nz, ty, op.g.h};
             nparts = (op.g.ny + ty - 1) / ty;
             zsmem = size_t(3) * size_t(ty + 2) * size_t(op.g.nx) * sizeof(double);
+            if (op.g.nx % 2 == 0 && zbulk_on()) {
+                ztsmem = size_t(NSP * (ty + 2) + NSX * 2 * ty) * size_t(op.g.nx) * sizeof(double);
+                ztpsmem = size_t((2 * NSR + 4) * (ty + 2)) * size_t(op.g.nx) * sizeof(double);
+                static bool attr = false;
+                if (!attr) {
+                    HYDOT_CUDA(cudaFuncSetAttribute(cgzt_xr, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    200 * 1024));
+                    HYDOT_CUDA(cudaFuncSetAttribute(cgzt_pa, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    200 * 1024));
+                    // same shared-memory carve-out for both kernels of an
+                    // iteration (no SM reconfiguration between launches)
+                    if (std::getenv("HYDOT_CG_CARVE")) {
+                        const int cv = std::atoi(std::getenv("HYDOT_CG_CARVE"));
+                        HYDOT_CUDA(cudaFuncSetAttribute(cgz_pa<3>, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
+                        HYDOT_CUDA(cudaFuncSetAttribute(cgzt_xr, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
+                    }
+                    attr = true;
+                }
+            }
         }
     }
     // One batch of up to 24 GB (all systems iterate together, HBM-bound).
@@ -790,12 +1049,22 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
         for (; it < limit; ++it) {
             dim3 grid = dim3(unsigned(nparts), unsigned(active.size()));
             if (zsmem) {
-                ZSEL(cgz_pa)<<<grid, ZT, zsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
-                                                      pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
-                                                      tol, fixed_iters > 0, dact.as<int>());
+                if (ztpsmem)
+                    cgzt_pa<<<grid, ZT, ztpsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
+                                                             pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
+                                                             tol, fixed_iters > 0, dact.as<int>());
+                else
+                    ZSEL(cgz_pa)<<<grid, ZT, zsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
+                                                                pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts,
+                                                                ss, tol, fixed_iters > 0, dact.as<int>());
                 c.check_launch();
-                ZSEL(cgz_xr)<<<grid, ZT, zsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), X, R.d(),
-                                                      pbuf(it), pA.d(), pB.d(), nparts, ss, dact.as<int>());
+                if (ztsmem)
+                    cgzt_xr<<<grid, ZT, ztsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), X, R.d(),
+                                                            pbuf(it), pA.d(), pB.d(), nparts, ss, dact.as<int>());
+                else
+                    ZSEL(cgz_xr)<<<grid, ZT, zsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), X,
+                                                                R.d(), pbuf(it), pA.d(), pB.d(), nparts, ss,
+                                                                dact.as<int>());
                 c.check_launch();
             } else {
             cg_pa<<<grid, CT, 0, c.stream>>>(op, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
@@ -829,7 +1098,11 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
         if (fixed_iters <= 0 && it >= limit) {
             // one more convergence check for systems finishing on the last step
             dim3 grid = dim3(unsigned(nparts), unsigned(active.size()));
-            if (zsmem)
+            if (ztpsmem)
+                cgzt_pa<<<grid, ZT, ztpsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
+                                                         pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
+                                                         tol, 0, dact.as<int>());
+            else if (zsmem)
                 ZSEL(cgz_pa)<<<grid, ZT, zsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
                                                       pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
                                                       tol, 0, dact.as<int>());

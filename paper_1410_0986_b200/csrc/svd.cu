@@ -329,7 +329,8 @@ __host__ __device__ constexpr int circ_col(int pos, int r, int np) {
 template <int R, int RT, int RBk>
 __global__ void __launch_bounds__(RT, 1) jacobi_rblk_k(int64_t m, int n, int nb, const int2* __restrict__ bpairs,
                                                       double* __restrict__ U, int64_t ldu, double tol,
-                                                      int* __restrict__ counters, int* __restrict__ sweeps_out) {
+                                                      int* __restrict__ counters, int* __restrict__ sweeps_out,
+                                                      int inner) {
     constexpr int NW = RT / 32;
     constexpr int RC = 2 * RBk;          // columns per block pair
     constexpr int RNV = 3 * RBk;         // dot products per sub-round
@@ -361,6 +362,7 @@ __global__ void __launch_bounds__(RT, 1) jacobi_rblk_k(int64_t m, int n, int nb,
                         const int64_t i = threadIdx.x + int64_t(rr) * RT;
                         x[rr][j] = (col[j] >= 0 && i < m) ? __ldcg(U + i + int64_t(col[j]) * ldu) : 0.0;
                     }
+                for (int rep = 0; rep < inner; ++rep)
 #pragma unroll
                 for (int sr = 0; sr < RC - 1; ++sr) {
                     double part[NVP];  // the sub-round's dot products, padded
@@ -584,7 +586,13 @@ void launch_rblk_t(Ctx& c, int64_t m, int64_t n, double* U, int64_t ldu, double 
     int grid = std::max(1, std::min(npb / 2, per_sm * c.num_sms));
     int64_t mm = m;
     int nn = int(n), nbb = nb;
-    void* args[] = {&mm, &nn, &nbb, &bp, &U, &ldu, &tol, &counters, &sweeps_out};
+    // HYDOT_JACOBI_INNER: mini-sweeps per block-pair visit (experiments)
+    static const int inner_env = [] {
+        const char* e = std::getenv("HYDOT_JACOBI_INNER");
+        return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    int inner = inner_env;
+    void* args[] = {&mm, &nn, &nbb, &bp, &U, &ldu, &tol, &counters, &sweeps_out, &inner};
     HYDOT_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_rblk_k<R, T, B>, dim3(grid), dim3(T), args, 0,
                                            c.stream));
     c.count();
