@@ -48,7 +48,26 @@ bool presort_tall() {
 // SVD of an n x n upper triangle R1 that came from the QR of norm-ordered
 // columns: R1^T = Q2 R2, Jacobi on L = R2^T = Ux S Vx^T, so R1 = Ux S (Q2 Vx)^T.
 // Ux -> U (n x n), Q2 Vx -> V (n x n).
+// HYDOT_DUMP_CORES=dir: write every R1 (n >= 256) of the identity path as
+// raw float64 (column-major) for offline preconditioning experiments
+void dump_core(Ctx& c, const char* tag, int64_t m, int64_t n, const double* A, int64_t lda) {
+    static const char* dir = std::getenv("HYDOT_DUMP_CORES");
+    static int count = 0;
+    if (!dir || n < 256 || count >= 12) return;
+    std::vector<double> h(size_t(m * n));
+    DBuf t = dalloc(c, size_t(m * n));
+    copy2d(c, m, n, A, lda, t.d(), m);
+    c.d2h(h.data(), t.d(), h.size());
+    char path[512];
+    snprintf(path, sizeof path, "%s/%s_%02d_%lldx%lld.f64", dir, tag, count++, (long long)m, (long long)n);
+    if (FILE* f = fopen(path, "wb")) {
+        fwrite(h.data(), 8, h.size(), f);
+        fclose(f);
+    }
+}
+
 void svd_of_sorted_r(Ctx& c, int64_t n, const double* R1, double* U, std::vector<double>& s, double* V) {
+    dump_core(c, "r1", n, n, R1, n);
     QRFact q2;
     DBuf T = dalloc(c, size_t(n * n)), R2 = dalloc(c, size_t(n * n));
     transpose(c, n, n, R1, n, T.d(), n);  // R1^T
@@ -87,6 +106,7 @@ void jacobi_precond(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, 
                                cudaMemcpyHostToDevice, c.stream));
     DBuf Xp = dalloc(c, size_t(m * n));
     gather_cols(c, m, n, X, ldx, dperm.as<int>(), Xp.d(), m);
+    dump_core(c, "y", m, n, Xp.d(), m);
     QRFact q1, q2;
     geqrf(c, m, n, Xp.d(), m, q1);
     Xp.release();
