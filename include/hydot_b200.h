@@ -173,6 +173,12 @@ hydot_status hydot_factor_info(hydot_factor f, int64_t* rows, int64_t* cols, int
 /* copy U (rows x r) and V (cols x r) out; to_host selects host/device dst */
 hydot_status hydot_factor_download(hydot_ctx ctx, hydot_factor f, double* U, double* V,
                                    int to_host);
+/* device pointers of U and V.  A factor returned by
+ * hydot_recursive_lowrank holds its V implicitly (Householder Q of the root
+ * merge times a small matrix) until first use: asking for V here (or
+ * downloading it, or any product / save / agglomerate) forms it on the
+ * owning context's stream; hydot_recompress consumes the implicit form
+ * directly.  HYDOT_LAZY_ROOT=0 forms it at once. */
 hydot_status hydot_factor_device_ptrs(hydot_factor f, const double** U_dev, const double** V_dev);
 void hydot_factor_free(hydot_factor f);
 

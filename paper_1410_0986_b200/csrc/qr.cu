@@ -217,8 +217,18 @@ __global__ void __launch_bounds__(CT) qr_panel_cta(int mr, int jb, double* __res
         const int nq = jb - c - 1;
         for (int t = warp; t < nq; t += NW) {
             const double* pq = slab + int64_t(c + 1 + t) * mr;
-            double s = 0.0;
-            for (int i = c + 1 + lane; i < mr; i += 32) s += x[i] * pq[i];
+            // four independent partial sums: the dependent FMA chain over
+            // the column was the critical path
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int i = c + 1 + lane;
+            for (; i + 96 < mr; i += 128) {
+                s0 += x[i] * pq[i];
+                s1 += x[i + 32] * pq[i + 32];
+                s2 += x[i + 64] * pq[i + 64];
+                s3 += x[i + 96] * pq[i + 96];
+            }
+            for (; i < mr; i += 32) s0 += x[i] * pq[i];
+            double s = (s0 + s1) + (s2 + s3);
             for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
             if (lane == 0) {
                 s_dot[c + 1 + t] = s;
@@ -226,6 +236,7 @@ __global__ void __launch_bounds__(CT) qr_panel_cta(int mr, int jb, double* __res
             }
         }
         double nacc = 0.0;
+#pragma unroll 2
         for (int i = c + 1 + threadIdx.x; i < mr; i += CT) nacc += x[i] * x[i];
         for (int o = 16; o > 0; o >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, o);
         if (lane == 0) s_nrm[warp] = nacc;
@@ -247,6 +258,7 @@ __global__ void __launch_bounds__(CT) qr_panel_cta(int mr, int jb, double* __res
                 const double wq = s_pc[q] + scal * s_dot[q];
                 double* pq = slab + int64_t(q) * mr;
                 if (lane == 0) pq[c] -= tau * wq;  // v_c = 1
+#pragma unroll 4
                 for (int i = c + 1 + lane; i < mr; i += 32) pq[i] -= tau * (x[i] * scal) * wq;
             }
         }
