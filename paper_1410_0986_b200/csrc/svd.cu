@@ -323,18 +323,130 @@ __host__ __device__ constexpr int circ_col(int pos, int r, int np) {
     return pos == 0 ? 0 : ((pos - 1 + r) % (np - 1)) + 1;
 }
 
-// RBk = block width: 4 (8 columns per pair, 28-pair mini-sweep) or 2 (4
-// columns, 6 pairs) -- the narrow form keeps cores up to 6144 rows in
-// registers (12 rows x 4 columns per thread at 512 threads)
+// Sub-round schedules of a block pair (columns 0..RBk-1 = block A, RBk..2RBk-1
+// = block B), RBk disjoint column pairs each:
+//   kind 0 "mini":  circle method over all 2 RBk columns (2 RBk - 1 sub-rounds)
+//   kind 1 "cross": pair (k, RBk + (k + t) % RBk) (RBk sub-rounds: A x B once)
+//   kind 2 "intra": circle method inside A and inside B (RBk - 1 sub-rounds)
+template <int RBk>
+__device__ __forceinline__ void sched_pair(int kind, int sr, int k, int& p, int& o) {
+    constexpr int RC = 2 * RBk;
+    if (kind == 0) {
+        p = circ_col(k, sr, RC);
+        o = circ_col(RC - 1 - k, sr, RC);
+    } else if (kind == 1) {
+        p = k;
+        o = RBk + (k + sr) % RBk;
+    } else {
+        const int blk = k / (RBk / 2), kk = k % (RBk / 2);
+        p = blk * RBk + circ_col(kk, sr, RBk);
+        o = blk * RBk + circ_col(RBk - 1 - kk, sr, RBk);
+    }
+}
+
+// One sub-round on the register-resident block pair x: the RBk column-pair
+// dot products reduced over the CTA (warp transpose-reduce, one partial per
+// warp), a warp per pair forms the rotation from the actual column dots,
+// every thread applies the rotations to its rows.
+template <int R, int RT, int RBk>
+__device__ __forceinline__ void rblk_subround(int kind, int sr, double (&x)[R][2 * RBk], double (*red)[RT / 32],
+                                              double* tot, int lane, int warp, double tol, int& mine) {
+    constexpr int NW = RT / 32;
+    constexpr int RNV = 3 * RBk;
+    constexpr int NVP = RNV <= 8 ? 8 : 16;
+    double part[NVP];  // the sub-round's dot products, padded
+#pragma unroll
+    for (int k = 0; k < RBk; ++k) {
+        int p, o;
+        sched_pair<RBk>(kind, sr, k, p, o);
+        double a = 0.0, b = 0.0, g = 0.0;
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+            a += x[rr][p] * x[rr][p];
+            b += x[rr][o] * x[rr][o];
+            g += x[rr][p] * x[rr][o];
+        }
+        part[3 * k] = a;
+        part[3 * k + 1] = b;
+        part[3 * k + 2] = g;
+    }
+#pragma unroll
+    for (int v = RNV; v < NVP; ++v) part[v] = 0.0;
+    // warp reduce: plain butterflies down to NVP lanes, then a
+    // transpose-reduce -- lane l ends with quantity (l % NVP)
+#pragma unroll
+    for (int sft = 16; sft >= NVP; sft >>= 1)
+#pragma unroll
+        for (int v = 0; v < RNV; ++v) part[v] += __shfl_xor_sync(0xffffffffu, part[v], sft);
+#pragma unroll
+    for (int sft = NVP / 2; sft >= 1; sft >>= 1) {
+        const bool upper = (lane & sft) != 0;
+#pragma unroll
+        for (int j = 0; j < sft; ++j) {
+            const double send = upper ? part[j] : part[j + sft];
+            const double keep = upper ? part[j + sft] : part[j];
+            part[j] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+        }
+    }
+    if (lane < RNV) red[lane][warp] = part[0];
+    __syncthreads();
+    for (int k = warp; k < RBk; k += NW) {  // a warp finishes pair k, forms its rotation once
+        double A = lane < NW ? red[3 * k][lane] : 0.0;
+        double Bv = lane < NW ? red[3 * k + 1][lane] : 0.0;
+        double G = lane < NW ? red[3 * k + 2][lane] : 0.0;
+#pragma unroll
+        for (int sft = NW / 2; sft > 0; sft >>= 1) {
+            A += __shfl_xor_sync(0xffffffffu, A, sft);
+            Bv += __shfl_xor_sync(0xffffffffu, Bv, sft);
+            G += __shfl_xor_sync(0xffffffffu, G, sft);
+        }
+        if (lane == 0) {
+            double cs = 1.0, sn = 0.0, on = 0.0;
+            if (G != 0.0 && fabs(G) > tol * sqrt(A * Bv)) {
+                rot_params(A, Bv, G, cs, sn);
+                on = 1.0;
+            }
+            tot[3 * k] = cs;
+            tot[3 * k + 1] = sn;
+            tot[3 * k + 2] = on;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < RBk; ++k) {
+        int p, o;
+        sched_pair<RBk>(kind, sr, k, p, o);
+        if (tot[3 * k + 2] != 0.0) {
+            const double cs = tot[3 * k], sn = tot[3 * k + 1];
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) {
+                const double xp = x[rr][p], xo = x[rr][o];
+                x[rr][p] = cs * xp - sn * xo;
+                x[rr][o] = sn * xp + cs * xo;
+            }
+            if (threadIdx.x == 0) ++mine;
+        }
+    }
+}
+
+// RBk = block width: 4 (8 columns per pair) or 2 (4 columns) -- the narrow
+// form keeps cores up to 6144 rows in registers (12 rows x 4 columns per
+// thread at 512 threads).
+// Schedule per sweep (cross = 1, the default): in the sweep's first round
+// every block's own column pairs (intra, RBk - 1 sub-rounds), then in every
+// round the A x B cross pairs of the block pair (RBk sub-rounds): each
+// column pair once per sweep, ~n sub-rounds per sweep.  cross = 0 runs the
+// full 2 RBk - 1 sub-round mini-sweep on every block-pair visit (~2n per
+// sweep): on the path's cores cross needs 0-1 more sweeps but 34-42 % fewer
+// sub-rounds (offline, dumped cores).
 template <int R, int RT, int RBk>
 __global__ void __launch_bounds__(RT, 1) jacobi_rblk_k(int64_t m, int n, int nb, const int2* __restrict__ bpairs,
                                                       double* __restrict__ U, int64_t ldu, double tol,
                                                       int* __restrict__ counters, int* __restrict__ sweeps_out,
-                                                      int inner) {
+                                                      int cross) {
     constexpr int NW = RT / 32;
     constexpr int RC = 2 * RBk;          // columns per block pair
     constexpr int RNV = 3 * RBk;         // dot products per sub-round
-    constexpr int NVP = RNV <= 8 ? 8 : 16;  // padded to a power of two
     cg::grid_group grid = cg::this_grid();
     __shared__ double red[RNV][NW];
     __shared__ double tot[RNV];
@@ -362,80 +474,19 @@ __global__ void __launch_bounds__(RT, 1) jacobi_rblk_k(int64_t m, int n, int nb,
                         const int64_t i = threadIdx.x + int64_t(rr) * RT;
                         x[rr][j] = (col[j] >= 0 && i < m) ? __ldcg(U + i + int64_t(col[j]) * ldu) : 0.0;
                     }
-                for (int rep = 0; rep < inner; ++rep)
+                if (cross) {
+                    if (r == 0) {
 #pragma unroll
-                for (int sr = 0; sr < RC - 1; ++sr) {
-                    double part[NVP];  // the sub-round's dot products, padded
-#pragma unroll
-                    for (int k = 0; k < RBk; ++k) {
-                        const int p = circ_col(k, sr, RC), o = circ_col(RC - 1 - k, sr, RC);
-                        double a = 0.0, b = 0.0, g = 0.0;
-#pragma unroll
-                        for (int rr = 0; rr < R; ++rr) {
-                            a += x[rr][p] * x[rr][p];
-                            b += x[rr][o] * x[rr][o];
-                            g += x[rr][p] * x[rr][o];
-                        }
-                        part[3 * k] = a;
-                        part[3 * k + 1] = b;
-                        part[3 * k + 2] = g;
+                        for (int sr = 0; sr < RBk - 1; ++sr)
+                            rblk_subround<R, RT, RBk>(2, sr, x, red, tot, lane, warp, tol, mine);
                     }
 #pragma unroll
-                    for (int v = RNV; v < NVP; ++v) part[v] = 0.0;
-                    // warp reduce: plain butterflies down to NVP lanes, then a
-                    // transpose-reduce -- lane l ends with quantity (l % NVP)
+                    for (int t = 0; t < RBk; ++t)
+                        rblk_subround<R, RT, RBk>(1, t, x, red, tot, lane, warp, tol, mine);
+                } else {
 #pragma unroll
-                    for (int sft = 16; sft >= NVP; sft >>= 1)
-#pragma unroll
-                        for (int v = 0; v < RNV; ++v) part[v] += __shfl_xor_sync(0xffffffffu, part[v], sft);
-#pragma unroll
-                    for (int sft = NVP / 2; sft >= 1; sft >>= 1) {
-                        const bool upper = (lane & sft) != 0;
-#pragma unroll
-                        for (int j = 0; j < sft; ++j) {
-                            const double send = upper ? part[j] : part[j + sft];
-                            const double keep = upper ? part[j + sft] : part[j];
-                            part[j] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
-                        }
-                    }
-                    if (lane < RNV) red[lane][warp] = part[0];
-                    __syncthreads();
-                    for (int k = warp; k < RBk; k += NW) {  // a warp finishes pair k, forms its rotation once
-                        double A = lane < NW ? red[3 * k][lane] : 0.0;
-                        double Bv = lane < NW ? red[3 * k + 1][lane] : 0.0;
-                        double G = lane < NW ? red[3 * k + 2][lane] : 0.0;
-#pragma unroll
-                        for (int sft = NW / 2; sft > 0; sft >>= 1) {
-                            A += __shfl_xor_sync(0xffffffffu, A, sft);
-                            Bv += __shfl_xor_sync(0xffffffffu, Bv, sft);
-                            G += __shfl_xor_sync(0xffffffffu, G, sft);
-                        }
-                        if (lane == 0) {
-                            double cs = 1.0, sn = 0.0, on = 0.0;
-                            if (G != 0.0 && fabs(G) > tol * sqrt(A * Bv)) {
-                                rot_params(A, Bv, G, cs, sn);
-                                on = 1.0;
-                            }
-                            tot[3 * k] = cs;
-                            tot[3 * k + 1] = sn;
-                            tot[3 * k + 2] = on;
-                        }
-                    }
-                    __syncthreads();
-#pragma unroll
-                    for (int k = 0; k < RBk; ++k) {
-                        const int p = circ_col(k, sr, RC), o = circ_col(RC - 1 - k, sr, RC);
-                        if (tot[3 * k + 2] != 0.0) {
-                            const double cs = tot[3 * k], sn = tot[3 * k + 1];
-#pragma unroll
-                            for (int rr = 0; rr < R; ++rr) {
-                                const double xp = x[rr][p], xo = x[rr][o];
-                                x[rr][p] = cs * xp - sn * xo;
-                                x[rr][o] = sn * xp + cs * xo;
-                            }
-                            if (threadIdx.x == 0) ++mine;
-                        }
-                    }
+                    for (int sr = 0; sr < RC - 1; ++sr)
+                        rblk_subround<R, RT, RBk>(0, sr, x, red, tot, lane, warp, tol, mine);
                 }
 #pragma unroll
                 for (int j = 0; j < RC; ++j)
@@ -586,13 +637,13 @@ void launch_rblk_t(Ctx& c, int64_t m, int64_t n, double* U, int64_t ldu, double 
     int grid = std::max(1, std::min(npb / 2, per_sm * c.num_sms));
     int64_t mm = m;
     int nn = int(n), nbb = nb;
-    // HYDOT_JACOBI_INNER: mini-sweeps per block-pair visit (experiments)
-    static const int inner_env = [] {
-        const char* e = std::getenv("HYDOT_JACOBI_INNER");
-        return e ? std::max(1, std::atoi(e)) : 1;
+    // HYDOT_JACOBI_CROSS=0: full mini-sweep per block-pair visit
+    static const int cross_env = [] {
+        const char* e = std::getenv("HYDOT_JACOBI_CROSS");
+        return (e && e[0] == '0') ? 0 : 1;
     }();
-    int inner = inner_env;
-    void* args[] = {&mm, &nn, &nbb, &bp, &U, &ldu, &tol, &counters, &sweeps_out, &inner};
+    int cross = cross_env;
+    void* args[] = {&mm, &nn, &nbb, &bp, &U, &ldu, &tol, &counters, &sweeps_out, &cross};
     HYDOT_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_rblk_k<R, T, B>, dim3(grid), dim3(T), args, 0,
                                            c.stream));
     c.count();
