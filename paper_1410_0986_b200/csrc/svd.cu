@@ -603,13 +603,20 @@ bool rblk_shape(int64_t m, int64_t n, int& R, int& T, int& B) {
         const char* e = std::getenv("HYDOT_JACOBI_TMIN");
         return e ? std::max(64, std::atoi(e)) : 128;
     }();
+    // 256 threads may hold 9 rows each (1153-2304-row cores): fewer warps
+    // per sub-round reduction, 2172^2 core 131 -> 112 ms; at 128 threads 9
+    // rows measured slower than 256 x 5.  HYDOT_JACOBI_RMAX=5 disables.
+    static const int rmax256 = [] {
+        const char* e = std::getenv("HYDOT_JACOBI_RMAX");
+        return (e && std::atoi(e) < 9) ? RMAXR : 9;
+    }();
     B = RB;
     if ((n + RB - 1) / RB >= 4) {
         for (T = tmin; T <= 512; T *= 2) {
             R = int((m + T - 1) / T);
-            const int cap = T == 512 ? 5 : RMAXR;  // 512 threads: 128 registers each
+            const int cap = T == 512 ? 5 : T == 256 ? rmax256 : RMAXR;  // 512 threads: 128 registers each
             if (R <= cap) {
-                R = R <= 3 ? 3 : 5;  // instantiated row counts
+                R = R <= 3 ? 3 : R <= 5 ? 5 : 9;  // instantiated row counts
                 return true;
             }
         }
@@ -657,6 +664,11 @@ void launch_rblk(Ctx& c, int R, int T, int B, int64_t m, int64_t n, double* U, i
             case 9: launch_rblk_t<9, 512, 2>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
             default: launch_rblk_t<12, 512, 2>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
         }
+        return;
+    }
+    if (R == 9) {
+        if (T == 128) launch_rblk_t<9, 128, RB>(c, m, n, U, ldu, tol, counters, sweeps_out);
+        else launch_rblk_t<9, 256, RB>(c, m, n, U, ldu, tol, counters, sweeps_out);
         return;
     }
     const bool r3 = R == 3;
