@@ -353,7 +353,7 @@ __device__ __forceinline__ void rblk_subround(int kind, int sr, double (&x)[R][2
                                               double* tot, int lane, int warp, double tol, int& mine) {
     constexpr int NW = RT / 32;
     constexpr int RNV = 3 * RBk;
-    constexpr int NVP = RNV <= 8 ? 8 : 16;
+    constexpr int NVP = RNV <= 8 ? 8 : RNV <= 16 ? 16 : 32;
     double part[NVP];  // the sub-round's dot products, padded
 #pragma unroll
     for (int k = 0; k < RBk; ++k) {
@@ -617,6 +617,15 @@ bool rblk_shape(int64_t m, int64_t n, int& R, int& T, int& B) {
             const int cap = T == 512 ? 5 : T == 256 ? rmax256 : RMAXR;  // 512 threads: 128 registers each
             if (R <= cap) {
                 R = R <= 3 ? 3 : R <= 5 ? 5 : 9;  // instantiated row counts
+                // HYDOT_JACOBI_B8=1: 8-column blocks (half the block rounds
+                // and grid barriers, 8 pairs per sub-round) where registers
+                // allow -- measured slower (Jacobi 454 -> 566 ms per config-1
+                // step: 24-value reductions, register pressure), opt-in only
+                static const bool b8 = [] {
+                    const char* e = std::getenv("HYDOT_JACOBI_B8");
+                    return e && e[0] == '1';
+                }();
+                if (b8 && R <= 5 && T <= 256 && (n + 7) / 8 >= 4) B = 8;
                 return true;
             }
         }
@@ -664,6 +673,13 @@ void launch_rblk(Ctx& c, int R, int T, int B, int64_t m, int64_t n, double* U, i
             case 9: launch_rblk_t<9, 512, 2>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
             default: launch_rblk_t<12, 512, 2>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
         }
+        return;
+    }
+    if (B == 8) {
+        if (R == 3 && T == 128) launch_rblk_t<3, 128, 8>(c, m, n, U, ldu, tol, counters, sweeps_out);
+        else if (R == 3) launch_rblk_t<3, 256, 8>(c, m, n, U, ldu, tol, counters, sweeps_out);
+        else if (T == 128) launch_rblk_t<5, 128, 8>(c, m, n, U, ldu, tol, counters, sweeps_out);
+        else launch_rblk_t<5, 256, 8>(c, m, n, U, ldu, tol, counters, sweeps_out);
         return;
     }
     if (R == 9) {
