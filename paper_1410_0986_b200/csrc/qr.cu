@@ -20,6 +20,8 @@
 //          (4x fewer passes over the trailing matrix than 32-wide blocking).
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace cg = cooperative_groups;
@@ -408,6 +410,110 @@ void form_v_launch(Ctx& c, int64_t mr, int jb, const double* P, int64_t ld, doub
     c.check_launch();
 }
 
+// Sub-panel T in one launch: G = V^T V of the mr x jb (jb <= 32) unit
+// lower-trapezoidal V held in the factored panel P (implicit unit diagonal,
+// zeros above), reduced over row chunks, then T by the dlarft forward
+// recurrence T(0:c, c) = -tau_c T(0:c, 0:c) G(0:c, c), T(c, c) = tau_c.
+// Replaces form_v + the V^T V GEMM (+ split-K reduce) + larft_k of every
+// 32-wide sub-panel.  The last CTA to finish (atomic ticket) reduces the
+// per-CTA partial Grams in CTA order (deterministic) and forms T.
+constexpr int GT = 256;     // threads
+constexpr int GTILE = 128;  // rows staged per tile
+__global__ void __launch_bounds__(GT) gram_t32_k(int64_t mr, int jb, const double* __restrict__ P, int64_t ld,
+                                                 int64_t rows_per, const double* __restrict__ tau,
+                                                 double* __restrict__ T, double* __restrict__ part,
+                                                 unsigned* __restrict__ ticket) {
+    __shared__ double tile[GTILE][PB + 1];
+    __shared__ double Gs[PB][PB + 1];
+    __shared__ bool last;
+    const int npairs = jb * (jb + 1) / 2;
+    int ep[3], eq[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {  // entry e -> (p, q), p <= q, column-major upper
+        const int e = threadIdx.x + k * GT;
+        int q = 0;
+        while ((q + 1) * (q + 2) / 2 <= e) ++q;
+        ep[k] = e < npairs ? e - q * (q + 1) / 2 : -1;
+        eq[k] = q;
+    }
+    double acc[3] = {0.0, 0.0, 0.0};
+    const int64_t r0 = int64_t(blockIdx.x) * rows_per, r1 = min(mr, r0 + rows_per);
+    for (int64_t t0 = r0; t0 < r1; t0 += GTILE) {
+        const int nt = int(min(int64_t(GTILE), r1 - t0));
+        for (int e = threadIdx.x; e < GTILE * jb; e += GT) {
+            const int rr = e % GTILE, q = e / GTILE;
+            const int64_t i = t0 + rr;
+            double v = 0.0;
+            if (rr < nt) v = i > q ? P[i + int64_t(q) * ld] : (i == q ? 1.0 : 0.0);
+            tile[rr][q] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            if (ep[k] >= 0)
+                for (int rr = 0; rr < nt; ++rr) acc[k] += tile[rr][ep[k]] * tile[rr][eq[k]];
+        __syncthreads();
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        if (ep[k] >= 0) part[int64_t(blockIdx.x) * npairs + threadIdx.x + k * GT] = acc[k];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        if (ep[k] >= 0) {
+            double g = 0.0;
+            for (int b = 0; b < int(gridDim.x); ++b) g += __ldcg(part + int64_t(b) * npairs + threadIdx.x + k * GT);
+            Gs[ep[k]][eq[k]] = g;
+        }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // one warp: the column recurrence, lane i owns row i of T
+        const int i = threadIdx.x;
+        double trow[PB];
+#pragma unroll
+        for (int j = 0; j < PB; ++j) trow[j] = 0.0;
+        for (int c = 0; c < jb; ++c) {
+            const double tc = tau[c];
+            // y_i = sum_{j=i..c-1} T(i, j) G(j, c)  (T upper triangular)
+            double y = 0.0;
+#pragma unroll
+            for (int j = 0; j < PB; ++j)
+                if (j >= i && j < c) y += trow[j] * Gs[j][c];
+#pragma unroll
+            for (int j = 0; j < PB; ++j)
+                if (j == c) trow[j] = i < c ? -tc * y : (i == c ? tc : 0.0);
+        }
+        if (i < jb) {
+#pragma unroll
+            for (int j = 0; j < PB; ++j)
+                if (j < jb) T[i + int64_t(j) * NB] = trow[j];
+        }
+        if (i == 0) *ticket = 0u;  // ready for the next launch on this stream
+    }
+}
+
+void gram_t32(Ctx& c, int64_t mr, int jb, const double* P, int64_t ld, const double* tau, double* T,
+              double* part, unsigned* ticket) {
+    int G = int(std::min<int64_t>(c.num_sms, (mr + GTILE - 1) / GTILE));
+    G = std::max(G, 1);
+    const int64_t rows_per = (mr + G - 1) / G;
+    gram_t32_k<<<G, GT, 0, c.stream>>>(mr, jb, P, ld, rows_per, tau, T, part, ticket);
+    c.check_launch();
+}
+
+// HYDOT_QR_FUSED_T=0 restores the GEMM + larft_k sub-panel T
+bool fused_t32() {
+    static const bool on = [] {
+        const char* e = std::getenv("HYDOT_QR_FUSED_T");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void larft(Ctx& c, int jb, const double* G, int64_t ldg, const double* tau, double* T) {
     static bool attr = false;
     const int smem = (NB * (NB + 1) + (NB / 2) * (NB / 2 + 1)) * sizeof(double);
@@ -439,6 +545,9 @@ void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f
     DBuf W = dalloc(c, size_t(NB) * size_t(std::max<int64_t>(n, 1)));
     DBuf W2 = dalloc(c, size_t(NB) * size_t(std::max<int64_t>(n, 1)));
     DBuf Tp = dalloc(c, size_t(NB) * NB);
+    DBuf gpart = dalloc(c, size_t(c.num_sms) * (PB * (PB + 1) / 2));
+    DBuf gticket(c, sizeof(unsigned));
+    HYDOT_CUDA(cudaMemsetAsync(gticket.as<void>(), 0, sizeof(unsigned), c.stream));
     for (int64_t j0 = 0; j0 < k; j0 += NB) {
         const int jb = int(std::min<int64_t>(NB, k - j0));
         const int64_t mr = m - j0;
@@ -453,8 +562,12 @@ void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f
             if (rest > 0) {
                 // apply this sub-panel's reflector to the rest of the block
                 form_v_launch(c, pr, pb, Pp, m, V.d());
-                dgemm(c, true, false, pb, pb, pr, 1.0, V.d(), pr, V.d(), pr, 0.0, G.d(), pb);
-                larft(c, pb, G.d(), pb, f.tau.d() + j0 + p0, Tp.d());
+                if (fused_t32())
+                    gram_t32(c, pr, pb, Pp, m, f.tau.d() + j0 + p0, Tp.d(), gpart.d(), gticket.as<unsigned>());
+                else {
+                    dgemm(c, true, false, pb, pb, pr, 1.0, V.d(), pr, V.d(), pr, 0.0, G.d(), pb);
+                    larft(c, pb, G.d(), pb, f.tau.d() + j0 + p0, Tp.d());
+                }
                 double* Cm = Pp + int64_t(pb) * m;
                 dgemm(c, true, false, pb, rest, pr, 1.0, V.d(), pr, Cm, m, 0.0, W.d(), pb);
                 dgemm(c, true, false, pb, rest, pb, 1.0, Tp.d(), NB, W.d(), pb, 0.0, W2.d(), pb);
