@@ -754,6 +754,10 @@ __global__ void __launch_bounds__(ZT, 2) cgzt_xr(ZGeo g, int64_t N, int nl, int 
 // one block barrier per plane suffices).
 constexpr int NSR = 3;
 
+// NS raw planes in the ring, NPN p_new planes (4: one barrier per plane;
+// 3: a second barrier per plane, one more raw plane in flight in the same
+// shared memory)
+template <int NS, int NPN>
 __global__ void __launch_bounds__(ZT, 2) cgzt_pa(ZGeo g, int64_t N, int nl, int k0, int it,
                                                const double* __restrict__ sig,
                                                const double* __restrict__ sigp,
@@ -764,7 +768,7 @@ __global__ void __launch_bounds__(ZT, 2) cgzt_pa(ZGeo g, int64_t N, int nl, int 
                                                SysState* __restrict__ st, double tol, int fixed,
                                                const int* __restrict__ act) {
     extern __shared__ __align__(16) double zs[];
-    __shared__ __align__(8) uint64_t bar[NSR];
+    __shared__ __align__(8) uint64_t bar[NS];
     __shared__ double sh[ZT / 32];
     __shared__ double bc;
     const int sys = act[blockIdx.y];
@@ -799,22 +803,22 @@ __global__ void __launch_bounds__(ZT, 2) cgzt_pa(ZGeo g, int64_t N, int nl, int 
     const double* po = Pold + int64_t(sys) * N;
     double* p = Pnew + int64_t(sys) * N;
     const double sigma = sig[l], sigmap = sigp[l];
-    double* raw = zs;                 // NSR x (r | p_old) x W
-    double* pn = zs + 2 * NSR * z.W;  // 4 x W
+    double* raw = zs;                 // NS x (r | p_old) x W
+    double* pn = zs + 2 * NS * z.W;  // NPN x W
     const uint32_t bytes = uint32_t(z.hi - z.lo) * 8u;
     auto issue = [&](int j) {
-        const int sl = j % NSR;
+        const int sl = j % NS;
         mb_expect(&bar[sl], 2u * bytes);
         const int64_t o = j * plane + z.base + z.lo;
         bulk_load(raw + (2 * sl) * z.W + z.lo, r + o, bytes, &bar[sl]);
         bulk_load(raw + (2 * sl + 1) * z.W + z.lo, po + o, bytes, &bar[sl]);
     };
     auto convert = [&](int j) {  // pn[j % 4] = r + beta p_old on the in-grid rows
-        const int sl = j % NSR;
-        mb_wait(&bar[sl], uint32_t((j / NSR) & 1));
+        const int sl = j % NS;
+        mb_wait(&bar[sl], uint32_t((j / NS) & 1));
         const double* rs = raw + (2 * sl) * z.W;
         const double* ps = rs + z.W;
-        double* out = pn + (j & 3) * z.W;
+        double* out = pn + (j % NPN) * z.W;
 #pragma unroll
         for (int k = 0; k < ZE; ++k) {
             const int e = threadIdx.x + k * ZT;
@@ -822,31 +826,31 @@ __global__ void __launch_bounds__(ZT, 2) cgzt_pa(ZGeo g, int64_t N, int nl, int 
         }
     };
     if (threadIdx.x == 0) {
-        for (int i = 0; i < NSR; ++i) mb_init(&bar[i]);
+        for (int i = 0; i < NS; ++i) mb_init(&bar[i]);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (int e = threadIdx.x; e < 4 * z.W; e += ZT) pn[e] = 0.0;  // out-of-grid halo rows
+    for (int e = threadIdx.x; e < NPN * z.W; e += ZT) pn[e] = 0.0;  // out-of-grid halo rows
     __syncthreads();
     if (threadIdx.x == 0)
-        for (int j = 0; j < NSR && j < g.nz; ++j) issue(j);
+        for (int j = 0; j < NS && j < g.nz; ++j) issue(j);
     convert(0);
     __syncthreads();
-    if (threadIdx.x == 0 && NSR < g.nz) {
+    if (threadIdx.x == 0 && NS < g.nz) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(NSR);
+        issue(NS);
     }
     double acc = 0.0;
     for (int iz = 0; iz < g.nz; ++iz) {
         const int j = iz + 1;
         if (j < g.nz) convert(j);
         __syncthreads();
-        if (threadIdx.x == 0 && j + NSR < g.nz) {
+        if (threadIdx.x == 0 && j + NS < g.nz) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(j + NSR);  // into raw(j)'s slot, converted above
+            issue(j + NS);  // into raw(j)'s slot, converted above
         }
-        const double* c = pn + (iz & 3) * z.W;
-        const double* dn = pn + ((iz + 3) & 3) * z.W;
-        const double* up = pn + ((iz + 1) & 3) * z.W;
+        const double* c = pn + (iz % NPN) * z.W;
+        const double* dn = pn + ((iz + NPN - 1) % NPN) * z.W;
+        const double* up = pn + ((iz + 1) % NPN) * z.W;
         const ZDiag d = zdiag(g.nz, g.h, iz, sigma, sigmap);
 #pragma unroll
         for (int k = 0; k < ZO; ++k) {
@@ -858,6 +862,7 @@ __global__ void __launch_bounds__(ZT, 2) cgzt_pa(ZGeo g, int64_t N, int nl, int 
                 acc += pi * ap;
             }
         }
+        if (NPN == 3) __syncthreads();  // pn(iz-1)'s slot is refilled next
     }
     const double t = block_sum(acc, sh);
     if (threadIdx.x == 0) partA[int64_t(sys) * nparts + blockIdx.x] = t;
@@ -873,6 +878,17 @@ int zmarch_occ() {
     return o;
 }
 #define ZSEL(k) (zmarch_occ() == 3 ? k<3> : k<4>)
+
+// HYDOT_CG_PA_DEEP=1: cgzt_pa with 4 raw planes and 3 p_new planes (one
+// more plane in flight, one more barrier per plane: measured 0.493 -> 0.503 s
+// on config 1, so opt-in only)
+bool zpa_deep() {
+    static const bool on = [] {
+        const char* e = std::getenv("HYDOT_CG_PA_DEEP");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
 
 // bulk-copy x/r kernel for even nx (HYDOT_CG_BULK=0 keeps the register one)
 bool zbulk_on() {
@@ -968,18 +984,21 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
             zsmem = size_t(3) * size_t(ty + 2) * size_t(op.g.nx) * sizeof(double);
             if (op.g.nx % 2 == 0 && zbulk_on()) {
                 ztsmem = size_t(NSP * (ty + 2) + NSX * 2 * ty) * size_t(op.g.nx) * sizeof(double);
-                ztpsmem = size_t((2 * NSR + 4) * (ty + 2)) * size_t(op.g.nx) * sizeof(double);
+                ztpsmem = zpa_deep() ? size_t((2 * 4 + 3) * (ty + 2)) * size_t(op.g.nx) * sizeof(double)
+                                     : size_t((2 * NSR + 4) * (ty + 2)) * size_t(op.g.nx) * sizeof(double);
                 static bool attr = false;
                 if (!attr) {
                     HYDOT_CUDA(cudaFuncSetAttribute(cgzt_xr, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     200 * 1024));
-                    HYDOT_CUDA(cudaFuncSetAttribute(cgzt_pa, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                    HYDOT_CUDA(cudaFuncSetAttribute(cgzt_pa<NSR, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    200 * 1024));
+                    HYDOT_CUDA(cudaFuncSetAttribute(cgzt_pa<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     200 * 1024));
                     // same shared-memory carve-out for both kernels of an
                     // iteration (no SM reconfiguration between launches)
                     if (std::getenv("HYDOT_CG_CARVE")) {
                         const int cv = std::atoi(std::getenv("HYDOT_CG_CARVE"));
-                        HYDOT_CUDA(cudaFuncSetAttribute(cgz_pa<3>, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
+                        HYDOT_CUDA(cudaFuncSetAttribute(cgzt_pa<NSR, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
                         HYDOT_CUDA(cudaFuncSetAttribute(cgzt_xr, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
                     }
                     attr = true;
@@ -1050,7 +1069,7 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
             dim3 grid = dim3(unsigned(nparts), unsigned(active.size()));
             if (zsmem) {
                 if (ztpsmem)
-                    cgzt_pa<<<grid, ZT, ztpsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
+                    (zpa_deep() ? cgzt_pa<4, 3> : cgzt_pa<NSR, 4>)<<<grid, ZT, ztpsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
                                                              pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
                                                              tol, fixed_iters > 0, dact.as<int>());
                 else
@@ -1099,7 +1118,7 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
             // one more convergence check for systems finishing on the last step
             dim3 grid = dim3(unsigned(nparts), unsigned(active.size()));
             if (ztpsmem)
-                cgzt_pa<<<grid, ZT, ztpsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
+                (zpa_deep() ? cgzt_pa<4, 3> : cgzt_pa<NSR, 4>)<<<grid, ZT, ztpsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
                                                          pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
                                                          tol, 0, dact.as<int>());
             else if (zsmem)
