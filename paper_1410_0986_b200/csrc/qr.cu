@@ -57,8 +57,8 @@ __global__ void __launch_bounds__(PT) qr_panel_coop(int64_t mr, int jb, double* 
                                                     double* __restrict__ tau_out, PanelBufs buf) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double slab[];  // rows_per x PB (ld rows_per) when SMEM
-    __shared__ double red[PT / 32][PB + 1];
-    __shared__ double wsh[PB];
+    __shared__ double red[2][PT / 32][PB + 1];  // by partial parity: no barrier before reuse
+    __shared__ double wraw[PB], wsh[PB];
     __shared__ double sc[3];
     const int G = gridDim.x;
     const int64_t r0 = int64_t(blockIdx.x) * rows_per;
@@ -103,9 +103,8 @@ __global__ void __launch_bounds__(PT) qr_panel_coop(int64_t mr, int jb, double* 
                 acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
             }
         }
-        __syncthreads();  // red[] may still be read by the previous reduction
-        red[warp][lane] = acc[0];
-        if (lane == 0) red[warp][PB] = nacc;
+        red[par][warp][lane] = acc[0];
+        if (lane == 0) red[par][warp][PB] = nacc;
         __syncthreads();
         // the 32 dots and the norm summed over the 16 warps with shuffles,
         // one half-warp per quantity; slot 0 (dot 0 is never needed: q > col
@@ -113,7 +112,7 @@ __global__ void __launch_bounds__(PT) qr_panel_coop(int64_t mr, int jb, double* 
         {
             const int slot = 2 * warp + (lane >> 4), hl = lane & 15;
             const int q = slot == 0 ? PB : slot;
-            double t = (q <= PB && hl < PT / 32) ? red[hl][q] : 0.0;
+            double t = (q <= PB && hl < PT / 32) ? red[par][hl][q] : 0.0;
 #pragma unroll
             for (int o = 8; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
             if (hl == 0 && q <= PB) {
@@ -152,21 +151,20 @@ __global__ void __launch_bounds__(PT) qr_panel_coop(int64_t mr, int jb, double* 
                 double s = 0.0;
                 for (int p = lane; p < G; p += 32) s += buf.dot[(int64_t(par) * GMAX + p) * PB + q];
                 s = warp_sum(s);
-                if (lane == 0) wsh[q] = s;  // raw x^T P_q; scaled below
+                if (lane == 0) wraw[q] = s;  // raw x^T P_q; scaled below
             }
         }
         __syncthreads();
         const double tau = sc[0], beta = sc[1], scal = sc[2];
-        double wq_own = 0.0;
         if (threadIdx.x < PB) {
             const int q = threadIdx.x;
+            double wq = 0.0;
             if (q > c && q < jb) {
                 const double pc = buf.row[par * PB + q];
-                wq_own = pc + scal * (wsh[q] - buf.row[par * PB + c] * pc);  // v^T P_q, v_c = 1
+                wq = pc + scal * (wraw[q] - buf.row[par * PB + c] * pc);  // v^T P_q, v_c = 1
             }
+            wsh[q] = wq;
         }
-        __syncthreads();
-        if (threadIdx.x < PB) wsh[threadIdx.x] = wq_own;
         __syncthreads();
         // ---- apply H_c to the rest of the panel (own rows), store v
         for (int64_t i = max(r0, int64_t(c)) + threadIdx.x; i < r1; i += PT) {
