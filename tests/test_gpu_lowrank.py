@@ -167,6 +167,54 @@ def test_recompress_lazy_root_matches_dense(ctx):
     assert fro(U.cpu().numpy() @ V.cpu().numpy().T - B) <= 1e-9 * fro(B)
 
 
+def _lazy_root(ctx, seed=3):
+    from paper_1410_0986_b200 import lowrank as lr
+    rng = np.random.default_rng(11)
+    ns, rows_per, cols = 4, 20, 3000
+    H = random_lowrank(rng, ns * rows_per, cols, 40, 1e-7)
+    pos = np.array([[(s % 2) * 1.0, (s // 2) * 1.0] for s in range(ns)])
+    tree = lr.ClusterTree(pos, [0, 0], [1, 1])
+    Ht = torch.as_tensor(H).cuda()
+
+    class Prov:
+        rows_per_source = rows_per
+        cols = 3000
+
+        @staticmethod
+        def block(s):
+            return Ht[s * rows_per:(s + 1) * rows_per]
+
+    return lr.recursive_lowrank(ctx, tree, 1e-9, Prov, lr.RecursiveOptions(seed=seed)), H
+
+
+def test_lazy_root_every_consumer_sees_the_same_factor(ctx, tmp_path):
+    """Each consumer of a fresh (lazy-V) root factor materialises V first:
+    device pointers, products, save, agglomerate -- all equal to the same
+    operations on the materialised copy."""
+    from paper_1410_0986_b200 import lowrank as lr
+    ref_rec, _ = _lazy_root(ctx)
+    U, V = ref_rec.factor.U, ref_rec.factor.V            # materialised copy
+    X = torch.randn(3000, 2, dtype=torch.float64, device="cuda")
+    want = U @ (V.T @ X)
+    rec, _ = _lazy_root(ctx)                             # fresh lazy root each time
+    assert float(torch.linalg.norm(lr.lr_matvec(ctx, rec.factor, X) - want)) <= 1e-12 * float(torch.linalg.norm(want))
+    rec, _ = _lazy_root(ctx)
+    up, vp = rec.factor.device_ptrs()
+    assert bool(up) and bool(vp)  # non-NULL device pointers
+    assert torch.equal(rec.factor.V, V)
+    rec, _ = _lazy_root(ctx)
+    path = str(tmp_path / "f.bin")
+    lr.save_factor(path, rec.factor)
+    g, _ = lr.load_factor(ctx, path)
+    assert torch.equal(g.V, V) and torch.equal(g.U, U)
+    rec, _ = _lazy_root(ctx)
+    dense = lr.LowRankFactor.from_tensors(ctx, U, V)
+    a = lr.agglomerate(ctx, rec.factor, dense, 1e-9, 5)
+    b = lr.agglomerate(ctx, lr.LowRankFactor.from_tensors(ctx, U, V), dense, 1e-9, 5)
+    assert a.rank() == b.rank()
+    assert torch.equal(a.dense(), b.dense())
+
+
 def test_born_pipeline_parity_small(ctx, oracle):
     """fields -> Born blocks -> recursive compression -> recompress -> J~ products,
     device vs oracle on identical (device-computed) fields."""
