@@ -25,6 +25,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <numeric>
+#include <string>
 
 #include "internal.h"
 
@@ -443,7 +444,7 @@ template <int R, int RT, int RBk>
 __global__ void __launch_bounds__(RT, 1) jacobi_rblk_k(int64_t m, int n, int nb, const int2* __restrict__ bpairs,
                                                       double* __restrict__ U, int64_t ldu, double tol,
                                                       int* __restrict__ counters, int* __restrict__ sweeps_out,
-                                                      int cross) {
+                                                      int cross, int stop_thr) {
     constexpr int NW = RT / 32;
     constexpr int RC = 2 * RBk;          // columns per block pair
     constexpr int RNV = 3 * RBk;         // dot products per sub-round
@@ -500,7 +501,7 @@ __global__ void __launch_bounds__(RT, 1) jacobi_rblk_k(int64_t m, int n, int nb,
         }
         if (threadIdx.x == 0 && mine) atomicAdd(&counters[sweep], mine);
         grid.sync();
-        if (*((volatile int*)&counters[sweep]) == 0) break;
+        if (*((volatile int*)&counters[sweep]) <= stop_thr) break;  // stop_thr > 0: the host checks the rest
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) *sweeps_out = sweep;
 }
@@ -536,6 +537,82 @@ __global__ void finish_k(int64_t m, int n, const int* __restrict__ perm, const d
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x)
         Vo[i + int64_t(j) * ldvo] = V[i + int64_t(src) * ldv];
+}
+
+// Convergence check on the Gram matrix G = U^T U (one DMMA GEMM): list the
+// pairs i < j with |g_ij| > tol sqrt(g_ii g_jj) -- the one-sided Jacobi
+// rotation test of every pair on the current U.  The list order is made
+// deterministic on the host (sorted).
+__global__ void jacobi_violations_k(int n, const double* __restrict__ G, int64_t ldg, double tol,
+                                    int cap, int* __restrict__ count, int2* __restrict__ list) {
+    const int j = blockIdx.x;
+    const double gjj = G[j + int64_t(j) * ldg];
+    for (int i = threadIdx.x; i < j; i += blockDim.x) {
+        const double g = G[i + int64_t(j) * ldg];
+        const double gii = G[i + int64_t(i) * ldg];
+        if (g != 0.0 && fabs(g) > tol * sqrt(gii * gjj)) {
+            const int k = atomicAdd(count, 1);
+            if (k < cap) list[k] = make_int2(i, j);
+        }
+    }
+}
+
+// Rotate the listed column pairs in order (one CTA), each from its actual
+// column dot products -- the point driver's rotation.
+__global__ void __launch_bounds__(512) jacobi_fix_k(int64_t m, int np, const int2* __restrict__ list,
+                                                    double* __restrict__ U, int64_t ldu, double tol) {
+    __shared__ double red[3][16];
+    __shared__ double rot[3];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int k = 0; k < np; ++k) {
+        const int2 pq = list[k];
+        double* up = U + int64_t(pq.x) * ldu;
+        double* uq = U + int64_t(pq.y) * ldu;
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+            const double x = up[i], y = uq[i];
+            a += x * x;
+            b += y * y;
+            g += x * y;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+            g += __shfl_xor_sync(0xffffffffu, g, o);
+        }
+        if (lane == 0) {
+            red[0][warp] = a;
+            red[1][warp] = b;
+            red[2][warp] = g;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double A = 0.0, B = 0.0, Gv = 0.0;
+            for (int w = 0; w < int(blockDim.x >> 5); ++w) {
+                A += red[0][w];
+                B += red[1][w];
+                Gv += red[2][w];
+            }
+            double cs = 1.0, sn = 0.0, on = 0.0;
+            if (Gv != 0.0 && fabs(Gv) > tol * sqrt(A * B)) {
+                rot_params(A, B, Gv, cs, sn);
+                on = 1.0;
+            }
+            rot[0] = cs;
+            rot[1] = sn;
+            rot[2] = on;
+        }
+        __syncthreads();
+        if (rot[2] != 0.0) {
+            const double cs = rot[0], sn = rot[1];
+            for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+                const double x = up[i], y = uq[i];
+                up[i] = cs * x - sn * y;
+                uq[i] = sn * x + cs * y;
+            }
+        }
+        __syncthreads();
+    }
 }
 
 // circle-method tournament: rounds x (np/2) pairs
@@ -644,7 +721,7 @@ bool rblk_shape(int64_t m, int64_t n, int& R, int& T, int& B) {
 
 template <int R, int T, int B>
 void launch_rblk_t(Ctx& c, int64_t m, int64_t n, double* U, int64_t ldu, double tol, int* counters,
-                   int* sweeps_out) {
+                   int* sweeps_out, int stop_thr) {
     int nb = int((n + B - 1) / B);
     int npb = 0;
     const int2* bp = device_pairs(nb, npb);
@@ -659,44 +736,44 @@ void launch_rblk_t(Ctx& c, int64_t m, int64_t n, double* U, int64_t ldu, double 
         return (e && e[0] == '0') ? 0 : 1;
     }();
     int cross = cross_env;
-    void* args[] = {&mm, &nn, &nbb, &bp, &U, &ldu, &tol, &counters, &sweeps_out, &cross};
+    void* args[] = {&mm, &nn, &nbb, &bp, &U, &ldu, &tol, &counters, &sweeps_out, &cross, &stop_thr};
     HYDOT_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_rblk_k<R, T, B>, dim3(grid), dim3(T), args, 0,
                                            c.stream));
     c.count();
 }
 
 void launch_rblk(Ctx& c, int R, int T, int B, int64_t m, int64_t n, double* U, int64_t ldu, double tol,
-                 int* counters, int* sweeps_out) {
+                 int* counters, int* sweeps_out, int stop_thr) {
     if (B == 2) {
         switch (R) {
-            case 6: launch_rblk_t<6, 512, 2>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
-            case 9: launch_rblk_t<9, 512, 2>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
-            default: launch_rblk_t<12, 512, 2>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
+            case 6: launch_rblk_t<6, 512, 2>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr); break;
+            case 9: launch_rblk_t<9, 512, 2>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr); break;
+            default: launch_rblk_t<12, 512, 2>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr); break;
         }
         return;
     }
     if (B == 8) {
-        if (R == 3 && T == 128) launch_rblk_t<3, 128, 8>(c, m, n, U, ldu, tol, counters, sweeps_out);
-        else if (R == 3) launch_rblk_t<3, 256, 8>(c, m, n, U, ldu, tol, counters, sweeps_out);
-        else if (T == 128) launch_rblk_t<5, 128, 8>(c, m, n, U, ldu, tol, counters, sweeps_out);
-        else launch_rblk_t<5, 256, 8>(c, m, n, U, ldu, tol, counters, sweeps_out);
+        if (R == 3 && T == 128) launch_rblk_t<3, 128, 8>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr);
+        else if (R == 3) launch_rblk_t<3, 256, 8>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr);
+        else if (T == 128) launch_rblk_t<5, 128, 8>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr);
+        else launch_rblk_t<5, 256, 8>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr);
         return;
     }
     if (R == 9) {
-        if (T == 128) launch_rblk_t<9, 128, RB>(c, m, n, U, ldu, tol, counters, sweeps_out);
-        else launch_rblk_t<9, 256, RB>(c, m, n, U, ldu, tol, counters, sweeps_out);
+        if (T == 128) launch_rblk_t<9, 128, RB>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr);
+        else launch_rblk_t<9, 256, RB>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr);
         return;
     }
     const bool r3 = R == 3;
     switch (T) {
-        case 64: r3 ? launch_rblk_t<3, 64, RB>(c, m, n, U, ldu, tol, counters, sweeps_out)
-                    : launch_rblk_t<5, 64, RB>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
-        case 128: r3 ? launch_rblk_t<3, 128, RB>(c, m, n, U, ldu, tol, counters, sweeps_out)
-                     : launch_rblk_t<5, 128, RB>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
-        case 256: r3 ? launch_rblk_t<3, 256, RB>(c, m, n, U, ldu, tol, counters, sweeps_out)
-                     : launch_rblk_t<5, 256, RB>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
-        default: r3 ? launch_rblk_t<3, 512, RB>(c, m, n, U, ldu, tol, counters, sweeps_out)
-                    : launch_rblk_t<5, 512, RB>(c, m, n, U, ldu, tol, counters, sweeps_out); break;
+        case 64: r3 ? launch_rblk_t<3, 64, RB>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr)
+                    : launch_rblk_t<5, 64, RB>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr); break;
+        case 128: r3 ? launch_rblk_t<3, 128, RB>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr)
+                     : launch_rblk_t<5, 128, RB>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr); break;
+        case 256: r3 ? launch_rblk_t<3, 256, RB>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr)
+                     : launch_rblk_t<5, 256, RB>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr); break;
+        default: r3 ? launch_rblk_t<3, 512, RB>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr)
+                    : launch_rblk_t<5, 512, RB>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr); break;
     }
 }
 
@@ -718,6 +795,71 @@ bool stats_on() {
     return on != 0;
 }
 
+}  // namespace
+
+namespace {
+// HYDOT_JACOBI_TAIL=0: plain sweeps to a zero-rotation sweep
+bool gram_tail_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("HYDOT_JACOBI_TAIL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// Register block-Jacobi to convergence.  The last sweeps of a one-sided
+// Jacobi rotate a handful of pairs (e.g. ... 3791, 8, 0 on the 2172^2 root
+// core) and the final one only verifies.  Sweeps therefore stop once a sweep
+// rotates <= 12 n pairs; then the rotation test of every pair is evaluated at
+// once on G = U^T U (one GEMM), the few violating pairs are rotated from
+// their actual columns (jacobi_fix_k), and the test repeats -- the stopping
+// state is the sweep criterion (no pair fails the test, at 2 tol: see
+// below).  Too many violations fall back to sweeps.
+void rblk_converge(Ctx& c, int R, int T, int B, int64_t m, int64_t n, double* U, double tol, DBuf& sw) {
+    int* counters = sw.as<int>();
+    int* sweeps_out = sw.as<int>() + kMaxSweeps;
+    if (!gram_tail_on() || n < 64) {
+        launch_rblk(c, R, T, B, m, n, U, m, tol, counters, sweeps_out, 0);
+        return;
+    }
+    // a sweep of <= 12 n rotations is followed by one of at most a few hundred
+    // on the path's cores; fixing a pair costs ~1/100 of a sweep at n = 300
+    const int cap = int(std::clamp<int64_t>(n / 4, 16, 256));
+    launch_rblk(c, R, T, B, m, n, U, m, tol, counters, sweeps_out, int(std::min<int64_t>(12 * n, 1 << 30)));
+    DBuf G = dalloc(c, size_t(n * n));
+    DBuf cnt(c, sizeof(int));
+    DBuf lst(c, sizeof(int2) * cap);
+    for (int round = 0; round < 4; ++round) {
+        dgemm(c, true, false, n, n, m, 1.0, U, m, U, m, 0.0, G.d(), n);
+        HYDOT_CUDA(cudaMemsetAsync(cnt.as<void>(), 0, sizeof(int), c.stream));
+        // test at 2 tol: tol = sqrt(m) eps is the rounding level of a column
+        // dot product itself, so pairs within a factor 2 of it are noise
+        // (the GEMM and the fix kernel sum in different orders and would
+        // disagree on them forever); real violations are far above
+        jacobi_violations_k<<<unsigned(n), 128, 0, c.stream>>>(int(n), G.d(), n, 2.0 * tol, cap, cnt.as<int>(),
+                                                             lst.as<int2>());
+        c.check_launch();
+        int nv = 0;
+        HYDOT_CUDA(cudaMemcpyAsync(&nv, cnt.as<void>(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        if (stats_on()) fprintf(stderr, "[jacobi-tail] n=%lld round=%d violations=%d\n", (long long)n, round, nv);
+        if (nv == 0) return;
+        if (nv > cap) break;
+        std::vector<int2> h(static_cast<size_t>(nv));
+        HYDOT_CUDA(cudaMemcpyAsync(h.data(), lst.as<void>(), sizeof(int2) * size_t(nv), cudaMemcpyDeviceToHost,
+                                   c.stream));
+        c.sync();
+        std::sort(h.begin(), h.end(), [](int2 a, int2 b) { return a.y != b.y ? a.y < b.y : a.x < b.x; });
+        HYDOT_CUDA(cudaMemcpyAsync(lst.as<void>(), h.data(), sizeof(int2) * size_t(nv), cudaMemcpyHostToDevice,
+                                   c.stream));
+        jacobi_fix_k<<<1, 512, 0, c.stream>>>(m, nv, lst.as<int2>(), U, m, tol);
+        c.check_launch();
+        c.sync();  // h goes out of scope
+    }
+    // many violations left: plain sweeps to convergence
+    HYDOT_CUDA(cudaMemsetAsync(counters, 0, sizeof(int) * kMaxSweeps, c.stream));
+    launch_rblk(c, R, T, B, m, n, U, m, tol, counters, sweeps_out, 0);
+}
 }  // namespace
 
 StrictSVD::StrictSVD() : prev_(g_strict_svd) { g_strict_svd = true; }
@@ -769,7 +911,7 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
     } else if (int rbR = 0, rbT = 0, rbB = 0; n >= 2 && !strict_svd_flag() && lazy_v_enabled() && atol == 0.0 &&
                                                rblk_shape(m, n, rbR, rbT, rbB)) {
         lazy_v = true;
-        launch_rblk(c, rbR, rbT, rbB, m, n, U.d(), m, tol, sw.as<int>(), sw.as<int>() + kMaxSweeps);
+        rblk_converge(c, rbR, rbT, rbB, m, n, U.d(), tol, sw);
     } else {
         set_identity(c, n, n, V.d(), n);
         if (n >= 2) {
@@ -812,8 +954,14 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
                                    cudaMemcpyDeviceToHost, c.stream));
         c.sync();
         double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
-        fprintf(stderr, "[jacobi] m=%lld n=%lld sweeps=%d ms=%.3f\n", (long long)m, (long long)n,
-                sweeps, dt * 1e3);
+        int rots[kMaxSweeps + 1];
+        HYDOT_CUDA(cudaMemcpyAsync(rots, sw.as<int>(), sizeof(int) * (kMaxSweeps + 1), cudaMemcpyDeviceToHost,
+                                   c.stream));
+        c.sync();
+        std::string rs;
+        for (int i = 0; i <= sweeps && i < kMaxSweeps; ++i) rs += std::to_string(rots[i]) + " ";
+        fprintf(stderr, "[jacobi] m=%lld n=%lld sweeps=%d ms=%.3f rot/sweep: %s\n", (long long)m, (long long)n,
+                sweeps, dt * 1e3, rs.c_str());
     }
     DBuf sd = dalloc(c, size_t(n));
     colnorm_k<<<unsigned(n), 256, 0, c.stream>>>(m, int(n), U.d(), m, sd.d());
