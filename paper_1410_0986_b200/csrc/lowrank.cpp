@@ -355,8 +355,10 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
         ldb = n;
     }
     charge(l, cat, 2.0 * double(m) * double(n) * double(qc));
+    // V of the tall branch always comes back implicit (Q [Ur; 0]): only the
+    // kept columns are then formed (or, with lazy_v, none until first use)
     auto lz = std::make_shared<LazyV>();
-    SVDd svdB = fast_thin_svd_impl(c, Btp, ldb, true, qc, n, l, cat, nullptr, lazy_v ? lz.get() : nullptr);
+    SVDd svdB = fast_thin_svd_impl(c, Btp, ldb, true, qc, n, l, cat, nullptr, lz.get());
     const std::vector<double>& s = svdB.s;
     const double s1 = s.empty() ? 0.0 : s[0];
     int64_t keep = 0;
@@ -391,6 +393,7 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
     }
     charge(l, cat, 2.0 * double(m) * double(keep) * double(qc));
     charge(l, cat, 1.0 * double(n) * double(keep));  // :193-197
+    if (!lazy_v) materialize_v(c, f);
     return f;
 }
 
