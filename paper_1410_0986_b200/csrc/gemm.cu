@@ -94,7 +94,8 @@ struct Tile {
     static constexpr int A_ELEMS = (BM + 4) * BK > BM * (BK + 4) ? (BM + 4) * BK : BM * (BK + 4);
     static constexpr int B_ELEMS = (BN + 4) * BK > BN * (BK + 4) ? (BN + 4) * BK : BN * (BK + 4);
     static constexpr size_t SMEM = size_t(STAGES) * (A_ELEMS + B_ELEMS) * sizeof(double);
-    static constexpr int MIN_CTAS = NT <= 128 ? 3 : 1;  // 64x64: 12 resident warps per SM
+    // 64x64: 3 CTAs (12 warps) per SM; 128x64 (64x32 warp tiles): 2
+    static constexpr int MIN_CTAS = NT <= 128 ? (BM * BN <= 4096 ? 3 : 2) : 1;
 };
 
 template <bool TA, bool TB, int BM, int BN, int WM, int WN>
@@ -358,8 +359,18 @@ void dgemm(Ctx& c, bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alp
         c.check_launch();
         return;
     }
-    // large output tiles where the 128x128 grid fills the GPU
-    run_tiles<64, 64, 32, 32>(c, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+    // HYDOT_GEMM_BIG=1: 128x64 CTA tiles (64x32 warp tiles: 16 DMMAs per 12
+    // fragment loads instead of 8 per 8) when m >= 128 -- measured slower on
+    // every path shape (254 registers, 2 CTAs/SM: QR W = V^T C 28 -> 18.6
+    // TF/s, C -= V W 29.6 -> 26 TF/s), kept opt-in for experiments
+    static const bool big = [] {
+        const char* e = std::getenv("HYDOT_GEMM_BIG");
+        return e && e[0] == '1';
+    }();
+    if (big && m >= 128 && n >= 64)
+        run_tiles<128, 64, 64, 32>(c, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+    else
+        run_tiles<64, 64, 32, 32>(c, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
 }
 
 }  // namespace hydot
