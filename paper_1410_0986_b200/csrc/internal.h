@@ -199,8 +199,9 @@ struct QRFact {
 };
 constexpr int kQRBlock = 128;  // block-reflector width (qr.cu)
 void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f);
-// Y (m x k) := Q Y (trans=false) or Q^T Y
-void apply_q(Ctx& c, const QRFact& f, bool trans, int64_t k, double* Y, int64_t ldy);
+// Y (m x k) := Q Y (trans=false) or Q^T Y.  nz_rows >= 0 (Q Y only): Y's
+// rows >= nz_rows are zero on entry (the Q [Z; 0] products).
+void apply_q(Ctx& c, const QRFact& f, bool trans, int64_t k, double* Y, int64_t ldy, int64_t nz_rows = -1);
 
 // While alive, Jacobi SVDs accumulate V for every column (full BDCSVD
 // contract, e.g. hydot_thin_svd); otherwise the large driver recovers V

@@ -128,7 +128,7 @@ void jacobi_precond(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, 
     scatter_rows(c, n, n, Vx.d(), n, dperm.as<int>(), V, ldv);  // V = P Vr
     fill(c, m, n, 0.0, U, ldu);
     copy2d(c, n, n, Ux.d(), n, U, ldu);
-    apply_q(c, q1, false, n, U, ldu);  // U = Q1 [Ur; 0]
+    apply_q(c, q1, false, n, U, ldu, n);  // U = Q1 [Ur; 0]
     c.sync();  // host perm vector goes out of scope
 }
 
@@ -251,7 +251,7 @@ SVDd fast_thin_svd_impl(Ctx& c, const double* S, int64_t ld, bool trans, int64_t
         o.U = dalloc(c, size_t(m * n));
         fill(c, m, n, 0.0, o.U.d(), m);
         copy2d(c, n, n, Ur.d(), n, o.U.d(), m);
-        apply_q(c, qf, false, n, o.U.d(), m);
+        apply_q(c, qf, false, n, o.U.d(), m, n);
         return o;
     }
     return thin_svd(c, S, ld, trans, m, n, l, cat);  // lowrank.cpp:88-92
@@ -270,7 +270,7 @@ void materialize_v(Ctx& c, Factor& f) {
     if (f.rank > 0) {
         fill(c, f.cols, f.rank, 0.0, f.V.d(), f.cols);
         copy2d(c, L.zr, f.rank, L.Z.d(), L.zr, f.V.d(), f.cols);
-        apply_q(c, L.q, false, f.rank, f.V.d(), f.cols);
+        apply_q(c, L.q, false, f.rank, f.V.d(), f.cols, L.zr);
     }
     c.sync();
     f.lazy.reset();
@@ -494,7 +494,7 @@ Factor recompress(Ctx& c, const Factor& f, double eps, int rank, Ledger* l) {
     if (keep > 0) {
         fill(c, M, keep, 0.0, out.U.d(), M);
         copy2d(c, r, keep, svd.U.d(), r, out.U.d(), M);
-        apply_q(c, qu, false, keep, out.U.d(), M);
+        apply_q(c, qu, false, keep, out.U.d(), M, r);
         DBuf sd = dalloc(c, size_t(keep));
         HYDOT_CUDA(cudaMemcpyAsync(sd.d(), s.data(), size_t(keep) * 8, cudaMemcpyHostToDevice,
                                    c.stream));
@@ -503,15 +503,15 @@ Factor recompress(Ctx& c, const Factor& f, double eps, int rank, Ledger* l) {
             fill(c, vm, keep, 0.0, small.d(), vm);
             copy2d(c, r, keep, svd.V.d(), r, small.d(), vm);
             scale_cols(c, r, keep, small.d(), vm, sd.d());
-            apply_q(c, qv, false, keep, small.d(), vm);
+            apply_q(c, qv, false, keep, small.d(), vm, r);
             fill(c, N, keep, 0.0, out.V.d(), N);
             copy2d(c, vm, keep, small.d(), vm, out.V.d(), N);
-            apply_q(c, lv->q, false, keep, out.V.d(), N);
+            apply_q(c, lv->q, false, keep, out.V.d(), N, vm);
         } else {
             fill(c, N, keep, 0.0, out.V.d(), N);
             copy2d(c, r, keep, svd.V.d(), r, out.V.d(), N);
             scale_cols(c, r, keep, out.V.d(), N, sd.d());
-            apply_q(c, qv, false, keep, out.V.d(), N);
+            apply_q(c, qv, false, keep, out.V.d(), N, r);
         }
         c.sync();
     }

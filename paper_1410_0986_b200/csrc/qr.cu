@@ -464,9 +464,16 @@ __global__ void __launch_bounds__(GT) gram_t32_k(int64_t mr, int jb, const doubl
 #pragma unroll
     for (int k = 0; k < 3; ++k)
         if (ep[k] >= 0) {
-            double g = 0.0;
-            for (int b = 0; b < int(gridDim.x); ++b) g += __ldcg(part + int64_t(b) * npairs + threadIdx.x + k * GT);
-            Gs[ep[k]][eq[k]] = g;
+            // 8 independent partial sums (the loads overlap instead of one
+            // dependent L2 round trip per CTA), combined in a fixed order
+            const double* pp = part + threadIdx.x + k * GT;
+            double g8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            int b = 0;
+            for (; b + 8 <= int(gridDim.x); b += 8)
+#pragma unroll
+                for (int u = 0; u < 8; ++u) g8[u] += __ldcg(pp + int64_t(b + u) * npairs);
+            for (; b < int(gridDim.x); ++b) g8[0] += __ldcg(pp + int64_t(b) * npairs);
+            Gs[ep[k]][eq[k]] = ((g8[0] + g8[1]) + (g8[2] + g8[3])) + ((g8[4] + g8[5]) + (g8[6] + g8[7]));
         }
     __syncthreads();
     if (threadIdx.x < 32) {  // one warp: the column recurrence, lane i owns row i of T
@@ -586,7 +593,7 @@ void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f
     }
 }
 
-void apply_q(Ctx& c, const QRFact& f, bool trans, int64_t k, double* Y, int64_t ldy) {
+void apply_q(Ctx& c, const QRFact& f, bool trans, int64_t k, double* Y, int64_t ldy, int64_t nz_rows) {
     StageTimer _t(c, "qr_apply_q", f.m, f.n, k, 4.0 * double(f.m) * double(std::min(f.m, f.n)) * double(k));
     const int64_t m = f.m, kk = std::min(f.m, f.n);
     if (k <= 0 || kk <= 0) return;
@@ -594,17 +601,24 @@ void apply_q(Ctx& c, const QRFact& f, bool trans, int64_t k, double* Y, int64_t 
     DBuf W = dalloc(c, size_t(NB) * size_t(k));
     DBuf W2 = dalloc(c, size_t(NB) * size_t(k));
     const int64_t nblk = (kk + NB - 1) / NB;
+    // Q [Z; 0] (nz_rows = rows of Z): rows >= nzr of Y are still zero, so
+    // the first block applied reads only Y[j0, nzr) in W = V^T Y, and blocks
+    // entirely below nzr leave Y unchanged
+    int64_t nzr = (nz_rows >= 0 && !trans) ? std::min(nz_rows, m) : m;
     for (int64_t bi = 0; bi < nblk; ++bi) {
         const int64_t b = trans ? bi : (nblk - 1 - bi);
         const int64_t j0 = b * NB;
         const int jb = int(std::min<int64_t>(NB, kk - j0));
         const int64_t mr = m - j0;
+        if (j0 >= nzr) continue;  // H_b acts on zero rows only
+        const int64_t kr = std::min(mr, nzr - j0);
         form_v_launch(c, mr, jb, f.a.d() + j0 + j0 * m, m, V.d());
         double* Ys = Y + j0;
-        dgemm(c, true, false, jb, k, mr, 1.0, V.d(), mr, Ys, ldy, 0.0, W.d(), jb);
+        dgemm(c, true, false, jb, k, kr, 1.0, V.d(), mr, Ys, ldy, 0.0, W.d(), jb);
         // Q Y uses T, Q^T Y uses T^T
         dgemm(c, trans, false, jb, k, jb, 1.0, f.T.d() + j0 * NB, NB, W.d(), jb, 0.0, W2.d(), jb);
         dgemm(c, false, false, mr, k, jb, -1.0, V.d(), mr, W2.d(), jb, 1.0, Ys, ldy);
+        nzr = m;  // rows >= j0 are dense from here on
     }
 }
 
