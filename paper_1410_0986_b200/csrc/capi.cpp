@@ -146,6 +146,11 @@ hydot_status hydot_ctx_destroy(hydot_ctx ctx) {
     hydot_status st = guard(ctx->c.get(), [&] {
         Ctx& c = *ctx->c;
         c.sync();
+        if (c.side) {
+            cudaStreamSynchronize(c.side);
+            cudaStreamDestroy(c.side);
+            c.side = nullptr;
+        }
         if (c.pinned) cudaFreeHost(c.pinned);
         c.pinned = nullptr;
         if (c.jump_dev) cudaFree(c.jump_dev);
@@ -377,7 +382,7 @@ hydot_status hydot_factor_download(hydot_ctx ctx, hydot_factor f, double* U, dou
 
 hydot_status hydot_factor_device_ptrs(hydot_factor f, const double** U_dev, const double** V_dev) {
     if (!f) return HYDOT_EINVAL;
-    if (V_dev && f->f.lazy) {
+    if (V_dev && (f->f.lazy || f->f.pending)) {
         if (!f->owner) return HYDOT_ERUNTIME;
         hydot_status st = guard(f->owner.get(), [&] {
             cudaSetDevice(f->owner->device);

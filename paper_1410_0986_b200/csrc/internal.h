@@ -30,6 +30,13 @@ struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t own_stream = nullptr;
+    // side stream for work whose result is consumed later (the V of a
+    // finished node while the next node's decisions run); created on demand
+    cudaStream_t side = nullptr;
+    cudaStream_t side_stream() {
+        if (!side) HYDOT_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        return side;
+    }
     std::string err;
     int64_t launches = 0;
     int num_sms = 148;

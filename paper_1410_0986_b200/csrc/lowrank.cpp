@@ -263,7 +263,14 @@ SVDd fast_thin_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, i
     return fast_thin_svd_impl(c, S, ld, trans, m, n, l, cat, nullptr, nullptr);
 }
 
+void wait_v(Ctx& c, const Factor& f) {
+    if (!f.pending) return;
+    HYDOT_CUDA(cudaStreamWaitEvent(c.stream, f.pending->ev, 0));
+    f.pending.reset();  // the held inputs are released in c.stream order
+}
+
 void materialize_v(Ctx& c, Factor& f) {
+    wait_v(c, f);
     if (!f.lazy) return;
     const LazyV& L = *f.lazy;
     f.V = dalloc(c, size_t(std::max<int64_t>(f.cols * f.rank, 1)));
@@ -274,6 +281,53 @@ void materialize_v(Ctx& c, Factor& f) {
     }
     c.sync();
     f.lazy.reset();
+}
+
+// HYDOT_ASYNC_V=0 forms every non-root V in line
+bool async_v_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("HYDOT_ASYNC_V");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// V = Q [Z; 0] on the side stream: the next node only needs this node's
+// rank (host), so its sketch / QR / Jacobi overlap the Q application (the
+// small-core Jacobi leaves most SMs idle).  f.V is allocated on c.stream
+// (freed in its order); the side stream starts after everything c.stream
+// has issued and its temporaries live and die on the side stream; the
+// Householder factor and Z stay held until a consumer waits (wait_v).
+void materialize_v_async(Ctx& c, Factor& f) {
+    if (!f.lazy) return;
+    if (!async_v_on() || f.rank == 0) {
+        materialize_v(c, f);
+        return;
+    }
+    const std::shared_ptr<LazyV> L = f.lazy;
+    f.V = dalloc(c, size_t(f.cols * f.rank));
+    cudaEvent_t start = nullptr;
+    HYDOT_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    HYDOT_CUDA(cudaEventRecord(start, c.stream));
+    cudaStream_t main = c.stream, side = c.side_stream();
+    HYDOT_CUDA(cudaStreamWaitEvent(side, start, 0));
+    cudaEventDestroy(start);  // released once recorded work completes
+    auto pend = std::make_shared<Factor::Pending>();
+    pend->hold = L;
+    c.stream = side;
+    try {
+        fill(c, f.cols, f.rank, 0.0, f.V.d(), f.cols);
+        copy2d(c, L->zr, f.rank, L->Z.d(), L->zr, f.V.d(), f.cols);
+        apply_q(c, L->q, false, f.rank, f.V.d(), f.cols, L->zr);
+        HYDOT_CUDA(cudaEventCreateWithFlags(&pend->ev, cudaEventDisableTiming));
+        HYDOT_CUDA(cudaEventRecord(pend->ev, side));
+    } catch (...) {
+        c.stream = main;
+        throw;
+    }
+    c.stream = main;
+    f.lazy.reset();
+    f.pending = pend;
 }
 
 // HYDOT_TRACE_RANDSVD=1: one stderr line per sketch pass / Q = I decision
@@ -393,7 +447,7 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
     }
     charge(l, cat, 2.0 * double(m) * double(keep) * double(qc));
     charge(l, cat, 1.0 * double(n) * double(keep));  // :193-197
-    if (!lazy_v) materialize_v(c, f);
+    if (!lazy_v) materialize_v_async(c, f);
     return f;
 }
 
@@ -412,6 +466,8 @@ Factor agglomerate(Ctx& c, const Factor& f1, const Factor& f2, double eps, uint6
         out.flagged = f1.flagged || f2.flagged;
         return out;
     }
+    wait_v(c, f1);
+    wait_v(c, f2);
     // W = [V1^T; V2^T] held as W^T = [V1 V2] (n x (r1+r2))  :339-341
     DBuf Wt = dalloc(c, size_t(n * (r1 + r2)));
     copy2d(c, n, r1, f1.V.d(), n, Wt.d(), n);
@@ -433,6 +489,7 @@ Factor agglomerate(Ctx& c, const Factor& f1, const Factor& f2, double eps, uint6
     }
     out.V = std::move(inner.V);
     out.lazy = std::move(inner.lazy);
+    out.pending = std::move(inner.pending);
     out.flagged = f1.flagged || f2.flagged || inner.flagged;  // :357
     return out;
 }
@@ -450,6 +507,7 @@ Factor recompress(Ctx& c, const Factor& f, double eps, int rank, Ledger* l) {
     charge(l, HYDOT_CAT_RECOMPRESS, qr_flops(double(M), double(r)) + qr_flops(double(N), double(r)));
     // V = Q_W [Z; 0] (lazy root): QR(V) = Q_W blkdiag(Q_Z, I) [R_Z; 0], so
     // only the small zr x r Z is factored and Q_W is applied once at the end
+    wait_v(c, f);
     const LazyV* lv = f.lazy.get();
     QRFact qu, qv;
     geqrf(c, M, r, f.U.d(), M, qu);  // :564

@@ -28,9 +28,23 @@ struct Factor {
     int method = HYDOT_METHOD_NONE;
     bool flagged = false;
     std::shared_ptr<LazyV> lazy;  // non-null: V is Q [Z; 0] (V itself empty)
+    // non-null: V is being formed on the side stream; valid once `ev` has
+    // completed; `hold` keeps the inputs of that work alive until then
+    struct Pending {
+        cudaEvent_t ev = nullptr;
+        std::shared_ptr<LazyV> hold;
+        ~Pending() {
+            if (ev) cudaEventDestroy(ev);
+        }
+    };
+    mutable std::shared_ptr<Pending> pending;
 };
-// V := Q [Z; 0] in place (no-op for a dense factor)
+// V := Q [Z; 0] in place (no-op for a dense factor); waits for a pending V
 void materialize_v(Ctx& c, Factor& f);
+// start forming V on the side stream (returns at once; consumers call wait_v)
+void materialize_v_async(Ctx& c, Factor& f);
+// make V (dense or pending) usable on c.stream
+void wait_v(Ctx& c, const Factor& f);
 
 // thin SVD result: U m x k, s (host), V n x k
 struct SVDd {
