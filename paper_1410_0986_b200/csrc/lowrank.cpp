@@ -510,11 +510,57 @@ Factor recompress(Ctx& c, const Factor& f, double eps, int rank, Ledger* l) {
     wait_v(c, f);
     const LazyV* lv = f.lazy.get();
     QRFact qu, qv;
-    geqrf(c, M, r, f.U.d(), M, qu);  // :564
+    // the two QRs are independent and latency-bound: QR(U) runs on the side
+    // stream next to QR(V) (or QR(Z)); `side_done` orders the frees of qu
+    // (allocated on the side stream) after every use on c.stream
+    cudaStream_t main = c.stream;
+    // only when both cooperative panel grids (<= one CTA per 64 rows, at
+    // most one per SM) fit on the device together: two partially resident
+    // cooperative grids must never wait on each other
+    auto panel_ctas = [&](int64_t rows) { return std::min<int64_t>(c.num_sms, (rows + 63) / 64); };
+    const bool overlap = async_v_on() && panel_ctas(M) + panel_ctas(lv ? lv->zr : N) <= c.num_sms;
+    struct SideJoin {
+        Ctx& c;
+        cudaStream_t main;
+        bool on;
+        ~SideJoin() {
+            if (!on) return;
+            cudaEvent_t e;
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess) {
+                cudaEventRecord(e, main);
+                cudaStreamWaitEvent(c.side, e, 0);
+                cudaEventDestroy(e);
+            }
+        }
+    } side_done{c, main, overlap};
+    cudaEvent_t ev_u = nullptr;
+    if (overlap) {
+        cudaEvent_t ev0;
+        HYDOT_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+        HYDOT_CUDA(cudaEventRecord(ev0, main));
+        HYDOT_CUDA(cudaStreamWaitEvent(c.side_stream(), ev0, 0));
+        cudaEventDestroy(ev0);
+        c.stream = c.side;
+        try {
+            geqrf(c, M, r, f.U.d(), M, qu);  // :564
+        } catch (...) {
+            c.stream = main;
+            throw;
+        }
+        HYDOT_CUDA(cudaEventCreateWithFlags(&ev_u, cudaEventDisableTiming));
+        HYDOT_CUDA(cudaEventRecord(ev_u, c.side));
+        c.stream = main;
+    } else {
+        geqrf(c, M, r, f.U.d(), M, qu);  // :564
+    }
     if (lv)
         geqrf(c, lv->zr, r, lv->Z.d(), lv->zr, qv);
     else
         geqrf(c, N, r, f.V.d(), N, qv);
+    if (ev_u) {
+        HYDOT_CUDA(cudaStreamWaitEvent(main, ev_u, 0));
+        cudaEventDestroy(ev_u);
+    }
     const int64_t vm = lv ? lv->zr : N;
     DBuf Ru = dalloc(c, size_t(r * r)), Rv = dalloc(c, size_t(r * r)), core = dalloc(c, size_t(r * r));
     extract_upper(c, r, qu.a.d(), M, Ru.d(), r);
