@@ -13,7 +13,10 @@
  *    "_h" pointers are host memory.  No borrowed pointer is retained after a
  *    call returns.
  *  - Every call is stream-ordered on the context's stream and synchronous
- *    from the caller's view for its host outputs.
+ *    from the caller's view for its host outputs.  Internally the context
+ *    also uses one side stream (a node's V formed while the next node
+ *    decides); it is joined to the context's stream by events before any
+ *    result is handed out, so callers only ever see the context's stream.
  *  - Errors: a status code; hydot_last_error(ctx) returns the message.
  *    HYDOT_EINVAL  <-> std::invalid_argument in the reference,
  *    HYDOT_ERUNTIME<-> std::runtime_error (messages keep the reference
