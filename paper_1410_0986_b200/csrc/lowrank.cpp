@@ -266,6 +266,7 @@ SVDd fast_thin_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, i
 void wait_v(Ctx& c, const Factor& f) {
     if (!f.pending) return;
     HYDOT_CUDA(cudaStreamWaitEvent(c.stream, f.pending->ev, 0));
+    f.pending->waited = true;
     f.pending.reset();  // the held inputs are released in c.stream order
 }
 

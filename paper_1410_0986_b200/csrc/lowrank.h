@@ -33,10 +33,16 @@ struct Factor {
     struct Pending {
         cudaEvent_t ev = nullptr;
         std::shared_ptr<LazyV> hold;
+        bool waited = false;  // a stream waits on ev (wait_v)
         ~Pending() {
+            // a factor dropped before any consumer waited: V (freed in
+            // c.stream order) may still be written on the side stream
+            if (ev && !waited) cudaEventSynchronize(ev);
             if (ev) cudaEventDestroy(ev);
         }
     };
+    // declared last: destroyed (and, if never waited on, synchronised) before
+    // the buffers above are released
     mutable std::shared_ptr<Pending> pending;
 };
 // V := Q [Z; 0] in place (no-op for a dense factor); waits for a pending V
