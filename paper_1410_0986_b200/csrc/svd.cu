@@ -41,11 +41,28 @@ constexpr int JT = 256;  // threads per CTA of the large driver
 // t = sign(d) g / (|d| + sqrt(d^2 + g^2)), d = (b - a) / 2 -- the usual
 // zeta = d / g form multiplied through by |g| (one division, one sqrt and
 // one rsqrt on the critical path instead of three divisions and two sqrts)
+//
+// Default form: two reciprocal square roots on the critical path, no
+// division or square root -- with r = 1/rho, rho = sqrt(d^2 + g^2),
+// x = |d|/rho = cos 2theta:  cs = sqrt((1 + x)/2),  sn = sign(d) g r / (2 cs)
+// = sign(d) (g r / 2) rsqrt((1 + x)/2); cs^2 + sn^2 = 1 identically.
+// HYDOT_ROT_FORM=0 (compile time) keeps the t-form.
+#ifndef HYDOT_ROT_FORM
+#define HYDOT_ROT_FORM 1
+#endif
 __device__ __forceinline__ void rot_params(double a, double b, double g, double& cs, double& sn) {
     const double d = 0.5 * (b - a);
+#if HYDOT_ROT_FORM
+    const double r = rsqrt(fma(d, d, g * g));
+    const double h = fma(0.5 * fabs(d), r, 0.5);  // (1 + x) / 2 in (1/2, 1]
+    const double ih = rsqrt(h);
+    cs = h * ih;
+    sn = copysign(1.0, d) * (0.5 * g * r) * ih;
+#else
     const double t = copysign(1.0, d) * g / (fabs(d) + sqrt(fma(d, d, g * g)));
     cs = rsqrt(fma(t, t, 1.0));
     sn = cs * t;
+#endif
 }
 
 // one warp orthogonalises columns p, q of U (m rows) and rotates V (n rows);
