@@ -151,6 +151,8 @@ hydot_status hydot_ctx_destroy(hydot_ctx ctx) {
             cudaStreamDestroy(c.side);
             c.side = nullptr;
         }
+        if (c.coop_ev) cudaEventDestroy(c.coop_ev);
+        c.coop_ev = nullptr;
         if (c.pinned) cudaFreeHost(c.pinned);
         c.pinned = nullptr;
         if (c.jump_dev) cudaFree(c.jump_dev);

@@ -37,6 +37,23 @@ struct Ctx {
         if (!side) HYDOT_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
         return side;
     }
+    // Cooperative launches of both streams form one chain (each waits for
+    // the previous one to finish): a cooperative grid then only ever shares
+    // the GPU with ordinary kernels, which always complete, so two partially
+    // resident grids can never wait on each other.  coop_unchained: the
+    // caller has proven that the grids in flight fit the device together.
+    cudaEvent_t coop_ev = nullptr;
+    bool coop_recorded = false;
+    bool coop_unchained = false;
+    void coop_launch(const void* kern, dim3 grid, dim3 block, void** args, size_t smem) {
+        if (!coop_unchained && coop_recorded) HYDOT_CUDA(cudaStreamWaitEvent(stream, coop_ev, 0));
+        HYDOT_CUDA(cudaLaunchCooperativeKernel(kern, grid, block, args, smem, stream));
+        if (!coop_unchained) {
+            if (!coop_ev) HYDOT_CUDA(cudaEventCreateWithFlags(&coop_ev, cudaEventDisableTiming));
+            HYDOT_CUDA(cudaEventRecord(coop_ev, stream));
+            coop_recorded = true;
+        }
+    }
     std::string err;
     int64_t launches = 0;
     int num_sms = 148;

@@ -175,13 +175,47 @@ SVDd thin_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, int64_
 }
 
 namespace {
+// The presorted tall QR of the Q = I branch, started speculatively (see
+// randsvd).  Its buffers are allocated on c.stream; the side stream fills
+// them; `ev` marks completion.  Unused, it makes c.stream wait for `ev`
+// before its buffers are released.
+struct TallSpec {
+    Ctx* c = nullptr;
+    const double* src = nullptr;
+    int64_t ld = 0, m = 0, n = 0;
+    std::vector<int> perm;
+    DBuf dperm;
+    QRFact qf;
+    cudaEvent_t ev = nullptr;
+    bool used = false;
+    ~TallSpec() {
+        if (ev) {
+            if (!used && c) cudaStreamWaitEvent(c->stream, ev, 0);
+            cudaEventDestroy(ev);
+        }
+    }
+};
+
+// column order by decreasing norm of the m x n matrix L
+void presort_perm(Ctx& c, int64_t m, int64_t n, const double* Lp, int64_t ldl, std::vector<int>& perm) {
+    DBuf nrm = dalloc(c, size_t(n));
+    col_norms(c, m, n, Lp, ldl, nrm.d());
+    std::vector<double> hn(static_cast<size_t>(n));
+    c.d2h(hn.data(), nrm.d(), size_t(n));
+    perm.resize(static_cast<size_t>(n));
+    for (int64_t j = 0; j < n; ++j) perm[size_t(j)] = int(j);
+    std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return hn[size_t(a)] > hn[size_t(b)]; });
+}
+}  // namespace
+
+namespace {
 // lazyU / lazyV: the caller accepts U (resp. V) as Q [Ur; 0] when the tall
 // branch produces it (the request is forwarded through the transposed
 // recursion); the SVDd's U (V) is then left empty.
 SVDd fast_thin_svd_impl(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, int64_t n,
-                        Ledger* l, int cat, LazyV* lazyU, LazyV* lazyV) {
+                        Ledger* l, int cat, LazyV* lazyU, LazyV* lazyV, TallSpec* spec = nullptr) {
     if (n >= 2 * m && m > 0) {  // lowrank.cpp:66-72
-        SVDd t = fast_thin_svd_impl(c, S, ld, !trans, n, m, l, cat, lazyV, lazyU);
+        SVDd t = fast_thin_svd_impl(c, S, ld, !trans, n, m, l, cat, lazyV, lazyU, spec);
         SVDd o;
         o.m = m;
         o.n = n;
@@ -219,21 +253,26 @@ SVDd fast_thin_svd_impl(Ctx& c, const double* S, int64_t ld, bool trans, int64_t
             // preconditioner's first QR, so only R1^T's QR remains
             // (A = (Q Ux) S (P Q2 Vx)^T) -- one n x n QR and one n x n
             // Q-application fewer than sorting R afterwards
-            DBuf nrm = dalloc(c, size_t(n));
-            col_norms(c, m, n, Lp, ldl, nrm.d());
-            std::vector<double> hn(static_cast<size_t>(n));
-            c.d2h(hn.data(), nrm.d(), size_t(n));
-            std::vector<int> perm(static_cast<size_t>(n));
-            for (int64_t j = 0; j < n; ++j) perm[size_t(j)] = int(j);
-            std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return hn[size_t(a)] > hn[size_t(b)]; });
-            DBuf dperm(c, size_t(n) * sizeof(int));
-            HYDOT_CUDA(cudaMemcpyAsync(dperm.as<void>(), perm.data(), size_t(n) * sizeof(int),
-                                       cudaMemcpyHostToDevice, c.stream));
-            DBuf As = dalloc(c, size_t(m * n));
-            gather_cols(c, m, n, Lp, ldl, dperm.as<int>(), As.d(), m);
+            std::vector<int> perm;
+            DBuf dperm;
+            if (spec && spec->ev && !trans && spec->src == Lp && spec->ld == ldl && spec->m == m &&
+                spec->n == n) {  // started speculatively on the side stream
+                HYDOT_CUDA(cudaStreamWaitEvent(c.stream, spec->ev, 0));
+                spec->used = true;
+                perm = std::move(spec->perm);
+                dperm = std::move(spec->dperm);
+                qf = std::move(spec->qf);
+            } else {
+                presort_perm(c, m, n, Lp, ldl, perm);
+                dperm = DBuf(c, size_t(n) * sizeof(int));
+                HYDOT_CUDA(cudaMemcpyAsync(dperm.as<void>(), perm.data(), size_t(n) * sizeof(int),
+                                           cudaMemcpyHostToDevice, c.stream));
+                DBuf As = dalloc(c, size_t(m * n));
+                gather_cols(c, m, n, Lp, ldl, dperm.as<int>(), As.d(), m);
+                tmp.release();
+                geqrf(c, m, n, As.d(), m, qf);
+            }
             tmp.release();
-            geqrf(c, m, n, As.d(), m, qf);
-            As.release();
             DBuf R1 = dalloc(c, size_t(n * n)), Vr = dalloc(c, size_t(n * n));
             extract_upper(c, n, qf.a.d(), m, R1.d(), n);
             svd_of_sorted_r(c, n, R1.d(), Ur.d(), o.s, Vr.d());
@@ -282,6 +321,15 @@ void materialize_v(Ctx& c, Factor& f) {
     }
     c.sync();
     f.lazy.reset();
+}
+
+// HYDOT_SPECULATE=0: no speculative Q = I branch QR
+bool speculate_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("HYDOT_SPECULATE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 
 // HYDOT_ASYNC_V=0 forms every non-root V in line
@@ -356,6 +404,49 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
     DBuf YP;
     int64_t qc = 0;
     bool identity = false;
+    // Speculation: when the first sketch pass will be followed, if rejected,
+    // by Q = I (the doubled rank reaches nmax) -- nearly every call of the
+    // path -- the Q = I branch's presorted tall QR of A^T starts now on the
+    // side stream, beside the sketch pass.  An accepted pass discards it.
+    std::unique_ptr<TallSpec> spec;
+    {
+        const int64_t r1 = r, rs1 = std::min<int64_t>(r1 + p, nmax);
+        const int64_t r2 = std::min<int64_t>(2 * r1, nmax), rs2 = std::min<int64_t>(r2 + p, nmax);
+        if (!(rs1 >= nmax && m <= n) && rs2 >= nmax && m <= n && n >= 2 * m && m > 48 &&
+            presort_tall() && async_v_on() && speculate_on()) {
+            spec.reset(new TallSpec());
+            spec->c = &c;
+            spec->src = At;
+            spec->ld = lda;
+            spec->m = n;
+            spec->n = m;
+            presort_perm(c, n, m, At, lda, spec->perm);
+            spec->dperm = DBuf(c, size_t(m) * sizeof(int));
+            HYDOT_CUDA(cudaMemcpyAsync(spec->dperm.as<void>(), spec->perm.data(), size_t(m) * sizeof(int),
+                                       cudaMemcpyHostToDevice, c.stream));
+            spec->qf.a = dalloc(c, size_t(n * m));  // on c.stream: freed in its order
+            spec->qf.tau = dalloc(c, size_t(m));
+            spec->qf.T = dalloc(c, size_t(kQRBlock) * size_t(m));
+            cudaEvent_t start;
+            HYDOT_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+            HYDOT_CUDA(cudaEventRecord(start, c.stream));
+            cudaStream_t main = c.stream, side = c.side_stream();
+            HYDOT_CUDA(cudaStreamWaitEvent(side, start, 0));
+            cudaEventDestroy(start);
+            c.stream = side;
+            try {
+                DBuf As = dalloc(c, size_t(n * m));
+                gather_cols(c, n, m, At, lda, spec->dperm.as<int>(), As.d(), n);
+                geqrf(c, n, m, As.d(), n, spec->qf);
+                HYDOT_CUDA(cudaEventCreateWithFlags(&spec->ev, cudaEventDisableTiming));
+                HYDOT_CUDA(cudaEventRecord(spec->ev, side));
+            } catch (...) {
+                c.stream = main;
+                throw;
+            }
+            c.stream = main;
+        }
+    }
     while (true) {
         const int64_t rs = std::min<int64_t>(r + p, nmax);
         if (rs >= nmax && m <= n) {  // lowrank.cpp:159-164: Q = I_m
@@ -413,7 +504,7 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
     // V of the tall branch always comes back implicit (Q [Ur; 0]): only the
     // kept columns are then formed (or, with lazy_v, none until first use)
     auto lz = std::make_shared<LazyV>();
-    SVDd svdB = fast_thin_svd_impl(c, Btp, ldb, true, qc, n, l, cat, nullptr, lz.get());
+    SVDd svdB = fast_thin_svd_impl(c, Btp, ldb, true, qc, n, l, cat, nullptr, lz.get(), identity ? spec.get() : nullptr);
     const std::vector<double>& s = svdB.s;
     const double s1 = s.empty() ? 0.0 : s[0];
     int64_t keep = 0;
@@ -535,6 +626,12 @@ Factor recompress(Ctx& c, const Factor& f, double eps, int rank, Ledger* l) {
         }
     } side_done{c, main, overlap};
     cudaEvent_t ev_u = nullptr;
+    struct Unchain {
+        Ctx& c;
+        bool prev;
+        Unchain(Ctx& cc, bool on) : c(cc), prev(cc.coop_unchained) { c.coop_unchained = prev || on; }
+        ~Unchain() { c.coop_unchained = prev; }
+    } unchain{c, overlap};  // both panel grids fit the device together (checked above)
     if (overlap) {
         cudaEvent_t ev0;
         HYDOT_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
@@ -562,6 +659,7 @@ Factor recompress(Ctx& c, const Factor& f, double eps, int rank, Ledger* l) {
         HYDOT_CUDA(cudaStreamWaitEvent(main, ev_u, 0));
         cudaEventDestroy(ev_u);
     }
+    c.coop_unchained = unchain.prev;  // later cooperative launches chain again
     const int64_t vm = lv ? lv->zr : N;
     DBuf Ru = dalloc(c, size_t(r * r)), Rv = dalloc(c, size_t(r * r)), core = dalloc(c, size_t(r * r));
     extract_upper(c, r, qu.a.d(), M, Ru.d(), r);

@@ -394,11 +394,9 @@ void panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, const
     PanelBufs b = pbuf;
     void* args[] = {&mr, &jb, &P, &ld, &rows_per, &tau, &b};
     if (use_smem)
-        HYDOT_CUDA(cudaLaunchCooperativeKernel((void*)qr_panel_coop<true>, dim3(G), dim3(PT), args,
-                                               smem, c.stream));
+        c.coop_launch((void*)qr_panel_coop<true>, dim3(G), dim3(PT), args, smem);
     else
-        HYDOT_CUDA(cudaLaunchCooperativeKernel((void*)qr_panel_coop<false>, dim3(G), dim3(PT), args, 0,
-                                               c.stream));
+        c.coop_launch((void*)qr_panel_coop<false>, dim3(G), dim3(PT), args, 0);
     c.count();
 }
 
@@ -536,9 +534,11 @@ void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f
     StageTimer _t(c, "qr_geqrf", m, n, -1, 2.0 * double(m) * double(n) * double(n));
     f.m = m;
     f.n = n;
-    f.a = dalloc(c, size_t(std::max<int64_t>(m * n, 1)));
-    f.tau = dalloc(c, size_t(std::max<int64_t>(n, 1)));
-    f.T = dalloc(c, size_t(NB) * size_t(std::max<int64_t>(n, 1)));
+    // buffers may be preallocated by the caller (on another stream)
+    if (f.a.bytes() < size_t(std::max<int64_t>(m * n, 1)) * 8) f.a = dalloc(c, size_t(std::max<int64_t>(m * n, 1)));
+    if (f.tau.bytes() < size_t(std::max<int64_t>(n, 1)) * 8) f.tau = dalloc(c, size_t(std::max<int64_t>(n, 1)));
+    if (f.T.bytes() < size_t(NB) * size_t(std::max<int64_t>(n, 1)) * 8)
+        f.T = dalloc(c, size_t(NB) * size_t(std::max<int64_t>(n, 1)));
     copy2d(c, m, n, A, lda, f.a.d(), m);
     const int64_t k = std::min(m, n);
     if (k <= 0) return;

@@ -754,8 +754,7 @@ void launch_rblk_t(Ctx& c, int64_t m, int64_t n, double* U, int64_t ldu, double 
     }();
     int cross = cross_env;
     void* args[] = {&mm, &nn, &nbb, &bp, &U, &ldu, &tol, &counters, &sweeps_out, &cross, &stop_thr};
-    HYDOT_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_rblk_k<R, T, B>, dim3(grid), dim3(T), args, 0,
-                                           c.stream));
+    c.coop_launch((void*)jacobi_rblk_k<R, T, B>, dim3(grid), dim3(T), args, 0);
     c.count();
 }
 
@@ -960,8 +959,7 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
             const int2* pp = dpairs;
             void* args[] = {&mm, &nn, &npp, &pp, &up, &ldu, &vp, &ldv, &tl, &at, &cnt, &so};
             void* rargs[] = {&mm, &nn, &npp, &pp, &up, &ldu, &tl, &cnt, &so};
-            HYDOT_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(JT), reg_mode ? rargs : args,
-                                                   0, c.stream));
+            c.coop_launch(kern, dim3(grid), dim3(JT), reg_mode ? rargs : args, 0);
             c.count();
         }
     }
