@@ -841,7 +841,11 @@ void rblk_converge(Ctx& c, int R, int T, int B, int64_t m, int64_t n, double* U,
     // a sweep of <= 12 n rotations is followed by one of at most a few hundred
     // on the path's cores; fixing a pair costs ~1/100 of a sweep at n = 300
     const int cap = int(std::clamp<int64_t>(n / 4, 16, 256));
-    launch_rblk(c, R, T, B, m, n, U, m, tol, counters, sweeps_out, int(std::min<int64_t>(12 * n, 1 << 30)));
+    static const int tailk = [] {  // HYDOT_JACOBI_TAILK: the stop threshold in units of n
+        const char* e = std::getenv("HYDOT_JACOBI_TAILK");
+        return e ? std::max(1, std::atoi(e)) : 12;
+    }();
+    launch_rblk(c, R, T, B, m, n, U, m, tol, counters, sweeps_out, int(std::min<int64_t>(tailk * n, 1 << 30)));
     DBuf G = dalloc(c, size_t(n * n));
     DBuf cnt(c, sizeof(int));
     DBuf lst(c, sizeof(int2) * cap);
