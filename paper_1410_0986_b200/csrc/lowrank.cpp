@@ -412,7 +412,11 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
     {
         const int64_t r1 = r, rs1 = std::min<int64_t>(r1 + p, nmax);
         const int64_t r2 = std::min<int64_t>(2 * r1, nmax), rs2 = std::min<int64_t>(r2 + p, nmax);
-        if (!(rs1 >= nmax && m <= n) && rs2 >= nmax && m <= n && n >= 2 * m && m > 48 &&
+        // the speculative copy + factor hold 2 n m doubles beside the pass:
+        // capped at 16 GB (config 1's root needs 3.8 GB); cudaMemGetInfo is
+        // not used here -- it cost 2 % of the step and most of the e2e overlap
+        const bool small = double(n) * double(m) * 16.0 <= 16.0 * double(1ull << 30);
+        if (!(rs1 >= nmax && m <= n) && rs2 >= nmax && m <= n && n >= 2 * m && m > 48 && small &&
             presort_tall() && async_v_on() && speculate_on()) {
             spec.reset(new TallSpec());
             spec->c = &c;
