@@ -48,9 +48,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-sample", type=int, default=1, help="cpu_baseline: leaf clusters timed")
+    ap.add_argument("--cpu-sample", type=int, default=1, help="cpu_baseline: sources timed")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -339,9 +339,8 @@ def run_b200(args):
         # ---- CPU baseline (rank 0, N=1 only): the oracle on a bounded sample
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            Fg = np.zeros((len(st.points), cfg.n_lambda, g.N))
-            Fg[pts] = Fh.numpy()
-            cpu = cpu_sample(st, tree, eps, Fg, threads=1, leaves=args.cpu_sample)
+            Fhn = Fh.numpy()
+            cpu = cpu_sample(st, eps, lambda p: Fhn[loc[p]], threads=1, n_src=args.cpu_sample)
 
         out = {
             "metric": "(s,d) Born blocks compressed/s",
@@ -355,7 +354,7 @@ def run_b200(args):
             "scaling": "strong",
             "vs_baseline": None,
             "dtype": "f64",
-            "data": "synthetic (seeded BASELINE config-1 physics, configs.py; fields from the GPU CG)",
+            "data": f"synthetic (seeded BASELINE {cfg.name} physics, configs.py; fields from the GPU CG)",
             "config": {"workload": f"{cfg.name}: compress_H = Born assembly + recursive randSVD + merges + recompress",
                        "n": cfg.n, "N": g.N, "n_sources": cfg.n_sources, "n_det": cfg.n_det,
                        "n_lambda": cfg.n_lambda, "n_chrom": cfg.n_chrom, "M": cfg.M,
@@ -460,29 +459,56 @@ def global_perm(tree, plan, rows_per, st):
     return np.asarray(out, dtype=np.int32)
 
 
-def cpu_sample(st, tree, eps, Fh, threads: int, leaves: int = 1):
-    """Oracle restatement timed on the host: the first `leaves` leaf clusters
-    of the tree (leaf randsvds + their within-leaf agglomerate) of the same
-    workload; value in blocks/s."""
+def sample_sources(st, n_src):
+    """The first `n_src` sources in the tree's leaf order (the order in which
+    recursive_lowrank meets them, lowrank.cpp:480-488)."""
+    from_tree = []
+
+    def walk(nodes, u):
+        nd = nodes[u]
+        if nd["left"] < 0:
+            from_tree.extend(nd["idx"])
+        else:
+            walk(nodes, nd["left"])
+            walk(nodes, nd["right"])
+    from oracle import oracle as o
+    t = o.ClusterTree(st.source_xy, st.box_lo, st.box_hi)
+    walk(t.nodes, t.root)
+    return [int(s) for s in from_tree[:n_src]]
+
+
+def sample_points(st, srcs):
+    cfg = st.cfg
+    return sorted({int(st.source_point[s]) for s in srcs} |
+                  {int(st.detector_point[s, d]) for s in srcs for d in range(cfg.n_det)})
+
+
+def cpu_sample(st, eps, field, threads: int, n_src: int = 1):
+    """Oracle restatement timed on the host: the leaf compression of the
+    first `n_src` sources of the tree's leaf order (their randsvds with the
+    reference's leaf-hint chain starting at r0 = 1, plus their agglomerate
+    when n_src = 2) on the same workload; `field(point)` -> (n_lambda, N)
+    host array.  Value in blocks/s."""
     from oracle import oracle as o
     o.set_threads(threads)
     cfg = st.cfg
-    otree = o.ClusterTree(st.source_xy, st.box_lo, st.box_hi)
-    leaf_nodes = [v for v, n in enumerate(otree.nodes) if n["left"] < 0][:leaves]
-    srcs = [s for v in leaf_nodes for s in otree.nodes[v]["idx"]]
-    inc = [Fh[st.source_point[s]].T for s in srcs]
-    adj = [[Fh[st.detector_point[s, d]].T for d in range(cfg.n_det)] for s in srcs]
+    srcs = sample_sources(st, n_src)
+    inc = [np.ascontiguousarray(field(int(st.source_point[s])).T) for s in srcs]
+    adj = [[np.ascontiguousarray(field(int(st.detector_point[s, d])).T) for d in range(cfg.n_det)]
+           for s in srcs]
     w = np.full(cfg.N, cfg.h ** 3)
     # a sub-tree over just these sources reproduces the leaf work
-    pos = st.source_xy[srcs]
-    sub = o.ClusterTree(pos, st.box_lo, st.box_hi)
+    sub = o.ClusterTree(st.source_xy[srcs], st.box_lo, st.box_hi)
     t0 = time.perf_counter()
     o.recursive_lowrank_born(sub, eps, inc, adj, w, 1.0, seed=cfg.seed)
     dt = time.perf_counter() - t0
     blocks = len(srcs) * cfg.n_det
+    what = "leaf randsvd" if len(srcs) == 1 else "leaf randsvds + their agglomerate"
     return {"value": blocks / dt, "unit": "blocks/s", "cores": threads, "kind": "port",
-            "sample": f"{len(srcs)} sources ({blocks} (s,d) blocks) of {cfg.name}: leaf randsvds + "
-                      f"their agglomerate, {dt:.2f} s; excludes the upper merges (an optimistic CPU rate)",
+            "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
+            "sample": f"{len(srcs)} source(s) ({blocks} (s,d) blocks) of {cfg.name}: {what} "
+                      f"(m={cfg.rows_per_source} x N={cfg.N}, first leaf of the hint chain, r0=1), "
+                      f"{dt:.2f} s; excludes assembly-free upper merges and recompress (an optimistic CPU rate)",
             "seconds": dt}
 
 
@@ -642,38 +668,58 @@ def run_pals(args):
 
 
 # ---------------------------------------------------------- reference arm --
+def load_configs():
+    """configs.py (numpy only) loaded by path: importing the package would
+    load libhydot_b200.so, which the reference arm must not touch."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "hydot_configs", os.path.join(ROOT, "paper_1410_0986_b200", "configs.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules["hydot_configs"] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def run_reference(args):
     rank, world, local = dist_info()
     if rank != 0:
         return  # rank 0 alone runs the CPU reference
-    from paper_1410_0986_b200 import configs
+    configs = load_configs()
     from oracle import oracle as o
     cfg = configs.CONFIGS[args.config]
     st = configs.make_setup(cfg)
     threads = os.cpu_count() or 1
     o.set_threads(threads)
-    # the oracle's own CPU CG produces the fields of the sampled sources
-    g = st.grid()
+    # the oracle's own CPU CG produces the fields of the sampled source
+    g = st.host_grid()
     otree = o.ClusterTree(st.source_xy, st.box_lo, st.box_hi)
     eps = configs.compression_tolerance(st, otree.depth())
-    leaf = [v for v, n in enumerate(otree.nodes) if n["left"] < 0][0]
-    srcs = otree.nodes[leaf]["idx"]
-    pts = sorted({int(st.source_point[s]) for s in srcs} |
-                 {int(st.detector_point[s, d]) for s in srcs for d in range(cfg.n_det)})
+    srcs = sample_sources(st, args.cpu_sample)
+    pts = sample_points(st, srcs)
     Fo, _, _ = o.fields((g.nx, g.ny, g.nz), g.h, st.sigma, st.sigma_prime, st.inv_D,
                         st.points[pts], tol=1e-10, threads=threads)
     nl = cfg.n_lambda
-    Fh = np.zeros((len(st.points), nl, g.N))
-    for k, p in enumerate(pts):
-        Fh[p] = Fo[:, k * nl:(k + 1) * nl].T
+    col = {p: k for k, p in enumerate(pts)}
 
-    class Tree:
-        pass
+    def field(p):
+        k = col[p]
+        return Fo[:, k * nl:(k + 1) * nl].T
 
     times = []
     res = None
     for i in range(args.warmup + args.steps):
-        r = cpu_sample(st, otree, eps, Fh, threads=threads, leaves=1)
+        r = cpu_sample(st, eps, field, threads=threads, n_src=args.cpu_sample)
         if i >= args.warmup:
             times.append(r["seconds"])
             res = r
@@ -683,10 +729,13 @@ def run_reference(args):
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (seeded BASELINE config-1 physics)", "impl": "reference",
-           "config": {"workload": f"{cfg.name}: one leaf cluster per step (bounded CPU sample)",
-                      "n": cfg.n, "N": g.N},
+           "data": f"synthetic (seeded BASELINE {cfg.name} physics)", "impl": "reference",
+           "config": {"workload": f"{cfg.name}: compress_H leaf work, one source leaf per step "
+                                  f"(bounded CPU sample)",
+                      "n": cfg.n, "N": g.N, "n_sources": cfg.n_sources, "n_det": cfg.n_det,
+                      "n_lambda": cfg.n_lambda, "M": cfg.M},
            "cpu_baseline": {"value": value, "unit": "blocks/s", "cores": threads, "kind": "port",
+                            "cpu_model": cpu_model(),
                             "sample": res["sample"] if res else ""},
            "e2e": {"value": value, "unit": "blocks/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}

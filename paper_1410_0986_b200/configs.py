@@ -89,6 +89,23 @@ class Setup:
         n = self.cfg.n
         return Grid7(n, n, n, self.cfg.h)
 
+    def host_grid(self):
+        """The same vertex grid without the device package (CPU reference arm)."""
+        n = self.cfg.n
+        return HostGrid(n, n, n, self.cfg.h)
+
+
+@dataclass
+class HostGrid:
+    nx: int
+    ny: int
+    nz: int
+    h: float
+
+    @property
+    def N(self) -> int:
+        return self.nx * self.ny * self.nz
+
 
 def make_setup(cfg: Config) -> Setup:
     rng = np.random.default_rng(cfg.seed)
