@@ -328,8 +328,11 @@ hydot_status hydot_factor_load(hydot_ctx ctx, const char* path, hydot_factor* ou
 hydot_status hydot_block_save(hydot_ctx ctx, const double* block_dev, int64_t rows, int64_t cols,
                               int64_t ld, const char* path);
 hydot_status hydot_block_file_info(const char* path, int64_t* rows, int64_t* cols);
+/* rows_cap: rows the device buffer holds (row stride ld >= cols); a file
+ * whose header exceeds rows_cap x ld is rejected (HYDOT_EINVAL) before any
+ * device write. */
 hydot_status hydot_block_load(hydot_ctx ctx, const char* path, double* block_dev, int64_t ld,
-                              int64_t* rows, int64_t* cols);
+                              int64_t rows_cap, int64_t* rows, int64_t* cols);
 
 /* ---------------------------------------------------------------- pals -- */
 /* Parametric level-set reconstruction, the caller of the compressed

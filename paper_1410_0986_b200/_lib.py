@@ -155,7 +155,7 @@ SIGNATURES = {
     "hydot_factor_load": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp), _ip, C.c_int64]),
     "hydot_block_save": (C.c_int, [_vp, _dp, C.c_int64, C.c_int64, C.c_int64, C.c_char_p]),
     "hydot_block_file_info": (C.c_int, [C.c_char_p, _i64p, _i64p]),
-    "hydot_block_load": (C.c_int, [_vp, C.c_char_p, _dp, C.c_int64, _i64p, _i64p]),
+    "hydot_block_load": (C.c_int, [_vp, C.c_char_p, _dp, C.c_int64, C.c_int64, _i64p, _i64p]),
     "hydot_apply_fem": (C.c_int, [_vp, C.POINTER(GridGeom), C.c_double, C.c_double, _dp, _dp]),
     "hydot_fields_solve_fem": (C.c_int, [_vp, C.POINTER(GridGeom), C.c_int, _dp, _dp, _dp, _dp, C.c_int,
                                          C.c_double, C.c_int, C.c_int, _dp, _ip, _dp]),

@@ -131,7 +131,7 @@ def load_block(ctx: Context, path: str) -> torch.Tensor:
     out = ctx.empty(max(rows.value, 1), max(cols.value, 1))[:rows.value, :cols.value]
     r2, c2 = C.c_int64(), C.c_int64()
     check(lib().hydot_block_load(ctx.h, os.fsencode(path), dptr(out), max(cols.value, 1),
-                                 C.byref(r2), C.byref(c2)), ctx.h)
+                                 rows.value, C.byref(r2), C.byref(c2)), ctx.h)
     return out
 
 

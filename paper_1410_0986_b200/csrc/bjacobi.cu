@@ -1,0 +1,464 @@
+// bjacobi.cu -- block one-sided Jacobi on the FP64 tensor cores (DMMA) for
+// the large SVD cores of the path: the R factors behind Eigen's BDCSVD calls
+// (lowrank.cpp:43-49, 79, 88, 568) once they reach hundreds to thousands of
+// columns (config 2's root merge core is 5686 x 5686).
+//
+// The point drivers of svd.cu orthogonalise one column pair per rotation, so
+// every sub-round costs an m-long CTA reduction and a barrier, and a sweep
+// streams the matrix once per block round at ~1 flop/byte.  Here the columns
+// are grouped in blocks of BW = 16; a tournament (circle method) over the
+// blocks pairs them up, and one visit of a block pair X_p = [X_i X_j]
+// (m x 32) is
+//   1. G_p = X_p^T X_p             (DMMA, rows split in chunks, partial
+//                                    Grams summed in a fixed chunk order)
+//   2. G_p = Q_p D Q_p^T           (cyclic two-sided Jacobi on the 32 x 32
+//                                    Gram in shared memory, by the CTA that
+//                                    completes the pair's last chunk)
+//   3. X_p <- X_p Q_p              (DMMA, in place, row chunks)
+// so a sweep is 8 m n^2 tensor-core flops plus ~3 passes over the matrix per
+// block round, with two grid barriers per round (one cooperative launch per
+// sweep).  Accuracy: the Gram entries carry errors ~ m eps |x_k| |x_l|, i.e.
+// relative to each column pair, and two-sided Jacobi on a positive
+// semidefinite matrix with the relative stopping test |g_kl| <= tol
+// sqrt(g_kk g_ll) is relatively accurate (Demmel-Veselic); the update is an
+// orthogonal transformation of the columns, as in the point method.  A pair
+// whose Gram passes the test is left untouched; a sweep in which no pair
+// rotates ends the iteration, and the columns are then those of a converged
+// one-sided Jacobi (sigma_j = |x_j|, U = x_j / sigma_j).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <numeric>
+#include <vector>
+
+#include "internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace hydot {
+namespace {
+
+constexpr int BW = 16;        // columns per block
+constexpr int PW = 2 * BW;    // columns per block pair
+constexpr int SUB = 64;       // rows per shared-memory sub-tile
+constexpr int NTH = 128;      // threads per CTA (4 warps)
+constexpr int XS = SUB + 4;   // X sub-tile stride ([col][row], conflict-free fragments)
+constexpr int QS = PW + 4;    // Q stride ([out col][in col])
+constexpr int GS = PW + 1;    // eigen-solver stride
+constexpr int kInner = 30;    // max inner sweeps on one pair Gram
+constexpr int kMaxBSweeps = 40;
+
+struct BJArgs {
+    int64_t m;
+    int n, nbp, per, rounds;
+    const int2* pairs;  // rounds x per block pairs (circle method)
+    double* U;
+    int64_t ldu;
+    double tol, flag_tol;
+    int nch, rch;
+    double* gws;  // per x nch x PW*PW partial Grams
+    double* qws;  // per x PW*PW rotations
+    int* flag;    // per: 1 = rotate this round
+    int* cnt;     // per: chunk arrival counters (self-resetting)
+    int* stats;   // [0] pairs rotated this sweep, [1] inner rotations
+};
+
+__device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, double b0) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 "
+        "{%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+        : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+        : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// rotation annihilating g of the 2x2 Gram [[a, g], [g, b]] (svd.cu's form:
+// cos 2theta from a reciprocal square root, no division)
+__device__ __forceinline__ void rot2(double a, double b, double g, double& cs, double& sn) {
+    const double d = 0.5 * (b - a);
+    const double r = rsqrt(fma(d, d, g * g));
+    const double h = fma(0.5 * fabs(d), r, 0.5);
+    const double ih = rsqrt(h);
+    cs = h * ih;
+    sn = copysign(1.0, d) * (0.5 * g * r) * ih;
+}
+
+__device__ __forceinline__ int circ(int pos, int r, int np) {
+    return pos == 0 ? 0 : ((pos - 1 + r) % (np - 1)) + 1;
+}
+
+// global column of pair-local column j (-1: padding / dummy block)
+__device__ __forceinline__ int pair_col(int2 bp, int j, int n) {
+    const int blk = j < BW ? bp.x : bp.y;
+    const int c = blk * BW + (j & (BW - 1));
+    return c < n ? c : -1;
+}
+
+// load rows [r, r+SUB) of the pair's 32 columns into xs[col][row] (zeros
+// outside), coalesced along rows
+__device__ __forceinline__ void load_sub(double* xs, const double* __restrict__ U, int64_t ldu,
+                                         const int* col, int64_t r, int64_t rend) {
+#pragma unroll 4
+    for (int e = threadIdx.x; e < SUB * PW; e += NTH) {
+        const int i = e & (SUB - 1), j = e / SUB;
+        const int64_t gi = r + i;
+        const int cj = col[j];
+        xs[j * XS + i] = (cj >= 0 && gi < rend) ? __ldcg(U + gi + int64_t(cj) * ldu) : 0.0;
+    }
+}
+
+// ---- phase 1: partial Gram of one (pair, row chunk) unit; the CTA that
+// completes a pair's last chunk diagonalises its Gram
+__device__ void eig_pair(const BJArgs& a, int q, double* smem);
+
+__device__ void gram_unit(const BJArgs& a, int2 bp, int q, int ch, double* smem, int* col) {
+    double* xs = smem;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wi = (warp & 1) * 16, wj = (warp >> 1) * 16;
+    double acc[2][4];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+    const int64_t r0 = int64_t(ch) * a.rch, r1 = min(a.m, r0 + a.rch);
+    for (int64_t r = r0; r < r1; r += SUB) {
+        __syncthreads();
+        load_sub(xs, a.U, a.ldu, col, r, r1);
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < SUB; kk += 4) {
+            // A = X^T (i = column, k = row), B = X (k = row, j = column)
+            const double a0 = xs[(wi + g) * XS + kk + t];
+            const double a1 = xs[(wi + g + 8) * XS + kk + t];
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) dmma(acc[ni], a0, a1, xs[(wj + ni * 8 + g) * XS + kk + t]);
+        }
+    }
+    double* out = a.gws + (int64_t(q) * a.nch + ch) * (PW * PW);
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int i = wi + g + ((v & 2) ? 8 : 0);
+            const int j = wj + ni * 8 + 2 * t + (v & 1);
+            __stcg(out + i + j * PW, acc[ni][v]);
+        }
+    __threadfence();
+    __syncthreads();
+    __shared__ int last;
+    if (threadIdx.x == 0) last = atomicAdd(a.cnt + q, 1) == a.nch - 1;
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        eig_pair(a, q, smem);
+        if (threadIdx.x == 0) a.cnt[q] = 0;
+    }
+}
+
+// Cyclic two-sided Jacobi on the pair Gram: G <- J^T G J, Q <- Q J, 16
+// disjoint rotations per round (circle method over 32 indices).  The
+// eigenvector columns leave sorted by decreasing diagonal.
+__device__ void eig_pair(const BJArgs& a, int q, double* smem) {
+    double* G = smem;              // PW x GS
+    double* Q = smem + PW * GS;    // PW x GS
+    __shared__ double rc[PW / 2], rs[PW / 2];
+    __shared__ int rp[PW / 2], ro[PW / 2];
+    __shared__ int any, rot_total;
+    __shared__ double dsum[PW];
+    __shared__ int perm[PW];
+    const double* part = a.gws + int64_t(q) * a.nch * (PW * PW);
+    for (int e = threadIdx.x; e < PW * PW; e += NTH) {
+        double s = 0.0;
+        for (int c = 0; c < a.nch; ++c) s += __ldcg(part + int64_t(c) * (PW * PW) + e);
+        const int i = e % PW, j = e / PW;
+        G[i * GS + j] = s;
+        Q[i * GS + j] = i == j ? 1.0 : 0.0;
+    }
+    if (threadIdx.x == 0) {
+        any = 0;
+        rot_total = 0;
+    }
+    __syncthreads();
+    // the pair decision: any scaled off-diagonal above flag_tol
+    for (int e = threadIdx.x; e < PW * PW; e += NTH) {
+        const int i = e % PW, j = e / PW;
+        if (i < j) {
+            const double gij = G[i * GS + j];
+            if (gij != 0.0 && fabs(gij) > a.flag_tol * sqrt(G[i * GS + i] * G[j * GS + j])) any = 1;
+        }
+    }
+    __syncthreads();
+    if (!any) {
+        if (threadIdx.x == 0) a.flag[q] = 0;
+        return;
+    }
+    for (int sw = 0; sw < kInner; ++sw) {
+        __shared__ int rotated;
+        if (threadIdx.x == 0) rotated = 0;
+        __syncthreads();
+        for (int r = 0; r < PW - 1; ++r) {
+            if (threadIdx.x < PW / 2) {
+                const int k = threadIdx.x;
+                int p = circ(k, r, PW), o = circ(PW - 1 - k, r, PW);
+                if (p > o) {
+                    const int tmp = p;
+                    p = o;
+                    o = tmp;
+                }
+                const double app = G[p * GS + p], aoo = G[o * GS + o], apo = G[p * GS + o];
+                double cs = 1.0, sn = 0.0;
+                if (apo != 0.0 && fabs(apo) > a.tol * sqrt(app * aoo)) {
+                    rot2(app, aoo, apo, cs, sn);
+                    atomicAdd(&rotated, 1);
+                }
+                rc[k] = cs;
+                rs[k] = sn;
+                rp[k] = p;
+                ro[k] = o;
+            }
+            __syncthreads();
+            // rows: G <- J^T G  (row p' = c row_p - s row_o, row o' = s row_p + c row_o)
+            for (int e = threadIdx.x; e < (PW / 2) * PW; e += NTH) {
+                const int k = e / PW, x = e % PW;
+                if (rs[k] != 0.0) {
+                    const int p = rp[k], o = ro[k];
+                    const double gp = G[p * GS + x], go = G[o * GS + x];
+                    G[p * GS + x] = rc[k] * gp - rs[k] * go;
+                    G[o * GS + x] = rs[k] * gp + rc[k] * go;
+                }
+            }
+            __syncthreads();
+            // columns: G <- G J, Q <- Q J
+            for (int e = threadIdx.x; e < (PW / 2) * PW; e += NTH) {
+                const int k = e / PW, x = e % PW;
+                if (rs[k] != 0.0) {
+                    const int p = rp[k], o = ro[k];
+                    const double gp = G[x * GS + p], go = G[x * GS + o];
+                    G[x * GS + p] = rc[k] * gp - rs[k] * go;
+                    G[x * GS + o] = rs[k] * gp + rc[k] * go;
+                    const double qp = Q[x * GS + p], qo = Q[x * GS + o];
+                    Q[x * GS + p] = rc[k] * qp - rs[k] * qo;
+                    Q[x * GS + o] = rs[k] * qp + rc[k] * qo;
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x < PW / 2 && rs[threadIdx.x] != 0.0) {  // annihilated exactly
+                const int p = rp[threadIdx.x], o = ro[threadIdx.x];
+                G[p * GS + o] = 0.0;
+                G[o * GS + p] = 0.0;
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) rot_total += rotated;
+        __syncthreads();
+        if (rotated == 0) break;
+    }
+    // sort by decreasing diagonal (stable rank order)
+    if (threadIdx.x < PW) dsum[threadIdx.x] = G[threadIdx.x * GS + threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x < PW) {
+        const int j = threadIdx.x;
+        const double dj = dsum[j];
+        int rank = 0;
+        for (int k = 0; k < PW; ++k) {
+            const double dk = dsum[k];
+            rank += (dk > dj) || (dk == dj && k < j);
+        }
+        perm[rank] = j;
+    }
+    __syncthreads();
+    double* qo = a.qws + int64_t(q) * (PW * PW);
+    for (int e = threadIdx.x; e < PW * PW; e += NTH) {
+        const int i = e % PW, j = e / PW;
+        __stcg(qo + i + j * PW, Q[i * GS + perm[j]]);
+    }
+    if (threadIdx.x == 0) {
+        a.flag[q] = 1;
+        atomicAdd(a.stats, 1);
+        atomicAdd(a.stats + 1, rot_total);
+    }
+    __threadfence();
+}
+
+// ---- phase 3: X_p(rows of the chunk) <- X_p Q_p
+__device__ void update_unit(const BJArgs& a, int q, int ch, double* smem, const int* col) {
+    double* xs = smem;            // PW x XS
+    double* qs = smem + PW * XS;  // PW x QS: qs[j * QS + k] = Q(k, j)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const double* qg = a.qws + int64_t(q) * (PW * PW);
+    __syncthreads();
+    for (int e = threadIdx.x; e < PW * PW; e += NTH) {
+        const int k = e % PW, j = e / PW;
+        qs[j * QS + k] = __ldcg(qg + e);
+    }
+    const int64_t r0 = int64_t(ch) * a.rch, r1 = min(a.m, r0 + a.rch);
+    const int wr = warp * 16;  // the warp's 16 rows of the 64-row sub-tile
+    for (int64_t r = r0; r < r1; r += SUB) {
+        __syncthreads();
+        load_sub(xs, a.U, a.ldu, col, r, r1);
+        __syncthreads();
+        double acc[4][4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < PW; kk += 4) {
+            // A = X (i = row, k = column): xs[k * XS + i]
+            const double a0 = xs[(kk + t) * XS + wr + g];
+            const double a1 = xs[(kk + t) * XS + wr + g + 8];
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) dmma(acc[ni], a0, a1, qs[(ni * 8 + g) * QS + kk + t]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int i = wr + g + ((v & 2) ? 8 : 0);
+                const int j = ni * 8 + 2 * t + (v & 1);
+                xs[j * XS + i] = acc[ni][v];
+            }
+        __syncthreads();
+#pragma unroll 4
+        for (int e = threadIdx.x; e < SUB * PW; e += NTH) {
+            const int i = e & (SUB - 1), j = e / SUB;
+            const int64_t gi = r + i;
+            const int cj = col[j];
+            if (cj >= 0 && gi < r1) __stcg(a.U + gi + int64_t(cj) * a.ldu, xs[j * XS + i]);
+        }
+    }
+}
+
+constexpr int SMEM_DOUBLES = PW * XS + PW * QS > 2 * PW * GS ? PW * XS + PW * QS : 2 * PW * GS;
+
+__global__ void __launch_bounds__(NTH, 4) bjacobi_sweep_k(BJArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ __align__(16) double smem[SMEM_DOUBLES];
+    __shared__ int col[PW];
+    const int units = a.per * a.nch;
+    for (int r = 0; r < a.rounds; ++r) {
+        const int2* rp = a.pairs + int64_t(r) * a.per;
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+            const int q = u / a.nch, ch = u % a.nch;
+            const int2 bp = rp[q];
+            __syncthreads();
+            if (threadIdx.x < PW) col[threadIdx.x] = pair_col(bp, threadIdx.x, a.n);
+            __syncthreads();
+            gram_unit(a, bp, q, ch, smem, col);
+        }
+        grid.sync();
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+            const int q = u / a.nch, ch = u % a.nch;
+            if (!__ldcg(a.flag + q)) continue;
+            const int2 bp = rp[q];
+            __syncthreads();
+            if (threadIdx.x < PW) col[threadIdx.x] = pair_col(bp, threadIdx.x, a.n);
+            __syncthreads();
+            update_unit(a, q, ch, smem, col);
+        }
+        grid.sync();
+    }
+}
+
+std::vector<int2> block_tournament(int nbp) {
+    std::vector<int> p(static_cast<size_t>(nbp));
+    std::iota(p.begin(), p.end(), 0);
+    std::vector<int2> out;
+    out.reserve(size_t(nbp / 2) * size_t(nbp - 1));
+    for (int r = 0; r < nbp - 1; ++r) {
+        for (int i = 0; i < nbp / 2; ++i) {
+            const int x = p[size_t(i)], y = p[size_t(nbp - 1 - i)];
+            out.push_back(make_int2(std::min(x, y), std::max(x, y)));
+        }
+        const int last = p[size_t(nbp - 1)];
+        for (int i = nbp - 1; i > 1; --i) p[size_t(i)] = p[size_t(i - 1)];
+        p[1] = last;
+    }
+    return out;
+}
+
+bool bj_stats() {
+    static const bool on = [] {
+        const char* e = std::getenv("HYDOT_JACOBI_STATS");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+}  // namespace
+
+// Minimum core order for the block driver (below it the register point
+// drivers of svd.cu are latency-optimal).  HYDOT_BJACOBI_MIN overrides.
+int64_t bjacobi_min_n() {
+    static const int64_t v = [] {
+        const char* e = std::getenv("HYDOT_BJACOBI_MIN");
+        return e ? int64_t(std::atoll(e)) : int64_t(640);
+    }();
+    return v;
+}
+
+// Orthogonalise the columns of U (m x n, ld m, m >= n) in place to the
+// one-sided Jacobi criterion (pairs within flag_tol = 2 tol).  Returns the
+// number of sweeps.
+int bjacobi_converge(Ctx& c, int64_t m, int64_t n, double* U, double tol) {
+    const int nb = int((n + BW - 1) / BW);
+    const int nbp = nb + (nb & 1);
+    const int per = nbp / 2, rounds = nbp - 1;
+    std::vector<int2> pairs = block_tournament(nbp);
+    DBuf dpairs(c, pairs.size() * sizeof(int2));
+    HYDOT_CUDA(cudaMemcpyAsync(dpairs.as<void>(), pairs.data(), pairs.size() * sizeof(int2),
+                               cudaMemcpyHostToDevice, c.stream));
+    int per_sm = 0;
+    HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bjacobi_sweep_k, NTH, 0));
+    const int max_grid = std::max(1, per_sm) * c.num_sms;
+    // row chunks: enough (pair, chunk) units to fill the grid twice
+    const int64_t subs = (m + SUB - 1) / SUB;
+    int64_t nch = std::clamp<int64_t>((2 * int64_t(max_grid) + per - 1) / per, 1, subs);
+    const int64_t rch = ((m + nch - 1) / nch + SUB - 1) / SUB * SUB;
+    nch = (m + rch - 1) / rch;
+    const int units = int(per * nch);
+    const int grid = std::min(units, max_grid);
+    DBuf gws = dalloc(c, size_t(per) * size_t(nch) * PW * PW);
+    DBuf qws = dalloc(c, size_t(per) * PW * PW);
+    DBuf ints(c, sizeof(int) * size_t(2 * per + 2));
+    HYDOT_CUDA(cudaMemsetAsync(ints.as<void>(), 0, sizeof(int) * size_t(2 * per + 2), c.stream));
+    BJArgs a;
+    a.m = m;
+    a.n = int(n);
+    a.nbp = nbp;
+    a.per = per;
+    a.rounds = rounds;
+    a.pairs = dpairs.as<int2>();
+    a.U = U;
+    a.ldu = m;
+    a.tol = tol;
+    a.flag_tol = 2.0 * tol;  // tol is itself the rounding level of a column dot product
+    a.nch = int(nch);
+    a.rch = int(rch);
+    a.gws = gws.d();
+    a.qws = qws.d();
+    a.flag = ints.as<int>();
+    a.cnt = ints.as<int>() + per;
+    a.stats = ints.as<int>() + 2 * per;
+    int sweeps = 0;
+    for (; sweeps < kMaxBSweeps; ++sweeps) {
+        HYDOT_CUDA(cudaMemsetAsync(a.stats, 0, 2 * sizeof(int), c.stream));
+        void* args[] = {&a};
+        c.coop_launch((void*)bjacobi_sweep_k, dim3(grid), dim3(NTH), args, 0);
+        c.count();
+        int st[2] = {0, 0};
+        HYDOT_CUDA(cudaMemcpyAsync(st, a.stats, sizeof st, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        if (bj_stats())
+            fprintf(stderr, "[bjacobi] m=%lld n=%lld sweep=%d pairs_rotated=%d inner_rotations=%d (of %d pairs)\n",
+                    (long long)m, (long long)n, sweeps, st[0], st[1], per * rounds);
+        if (st[0] == 0) break;
+    }
+    return sweeps + 1;
+}
+
+}  // namespace hydot

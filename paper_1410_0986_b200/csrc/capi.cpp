@@ -634,7 +634,7 @@ hydot_status hydot_thin_svd(hydot_ctx ctx, int64_t m, int64_t n, const double* a
         if (m < 0 || n < 0 || lda < m) throw std::invalid_argument("thin_svd: bad dimensions");
         // full orthonormal U, V like Eigen::BDCSVD; HYDOT_THIN_SVD_PATH=1
         // runs the path's own (lazy-V) variant instead, for profiling
-        static const bool path_mode = [] {
+        const bool path_mode = [] {
             const char* e = std::getenv("HYDOT_THIN_SVD_PATH");
             return e && e[0] == '1';
         }();
@@ -857,13 +857,14 @@ hydot_status hydot_block_file_info(const char* path, int64_t* rows, int64_t* col
     });
 }
 
-hydot_status hydot_block_load(hydot_ctx ctx, const char* path, double* block_dev, int64_t ld, int64_t* rows,
-                              int64_t* cols) {
+hydot_status hydot_block_load(hydot_ctx ctx, const char* path, double* block_dev, int64_t ld, int64_t rows_cap,
+                              int64_t* rows, int64_t* cols) {
     return guard(ctx ? ctx->c.get() : nullptr, [&] {
         Ctx& c = ctx_of(ctx);
         if (!path || !block_dev) throw std::invalid_argument("load_block: bad arguments");
         int64_t r = 0, k = 0;
-        load_block_file(c, path, block_dev, ld, r, k);
+        if (rows_cap < 0) throw std::invalid_argument("load_block: bad arguments");
+        load_block_file(c, path, block_dev, ld, rows_cap, r, k);
         if (rows) *rows = r;
         if (cols) *cols = k;
     });

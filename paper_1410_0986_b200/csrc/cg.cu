@@ -986,8 +986,8 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
                 ztsmem = size_t(NSP * (ty + 2) + NSX * 2 * ty) * size_t(op.g.nx) * sizeof(double);
                 ztpsmem = zpa_deep() ? size_t((2 * 4 + 3) * (ty + 2)) * size_t(op.g.nx) * sizeof(double)
                                      : size_t((2 * NSR + 4) * (ty + 2)) * size_t(op.g.nx) * sizeof(double);
-                static bool attr = false;
-                if (!attr) {
+                static AttrGate attr;
+                attr_once(attr, c.device, [&] {
                     HYDOT_CUDA(cudaFuncSetAttribute(cgzt_xr, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     200 * 1024));
                     HYDOT_CUDA(cudaFuncSetAttribute(cgzt_pa<NSR, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1001,8 +1001,7 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
                         HYDOT_CUDA(cudaFuncSetAttribute(cgzt_pa<NSR, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
                         HYDOT_CUDA(cudaFuncSetAttribute(cgzt_xr, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
                     }
-                    attr = true;
-                }
+                });
             }
         }
     }

@@ -156,7 +156,8 @@ void block_file_info(const std::string& path, int64_t& rows, int64_t& cols) {
     cols = int64_t(hdr[1]);
 }
 
-void load_block_file(Ctx& c, const std::string& path, double* block, int64_t ld, int64_t& rows, int64_t& cols) {
+void load_block_file(Ctx& c, const std::string& path, double* block, int64_t ld, int64_t rows_cap, int64_t& rows,
+                     int64_t& cols) {
     File in(path, "rb");
     if (!in.f) throw std::runtime_error("cannot read block: " + path);
     double hdr[2];
@@ -165,6 +166,7 @@ void load_block_file(Ctx& c, const std::string& path, double* block, int64_t ld,
     rows = int64_t(hdr[0]);
     cols = int64_t(hdr[1]);
     if (ld < cols) throw std::invalid_argument("load_block: leading dimension smaller than the block");
+    if (rows > rows_cap) throw std::invalid_argument("load_block: block has more rows than the buffer holds");
     if (rows <= 0 || cols <= 0) return;
     const int64_t chunk = std::max<int64_t>(1, int64_t(kChunkBytes / 8) / cols);
     std::unique_ptr<double[]> h(new double[size_t(std::min(rows, chunk) * cols)]);

@@ -296,8 +296,8 @@ void run_tiles(Ctx& c, bool ta, bool tb, int64_t m, int64_t n, int64_t k, double
     dim3 grid = dim3(unsigned(tm), unsigned(tn), unsigned(splits));
     DBuf ws;
     if (splits > 1) ws = dalloc(c, size_t(splits * m * n));
-    static bool attr = false;
-    if (!attr) {
+    static AttrGate attr;
+    attr_once(attr, c.device, [&] {
         HYDOT_CUDA(cudaFuncSetAttribute(dgemm_kernel<false, false, BM, BN, WM, WN>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(T::SMEM)));
         HYDOT_CUDA(cudaFuncSetAttribute(dgemm_kernel<false, true, BM, BN, WM, WN>,
@@ -306,8 +306,7 @@ void run_tiles(Ctx& c, bool ta, bool tb, int64_t m, int64_t n, int64_t k, double
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(T::SMEM)));
         HYDOT_CUDA(cudaFuncSetAttribute(dgemm_kernel<true, true, BM, BN, WM, WN>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(T::SMEM)));
-        attr = true;
-    }
+    });
     const bool vecA = (lda % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0);
     const bool vecB = (ldb % 2 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0);
     auto launch = [&](auto kern) {

@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -25,6 +26,23 @@ struct CudaError : std::runtime_error {
     } while (0)
 
 struct RngTables;
+
+// Function attributes (cudaFuncSetAttribute) are per device: a call site
+// sets them once for every device a context of this process uses, under a
+// lock (contexts on several GPUs may run on different host threads).
+struct AttrGate {
+    std::mutex mu;
+    uint64_t done = 0;
+};
+template <class F>
+void attr_once(AttrGate& g, int device, F&& set) {
+    std::lock_guard<std::mutex> lk(g.mu);
+    const uint64_t bit = 1ull << (device & 63);
+    if (!(g.done & bit)) {
+        set();
+        g.done |= bit;
+    }
+}
 
 struct Ctx {
     int device = 0;
@@ -130,6 +148,7 @@ class DBuf {
             cudaError_t e = cudaMallocAsync(&p_, bytes, s_);
             if (e != cudaSuccess) {
                 p_ = nullptr;
+                cudaGetLastError();  // do not leave the failed allocation as the sticky last error
                 throw std::bad_alloc();
             }
         }
@@ -238,6 +257,11 @@ struct StrictSVD {
 // svd.cu : one-sided Jacobi thin SVD of X (m x n, m >= n); s descending.
 void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, double* U,
                 int64_t ldu, std::vector<double>& s, double* V, int64_t ldv);
+
+// bjacobi.cu: block one-sided Jacobi (DMMA Gram + pair eigen-solve + DMMA
+// update) to convergence on U (m x n, ld m); returns the sweep count
+int bjacobi_converge(Ctx& c, int64_t m, int64_t n, double* U, double tol);
+int64_t bjacobi_min_n();
 
 // cg.cu
 struct CGStats {

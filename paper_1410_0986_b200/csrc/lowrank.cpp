@@ -418,19 +418,26 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
         const bool small = double(n) * double(m) * 16.0 <= 16.0 * double(1ull << 30);
         if (!(rs1 >= nmax && m <= n) && rs2 >= nmax && m <= n && n >= 2 * m && m > 48 && small &&
             presort_tall() && async_v_on() && speculate_on()) {
-            spec.reset(new TallSpec());
-            spec->c = &c;
-            spec->src = At;
-            spec->ld = lda;
-            spec->m = n;
-            spec->n = m;
-            presort_perm(c, n, m, At, lda, spec->perm);
-            spec->dperm = DBuf(c, size_t(m) * sizeof(int));
-            HYDOT_CUDA(cudaMemcpyAsync(spec->dperm.as<void>(), spec->perm.data(), size_t(m) * sizeof(int),
-                                       cudaMemcpyHostToDevice, c.stream));
-            spec->qf.a = dalloc(c, size_t(n * m));  // on c.stream: freed in its order
-            spec->qf.tau = dalloc(c, size_t(m));
-            spec->qf.T = dalloc(c, size_t(kQRBlock) * size_t(m));
+            // speculation is optional: if its buffers do not fit, run without it
+            try {
+                spec.reset(new TallSpec());
+                spec->c = &c;
+                spec->src = At;
+                spec->ld = lda;
+                spec->m = n;
+                spec->n = m;
+                presort_perm(c, n, m, At, lda, spec->perm);
+                spec->dperm = DBuf(c, size_t(m) * sizeof(int));
+                HYDOT_CUDA(cudaMemcpyAsync(spec->dperm.as<void>(), spec->perm.data(), size_t(m) * sizeof(int),
+                                           cudaMemcpyHostToDevice, c.stream));
+                spec->qf.a = dalloc(c, size_t(n * m));  // on c.stream: freed in its order
+                spec->qf.tau = dalloc(c, size_t(m));
+                spec->qf.T = dalloc(c, size_t(kQRBlock) * size_t(m));
+            } catch (const std::bad_alloc&) {
+                spec.reset();  // no event yet: nothing was issued on the side stream
+            }
+        }
+        if (spec) {
             cudaEvent_t start;
             HYDOT_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
             HYDOT_CUDA(cudaEventRecord(start, c.stream));
@@ -444,8 +451,15 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
                 geqrf(c, n, m, As.d(), n, spec->qf);
                 HYDOT_CUDA(cudaEventCreateWithFlags(&spec->ev, cudaEventDisableTiming));
                 HYDOT_CUDA(cudaEventRecord(spec->ev, side));
+            } catch (const std::bad_alloc&) {
+                // the side stream may still write spec's buffers (allocated in
+                // c.stream order): finish it before they are released
+                c.stream = main;
+                cudaStreamSynchronize(side);
+                spec.reset();
             } catch (...) {
                 c.stream = main;
+                cudaStreamSynchronize(side);
                 throw;
             }
             c.stream = main;
@@ -558,8 +572,7 @@ Factor agglomerate(Ctx& c, const Factor& f1, const Factor& f2, double eps, uint6
     out.cols = n;
     out.tol = eps;
     out.method = HYDOT_METHOD_AGGLOMERATE;
-    if (r1 + r2 == 0) {  // :333-337
-        out.flagged = f1.flagged || f2.flagged;
+    if (r1 + r2 == 0) {  // :333-337 (the reference returns flagged = false here)
         return out;
     }
     wait_v(c, f1);

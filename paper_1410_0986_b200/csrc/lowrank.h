@@ -113,6 +113,9 @@ Factor load_factor_file(Ctx& c, const std::string& path, std::vector<int>& perm)
 void save_block_file(Ctx& c, const std::string& path, const double* block, int64_t rows, int64_t cols,
                      int64_t ld);
 void block_file_info(const std::string& path, int64_t& rows, int64_t& cols);
-void load_block_file(Ctx& c, const std::string& path, double* block, int64_t ld, int64_t& rows, int64_t& cols);
+// rows_cap: rows the caller's buffer holds (row stride ld); a larger file is
+// rejected before any device write
+void load_block_file(Ctx& c, const std::string& path, double* block, int64_t ld, int64_t rows_cap, int64_t& rows,
+                     int64_t& cols);
 
 }  // namespace hydot

@@ -253,12 +253,11 @@ void skinny_tn_t(Ctx& c, int64_t K, int64_t R, int q, const double* A, int64_t l
     int64_t jgroup = std::max<int64_t>(8, (R + groups - 1) / groups);
     groups = (R + jgroup - 1) / jgroup;
     DBuf part = dalloc(c, size_t(nchunks * R * q));
-    static bool attr = false;
-    if (!attr) {
+    static AttrGate attr;
+    attr_once(attr, c.device, [&] {
         HYDOT_CUDA(cudaFuncSetAttribute(skinny_tn_k<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         int(T * Q * 8)));
-        attr = true;
-    }
+    });
     skinny_tn_k<Q><<<dim3(unsigned(nchunks), unsigned(groups)), SK_T, size_t(T * Q * 8), c.stream>>>(
         K, R, T, A, lda, X, ldx, part.d(), jgroup, q);
     c.check_launch();
@@ -277,12 +276,11 @@ void skinny_nn_t(Ctx& c, int64_t M, int64_t R, int q, const double* A, int64_t l
     RC = std::min<int64_t>(RC, 16384 / Q);
     nch = (R + RC - 1) / RC;
     DBuf part = dalloc(c, size_t(nch * q * M));
-    static bool attr = false;
-    if (!attr) {
+    static AttrGate attr;
+    attr_once(attr, c.device, [&] {
         HYDOT_CUDA(cudaFuncSetAttribute(skinny_nn_k<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         16384 * 8));
-        attr = true;
-    }
+    });
     skinny_nn_k<Q><<<dim3(unsigned(rb), unsigned(nch)), SK_T, size_t(RC * Q * 8), c.stream>>>(
         M, R, RC, A, lda, Z, ldz, part.d(), q);
     c.check_launch();

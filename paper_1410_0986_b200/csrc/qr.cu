@@ -358,15 +358,14 @@ __global__ void __launch_bounds__(LT) larft_k(int jb, const double* __restrict__
 
 void panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, const PanelBufs& pbuf) {
     StageTimer _t(c, "qr_panel", mr, jb, -1, 2.0 * double(mr) * jb * jb, 16.0 * double(mr) * jb);
-    static bool attr = false;
+    static AttrGate attr;
     const size_t smem_cap = 200 * 1024;
     if (mr <= kCtaRows) {  // short panels: one CTA, the whole panel on-chip
-        static bool cattr = false;
-        if (!cattr) {
+        static AttrGate cattr;
+        attr_once(cattr, c.device, [&] {
             HYDOT_CUDA(cudaFuncSetAttribute(qr_panel_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             int(smem_cap)));
-            cattr = true;
-        }
+        });
         qr_panel_cta<<<1, CT, size_t(mr) * jb * sizeof(double), c.stream>>>(int(mr), jb, P, ld, tau);
         c.check_launch();
         return;
@@ -380,11 +379,10 @@ void panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, const
     if (G > GMAX) throw std::runtime_error("qr panel: grid too large");
     const size_t smem = size_t(rows_per) * PB * sizeof(double);
     const bool use_smem = smem <= smem_cap;
-    if (!attr) {
+    attr_once(attr, c.device, [&] {
         HYDOT_CUDA(cudaFuncSetAttribute(qr_panel_coop<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         int(smem_cap)));
-        attr = true;
-    }
+    });
     int per_sm = 0;
     if (use_smem)
         HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qr_panel_coop<true>, PT, smem));
@@ -518,12 +516,11 @@ bool fused_t32() {
 }
 
 void larft(Ctx& c, int jb, const double* G, int64_t ldg, const double* tau, double* T) {
-    static bool attr = false;
+    static AttrGate attr;
     const int smem = (NB * (NB + 1) + (NB / 2) * (NB / 2 + 1)) * sizeof(double);
-    if (!attr) {
+    attr_once(attr, c.device, [&] {
         HYDOT_CUDA(cudaFuncSetAttribute(larft_k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-    }
+    });
     larft_k<<<1, LT, smem, c.stream>>>(jb, G, ldg, tau, T);
     c.check_launch();
 }

@@ -451,14 +451,13 @@ const uint64_t* device_jumps(Ctx& c, int64_t upto) {
 
 RngStream::RngStream(Ctx& c, uint64_t seed) : c_(c), seed_(seed) {
     prefix_.alloc(c, size_t(mt::PREFIX) * 8);
-    static bool attr = false;
-    if (!attr) {
+    static AttrGate attr;
+    attr_once(attr, c.device, [&] {
         HYDOT_CUDA(cudaFuncSetAttribute(rng_prefix_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         mt::PREFIX * 8));
         HYDOT_CUDA(cudaFuncSetAttribute(rng_jump_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         mt::PREFIX * 8));
-        attr = true;
-    }
+    });
     rng_prefix_k<<<1, 160, size_t(mt::PREFIX) * 8, c.stream>>>(seed, prefix_.as<uint64_t>());
     c.check_launch();
 }

@@ -651,28 +651,36 @@ std::vector<int2> tournament(int n, int& np) {
     return out;
 }
 
-// per-process cache of tournament tables on the device (keyed by n)
+// per-process cache of tournament tables in device memory, keyed by
+// (device, n); contexts on several devices may use it from several threads
 struct PairCache {
-    int n = -1, np = 0;
+    int device = -1, n = -1, np = 0;
     int2* dev = nullptr;
 };
 
-const int2* device_pairs(int n, int& np) {
+const int2* device_pairs(Ctx& c, int n, int& np) {
+    static std::mutex mu;
     static std::vector<PairCache> cache;
+    std::lock_guard<std::mutex> lk(mu);
     for (auto& e : cache)
-        if (e.n == n) {
+        if (e.n == n && e.device == c.device) {
             np = e.np;
             return e.dev;
         }
     std::vector<int2> pairs = tournament(n, np);
     PairCache pc;
+    pc.device = c.device;
     pc.n = n;
     pc.np = np;
     HYDOT_CUDA(cudaMalloc(&pc.dev, std::max<size_t>(pairs.size(), 1) * sizeof(int2)));
     if (!pairs.empty())
         HYDOT_CUDA(cudaMemcpy(pc.dev, pairs.data(), pairs.size() * sizeof(int2), cudaMemcpyHostToDevice));
     if (cache.size() > 256) {
+        int cur = 0;  // cudaFree synchronises the device: in-flight users finish first
+        cudaGetDevice(&cur);
+        cudaSetDevice(cache.front().device);
         cudaFree(cache.front().dev);
+        cudaSetDevice(cur);
         cache.erase(cache.begin());
     }
     cache.push_back(pc);
@@ -741,7 +749,7 @@ void launch_rblk_t(Ctx& c, int64_t m, int64_t n, double* U, int64_t ldu, double 
                    int* sweeps_out, int stop_thr) {
     int nb = int((n + B - 1) / B);
     int npb = 0;
-    const int2* bp = device_pairs(nb, npb);
+    const int2* bp = device_pairs(c, nb, npb);
     int per_sm = 0;
     HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_rblk_k<R, T, B>, T, 0));
     int grid = std::max(1, std::min(npb / 2, per_sm * c.num_sms));
@@ -897,7 +905,7 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
     if (stats_on()) c.sync();
     const auto t_start = std::chrono::steady_clock::now();
     int np = 0;
-    const int2* dpairs = device_pairs(int(n), np);
+    const int2* dpairs = device_pairs(c, int(n), np);
     DBuf U = dalloc(c, size_t(m * n));
     DBuf V = dalloc(c, size_t(n * n));
     copy2d(c, m, n, X, ldx, U.d(), m);
@@ -919,15 +927,20 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
     // (a U-only single-CTA variant for 110 < n <= 160 measured 2x slower
     // than the multi-SM block driver: one SM's FP64 rate bounds each round)
     if (n >= 2 && smem <= 200 * 1024) {
-        static bool attr = false;
-        if (!attr) {
+        static AttrGate attr;
+        attr_once(attr, c.device, [&] {
             HYDOT_CUDA(cudaFuncSetAttribute(jacobi_smem_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             210 * 1024));
-            attr = true;
-        }
+        });
         jacobi_smem_k<<<1, 1024, smem, c.stream>>>(int(m), int(n), np, dpairs, U.d(), m, V.d(), n,
                                                     tol, atol, sw.as<int>() + kMaxSweeps);
         c.check_launch();
+    } else if (n >= bjacobi_min_n() && !strict_svd_flag() && lazy_v_enabled() && atol == 0.0) {
+        lazy_v = true;
+        const int sweeps = bjacobi_converge(c, m, n, U.d(), tol);
+        HYDOT_CUDA(cudaMemcpyAsync(sw.as<int>() + kMaxSweeps, &sweeps, sizeof(int), cudaMemcpyHostToDevice,
+                                   c.stream));
+        c.sync();
     } else if (int rbR = 0, rbT = 0, rbB = 0; n >= 2 && !strict_svd_flag() && lazy_v_enabled() && atol == 0.0 &&
                                                rblk_shape(m, n, rbR, rbT, rbB)) {
         lazy_v = true;

@@ -77,3 +77,25 @@ def test_block_save_load(ctx, tmp_path):
     bad.write_bytes(struct.pack("<dd", -1.0, 2.0))
     with pytest.raises(Exception, match="corrupt block file"):
         born.load_block(ctx, str(bad))
+
+
+def test_block_load_rejects_a_file_larger_than_the_buffer(ctx, tmp_path):
+    """hydot_block_load takes the buffer's row capacity: a header larger than
+    rows_cap x ld is refused before any device write."""
+    import ctypes as C
+    import os
+    from paper_1410_0986_b200 import born
+    from paper_1410_0986_b200._lib import check, lib
+    from paper_1410_0986_b200.core import dptr
+    B = np.arange(12.0 * 7).reshape(12, 7)
+    path = str(tmp_path / "big.bin")
+    born.save_block(ctx, path, torch.as_tensor(B).cuda())
+    guard = torch.full((5 * 7 + 64,), -1.0, dtype=torch.float64, device="cuda")
+    r, c = C.c_int64(), C.c_int64()
+    with pytest.raises(ValueError, match="more rows than the buffer"):
+        check(lib().hydot_block_load(ctx.h, os.fsencode(path), dptr(guard), 7, 5, C.byref(r), C.byref(c)),
+              ctx.h)
+    assert bool(torch.all(guard == -1.0))  # nothing written
+    with pytest.raises(ValueError, match="leading dimension"):
+        check(lib().hydot_block_load(ctx.h, os.fsencode(path), dptr(guard), 6, 12, C.byref(r), C.byref(c)),
+              ctx.h)
