@@ -39,7 +39,7 @@ constexpr uint64_t UM = 0xFFFFFFFF80000000ULL, LM = 0x7FFFFFFFULL;
 constexpr uint64_t F = 6364136223846793005ULL;
 constexpr int L = 19937;              // degree of phi
 constexpr int PW = (L + 63) / 64;     // words per polynomial (312)
-constexpr int64_t S = 312LL * 256;    // outputs per chunk (even)
+constexpr int64_t S = 312LL * 1024;   // outputs per chunk (even; one jump per chunk)
 constexpr int PREFIX = 312 * 65;      // z_0 .. z_{20279} >= L + 311
 
 __host__ __device__ inline uint64_t mix(uint64_t a, uint64_t b) {

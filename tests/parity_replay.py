@@ -37,7 +37,7 @@ TOL_SIGMA = 1e-8
 TOL_J = 1e-8
 
 
-def factor_diff(Ug, Vg, Uo, Vo, chunk=2048):
+def factor_diff(Ug, Vg, Uo, Vo, chunk=1024):
     """||Ug Vg^T - Uo Vo^T||_F and ||Uo Vo^T||_F, row chunks on the device."""
     dev = Ug.device
     Uo = torch.as_tensor(Uo, device=dev)

@@ -56,12 +56,13 @@ def test_born_block_bitwise(ctx, oracle):
 def test_mt19937_64_engine_bits(ctx, oracle):
     import paper_1410_0986_b200 as h
     for seed in (0, 5489, 20240811 + 0x9e3779b97f4a7c15, 2**64 - 1):
-        want = oracle.mt19937_64(seed, 200000)
-        got = h.mt19937_64(ctx, seed, 0, 200000).cpu().numpy().view(np.uint64)
+        want = oracle.mt19937_64(seed, 1000000)
+        got = h.mt19937_64(ctx, seed, 0, 1000000).cpu().numpy().view(np.uint64)
         assert np.array_equal(got, want)
-        # a window straddling several jump-ahead chunks
-        got2 = h.mt19937_64(ctx, seed, 150000, 40000).cpu().numpy().view(np.uint64)
-        assert np.array_equal(got2, want[150000:190000])
+        # windows straddling jump-ahead chunk boundaries (S = 312 * 1024)
+        for off, cnt in ((300000, 40000), (600000, 400000)):
+            got2 = h.mt19937_64(ctx, seed, off, cnt).cpu().numpy().view(np.uint64)
+            assert np.array_equal(got2, want[off:off + cnt])
 
 
 def test_gaussian_stream_matches_libstdcxx(ctx, oracle):

@@ -67,6 +67,8 @@ def _driver_matches_replay(d, rep, froot):
     """The library's recursive_lowrank (speculation, side-stream V, lazy root
     V) gives the replay's ranks and root factor."""
     from paper_1410_0986_b200 import lowrank as lr
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()  # the replay's block and checker temporaries
     rec = lr.recursive_lowrank(d["ctx"], d["tree"], d["eps"],
                                lr.BornFieldsProvider(d["inc"], d["adj"], d["w"], 1.0),
                                lr.RecursiveOptions(seed=d["cfg"].seed))
@@ -123,6 +125,7 @@ def test_config2_subtree_root_and_recompress_match_oracle(oracle):
                  check=lambda v: v in check)
     froot = rep.run()
     assert rep.checked == 8 + 4 + 3 + 1
+    _write_log("cfg2-replay", rep, {"seconds": time.perf_counter() - t0})
     _driver_matches_replay(d, rep, froot)
     del d["F"], d["inc"], d["adj"]
     torch.cuda.empty_cache()
