@@ -391,6 +391,11 @@ typedef struct hydot_recon_config {
     int max_outer, max_inner, max_retries;
     double gamma, nu0, stagnation_tol;
     const double* fixed_c_h; /* n_species, or NULL to solve for c */
+    /* BASELINE config 4 benchmark knob (0 = the reference loop): after each
+     * Gauss-Newton step's Jacobian, normal_blocks J~x products on the step's
+     * chromophore-expanded shape-Jacobian columns and as many J~^T y on
+     * y = W^2 J~x (E_c axis from ext_h, the operator's row permutation). */
+    int normal_blocks;
 } hydot_recon_config;
 
 /* TraceRow (pals.hpp:77-84). */
@@ -413,6 +418,7 @@ typedef struct hydot_recon_result {
     double resnorm;
     int converged, flagged;
     int64_t hmv_calls, hmv_columns;
+    int64_t normal_columns; /* J~x columns issued by normal_blocks (as many J~^T y) */
 } hydot_recon_result;
 
 /* reconstruct (pals.cpp:193-295): alternating concentration / shape

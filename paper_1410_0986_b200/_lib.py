@@ -70,7 +70,7 @@ class Hop(C.Structure):
 class ReconConfig(C.Structure):
     _fields_ = [("max_outer", C.c_int), ("max_inner", C.c_int), ("max_retries", C.c_int),
                 ("gamma", C.c_double), ("nu0", C.c_double), ("stagnation_tol", C.c_double),
-                ("fixed_c_h", _dp)]
+                ("fixed_c_h", _dp), ("normal_blocks", C.c_int)]
 
 
 class TraceRowC(C.Structure):
@@ -82,7 +82,7 @@ class ReconResultC(C.Structure):
     _fields_ = [("p", PalsParams), ("c_h", _dp), ("trace_h", C.POINTER(TraceRowC)),
                 ("trace_cap", C.c_int), ("trace_len", C.c_int), ("resnorm", C.c_double),
                 ("converged", C.c_int), ("flagged", C.c_int), ("hmv_calls", C.c_int64),
-                ("hmv_columns", C.c_int64)]
+                ("hmv_columns", C.c_int64), ("normal_columns", C.c_int64)]
 
 
 # name -> (restype, argtypes); exactly the declarations of include/hydot_b200.h

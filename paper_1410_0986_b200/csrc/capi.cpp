@@ -587,42 +587,8 @@ hydot_status hydot_j_matmat(hydot_ctx ctx, hydot_factor f, int trans, int b, con
         if (!f || !row_perm_dev || !eps_c_dev || n_lambda < 1 || n_c < 1 || b < 0)
             throw std::invalid_argument("J matmat: bad arguments");
         const Factor& F = dense(c, f);
-        const int64_t M = F.rows, N = F.cols, R = F.rank;
-        const int64_t q = int64_t(b) * n_c;
-        if (b == 0) return;
-        if (!trans) {
-            if (ldx != N * n_c || ldy < M) throw std::invalid_argument("J matvec: dimension mismatch");
-            if (R == 0) {
-                fill(c, M, b, 0.0, Y_dev, ldy);
-                c.sync();
-                return;
-            }
-            DBuf Z = dalloc(c, size_t(R * q)), T = dalloc(c, size_t(M * q));
-            if (skinny_ok(int(q))) {
-                skinny_tn(c, N, R, int(q), F.V.d(), N, X_dev, N, Z.d(), R);
-                skinny_nn(c, M, R, int(q), F.U.d(), M, Z.d(), R, T.d(), M);
-            } else {
-                dgemm(c, true, false, R, q, N, 1.0, F.V.d(), N, X_dev, N, 0.0, Z.d(), R);
-                dgemm(c, false, false, M, q, R, 1.0, F.U.d(), M, Z.d(), R, 0.0, T.d(), M);
-            }
-            j_combine(c, M, b, n_c, n_lambda, T.d(), M, row_perm_dev, eps_c_dev, Y_dev, ldy);
-        } else {
-            if (ldx < M || ldy != N * n_c) throw std::invalid_argument("J rmatvec: dimension mismatch");
-            if (R == 0) {
-                fill(c, N * n_c, b, 0.0, Y_dev, ldy);
-                c.sync();
-                return;
-            }
-            DBuf G = dalloc(c, size_t(M * q)), W = dalloc(c, size_t(R * q));
-            j_gather_scale(c, M, b, n_c, n_lambda, X_dev, ldx, row_perm_dev, eps_c_dev, G.d(), M);
-            if (skinny_ok(int(q))) {
-                skinny_tn(c, M, R, int(q), F.U.d(), M, G.d(), M, W.d(), R);
-                skinny_nn(c, N, R, int(q), F.V.d(), N, W.d(), R, Y_dev, N);
-            } else {
-                dgemm(c, true, false, R, q, M, 1.0, F.U.d(), M, G.d(), M, 0.0, W.d(), R);
-                dgemm(c, false, false, N, q, R, 1.0, F.V.d(), N, W.d(), R, 0.0, Y_dev, N);
-            }
-        }
+        j_matmat(c, F.U.d(), F.V.d(), F.rows, F.cols, F.rank, trans != 0, b, row_perm_dev, eps_c_dev, n_lambda, n_c,
+                 X_dev, ldx, Y_dev, ldy);
         c.sync();
     });
 }
@@ -775,6 +741,8 @@ hydot_status hydot_pals_reconstruct(hydot_ctx ctx, const hydot_hop* op, const hy
         rc.nu0 = cfg->nu0;
         rc.stagnation_tol = cfg->stagnation_tol;
         if (cfg->fixed_c_h) rc.fixed_c.assign(cfg->fixed_c_h, cfg->fixed_c_h + n_species);
+        if (cfg->normal_blocks < 0) throw std::invalid_argument("reconstruct: normal_blocks < 0");
+        rc.normal_blocks = cfg->normal_blocks;
         hydot::pals::Recon r = hydot::pals::reconstruct(c, hop_of(c, op), geom_of(geom), ext_h, n_lambda, n_species,
                                                         y_dev, w_dev, p0, noise_norm, rc, mu_truth_dev);
         std::copy(r.p.alpha.begin(), r.p.alpha.end(), out->p.alpha);
@@ -794,6 +762,7 @@ hydot_status hydot_pals_reconstruct(hydot_ctx ctx, const hydot_hop* op, const hy
         out->flagged = r.flagged ? 1 : 0;
         out->hmv_calls = r.hmv_calls;
         out->hmv_columns = r.hmv_columns;
+        out->normal_columns = r.normal_columns;
     });
 }
 

@@ -284,6 +284,12 @@ void j_combine(Ctx& c, int64_t M, int b, int nc, int nl, const double* T, int64_
                const int* row_perm, const double* eps_c, double* Y, int64_t ldy);
 void j_gather_scale(Ctx& c, int64_t M, int b, int nc, int nl, const double* X, int64_t ldx,
                     const int* row_perm, const double* eps_c, double* G, int64_t ldg);
+void j_matmat(Ctx& c, const double* U, const double* V, int64_t M, int64_t N, int64_t R, bool trans, int b,
+              const int* row_perm, const double* eps_c, int nl, int nc, const double* X, int64_t ldx, double* Y,
+              int64_t ldy);
+void kron_conc(Ctx& c, int64_t N, int b, int nc, const double* conc_dev, const double* D, int64_t ldd,
+               double* X, int64_t ldx);
+void wsq_rows(Ctx& c, int64_t M, int b, const double* w, const double* X, int64_t ldx, double* Y, int64_t ldy);
 // tall-skinny products for q <= 16 right-hand sides (HBM streams):
 // Z (R x q) = A^T X with A K x R;  Y (M x q) = A Z with A M x R
 bool skinny_ok(int q);

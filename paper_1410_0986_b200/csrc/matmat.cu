@@ -44,7 +44,90 @@ __global__ void j_gather_scale_k(int64_t M, int b, int nc, int nl, const double*
     }
 }
 
+// X[c*N + v, j] = conc[c] * D[v, j]  (the chromophore axis of a shape
+// perturbation: delta c_c(v) = conc_c * dmu(v), pals.cpp:124-135)
+__global__ void kron_conc_k(int64_t N, int b, int nc, const double* __restrict__ conc,
+                            const double* __restrict__ D, int64_t ldd, double* __restrict__ X, int64_t ldx) {
+    const int64_t total = N * b * nc;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t v = e % N;
+        const int64_t rest = e / N;
+        const int c = int(rest % nc), j = int(rest / nc);
+        X[int64_t(c) * N + v + int64_t(j) * ldx] = conc[c] * D[v + int64_t(j) * ldd];
+    }
+}
+
+// Y[i, j] = w[i]^2 * X[i, j]
+__global__ void wsq_rows_k(int64_t M, int b, const double* __restrict__ w, const double* __restrict__ X,
+                           int64_t ldx, double* __restrict__ Y, int64_t ldy) {
+    const int64_t total = M * b;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = e % M;
+        const int j = int(e / M);
+        Y[i + int64_t(j) * ldy] = w[i] * w[i] * X[i + int64_t(j) * ldx];
+    }
+}
+
 }  // namespace
+
+void kron_conc(Ctx& c, int64_t N, int b, int nc, const double* conc_dev, const double* D, int64_t ldd,
+               double* X, int64_t ldx) {
+    const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((N * b * nc + 255) / 256, int64_t(c.num_sms) * 8)));
+    kron_conc_k<<<blocks, 256, 0, c.stream>>>(N, b, nc, conc_dev, D, ldd, X, ldx);
+    c.check_launch();
+}
+
+void wsq_rows(Ctx& c, int64_t M, int b, const double* w, const double* X, int64_t ldx, double* Y, int64_t ldy) {
+    const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((M * b + 255) / 256, int64_t(c.num_sms) * 8)));
+    wsq_rows_k<<<blocks, 256, 0, c.stream>>>(M, b, w, X, ldx, Y, ldy);
+    c.check_launch();
+}
+
+// J~ X (trans = false: X (N nc) x b -> Y M x b) or J~^T X (X M x b -> Y
+// (N nc) x b): permuted_matvec (experiments.cpp:255-262) with the E_c axis
+// (born.cpp:118-127, pals.cpp:124-135) on the factor U V^T of H.
+void j_matmat(Ctx& c, const double* U, const double* V, int64_t M, int64_t N, int64_t R, bool trans, int b,
+              const int* row_perm, const double* eps_c, int nl, int nc, const double* X, int64_t ldx, double* Y,
+              int64_t ldy) {
+    const int64_t q = int64_t(b) * nc;
+    if (b == 0) return;
+    const double flops = 2.0 * double(R) * double(q) * double(N + M);
+    const double bytes = 8.0 * (double(N) * R + double(M) * R + double(q) * N + double(b) * M);
+    StageTimer _t(c, trans ? "j_matmat_adj" : "j_matmat_fwd", M, N, b, flops, bytes);
+    if (!trans) {
+        if (ldx != N * nc || ldy < M) throw std::invalid_argument("J matvec: dimension mismatch");
+        if (R == 0) {
+            fill(c, M, b, 0.0, Y, ldy);
+            return;
+        }
+        DBuf Z = dalloc(c, size_t(R * q)), T = dalloc(c, size_t(M * q));
+        if (skinny_ok(int(q))) {
+            skinny_tn(c, N, R, int(q), V, N, X, N, Z.d(), R);
+            skinny_nn(c, M, R, int(q), U, M, Z.d(), R, T.d(), M);
+        } else {
+            dgemm(c, true, false, R, q, N, 1.0, V, N, X, N, 0.0, Z.d(), R);
+            dgemm(c, false, false, M, q, R, 1.0, U, M, Z.d(), R, 0.0, T.d(), M);
+        }
+        j_combine(c, M, b, nc, nl, T.d(), M, row_perm, eps_c, Y, ldy);
+    } else {
+        if (ldx < M || ldy != N * nc) throw std::invalid_argument("J rmatvec: dimension mismatch");
+        if (R == 0) {
+            fill(c, N * nc, b, 0.0, Y, ldy);
+            return;
+        }
+        DBuf G = dalloc(c, size_t(M * q)), W = dalloc(c, size_t(R * q));
+        j_gather_scale(c, M, b, nc, nl, X, ldx, row_perm, eps_c, G.d(), M);
+        if (skinny_ok(int(q))) {
+            skinny_tn(c, M, R, int(q), U, M, G.d(), M, W.d(), R);
+            skinny_nn(c, N, R, int(q), V, N, W.d(), R, Y, N);
+        } else {
+            dgemm(c, true, false, R, q, M, 1.0, U, M, G.d(), M, 0.0, W.d(), R);
+            dgemm(c, false, false, N, q, R, 1.0, V, N, W.d(), R, 0.0, Y, N);
+        }
+    }
+}
 
 void j_combine(Ctx& c, int64_t M, int b, int nc, int nl, const double* T, int64_t ldt,
                const int* row_perm, const double* eps_c, double* Y, int64_t ldy) {

@@ -85,6 +85,12 @@ struct ReconCfg {  // ReconConfig (pals.hpp:67-75)
     int max_outer = 30, max_inner = 5, max_retries = 8;
     double gamma = 1.2, nu0 = 1.0, stagnation_tol = 1e-6;
     std::vector<double> fixed_c;
+    // BASELINE config 4's per-step work (a benchmark knob, not part of
+    // pals.cpp): after each Gauss-Newton step's Jacobian, `normal_blocks`
+    // J~x products on the step's chromophore-expanded shape-Jacobian columns
+    // x_k = c (x) dmu/dp_k and as many J~^T y products on y = W^2 J~ x (the
+    // normal-equation products of the step); 0 = off
+    int normal_blocks = 0;
 };
 struct Recon {  // ReconResult (pals.hpp:86-93)
     Params p;
@@ -93,6 +99,7 @@ struct Recon {  // ReconResult (pals.hpp:86-93)
     double resnorm = 0.0;
     bool converged = false, flagged = false;
     int64_t hmv_calls = 0, hmv_columns = 0;
+    int64_t normal_columns = 0;  // J~x (and as many J~^T y) columns of normal_blocks
 };
 // reconstruct (pals.cpp:193-295)
 Recon reconstruct(Ctx& c, const Hop& h, const Geom& g, const double* ext_h, int nl, int nsp,

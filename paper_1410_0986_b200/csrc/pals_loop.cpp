@@ -258,6 +258,35 @@ Recon reconstruct(Ctx& c, const Hop& h, const Geom& g, const double* ext_h, int 
     DBuf HJ = dalloc(c, size_t(M) * std::max(np5, 1)), J = dalloc(c, size_t(M) * std::max(np5, 1));
     DBuf tmp = mu_truth ? dalloc(c, size_t(N)) : DBuf();
     HYDOT_CUDA(cudaMemcpyAsync(ext_d.d(), ext_h, size_t(nl) * nsp * 8, cudaMemcpyHostToDevice, c.stream));
+    // normal-equation blocks (cfg.normal_blocks): X (N nsp) x b, Y M x b, Z (N nsp) x b
+    const int nbk = nsp > 0 ? std::min(cfg.normal_blocks, std::max(np5, 0)) : 0;
+    DBuf nX, nY, nW, nZ, nconc, nperm;
+    if (nbk > 0) {
+        nX = dalloc(c, size_t(N) * nsp * nbk);
+        nY = dalloc(c, size_t(M) * nbk);
+        nW = dalloc(c, size_t(M) * nbk);
+        nZ = dalloc(c, size_t(N) * nsp * nbk);
+        nconc = dalloc(c, size_t(nsp));
+        if (!h.perm) {
+            std::vector<int> id(static_cast<size_t>(M));
+            for (int64_t i = 0; i < M; ++i) id[size_t(i)] = int(i);
+            nperm = DBuf(c, size_t(M) * sizeof(int));
+            HYDOT_CUDA(cudaMemcpyAsync(nperm.as<void>(), id.data(), size_t(M) * sizeof(int), cudaMemcpyHostToDevice,
+                                       c.stream));
+            c.sync();
+        }
+    }
+    auto normal_products = [&]() {
+        HYDOT_CUDA(cudaMemcpyAsync(nconc.d(), res.c.data(), size_t(nsp) * 8, cudaMemcpyHostToDevice, c.stream));
+        kron_conc(c, N, nbk, nsp, nconc.d(), dmudp.d(), N, nX.d(), N * nsp);
+        const int* perm = h.perm ? h.perm : nperm.as<int>();
+        j_matmat(c, h.f->U.d(), h.f->V.d(), M, N, h.f->rank, false, nbk, perm, ext_d.d(), nl, nsp, nX.d(), N * nsp,
+                 nY.d(), M);
+        wsq_rows(c, M, nbk, w, nY.d(), M, nW.d(), M);
+        j_matmat(c, h.f->U.d(), h.f->V.d(), M, N, h.f->rank, true, nbk, perm, ext_d.d(), nl, nsp, nW.d(), M,
+                 nZ.d(), N * nsp);
+        res.normal_columns += nbk;
+    };
 
     auto Hmv = [&](int b, const double* X, double* Y) {
         hmv(c, h, b, X, N, Y, M);
@@ -317,6 +346,7 @@ Recon reconstruct(Ctx& c, const Hop& h, const Geom& g, const double* ext_h, int 
             eval(c, EVAL_JACOBIAN, g, res.p, dmudp.d(), N);
             Hmv(np5, dmudp.d(), HJ.d());
             jscale(c, M, np5, nl, w, ebar_d.d(), HJ.d(), M, J.d(), M);
+            if (nbk > 0) normal_products();
             bool accepted = false;
             double nu_try = nu;
             for (int attempt = 0; attempt < cfg.max_retries; ++attempt) {

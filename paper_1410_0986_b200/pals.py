@@ -237,6 +237,8 @@ class ReconConfig:
     nu0: float = 1.0
     stagnation_tol: float = 1e-6
     fixed_c: List[float] = field(default_factory=list)
+    # BASELINE config 4 knob: J~x / J~^T y normal-equation blocks per GN step
+    normal_blocks: int = 0
 
 
 @dataclass
@@ -259,6 +261,7 @@ class ReconResult:
     flagged: bool = False
     hmv_calls: int = 0
     hmv_columns: int = 0
+    normal_columns: int = 0
 
 
 def reconstruct(ctx: Context, y, H: HOperator, g: GridGeom, ext, init: PaLSParams, w_diag,
@@ -277,7 +280,8 @@ def reconstruct(ctx: Context, y, H: HOperator, g: GridGeom, ext, init: PaLSParam
     if cfg.fixed_c:
         fixed = np.ascontiguousarray(cfg.fixed_c, dtype=np.float64)
     rc = _ReconConfigC(cfg.max_outer, cfg.max_inner, cfg.max_retries, cfg.gamma, cfg.nu0,
-                       cfg.stagnation_tol, None if fixed is None else fixed.ctypes.data_as(_dp))
+                       cfg.stagnation_tol, None if fixed is None else fixed.ctypes.data_as(_dp),
+                       int(cfg.normal_blocks))
     n = init.np()
     ao, bo, co = np.zeros(n), np.zeros(n), np.zeros((n, 3), order="F")
     cc = np.zeros(max(nsp, 1))
@@ -297,7 +301,7 @@ def reconstruct(ctx: Context, y, H: HOperator, g: GridGeom, ext, init: PaLSParam
             for t in trace[:min(out.trace_len, trace_cap)]]
     p = PaLSParams(ao, bo, np.ascontiguousarray(co), init.tau_level, init.eps_H, init.nu_norm)
     return ReconResult(p, list(cc[:nsp]), rows, out.resnorm, bool(out.converged),
-                       bool(out.flagged), out.hmv_calls, out.hmv_columns)
+                       bool(out.flagged), out.hmv_calls, out.hmv_columns, out.normal_columns)
 
 
 def write_trace(path: str, trace: List[TraceRow]) -> None:

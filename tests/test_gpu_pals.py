@@ -175,6 +175,28 @@ def test_reconstruct_compressed_permuted_operator(ctx):
     _compare_recon(r, o)
 
 
+def test_reconstruct_normal_blocks_leave_the_loop_unchanged(ctx):
+    """BASELINE config 4's per-step J~x / J~^T y blocks (ReconConfig.
+    normal_blocks) are extra products: the trace and the result are those of
+    the reference loop, and every GN step issues exactly the requested
+    columns (8 here; the benchmark uses 64)."""
+    from paper_1410_0986_b200 import pals
+    P = pf.recon_problem(9)
+    H = P["H"]
+    perm = np.random.default_rng(4).permutation(H.shape[0]).astype(np.int32)
+    Up = np.eye(H.shape[0])[perm]
+    op, _ = _hop(ctx, Up, H.T, perm)
+    base = dict(max_outer=4, max_inner=2, fixed_c=list(P["c_true"]))
+    args = (ctx, P["y"], op, _geom(P["geom"]), P["ext"], _params(P["init"]), P["w"], P["noise_norm"])
+    r0 = pals.reconstruct(*args, pals.ReconConfig(**base))
+    r1 = pals.reconstruct(*args, pals.ReconConfig(normal_blocks=8, **base))
+    assert [(t.outer, t.inner, t.resnorm, t.accepted) for t in r0.trace] == \
+        [(t.outer, t.inner, t.resnorm, t.accepted) for t in r1.trace]
+    np.testing.assert_array_equal(r0.p.alpha, r1.p.alpha)
+    gn = len({(t.outer, t.inner) for t in r1.trace if t.inner >= 0})
+    assert r0.normal_columns == 0 and r1.normal_columns == 8 * gn
+
+
 def test_reconstruct_argument_errors(ctx):
     from paper_1410_0986_b200 import pals
     P = pf.recon_problem(9)
