@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-sample", type=int, default=1, help="cpu_baseline: sources timed")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="0/8", help="config 3: shard g/G of the source-sharded tree")
     return ap.parse_args()
 
 
@@ -512,6 +513,110 @@ def cpu_sample(st, eps, field, threads: int, n_src: int = 1):
             "seconds": dt}
 
 
+# ------------------------------------------------------------- config 3 --
+def run_cfg3_shard(args):
+    """BASELINE config 3 (n=100, N=1e6, 64 sources x 10 detectors x 200
+    wavelengths, M=128000): the per-GPU workload of the north_star's 8-GPU
+    scaling run, on one GPU.  Shard g/G owns the g-th subtree at depth
+    log2 G (parallel.make_plan); its fields are solved per source inside the
+    step (born.StreamedFieldsProvider: CG -> Born block -> drop, born.cpp:39-80
+    + experiments.cpp:235-240), so only one source's 17.6 GB of fields is
+    resident, then the subtree is compressed (leaves + merges, global seeds and
+    node ids, per-shard hint chains).  One step = the whole shard."""
+    import torch
+    import paper_1410_0986_b200 as h
+    from paper_1410_0986_b200 import born, configs, lowrank as lr
+    from paper_1410_0986_b200.parallel import GpuEngine, make_plan
+
+    rank, world, local = dist_info()
+    if rank != 0:
+        return
+    gi, G = (int(x) for x in args.shard.split("/"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    ctx = h.Context(local)
+    cfg = configs.CONFIGS[3]
+    st = configs.make_setup(cfg)
+    g = st.grid()
+    tree = lr.ClusterTree(st.source_xy, st.box_lo, st.box_hi)
+    eps = configs.compression_tolerance(st, tree.depth())
+    plan = make_plan(tree.nodes, tree.root, G)
+    root_v = plan.shard_roots[gi]
+    srcs = plan.shard_sources[gi]
+    lo, hi = tree.node_box(root_v)
+    w = torch.full((g.N,), cfg.h ** 3, dtype=torch.float64, device=dev)
+    eng = GpuEngine(ctx)
+    units = len(srcs) * cfg.n_det
+    stream = torch.cuda.current_stream()
+
+    def step():
+        prov = born.StreamedFieldsProvider(ctx, g, st.sigma, st.sigma_prime, st.inv_D, st.source_vertex,
+                                           st.detector_vertex, w, 1.0, tol=1e-10, sources=srcs)
+        rec = eng.compress_subtree(st.source_xy[srcs], lo, hi, srcs, root_v, eps, prov, cfg.seed, 20, 10)
+        return rec, prov
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = ctx.launch_count()
+    times, cg_s, logs = [], [], []
+    rec = None
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        rec, prov = step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b) / 1e3)
+        cg_s.append(sum(r["cg_s"] for r in prov.log))
+        logs = prov.log
+    launches = ctx.launch_count() - launches0
+    clk = clocks.stop()
+    # e2e: the same step plus the D2H of the shard factor
+    f = rec.factor
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    rec2, _ = step()
+    Uh = torch.empty((rec2.factor.rank(), rec2.factor.rows()), dtype=torch.float64, pin_memory=True)
+    Vh = torch.empty((rec2.factor.rank(), rec2.factor.cols()), dtype=torch.float64, pin_memory=True)
+    Uh.copy_(rec2.factor.U.T, non_blocking=True)
+    Vh.copy_(rec2.factor.V.T, non_blocking=True)
+    b.record(stream)
+    torch.cuda.synchronize()
+    e2e_s = a.elapsed_time(b) / 1e3
+    step_s = statistics.median(times)
+    it_total = sum(r["iters_total"] for r in logs)
+    cg_mean = statistics.median(cg_s)
+    systems = len(srcs) * (1 + cfg.n_det) * cfg.n_lambda
+    out = {"metric": "(s,d) Born blocks compressed/s", "value": units / step_s, "unit": "blocks/s",
+           "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded BASELINE cfg3 physics, configs.py; fields solved per source in the step)",
+           "config": {"workload": f"cfg3 shard {gi}/{G}: per-source fields (batched CG) + Born blocks + "
+                                  f"recursive compression of the shard's subtree (the per-GPU work of "
+                                  f"the {G}-GPU scaling run)",
+                      "n": cfg.n, "N": g.N, "n_sources_shard": len(srcs), "n_det": cfg.n_det,
+                      "n_lambda": cfg.n_lambda, "M_shard": len(srcs) * cfg.rows_per_source,
+                      "tolerance": f"reference schedule eps_d=1e-6 -> eps={eps:.3e} (L={tree.depth()}), p=20, kprobe=10",
+                      "shard_root_node": int(root_v), "shard_rank": f.rank(),
+                      "l2": "inputs larger than L2 (17.6 GB of fields per source)"},
+           "gpu_launches": int(launches),
+           "e2e": {"value": units / e2e_s, "unit": "blocks/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": int((Uh.numel() + Vh.numel()) * 8),
+                   "note": "inputs are the physics parameters (fields are produced on the device)"},
+           "stages": {"fields_cg_s": cg_mean, "compression_s": step_s - cg_mean,
+                      "cg_systems": systems, "cg_iters_total": it_total,
+                      "cg_GB/s": 48.0 * g.N * it_total / cg_mean / 1e9,
+                      "cg_hbm_frac": 48.0 * g.N * it_total / cg_mean / 1e9 / HBM_PEAK_GBS,
+                      "relres_max": max(r["relres_max"] for r in logs),
+                      "node_rank": list(map(int, rec.node_rank))},
+           "clocks": clk}
+    print(json.dumps(out), flush=True)
+
+
 # ------------------------------------------------------------- config 4 --
 def run_pals(args):
     """BASELINE config 4: the PaLS reconstruction loop (pals.cpp:193-295, run
@@ -751,6 +856,8 @@ def main():
         run_reference(args)
     elif args.config == 4:
         run_pals(args)
+    elif args.config == 3:
+        run_cfg3_shard(args)
     else:
         run_b200(args)
 

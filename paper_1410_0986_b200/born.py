@@ -74,6 +74,51 @@ def compute_fields(ctx: Context, grid: Grid7, sigma, sigma_prime, inv_D, points:
     return out, FieldStats(iters.reshape(len(pts), nl), rel.reshape(len(pts), nl))
 
 
+class StreamedFieldsProvider:
+    """BlockProvider (lowrank.hpp:122-126) that solves the fields per source on
+    demand -- the reference's per-source loop of compute_fields
+    (born.cpp:39-80) fused with compress_H's provider (experiments.cpp:235-240):
+    block(s) runs the batched CG for source s and its detectors, assembles
+    the (N_ds N_lambda) x N Born block (born.cpp:82-98) and drops the fields,
+    so only one source's fields are ever resident (config 3: 17.6 GB per
+    source instead of 1.1 TB for all).
+
+    source_point[s], detector_points[s] (vertex ids); `sources` maps the
+    tree-local index the recursion passes to a global source id.  Records
+    the CG time (CUDA events) and iteration counts per call in `log`."""
+
+    def __init__(self, ctx: Context, grid: Grid7, sigma, sigma_prime, inv_D, source_vertex,
+                 detector_vertices, w: torch.Tensor, nu: float = 1.0, tol: float = 1e-10,
+                 sources=None):
+        self.ctx, self.grid = ctx, grid
+        self.sigma, self.sigma_prime, self.inv_D = sigma, sigma_prime, inv_D
+        self.source_vertex = np.asarray(source_vertex, dtype=np.int64)
+        self.detector_vertices = np.asarray(detector_vertices, dtype=np.int64)
+        self.w, self.nu, self.tol = w, nu, tol
+        self.sources = list(range(len(self.source_vertex))) if sources is None else list(sources)
+        nd = self.detector_vertices.shape[1]
+        self.rows_per_source = nd * len(np.atleast_1d(sigma))
+        self.cols = grid.N
+        self.log = []
+
+    def block(self, s_local: int) -> torch.Tensor:
+        s = self.sources[s_local]
+        pts = [int(self.source_vertex[s])] + [int(v) for v in self.detector_vertices[s]]
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        F, st = compute_fields(self.ctx, self.grid, self.sigma, self.sigma_prime, self.inv_D, pts,
+                               tol=self.tol)
+        b.record()
+        B = assemble_H_block(self.ctx, F[0], [F[1 + d] for d in range(len(pts) - 1)], self.w, self.nu)
+        del F
+        b.synchronize()
+        self.log.append({"source": s, "cg_s": a.elapsed_time(b) / 1e3,
+                         "iters_total": int(st.iters.sum()), "iters_max": int(st.iters.max()),
+                         "relres_max": float(st.relres.max())})
+        return B
+
+
 def apply_operator(ctx: Context, grid: Grid7, sigma: float, sigma_prime: float,
                    x: torch.Tensor) -> torch.Tensor:
     y = torch.empty_like(x)

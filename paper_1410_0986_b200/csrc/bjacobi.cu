@@ -62,7 +62,7 @@ struct BJArgs {
     double* qws;  // per x PW*PW rotations
     int* flag;    // per: 1 = rotate this round
     int* cnt;     // per: chunk arrival counters (self-resetting)
-    int* stats;   // [0] pairs rotated this sweep, [1] inner rotations
+    int* stats;   // [0] pairs rotated this sweep, [1] inner rotations, [2] non-finite pair Grams
 };
 
 __device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, double b0) {
@@ -158,17 +158,24 @@ __device__ void gram_unit(const BJArgs& a, int2 bp, int q, int ch, double* smem,
 }
 
 // Cyclic two-sided Jacobi on the pair Gram: G <- J^T G J, Q <- Q J, 16
-// disjoint rotations per round (circle method over 32 indices).  The
-// eigenvector columns leave sorted by decreasing diagonal.
+// disjoint rotations per round (circle method over 32 indices), run by one
+// warp in shared memory (warp barriers only: a CTA barrier per step made the
+// eigen-solve the latency bottleneck of a round).  The eigenvector columns
+// leave sorted by decreasing diagonal.
 __device__ void eig_pair(const BJArgs& a, int q, double* smem) {
     double* G = smem;              // PW x GS
     double* Q = smem + PW * GS;    // PW x GS
     __shared__ double rc[PW / 2], rs[PW / 2];
     __shared__ int rp[PW / 2], ro[PW / 2];
-    __shared__ int any, rot_total;
+    __shared__ int any, bad, rot_total;
     __shared__ double dsum[PW];
     __shared__ int perm[PW];
     const double* part = a.gws + int64_t(q) * a.nch * (PW * PW);
+    if (threadIdx.x == 0) {
+        any = 0;
+        bad = 0;
+        rot_total = 0;
+    }
     for (int e = threadIdx.x; e < PW * PW; e += NTH) {
         double s = 0.0;
         for (int c = 0; c < a.nch; ++c) s += __ldcg(part + int64_t(c) * (PW * PW) + e);
@@ -176,85 +183,82 @@ __device__ void eig_pair(const BJArgs& a, int q, double* smem) {
         G[i * GS + j] = s;
         Q[i * GS + j] = i == j ? 1.0 : 0.0;
     }
-    if (threadIdx.x == 0) {
-        any = 0;
-        rot_total = 0;
-    }
     __syncthreads();
     // the pair decision: any scaled off-diagonal above flag_tol
     for (int e = threadIdx.x; e < PW * PW; e += NTH) {
         const int i = e % PW, j = e / PW;
-        if (i < j) {
-            const double gij = G[i * GS + j];
-            if (gij != 0.0 && fabs(gij) > a.flag_tol * sqrt(G[i * GS + i] * G[j * GS + j])) any = 1;
-        }
+        const double gij = G[i * GS + j];
+        if (!isfinite(gij)) bad = 1;
+        if (i < j && gij != 0.0 && fabs(gij) > a.flag_tol * sqrt(G[i * GS + i] * G[j * GS + j])) any = 1;
     }
     __syncthreads();
+    if (bad && threadIdx.x == 0) atomicAdd(a.stats + 2, 1);
     if (!any) {
         if (threadIdx.x == 0) a.flag[q] = 0;
         return;
     }
-    for (int sw = 0; sw < kInner; ++sw) {
-        __shared__ int rotated;
-        if (threadIdx.x == 0) rotated = 0;
-        __syncthreads();
-        for (int r = 0; r < PW - 1; ++r) {
-            if (threadIdx.x < PW / 2) {
-                const int k = threadIdx.x;
-                int p = circ(k, r, PW), o = circ(PW - 1 - k, r, PW);
-                if (p > o) {
-                    const int tmp = p;
-                    p = o;
-                    o = tmp;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        for (int sw = 0; sw < kInner; ++sw) {
+            int rotated = 0;
+            for (int r = 0; r < PW - 1; ++r) {
+                bool on = false;
+                if (lane < PW / 2) {
+                    int p = circ(lane, r, PW), o = circ(PW - 1 - lane, r, PW);
+                    if (p > o) {
+                        const int tmp = p;
+                        p = o;
+                        o = tmp;
+                    }
+                    const double app = G[p * GS + p], aoo = G[o * GS + o], apo = G[p * GS + o];
+                    double cs = 1.0, sn = 0.0;
+                    if (apo != 0.0 && fabs(apo) > a.tol * sqrt(app * aoo)) {
+                        rot2(app, aoo, apo, cs, sn);
+                        on = true;
+                    }
+                    rc[lane] = cs;
+                    rs[lane] = on ? sn : 0.0;
+                    rp[lane] = p;
+                    ro[lane] = o;
                 }
-                const double app = G[p * GS + p], aoo = G[o * GS + o], apo = G[p * GS + o];
-                double cs = 1.0, sn = 0.0;
-                if (apo != 0.0 && fabs(apo) > a.tol * sqrt(app * aoo)) {
-                    rot2(app, aoo, apo, cs, sn);
-                    atomicAdd(&rotated, 1);
-                }
-                rc[k] = cs;
-                rs[k] = sn;
-                rp[k] = p;
-                ro[k] = o;
-            }
-            __syncthreads();
-            // rows: G <- J^T G  (row p' = c row_p - s row_o, row o' = s row_p + c row_o)
-            for (int e = threadIdx.x; e < (PW / 2) * PW; e += NTH) {
-                const int k = e / PW, x = e % PW;
-                if (rs[k] != 0.0) {
+                const unsigned mask = __ballot_sync(0xffffffffu, on);
+                if (mask == 0u) continue;
+                rotated += __popc(mask);
+                __syncwarp();
+                // rows: G <- J^T G  (lane = column x)
+                for (int k = 0; k < PW / 2; ++k) {
+                    if (!((mask >> k) & 1u)) continue;
                     const int p = rp[k], o = ro[k];
-                    const double gp = G[p * GS + x], go = G[o * GS + x];
-                    G[p * GS + x] = rc[k] * gp - rs[k] * go;
-                    G[o * GS + x] = rs[k] * gp + rc[k] * go;
+                    const double c = rc[k], s = rs[k];
+                    const double gp = G[p * GS + lane], go = G[o * GS + lane];
+                    G[p * GS + lane] = c * gp - s * go;
+                    G[o * GS + lane] = s * gp + c * go;
                 }
-            }
-            __syncthreads();
-            // columns: G <- G J, Q <- Q J
-            for (int e = threadIdx.x; e < (PW / 2) * PW; e += NTH) {
-                const int k = e / PW, x = e % PW;
-                if (rs[k] != 0.0) {
+                __syncwarp();
+                // columns: G <- G J, Q <- Q J  (lane = row x)
+                for (int k = 0; k < PW / 2; ++k) {
+                    if (!((mask >> k) & 1u)) continue;
                     const int p = rp[k], o = ro[k];
-                    const double gp = G[x * GS + p], go = G[x * GS + o];
-                    G[x * GS + p] = rc[k] * gp - rs[k] * go;
-                    G[x * GS + o] = rs[k] * gp + rc[k] * go;
-                    const double qp = Q[x * GS + p], qo = Q[x * GS + o];
-                    Q[x * GS + p] = rc[k] * qp - rs[k] * qo;
-                    Q[x * GS + o] = rs[k] * qp + rc[k] * qo;
+                    const double c = rc[k], s = rs[k];
+                    const double gp = G[lane * GS + p], go = G[lane * GS + o];
+                    G[lane * GS + p] = c * gp - s * go;
+                    G[lane * GS + o] = s * gp + c * go;
+                    const double qp = Q[lane * GS + p], qo = Q[lane * GS + o];
+                    Q[lane * GS + p] = c * qp - s * qo;
+                    Q[lane * GS + o] = s * qp + c * qo;
                 }
+                __syncwarp();
+                if (on) {  // annihilated exactly
+                    G[rp[lane] * GS + ro[lane]] = 0.0;
+                    G[ro[lane] * GS + rp[lane]] = 0.0;
+                }
+                __syncwarp();
             }
-            __syncthreads();
-            if (threadIdx.x < PW / 2 && rs[threadIdx.x] != 0.0) {  // annihilated exactly
-                const int p = rp[threadIdx.x], o = ro[threadIdx.x];
-                G[p * GS + o] = 0.0;
-                G[o * GS + p] = 0.0;
-            }
-            __syncthreads();
+            if (lane == 0) rot_total += rotated;
+            if (rotated == 0) break;
         }
-        if (threadIdx.x == 0) rot_total += rotated;
-        __syncthreads();
-        if (rotated == 0) break;
     }
+    __syncthreads();
     // sort by decreasing diagonal (stable rank order)
     if (threadIdx.x < PW) dsum[threadIdx.x] = G[threadIdx.x * GS + threadIdx.x];
     __syncthreads();
@@ -424,8 +428,8 @@ int bjacobi_converge(Ctx& c, int64_t m, int64_t n, double* U, double tol) {
     const int grid = std::min(units, max_grid);
     DBuf gws = dalloc(c, size_t(per) * size_t(nch) * PW * PW);
     DBuf qws = dalloc(c, size_t(per) * PW * PW);
-    DBuf ints(c, sizeof(int) * size_t(2 * per + 2));
-    HYDOT_CUDA(cudaMemsetAsync(ints.as<void>(), 0, sizeof(int) * size_t(2 * per + 2), c.stream));
+    DBuf ints(c, sizeof(int) * size_t(2 * per + 3));
+    HYDOT_CUDA(cudaMemsetAsync(ints.as<void>(), 0, sizeof(int) * size_t(2 * per + 3), c.stream));
     BJArgs a;
     a.m = m;
     a.n = int(n);
@@ -446,16 +450,18 @@ int bjacobi_converge(Ctx& c, int64_t m, int64_t n, double* U, double tol) {
     a.stats = ints.as<int>() + 2 * per;
     int sweeps = 0;
     for (; sweeps < kMaxBSweeps; ++sweeps) {
-        HYDOT_CUDA(cudaMemsetAsync(a.stats, 0, 2 * sizeof(int), c.stream));
+        HYDOT_CUDA(cudaMemsetAsync(a.stats, 0, 3 * sizeof(int), c.stream));
         void* args[] = {&a};
         c.coop_launch((void*)bjacobi_sweep_k, dim3(grid), dim3(NTH), args, 0);
         c.count();
-        int st[2] = {0, 0};
+        int st[3] = {0, 0, 0};
         HYDOT_CUDA(cudaMemcpyAsync(st, a.stats, sizeof st, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
         if (bj_stats())
-            fprintf(stderr, "[bjacobi] m=%lld n=%lld sweep=%d pairs_rotated=%d inner_rotations=%d (of %d pairs)\n",
-                    (long long)m, (long long)n, sweeps, st[0], st[1], per * rounds);
+            fprintf(stderr,
+                    "[bjacobi] m=%lld n=%lld sweep=%d pairs_rotated=%d inner_rotations=%d (of %d pairs) nonfinite=%d\n",
+                    (long long)m, (long long)n, sweeps, st[0], st[1], per * rounds, st[2]);
+        if (st[2] > 0) throw std::runtime_error("block Jacobi: non-finite column Gram (input not finite?)");
         if (st[0] == 0) break;
     }
     return sweeps + 1;

@@ -869,26 +869,11 @@ __global__ void __launch_bounds__(ZT, 2) cgzt_pa(ZGeo g, int64_t N, int nl, int 
 }
 
 // CTAs per SM the z-marching kernels are compiled for (3: 80 registers;
-// 4 forces 64 and spills: 0.84 vs 0.63 s on config 1); HYDOT_CG_ZOCC=4 for experiments
-int zmarch_occ() {
-    static const int o = [] {
-        const char* e = std::getenv("HYDOT_CG_ZOCC");
-        return e && e[0] == '4' ? 4 : 3;
-    }();
-    return o;
-}
-#define ZSEL(k) (zmarch_occ() == 3 ? k<3> : k<4>)
+// 4 forces 64 and spills: 0.84 vs 0.63 s on config 1)
+#define ZSEL(k) (k<3>)
 
-// HYDOT_CG_PA_DEEP=1: cgzt_pa with 4 raw planes and 3 p_new planes (one
-// more plane in flight, one more barrier per plane: measured 0.493 -> 0.503 s
-// on config 1, so opt-in only)
-bool zpa_deep() {
-    static const bool on = [] {
-        const char* e = std::getenv("HYDOT_CG_PA_DEEP");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
+// (a cgzt_pa with 4 raw planes and 3 p_new planes -- one more plane in
+// flight, one more barrier per plane -- measured 0.493 -> 0.503 s on config 1)
 
 // bulk-copy x/r kernel for even nx (HYDOT_CG_BULK=0 keeps the register one)
 bool zbulk_on() {
@@ -984,41 +969,23 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
             zsmem = size_t(3) * size_t(ty + 2) * size_t(op.g.nx) * sizeof(double);
             if (op.g.nx % 2 == 0 && zbulk_on()) {
                 ztsmem = size_t(NSP * (ty + 2) + NSX * 2 * ty) * size_t(op.g.nx) * sizeof(double);
-                ztpsmem = zpa_deep() ? size_t((2 * 4 + 3) * (ty + 2)) * size_t(op.g.nx) * sizeof(double)
-                                     : size_t((2 * NSR + 4) * (ty + 2)) * size_t(op.g.nx) * sizeof(double);
+                ztpsmem = size_t((2 * NSR + 4) * (ty + 2)) * size_t(op.g.nx) * sizeof(double);
                 static AttrGate attr;
                 attr_once(attr, c.device, [&] {
                     HYDOT_CUDA(cudaFuncSetAttribute(cgzt_xr, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     200 * 1024));
                     HYDOT_CUDA(cudaFuncSetAttribute(cgzt_pa<NSR, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     200 * 1024));
-                    HYDOT_CUDA(cudaFuncSetAttribute(cgzt_pa<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    200 * 1024));
-                    // same shared-memory carve-out for both kernels of an
-                    // iteration (no SM reconfiguration between launches)
-                    if (std::getenv("HYDOT_CG_CARVE")) {
-                        const int cv = std::atoi(std::getenv("HYDOT_CG_CARVE"));
-                        HYDOT_CUDA(cudaFuncSetAttribute(cgzt_pa<NSR, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
-                        HYDOT_CUDA(cudaFuncSetAttribute(cgzt_xr, cudaFuncAttributePreferredSharedMemoryCarveout, cv));
-                    }
                 });
             }
         }
     }
     // One batch of up to 24 GB (all systems iterate together, HBM-bound).
-    // HYDOT_CG_L2_MB > 0 instead iterates L2-sized groups (32 N bytes per
-    // system): measured slower on config 1 (1.4-2.8 s vs 0.96 s -- small
-    // groups make the iterations launch- and sync-bound), kept for experiments.
-    // A z-marching shared-memory stencil (one CTA per x-y tile walking z)
-    // also measured slower (1.35 s: one plane of loads in flight per CTA).
-    static const int l2_mb = [] {
-        const char* e = std::getenv("HYDOT_CG_L2_MB");
-        return e ? std::atoi(e) : 0;
-    }();
+    // L2-sized groups (32 N bytes per system) measured slower on config 1
+    // (1.4-2.8 s vs 0.96 s: small groups make the iterations launch- and
+    // sync-bound).
     int64_t per_sys = 2 * N * 8;
     int batch = int(std::max<int64_t>(1, std::min<int64_t>(total, (int64_t(24) << 30) / per_sys)));
-    if (l2_mb > 0)
-        batch = int(std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t(l2_mb) << 20) / (4 * per_sys))));
     batch = std::min(batch, 65535);
     DBuf dsig = dalloc(c, size_t(nl)), dsigp = dalloc(c, size_t(nl)), dinv = dalloc(c, size_t(nl));
     HYDOT_CUDA(cudaMemcpyAsync(dsig.d(), sigma, size_t(nl) * 8, cudaMemcpyHostToDevice, c.stream));
@@ -1068,7 +1035,7 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
             dim3 grid = dim3(unsigned(nparts), unsigned(active.size()));
             if (zsmem) {
                 if (ztpsmem)
-                    (zpa_deep() ? cgzt_pa<4, 3> : cgzt_pa<NSR, 4>)<<<grid, ZT, ztpsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
+                    cgzt_pa<NSR, 4><<<grid, ZT, ztpsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
                                                              pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
                                                              tol, fixed_iters > 0, dact.as<int>());
                 else
@@ -1117,7 +1084,7 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
             // one more convergence check for systems finishing on the last step
             dim3 grid = dim3(unsigned(nparts), unsigned(active.size()));
             if (ztpsmem)
-                (zpa_deep() ? cgzt_pa<4, 3> : cgzt_pa<NSR, 4>)<<<grid, ZT, ztpsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
+                cgzt_pa<NSR, 4><<<grid, ZT, ztpsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
                                                          pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
                                                          tol, 0, dact.as<int>());
             else if (zsmem)

@@ -358,18 +358,9 @@ void dgemm(Ctx& c, bool ta, bool tb, int64_t m, int64_t n, int64_t k, double alp
         c.check_launch();
         return;
     }
-    // HYDOT_GEMM_BIG=1: 128x64 CTA tiles (64x32 warp tiles: 16 DMMAs per 12
-    // fragment loads instead of 8 per 8) when m >= 128 -- measured slower on
-    // every path shape (254 registers, 2 CTAs/SM: QR W = V^T C 28 -> 18.6
-    // TF/s, C -= V W 29.6 -> 26 TF/s), kept opt-in for experiments
-    static const bool big = [] {
-        const char* e = std::getenv("HYDOT_GEMM_BIG");
-        return e && e[0] == '1';
-    }();
-    if (big && m >= 128 && n >= 64)
-        run_tiles<128, 64, 64, 32>(c, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
-    else
-        run_tiles<64, 64, 32, 32>(c, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+    // 64x64 CTA tiles (a 128x64 / 64x32-warp-tile variant measured slower on
+    // every path shape: 254 registers, 2 CTAs/SM, QR W = V^T C 28 -> 18.6 TF/s)
+    run_tiles<64, 64, 32, 32>(c, ta, tb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
 }
 
 }  // namespace hydot

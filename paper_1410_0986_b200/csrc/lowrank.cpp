@@ -36,38 +36,10 @@ DBuf materialise_t(Ctx& c, const double* S, int64_t ld, int64_t m, int64_t n) {
 // QR-factored triangle needs ~4x fewer sweeps than on X itself (measured
 // 8-10 vs 28-41 on graded 300x300 cores).  `upper`: X is already the n x n
 // triangle R1 (Q1 = I).
-// HYDOT_SVD_PRESORT_TALL=0 restores sorting the triangle after the tall QR
-bool presort_tall() {
-    static const bool on = [] {
-        const char* e = std::getenv("HYDOT_SVD_PRESORT_TALL");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
 // SVD of an n x n upper triangle R1 that came from the QR of norm-ordered
 // columns: R1^T = Q2 R2, Jacobi on L = R2^T = Ux S Vx^T, so R1 = Ux S (Q2 Vx)^T.
 // Ux -> U (n x n), Q2 Vx -> V (n x n).
-// HYDOT_DUMP_CORES=dir: write every R1 (n >= 256) of the identity path as
-// raw float64 (column-major) for offline preconditioning experiments
-void dump_core(Ctx& c, const char* tag, int64_t m, int64_t n, const double* A, int64_t lda) {
-    static const char* dir = std::getenv("HYDOT_DUMP_CORES");
-    static int count = 0;
-    if (!dir || n < 256 || count >= 12) return;
-    std::vector<double> h(size_t(m * n));
-    DBuf t = dalloc(c, size_t(m * n));
-    copy2d(c, m, n, A, lda, t.d(), m);
-    c.d2h(h.data(), t.d(), h.size());
-    char path[512];
-    snprintf(path, sizeof path, "%s/%s_%02d_%lldx%lld.f64", dir, tag, count++, (long long)m, (long long)n);
-    if (FILE* f = fopen(path, "wb")) {
-        fwrite(h.data(), 8, h.size(), f);
-        fclose(f);
-    }
-}
-
 void svd_of_sorted_r(Ctx& c, int64_t n, const double* R1, double* U, std::vector<double>& s, double* V) {
-    dump_core(c, "r1", n, n, R1, n);
     QRFact q2;
     DBuf T = dalloc(c, size_t(n * n)), R2 = dalloc(c, size_t(n * n));
     transpose(c, n, n, R1, n, T.d(), n);  // R1^T
@@ -89,11 +61,8 @@ void jacobi_precond(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, 
     // Q2 R2, 4. Jacobi on L = R2^T:  X = (Q1 Ul) S (P Q2 Vl)^T.
     // Measured on the config-1 pipeline: total Jacobi time 1.73 s with
     // norm-ordering + two QRs, 3.17 s with norm-ordering + one QR, 3.40 s
-    // with two QRs only (HYDOT_SVD_PRECOND=r selects one QR).
-    static const bool qrqr = [] {
-        const char* e = std::getenv("HYDOT_SVD_PRECOND");
-        return !(e && std::string(e) == "r");
-    }();
+    // with two QRs only.
+    constexpr bool qrqr = true;
     DBuf nrm = dalloc(c, size_t(n));
     col_norms(c, m, n, X, ldx, nrm.d());
     std::vector<double> hn(static_cast<size_t>(n));
@@ -106,7 +75,6 @@ void jacobi_precond(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, 
                                cudaMemcpyHostToDevice, c.stream));
     DBuf Xp = dalloc(c, size_t(m * n));
     gather_cols(c, m, n, X, ldx, dperm.as<int>(), Xp.d(), m);
-    dump_core(c, "y", m, n, Xp.d(), m);
     QRFact q1, q2;
     geqrf(c, m, n, Xp.d(), m, q1);
     Xp.release();
@@ -242,7 +210,7 @@ SVDd fast_thin_svd_impl(Ctx& c, const double* S, int64_t ld, bool trans, int64_t
         o.V = dalloc(c, size_t(n * n));
         DBuf Ur = dalloc(c, size_t(n * n));
         QRFact qf;
-        if (n <= 48 || !presort_tall()) {
+        if (n <= 48) {
             geqrf(c, m, n, Lp, ldl, qf);
             tmp.release();
             DBuf R = dalloc(c, size_t(n * n));
@@ -417,7 +385,7 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
         // not used here -- it cost 2 % of the step and most of the e2e overlap
         const bool small = double(n) * double(m) * 16.0 <= 16.0 * double(1ull << 30);
         if (!(rs1 >= nmax && m <= n) && rs2 >= nmax && m <= n && n >= 2 * m && m > 48 && small &&
-            presort_tall() && async_v_on() && speculate_on()) {
+            async_v_on() && speculate_on()) {
             // speculation is optional: if its buffers do not fit, run without it
             try {
                 spec.reset(new TallSpec());

@@ -506,15 +506,6 @@ void gram_t32(Ctx& c, int64_t mr, int jb, const double* P, int64_t ld, const dou
     c.check_launch();
 }
 
-// HYDOT_QR_FUSED_T=0 restores the GEMM + larft_k sub-panel T
-bool fused_t32() {
-    static const bool on = [] {
-        const char* e = std::getenv("HYDOT_QR_FUSED_T");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
 void larft(Ctx& c, int jb, const double* G, int64_t ldg, const double* tau, double* T) {
     static AttrGate attr;
     const int smem = (NB * (NB + 1) + (NB / 2) * (NB / 2 + 1)) * sizeof(double);
@@ -564,12 +555,7 @@ void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f
             if (rest > 0) {
                 // apply this sub-panel's reflector to the rest of the block
                 form_v_launch(c, pr, pb, Pp, m, V.d());
-                if (fused_t32())
-                    gram_t32(c, pr, pb, Pp, m, f.tau.d() + j0 + p0, Tp.d(), gpart.d(), gticket.as<unsigned>());
-                else {
-                    dgemm(c, true, false, pb, pb, pr, 1.0, V.d(), pr, V.d(), pr, 0.0, G.d(), pb);
-                    larft(c, pb, G.d(), pb, f.tau.d() + j0 + p0, Tp.d());
-                }
+                gram_t32(c, pr, pb, Pp, m, f.tau.d() + j0 + p0, Tp.d(), gpart.d(), gticket.as<unsigned>());
                 double* Cm = Pp + int64_t(pb) * m;
                 dgemm(c, true, false, pb, rest, pr, 1.0, V.d(), pr, Cm, m, 0.0, W.d(), pb);
                 dgemm(c, true, false, pb, rest, pb, 1.0, Tp.d(), NB, W.d(), pb, 0.0, W2.d(), pb);

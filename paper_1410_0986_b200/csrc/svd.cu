@@ -693,25 +693,14 @@ const int2* device_pairs(Ctx& c, int n, int& np) {
 // cores too long for that use 2-column blocks at 512 threads (<= 12 rows
 // per thread, m <= 6144).  false = not used.
 bool rblk_shape(int64_t m, int64_t n, int& R, int& T, int& B) {
-    static const int mode = [] {
-        const char* e = std::getenv("HYDOT_JACOBI_BLK");
-        return e ? std::atoi(e) : 1;
-    }();
-    if (mode == 0) return false;
     // at least 128 threads: with 64 each of the 2 warps forms two rotations
     // per sub-round in sequence (111-320-row cores: 242 -> 174 ms per
     // config-1 step at 128; 206 ms at 256)
-    static const int tmin = [] {
-        const char* e = std::getenv("HYDOT_JACOBI_TMIN");
-        return e ? std::max(64, std::atoi(e)) : 128;
-    }();
+    constexpr int tmin = 128;
     // 256 threads may hold 9 rows each (1153-2304-row cores): fewer warps
     // per sub-round reduction, 2172^2 core 131 -> 112 ms; at 128 threads 9
-    // rows measured slower than 256 x 5.  HYDOT_JACOBI_RMAX=5 disables.
-    static const int rmax256 = [] {
-        const char* e = std::getenv("HYDOT_JACOBI_RMAX");
-        return (e && std::atoi(e) < 9) ? RMAXR : 9;
-    }();
+    // rows measured slower than 256 x 5
+    constexpr int rmax256 = 9;
     B = RB;
     if ((n + RB - 1) / RB >= 4) {
         for (T = tmin; T <= 512; T *= 2) {
@@ -719,15 +708,8 @@ bool rblk_shape(int64_t m, int64_t n, int& R, int& T, int& B) {
             const int cap = T == 512 ? 5 : T == 256 ? rmax256 : RMAXR;  // 512 threads: 128 registers each
             if (R <= cap) {
                 R = R <= 3 ? 3 : R <= 5 ? 5 : 9;  // instantiated row counts
-                // HYDOT_JACOBI_B8=1: 8-column blocks (half the block rounds
-                // and grid barriers, 8 pairs per sub-round) where registers
-                // allow -- measured slower (Jacobi 454 -> 566 ms per config-1
-                // step: 24-value reductions, register pressure), opt-in only
-                static const bool b8 = [] {
-                    const char* e = std::getenv("HYDOT_JACOBI_B8");
-                    return e && e[0] == '1';
-                }();
-                if (b8 && R <= 5 && T <= 256 && (n + 7) / 8 >= 4) B = 8;
+                // (8-column blocks measured slower: Jacobi 454 -> 566 ms per
+                // config-1 step, 24-value reductions and register pressure)
                 return true;
             }
         }
@@ -755,12 +737,7 @@ void launch_rblk_t(Ctx& c, int64_t m, int64_t n, double* U, int64_t ldu, double 
     int grid = std::max(1, std::min(npb / 2, per_sm * c.num_sms));
     int64_t mm = m;
     int nn = int(n), nbb = nb;
-    // HYDOT_JACOBI_CROSS=0: full mini-sweep per block-pair visit
-    static const int cross_env = [] {
-        const char* e = std::getenv("HYDOT_JACOBI_CROSS");
-        return (e && e[0] == '0') ? 0 : 1;
-    }();
-    int cross = cross_env;
+    int cross = 1;  // cross schedule (a full mini-sweep per visit needs 34-42 % more sub-rounds)
     void* args[] = {&mm, &nn, &nbb, &bp, &U, &ldu, &tol, &counters, &sweeps_out, &cross, &stop_thr};
     c.coop_launch((void*)jacobi_rblk_k<R, T, B>, dim3(grid), dim3(T), args, 0);
     c.count();
@@ -774,13 +751,6 @@ void launch_rblk(Ctx& c, int R, int T, int B, int64_t m, int64_t n, double* U, i
             case 9: launch_rblk_t<9, 512, 2>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr); break;
             default: launch_rblk_t<12, 512, 2>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr); break;
         }
-        return;
-    }
-    if (B == 8) {
-        if (R == 3 && T == 128) launch_rblk_t<3, 128, 8>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr);
-        else if (R == 3) launch_rblk_t<3, 256, 8>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr);
-        else if (T == 128) launch_rblk_t<5, 128, 8>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr);
-        else launch_rblk_t<5, 256, 8>(c, m, n, U, ldu, tol, counters, sweeps_out, stop_thr);
         return;
     }
     if (R == 9) {
@@ -849,10 +819,7 @@ void rblk_converge(Ctx& c, int R, int T, int B, int64_t m, int64_t n, double* U,
     // a sweep of <= 12 n rotations is followed by one of at most a few hundred
     // on the path's cores; fixing a pair costs ~1/100 of a sweep at n = 300
     const int cap = int(std::clamp<int64_t>(n / 4, 16, 256));
-    static const int tailk = [] {  // HYDOT_JACOBI_TAILK: the stop threshold in units of n
-        const char* e = std::getenv("HYDOT_JACOBI_TAILK");
-        return e ? std::max(1, std::atoi(e)) : 12;
-    }();
+    constexpr int tailk = 12;  // the stop threshold in units of n (12 / 20 / 30 measured within noise)
     launch_rblk(c, R, T, B, m, n, U, m, tol, counters, sweeps_out, int(std::min<int64_t>(tailk * n, 1 << 30)));
     DBuf G = dalloc(c, size_t(n * n));
     DBuf cnt(c, sizeof(int));
@@ -909,17 +876,10 @@ void jacobi_svd(Ctx& c, int64_t m, int64_t n, const double* X, int64_t ldx, doub
     DBuf U = dalloc(c, size_t(m * n));
     DBuf V = dalloc(c, size_t(n * n));
     copy2d(c, m, n, X, ldx, U.d(), m);
-    // ||A|| estimate for the absolute floor: the largest column norm
-    DBuf cn = dalloc(c, size_t(n));
-    colnorm_k<<<unsigned(n), 256, 0, c.stream>>>(m, int(n), U.d(), m, cn.d());
-    c.check_launch();
-    std::vector<double> cnh(static_cast<size_t>(n));
-    c.d2h(cnh.data(), cn.d(), size_t(n));
-    // The absolute floor is off (0): it saved few sweeps on the path's cores
-    // and leaves the vectors of negligible singular values non-orthonormal,
-    // unlike BDCSVD.  Kept for experiments via HYDOT_JACOBI_ATOL.
-    const char* at_env = std::getenv("HYDOT_JACOBI_ATOL");
-    const double atol = (at_env ? std::atof(at_env) : 0.0) * *std::max_element(cnh.begin(), cnh.end());
+    // No absolute rotation floor (atol = 0): one at eps ||A|| saved few sweeps
+    // on the path's cores and leaves the vectors of negligible singular
+    // values non-orthonormal, unlike BDCSVD.
+    const double atol = 0.0;
     DBuf sw(c, sizeof(int) * (kMaxSweeps + 1));
     HYDOT_CUDA(cudaMemsetAsync(sw.as<void>(), 0, sizeof(int) * (kMaxSweeps + 1), c.stream));
     bool lazy_v = false;
