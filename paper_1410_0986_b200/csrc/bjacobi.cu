@@ -85,7 +85,10 @@ __device__ __forceinline__ void rot2(double a, double b, double g, double& cs, d
 }
 
 __device__ __forceinline__ int circ(int pos, int r, int np) {
-    return pos == 0 ? 0 : ((pos - 1 + r) % (np - 1)) + 1;
+    if (pos == 0) return 0;
+    int v = pos - 1 + r;  // < 2 (np - 1)
+    if (v >= np - 1) v -= np - 1;
+    return v + 1;
 }
 
 // global column of pair-local column j (-1: padding / dummy block)
@@ -202,6 +205,7 @@ __device__ void eig_pair(const BJArgs& a, int q, double* smem) {
         for (int sw = 0; sw < kInner; ++sw) {
             int rotated = 0;
             for (int r = 0; r < PW - 1; ++r) {
+                // circle-method pair of slot k = lane (k < 16) in round r
                 bool on = false;
                 if (lane < PW / 2) {
                     int p = circ(lane, r, PW), o = circ(PW - 1 - lane, r, PW);
@@ -225,27 +229,44 @@ __device__ void eig_pair(const BJArgs& a, int q, double* smem) {
                 if (mask == 0u) continue;
                 rotated += __popc(mask);
                 __syncwarp();
-                // rows: G <- J^T G  (lane = column x)
-                for (int k = 0; k < PW / 2; ++k) {
-                    if (!((mask >> k) & 1u)) continue;
-                    const int p = rp[k], o = ro[k];
-                    const double c = rc[k], s = rs[k];
-                    const double gp = G[p * GS + lane], go = G[o * GS + lane];
-                    G[p * GS + lane] = c * gp - s * go;
-                    G[o * GS + lane] = s * gp + c * go;
+                // every index is in exactly one slot: a lane updates a whole
+                // column (rows phase) or row (columns phase), 8 slots at a
+                // time with all their loads issued before any store
+                constexpr int H = PW / 4;
+#pragma unroll
+                for (int h0 = 0; h0 < PW / 2; h0 += H) {  // rows: G <- J^T G (lane = column)
+                    double vp[H], vo[H];
+#pragma unroll
+                    for (int k = 0; k < H; ++k) {
+                        vp[k] = G[rp[h0 + k] * GS + lane];
+                        vo[k] = G[ro[h0 + k] * GS + lane];
+                    }
+#pragma unroll
+                    for (int k = 0; k < H; ++k) {
+                        const double c = rc[h0 + k], sn = rs[h0 + k];
+                        G[rp[h0 + k] * GS + lane] = c * vp[k] - sn * vo[k];
+                        G[ro[h0 + k] * GS + lane] = sn * vp[k] + c * vo[k];
+                    }
                 }
                 __syncwarp();
-                // columns: G <- G J, Q <- Q J  (lane = row x)
-                for (int k = 0; k < PW / 2; ++k) {
-                    if (!((mask >> k) & 1u)) continue;
-                    const int p = rp[k], o = ro[k];
-                    const double c = rc[k], s = rs[k];
-                    const double gp = G[lane * GS + p], go = G[lane * GS + o];
-                    G[lane * GS + p] = c * gp - s * go;
-                    G[lane * GS + o] = s * gp + c * go;
-                    const double qp = Q[lane * GS + p], qo = Q[lane * GS + o];
-                    Q[lane * GS + p] = c * qp - s * qo;
-                    Q[lane * GS + o] = s * qp + c * qo;
+#pragma unroll
+                for (int h0 = 0; h0 < PW / 2; h0 += H) {  // columns: G <- G J, Q <- Q J (lane = row)
+                    double vp[H], vo[H], wp[H], wo[H];
+#pragma unroll
+                    for (int k = 0; k < H; ++k) {
+                        vp[k] = G[lane * GS + rp[h0 + k]];
+                        vo[k] = G[lane * GS + ro[h0 + k]];
+                        wp[k] = Q[lane * GS + rp[h0 + k]];
+                        wo[k] = Q[lane * GS + ro[h0 + k]];
+                    }
+#pragma unroll
+                    for (int k = 0; k < H; ++k) {
+                        const double c = rc[h0 + k], sn = rs[h0 + k];
+                        G[lane * GS + rp[h0 + k]] = c * vp[k] - sn * vo[k];
+                        G[lane * GS + ro[h0 + k]] = sn * vp[k] + c * vo[k];
+                        Q[lane * GS + rp[h0 + k]] = c * wp[k] - sn * wo[k];
+                        Q[lane * GS + ro[h0 + k]] = sn * wp[k] + c * wo[k];
+                    }
                 }
                 __syncwarp();
                 if (on) {  // annihilated exactly
