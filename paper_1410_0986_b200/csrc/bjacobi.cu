@@ -47,7 +47,13 @@ constexpr int NTH = 128;      // threads per CTA (4 warps)
 constexpr int XS = SUB + 4;   // X sub-tile stride ([col][row], conflict-free fragments)
 constexpr int QS = PW + 4;    // Q stride ([out col][in col])
 constexpr int GS = PW + 1;    // eigen-solver stride
-constexpr int kInner = 30;    // max inner sweeps on one pair Gram
+// Inner sweeps per pair visit: the pair Gram is diagonalised only to a
+// threshold 1e-4 x its initial largest scaled off-diagonal (floor tol), at
+// most kInner sweeps -- the outer sweeps converge quadratically anyway, and
+// on strongly graded pairs the inner rotations' own rounding keeps tiny
+// off-diagonals above tol forever (an uncapped solve ran 30 sweeps there).
+constexpr int kInner = 4;
+constexpr double kInnerRel = 1e-4;
 constexpr int kMaxBSweeps = 40;
 
 struct BJArgs {
@@ -62,7 +68,7 @@ struct BJArgs {
     double* qws;  // per x PW*PW rotations
     int* flag;    // per: 1 = rotate this round
     int* cnt;     // per: chunk arrival counters (self-resetting)
-    int* stats;   // [0] pairs rotated this sweep, [1] inner rotations, [2] non-finite pair Grams
+    int* stats;   // [0] pairs rotated this sweep, [1] inner rotations, [2] non-finite pair Grams, [3] inner sweeps
 };
 
 __device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, double b0) {
@@ -102,12 +108,20 @@ __device__ __forceinline__ int pair_col(int2 bp, int j, int n) {
 // outside), coalesced along rows
 __device__ __forceinline__ void load_sub(double* xs, const double* __restrict__ U, int64_t ldu,
                                          const int* col, int64_t r, int64_t rend) {
-#pragma unroll 4
-    for (int e = threadIdx.x; e < SUB * PW; e += NTH) {
+    constexpr int PER = SUB * PW / NTH;  // 16 loads per thread, all in flight at once
+    double v[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int e = threadIdx.x + k * NTH;
         const int i = e & (SUB - 1), j = e / SUB;
         const int64_t gi = r + i;
         const int cj = col[j];
-        xs[j * XS + i] = (cj >= 0 && gi < rend) ? __ldcg(U + gi + int64_t(cj) * ldu) : 0.0;
+        v[k] = (cj >= 0 && gi < rend) ? __ldcg(U + gi + int64_t(cj) * ldu) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int e = threadIdx.x + k * NTH;
+        xs[(e / SUB) * XS + (e & (SUB - 1))] = v[k];
     }
 }
 
@@ -170,7 +184,8 @@ __device__ void eig_pair(const BJArgs& a, int q, double* smem) {
     double* Q = smem + PW * GS;    // PW x GS
     __shared__ double rc[PW / 2], rs[PW / 2];
     __shared__ int rp[PW / 2], ro[PW / 2];
-    __shared__ int any, bad, rot_total;
+    __shared__ int any, bad, rot_total, sweeps_total;
+    __shared__ unsigned long long off0_bits;
     __shared__ double dsum[PW];
     __shared__ int perm[PW];
     const double* part = a.gws + int64_t(q) * a.nch * (PW * PW);
@@ -178,6 +193,8 @@ __device__ void eig_pair(const BJArgs& a, int q, double* smem) {
         any = 0;
         bad = 0;
         rot_total = 0;
+        sweeps_total = 0;
+        off0_bits = 0ull;
     }
     for (int e = threadIdx.x; e < PW * PW; e += NTH) {
         double s = 0.0;
@@ -192,7 +209,14 @@ __device__ void eig_pair(const BJArgs& a, int q, double* smem) {
         const int i = e % PW, j = e / PW;
         const double gij = G[i * GS + j];
         if (!isfinite(gij)) bad = 1;
-        if (i < j && gij != 0.0 && fabs(gij) > a.flag_tol * sqrt(G[i * GS + i] * G[j * GS + j])) any = 1;
+        if (i < j && gij != 0.0) {
+            const double sc = fabs(gij) / sqrt(G[i * GS + i] * G[j * GS + j]);
+            if (sc > a.flag_tol) {
+                any = 1;
+                // non-negative doubles order like their bit patterns
+                atomicMax(&off0_bits, (unsigned long long)__double_as_longlong(sc));
+            }
+        }
     }
     __syncthreads();
     if (bad && threadIdx.x == 0) atomicAdd(a.stats + 2, 1);
@@ -202,6 +226,7 @@ __device__ void eig_pair(const BJArgs& a, int q, double* smem) {
     }
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
+        const double tin = fmax(a.tol, kInnerRel * __longlong_as_double((long long)off0_bits));
         for (int sw = 0; sw < kInner; ++sw) {
             int rotated = 0;
             for (int r = 0; r < PW - 1; ++r) {
@@ -216,7 +241,7 @@ __device__ void eig_pair(const BJArgs& a, int q, double* smem) {
                     }
                     const double app = G[p * GS + p], aoo = G[o * GS + o], apo = G[p * GS + o];
                     double cs = 1.0, sn = 0.0;
-                    if (apo != 0.0 && fabs(apo) > a.tol * sqrt(app * aoo)) {
+                    if (apo != 0.0 && fabs(apo) > tin * sqrt(app * aoo)) {
                         rot2(app, aoo, apo, cs, sn);
                         on = true;
                     }
@@ -275,7 +300,10 @@ __device__ void eig_pair(const BJArgs& a, int q, double* smem) {
                 }
                 __syncwarp();
             }
-            if (lane == 0) rot_total += rotated;
+            if (lane == 0) {
+                rot_total += rotated;
+                ++sweeps_total;
+            }
             if (rotated == 0) break;
         }
     }
@@ -303,6 +331,7 @@ __device__ void eig_pair(const BJArgs& a, int q, double* smem) {
         a.flag[q] = 1;
         atomicAdd(a.stats, 1);
         atomicAdd(a.stats + 1, rot_total);
+        atomicAdd(a.stats + 3, sweeps_total);
     }
     __threadfence();
 }
@@ -348,7 +377,7 @@ __device__ void update_unit(const BJArgs& a, int q, int ch, double* smem, const 
                 xs[j * XS + i] = acc[ni][v];
             }
         __syncthreads();
-#pragma unroll 4
+#pragma unroll
         for (int e = threadIdx.x; e < SUB * PW; e += NTH) {
             const int i = e & (SUB - 1), j = e / SUB;
             const int64_t gi = r + i;
@@ -449,8 +478,8 @@ int bjacobi_converge(Ctx& c, int64_t m, int64_t n, double* U, double tol) {
     const int grid = std::min(units, max_grid);
     DBuf gws = dalloc(c, size_t(per) * size_t(nch) * PW * PW);
     DBuf qws = dalloc(c, size_t(per) * PW * PW);
-    DBuf ints(c, sizeof(int) * size_t(2 * per + 3));
-    HYDOT_CUDA(cudaMemsetAsync(ints.as<void>(), 0, sizeof(int) * size_t(2 * per + 3), c.stream));
+    DBuf ints(c, sizeof(int) * size_t(2 * per + 4));
+    HYDOT_CUDA(cudaMemsetAsync(ints.as<void>(), 0, sizeof(int) * size_t(2 * per + 4), c.stream));
     BJArgs a;
     a.m = m;
     a.n = int(n);
@@ -471,17 +500,18 @@ int bjacobi_converge(Ctx& c, int64_t m, int64_t n, double* U, double tol) {
     a.stats = ints.as<int>() + 2 * per;
     int sweeps = 0;
     for (; sweeps < kMaxBSweeps; ++sweeps) {
-        HYDOT_CUDA(cudaMemsetAsync(a.stats, 0, 3 * sizeof(int), c.stream));
+        HYDOT_CUDA(cudaMemsetAsync(a.stats, 0, 4 * sizeof(int), c.stream));
         void* args[] = {&a};
         c.coop_launch((void*)bjacobi_sweep_k, dim3(grid), dim3(NTH), args, 0);
         c.count();
-        int st[3] = {0, 0, 0};
+        int st[4] = {0, 0, 0, 0};
         HYDOT_CUDA(cudaMemcpyAsync(st, a.stats, sizeof st, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
         if (bj_stats())
             fprintf(stderr,
-                    "[bjacobi] m=%lld n=%lld sweep=%d pairs_rotated=%d inner_rotations=%d (of %d pairs) nonfinite=%d\n",
-                    (long long)m, (long long)n, sweeps, st[0], st[1], per * rounds, st[2]);
+                    "[bjacobi] m=%lld n=%lld sweep=%d pairs_rotated=%d inner_rotations=%d inner_sweeps=%d (of %d "
+                    "pairs) nonfinite=%d\n",
+                    (long long)m, (long long)n, sweeps, st[0], st[1], st[3], per * rounds, st[2]);
         if (st[2] > 0) throw std::runtime_error("block Jacobi: non-finite column Gram (input not finite?)");
         if (st[0] == 0) break;
     }
