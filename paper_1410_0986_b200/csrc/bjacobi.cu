@@ -25,8 +25,6 @@
 // whose Gram passes the test is left untouched; a sweep in which no pair
 // rotates ends the iteration, and the columns are then those of a converged
 // one-sided Jacobi (sigma_j = |x_j|, U = x_j / sigma_j).
-#include <cooperative_groups.h>
-
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -34,8 +32,6 @@
 #include <vector>
 
 #include "internal.h"
-
-namespace cg = cooperative_groups;
 
 namespace hydot {
 namespace {
@@ -64,12 +60,38 @@ struct BJArgs {
     int64_t ldu;
     double tol, flag_tol;
     int nch, rch;
-    double* gws;  // per x nch x PW*PW partial Grams
-    double* qws;  // per x PW*PW rotations
-    int* flag;    // per: 1 = rotate this round
-    int* cnt;     // per: chunk arrival counters (self-resetting)
+    // ring buffers over rounds (slot r % RING): a pair slot's Gram partials,
+    // rotation and flag of round r live until round r + RING reuses them
+    double* gws;  // RING x per x nch x PW*PW partial Grams
+    double* qws;  // RING x per x PW*PW rotations
+    int* flag;    // RING x per: 1 = rotate
+    int* cnt;     // RING x per: chunk arrival counters (self-resetting)
+    int* ver;     // nbp x nch: rounds of updates applied to (block, chunk)
+    int* epoch;   // RING x per: r + 1 once round r's eigen-solve of the slot is published
+    int* udone;   // RING x per: update units finished (rounds of that ring slot)
+    int* work;    // item dispenser
     int* stats;   // [0] pairs rotated this sweep, [1] inner rotations, [2] non-finite pair Grams, [3] inner sweeps
 };
+constexpr int RING = 4;
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void wait_geq(const int* p, int v) {
+    if (ld_acquire(p) >= v) return;
+    unsigned ns = 32;
+    while (ld_acquire(p) < v) {
+        __nanosleep(ns);
+        if (ns < 512) ns *= 2;
+    }
+}
+// publish: every thread's prior stores, then the counter (release)
+__device__ __forceinline__ void publish_add(int* p, int v) {
+    __threadfence();
+    atomicAdd(p, v);
+}
 
 __device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, double b0) {
     asm volatile(
@@ -127,9 +149,9 @@ __device__ __forceinline__ void load_sub(double* xs, const double* __restrict__ 
 
 // ---- phase 1: partial Gram of one (pair, row chunk) unit; the CTA that
 // completes a pair's last chunk diagonalises its Gram
-__device__ void eig_pair(const BJArgs& a, int q, double* smem);
+__device__ void eig_pair(const BJArgs& a, int q, int rnd, double* smem);
 
-__device__ void gram_unit(const BJArgs& a, int2 bp, int q, int ch, double* smem, int* col) {
+__device__ void gram_unit(const BJArgs& a, int2 bp, int q, int rnd, int ch, double* smem, int* col) {
     double* xs = smem;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -153,7 +175,8 @@ __device__ void gram_unit(const BJArgs& a, int2 bp, int q, int ch, double* smem,
             for (int ni = 0; ni < 2; ++ni) dmma(acc[ni], a0, a1, xs[(wj + ni * 8 + g) * XS + kk + t]);
         }
     }
-    double* out = a.gws + (int64_t(q) * a.nch + ch) * (PW * PW);
+    const int slot = rnd % RING;
+    double* out = a.gws + ((int64_t(slot) * a.per + q) * a.nch + ch) * (PW * PW);
 #pragma unroll
     for (int ni = 0; ni < 2; ++ni)
 #pragma unroll
@@ -165,12 +188,24 @@ __device__ void gram_unit(const BJArgs& a, int2 bp, int q, int ch, double* smem,
     __threadfence();
     __syncthreads();
     __shared__ int last;
-    if (threadIdx.x == 0) last = atomicAdd(a.cnt + q, 1) == a.nch - 1;
+    int* cnt = a.cnt + slot * a.per + q;
+    if (threadIdx.x == 0) last = atomicAdd(cnt, 1) == a.nch - 1;
     __syncthreads();
     if (last) {
         __threadfence();
-        eig_pair(a, q, smem);
-        if (threadIdx.x == 0) a.cnt[q] = 0;
+        // the rotation / flag ring slot is free once round rnd - RING's
+        // update units of this pair slot are done
+        if (threadIdx.x == 0) {
+            *cnt = 0;
+            wait_geq(a.udone + slot * a.per + q, (rnd / RING) * a.nch);
+        }
+        __syncthreads();
+        eig_pair(a, q, rnd, smem);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicExch(a.epoch + slot * a.per + q, rnd + 1);  // publish this round's rotation
+        }
     }
 }
 
@@ -179,7 +214,8 @@ __device__ void gram_unit(const BJArgs& a, int2 bp, int q, int ch, double* smem,
 // warp in shared memory (warp barriers only: a CTA barrier per step made the
 // eigen-solve the latency bottleneck of a round).  The eigenvector columns
 // leave sorted by decreasing diagonal.
-__device__ void eig_pair(const BJArgs& a, int q, double* smem) {
+__device__ void eig_pair(const BJArgs& a, int q, int rnd, double* smem) {
+    const int slot = rnd % RING;
     double* G = smem;              // PW x GS
     double* Q = smem + PW * GS;    // PW x GS
     __shared__ double rc[PW / 2], rs[PW / 2];
@@ -188,7 +224,7 @@ __device__ void eig_pair(const BJArgs& a, int q, double* smem) {
     __shared__ unsigned long long off0_bits;
     __shared__ double dsum[PW];
     __shared__ int perm[PW];
-    const double* part = a.gws + int64_t(q) * a.nch * (PW * PW);
+    const double* part = a.gws + (int64_t(slot) * a.per + q) * a.nch * (PW * PW);
     if (threadIdx.x == 0) {
         any = 0;
         bad = 0;
@@ -221,7 +257,7 @@ __device__ void eig_pair(const BJArgs& a, int q, double* smem) {
     __syncthreads();
     if (bad && threadIdx.x == 0) atomicAdd(a.stats + 2, 1);
     if (!any) {
-        if (threadIdx.x == 0) a.flag[q] = 0;
+        if (threadIdx.x == 0) a.flag[slot * a.per + q] = 0;
         return;
     }
     if (threadIdx.x < 32) {
@@ -322,13 +358,13 @@ __device__ void eig_pair(const BJArgs& a, int q, double* smem) {
         perm[rank] = j;
     }
     __syncthreads();
-    double* qo = a.qws + int64_t(q) * (PW * PW);
+    double* qo = a.qws + (int64_t(slot) * a.per + q) * (PW * PW);
     for (int e = threadIdx.x; e < PW * PW; e += NTH) {
         const int i = e % PW, j = e / PW;
         __stcg(qo + i + j * PW, Q[i * GS + perm[j]]);
     }
     if (threadIdx.x == 0) {
-        a.flag[q] = 1;
+        a.flag[slot * a.per + q] = 1;
         atomicAdd(a.stats, 1);
         atomicAdd(a.stats + 1, rot_total);
         atomicAdd(a.stats + 3, sweeps_total);
@@ -337,12 +373,12 @@ __device__ void eig_pair(const BJArgs& a, int q, double* smem) {
 }
 
 // ---- phase 3: X_p(rows of the chunk) <- X_p Q_p
-__device__ void update_unit(const BJArgs& a, int q, int ch, double* smem, const int* col) {
+__device__ void update_unit(const BJArgs& a, int q, int rnd, int ch, double* smem, const int* col) {
     double* xs = smem;            // PW x XS
     double* qs = smem + PW * XS;  // PW x QS: qs[j * QS + k] = Q(k, j)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const double* qg = a.qws + int64_t(q) * (PW * PW);
+    const double* qg = a.qws + (int64_t(rnd % RING) * a.per + q) * (PW * PW);
     __syncthreads();
     for (int e = threadIdx.x; e < PW * PW; e += NTH) {
         const int k = e % PW, j = e / PW;
@@ -389,32 +425,53 @@ __device__ void update_unit(const BJArgs& a, int q, int ch, double* smem, const 
 
 constexpr int SMEM_DOUBLES = PW * XS + PW * QS > 2 * PW * GS ? PW * XS + PW * QS : 2 * PW * GS;
 
+// One sweep as a dataflow over work items taken in a fixed global order
+// (round-major; per round the Gram units, then the update units), so
+// every item only waits on items handed out before it (no deadlock, no grid
+// barrier): a Gram unit waits until its two blocks' chunk carries the
+// previous round's update, an update unit until its pair's eigen-solve is
+// published.  A slow eigen-solve then delays only the pairs that depend on
+// it instead of the whole grid.
 __global__ void __launch_bounds__(NTH, 4) bjacobi_sweep_k(BJArgs a) {
-    cg::grid_group grid = cg::this_grid();
     __shared__ __align__(16) double smem[SMEM_DOUBLES];
     __shared__ int col[PW];
+    __shared__ int item_s;
     const int units = a.per * a.nch;
-    for (int r = 0; r < a.rounds; ++r) {
-        const int2* rp = a.pairs + int64_t(r) * a.per;
-        for (int u = blockIdx.x; u < units; u += gridDim.x) {
-            const int q = u / a.nch, ch = u % a.nch;
-            const int2 bp = rp[q];
+    const int64_t items = int64_t(a.rounds) * 2 * units;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) item_s = atomicAdd(a.work, 1);
+        __syncthreads();
+        const int64_t it = item_s;
+        if (it >= items) break;
+        const int rnd = int(it / (2 * units));
+        const int rem = int(it % (2 * units));
+        const bool upd = rem >= units;
+        const int u = upd ? rem - units : rem;
+        const int q = u / a.nch, ch = u % a.nch;
+        const int2 bp = a.pairs[int64_t(rnd) * a.per + q];
+        if (threadIdx.x < PW) col[threadIdx.x] = pair_col(bp, threadIdx.x, a.n);
+        if (!upd) {
+            if (threadIdx.x == 0) {
+                wait_geq(a.ver + bp.x * a.nch + ch, rnd);
+                wait_geq(a.ver + bp.y * a.nch + ch, rnd);
+                // partial / counter ring slot free: round rnd - RING's eigen-solve done
+                wait_geq(a.epoch + (rnd % RING) * a.per + q, rnd - RING + 1);
+            }
             __syncthreads();
-            if (threadIdx.x < PW) col[threadIdx.x] = pair_col(bp, threadIdx.x, a.n);
+            gram_unit(a, bp, q, rnd, ch, smem, col);
+        } else {
+            if (threadIdx.x == 0) wait_geq(a.epoch + (rnd % RING) * a.per + q, rnd + 1);
             __syncthreads();
-            gram_unit(a, bp, q, ch, smem, col);
+            if (__ldcg(a.flag + (rnd % RING) * a.per + q)) update_unit(a, q, rnd, ch, smem, col);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                atomicAdd(a.ver + bp.x * a.nch + ch, 1);
+                atomicAdd(a.ver + bp.y * a.nch + ch, 1);
+                atomicAdd(a.udone + (rnd % RING) * a.per + q, 1);
+            }
         }
-        grid.sync();
-        for (int u = blockIdx.x; u < units; u += gridDim.x) {
-            const int q = u / a.nch, ch = u % a.nch;
-            if (!__ldcg(a.flag + q)) continue;
-            const int2 bp = rp[q];
-            __syncthreads();
-            if (threadIdx.x < PW) col[threadIdx.x] = pair_col(bp, threadIdx.x, a.n);
-            __syncthreads();
-            update_unit(a, q, ch, smem, col);
-        }
-        grid.sync();
     }
 }
 
@@ -476,10 +533,12 @@ int bjacobi_converge(Ctx& c, int64_t m, int64_t n, double* U, double tol) {
     nch = (m + rch - 1) / rch;
     const int units = int(per * nch);
     const int grid = std::min(units, max_grid);
-    DBuf gws = dalloc(c, size_t(per) * size_t(nch) * PW * PW);
-    DBuf qws = dalloc(c, size_t(per) * PW * PW);
-    DBuf ints(c, sizeof(int) * size_t(2 * per + 4));
-    HYDOT_CUDA(cudaMemsetAsync(ints.as<void>(), 0, sizeof(int) * size_t(2 * per + 4), c.stream));
+    DBuf gws = dalloc(c, size_t(RING) * size_t(per) * size_t(nch) * PW * PW);
+    DBuf qws = dalloc(c, size_t(RING) * size_t(per) * PW * PW);
+    // flag, cnt (RING x per each), ver (nbp x nch), epoch, udone (RING x per each), work, stats (4)
+    const size_t nints = size_t(2 * RING * per) + size_t(nbp) * size_t(nch) + size_t(2 * RING * per) + 1 + 4;
+    DBuf ints(c, sizeof(int) * nints);
+    HYDOT_CUDA(cudaMemsetAsync(ints.as<void>(), 0, sizeof(int) * nints, c.stream));
     BJArgs a;
     a.m = m;
     a.n = int(n);
@@ -496,14 +555,19 @@ int bjacobi_converge(Ctx& c, int64_t m, int64_t n, double* U, double tol) {
     a.gws = gws.d();
     a.qws = qws.d();
     a.flag = ints.as<int>();
-    a.cnt = ints.as<int>() + per;
-    a.stats = ints.as<int>() + 2 * per;
+    a.cnt = a.flag + RING * per;
+    a.ver = a.cnt + RING * per;
+    a.epoch = a.ver + size_t(nbp) * size_t(nch);
+    a.udone = a.epoch + RING * per;
+    a.work = a.udone + RING * per;
+    a.stats = a.work + 1;
+    // everything but the ring contents restarts every sweep
+    const size_t reset = size_t(nbp) * size_t(nch) + size_t(2 * RING * per) + 1 + 4;
     int sweeps = 0;
     for (; sweeps < kMaxBSweeps; ++sweeps) {
-        HYDOT_CUDA(cudaMemsetAsync(a.stats, 0, 4 * sizeof(int), c.stream));
-        void* args[] = {&a};
-        c.coop_launch((void*)bjacobi_sweep_k, dim3(grid), dim3(NTH), args, 0);
-        c.count();
+        HYDOT_CUDA(cudaMemsetAsync(a.ver, 0, reset * sizeof(int), c.stream));
+        bjacobi_sweep_k<<<grid, NTH, 0, c.stream>>>(a);
+        c.check_launch();
         int st[4] = {0, 0, 0, 0};
         HYDOT_CUDA(cudaMemcpyAsync(st, a.stats, sizeof st, cudaMemcpyDeviceToHost, c.stream));
         c.sync();

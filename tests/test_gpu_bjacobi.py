@@ -48,10 +48,13 @@ def test_block_jacobi_core_matches_oracle(ctx, oracle, m, n, decades, clusters):
     Dg = (fg.U @ fg.V.T).cpu().numpy()
     nA = np.linalg.norm(A)
     assert np.linalg.norm(Dg - fo.dense()) <= 1e-8 * nA
-    # the factor's U columns are orthonormal (converged one-sided Jacobi)
-    U = fg.U
+    # the factor's leading U columns are orthonormal (the lazy-V recovery
+    # V = X^T W S^-2 carries eps ||X|| / s_j per column: only columns with
+    # s_j well above eps s_1 are orthonormal to working precision)
+    k = int(np.sum(sg > 1e-6 * sg[0]))
+    U = fg.U[:, :k]
     G = U.T @ U
-    assert float(torch.max(torch.abs(G - torch.eye(G.shape[0], dtype=G.dtype, device=G.device)))) <= 1e-10
+    assert float(torch.max(torch.abs(G - torch.eye(k, dtype=G.dtype, device=G.device)))) <= 1e-9
 
 
 def test_block_jacobi_thin_svd_square(ctx):
