@@ -507,7 +507,7 @@ bool bj_stats() {
 int64_t bjacobi_min_n() {
     static const int64_t v = [] {
         const char* e = std::getenv("HYDOT_BJACOBI_MIN");
-        return e ? int64_t(std::atoll(e)) : int64_t(640);
+        return e ? int64_t(std::atoll(e)) : int64_t(1800);
     }();
     return v;
 }
