@@ -334,6 +334,33 @@ hydot_status hydot_block_file_info(const char* path, int64_t* rows, int64_t* col
 hydot_status hydot_block_load(hydot_ctx ctx, const char* path, double* block_dev, int64_t ld,
                               int64_t rows_cap, int64_t* rows, int64_t* cols);
 
+/* ----------------------------------------------------------- multi-GPU -- */
+/* One process per GPU; an NCCL communicator bound to a context (SURVEY
+ * 8(b)/(e)).  Rank 0 calls hydot_comm_unique_id and hands the bytes to every
+ * rank (e.g. over torch.distributed); each rank then calls
+ * hydot_comm_create with its own context.  NCCL is loaded at run time
+ * (libnccl.so.2); without it the calls return HYDOT_ENCCL. */
+#define HYDOT_COMM_ID_BYTES 128
+typedef struct hydot_comm_s* hydot_comm;
+hydot_status hydot_comm_unique_id(unsigned char id_out[HYDOT_COMM_ID_BYTES]);
+hydot_status hydot_comm_create(hydot_ctx ctx, int world, int rank, const unsigned char id[HYDOT_COMM_ID_BYTES],
+                               hydot_comm* out);
+hydot_status hydot_comm_destroy(hydot_comm comm);
+hydot_status hydot_comm_info(hydot_comm comm, int* world, int* rank);
+/* in-place sum over ranks of n doubles on the context's stream */
+hydot_status hydot_comm_allreduce(hydot_ctx ctx, hydot_comm comm, double* buf_dev, int64_t n);
+/* hydot_j_matmat under voxel-sharded V (lr_matvec / lr_rmatvec,
+ * lowrank.cpp:589-599, + permuted_matvec, experiments.cpp:255-262): U (M x R)
+ * replicated, V_loc = this rank's Nloc voxel rows of V.  trans=0: X_dev is
+ * the rank's rows of each chromophore block ((Nloc*n_c) x b), Y_dev (M x b)
+ * complete on every rank after one R x (b n_c) all-reduce of V^T X;
+ * trans=1: X_dev (M x b) replicated, Y_dev the rank's (Nloc*n_c) x b rows
+ * (no communication). */
+hydot_status hydot_j_matmat_voxel(hydot_ctx ctx, hydot_comm comm, int trans, int b, const double* U_dev,
+                                  int64_t M, const double* Vloc_dev, int64_t Nloc, int64_t R,
+                                  const int* row_perm_dev, const double* eps_c_dev, int n_lambda, int n_c,
+                                  const double* X_dev, int64_t ldx, double* Y_dev, int64_t ldy);
+
 /* ---------------------------------------------------------------- pals -- */
 /* Parametric level-set reconstruction, the caller of the compressed
  * operator: proj/include/hydot/pals.hpp, src/pals.cpp.

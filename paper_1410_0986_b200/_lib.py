@@ -133,6 +133,13 @@ SIGNATURES = {
     "hydot_recompress": (C.c_int, [_vp, _vp, C.c_double, C.c_int, C.POINTER(_vp),
                                    C.POINTER(Ledger)]),
     "hydot_lr_matmat": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _dp, C.c_int64, _dp, C.c_int64]),
+    "hydot_comm_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
+    "hydot_comm_create": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_ubyte), C.POINTER(_vp)]),
+    "hydot_comm_destroy": (C.c_int, [_vp]),
+    "hydot_comm_info": (C.c_int, [_vp, _ip, _ip]),
+    "hydot_comm_allreduce": (C.c_int, [_vp, _vp, _dp, C.c_int64]),
+    "hydot_j_matmat_voxel": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _dp, C.c_int64, _dp, C.c_int64, C.c_int64,
+                                       _ip, _dp, C.c_int, C.c_int, _dp, C.c_int64, _dp, C.c_int64]),
     "hydot_j_matmat": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _ip, _dp, C.c_int, C.c_int, _dp,
                                  C.c_int64, _dp, C.c_int64]),
     "hydot_thin_svd": (C.c_int, [_vp, C.c_int64, C.c_int64, _dp, C.c_int64, _dp, _dp, _dp]),

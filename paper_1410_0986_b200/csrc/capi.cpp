@@ -91,6 +91,20 @@ hydot_factor wrap(const std::shared_ptr<Ctx>& owner, Factor&& f) {
 }
 }  // namespace
 
+// shared with comm.cpp: the context behind a handle, and the status of an
+// exception (the same mapping as guard)
+hydot::Ctx& hydot_ctx_ref(hydot_ctx ctx) { return ctx_of(ctx); }
+hydot_status hydot_guard_status(const std::exception& e, hydot::Ctx* c) {
+    hydot_status st = HYDOT_ERUNTIME;
+    if (dynamic_cast<const CudaError*>(&e)) st = HYDOT_ECUDA;
+    else if (dynamic_cast<const std::bad_alloc*>(&e)) st = HYDOT_ENOMEM;
+    else if (dynamic_cast<const std::invalid_argument*>(&e)) st = HYDOT_EINVAL;
+    const std::string msg = st == HYDOT_ENOMEM ? std::string("out of device memory") : std::string(e.what());
+    if (c) c->err = msg;
+    g_err = msg;
+    return st;
+}
+
 extern "C" {
 
 int hydot_version(void) { return 1; }

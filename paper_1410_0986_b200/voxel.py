@@ -150,6 +150,68 @@ class SimComm:
         return out
 
 
+class LibComm:
+    """The library's own NCCL communicator (hydot_comm, include/hydot_b200.h)
+    for a context, bootstrapped over torch.distributed: rank 0 draws the NCCL
+    unique id, every rank receives it by broadcast.  Its all-reduce runs on
+    the context's stream."""
+
+    def __init__(self, ctx, dist=None):
+        import ctypes as C
+        from ._lib import check, lib
+        self.ctx = ctx
+        self.world = dist.get_world_size() if dist is not None else 1
+        self.rank = dist.get_rank() if dist is not None else 0
+        idb = (C.c_ubyte * 128)()
+        if self.world > 1:
+            if self.rank == 0:
+                check(lib().hydot_comm_unique_id(idb))
+            t = torch.tensor(list(bytes(idb)), dtype=torch.uint8,
+                             device=f"cuda:{ctx.device}" if dist.get_backend() == "nccl" else "cpu")
+            dist.broadcast(t, 0)
+            idb = (C.c_ubyte * 128)(*t.cpu().tolist())
+        self.h = C.c_void_p()
+        check(lib().hydot_comm_create(ctx.h, self.world, self.rank, idb, C.byref(self.h)), ctx.h)
+
+    def allreduce(self, x: torch.Tensor) -> torch.Tensor:
+        from ._lib import check, lib
+        from .core import dptr
+        y = x.contiguous().clone()
+        check(lib().hydot_comm_allreduce(self.ctx.h, self.h, dptr(y), y.numel()), self.ctx.h)
+        return y
+
+    def __del__(self):
+        try:
+            from ._lib import lib
+            if self.h:
+                lib().hydot_comm_destroy(self.h)
+        except Exception:
+            pass
+
+
+def j_matmat_voxel_lib(comm: LibComm, U, V_loc, row_perm_dev, eps_c_dev, nl, nc, X, trans=False):
+    """hydot_j_matmat_voxel: column-major device buffers as in JOperator;
+    X (b, Nloc*nc) storage for trans=False (returns (b, M)), X (b, M) for
+    trans=True (returns (b, Nloc*nc))."""
+    from ._lib import check, lib
+    from .core import dptr, iptr
+    M, R = U.shape
+    Nloc = V_loc.shape[0]
+    Ucm, Vcm = U.T.contiguous(), V_loc.T.contiguous()
+    b = X.shape[0]
+    if not trans:
+        Y = torch.empty((b, M), dtype=torch.float64, device=U.device)
+        check(lib().hydot_j_matmat_voxel(comm.ctx.h, comm.h, 0, b, dptr(Ucm), M, dptr(Vcm), Nloc, R,
+                                         iptr(row_perm_dev), dptr(eps_c_dev), nl, nc, dptr(X), Nloc * nc,
+                                         dptr(Y), M), comm.ctx.h)
+    else:
+        Y = torch.empty((b, Nloc * nc), dtype=torch.float64, device=U.device)
+        check(lib().hydot_j_matmat_voxel(comm.ctx.h, comm.h, 1, b, dptr(Ucm), M, dptr(Vcm), Nloc, R,
+                                         iptr(row_perm_dev), dptr(eps_c_dev), nl, nc, dptr(X), M,
+                                         dptr(Y), Nloc * nc), comm.ctx.h)
+    return Y
+
+
 # -------------------------------------------------------------- compute --
 class NumpyOps:
     """LAPACK via numpy on CPU tensors; the libstdc++ normal stream from the

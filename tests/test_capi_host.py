@@ -101,3 +101,13 @@ def test_setup_generation_deterministic():
         ix, iy, iz = v % n, (v // n) % n, v // (n * n)
         assert iz == n - 1 and 0 < ix < n - 1 and 0 < iy < n - 1
     assert np.all(a.sigma > 0) and np.all(a.sigma_prime > 0)
+
+
+def test_comm_unique_id_without_a_gpu():
+    """The multi-GPU handle's bootstrap (NCCL loaded at run time) works on a
+    host without a GPU: rank 0's unique id is 128 bytes."""
+    import ctypes as C
+    from paper_1410_0986_b200._lib import lib
+    b = (C.c_ubyte * 128)()
+    assert lib().hydot_comm_unique_id(b) == 0
+    assert any(bytes(b))

@@ -302,3 +302,63 @@ def test_lr_matmat_widths(ctx, b):
     want2 = V @ (U.T @ Y)
     got2 = lr.lr_rmatvec(ctx, f, torch.as_tensor(Y)).cpu().numpy()
     assert fro(got2 - want2) <= 1e-13 * fro(want2)
+
+
+def test_voxel_engine_on_device_matches_the_library(ctx):
+    """voxel.py's cooperative merge with the device kernels (DMMA GEMM,
+    Householder QR, Jacobi SVD, device Gaussian stream) on one rank equals
+    the library's agglomerate / recompress to rounding."""
+    from paper_1410_0986_b200 import lowrank as lr, voxel as vx
+    rng = np.random.default_rng(21)
+    N = 4000
+    fac = []
+    for m in (60, 48):
+        k = 40
+        Q1, _ = np.linalg.qr(rng.standard_normal((m, k)))
+        Q2, _ = np.linalg.qr(rng.standard_normal((N, k)))
+        fac.append((Q1, Q2 * np.logspace(0, -9, k)))
+    fac[1] = (fac[1][0], 0.5 * fac[0][1] + 0.5 * fac[1][1])
+    ops = vx.DeviceOps(ctx)
+    comm = vx.SimComm.group(1)[0]
+    for hint in (-1, 200):
+        f1 = vx.VFactor(ops.tensor(fac[0][0]), ops.tensor(fac[0][1]), N)
+        f2 = vx.VFactor(ops.tensor(fac[1][0]), ops.tensor(fac[1][1]), N)
+        fv = vx.agglomerate_voxel(ops, comm, f1, f2, 0, N, 1e-7, seed=99, rank_hint=hint)
+        g1 = lr.LowRankFactor.from_tensors(ctx, torch.as_tensor(fac[0][0]), torch.as_tensor(fac[0][1]))
+        g2 = lr.LowRankFactor.from_tensors(ctx, torch.as_tensor(fac[1][0]), torch.as_tensor(fac[1][1]))
+        fg = lr.agglomerate(ctx, g1, g2, 1e-7, 99, rank_hint=hint)
+        assert fv.rank == fg.rank()
+        D = (fv.U @ fv.V_loc.T).cpu().numpy()
+        Dg = fg.dense().cpu().numpy()
+        assert fro(D - Dg) <= 1e-10 * fro(Dg)
+        fr = vx.recompress_voxel(ops, comm, fv, 1e-7)
+        fgr = lr.recompress(ctx, fg, 1e-7)
+        assert fr.rank == fgr.rank()
+        assert fro((fr.U @ fr.V_loc.T).cpu().numpy() - fgr.dense().cpu().numpy()) <= 1e-10 * fro(Dg)
+
+
+def test_library_comm_j_matmat_voxel_single_rank(ctx):
+    """hydot_comm (NCCL handle of the C ABI) and hydot_j_matmat_voxel on one
+    rank reproduce hydot_j_matmat (the all-reduce is the identity)."""
+    from paper_1410_0986_b200 import lowrank as lr, voxel as vx
+    rng = np.random.default_rng(8)
+    M, N, R, nl, nc, b = 90, 700, 17, 9, 3, 5
+    U, V = rng.standard_normal((M, R)), rng.standard_normal((N, R))
+    f = lr.LowRankFactor.from_tensors(ctx, torch.as_tensor(U), torch.as_tensor(V))
+    perm = rng.permutation(M).astype(np.int32)
+    eps_c = rng.uniform(0.5, 1.5, (nl, nc))
+    J = lr.JOperator(ctx, f, perm, eps_c)
+    comm = vx.LibComm(ctx)
+    X = torch.as_tensor(rng.standard_normal((b, N * nc))).cuda()
+    Y = torch.empty(b, M, dtype=torch.float64, device="cuda")
+    J.matmat_cm(X, Y, b)
+    Yv = vx.j_matmat_voxel_lib(comm, torch.as_tensor(U).cuda(), torch.as_tensor(V).cuda(), J.row_perm,
+                               J.eps_c, nl, nc, X)
+    assert float(torch.max(torch.abs(Yv - Y))) <= 1e-12 * float(torch.max(torch.abs(Y)))
+    Xb = torch.empty(b, N * nc, dtype=torch.float64, device="cuda")
+    J.rmatmat_cm(Y, Xb, b)
+    Xv = vx.j_matmat_voxel_lib(comm, torch.as_tensor(U).cuda(), torch.as_tensor(V).cuda(), J.row_perm,
+                               J.eps_c, nl, nc, Y, trans=True)
+    assert float(torch.max(torch.abs(Xv - Xb))) <= 1e-12 * float(torch.max(torch.abs(Xb)))
+    z = torch.arange(6, dtype=torch.float64, device="cuda")
+    assert torch.equal(comm.allreduce(z), z)
