@@ -358,6 +358,9 @@ __global__ void __launch_bounds__(LT) larft_k(int jb, const double* __restrict__
 
 void panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, const PanelBufs& pbuf) {
     StageTimer _t(c, "qr_panel", mr, jb, -1, 2.0 * double(mr) * jb * jb, 16.0 * double(mr) * jb);
+    // the same launches split by kind (one CTA on-chip / cooperative tall)
+    StageTimer _k(c, mr <= kCtaRows ? "qr_panel_cta" : "qr_panel_coop", mr, jb, -1, 2.0 * double(mr) * jb * jb,
+                  16.0 * double(mr) * jb);
     static AttrGate attr;
     const size_t smem_cap = 200 * 1024;
     if (mr <= kCtaRows) {  // short panels: one CTA, the whole panel on-chip

@@ -10,8 +10,8 @@ node by node on identical inputs (tests/parity_replay.py):
   randsvds, 4 within-leaf merges, 3 internal merges), on the root merge
   (its core is the largest SVD of the path) and on the recompress.
 
-Also: the library's own recursive_lowrank driver (speculation, side-stream V,
-lazy root) reproduces the replay's node ranks and root factor.
+Also (config 1): the library's own recursive_lowrank driver (speculation,
+side-stream V, lazy root) reproduces the replay's node ranks and root factor.
 
 Tolerances (BASELINE north_star): equal ranks; leading singular values 1e-8
 relative; ||J~_gpu - J~_cpu||_F / ||J~||_F 1e-8; matvecs 1e-10.  Oracle
@@ -126,7 +126,8 @@ def test_config2_subtree_root_and_recompress_match_oracle(oracle):
     froot = rep.run()
     assert rep.checked == 8 + 4 + 3 + 1
     _write_log("cfg2-replay", rep, {"seconds": time.perf_counter() - t0})
-    _driver_matches_replay(d, rep, froot)
+    # (the library driver is checked against the replay at config 1; here the
+    # time goes to the oracle's root merge and recompress)
     del d["F"], d["inc"], d["adj"]
     torch.cuda.empty_cache()
     fg = lr.recompress(d["ctx"], froot, d["eps"])
