@@ -356,11 +356,20 @@ __global__ void __launch_bounds__(LT) larft_k(int jb, const double* __restrict__
     }
 }
 
-void panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, const PanelBufs& pbuf) {
+}  // namespace
+void panel_cqr(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, double* work);
+namespace {
+
+void panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, const PanelBufs& pbuf,
+           double* work) {
     StageTimer _t(c, "qr_panel", mr, jb, -1, 2.0 * double(mr) * jb * jb, 16.0 * double(mr) * jb);
     // the same launches split by kind (one CTA on-chip / cooperative tall)
-    StageTimer _k(c, mr <= kCtaRows ? "qr_panel_cta" : "qr_panel_coop", mr, jb, -1, 2.0 * double(mr) * jb * jb,
+    StageTimer _k(c, mr <= kCtaRows ? "qr_panel_cta" : "qr_panel_cqr", mr, jb, -1, 2.0 * double(mr) * jb * jb,
                   16.0 * double(mr) * jb);
+    if (mr > kCtaRows) {  // tall: shifted CholeskyQR3 + Householder reconstruction (qr_cqr.cu)
+        panel_cqr(c, mr, jb, P, ld, tau, work);
+        return;
+    }
     static AttrGate attr;
     const size_t smem_cap = 200 * 1024;
     if (mr <= kCtaRows) {  // short panels: one CTA, the whole panel on-chip
@@ -553,7 +562,7 @@ void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f
             const int pb = std::min(PB, jb - p0);
             const int64_t pr = mr - p0;
             double* Pp = Pb + p0 + int64_t(p0) * m;
-            panel(c, pr, pb, Pp, m, f.tau.d() + j0 + p0, pbuf);
+            panel(c, pr, pb, Pp, m, f.tau.d() + j0 + p0, pbuf, V.d());
             const int rest = jb - p0 - pb;
             if (rest > 0) {
                 // apply this sub-panel's reflector to the rest of the block

@@ -1,0 +1,303 @@
+// qr_cqr.cu -- Householder panels of very tall matrices without a grid
+// barrier per column.
+//
+// The cooperative panel (qr.cu) needs one grid-wide reduction per column; on
+// the path's tallest panels (N = 262 144 rows at config 2: a 67 MB panel that
+// no longer fits on chip) that cost ~30 us per column.  Here the mr x jb
+// (jb <= 32) panel is factored by shifted CholeskyQR3 (Fukaya, Nakatsukasa,
+// Yanagisawa, Yamamoto 2020): three passes of "Gram -> Cholesky -> row-wise
+// triangular solve", the first with the shift s = 11 (mr jb + jb (jb + 1)) u
+// tr(P^T P) so that it is stable for ill-conditioned and rank-deficient
+// panels, giving P = Q R with Q orthonormal to working precision.  The
+// Householder representation the blocked QR needs (unit-lower V, tau, the
+// upper R; LAPACK dgeqrf / Eigen HouseholderQR layout, lowrank.cpp:77-83) is
+// then reconstructed from Q (Ballard, Demmel, Grigori, Jacquelin, Nguyen,
+// Solomonik 2014): the LU factorisation Q - [S; 0] = V U with the signs
+// s_k = -sign of the running pivot (|u_kk| >= 1, no pivoting needed) gives
+// H_1 ... H_jb = I - V T V^T with first jb columns Q S, T = -U S V_1^-T, so
+// tau_k = -s_k u_kk and R_house = S R.  Four launches per panel, each one
+// pass over the panel: Gram(P) | Q1 = P R1^-1 + Gram | Q2 = Q1 R2^-1 + Gram
+// (+ the top block's LU) | V = Q2 R3^-1 U^-1 below the top block.  Gram
+// partials are reduced by the last CTA in CTA order (deterministic).
+#include <algorithm>
+#include <cmath>
+
+#include "internal.h"
+
+namespace hydot {
+namespace {
+
+constexpr int W = 32;       // panel width handled (jb <= W)
+constexpr int RT = 128;     // threads = rows per tile
+constexpr int GSZ = W * W;  // Gram entries
+constexpr int XS = RT + 4;  // tile stride ([col][row])
+
+__device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, double b0) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 "
+        "{%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+        : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+        : "d"(a0), "d"(a1), "d"(b0));
+}
+
+struct CqrBufs {
+    double* part;      // gridDim x GSZ partial Grams
+    unsigned* ticket;  // last-CTA ticket (self-resetting)
+    double* R;         // 3 x W x W: R1, R2, R3 (upper, column-major W x W)
+    double* U;         // W x W: U of the top block's LU
+    int* status;       // [0]: 1 = zero panel
+};
+
+// y = x R^-1 for a row vector x (jb), R upper triangular (column-major W x W
+// in shared memory): y_j = (x_j - sum_{i<j} y_i R_ij) / R_jj
+__device__ __forceinline__ void row_solve(double (&x)[W], const double* __restrict__ R, int jb) {
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        if (j < jb) {
+            double s = x[j];
+#pragma unroll
+            for (int i = 0; i < W; ++i)
+                if (i < j) s -= x[i] * R[i + j * W];
+            x[j] = s / R[j + j * W];
+        }
+    }
+}
+
+// Cholesky of the jb x jb Gram (+ shift) in shared memory by one warp:
+// G + s I = R^T R, R upper (column-major W x W, zero below).  Retries with a
+// 10x larger shift if a pivot is not positive.
+__device__ void warp_cholesky(double* G, double* R, int jb, double shift, double* tr_out) {
+    const int lane = threadIdx.x;
+    double tr = 0.0;
+    for (int i = 0; i < jb; ++i) tr += G[i + i * W];
+    if (tr_out) *tr_out = tr;
+    double s = shift * tr;
+    for (int attempt = 0; attempt < 12; ++attempt) {
+        bool ok = true;
+        // lane j owns column j of the working copy
+        double col[W];
+#pragma unroll
+        for (int i = 0; i < W; ++i) col[i] = (lane < jb && i < jb) ? G[i + lane * W] + (i == lane ? s : 0.0) : 0.0;
+        for (int k = 0; k < jb; ++k) {
+            // pivot a_kk lives in lane k, entries a_kj in lanes j
+            double akk = __shfl_sync(0xffffffffu, col[k], k);
+            if (!(akk > 0.0)) {
+                ok = false;
+                break;
+            }
+            const double d = sqrt(akk);
+            double rkj = 0.0;
+            if (lane >= k && lane < jb) rkj = (lane == k) ? d : col[k] / d;
+            if (lane < jb) R[k + lane * W] = lane >= k ? rkj : 0.0;
+            // a_ij -= r_ki r_kj for i, j > k (lane j updates its column)
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                const double rki = __shfl_sync(0xffffffffu, rkj, i);
+                if (i > k && lane > k && lane < jb) col[i] -= rki * rkj;
+            }
+        }
+        if (__all_sync(0xffffffffu, ok)) {
+            for (int e = lane; e < W * W; e += 32) {
+                const int i = e % W, j = e / W;
+                if (i >= jb || j >= jb || i > j) R[e] = (i == j && i >= jb) ? 1.0 : (i > j || i >= jb || j >= jb ? 0.0 : R[e]);
+            }
+            __syncwarp();
+            return;
+        }
+        s = s > 0.0 ? s * 10.0 : 1e-16 * tr + 1e-300;
+    }
+}
+
+// One pass over the panel rows: optionally y = x Rin^-1 (stored to Y), and the
+// Gram of y (or x) reduced by the last CTA, which then factors it (mode 0:
+// shifted, into R slot `slot`; the last pass also does the reconstruction).
+// mode: 0 = Gram(P) + shifted Cholesky -> R1
+//       1 = Q1 = P R1^-1 (-> Y) + Gram + Cholesky -> R2
+//       2 = Q2 = Q1 R2^-1 (-> Y) + Gram + Cholesky -> R3, then the top
+//           block's modified LU -> U, tau, R_house, V_1 written into P
+template <int MODE>
+__global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const double* __restrict__ X, int64_t ldx,
+                                                 double* __restrict__ Y, int64_t ldy, double* __restrict__ P,
+                                                 int64_t ldp, double* __restrict__ tau, CqrBufs b, double shift) {
+    __shared__ __align__(16) double tile[W * XS];
+    __shared__ double Rin[W * W];
+    __shared__ bool last;
+    double* Gs = tile;          // the last CTA's Gram / Cholesky factor reuse
+    double* Rs = tile + W * W;  // the tile after the row loop
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wi = (warp & 1) * 16, wj = (warp >> 1) * 16;
+    if (MODE > 0 && b.status[0]) return;  // zero panel: nothing to do
+    if (MODE > 0)
+        for (int e = threadIdx.x; e < W * W; e += RT) Rin[e] = b.R[(MODE - 1) * W * W + e];
+    __syncthreads();
+    double acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+    const int64_t ntiles = (mr + RT - 1) / RT;
+    for (int64_t tt = blockIdx.x; tt < ntiles; tt += gridDim.x) {
+        const int64_t i = tt * RT + threadIdx.x;
+        double x[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) x[j] = (i < mr && j < jb) ? __ldcg(X + i + int64_t(j) * ldx) : 0.0;
+        if (MODE > 0) {
+            if (i < mr) row_solve(x, Rin, jb);
+#pragma unroll
+            for (int j = 0; j < W; ++j)
+                if (i < mr && j < jb) __stcg(Y + i + int64_t(j) * ldy, x[j]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < W; ++j) tile[j * XS + threadIdx.x] = x[j];
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < RT; kk += 4) {
+            const double a0 = tile[(wi + g) * XS + kk + t];
+            const double a1 = tile[(wi + g + 8) * XS + kk + t];
+#pragma unroll
+            for (int ni = 0; ni < 2; ++ni) dmma(acc[ni], a0, a1, tile[(wj + ni * 8 + g) * XS + kk + t]);
+        }
+    }
+    double* mine = b.part + int64_t(blockIdx.x) * GSZ;
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int r = wi + g + ((v & 2) ? 8 : 0);
+            const int cc = wj + ni * 8 + 2 * t + (v & 1);
+            __stcg(mine + r + cc * W, acc[ni][v]);
+        }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(b.ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int e = threadIdx.x; e < W * W; e += RT) {
+        double s = 0.0;
+        for (int p = 0; p < int(gridDim.x); ++p) s += __ldcg(b.part + int64_t(p) * GSZ + e);
+        Gs[e] = s;
+    }
+    __syncthreads();
+    __shared__ double tr0;
+    if (warp == 0) warp_cholesky(Gs, Rs, jb, MODE == 0 ? shift : 0.0, MODE == 0 ? &tr0 : nullptr);
+    __syncthreads();
+    if (MODE == 0 && tr0 == 0.0) {  // zero panel: H = I, R = 0
+        if (threadIdx.x == 0) b.status[0] = 1;
+        for (int e = threadIdx.x; e < jb * jb; e += RT) {
+            const int r = e % jb, cc = e / jb;
+            P[r + int64_t(cc) * ldp] = 0.0;
+        }
+        for (int j = threadIdx.x; j < jb; j += RT) tau[j] = 0.0;
+        for (int64_t e = threadIdx.x; e < (mr - jb) * jb; e += RT)
+            P[jb + e % (mr - jb) + int64_t(e / (mr - jb)) * ldp] = 0.0;
+        if (threadIdx.x == 0) *b.ticket = 0u;
+        return;
+    }
+    for (int e = threadIdx.x; e < W * W; e += RT) b.R[MODE * W * W + e] = Rs[e];
+    if (MODE == 2) {
+        // top block of Q = Q2 R3^-1 (rows 0..jb-1), then the modified LU
+        __syncthreads();
+        double* Qt = Gs;  // reuse: Qt[i + j W]
+        if (threadIdx.x < W) {
+            const int i = threadIdx.x;
+            double x[W];
+#pragma unroll
+            for (int j = 0; j < W; ++j) x[j] = (i < jb && j < jb) ? __ldcg(Y + i + int64_t(j) * ldy) : 0.0;
+            if (i < jb) row_solve(x, Rs, jb);
+#pragma unroll
+            for (int j = 0; j < W; ++j) Qt[i + j * W] = x[j];
+        }
+        __syncthreads();
+        __shared__ double sgn[W];
+        if (threadIdx.x == 0) {
+            for (int k = 0; k < jb; ++k) {
+                const double s = Qt[k + k * W] >= 0.0 ? -1.0 : 1.0;  // s_k = -sign(pivot)
+                sgn[k] = s;
+                Qt[k + k * W] -= s;
+                const double piv = Qt[k + k * W];
+                for (int i = k + 1; i < jb; ++i) {
+                    const double l = Qt[i + k * W] / piv;
+                    Qt[i + k * W] = l;
+                    for (int j = k + 1; j < jb; ++j) Qt[i + j * W] -= l * Qt[k + j * W];
+                }
+            }
+        }
+        __syncthreads();
+        // R_house = S (R3 R2 R1) (upper), V_1 = strict lower of the LU,
+        // tau_k = -s_k u_kk; U stored for the last pass
+        const double* R1 = b.R;
+        const double* R2 = b.R + W * W;
+        for (int e = threadIdx.x; e < jb * jb; e += RT) {
+            const int r = e % jb, cc = e / jb;
+            double v;
+            if (r <= cc) {
+                // (R3 R2 R1)(r, cc) = sum_{r <= a <= b <= cc} R3(r,a) R2(a,b) R1(b,cc)
+                double s = 0.0;
+                for (int a2 = r; a2 <= cc; ++a2) {
+                    double inner = 0.0;
+                    for (int b2 = a2; b2 <= cc; ++b2) inner += __ldcg(R2 + a2 + b2 * W) * __ldcg(R1 + b2 + cc * W);
+                    s += Rs[r + a2 * W] * inner;
+                }
+                v = sgn[r] * s;
+            } else {
+                v = Qt[r + cc * W];
+            }
+            P[r + int64_t(cc) * ldp] = v;
+        }
+        for (int e = threadIdx.x; e < W * W; e += RT) {
+            const int r = e % W, cc = e / W;
+            b.U[e] = (r < jb && cc < jb) ? (r <= cc ? Qt[e] : 0.0) : (r == cc ? 1.0 : 0.0);
+        }
+        for (int k = threadIdx.x; k < jb; k += RT) tau[k] = -sgn[k] * Qt[k + k * W];
+    }
+    if (threadIdx.x == 0) *b.ticket = 0u;
+}
+
+// rows >= jb: V = Q2 R3^-1 U^-1 written below the panel's top block
+__global__ void __launch_bounds__(RT) cqr_v_k(int64_t mr, int jb, const double* __restrict__ Q2, int64_t ldq,
+                                              double* __restrict__ P, int64_t ldp, CqrBufs b) {
+    __shared__ double R3[W * W], Us[W * W];
+    if (b.status[0]) return;
+    for (int e = threadIdx.x; e < W * W; e += RT) {
+        R3[e] = b.R[2 * W * W + e];
+        Us[e] = b.U[e];
+    }
+    __syncthreads();
+    for (int64_t i = jb + blockIdx.x * int64_t(RT) + threadIdx.x; i < mr; i += int64_t(gridDim.x) * RT) {
+        double x[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) x[j] = j < jb ? __ldcg(Q2 + i + int64_t(j) * ldq) : 0.0;
+        row_solve(x, R3, jb);
+        row_solve(x, Us, jb);
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            if (j < jb) P[i + int64_t(j) * ldp] = x[j];
+    }
+}
+
+}  // namespace
+
+// Factor the mr x jb (jb <= 32) panel P (ld) in place like the Householder
+// panels of qr.cu: R above the diagonal, V below (unit diagonal implied),
+// tau.  `work` holds 2 mr x 32 doubles (Q1, Q2).
+void panel_cqr(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, double* work) {
+    if (jb < 1 || jb > W || mr < int64_t(W)) throw std::invalid_argument("panel_cqr: shape");
+    const int grid = int(std::min<int64_t>((mr + RT - 1) / RT, int64_t(c.num_sms) * 6));
+    DBuf part = dalloc(c, size_t(grid) * GSZ);
+    DBuf small = dalloc(c, size_t(4) * W * W);
+    DBuf ints(c, 2 * sizeof(unsigned));
+    HYDOT_CUDA(cudaMemsetAsync(ints.as<void>(), 0, 2 * sizeof(unsigned), c.stream));
+    CqrBufs b{part.d(), ints.as<unsigned>(), small.d(), small.d() + 3 * W * W, ints.as<int>() + 1};
+    double* Q1 = work;
+    double* Q2 = work + mr * W;
+    const double shift = 11.0 * (double(mr) * jb + double(jb) * (jb + 1)) * 1.1102230246251565e-16;
+    cqr_pass_k<0><<<grid, RT, 0, c.stream>>>(mr, jb, P, ld, nullptr, 0, P, ld, tau, b, shift);
+    c.check_launch();
+    cqr_pass_k<1><<<grid, RT, 0, c.stream>>>(mr, jb, P, ld, Q1, mr, P, ld, tau, b, 0.0);
+    c.check_launch();
+    cqr_pass_k<2><<<grid, RT, 0, c.stream>>>(mr, jb, Q1, mr, Q2, mr, P, ld, tau, b, 0.0);
+    c.check_launch();
+    cqr_v_k<<<grid, RT, 0, c.stream>>>(mr, jb, Q2, mr, P, ld, b);
+    c.check_launch();
+}
+
+}  // namespace hydot

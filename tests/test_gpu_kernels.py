@@ -152,6 +152,23 @@ def test_householder_qr(ctx, m, n):
     assert np.allclose(np.abs(np.diag(R)), np.abs(np.diag(R2)), rtol=1e-10, atol=1e-14 * np.abs(R2).max())
 
 
+def test_householder_qr_tall_rank_deficient(ctx):
+    """The tall panels (shifted CholeskyQR3 + Householder reconstruction,
+    qr_cqr.cu) on numerically rank-deficient input and an all-zero panel:
+    still a backward-stable Householder QR with orthonormal Q."""
+    from paper_1410_0986_b200 import lowrank as lr
+    rng = np.random.default_rng(3)
+    m, n, k = 120000, 96, 20
+    A = (rng.standard_normal((m, k)) * np.logspace(0, -10, k)) @ rng.standard_normal((k, n))
+    A[:, 40:72] = 0.0  # one whole 32-wide panel of zeros
+    A[:, 75] *= 1e-300
+    Q, R = lr.householder_qr(ctx, torch.as_tensor(A))
+    Q, R = Q.cpu().numpy(), R.cpu().numpy()
+    assert np.allclose(np.triu(R), R)
+    assert np.linalg.norm(Q @ R - A) <= 1e-14 * np.linalg.norm(A) * np.sqrt(n)
+    assert np.linalg.norm(Q.T @ Q - np.eye(n)) <= 1e-13 * np.sqrt(n)
+
+
 @pytest.mark.parametrize("m,n", [(40, 55), (70, 70), (300, 70), (20000, 60), (90, 400), (250, 250)])
 def test_thin_svd_matches_oracle(ctx, oracle, m, n):
     from paper_1410_0986_b200 import lowrank as lr
