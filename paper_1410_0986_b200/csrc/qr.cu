@@ -54,7 +54,11 @@ struct PanelBufs {
 template <bool SMEM>
 __global__ void __launch_bounds__(PT) qr_panel_coop(int64_t mr, int jb, double* __restrict__ P,
                                                     int64_t ld, int64_t rows_per,
-                                                    double* __restrict__ tau_out, PanelBufs buf) {
+                                                    double* __restrict__ tau_out, PanelBufs buf,
+                                                    const int* __restrict__ only_if) {
+    // only_if (device flag, may be null): run only when it is 2 -- the
+    // CholeskyQR panel found its Q not orthonormal and left P untouched
+    if (only_if && *only_if != 2) return;
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double slab[];  // rows_per x PB (ld rows_per) when SMEM
     __shared__ double red[2][PT / 32][PB + 1];  // by partial parity: no barrier before reuse
@@ -357,18 +361,25 @@ __global__ void __launch_bounds__(LT) larft_k(int jb, const double* __restrict__
 }
 
 }  // namespace
-void panel_cqr(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, double* work);
+// returns the device flag (0 ok, 1 zero panel, 2 fall back to Householder)
+const int* panel_cqr(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, double* work,
+                     double* scratch);
+int64_t cqr_scratch_doubles(const Ctx& c);
 namespace {
 
 void panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, const PanelBufs& pbuf,
-           double* work) {
+           double* work, double* cqr_scratch) {
     StageTimer _t(c, "qr_panel", mr, jb, -1, 2.0 * double(mr) * jb * jb, 16.0 * double(mr) * jb);
     // the same launches split by kind (one CTA on-chip / cooperative tall)
     StageTimer _k(c, mr <= kCtaRows ? "qr_panel_cta" : "qr_panel_cqr", mr, jb, -1, 2.0 * double(mr) * jb * jb,
                   16.0 * double(mr) * jb);
-    if (mr > kCtaRows) {  // tall: shifted CholeskyQR3 + Householder reconstruction (qr_cqr.cu)
-        panel_cqr(c, mr, jb, P, ld, tau, work);
-        return;
+    const int* only_if = nullptr;
+    if (mr > kCtaRows) {
+        // tall: shifted CholeskyQR3 + Householder reconstruction (qr_cqr.cu);
+        // a panel whose Q comes out non-orthonormal (numerically rank-deficient
+        // within the panel) is redone by the cooperative Householder kernel
+        // below, which then runs only on that device flag
+        only_if = panel_cqr(c, mr, jb, P, ld, tau, work, cqr_scratch);
     }
     static AttrGate attr;
     const size_t smem_cap = 200 * 1024;
@@ -402,7 +413,7 @@ void panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, const
         HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qr_panel_coop<false>, PT, 0));
     if (per_sm * c.num_sms < G) throw std::runtime_error("qr panel: cooperative grid does not fit");
     PanelBufs b = pbuf;
-    void* args[] = {&mr, &jb, &P, &ld, &rows_per, &tau, &b};
+    void* args[] = {&mr, &jb, &P, &ld, &rows_per, &tau, &b, &only_if};
     if (use_smem)
         c.coop_launch((void*)qr_panel_coop<true>, dim3(G), dim3(PT), args, smem);
     else
@@ -546,6 +557,7 @@ void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f
     DBuf pb_mem = dalloc(c, size_t(2) * GMAX + size_t(2) * GMAX * PB + 2 * PB);
     PanelBufs pbuf{pb_mem.d(), pb_mem.d() + 2 * GMAX, pb_mem.d() + 2 * GMAX + 2 * GMAX * PB};
     DBuf V = dalloc(c, size_t(m) * NB);
+    DBuf cqr = dalloc(c, size_t(cqr_scratch_doubles(c)));
     DBuf G = dalloc(c, size_t(NB) * NB);
     DBuf W = dalloc(c, size_t(NB) * size_t(std::max<int64_t>(n, 1)));
     DBuf W2 = dalloc(c, size_t(NB) * size_t(std::max<int64_t>(n, 1)));
@@ -562,7 +574,7 @@ void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f
             const int pb = std::min(PB, jb - p0);
             const int64_t pr = mr - p0;
             double* Pp = Pb + p0 + int64_t(p0) * m;
-            panel(c, pr, pb, Pp, m, f.tau.d() + j0 + p0, pbuf, V.d());
+            panel(c, pr, pb, Pp, m, f.tau.d() + j0 + p0, pbuf, V.d(), cqr.d());
             const int rest = jb - p0 - pb;
             if (rest > 0) {
                 // apply this sub-panel's reflector to the rest of the block

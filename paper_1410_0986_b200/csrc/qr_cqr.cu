@@ -21,6 +21,8 @@
 // partials are reduced by the last CTA in CTA order (deterministic).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -45,8 +47,13 @@ struct CqrBufs {
     unsigned* ticket;  // last-CTA ticket (self-resetting)
     double* R;         // 3 x W x W: R1, R2, R3 (upper, column-major W x W)
     double* U;         // W x W: U of the top block's LU
-    int* status;       // [0]: 1 = zero panel
+    int* status;       // [0]: 1 = zero panel, 2 = Q not orthonormal (fall back)
 };
+
+// |G3 - I| bound below which Q2 is treated as orthonormal (then Q = Q2 R3^-1
+// is orthonormal to working precision); above it the panel is left to the
+// Householder kernel
+constexpr double kOrthTol = 1e-6;
 
 // y = x R^-1 for a row vector x (jb), R upper triangular (column-major W x W
 // in shared memory): y_j = (x_j - sum_{i<j} y_i R_ij) / R_jj
@@ -192,6 +199,24 @@ __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const doubl
         if (threadIdx.x == 0) *b.ticket = 0u;
         return;
     }
+    if (MODE == 2) {  // Q2 must be orthonormal to O(sqrt u) for the reconstruction
+        __shared__ int bad;
+        if (threadIdx.x == 0) bad = 0;
+        __syncthreads();
+        for (int e = threadIdx.x; e < jb * jb; e += RT) {
+            const int r = e % jb, cc = e / jb;
+            const double v = Gs[r + cc * W] - (r == cc ? 1.0 : 0.0);
+            if (!(fabs(v) <= kOrthTol)) bad = 1;
+        }
+        __syncthreads();
+        if (bad) {
+            if (threadIdx.x == 0) {
+                b.status[0] = 2;
+                *b.ticket = 0u;
+            }
+            return;
+        }
+    }
     for (int e = threadIdx.x; e < W * W; e += RT) b.R[MODE * W * W + e] = Rs[e];
     if (MODE == 2) {
         // top block of Q = Q2 R3^-1 (rows 0..jb-1), then the modified LU
@@ -278,15 +303,20 @@ __global__ void __launch_bounds__(RT) cqr_v_k(int64_t mr, int jb, const double* 
 
 // Factor the mr x jb (jb <= 32) panel P (ld) in place like the Householder
 // panels of qr.cu: R above the diagonal, V below (unit diagonal implied),
-// tau.  `work` holds 2 mr x 32 doubles (Q1, Q2).
-void panel_cqr(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, double* work) {
+// tau.  `work` holds 2 mr x 32 doubles (Q1, Q2), `scratch` cqr_scratch_doubles()
+// (it must outlive the caller's use of the returned flag).  Returns the
+// device status flag: 2 = P untouched, the caller factors it by Householder.
+int64_t cqr_scratch_doubles(const Ctx& c) { return int64_t(c.num_sms) * 6 * GSZ + 4 * W * W + 2; }
+
+const int* panel_cqr(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, double* work,
+                     double* scratch) {
     if (jb < 1 || jb > W || mr < int64_t(W)) throw std::invalid_argument("panel_cqr: shape");
     const int grid = int(std::min<int64_t>((mr + RT - 1) / RT, int64_t(c.num_sms) * 6));
-    DBuf part = dalloc(c, size_t(grid) * GSZ);
-    DBuf small = dalloc(c, size_t(4) * W * W);
-    DBuf ints(c, 2 * sizeof(unsigned));
-    HYDOT_CUDA(cudaMemsetAsync(ints.as<void>(), 0, 2 * sizeof(unsigned), c.stream));
-    CqrBufs b{part.d(), ints.as<unsigned>(), small.d(), small.d() + 3 * W * W, ints.as<int>() + 1};
+    double* part = scratch;
+    double* small = scratch + int64_t(c.num_sms) * 6 * GSZ;
+    unsigned* ints = reinterpret_cast<unsigned*>(small + 4 * W * W);
+    HYDOT_CUDA(cudaMemsetAsync(ints, 0, 2 * sizeof(unsigned), c.stream));
+    CqrBufs b{part, ints, small, small + 3 * W * W, reinterpret_cast<int*>(ints + 1)};
     double* Q1 = work;
     double* Q2 = work + mr * W;
     const double shift = 11.0 * (double(mr) * jb + double(jb) * (jb + 1)) * 1.1102230246251565e-16;
@@ -298,6 +328,23 @@ void panel_cqr(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, d
     c.check_launch();
     cqr_v_k<<<grid, RT, 0, c.stream>>>(mr, jb, Q2, mr, P, ld, b);
     c.check_launch();
+    static const bool stats = [] {  // HYDOT_QR_STATS=1: report panels that fall back
+        const char* e = std::getenv("HYDOT_QR_STATS");
+        return e && e[0] == '1';
+    }();
+    if (stats) {
+        int st = 0;
+        HYDOT_CUDA(cudaMemcpyAsync(&st, b.status, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        static long n_all = 0, n_fb = 0, n_zero = 0;
+        ++n_all;
+        n_fb += st == 2;
+        n_zero += st == 1;
+        if (st == 2 || (n_all % 500) == 0)
+            fprintf(stderr, "[cqr] mr=%lld jb=%d status=%d (panels %ld, fallbacks %ld, zero %ld)\n", (long long)mr,
+                    jb, st, n_all, n_fb, n_zero);
+    }
+    return b.status;
 }
 
 }  // namespace hydot
