@@ -178,10 +178,32 @@ __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const doubl
     __syncthreads();
     if (!last) return;
     __threadfence();
-    for (int e = threadIdx.x; e < W * W; e += RT) {
-        double s = 0.0;
-        for (int p = 0; p < int(gridDim.x); ++p) s += __ldcg(b.part + int64_t(p) * GSZ + e);
-        Gs[e] = s;
+    {
+        // every thread sums its 8 entries over the CTAs' partials in CTA
+        // order, four partials per step with all 32 loads in flight (a
+        // one-load-at-a-time walk over ~150 partials was the pass's cost)
+        constexpr int EPT = W * W / RT;  // 8
+        double s[EPT];
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) s[k] = 0.0;
+        const int np = int(gridDim.x);
+        int p = 0;
+        for (; p + 4 <= np; p += 4) {
+            double v[4][EPT];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int k = 0; k < EPT; ++k) v[q][k] = __ldcg(b.part + int64_t(p + q) * GSZ + threadIdx.x + k * RT);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int k = 0; k < EPT; ++k) s[k] += v[q][k];
+        }
+        for (; p < np; ++p)
+#pragma unroll
+            for (int k = 0; k < EPT; ++k) s[k] += __ldcg(b.part + int64_t(p) * GSZ + threadIdx.x + k * RT);
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) Gs[threadIdx.x + k * RT] = s[k];
     }
     __syncthreads();
     __shared__ double tr0;
@@ -311,7 +333,9 @@ int64_t cqr_scratch_doubles(const Ctx& c) { return int64_t(c.num_sms) * 6 * GSZ 
 const int* panel_cqr(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, double* work,
                      double* scratch) {
     if (jb < 1 || jb > W || mr < int64_t(W)) throw std::invalid_argument("panel_cqr: shape");
-    const int grid = int(std::min<int64_t>((mr + RT - 1) / RT, int64_t(c.num_sms) * 6));
+    // one CTA per SM: each streams ~1/148 of the rows; fewer partials keep
+    // the last CTA's reduction short
+    const int grid = int(std::min<int64_t>((mr + RT - 1) / RT, int64_t(c.num_sms)));
     double* part = scratch;
     double* small = scratch + int64_t(c.num_sms) * 6 * GSZ;
     unsigned* ints = reinterpret_cast<unsigned*>(small + 4 * W * W);
