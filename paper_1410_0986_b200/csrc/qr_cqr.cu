@@ -56,57 +56,62 @@ struct CqrBufs {
 constexpr double kOrthTol = 1e-6;
 
 // y = x R^-1 for a row vector x (jb), R upper triangular (column-major W x W
-// in shared memory): y_j = (x_j - sum_{i<j} y_i R_ij) / R_jj
-__device__ __forceinline__ void row_solve(double (&x)[W], const double* __restrict__ R, int jb) {
+// in shared memory), invd[j] = 1 / R_jj: y_j = (x_j - sum_{i<j} y_i R_ij) /
+// R_jj by substitution (backward stable per row), the inner sum split in
+// four independent chains
+__device__ __forceinline__ void row_solve(double (&x)[W], const double* __restrict__ R,
+                                          const double* __restrict__ invd, int jb) {
 #pragma unroll
     for (int j = 0; j < W; ++j) {
         if (j < jb) {
-            double s = x[j];
+            double s0 = x[j], s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
-            for (int i = 0; i < W; ++i)
-                if (i < j) s -= x[i] * R[i + j * W];
-            x[j] = s / R[j + j * W];
+            for (int i = 0; i < W; i += 4) {
+                if (i < j) s0 -= x[i] * R[i + j * W];
+                if (i + 1 < j) s1 -= x[i + 1] * R[i + 1 + j * W];
+                if (i + 2 < j) s2 -= x[i + 2] * R[i + 2 + j * W];
+                if (i + 3 < j) s3 -= x[i + 3] * R[i + 3 + j * W];
+            }
+            x[j] = ((s0 + s1) + (s2 + s3)) * invd[j];
         }
     }
 }
 
-// Cholesky of the jb x jb Gram (+ shift) in shared memory by one warp:
-// G + s I = R^T R, R upper (column-major W x W, zero below).  Retries with a
+// Cholesky of the jb x jb Gram (+ shift) by one warp in shared memory:
+// G + s I = R^T R, R upper (column-major W x W; identity outside jb, zero
+// below the diagonal).  The working copy A is destroyed.  Retries with a
 // 10x larger shift if a pivot is not positive.
-__device__ void warp_cholesky(double* G, double* R, int jb, double shift, double* tr_out) {
+__device__ void warp_cholesky(const double* G, double* A, double* R, int jb, double shift, double* tr_out) {
     const int lane = threadIdx.x;
     double tr = 0.0;
     for (int i = 0; i < jb; ++i) tr += G[i + i * W];
-    if (tr_out) *tr_out = tr;
+    if (tr_out && lane == 0) *tr_out = tr;
     double s = shift * tr;
     for (int attempt = 0; attempt < 12; ++attempt) {
+        // lane j owns column j (rows 0..j of the upper part)
+        for (int i = 0; i < W; ++i) A[i + lane * W] = (lane < jb && i < jb) ? G[i + lane * W] + (i == lane ? s : 0.0) : 0.0;
+        __syncwarp();
         bool ok = true;
-        // lane j owns column j of the working copy
-        double col[W];
-#pragma unroll
-        for (int i = 0; i < W; ++i) col[i] = (lane < jb && i < jb) ? G[i + lane * W] + (i == lane ? s : 0.0) : 0.0;
         for (int k = 0; k < jb; ++k) {
-            // pivot a_kk lives in lane k, entries a_kj in lanes j
-            double akk = __shfl_sync(0xffffffffu, col[k], k);
+            const double akk = A[k + k * W];
             if (!(akk > 0.0)) {
                 ok = false;
                 break;
             }
-            const double d = sqrt(akk);
+            const double d = sqrt(akk), id = 1.0 / d;
             double rkj = 0.0;
-            if (lane >= k && lane < jb) rkj = (lane == k) ? d : col[k] / d;
+            if (lane >= k && lane < jb) rkj = lane == k ? d : A[k + lane * W] * id;
             if (lane < jb) R[k + lane * W] = lane >= k ? rkj : 0.0;
-            // a_ij -= r_ki r_kj for i, j > k (lane j updates its column)
-#pragma unroll
-            for (int i = 0; i < W; ++i) {
-                const double rki = __shfl_sync(0xffffffffu, rkj, i);
-                if (i > k && lane > k && lane < jb) col[i] -= rki * rkj;
-            }
+            __syncwarp();
+            if (lane > k && lane < jb)  // a_ij -= r_ki r_kj, k < i <= j = lane
+                for (int i = k + 1; i <= lane; ++i) A[i + lane * W] -= R[k + i * W] * rkj;
+            __syncwarp();
         }
-        if (__all_sync(0xffffffffu, ok)) {
+        if (ok) {
             for (int e = lane; e < W * W; e += 32) {
                 const int i = e % W, j = e / W;
-                if (i >= jb || j >= jb || i > j) R[e] = (i == j && i >= jb) ? 1.0 : (i > j || i >= jb || j >= jb ? 0.0 : R[e]);
+                if (i >= jb || j >= jb) R[e] = i == j ? 1.0 : 0.0;
+                else if (i > j) R[e] = 0.0;
             }
             __syncwarp();
             return;
@@ -128,15 +133,22 @@ __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const doubl
                                                  int64_t ldp, double* __restrict__ tau, CqrBufs b, double shift) {
     __shared__ __align__(16) double tile[W * XS];
     __shared__ double Rin[W * W];
+    __shared__ double invd[W];
     __shared__ bool last;
-    double* Gs = tile;          // the last CTA's Gram / Cholesky factor reuse
-    double* Rs = tile + W * W;  // the tile after the row loop
+    // the last CTA reuses the tile after the row loop
+    double* Gs = tile;              // Gram, then Q's top block / LU
+    double* Rs = tile + W * W;      // this pass's Cholesky factor
+    double* Aw = tile + 2 * W * W;  // Cholesky working copy, then R2 R1
+    double* R12 = tile + 3 * W * W;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int wi = (warp & 1) * 16, wj = (warp >> 1) * 16;
     if (MODE > 0 && b.status[0]) return;  // zero panel: nothing to do
-    if (MODE > 0)
+    if (MODE > 0) {
         for (int e = threadIdx.x; e < W * W; e += RT) Rin[e] = b.R[(MODE - 1) * W * W + e];
+        __syncthreads();
+        if (threadIdx.x < W) invd[threadIdx.x] = 1.0 / Rin[threadIdx.x * (W + 1)];
+    }
     __syncthreads();
     double acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
     const int64_t ntiles = (mr + RT - 1) / RT;
@@ -146,7 +158,7 @@ __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const doubl
 #pragma unroll
         for (int j = 0; j < W; ++j) x[j] = (i < mr && j < jb) ? __ldcg(X + i + int64_t(j) * ldx) : 0.0;
         if (MODE > 0) {
-            if (i < mr) row_solve(x, Rin, jb);
+            if (i < mr) row_solve(x, Rin, invd, jb);
 #pragma unroll
             for (int j = 0; j < W; ++j)
                 if (i < mr && j < jb) __stcg(Y + i + int64_t(j) * ldy, x[j]);
@@ -207,7 +219,7 @@ __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const doubl
     }
     __syncthreads();
     __shared__ double tr0;
-    if (warp == 0) warp_cholesky(Gs, Rs, jb, MODE == 0 ? shift : 0.0, MODE == 0 ? &tr0 : nullptr);
+    if (warp == 0) warp_cholesky(Gs, Aw, Rs, jb, MODE == 0 ? shift : 0.0, MODE == 0 ? &tr0 : nullptr);
     __syncthreads();
     if (MODE == 0 && tr0 == 0.0) {  // zero panel: H = I, R = 0
         if (threadIdx.x == 0) b.status[0] = 1;
@@ -242,48 +254,55 @@ __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const doubl
     for (int e = threadIdx.x; e < W * W; e += RT) b.R[MODE * W * W + e] = Rs[e];
     if (MODE == 2) {
         // top block of Q = Q2 R3^-1 (rows 0..jb-1), then the modified LU
+        __shared__ double invr[W];
+        __shared__ double sgn[W];
+        if (threadIdx.x < W) invr[threadIdx.x] = 1.0 / Rs[threadIdx.x * (W + 1)];
+        for (int e = threadIdx.x; e < W * W; e += RT) {  // R12 = R2 R1 (upper)
+            const int r = e % W, cc = e / W;
+            double v = 0.0;
+            if (r <= cc && cc < jb)
+                for (int a2 = r; a2 <= cc; ++a2) v += __ldcg(b.R + W * W + r + a2 * W) * __ldcg(b.R + a2 + cc * W);
+            R12[e] = v;
+        }
         __syncthreads();
-        double* Qt = Gs;  // reuse: Qt[i + j W]
+        double* Qt = Gs;  // Qt[i + j W]
         if (threadIdx.x < W) {
             const int i = threadIdx.x;
             double x[W];
 #pragma unroll
             for (int j = 0; j < W; ++j) x[j] = (i < jb && j < jb) ? __ldcg(Y + i + int64_t(j) * ldy) : 0.0;
-            if (i < jb) row_solve(x, Rs, jb);
+            if (i < jb) row_solve(x, Rs, invr, jb);
 #pragma unroll
             for (int j = 0; j < W; ++j) Qt[i + j * W] = x[j];
         }
         __syncthreads();
-        __shared__ double sgn[W];
-        if (threadIdx.x == 0) {
+        if (warp == 0) {  // LU of Qt - S without pivoting, lane = row
             for (int k = 0; k < jb; ++k) {
-                const double s = Qt[k + k * W] >= 0.0 ? -1.0 : 1.0;  // s_k = -sign(pivot)
-                sgn[k] = s;
-                Qt[k + k * W] -= s;
-                const double piv = Qt[k + k * W];
-                for (int i = k + 1; i < jb; ++i) {
-                    const double l = Qt[i + k * W] / piv;
-                    Qt[i + k * W] = l;
-                    for (int j = k + 1; j < jb; ++j) Qt[i + j * W] -= l * Qt[k + j * W];
+                const double s = Qt[k + k * W] >= 0.0 ? -1.0 : 1.0;  // s_k = -sign(pivot): |u_kk| >= 1
+                __syncwarp();  // every lane has read the pivot before it changes
+                if (lane == 0) {
+                    sgn[k] = s;
+                    Qt[k + k * W] -= s;
                 }
+                __syncwarp();
+                const double ipiv = 1.0 / Qt[k + k * W];
+                if (lane > k && lane < jb) {
+                    const double l = Qt[lane + k * W] * ipiv;
+                    Qt[lane + k * W] = l;
+                    for (int j = k + 1; j < jb; ++j) Qt[lane + j * W] -= l * Qt[k + j * W];
+                }
+                __syncwarp();
             }
         }
         __syncthreads();
         // R_house = S (R3 R2 R1) (upper), V_1 = strict lower of the LU,
-        // tau_k = -s_k u_kk; U stored for the last pass
-        const double* R1 = b.R;
-        const double* R2 = b.R + W * W;
+        // tau_k = -s_k u_kk; U kept for the last pass
         for (int e = threadIdx.x; e < jb * jb; e += RT) {
             const int r = e % jb, cc = e / jb;
             double v;
             if (r <= cc) {
-                // (R3 R2 R1)(r, cc) = sum_{r <= a <= b <= cc} R3(r,a) R2(a,b) R1(b,cc)
                 double s = 0.0;
-                for (int a2 = r; a2 <= cc; ++a2) {
-                    double inner = 0.0;
-                    for (int b2 = a2; b2 <= cc; ++b2) inner += __ldcg(R2 + a2 + b2 * W) * __ldcg(R1 + b2 + cc * W);
-                    s += Rs[r + a2 * W] * inner;
-                }
+                for (int a2 = r; a2 <= cc; ++a2) s += Rs[r + a2 * W] * R12[a2 + cc * W];
                 v = sgn[r] * s;
             } else {
                 v = Qt[r + cc * W];
@@ -302,19 +321,24 @@ __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const doubl
 // rows >= jb: V = Q2 R3^-1 U^-1 written below the panel's top block
 __global__ void __launch_bounds__(RT) cqr_v_k(int64_t mr, int jb, const double* __restrict__ Q2, int64_t ldq,
                                               double* __restrict__ P, int64_t ldp, CqrBufs b) {
-    __shared__ double R3[W * W], Us[W * W];
+    __shared__ double R3[W * W], Us[W * W], i3[W], iu[W];
     if (b.status[0]) return;
     for (int e = threadIdx.x; e < W * W; e += RT) {
         R3[e] = b.R[2 * W * W + e];
         Us[e] = b.U[e];
     }
     __syncthreads();
+    if (threadIdx.x < W) {
+        i3[threadIdx.x] = 1.0 / R3[threadIdx.x * (W + 1)];
+        iu[threadIdx.x] = 1.0 / Us[threadIdx.x * (W + 1)];
+    }
+    __syncthreads();
     for (int64_t i = jb + blockIdx.x * int64_t(RT) + threadIdx.x; i < mr; i += int64_t(gridDim.x) * RT) {
         double x[W];
 #pragma unroll
         for (int j = 0; j < W; ++j) x[j] = j < jb ? __ldcg(Q2 + i + int64_t(j) * ldq) : 0.0;
-        row_solve(x, R3, jb);
-        row_solve(x, Us, jb);
+        row_solve(x, R3, i3, jb);
+        row_solve(x, Us, iu, jb);
 #pragma unroll
         for (int j = 0; j < W; ++j)
             if (j < jb) P[i + int64_t(j) * ldp] = x[j];
