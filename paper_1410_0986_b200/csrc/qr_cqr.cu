@@ -77,37 +77,48 @@ __device__ __forceinline__ void row_solve(double (&x)[W], const double* __restri
     }
 }
 
-// Cholesky of the jb x jb Gram (+ shift) by one warp in shared memory:
-// G + s I = R^T R, R upper (column-major W x W; identity outside jb, zero
-// below the diagonal).  The working copy A is destroyed.  Retries with a
+// v[k] for a runtime k without dynamic register indexing
+__device__ __forceinline__ double pick(const double (&v)[W], int k) {
+    double r = 0.0;
+#pragma unroll
+    for (int i = 0; i < W; ++i) r = i == k ? v[i] : r;
+    return r;
+}
+
+// Cholesky of the jb x jb Gram (+ shift) by one warp, lane j holding column
+// j in registers: G + s I = R^T R, R upper (column-major W x W in shared
+// memory; identity outside jb, zero below the diagonal).  Retries with a
 // 10x larger shift if a pivot is not positive.
-__device__ void warp_cholesky(const double* G, double* A, double* R, int jb, double shift, double* tr_out) {
+__device__ void warp_cholesky(const double* __restrict__ G, double* __restrict__ R, int jb, double shift,
+                              double* tr_out) {
     const int lane = threadIdx.x;
     double tr = 0.0;
     for (int i = 0; i < jb; ++i) tr += G[i + i * W];
     if (tr_out && lane == 0) *tr_out = tr;
     double s = shift * tr;
     for (int attempt = 0; attempt < 12; ++attempt) {
-        // lane j owns column j (rows 0..j of the upper part)
-        for (int i = 0; i < W; ++i) A[i + lane * W] = (lane < jb && i < jb) ? G[i + lane * W] + (i == lane ? s : 0.0) : 0.0;
-        __syncwarp();
+        double col[W];
+#pragma unroll
+        for (int i = 0; i < W; ++i) col[i] = (lane < jb && i < jb) ? G[i + lane * W] + (i == lane ? s : 0.0) : 0.0;
         bool ok = true;
         for (int k = 0; k < jb; ++k) {
-            const double akk = A[k + k * W];
+            const double akj = pick(col, k);
+            const double akk = __shfl_sync(0xffffffffu, akj, k);
             if (!(akk > 0.0)) {
                 ok = false;
                 break;
             }
-            const double d = sqrt(akk), id = 1.0 / d;
-            double rkj = 0.0;
-            if (lane >= k && lane < jb) rkj = lane == k ? d : A[k + lane * W] * id;
-            if (lane < jb) R[k + lane * W] = lane >= k ? rkj : 0.0;
-            __syncwarp();
-            if (lane > k && lane < jb)  // a_ij -= r_ki r_kj, k < i <= j = lane
-                for (int i = k + 1; i <= lane; ++i) A[i + lane * W] -= R[k + i * W] * rkj;
-            __syncwarp();
+            const double d = sqrt(akk);
+            const double rkj = (lane >= k && lane < jb) ? (lane == k ? d : akj / d) : 0.0;
+            if (lane < jb) R[k + lane * W] = rkj;
+#pragma unroll
+            for (int i = 0; i < W; ++i) {  // a_ij -= r_ki r_kj for i > k
+                const double rki = __shfl_sync(0xffffffffu, rkj, i);
+                if (i > k) col[i] -= rki * rkj;
+            }
         }
         if (ok) {
+            __syncwarp();
             for (int e = lane; e < W * W; e += 32) {
                 const int i = e % W, j = e / W;
                 if (i >= jb || j >= jb) R[e] = i == j ? 1.0 : 0.0;
@@ -138,8 +149,8 @@ __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const doubl
     // the last CTA reuses the tile after the row loop
     double* Gs = tile;              // Gram, then Q's top block / LU
     double* Rs = tile + W * W;      // this pass's Cholesky factor
-    double* Aw = tile + 2 * W * W;  // Cholesky working copy, then R2 R1
-    double* R12 = tile + 3 * W * W;
+    double* R12 = tile + 2 * W * W;  // R2 R1 (last pass)
+    double* R1s = tile + 3 * W * W;  // R1, then R2 staged from global (4 W W <= W XS)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int wi = (warp & 1) * 16, wj = (warp >> 1) * 16;
@@ -219,7 +230,7 @@ __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const doubl
     }
     __syncthreads();
     __shared__ double tr0;
-    if (warp == 0) warp_cholesky(Gs, Aw, Rs, jb, MODE == 0 ? shift : 0.0, MODE == 0 ? &tr0 : nullptr);
+    if (warp == 0) warp_cholesky(Gs, Rs, jb, MODE == 0 ? shift : 0.0, MODE == 0 ? &tr0 : nullptr);
     __syncthreads();
     if (MODE == 0 && tr0 == 0.0) {  // zero panel: H = I, R = 0
         if (threadIdx.x == 0) b.status[0] = 1;
@@ -257,13 +268,26 @@ __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const doubl
         __shared__ double invr[W];
         __shared__ double sgn[W];
         if (threadIdx.x < W) invr[threadIdx.x] = 1.0 / Rs[threadIdx.x * (W + 1)];
-        for (int e = threadIdx.x; e < W * W; e += RT) {  // R12 = R2 R1 (upper)
+        // R12 = R2 R1 (upper), both staged in shared memory (R2 into R12's
+        // space first, R1 beside it)
+        for (int e = threadIdx.x; e < W * W; e += RT) {
+            R12[e] = __ldcg(b.R + W * W + e);
+            R1s[e] = __ldcg(b.R + e);
+        }
+        __syncthreads();
+        double r12v[W * W / RT];
+#pragma unroll
+        for (int k = 0; k < W * W / RT; ++k) {
+            const int e = threadIdx.x + k * RT;
             const int r = e % W, cc = e / W;
             double v = 0.0;
             if (r <= cc && cc < jb)
-                for (int a2 = r; a2 <= cc; ++a2) v += __ldcg(b.R + W * W + r + a2 * W) * __ldcg(b.R + a2 + cc * W);
-            R12[e] = v;
+                for (int a2 = r; a2 <= cc; ++a2) v += R12[r + a2 * W] * R1s[a2 + cc * W];
+            r12v[k] = v;
         }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < W * W / RT; ++k) R12[threadIdx.x + k * RT] = r12v[k];
         __syncthreads();
         double* Qt = Gs;  // Qt[i + j W]
         if (threadIdx.x < W) {
@@ -276,23 +300,29 @@ __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const doubl
             for (int j = 0; j < W; ++j) Qt[i + j * W] = x[j];
         }
         __syncthreads();
-        if (warp == 0) {  // LU of Qt - S without pivoting, lane = row
+        if (warp == 0) {  // LU of Qt - S without pivoting: lane = row, in registers
+            double row[W];
+#pragma unroll
+            for (int j = 0; j < W; ++j) row[j] = Qt[lane + j * W];
             for (int k = 0; k < jb; ++k) {
-                const double s = Qt[k + k * W] >= 0.0 ? -1.0 : 1.0;  // s_k = -sign(pivot): |u_kk| >= 1
-                __syncwarp();  // every lane has read the pivot before it changes
-                if (lane == 0) {
-                    sgn[k] = s;
-                    Qt[k + k * W] -= s;
+                const double pk = __shfl_sync(0xffffffffu, pick(row, k), k);  // running pivot
+                const double sk = pk >= 0.0 ? -1.0 : 1.0;  // s_k = -sign(pivot): |u_kk| >= 1
+                if (lane == 0) sgn[k] = sk;
+                if (lane == k) {
+#pragma unroll
+                    for (int j = 0; j < W; ++j)
+                        if (j == k) row[j] -= sk;
                 }
-                __syncwarp();
-                const double ipiv = 1.0 / Qt[k + k * W];
-                if (lane > k && lane < jb) {
-                    const double l = Qt[lane + k * W] * ipiv;
-                    Qt[lane + k * W] = l;
-                    for (int j = k + 1; j < jb; ++j) Qt[lane + j * W] -= l * Qt[k + j * W];
+                const double l = (lane > k && lane < jb) ? pick(row, k) / (pk - sk) : 0.0;
+#pragma unroll
+                for (int j = 0; j < W; ++j) {
+                    const double ukj = __shfl_sync(0xffffffffu, row[j], k);
+                    if (j > k) row[j] -= l * ukj;
+                    else if (j == k && lane > k && lane < jb) row[j] = l;
                 }
-                __syncwarp();
             }
+#pragma unroll
+            for (int j = 0; j < W; ++j) Qt[lane + j * W] = row[j];
         }
         __syncthreads();
         // R_house = S (R3 R2 R1) (upper), V_1 = strict lower of the LU,
