@@ -42,6 +42,28 @@ __device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, doubl
         : "d"(a0), "d"(a1), "d"(b0));
 }
 
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(pred ? 8 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// stage rows [r0, r0 + RT) of the panel's jb columns into buf[col][row]
+// (zero-filled outside), 8-byte copies (any leading dimension)
+__device__ __forceinline__ void stage_tile(double* buf, const double* __restrict__ X, int64_t ldx, int64_t r0,
+                                           int64_t mr, int jb) {
+#pragma unroll 8
+    for (int e = threadIdx.x; e < RT * W; e += RT) {
+        const int i = e % RT, j = e / RT;
+        const bool ok = r0 + i < mr && j < jb;
+        cp_async8(buf + j * XS + i, ok ? X + r0 + i + int64_t(j) * ldx : X, ok);
+    }
+}
+
 struct CqrBufs {
     double* part;      // gridDim x GSZ partial Grams
     unsigned* ticket;  // last-CTA ticket (self-resetting)
@@ -142,7 +164,8 @@ template <int MODE>
 __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const double* __restrict__ X, int64_t ldx,
                                                  double* __restrict__ Y, int64_t ldy, double* __restrict__ P,
                                                  int64_t ldp, double* __restrict__ tau, CqrBufs b, double shift) {
-    __shared__ __align__(16) double tile[W * XS];
+    extern __shared__ __align__(16) double dyn[];  // 2 x W x XS: double-buffered row tiles
+    double* tile = dyn;
     __shared__ double Rin[W * W];
     __shared__ double invd[W];
     __shared__ bool last;
@@ -163,29 +186,41 @@ __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const doubl
     __syncthreads();
     double acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
     const int64_t ntiles = (mr + RT - 1) / RT;
-    for (int64_t tt = blockIdx.x; tt < ntiles; tt += gridDim.x) {
+    // tile k of this CTA lives in buffer k & 1; the next tile's copies are
+    // in flight while the current one is solved and accumulated
+    int64_t tt = blockIdx.x;
+    if (tt < ntiles) stage_tile(dyn, X, ldx, tt * RT, mr, jb);
+    cp_commit();
+    for (int k = 0; tt < ntiles; tt += gridDim.x, ++k) {
+        double* cur = dyn + (k & 1) * (W * XS);
+        double* nxt = dyn + ((k + 1) & 1) * (W * XS);
+        if (tt + gridDim.x < ntiles) stage_tile(nxt, X, ldx, (tt + gridDim.x) * RT, mr, jb);
+        cp_commit();
+        cp_wait<1>();
+        __syncthreads();
         const int64_t i = tt * RT + threadIdx.x;
-        double x[W];
-#pragma unroll
-        for (int j = 0; j < W; ++j) x[j] = (i < mr && j < jb) ? __ldcg(X + i + int64_t(j) * ldx) : 0.0;
         if (MODE > 0) {
+            double x[W];
+#pragma unroll
+            for (int j = 0; j < W; ++j) x[j] = cur[j * XS + threadIdx.x];
             if (i < mr) row_solve(x, Rin, invd, jb);
 #pragma unroll
-            for (int j = 0; j < W; ++j)
+            for (int j = 0; j < W; ++j) {
                 if (i < mr && j < jb) __stcg(Y + i + int64_t(j) * ldy, x[j]);
+                cur[j * XS + threadIdx.x] = x[j];
+            }
+            __syncthreads();
         }
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < W; ++j) tile[j * XS + threadIdx.x] = x[j];
-        __syncthreads();
 #pragma unroll
         for (int kk = 0; kk < RT; kk += 4) {
-            const double a0 = tile[(wi + g) * XS + kk + t];
-            const double a1 = tile[(wi + g + 8) * XS + kk + t];
+            const double a0 = cur[(wi + g) * XS + kk + t];
+            const double a1 = cur[(wi + g + 8) * XS + kk + t];
 #pragma unroll
-            for (int ni = 0; ni < 2; ++ni) dmma(acc[ni], a0, a1, tile[(wj + ni * 8 + g) * XS + kk + t]);
+            for (int ni = 0; ni < 2; ++ni) dmma(acc[ni], a0, a1, cur[(wj + ni * 8 + g) * XS + kk + t]);
         }
+        __syncthreads();  // cur is refilled two tiles later
     }
+    cp_wait<0>();
     double* mine = b.part + int64_t(blockIdx.x) * GSZ;
 #pragma unroll
     for (int ni = 0; ni < 2; ++ni)
@@ -351,6 +386,7 @@ __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const doubl
 // rows >= jb: V = Q2 R3^-1 U^-1 written below the panel's top block
 __global__ void __launch_bounds__(RT) cqr_v_k(int64_t mr, int jb, const double* __restrict__ Q2, int64_t ldq,
                                               double* __restrict__ P, int64_t ldp, CqrBufs b) {
+    extern __shared__ __align__(16) double dyn[];
     __shared__ double R3[W * W], Us[W * W], i3[W], iu[W];
     if (b.status[0]) return;
     for (int e = threadIdx.x; e < W * W; e += RT) {
@@ -362,17 +398,31 @@ __global__ void __launch_bounds__(RT) cqr_v_k(int64_t mr, int jb, const double* 
         i3[threadIdx.x] = 1.0 / R3[threadIdx.x * (W + 1)];
         iu[threadIdx.x] = 1.0 / Us[threadIdx.x * (W + 1)];
     }
-    __syncthreads();
-    for (int64_t i = jb + blockIdx.x * int64_t(RT) + threadIdx.x; i < mr; i += int64_t(gridDim.x) * RT) {
-        double x[W];
+    const int64_t ntiles = (mr + RT - 1) / RT;
+    int64_t tt = blockIdx.x;
+    if (tt < ntiles) stage_tile(dyn, Q2, ldq, tt * RT, mr, jb);
+    cp_commit();
+    for (int k = 0; tt < ntiles; tt += gridDim.x, ++k) {
+        double* cur = dyn + (k & 1) * (W * XS);
+        double* nxt = dyn + ((k + 1) & 1) * (W * XS);
+        if (tt + gridDim.x < ntiles) stage_tile(nxt, Q2, ldq, (tt + gridDim.x) * RT, mr, jb);
+        cp_commit();
+        cp_wait<1>();
+        __syncthreads();
+        const int64_t i = tt * RT + threadIdx.x;
+        if (i >= jb && i < mr) {
+            double x[W];
 #pragma unroll
-        for (int j = 0; j < W; ++j) x[j] = j < jb ? __ldcg(Q2 + i + int64_t(j) * ldq) : 0.0;
-        row_solve(x, R3, i3, jb);
-        row_solve(x, Us, iu, jb);
+            for (int j = 0; j < W; ++j) x[j] = cur[j * XS + threadIdx.x];
+            row_solve(x, R3, i3, jb);
+            row_solve(x, Us, iu, jb);
 #pragma unroll
-        for (int j = 0; j < W; ++j)
-            if (j < jb) P[i + int64_t(j) * ldp] = x[j];
+            for (int j = 0; j < W; ++j)
+                if (j < jb) P[i + int64_t(j) * ldp] = x[j];
+        }
+        __syncthreads();
     }
+    cp_wait<0>();
 }
 
 }  // namespace
@@ -398,13 +448,21 @@ const int* panel_cqr(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* 
     double* Q1 = work;
     double* Q2 = work + mr * W;
     const double shift = 11.0 * (double(mr) * jb + double(jb) * (jb + 1)) * 1.1102230246251565e-16;
-    cqr_pass_k<0><<<grid, RT, 0, c.stream>>>(mr, jb, P, ld, nullptr, 0, P, ld, tau, b, shift);
+    const size_t smem = size_t(2) * W * XS * sizeof(double);
+    static AttrGate attr;
+    attr_once(attr, c.device, [&] {
+        HYDOT_CUDA(cudaFuncSetAttribute(cqr_pass_k<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        HYDOT_CUDA(cudaFuncSetAttribute(cqr_pass_k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        HYDOT_CUDA(cudaFuncSetAttribute(cqr_pass_k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        HYDOT_CUDA(cudaFuncSetAttribute(cqr_v_k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    });
+    cqr_pass_k<0><<<grid, RT, smem, c.stream>>>(mr, jb, P, ld, nullptr, 0, P, ld, tau, b, shift);
     c.check_launch();
-    cqr_pass_k<1><<<grid, RT, 0, c.stream>>>(mr, jb, P, ld, Q1, mr, P, ld, tau, b, 0.0);
+    cqr_pass_k<1><<<grid, RT, smem, c.stream>>>(mr, jb, P, ld, Q1, mr, P, ld, tau, b, 0.0);
     c.check_launch();
-    cqr_pass_k<2><<<grid, RT, 0, c.stream>>>(mr, jb, Q1, mr, Q2, mr, P, ld, tau, b, 0.0);
+    cqr_pass_k<2><<<grid, RT, smem, c.stream>>>(mr, jb, Q1, mr, Q2, mr, P, ld, tau, b, 0.0);
     c.check_launch();
-    cqr_v_k<<<grid, RT, 0, c.stream>>>(mr, jb, Q2, mr, P, ld, b);
+    cqr_v_k<<<grid, RT, smem, c.stream>>>(mr, jb, Q2, mr, P, ld, b);
     c.check_launch();
     static const bool stats = [] {  // HYDOT_QR_STATS=1: report panels that fall back
         const char* e = std::getenv("HYDOT_QR_STATS");
