@@ -147,6 +147,31 @@ __device__ __forceinline__ void load_sub(double* xs, const double* __restrict__ 
     }
 }
 
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(pred ? 8 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// asynchronous load_sub: the copies land in xs while the previous sub-tile
+// is processed (double buffering inside a unit)
+__device__ __forceinline__ void stage_sub(double* xs, const double* __restrict__ U, int64_t ldu,
+                                          const int* col, int64_t r, int64_t rend) {
+#pragma unroll
+    for (int k = 0; k < SUB * PW / NTH; ++k) {
+        const int e = threadIdx.x + k * NTH;
+        const int i = e & (SUB - 1), j = e / SUB;
+        const int64_t gi = r + i;
+        const int cj = col[j];
+        const bool ok = cj >= 0 && gi < rend;
+        cp_async8(xs + j * XS + i, ok ? U + gi + int64_t(cj) * ldu : U, ok);
+    }
+}
+
 // ---- phase 1: partial Gram of one (pair, row chunk) unit; the CTA that
 // completes a pair's last chunk diagonalises its Gram
 __device__ void eig_pair(const BJArgs& a, int q, int rnd, double* smem);
@@ -162,19 +187,27 @@ __device__ void gram_unit(const BJArgs& a, int2 bp, int q, int rnd, int ch, doub
 #pragma unroll
         for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
     const int64_t r0 = int64_t(ch) * a.rch, r1 = min(a.m, r0 + a.rch);
-    for (int64_t r = r0; r < r1; r += SUB) {
-        __syncthreads();
-        load_sub(xs, a.U, a.ldu, col, r, r1);
+    const int nsub = int((r1 - r0 + SUB - 1) / SUB);
+    __syncthreads();
+    stage_sub(xs, a.U, a.ldu, col, r0, r1);
+    cp_commit();
+    for (int sb = 0; sb < nsub; ++sb) {
+        const double* cur = xs + (sb & 1) * (PW * XS);
+        if (sb + 1 < nsub) stage_sub(xs + ((sb + 1) & 1) * (PW * XS), a.U, a.ldu, col, r0 + int64_t(sb + 1) * SUB, r1);
+        cp_commit();
+        cp_wait<1>();
         __syncthreads();
 #pragma unroll
         for (int kk = 0; kk < SUB; kk += 4) {
             // A = X^T (i = column, k = row), B = X (k = row, j = column)
-            const double a0 = xs[(wi + g) * XS + kk + t];
-            const double a1 = xs[(wi + g + 8) * XS + kk + t];
+            const double a0 = cur[(wi + g) * XS + kk + t];
+            const double a1 = cur[(wi + g + 8) * XS + kk + t];
 #pragma unroll
-            for (int ni = 0; ni < 2; ++ni) dmma(acc[ni], a0, a1, xs[(wj + ni * 8 + g) * XS + kk + t]);
+            for (int ni = 0; ni < 2; ++ni) dmma(acc[ni], a0, a1, cur[(wj + ni * 8 + g) * XS + kk + t]);
         }
+        __syncthreads();
     }
+    cp_wait<0>();
     const int slot = rnd % RING;
     double* out = a.gws + ((int64_t(slot) * a.per + q) * a.nch + ch) * (PW * PW);
 #pragma unroll
@@ -374,8 +407,8 @@ __device__ void eig_pair(const BJArgs& a, int q, int rnd, double* smem) {
 
 // ---- phase 3: X_p(rows of the chunk) <- X_p Q_p
 __device__ void update_unit(const BJArgs& a, int q, int rnd, int ch, double* smem, const int* col) {
-    double* xs = smem;            // PW x XS
-    double* qs = smem + PW * XS;  // PW x QS: qs[j * QS + k] = Q(k, j)
+    double* xs = smem;                // 2 x PW x XS (double-buffered sub-tiles)
+    double* qs = smem + 2 * PW * XS;  // PW x QS: qs[j * QS + k] = Q(k, j)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
     const double* qg = a.qws + (int64_t(rnd % RING) * a.per + q) * (PW * PW);
@@ -386,9 +419,16 @@ __device__ void update_unit(const BJArgs& a, int q, int rnd, int ch, double* sme
     }
     const int64_t r0 = int64_t(ch) * a.rch, r1 = min(a.m, r0 + a.rch);
     const int wr = warp * 16;  // the warp's 16 rows of the 64-row sub-tile
-    for (int64_t r = r0; r < r1; r += SUB) {
-        __syncthreads();
-        load_sub(xs, a.U, a.ldu, col, r, r1);
+    const int nsub = int((r1 - r0 + SUB - 1) / SUB);
+    __syncthreads();
+    stage_sub(xs, a.U, a.ldu, col, r0, r1);
+    cp_commit();
+    for (int sb = 0; sb < nsub; ++sb) {
+        const int64_t r = r0 + int64_t(sb) * SUB;
+        double* cur = xs + (sb & 1) * (PW * XS);
+        if (sb + 1 < nsub) stage_sub(xs + ((sb + 1) & 1) * (PW * XS), a.U, a.ldu, col, r + SUB, r1);
+        cp_commit();
+        cp_wait<1>();
         __syncthreads();
         double acc[4][4];
 #pragma unroll
@@ -398,8 +438,8 @@ __device__ void update_unit(const BJArgs& a, int q, int rnd, int ch, double* sme
 #pragma unroll
         for (int kk = 0; kk < PW; kk += 4) {
             // A = X (i = row, k = column): xs[k * XS + i]
-            const double a0 = xs[(kk + t) * XS + wr + g];
-            const double a1 = xs[(kk + t) * XS + wr + g + 8];
+            const double a0 = cur[(kk + t) * XS + wr + g];
+            const double a1 = cur[(kk + t) * XS + wr + g + 8];
 #pragma unroll
             for (int ni = 0; ni < 4; ++ni) dmma(acc[ni], a0, a1, qs[(ni * 8 + g) * QS + kk + t]);
         }
@@ -410,7 +450,7 @@ __device__ void update_unit(const BJArgs& a, int q, int rnd, int ch, double* sme
             for (int v = 0; v < 4; ++v) {
                 const int i = wr + g + ((v & 2) ? 8 : 0);
                 const int j = ni * 8 + 2 * t + (v & 1);
-                xs[j * XS + i] = acc[ni][v];
+                cur[j * XS + i] = acc[ni][v];
             }
         __syncthreads();
 #pragma unroll
@@ -418,12 +458,14 @@ __device__ void update_unit(const BJArgs& a, int q, int rnd, int ch, double* sme
             const int i = e & (SUB - 1), j = e / SUB;
             const int64_t gi = r + i;
             const int cj = col[j];
-            if (cj >= 0 && gi < r1) __stcg(a.U + gi + int64_t(cj) * a.ldu, xs[j * XS + i]);
+            if (cj >= 0 && gi < r1) __stcg(a.U + gi + int64_t(cj) * a.ldu, cur[j * XS + i]);
         }
+        __syncthreads();  // cur is refilled by the next iteration's staging
     }
+    cp_wait<0>();
 }
 
-constexpr int SMEM_DOUBLES = PW * XS + PW * QS > 2 * PW * GS ? PW * XS + PW * QS : 2 * PW * GS;
+constexpr int SMEM_DOUBLES = 2 * PW * XS + PW * QS > 2 * PW * GS ? 2 * PW * XS + PW * QS : 2 * PW * GS;
 
 // One sweep as a dataflow over work items taken in a fixed global order
 // (round-major; per round the Gram units, then the update units), so
