@@ -111,6 +111,21 @@ hydot_status hydot_fields_solve(hydot_ctx ctx, const hydot_grid7* grid, int n_la
                                 double tol, int max_iter, int fixed_iters, double* out_dev,
                                 int* iters_h, double* relres_h);
 
+/* experiments::full_diffusion_forward (experiments.cpp:154-206; the
+ * nonlinear forward model) for the 7-point operator: per wavelength l and
+ * source s, x_tot solves (K + (sigma_l + dsigma_l mu(v)) M + sigma'_l R) x =
+ * e_{source_vertex[s]} and x_inc the same with mu = 0;
+ * y_total[(s*n_det + d)*n_lambda + l] = inv_D_l x_tot(detector_vertex[s*n_det + d]),
+ * y_incident likewise (y_scattered = y_total - y_incident).  dsigma_l =
+ * (sum_c c_pert_c eps_c(lambda_l)) nu / D_l; mu_dev: N vertex values
+ * (pals::shape).  Both solves use the same batched CG, so mu = 0 gives
+ * y_total == y_incident bitwise.  Outputs are device arrays. */
+hydot_status hydot_full_forward(hydot_ctx ctx, const hydot_grid7* grid, int n_lambda, const double* sigma_h,
+                                const double* sigma_prime_h, const double* inv_D_h, const double* dsigma_h,
+                                const double* mu_dev, const int64_t* source_vertex_h, int n_sources,
+                                const int64_t* detector_vertex_h, int n_det, double tol, int max_iter,
+                                int fixed_iters, double* y_total_dev, double* y_incident_dev, int* iters_max_h);
+
 /* y = A_l x for one shift (the operator the CG applies; for tests). */
 hydot_status hydot_apply7(hydot_ctx ctx, const hydot_grid7* grid, double sigma,
                           double sigma_prime, const double* x_dev, double* y_dev);

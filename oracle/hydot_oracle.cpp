@@ -587,7 +587,10 @@ struct Grid7 {
     bool dirichlet(int ix, int iy) const { return ix == 0 || ix == nx - 1 || iy == 0 || iy == ny - 1; }
 };
 
-static void apply7(const Grid7& g, double sigma, double sigmap, const double* x, double* y) {
+// mu (optional): the nonlinear forward model's perturbed medium, absorption
+// sigma + dsig mu_i per vertex (experiments.cpp:154-206, w = nu (mu_bg + dmu mu) / D)
+static void apply7(const Grid7& g, double sigma, double sigmap, const double* x, double* y,
+                   const double* mu = nullptr, double dsig = 0.0) {
     const double h = g.h;
     for (int iz = 0; iz < g.nz; ++iz) {
         const bool zb = (iz == 0 || iz == g.nz - 1);
@@ -621,7 +624,8 @@ static void apply7(const Grid7& g, double sigma, double sigmap, const double* x,
                     wsum = wsum + h;
                     nb = nb + h * x[i + plane];
                 }
-                double diag = wsum + sigma * V + sigmap * S;
+                const double sg = mu ? sigma + dsig * mu[i] : sigma;
+                double diag = wsum + sg * V + sigmap * S;
                 y[i] = diag * x[i] - nb;
             }
     }
@@ -631,7 +635,8 @@ static void apply7(const Grid7& g, double sigma, double sigmap, const double* x,
 // by CG on the SPD system).  Returns iterations used.  If fixed_iters > 0,
 // runs exactly that many iterations (parity mode).
 static int cg_solve(const Grid7& g, double sigma, double sigmap, const double* b, double* x,
-                    double tol, int max_iter, int fixed_iters, double* relres_out) {
+                    double tol, int max_iter, int fixed_iters, double* relres_out,
+                    const double* mu = nullptr, double dsig = 0.0) {
     const int64_t N = g.N();
     std::vector<double> r(b, b + N), p(b, b + N), q(static_cast<size_t>(N));
     std::fill(x, x + N, 0.0);
@@ -650,7 +655,7 @@ static int cg_solve(const Grid7& g, double sigma, double sigmap, const double* b
     }
     int limit = fixed_iters > 0 ? fixed_iters : max_iter;
     for (it = 0; it < limit;) {
-        apply7(g, sigma, sigmap, p.data(), q.data());
+        apply7(g, sigma, sigmap, p.data(), q.data(), mu, dsig);
         double pq = dot(p.data(), q.data());
         double alpha = rr / pq;
         for (int64_t i = 0; i < N; ++i) {
@@ -748,10 +753,25 @@ int oracle_apply7(int nx, int ny, int nz, double h, double sigma, double sigmap,
 
 // Fields for n_rhs unit-vertex sources x n_lambda shifts; out is
 // N x (n_rhs*nl), column k*nl+l, scaled by inv_D[l] (born.cpp:54-65).
+// dsig / mu non-null: the perturbed medium sigma_l + dsig_l mu(v) (the
+// nonlinear forward model's fields, experiments.cpp:154-206)
+int oracle_fields_var(int nx, int ny, int nz, double h, int nl, const double* sigma, const double* sigmap,
+                      const double* inv_D, const double* dsig, const double* mu, const int64_t* rhs_vertex,
+                      int n_rhs, double tol, int max_iter, int fixed_iters, int threads, double* out, int* iters,
+                      double* relres);
+
 int oracle_fields(int nx, int ny, int nz, double h, int nl, const double* sigma,
                   const double* sigmap, const double* inv_D, const int64_t* rhs_vertex, int n_rhs,
                   double tol, int max_iter, int fixed_iters, int threads, double* out, int* iters,
                   double* relres) {
+    return oracle_fields_var(nx, ny, nz, h, nl, sigma, sigmap, inv_D, nullptr, nullptr, rhs_vertex, n_rhs, tol,
+                             max_iter, fixed_iters, threads, out, iters, relres);
+}
+
+int oracle_fields_var(int nx, int ny, int nz, double h, int nl, const double* sigma, const double* sigmap,
+                      const double* inv_D, const double* dsig, const double* mu, const int64_t* rhs_vertex,
+                      int n_rhs, double tol, int max_iter, int fixed_iters, int threads, double* out, int* iters,
+                      double* relres) {
     return guard([&] {
         Grid7 g{nx, ny, nz, h};
         const int64_t N = g.N();
@@ -773,7 +793,7 @@ int oracle_fields(int nx, int ny, int nz, double h, int nl, const double* sigma,
                     double* x = out + int64_t(k) * N;
                     double rr;
                     int it = cg_solve(g, sigma[l], sigmap[l], b.data(), x, tol, max_iter,
-                                      fixed_iters, &rr);
+                                      fixed_iters, &rr, mu, dsig ? dsig[l] : 0.0);
                     for (int64_t i = 0; i < N; ++i) x[i] *= inv_D[l];
                     if (iters) iters[k] = it;
                     if (relres) relres[k] = rr;

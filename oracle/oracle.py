@@ -48,6 +48,9 @@ def lib():
         L.oracle_fields.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, _dp, _dp,
                                     _dp, _i64p, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
                                     _dp, _ip, _dp]
+        L.oracle_fields_var.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, _dp, _dp, _dp, _dp,
+                                        _dp, _i64p, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, _dp, _ip,
+                                        _dp]
         L.oracle_factor_free.argtypes = [C.c_void_p]
         L.oracle_factor_info.argtypes = [C.c_void_p, _i64p, _i64p, _i64p, _dp, _ip, _ip]
         L.oracle_factor_get.argtypes = [C.c_void_p, _dp, _dp]
@@ -163,6 +166,46 @@ def fields(shape, h, sigma, sigmap, inv_D, rhs_vertex, tol=1e-10, max_iter=10000
                                fixed_iters, threads, _d(out), iters.ctypes.data_as(_ip),
                                _d(rel)))
     return out, iters, rel
+
+
+def fields_var(shape, h, sigma, sigmap, inv_D, dsig, mu, rhs_vertex, tol=1e-10, max_iter=10000,
+               fixed_iters=0, threads=1):
+    """Fields of the perturbed medium sigma_l + dsig_l mu(v) (the nonlinear
+    forward model's solves, experiments.cpp:154-206); layout as fields()."""
+    nx, ny, nz = shape
+    N = nx * ny * nz
+    nl = len(sigma)
+    rv = np.ascontiguousarray(rhs_vertex, dtype=np.int64)
+    out = np.empty((N, len(rv) * nl), dtype=np.float64, order="F")
+    iters = np.zeros(len(rv) * nl, dtype=np.int32)
+    rel = np.zeros(len(rv) * nl, dtype=np.float64)
+    _check(lib().oracle_fields_var(nx, ny, nz, h, nl, _d(_f64(sigma)), _d(_f64(sigmap)), _d(_f64(inv_D)),
+                                   _d(_f64(dsig)), _d(_f64(mu)), rv.ctypes.data_as(_i64p), len(rv), tol,
+                                   max_iter, fixed_iters, threads, _d(out), iters.ctypes.data_as(_ip),
+                                   _d(rel)))
+    return out, iters, rel
+
+
+def full_forward(shape, h, sigma, sigmap, inv_D, dsig, mu, source_vertex, detector_vertex, tol=1e-10,
+                 fixed_iters=0, threads=1):
+    """experiments::full_diffusion_forward (experiments.cpp:154-206) for the
+    7-point operator: y_total / y_incident at the detector vertices,
+    measurement (s, d, l) -> (s * n_det + d) * n_lambda + l."""
+    nl = len(sigma)
+    src = np.asarray(source_vertex, dtype=np.int64)
+    det = np.asarray(detector_vertex, dtype=np.int64).reshape(len(src), -1)
+    nd = det.shape[1]
+    outs = []
+    for ds in (np.asarray(dsig, dtype=np.float64), np.zeros(nl)):
+        F, it, rel = fields_var(shape, h, sigma, sigmap, inv_D, ds, mu, src, tol=tol, fixed_iters=fixed_iters,
+                                threads=threads)
+        y = np.empty(len(src) * nd * nl)
+        for s in range(len(src)):
+            for d in range(nd):
+                for l in range(nl):
+                    y[(s * nd + d) * nl + l] = F[det[s, d], s * nl + l]
+        outs.append(y)
+    return outs[0], outs[1], outs[0] - outs[1]
 
 
 class Factor:

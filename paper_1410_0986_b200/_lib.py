@@ -133,6 +133,8 @@ SIGNATURES = {
     "hydot_recompress": (C.c_int, [_vp, _vp, C.c_double, C.c_int, C.POINTER(_vp),
                                    C.POINTER(Ledger)]),
     "hydot_lr_matmat": (C.c_int, [_vp, _vp, C.c_int, C.c_int, _dp, C.c_int64, _dp, C.c_int64]),
+    "hydot_full_forward": (C.c_int, [_vp, C.POINTER(Grid7), C.c_int, _dp, _dp, _dp, _dp, _dp, _i64p, C.c_int,
+                                     _i64p, C.c_int, C.c_double, C.c_int, C.c_int, _dp, _dp, _ip]),
     "hydot_comm_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
     "hydot_comm_create": (C.c_int, [_vp, C.c_int, C.c_int, C.POINTER(C.c_ubyte), C.POINTER(_vp)]),
     "hydot_comm_destroy": (C.c_int, [_vp]),

@@ -119,6 +119,44 @@ class StreamedFieldsProvider:
         return B
 
 
+@dataclass
+class FullForward:
+    """experiments::FullForward (experiments.hpp:39-45)."""
+    y_total: torch.Tensor
+    y_incident: torch.Tensor
+    y_scattered: torch.Tensor
+    iters_max: int
+
+
+def full_diffusion_forward(ctx: Context, grid: Grid7, sigma, sigma_prime, inv_D, dsigma, mu: torch.Tensor,
+                           source_vertex, detector_vertex, tol: float = 1e-10, max_iter: int = 20000,
+                           fixed_iters: int = 0) -> FullForward:
+    """full_diffusion_forward (experiments.cpp:154-206) on the device for the
+    7-point operator: the perturbed medium sigma_l + dsigma_l mu(v) and the
+    background, detector values (measurement (s, d, l) -> (s n_det + d)
+    n_lambda + l).  dsigma_l = nu (sum_c c_pert_c eps_c(lambda_l)) / D_l."""
+    sig = np.ascontiguousarray(sigma, dtype=np.float64)
+    sigp = np.ascontiguousarray(sigma_prime, dtype=np.float64)
+    invd = np.ascontiguousarray(inv_D, dtype=np.float64)
+    dsg = np.ascontiguousarray(dsigma, dtype=np.float64)
+    src = np.ascontiguousarray(source_vertex, dtype=np.int64)
+    det = np.ascontiguousarray(detector_vertex, dtype=np.int64).reshape(len(src), -1)
+    nl, ns, nd = sig.size, len(src), det.shape[1]
+    if mu.numel() != grid.N:
+        raise ValueError("full_forward: mu must hold one value per vertex")
+    mu = mu.to(device=f"cuda:{ctx.device}", dtype=torch.float64).contiguous()
+    yt = ctx.empty(ns * nd * nl)
+    yi = ctx.empty(ns * nd * nl)
+    it = C.c_int(0)
+    g = grid.c()
+    dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+    ip64 = lambda a: a.ctypes.data_as(C.POINTER(C.c_int64))
+    check(lib().hydot_full_forward(ctx.h, C.byref(g), nl, dp(sig), dp(sigp), dp(invd), dp(dsg), dptr(mu),
+                                   ip64(src), ns, ip64(det), nd, tol, max_iter, fixed_iters, dptr(yt), dptr(yi),
+                                   C.byref(it)), ctx.h)
+    return FullForward(yt, yi, yt - yi, it.value)
+
+
 def apply_operator(ctx: Context, grid: Grid7, sigma: float, sigma_prime: float,
                    x: torch.Tensor) -> torch.Tensor:
     y = torch.empty_like(x)

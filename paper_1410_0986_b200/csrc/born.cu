@@ -44,7 +44,26 @@ __global__ void born_block_k(int64_t N, int nl, const double* __restrict__ inc,
     }
 }
 
+// y[(s nd + d) nl + l] = F[s][l][det[s nd + d]]: detector values of point
+// fields (interpolate at a vertex, grid.cpp; measurement_index order
+// born.hpp:35-37)
+__global__ void gather_measure_k(int ns, int nd, int nl, int64_t N, const double* __restrict__ F,
+                                 const int64_t* __restrict__ det, double* __restrict__ y) {
+    const int total = ns * nd * nl;
+    for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < total; m += gridDim.x * blockDim.x) {
+        const int l = m % nl, sd = m / nl, s = sd / nd;
+        y[m] = F[(int64_t(s) * nl + l) * N + det[sd]];
+    }
+}
+
 }  // namespace
+
+void gather_measure(Ctx& c, int ns, int nd, int nl, int64_t N, const double* F, const int64_t* det_dev, double* y) {
+    const int total = ns * nd * nl;
+    const int blocks = std::max(1, std::min((total + 255) / 256, c.num_sms * 4));
+    gather_measure_k<<<blocks, 256, 0, c.stream>>>(ns, nd, nl, N, F, det_dev, y);
+    c.check_launch();
+}
 
 void born_block(Ctx& c, int64_t N, int nl, const double* inc, const double* const* adj_h, int nd,
                 const double* w, double nu, double* out, int64_t ld) {

@@ -247,6 +247,22 @@ hydot_status hydot_fields_solve(hydot_ctx ctx, const hydot_grid7* grid, int n_la
     });
 }
 
+hydot_status hydot_full_forward(hydot_ctx ctx, const hydot_grid7* grid, int n_lambda, const double* sigma_h,
+                                const double* sigma_prime_h, const double* inv_D_h, const double* dsigma_h,
+                                const double* mu_dev, const int64_t* source_vertex_h, int n_sources,
+                                const int64_t* detector_vertex_h, int n_det, double tol, int max_iter,
+                                int fixed_iters, double* y_total_dev, double* y_incident_dev, int* iters_max_h) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!grid || !sigma_h || !sigma_prime_h || !inv_D_h || !dsigma_h || !mu_dev || !source_vertex_h ||
+            !detector_vertex_h || !y_total_dev || !y_incident_dev)
+            throw std::invalid_argument("full_forward: null argument");
+        full_forward(c, *grid, n_lambda, sigma_h, sigma_prime_h, inv_D_h, dsigma_h, mu_dev, source_vertex_h,
+                     n_sources, detector_vertex_h, n_det, tol, max_iter, fixed_iters, y_total_dev, y_incident_dev,
+                     iters_max_h);
+    });
+}
+
 hydot_status hydot_apply_fem(hydot_ctx ctx, const hydot_grid_geom* geom, double sigma, double sigma_prime,
                              const double* x_dev, double* y_dev) {
     return guard(ctx ? ctx->c.get() : nullptr, [&] {

@@ -190,8 +190,21 @@ __device__ __forceinline__ double sum_parts(const double* __restrict__ parts, in
 struct Op7 {
     Stencil g;
     template <class Get>
-    __device__ __forceinline__ double operator()(int64_t i, double sigma, double sigmap, Get get) const {
+    __device__ __forceinline__ double operator()(int64_t i, double sigma, double sigmap, int, Get get) const {
         return stencil_at(g, sigma, sigmap, i, get);
+    }
+};
+
+// Op7Var: the same operator with a per-vertex absorption -- the lumped mass
+// weighted by sigma_l + dsig_l mu(v) (the nonlinear forward model's
+// K + M_w + sp R with w = nu (mu_bg + dmu_l mu) / D, experiments.cpp:154-206)
+struct Op7Var {
+    Stencil g;
+    const double* __restrict__ mu;    // N
+    const double* __restrict__ dsig;  // n_lambda
+    template <class Get>
+    __device__ __forceinline__ double operator()(int64_t i, double sigma, double sigmap, int l, Get get) const {
+        return stencil_at(g, __dadd_rn(sigma, __dmul_rn(dsig[l], mu[i])), sigmap, i, get);
     }
 };
 
@@ -207,7 +220,7 @@ struct OpFem {
     float inv_nx, inv_ny;
     const double* __restrict__ em;  // Ke (64) | Me (64) | Re (16)
     template <class Get>
-    __device__ __forceinline__ double operator()(int64_t i, double sigma, double sigmap, Get get) const {
+    __device__ __forceinline__ double operator()(int64_t i, double sigma, double sigmap, int, Get get) const {
         unsigned q1, ux, uy, uz;
         fdivmod(unsigned(i), unsigned(nx), inv_nx, q1, ux);
         fdivmod(q1, unsigned(ny), inv_ny, uz, uy);
@@ -357,7 +370,7 @@ __global__ void __launch_bounds__(CT, 4) cg_pa(Op op, int64_t N, int nl, int k0,
         const int64_t i = base + int64_t(k) * CT;
         if (i < N) {
             const double pi = pnew(i);
-            const double ap = op(i, sigma, sigmap, pnew);
+            const double ap = op(i, sigma, sigmap, l, pnew);
             p[i] = pi;
             acc += pi * ap;
         }
@@ -395,7 +408,7 @@ __global__ void __launch_bounds__(CT, 4) cg_xr(Op op, int64_t N, int nl, int k0,
     for (int k = 0; k < VPT; ++k) {
         const int64_t i = base + int64_t(k) * CT;
         if (i < N) {
-            const double q = op(i, sigma, sigmap, getp);
+            const double q = op(i, sigma, sigmap, l, getp);
             x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
             const double rn = __dsub_rn(r[i], __dmul_rn(alpha, q));
             r[i] = rn;
@@ -927,7 +940,7 @@ __global__ void apply_k(Op op, int64_t N, double sigma, double sigmap, const dou
     auto get = [&](int64_t j) { return x[j]; };
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < N;
          i += int64_t(gridDim.x) * blockDim.x)
-        y[i] = op(i, sigma, sigmap, get);
+        y[i] = op(i, sigma, sigmap, 0, get);
 }
 
 __global__ void count_active(int n, const SysState* __restrict__ st, int* __restrict__ out) {
@@ -1150,6 +1163,30 @@ void fields_solve(Ctx& c, const hydot_grid7& g, int nl, const double* sigma, con
     }
     cg_batch(c, Op7{make_stencil(g)}, N, nl, sigma, sigmap, inv_D, ridx, rw, b2, n_rhs, tol, max_iter,
              fixed_iters, out, stats);
+}
+
+// fields of the perturbed medium: sigma_l + dsig_l mu(v) per vertex (mu, dsig
+// device arrays; the vertex-parallel kernels -- this is not the hot path)
+void fields_solve_var(Ctx& c, const hydot_grid7& g, int nl, const double* sigma, const double* sigmap,
+                      const double* inv_D, const double* dsig_dev, const double* mu_dev, const int64_t* rhs_vertex,
+                      int n_rhs, double tol, int max_iter, int fixed_iters, double* out, CGStats* stats) {
+    check_grid(g.nx, g.ny, g.nz);
+    if (g.h <= 0) throw std::invalid_argument("fields_solve: bad grid");
+    if (nl <= 0 || n_rhs <= 0) throw std::invalid_argument("compute_fields: no wavelengths");
+    const int64_t N = int64_t(g.nx) * g.ny * g.nz;
+    std::vector<int64_t> ridx(size_t(n_rhs) * 8, -1);
+    std::vector<double> rw(size_t(n_rhs) * 8, 0.0), b2(size_t(n_rhs), 1.0);
+    for (int s = 0; s < n_rhs; ++s) {
+        int64_t v = rhs_vertex[s];
+        if (v < 0 || v >= N) throw std::invalid_argument("point_source_vector: point outside domain");
+        int ix = int(v % g.nx), iy = int((v / g.nx) % g.ny);
+        if (ix == 0 || ix == g.nx - 1 || iy == 0 || iy == g.ny - 1)
+            throw std::invalid_argument("source support falls entirely on the Dirichlet boundary");
+        ridx[size_t(s) * 8] = v;
+        rw[size_t(s) * 8] = 1.0;
+    }
+    cg_batch(c, Op7Var{make_stencil(g), mu_dev, dsig_dev}, N, nl, sigma, sigmap, inv_D, ridx, rw, b2, n_rhs, tol,
+             max_iter, fixed_iters, out, stats);
 }
 
 // ------------------------------------------------------------- FEM mode --

@@ -230,6 +230,8 @@ void scatter_rows(Ctx& c, int64_t rows, int64_t cols, const double* src, int64_t
                   const int* idx_dev, double* dst, int64_t ldd);  // dst[idx[i],:] = src[i,:]
 
 // born.cu
+// y[(s nd + d) nl + l] = F[s][l][det[s nd + d]] (F: ns x nl x N, device det)
+void gather_measure(Ctx& c, int ns, int nd, int nl, int64_t N, const double* F, const int64_t* det_dev, double* y);
 void born_block(Ctx& c, int64_t N, int nl, const double* inc, const double* const* adj_h, int nd,
                 const double* w, double nu, double* out, int64_t ld);
 
@@ -273,11 +275,23 @@ void fields_solve(Ctx& c, const hydot_grid7& g, int nl, const double* sigma,
                   double tol, int max_iter, int fixed_iters, double* out, CGStats* stats);
 void apply7(Ctx& c, const hydot_grid7& g, double sigma, double sigmap, const double* x,
             double* y);
+// the perturbed medium of the nonlinear forward model: per-vertex absorption
+// sigma_l + dsig_l mu(v) (dsig_dev: n_lambda, mu_dev: N)
+void fields_solve_var(Ctx& c, const hydot_grid7& g, int nl, const double* sigma, const double* sigmap,
+                      const double* inv_D, const double* dsig_dev, const double* mu_dev, const int64_t* rhs_vertex,
+                      int n_rhs, double tol, int max_iter, int fixed_iters, double* out, CGStats* stats);
 // the reference's trilinear-FEM operator K + sigma M + sigma' R (grid.cpp)
 void apply_fem(Ctx& c, const hydot_grid_geom& g, double sigma, double sigmap, const double* x, double* y);
 void fields_solve_fem(Ctx& c, const hydot_grid_geom& g, int nl, const double* sigma, const double* sigmap,
                       const double* inv_D, const double* points, int n_pts, double tol, int max_iter,
                       int fixed_iters, double* out, CGStats* stats);
+
+// forward.cpp: full_diffusion_forward (experiments.cpp:154-206) for the
+// 7-point operator; outputs ns x nd x nl measurements (device)
+void full_forward(Ctx& c, const hydot_grid7& g, int nl, const double* sigma, const double* sigmap,
+                  const double* inv_D, const double* dsigma, const double* mu_dev, const int64_t* src_h, int ns,
+                  const int64_t* det_h, int nd, double tol, int max_iter, int fixed_iters, double* y_tot,
+                  double* y_inc, int* iters_max);
 
 // matmat.cu
 void j_combine(Ctx& c, int64_t M, int b, int nc, int nl, const double* T, int64_t ldt,
