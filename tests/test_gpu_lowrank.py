@@ -362,3 +362,28 @@ def test_library_comm_j_matmat_voxel_single_rank(ctx):
     assert float(torch.max(torch.abs(Xv - Xb))) <= 1e-12 * float(torch.max(torch.abs(Xb)))
     z = torch.arange(6, dtype=torch.float64, device="cuda")
     assert torch.equal(comm.allreduce(z), z)
+
+
+def test_streamed_fields_provider_equals_resident_fields(ctx):
+    """born.StreamedFieldsProvider (config 3's per-source CG -> block -> drop)
+    gives the same compression as the provider over resident fields: every
+    CG system is independent of the batch it runs in."""
+    from paper_1410_0986_b200 import born, configs, lowrank as lr
+    cfg = configs.small_config(n=12, ns_x=2, ns_y=2, n_det=2, n_lambda=4)
+    st = configs.make_setup(cfg)
+    g = st.grid()
+    F, _ = born.compute_fields(ctx, g, st.sigma, st.sigma_prime, st.inv_D, st.points, tol=1e-10)
+    w = torch.full((g.N,), cfg.h ** 3, dtype=torch.float64, device="cuda")
+    tree = lr.ClusterTree(st.source_xy, st.box_lo, st.box_hi)
+    eps = configs.compression_tolerance(st, tree.depth())
+    inc = [F[st.source_point[s]] for s in range(cfg.n_sources)]
+    adj = [[F[st.detector_point[s, d]] for d in range(cfg.n_det)] for s in range(cfg.n_sources)]
+    r1 = lr.recursive_lowrank(ctx, tree, eps, lr.BornFieldsProvider(inc, adj, w, 1.0),
+                              lr.RecursiveOptions(seed=cfg.seed))
+    prov = born.StreamedFieldsProvider(ctx, g, st.sigma, st.sigma_prime, st.inv_D, st.source_vertex,
+                                       st.detector_vertex, w, 1.0, tol=1e-10)
+    r2 = lr.recursive_lowrank(ctx, tree, eps, prov, lr.RecursiveOptions(seed=cfg.seed))
+    assert list(r1.node_rank) == list(r2.node_rank)
+    assert len(prov.log) == cfg.n_sources and max(e["relres_max"] for e in prov.log) <= 1e-10
+    D1, D2 = r1.factor.dense(), r2.factor.dense()
+    assert float(torch.linalg.norm(D1 - D2)) <= 1e-13 * float(torch.linalg.norm(D1))
