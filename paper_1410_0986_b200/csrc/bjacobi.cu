@@ -27,6 +27,7 @@
 // one-sided Jacobi (sigma_j = |x_j|, U = x_j / sigma_j).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <numeric>
 #include <vector>
@@ -59,6 +60,8 @@ struct BJArgs {
     double* U;
     int64_t ldu;
     double tol, flag_tol;
+    int inner_cap;     // inner sweeps per pair visit (kInner)
+    double inner_rel;  // inner threshold relative to the pair's largest off-diagonal (kInnerRel)
     int nch, rch;
     // ring buffers over rounds (slot r % RING): a pair slot's Gram partials,
     // rotation and flag of round r live until round r + RING reuses them
@@ -295,8 +298,8 @@ __device__ void eig_pair(const BJArgs& a, int q, int rnd, double* smem) {
     }
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
-        const double tin = fmax(a.tol, kInnerRel * __longlong_as_double((long long)off0_bits));
-        for (int sw = 0; sw < kInner; ++sw) {
+        const double tin = fmax(a.tol, a.inner_rel * __longlong_as_double((long long)off0_bits));
+        for (int sw = 0; sw < a.inner_cap; ++sw) {
             int rotated = 0;
             for (int r = 0; r < PW - 1; ++r) {
                 // circle-method pair of slot k = lane (k < 16) in round r
@@ -592,6 +595,17 @@ int bjacobi_converge(Ctx& c, int64_t m, int64_t n, double* U, double tol) {
     a.ldu = m;
     a.tol = tol;
     a.flag_tol = 2.0 * tol;  // tol is itself the rounding level of a column dot product
+    // (experiment knobs: HYDOT_BJ_INNER=cap,rel)
+    a.inner_cap = kInner;
+    a.inner_rel = kInnerRel;
+    if (const char* e = std::getenv("HYDOT_BJ_INNER")) {
+        int cap = kInner;
+        double rel = kInnerRel;
+        if (sscanf(e, "%d,%lf", &cap, &rel) >= 1) {
+            a.inner_cap = std::max(1, cap);
+            a.inner_rel = rel;
+        }
+    }
     a.nch = int(nch);
     a.rch = int(rch);
     a.gws = gws.d();
