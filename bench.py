@@ -415,7 +415,18 @@ KERNEL_CLASSES = {
     "skinny_nn": ("hbm", "skinny_nn_k (U Z, b<=16)"),
     "born_block": ("hbm", "born_block_k"),
 }
-TRAFFIC = {}  # filled from profiles/ when an ncu --set full capture exists
+def _load_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of each kernel
+    class, from the committed ncu --set full capture (profiles/traffic_r02.json,
+    written by tools/traffic_from_ncu.py)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "traffic_r02.json")))
+        return {k: v for k, v in d.items() if isinstance(v, dict)}
+    except (OSError, ValueError):
+        return {}
+
+
+TRAFFIC = _load_traffic()
 
 
 def roofline_of(stages, steps):
@@ -435,7 +446,8 @@ def roofline_of(stages, steps):
         ach = v["bytes"] / secs / 1e9
         peak, unit = HBM_PEAK_GBS, "GB/s"
     return {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
-            "traffic": TRAFFIC.get(name), "kernel": what, "stage": name,
+            "traffic": (TRAFFIC.get(name) or {}).get("dram_bytes_per_launch"),
+            "traffic_detail": TRAFFIC.get(name), "kernel": what, "stage": name,
             "ms_per_step": v["ms_per_step"], "launch_groups_per_step": v["calls_per_step"],
             "peak_source": PEAK_SOURCE if bound == "tensor" else "MEASURED_PEAKS.json hbm_gbs"}
 
@@ -741,7 +753,8 @@ def run_pals(args):
     if gem and gem["ms_per_step"] > 0:
         ach = gem["flops"] / (gem["ms_per_step"] * psteps / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": ach / FP64_PEAK_TFLOPS, "traffic": TRAFFIC.get("gemm"), "stage": "gemm",
+                "frac": ach / FP64_PEAK_TFLOPS, "traffic": (TRAFFIC.get("gemm") or {}).get("dram_bytes_per_launch"),
+                "stage": "gemm",
                 "kernel": "dgemm_kernel (DMMA m16n8k4.f64): the J~ / J~^T blocks and the Hmv of the LM step",
                 "peak_source": PEAK_SOURCE}
     roof_jac = None
