@@ -11,15 +11,38 @@ import re
 import sys
 
 
+SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9,
+         "nsecond": 1.0, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1.0, "us": 1e3, "ms": 1e6}
+
+
 def rows(path):
+    """raw-page CSV: header row, units row, one row per launch; values scaled
+    to bytes / nanoseconds"""
     op = gzip.open if path.endswith(".gz") else open
     with op(path, "rt") as f:
         r = list(csv.reader(f))
-    head = r[0]
-    return [dict(zip(head, x)) for x in r[2:] if len(x) == len(head)]
+    head, units = r[0], r[1]
+    out = []
+    for x in r[2:]:
+        if len(x) != len(head):
+            continue
+        d = {}
+        for h, u, v in zip(head, units, x):
+            sc = SCALE.get(u.strip())
+            if sc is not None:
+                try:
+                    d[h] = float(v.replace(",", "")) * sc
+                    continue
+                except ValueError:
+                    pass
+            d[h] = v
+        out.append(d)
+    return out
 
 
 def num(v):
+    if isinstance(v, float):
+        return v
     try:
         return float(str(v).replace(",", ""))
     except ValueError:
