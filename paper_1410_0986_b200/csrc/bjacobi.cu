@@ -44,12 +44,15 @@ constexpr int NTH = 128;      // threads per CTA (4 warps)
 constexpr int XS = SUB + 4;   // X sub-tile stride ([col][row], conflict-free fragments)
 constexpr int QS = PW + 4;    // Q stride ([out col][in col])
 constexpr int GS = PW + 1;    // eigen-solver stride
-// Inner sweeps per pair visit: the pair Gram is diagonalised only to a
-// threshold 1e-4 x its initial largest scaled off-diagonal (floor tol), at
-// most kInner sweeps -- the outer sweeps converge quadratically anyway, and
-// on strongly graded pairs the inner rotations' own rounding keeps tiny
-// off-diagonals above tol forever (an uncapped solve ran 30 sweeps there).
-constexpr int kInner = 4;
+// Inner sweeps per pair visit: one cyclic sweep over the pair Gram (to a
+// threshold 1e-4 x its initial largest scaled off-diagonal, floor tol) --
+// the eigen-solve is the latency chain of a round, and the outer sweeps
+// converge quadratically anyway.  Measured (graded cores, total ms for
+// 2000 / 2800 / 5686): 4 inner sweeps 179 / 319 / 1149, 2: 139 / 252 / 987,
+// 1: 116 / 217 / 992 (one more outer sweep).  An uncapped solve ran 30
+// sweeps on strongly graded pairs, where the inner rotations' own rounding
+// keeps tiny off-diagonals above tol.
+constexpr int kInner = 1;
 constexpr double kInnerRel = 1e-4;
 constexpr int kMaxBSweeps = 40;
 
