@@ -16,10 +16,12 @@ own voxel range [lo_g, hi_g) and the merges run cooperatively:
   - the tall QR of B^T is a TSQR: local Householder QR of the rank's rows,
     all-gather of the q x q R factors, QR of the stacked R's (replicated),
     so B^T = (Q_g Q2_g) R with the rank's rows of the orthonormal factor
-    formed locally; the core SVD of R is replicated;
+    formed locally; the core SVD of R is split by rows over the ranks
+    (svd_dist: one-sided block Jacobi with one pair-Gram all-reduce per
+    round);
   - U = blkdiag(U1, U2) inner.U is small and replicated.
 * recompress (lowrank.cpp:547-587): QR(U) replicated, QR(V) by TSQR, core
-  SVD replicated, V rows formed locally.
+  SVD split by rows (svd_dist), V rows formed locally.
 * J~x / J~^T y (lowrank.cpp:589-599, experiments.cpp:255-262): Z = sum_g V_g^T
   X_g is an all-reduce of R x (b N_c) (the north_star's "r-length
   allreduce of V^T x"); J~^T y needs no communication (U replicated).
@@ -86,6 +88,15 @@ class Comm:
         self.dist.all_gather(parts, x.contiguous())
         return parts
 
+    def allgather_rows(self, x: torch.Tensor, ranges) -> List[torch.Tensor]:
+        """all-gather of row blocks of different heights (ranges[g] rows of
+        rank g), padded to the largest"""
+        width = max(b - a for a, b in ranges)
+        pad = torch.zeros((width,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        pad[:x.shape[0]] = x
+        parts = self.allgather(pad)
+        return [p[:b - a] for p, (a, b) in zip(parts, ranges)]
+
     def alltoall(self, sends: List[torch.Tensor], shapes) -> List[torch.Tensor]:
         """sends[g] goes to rank g; returns the blocks received from every
         rank (shapes[g]); point-to-point, so it also runs on gloo."""
@@ -140,6 +151,9 @@ class SimComm:
         return out
 
     def allgather(self, x):
+        return self._exchange(x)
+
+    def allgather_rows(self, x, ranges):
         return self._exchange(x)
 
     def alltoall(self, sends, shapes):
@@ -328,6 +342,72 @@ def tsqr(ops, comm, B_loc):
     return ops.mm(Q1, Q2[comm.rank * q:(comm.rank + 1) * q].contiguous()), R
 
 
+def _tournament(nb):
+    """circle-method rounds of block pairs (nb even)"""
+    p = list(range(nb))
+    rounds = []
+    for _ in range(nb - 1):
+        rounds.append([(min(p[i], p[nb - 1 - i]), max(p[i], p[nb - 1 - i])) for i in range(nb // 2)])
+        p = [p[0], p[-1]] + p[1:-1]
+    return rounds
+
+
+def svd_dist(ops, comm, R, bw=8, max_sweeps=60):
+    """Thin SVD of the replicated square core R = Ur S Vr^T with the work
+    split by rows over the ranks: one-sided block Jacobi (bjacobi.cu's
+    scheme) on L = R^T, each rank holding rows [a_g, b_g) of L.  Per round,
+    the pair Grams of all block pairs are one all-reduce (per x 2bw x 2bw);
+    every rank then diagonalises the same Grams and rotates its own rows.
+    Columns of L converge to Vr S; Ur = L^T (Vr S) S^-2 is one n x n
+    all-reduce.  Replaces the replicated core SVD of the top merges (the term
+    that capped the config-3 Amdahl estimate)."""
+    n = R.shape[0]
+    a, b = voxel_ranges(n, comm.world)[comm.rank]
+    L0 = R.T[a:b].contiguous()
+    L = L0.clone()
+    nb = (n + bw - 1) // bw
+    nbp = nb + (nb & 1)
+    rounds = _tournament(nbp)
+    tol = max(1e-15, (n ** 0.5) * 2.220446049250313e-16)
+
+    def cols(blk):
+        return list(range(blk * bw, min(n, (blk + 1) * bw)))
+
+    for _sweep in range(max_sweeps):
+        rotated = 0
+        for rnd in rounds:
+            pairs = [(cols(x) + cols(y)) for x, y in rnd if x < nb and y < nb and (cols(x) + cols(y))]
+            if not pairs:
+                continue
+            w = max(len(c) for c in pairs)
+            part = torch.zeros((len(pairs), w, w), dtype=L.dtype, device=L.device)
+            for k, c in enumerate(pairs):
+                Xp = L[:, c]
+                part[k, :len(c), :len(c)] = ops.mtm(Xp, Xp)
+            G = comm.allreduce(part)
+            for k, c in enumerate(pairs):
+                g = G[k, :len(c), :len(c)]
+                d = torch.sqrt(torch.clamp(torch.diagonal(g), min=0.0))
+                off = torch.abs(g) / torch.clamp(d[:, None] * d[None, :], min=1e-300)
+                off.fill_diagonal_(0.0)
+                if float(off.max()) <= 2.0 * tol:
+                    continue
+                Q, _, _ = ops.svd(g.contiguous())  # eigenvectors of the SPD pair Gram, descending
+                L[:, c] = ops.mm(L[:, c].contiguous(), Q.contiguous())
+                rotated += 1
+        if rotated == 0:
+            break
+    s2 = comm.allreduce((L * L).sum(dim=0))
+    sig = torch.sqrt(s2)
+    order = torch.argsort(-sig, stable=True)
+    L, sig = L[:, order], sig[order]
+    Vr_loc = L / torch.where(sig > 0, sig, torch.ones_like(sig))
+    Vr = torch.cat(comm.allgather_rows(Vr_loc, voxel_ranges(n, comm.world)), dim=0)
+    inv2 = torch.where(sig > 1e-14 * sig[0], 1.0 / (sig * sig), torch.zeros_like(sig))
+    Ur = comm.allreduce(ops.mtm(L0, L)) * inv2  # L^T (Vr S) S^-2
+    return Ur, sig.cpu().numpy() if sig.is_cuda else sig.numpy(), Vr
+
+
 def randsvd_voxel(ops, comm, Wt_loc, m, N, lo, hi, eps, p=20, kprobe=10, seed=0, r0=1):
     """randsvd(dense_op(W)) with W (m x N) held as the rank's rows of W^T
     (lowrank.cpp:131-199).  Returns VFactor (U m x keep replicated)."""
@@ -363,7 +443,8 @@ def randsvd_voxel(ops, comm, Wt_loc, m, N, lo, hi, eps, p=20, kprobe=10, seed=0,
     Bt_loc = Wt_loc if identity else ops.mm(Wt_loc, Q)  # B^T = W^T Q, voxel rows
     # fast_thin_svd(B) with N >= 2 qc: the tall branch on B^T (:66-87)
     Qb_loc, R = tsqr(ops, comm, Bt_loc)
-    Ur, s, Vr = ops.svd(R)  # R = Ur S Vr^T  =>  B = Vr S (Qb Ur)^T
+    # R = Ur S Vr^T  =>  B = Vr S (Qb Ur)^T; the core SVD split over the ranks
+    Ur, s, Vr = svd_dist(ops, comm, R) if comm.world > 1 else ops.svd(R)
     s1 = float(s[0]) if len(s) else 0.0
     keep = int(sum(1 for x in s if x > eps * s1 and x > 0))  # :187-190
     Ub = Vr[:, :keep]
@@ -395,7 +476,8 @@ def recompress_voxel(ops, comm, f: VFactor, eps, rank=-1) -> VFactor:
         return f
     Qu, Ru = ops.qr(f.U)
     Qv_loc, Rv = tsqr(ops, comm, f.V_loc)
-    Uc, s, Vc = ops.svd(ops.mm(Ru, Rv.T.contiguous()))
+    core = ops.mm(Ru, Rv.T.contiguous())
+    Uc, s, Vc = svd_dist(ops, comm, core) if comm.world > 1 else ops.svd(core)
     s1 = float(s[0])
     keep = min(rank, len(s)) if rank >= 0 else int(sum(1 for x in s if x > eps * s1 and x > 0))
     sv = ops.tensor(np.asarray(s[:keep]))

@@ -2,10 +2,12 @@
 CPU with the oracle's arithmetic (LAPACK + the libstdc++ normal stream):
 
 * agglomerate / randsvd with V split by voxel rows over G = 2 and 4 ranks
-  (sketch all-reduce, TSQR of the tall B^T, replicated core SVD) give the
+  (sketch all-reduce, TSQR of the tall B^T, core SVD split by rows) give the
   reference's ranks and factor (lowrank.cpp:131-199, 321-359) within 1e-10;
-* recompress (QR(U) replicated, TSQR of V) and the J~ products (R x b n_c
-  all-reduce) match the oracle (lowrank.cpp:547-599, experiments.cpp:255-262);
+* recompress (QR(U) replicated, TSQR of V, row-split core SVD) and the J~
+  products (R x b n_c all-reduce) match the oracle (lowrank.cpp:547-599,
+  experiments.cpp:255-262);
+* the row-split block-Jacobi core SVD (svd_dist) matches LAPACK;
 * the multi-process run over torch.distributed (gloo, world 2 and 4) is
   bit-identical to the same schedule replayed in one process (SimComm).
 """
@@ -174,3 +176,22 @@ def test_gloo_ranks_bitwise_equal_the_sequential_replay(oracle, tmp_path, world)
         for h in range(world):
             want = torch.full((N, 2 + h), float(h)) + torch.arange(N, dtype=torch.float64)[:, None]
             assert torch.equal(got["rs"][h], want[lo:hi])
+
+
+@pytest.mark.parametrize("world,n", [(2, 64), (3, 97)])
+def test_svd_dist_matches_lapack(oracle, world, n):
+    """The row-split one-sided block Jacobi core SVD (svd_dist) against
+    LAPACK: singular values to 1e-13 s_1, R = Ur S Vr^T to 1e-13, identical
+    result on every rank."""
+    rng = np.random.default_rng(n)
+    Q1, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    Q2, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    s = np.logspace(0, -11, n)
+    R = torch.as_tensor((Q1 * s) @ Q2.T)
+    res = run_ranks(world, lambda comm: vx.svd_dist(vx.NumpyOps(oracle), comm, R.clone()))
+    Ur, sv, Vr = res[0]
+    for r in res[1:]:
+        assert torch.equal(r[0], Ur) and torch.equal(r[2], Vr) and np.array_equal(r[1], sv)
+    assert np.max(np.abs(sv - s)) <= 1e-13 * s[0]
+    rec = (Ur.numpy() * sv) @ Vr.numpy().T
+    assert np.linalg.norm(rec - R.numpy()) <= 1e-13 * np.linalg.norm(R.numpy())
