@@ -37,13 +37,22 @@
 namespace hydot {
 namespace {
 
-constexpr int BW = 16;        // columns per block
-constexpr int PW = 2 * BW;    // columns per block pair
+// Block width BW = 16 (32-column pairs, warp eigen-solve) or 32 (64-column
+// pairs, CTA eigen-solve: half the block rounds per sweep, so half the passes
+// over a matrix too large for L2).
 constexpr int SUB = 64;       // rows per shared-memory sub-tile
 constexpr int NTH = 128;      // threads per CTA (4 warps)
 constexpr int XS = SUB + 4;   // X sub-tile stride ([col][row], conflict-free fragments)
-constexpr int QS = PW + 4;    // Q stride ([out col][in col])
-constexpr int GS = PW + 1;    // eigen-solver stride
+template <int BW>
+struct Geo {
+    static constexpr int PW = 2 * BW;  // columns per block pair
+    static constexpr int QS = PW + 4;  // Q stride ([out col][in col])
+    static constexpr int GS = PW + 1;  // eigen-solver stride
+    static constexpr int QD = PW / 2;  // a warp's Gram quadrant (QD x QD)
+    static constexpr int MI = QD / 16, NI = QD / 8;
+    static constexpr int NU = PW / 8;  // update: n8 tiles per warp row block
+    static constexpr int SMEM = 2 * PW * XS + PW * QS > 2 * PW * GS ? 2 * PW * XS + PW * QS : 2 * PW * GS;
+};
 // Inner sweeps per pair visit: one cyclic sweep over the pair Gram (to a
 // threshold 1e-4 x its initial largest scaled off-diagonal, floor tol) --
 // the eigen-solve is the latency chain of a round, and the outer sweeps
@@ -126,31 +135,11 @@ __device__ __forceinline__ int circ(int pos, int r, int np) {
 }
 
 // global column of pair-local column j (-1: padding / dummy block)
+template <int BW>
 __device__ __forceinline__ int pair_col(int2 bp, int j, int n) {
     const int blk = j < BW ? bp.x : bp.y;
     const int c = blk * BW + (j & (BW - 1));
     return c < n ? c : -1;
-}
-
-// load rows [r, r+SUB) of the pair's 32 columns into xs[col][row] (zeros
-// outside), coalesced along rows
-__device__ __forceinline__ void load_sub(double* xs, const double* __restrict__ U, int64_t ldu,
-                                         const int* col, int64_t r, int64_t rend) {
-    constexpr int PER = SUB * PW / NTH;  // 16 loads per thread, all in flight at once
-    double v[PER];
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-        const int e = threadIdx.x + k * NTH;
-        const int i = e & (SUB - 1), j = e / SUB;
-        const int64_t gi = r + i;
-        const int cj = col[j];
-        v[k] = (cj >= 0 && gi < rend) ? __ldcg(U + gi + int64_t(cj) * ldu) : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-        const int e = threadIdx.x + k * NTH;
-        xs[(e / SUB) * XS + (e & (SUB - 1))] = v[k];
-    }
 }
 
 __device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool pred) {
@@ -165,6 +154,7 @@ __device__ __forceinline__ void cp_wait() {
 
 // asynchronous load_sub: the copies land in xs while the previous sub-tile
 // is processed (double buffering inside a unit)
+template <int PW>
 __device__ __forceinline__ void stage_sub(double* xs, const double* __restrict__ U, int64_t ldu,
                                           const int* col, int64_t r, int64_t rend) {
 #pragma unroll
@@ -180,36 +170,51 @@ __device__ __forceinline__ void stage_sub(double* xs, const double* __restrict__
 
 // ---- phase 1: partial Gram of one (pair, row chunk) unit; the CTA that
 // completes a pair's last chunk diagonalises its Gram
+template <int BW>
 __device__ void eig_pair(const BJArgs& a, int q, int rnd, double* smem);
 
+template <int BW>
 __device__ void gram_unit(const BJArgs& a, int2 bp, int q, int rnd, int ch, double* smem, int* col) {
+    using Gm = Geo<BW>;
+    constexpr int PW = Gm::PW, QD = Gm::QD, MI = Gm::MI, NI = Gm::NI;
     double* xs = smem;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const int wi = (warp & 1) * 16, wj = (warp >> 1) * 16;
-    double acc[2][4];
+    const int wi = (warp & 1) * QD, wj = (warp >> 1) * QD;
+    double acc[MI][NI][4];
 #pragma unroll
-    for (int x = 0; x < 2; ++x)
+    for (int x = 0; x < MI; ++x)
 #pragma unroll
-        for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+        for (int y = 0; y < NI; ++y)
+#pragma unroll
+            for (int z = 0; z < 4; ++z) acc[x][y][z] = 0.0;
     const int64_t r0 = int64_t(ch) * a.rch, r1 = min(a.m, r0 + a.rch);
     const int nsub = int((r1 - r0 + SUB - 1) / SUB);
     __syncthreads();
-    stage_sub(xs, a.U, a.ldu, col, r0, r1);
+    stage_sub<PW>(xs, a.U, a.ldu, col, r0, r1);
     cp_commit();
     for (int sb = 0; sb < nsub; ++sb) {
         const double* cur = xs + (sb & 1) * (PW * XS);
-        if (sb + 1 < nsub) stage_sub(xs + ((sb + 1) & 1) * (PW * XS), a.U, a.ldu, col, r0 + int64_t(sb + 1) * SUB, r1);
+        if (sb + 1 < nsub)
+            stage_sub<PW>(xs + ((sb + 1) & 1) * (PW * XS), a.U, a.ldu, col, r0 + int64_t(sb + 1) * SUB, r1);
         cp_commit();
         cp_wait<1>();
         __syncthreads();
 #pragma unroll
         for (int kk = 0; kk < SUB; kk += 4) {
             // A = X^T (i = column, k = row), B = X (k = row, j = column)
-            const double a0 = cur[(wi + g) * XS + kk + t];
-            const double a1 = cur[(wi + g + 8) * XS + kk + t];
+            double a0[MI], a1[MI];
 #pragma unroll
-            for (int ni = 0; ni < 2; ++ni) dmma(acc[ni], a0, a1, cur[(wj + ni * 8 + g) * XS + kk + t]);
+            for (int mi = 0; mi < MI; ++mi) {
+                a0[mi] = cur[(wi + mi * 16 + g) * XS + kk + t];
+                a1[mi] = cur[(wi + mi * 16 + g + 8) * XS + kk + t];
+            }
+#pragma unroll
+            for (int ni = 0; ni < NI; ++ni) {
+                const double b0 = cur[(wj + ni * 8 + g) * XS + kk + t];
+#pragma unroll
+                for (int mi = 0; mi < MI; ++mi) dmma(acc[mi][ni], a0[mi], a1[mi], b0);
+            }
         }
         __syncthreads();
     }
@@ -217,13 +222,15 @@ __device__ void gram_unit(const BJArgs& a, int2 bp, int q, int rnd, int ch, doub
     const int slot = rnd % RING;
     double* out = a.gws + ((int64_t(slot) * a.per + q) * a.nch + ch) * (PW * PW);
 #pragma unroll
-    for (int ni = 0; ni < 2; ++ni)
+    for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const int i = wi + g + ((v & 2) ? 8 : 0);
-            const int j = wj + ni * 8 + 2 * t + (v & 1);
-            __stcg(out + i + j * PW, acc[ni][v]);
-        }
+        for (int ni = 0; ni < NI; ++ni)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int i = wi + mi * 16 + g + ((v & 2) ? 8 : 0);
+                const int j = wj + ni * 8 + 2 * t + (v & 1);
+                __stcg(out + i + j * PW, acc[mi][ni][v]);
+            }
     __threadfence();
     __syncthreads();
     __shared__ int last;
@@ -239,7 +246,7 @@ __device__ void gram_unit(const BJArgs& a, int2 bp, int q, int rnd, int ch, doub
             wait_geq(a.udone + slot * a.per + q, (rnd / RING) * a.nch);
         }
         __syncthreads();
-        eig_pair(a, q, rnd, smem);
+        eig_pair<BW>(a, q, rnd, smem);
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
@@ -253,7 +260,9 @@ __device__ void gram_unit(const BJArgs& a, int2 bp, int q, int rnd, int ch, doub
 // warp in shared memory (warp barriers only: a CTA barrier per step made the
 // eigen-solve the latency bottleneck of a round).  The eigenvector columns
 // leave sorted by decreasing diagonal.
+template <int BW>
 __device__ void eig_pair(const BJArgs& a, int q, int rnd, double* smem) {
+    constexpr int PW = Geo<BW>::PW, GS = Geo<BW>::GS;
     const int slot = rnd % RING;
     double* G = smem;              // PW x GS
     double* Q = smem + PW * GS;    // PW x GS
@@ -299,9 +308,83 @@ __device__ void eig_pair(const BJArgs& a, int q, int rnd, double* smem) {
         if (threadIdx.x == 0) a.flag[slot * a.per + q] = 0;
         return;
     }
-    if (threadIdx.x < 32) {
+    const double tin = fmax(a.tol, a.inner_rel * __longlong_as_double((long long)off0_bits));
+    if constexpr (BW == 32) {
+        // CTA solve of the 64 x 64 Gram: 32 rotations per round; the row and
+        // column phases are spread over the 4 warps (CTA barriers)
+        __shared__ int rmask[2];
+        for (int sw = 0; sw < a.inner_cap; ++sw) {
+            int rotated = 0;
+            for (int r = 0; r < PW - 1; ++r) {
+                if (threadIdx.x < PW / 2) {
+                    const int k = threadIdx.x;
+                    int p = circ(k, r, PW), o = circ(PW - 1 - k, r, PW);
+                    if (p > o) {
+                        const int tmp = p;
+                        p = o;
+                        o = tmp;
+                    }
+                    const double app = G[p * GS + p], aoo = G[o * GS + o], apo = G[p * GS + o];
+                    double cs = 1.0, sn = 0.0;
+                    bool on = false;
+                    if (apo != 0.0 && fabs(apo) > tin * sqrt(app * aoo)) {
+                        rot2(app, aoo, apo, cs, sn);
+                        on = true;
+                    }
+                    rc[k] = cs;
+                    rs[k] = on ? sn : 0.0;
+                    rp[k] = p;
+                    ro[k] = o;
+                    const unsigned mask = __ballot_sync(0xffffffffu, on);
+                    if (k == 0) rmask[r & 1] = int(__popc(mask));
+                }
+                __syncthreads();
+                const int nrot = rmask[r & 1];
+                if (nrot == 0) continue;  // uniform: no one wrote G this round
+                rotated += nrot;
+                // rows: G <- J^T G; item (slot k, column x)
+                for (int e = threadIdx.x; e < (PW / 2) * PW; e += NTH) {
+                    const int k = e / PW, x = e % PW;
+                    const double sn = rs[k];
+                    if (sn != 0.0) {
+                        const double c = rc[k];
+                        const int p = rp[k], o = ro[k];
+                        const double gp = G[p * GS + x], go = G[o * GS + x];
+                        G[p * GS + x] = c * gp - sn * go;
+                        G[o * GS + x] = sn * gp + c * go;
+                    }
+                }
+                __syncthreads();
+                // columns: G <- G J, Q <- Q J; item (slot k, row x)
+                for (int e = threadIdx.x; e < (PW / 2) * PW; e += NTH) {
+                    const int k = e / PW, x = e % PW;
+                    const double sn = rs[k];
+                    if (sn != 0.0) {
+                        const double c = rc[k];
+                        const int p = rp[k], o = ro[k];
+                        const double gp = G[x * GS + p], go = G[x * GS + o];
+                        G[x * GS + p] = c * gp - sn * go;
+                        G[x * GS + o] = sn * gp + c * go;
+                        const double qp = Q[x * GS + p], qo = Q[x * GS + o];
+                        Q[x * GS + p] = c * qp - sn * qo;
+                        Q[x * GS + o] = sn * qp + c * qo;
+                    }
+                }
+                __syncthreads();
+                if (threadIdx.x < PW / 2 && rs[threadIdx.x] != 0.0) {  // annihilated exactly
+                    G[rp[threadIdx.x] * GS + ro[threadIdx.x]] = 0.0;
+                    G[ro[threadIdx.x] * GS + rp[threadIdx.x]] = 0.0;
+                }
+                __syncthreads();
+            }
+            if (threadIdx.x == 0) {
+                rot_total += rotated;
+                ++sweeps_total;
+            }
+            if (rotated == 0) break;
+        }
+    } else if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
-        const double tin = fmax(a.tol, a.inner_rel * __longlong_as_double((long long)off0_bits));
         for (int sw = 0; sw < a.inner_cap; ++sw) {
             int rotated = 0;
             for (int r = 0; r < PW - 1; ++r) {
@@ -412,7 +495,10 @@ __device__ void eig_pair(const BJArgs& a, int q, int rnd, double* smem) {
 }
 
 // ---- phase 3: X_p(rows of the chunk) <- X_p Q_p
+template <int BW>
 __device__ void update_unit(const BJArgs& a, int q, int rnd, int ch, double* smem, const int* col) {
+    using Gm = Geo<BW>;
+    constexpr int PW = Gm::PW, QS = Gm::QS, NU = Gm::NU;
     double* xs = smem;                // 2 x PW x XS (double-buffered sub-tiles)
     double* qs = smem + 2 * PW * XS;  // PW x QS: qs[j * QS + k] = Q(k, j)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -427,18 +513,18 @@ __device__ void update_unit(const BJArgs& a, int q, int rnd, int ch, double* sme
     const int wr = warp * 16;  // the warp's 16 rows of the 64-row sub-tile
     const int nsub = int((r1 - r0 + SUB - 1) / SUB);
     __syncthreads();
-    stage_sub(xs, a.U, a.ldu, col, r0, r1);
+    stage_sub<PW>(xs, a.U, a.ldu, col, r0, r1);
     cp_commit();
     for (int sb = 0; sb < nsub; ++sb) {
         const int64_t r = r0 + int64_t(sb) * SUB;
         double* cur = xs + (sb & 1) * (PW * XS);
-        if (sb + 1 < nsub) stage_sub(xs + ((sb + 1) & 1) * (PW * XS), a.U, a.ldu, col, r + SUB, r1);
+        if (sb + 1 < nsub) stage_sub<PW>(xs + ((sb + 1) & 1) * (PW * XS), a.U, a.ldu, col, r + SUB, r1);
         cp_commit();
         cp_wait<1>();
         __syncthreads();
-        double acc[4][4];
+        double acc[NU][4];
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
+        for (int x = 0; x < NU; ++x)
 #pragma unroll
             for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
 #pragma unroll
@@ -447,11 +533,11 @@ __device__ void update_unit(const BJArgs& a, int q, int rnd, int ch, double* sme
             const double a0 = cur[(kk + t) * XS + wr + g];
             const double a1 = cur[(kk + t) * XS + wr + g + 8];
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) dmma(acc[ni], a0, a1, qs[(ni * 8 + g) * QS + kk + t]);
+            for (int ni = 0; ni < NU; ++ni) dmma(acc[ni], a0, a1, qs[(ni * 8 + g) * QS + kk + t]);
         }
         __syncthreads();
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
+        for (int ni = 0; ni < NU; ++ni)
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
                 const int i = wr + g + ((v & 2) ? 8 : 0);
@@ -471,7 +557,7 @@ __device__ void update_unit(const BJArgs& a, int q, int rnd, int ch, double* sme
     cp_wait<0>();
 }
 
-constexpr int SMEM_DOUBLES = 2 * PW * XS + PW * QS > 2 * PW * GS ? 2 * PW * XS + PW * QS : 2 * PW * GS;
+
 
 // One sweep as a dataflow over work items taken in a fixed global order
 // (round-major; per round the Gram units, then the update units), so
@@ -480,8 +566,10 @@ constexpr int SMEM_DOUBLES = 2 * PW * XS + PW * QS > 2 * PW * GS ? 2 * PW * XS +
 // previous round's update, an update unit until its pair's eigen-solve is
 // published.  A slow eigen-solve then delays only the pairs that depend on
 // it instead of the whole grid.
-__global__ void __launch_bounds__(NTH, 4) bjacobi_sweep_k(BJArgs a) {
-    __shared__ __align__(16) double smem[SMEM_DOUBLES];
+template <int BW>
+__global__ void __launch_bounds__(NTH, BW == 16 ? 4 : 2) bjacobi_sweep_k(BJArgs a) {
+    constexpr int PW = Geo<BW>::PW;
+    extern __shared__ __align__(16) double smem[];  // Geo<BW>::SMEM doubles
     __shared__ int col[PW];
     __shared__ int item_s;
     const int units = a.per * a.nch;
@@ -498,7 +586,7 @@ __global__ void __launch_bounds__(NTH, 4) bjacobi_sweep_k(BJArgs a) {
         const int u = upd ? rem - units : rem;
         const int q = u / a.nch, ch = u % a.nch;
         const int2 bp = a.pairs[int64_t(rnd) * a.per + q];
-        if (threadIdx.x < PW) col[threadIdx.x] = pair_col(bp, threadIdx.x, a.n);
+        if (threadIdx.x < PW) col[threadIdx.x] = pair_col<BW>(bp, threadIdx.x, a.n);
         if (!upd) {
             if (threadIdx.x == 0) {
                 wait_geq(a.ver + bp.x * a.nch + ch, rnd);
@@ -507,11 +595,11 @@ __global__ void __launch_bounds__(NTH, 4) bjacobi_sweep_k(BJArgs a) {
                 wait_geq(a.epoch + (rnd % RING) * a.per + q, rnd - RING + 1);
             }
             __syncthreads();
-            gram_unit(a, bp, q, rnd, ch, smem, col);
+            gram_unit<BW>(a, bp, q, rnd, ch, smem, col);
         } else {
             if (threadIdx.x == 0) wait_geq(a.epoch + (rnd % RING) * a.per + q, rnd + 1);
             __syncthreads();
-            if (__ldcg(a.flag + (rnd % RING) * a.per + q)) update_unit(a, q, rnd, ch, smem, col);
+            if (__ldcg(a.flag + (rnd % RING) * a.per + q)) update_unit<BW>(a, q, rnd, ch, smem, col);
             __syncthreads();
             if (threadIdx.x == 0) {
                 __threadfence();
@@ -563,7 +651,15 @@ int64_t bjacobi_min_n() {
 // Orthogonalise the columns of U (m x n, ld m, m >= n) in place to the
 // one-sided Jacobi criterion (pairs within flag_tol = 2 tol).  Returns the
 // number of sweeps.
-int bjacobi_converge(Ctx& c, int64_t m, int64_t n, double* U, double tol) {
+namespace {
+template <int BW>
+int bjacobi_run(Ctx& c, int64_t m, int64_t n, double* U, double tol) {
+    constexpr int PW = Geo<BW>::PW;
+    const size_t smem = size_t(Geo<BW>::SMEM) * sizeof(double);
+    static AttrGate attr;
+    attr_once(attr, c.device, [&] {
+        HYDOT_CUDA(cudaFuncSetAttribute(bjacobi_sweep_k<BW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    });
     const int nb = int((n + BW - 1) / BW);
     const int nbp = nb + (nb & 1);
     const int per = nbp / 2, rounds = nbp - 1;
@@ -572,7 +668,7 @@ int bjacobi_converge(Ctx& c, int64_t m, int64_t n, double* U, double tol) {
     HYDOT_CUDA(cudaMemcpyAsync(dpairs.as<void>(), pairs.data(), pairs.size() * sizeof(int2),
                                cudaMemcpyHostToDevice, c.stream));
     int per_sm = 0;
-    HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bjacobi_sweep_k, NTH, 0));
+    HYDOT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bjacobi_sweep_k<BW>, NTH, smem));
     const int max_grid = std::max(1, per_sm) * c.num_sms;
     // row chunks: enough (pair, chunk) units to fill the grid twice
     const int64_t subs = (m + SUB - 1) / SUB;
@@ -625,20 +721,33 @@ int bjacobi_converge(Ctx& c, int64_t m, int64_t n, double* U, double tol) {
     int sweeps = 0;
     for (; sweeps < kMaxBSweeps; ++sweeps) {
         HYDOT_CUDA(cudaMemsetAsync(a.ver, 0, reset * sizeof(int), c.stream));
-        bjacobi_sweep_k<<<grid, NTH, 0, c.stream>>>(a);
+        bjacobi_sweep_k<BW><<<grid, NTH, smem, c.stream>>>(a);
         c.check_launch();
         int st[4] = {0, 0, 0, 0};
         HYDOT_CUDA(cudaMemcpyAsync(st, a.stats, sizeof st, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
         if (bj_stats())
             fprintf(stderr,
-                    "[bjacobi] m=%lld n=%lld sweep=%d pairs_rotated=%d inner_rotations=%d inner_sweeps=%d (of %d "
-                    "pairs) nonfinite=%d\n",
-                    (long long)m, (long long)n, sweeps, st[0], st[1], st[3], per * rounds, st[2]);
+                    "[bjacobi] bw=%d m=%lld n=%lld sweep=%d pairs_rotated=%d inner_rotations=%d inner_sweeps=%d (of "
+                    "%d pairs) nonfinite=%d\n",
+                    BW, (long long)m, (long long)n, sweeps, st[0], st[1], st[3], per * rounds, st[2]);
         if (st[2] > 0) throw std::runtime_error("block Jacobi: non-finite column Gram (input not finite?)");
         if (st[0] == 0) break;
     }
     return sweeps + 1;
+}
+}  // namespace
+
+// Block width by core order: 32-column blocks once the core no longer fits
+// L2 (the sweep is then bound by the passes over the matrix, and BW = 32
+// halves them); 16 below.  HYDOT_BJACOBI_BW overrides (16 / 32).
+int bjacobi_converge(Ctx& c, int64_t m, int64_t n, double* U, double tol) {
+    static const int force = [] {
+        const char* e = std::getenv("HYDOT_BJACOBI_BW");
+        return e ? std::atoi(e) : 0;
+    }();
+    const bool wide = force ? force == 32 : n >= 4000;
+    return wide ? bjacobi_run<32>(c, m, n, U, tol) : bjacobi_run<16>(c, m, n, U, tol);
 }
 
 }  // namespace hydot
