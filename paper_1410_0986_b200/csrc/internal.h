@@ -334,8 +334,7 @@ class RngStream {
     int64_t n_chunks_ = 0;
     int64_t n_normals_ = 0;
     int64_t consumed_ = 0;
-    DBuf chunk_counts_;  // accepted attempts per chunk (device)
-    std::vector<int64_t> chunk_offsets_;
+    DBuf total_;  // accepted pairs of all chunks so far (device; the host keeps a lower bound)
 };
 bool rng_selftest_host();
 

@@ -426,6 +426,52 @@ __global__ void __launch_bounds__(256) rng_normals_k(const uint64_t* __restrict_
     }
 }
 
+// Chunk offsets without a host round trip: one CTA scans the accepted-pair
+// counts of this batch of chunks after the running total of the stream
+// (device-resident), writes each chunk's first pair index and advances the
+// total.  The host only keeps a lower bound of the total (10 sigma below the
+// binomial mean); a batch that falls short of it, or overflows the buffer
+// sized 10 sigma above, is impossible in practice and traps.
+__global__ void __launch_bounds__(1024) rng_scan_k(const int* __restrict__ counts, int nc,
+                                                   int64_t* __restrict__ total, int64_t* __restrict__ offs,
+                                                   int64_t lower_pairs, int64_t cap_pairs) {
+    __shared__ int64_t wsum[32];
+    __shared__ int64_t carry;
+    if (threadIdx.x == 0) carry = *total;
+    __syncthreads();
+    for (int b0 = 0; b0 < nc; b0 += blockDim.x) {
+        const int k = b0 + threadIdx.x;
+        int64_t v = k < nc ? counts[k] : 0;
+        // inclusive warp scan, then across warps
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+        }
+        if (lane == 31) wsum[warp] = v;
+        __syncthreads();
+        if (warp == 0) {
+            int64_t w = lane < int(blockDim.x >> 5) ? wsum[lane] : 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t u = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += u;
+            }
+            wsum[lane] = w;
+        }
+        __syncthreads();
+        const int64_t incl = v + (warp > 0 ? wsum[warp - 1] : 0);
+        const int64_t excl = incl - (k < nc ? counts[k] : 0);
+        if (k < nc) offs[k] = carry + excl;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry += incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        if (carry < lower_pairs || carry > cap_pairs) __trap();  // > 10 sigma off the binomial mean
+        *total = carry;
+    }
+}
+
 // per-ctx device copy of the jump table (grown on demand)
 const uint64_t* device_jumps(Ctx& c, int64_t upto) {
     if (c.jump_n < upto) {
@@ -464,6 +510,15 @@ RngStream::RngStream(Ctx& c, uint64_t seed) : c_(c), seed_(seed) {
 
 RngStream::~RngStream() = default;
 
+// accepted polar pairs per chunk: S/2 attempts, p = pi/4; the host keeps
+// the mean - 10 sigma lower bound, buffers are sized mean + 10 sigma
+namespace {
+constexpr double kPairs = double(mt::S / 2) * 0.7853981633974483;
+inline double pairs_sigma(int64_t nc) {
+    return std::sqrt(double(nc) * double(mt::S / 2) * 0.7853981633974483 * (1.0 - 0.7853981633974483));
+}
+}  // namespace
+
 void RngStream::generate_chunks(int64_t c_end) {
     const int64_t c0 = n_chunks_;
     const int64_t nc = c_end - c0;
@@ -473,42 +528,41 @@ void RngStream::generate_chunks(int64_t c_end) {
     DBuf raw(c_, size_t(nc) * size_t(mt::S) * 8);
     DBuf counts(c_, size_t(nc) * sizeof(int));
     DBuf offs(c_, size_t(nc) * sizeof(int64_t));
+    if (!total_.bytes()) {
+        total_ = DBuf(c_, sizeof(int64_t));
+        HYDOT_CUDA(cudaMemsetAsync(total_.as<void>(), 0, sizeof(int64_t), c_.stream));
+    }
     rng_jump_k<<<unsigned((nc + JCH - 1) / JCH), JPC * JCH, size_t(mt::PREFIX) * 8, c_.stream>>>(
         prefix_.as<uint64_t>(), jumps, c0, nc, windows.as<uint64_t>());
     c_.check_launch();
     rng_generate_k<<<unsigned(nc), 160, 0, c_.stream>>>(windows.as<uint64_t>(), raw.as<uint64_t>(),
                                                         counts.as<int>());
     c_.check_launch();
-    std::vector<int> hc(static_cast<size_t>(nc));
-    HYDOT_CUDA(cudaMemcpyAsync(hc.data(), counts.as<void>(), size_t(nc) * sizeof(int),
-                               cudaMemcpyDeviceToHost, c_.stream));
-    c_.sync();
-    std::vector<int64_t> ho(static_cast<size_t>(nc));
-    int64_t run = n_normals_ / 2;
-    for (int64_t k = 0; k < nc; ++k) {
-        ho[size_t(k)] = run;
-        run += hc[size_t(k)];
-    }
-    const int64_t new_total = 2 * run;
-    HYDOT_CUDA(cudaMemcpyAsync(offs.as<void>(), ho.data(), size_t(nc) * sizeof(int64_t),
-                               cudaMemcpyHostToDevice, c_.stream));
-    if (int64_t(normals_.bytes() / 8) < new_total) {
-        DBuf nb(c_, size_t(std::max<int64_t>(new_total, int64_t(normals_.bytes() / 8) * 3 / 2)) * 8);
-        if (n_normals_ > 0)
-            HYDOT_CUDA(cudaMemcpyAsync(nb.as<void>(), normals_.as<void>(), size_t(n_normals_) * 8,
-                                       cudaMemcpyDeviceToDevice, c_.stream));
+    // pair totals after all c_end chunks: lower bound kept on the host, the
+    // buffer sized for the upper bound
+    const double sd = pairs_sigma(c_end);
+    const int64_t lower = int64_t(std::floor(double(c_end) * kPairs - 10.0 * sd));
+    const int64_t upper = int64_t(std::ceil(double(c_end) * kPairs + 10.0 * sd));
+    rng_scan_k<<<1, 1024, 0, c_.stream>>>(counts.as<int>(), int(nc), total_.as<int64_t>(), offs.as<int64_t>(),
+                                          std::max<int64_t>(lower, 0), upper);
+    c_.check_launch();
+    const int64_t cap = 2 * upper;  // normals
+    if (int64_t(normals_.bytes() / 8) < cap) {
+        DBuf nb(c_, size_t(std::max<int64_t>(cap, int64_t(normals_.bytes() / 8) * 3 / 2)) * 8);
+        if (normals_.bytes())
+            HYDOT_CUDA(cudaMemcpyAsync(nb.as<void>(), normals_.as<void>(), normals_.bytes(), cudaMemcpyDeviceToDevice,
+                                       c_.stream));
         normals_ = std::move(nb);
     }
-    rng_normals_k<<<unsigned(nc), 256, 0, c_.stream>>>(raw.as<uint64_t>(), offs.as<int64_t>(),
-                                                       normals_.d());
+    rng_normals_k<<<unsigned(nc), 256, 0, c_.stream>>>(raw.as<uint64_t>(), offs.as<int64_t>(), normals_.d());
     c_.check_launch();
     n_chunks_ = c_end;
-    n_normals_ = new_total;
+    n_normals_ = 2 * std::max<int64_t>(lower, 0);  // normals certainly present
 }
 
 void RngStream::ensure_normals(int64_t upto) {
     while (n_normals_ < upto) {
-        double per_chunk = double(mt::S) * 0.7853981633974483 * 0.995;
+        double per_chunk = double(mt::S) * 0.7853981633974483 * 0.995;  // normals per chunk, with slack
         int64_t extra = int64_t(std::ceil(double(upto - n_normals_) / per_chunk)) + 1;
         extra = std::min<int64_t>(extra, 1024);
         generate_chunks(n_chunks_ + extra);
