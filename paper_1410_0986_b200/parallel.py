@@ -74,25 +74,32 @@ def make_plan(nodes, root: int, world: int) -> ShardPlan:
     return ShardPlan(world, d, frontier, [list(nodes[v]["idx"]) for v in frontier], owner, merges)
 
 
+def _wire(dist, device):
+    """the device messages travel on: the tensors' own device with NCCL, host
+    memory with gloo (which has no device-tensor send / recv)"""
+    return torch.device("cpu") if dist.get_backend() == "gloo" else device
+
+
 def _send_factor(U: torch.Tensor, V: torch.Tensor, flagged: bool, dst: int, dist):
-    hdr = torch.tensor([U.shape[0], V.shape[0], U.shape[1], int(flagged)], dtype=torch.int64,
-                       device=U.device)
+    w = _wire(dist, U.device)
+    hdr = torch.tensor([U.shape[0], V.shape[0], U.shape[1], int(flagged)], dtype=torch.int64, device=w)
     dist.send(hdr, dst)
     if U.shape[1]:
-        dist.send(U.contiguous(), dst)
-        dist.send(V.contiguous(), dst)
+        dist.send(U.contiguous().to(w), dst)
+        dist.send(V.contiguous().to(w), dst)
 
 
 def _recv_factor(src: int, device, dist):
-    hdr = torch.empty(4, dtype=torch.int64, device=device)
+    w = _wire(dist, device)
+    hdr = torch.empty(4, dtype=torch.int64, device=w)
     dist.recv(hdr, src)
     rows, cols, rank, flagged = (int(x) for x in hdr.tolist())
-    U = torch.empty(rows, rank, dtype=torch.float64, device=device)
-    V = torch.empty(cols, rank, dtype=torch.float64, device=device)
+    U = torch.empty(rows, rank, dtype=torch.float64, device=w)
+    V = torch.empty(cols, rank, dtype=torch.float64, device=w)
     if rank:
         dist.recv(U, src)
         dist.recv(V, src)
-    return U, V, bool(flagged)
+    return U.to(device), V.to(device), bool(flagged)
 
 
 def reduce_tree(plan: ShardPlan, rank: int, local_factor, engine, eps: float, seed: int, p: int,
