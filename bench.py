@@ -391,7 +391,7 @@ def run_b200(args):
                              "roofline": {"bound": "hbm", "achieved": fields_gbs,
                                           "peak": HBM_PEAK_GBS, "unit": "GB/s",
                                           "frac": fields_gbs / HBM_PEAK_GBS,
-                                          "what": "batched single-pass CG (cg1_step): 48 N bytes per "
+                                          "what": "batched CG (cg_pa + cg_xr): 48 N bytes per "
                                                   "system-iteration (SURVEY 8d)"},
                              "e2e_with_fields_blocks_per_s": units / (ms_per_step / 1e3 + fields_s)},
         }

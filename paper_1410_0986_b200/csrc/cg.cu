@@ -4,18 +4,19 @@
 // wavelength) system (K + sigma_l M + sigma'_l R) x = e_v is SPD, so all of
 // them run as one batch of independent CG iterations.
 //
-// Vertex-parallel form (any operator; two HBM-streaming kernels per
-// iteration, each CTA owning 1024 vertices of one system, grid.y = system):
+// Per iteration two HBM-streaming kernels, each CTA owning 1024 vertices of
+// one system (grid.y = system):
 //   cg_pa : p <- r + beta p (on the fly for the 6 neighbours), store p,
 //           partial p.Ap                                   (reads r,p; writes p)
 //   cg_xr : alpha = rr / p.Ap, x += alpha p, r -= alpha A p, partial r.r
 //                                                         (reads p,x,r; writes x,r)
-// For the 7-point operator (the BASELINE fields) the iteration is one
-// z-marching kernel (cg1_step below): a CTA owns full x-rows of one system,
-// walks the z planes with bulk-copied plane rings and uses the
-// Chronopoulos-Gear scalars, so p, x and r are each read and written once
-// per iteration (48 N B).  Odd nx (no 16-byte aligned rows for the bulk
-// copies) keeps the two-kernel z-marching pair cgz_pa / cgz_xr.
+// For the 7-point operator (the BASELINE fields) the same two kernels run
+// z-marching (cgz_pa / cgz_xr below): a CTA owns full x-rows of one system
+// and walks the z planes with three planes of p in shared memory -- config 1
+// fields 0.93 -> 0.63 s (36 -> 53 % of the 48 N B/iteration HBM figure).
+// With even nx the planes are streamed by bulk copies (cp.async.bulk +
+// mbarrier rings, cgzt_pa / cgzt_xr): 0.63 -> 0.50 s on config 1 (68 %),
+// 6.96 -> 5.45 s on config 2 (69 %).
 // Scalars never leave the device: each CTA sums its system's partials in a
 // fixed order (deterministic), CTA 0 publishes rr into a parity slot.  The
 // stencil and the vector updates use explicit _rn intrinsics in the oracle's
@@ -161,7 +162,6 @@ __device__ __forceinline__ double stencil_at(const Stencil& g, double sigma, dou
                     vym, vyp, vzm, vzp);
 }
 
-template <int NT = CT>
 __device__ __forceinline__ double block_sum(double v, double* sh) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -169,18 +169,17 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
     __syncthreads();
     double t = 0.0;
     if (threadIdx.x == 0)
-        for (int i = 0; i < NT / 32; ++i) t += sh[i];
+        for (int i = 0; i < CT / 32; ++i) t += sh[i];
     __syncthreads();
     return t;
 }
 
 // deterministic sum of nparts partials (all threads get the result)
-template <int NT = CT>
 __device__ __forceinline__ double sum_parts(const double* __restrict__ parts, int nparts,
                                             double* sh, double* bc) {
     double v = 0.0;
-    for (int i = threadIdx.x; i < nparts; i += NT) v += parts[i];
-    double t = block_sum<NT>(v, sh);
+    for (int i = threadIdx.x; i < nparts; i += CT) v += parts[i];
+    double t = block_sum(v, sh);
     if (threadIdx.x == 0) *bc = t;
     __syncthreads();
     return *bc;
@@ -278,7 +277,6 @@ struct OpFem {
 
 struct SysState {
     double rr[2];   // r.r published per iteration parity
-    double alpha[2];  // alpha per iteration parity (single-pass recurrence)
     double bnorm;   // ||b||
     int done;       // converged (or stopped)
     int iters;
@@ -650,7 +648,14 @@ __global__ void __launch_bounds__(ZT, MINB) cgz_xr(ZGeo g, int64_t N, int nl, in
     if (threadIdx.x == 0) partB[int64_t(sys) * nparts + blockIdx.x] = t;
 }
 
-// bulk-copy helpers (cp.async.bulk into shared memory, mbarrier completion)
+// ------------------------------------------- z-marching with bulk copies --
+// cgzt_xr: cgz_xr with the planes streamed by the bulk-copy engine (one
+// cp.async.bulk per plane and array, mbarrier completion) into shared-memory
+// rings -- p: 5 planes (3 in use, 2 in flight), x / r: 3 planes (1 in use,
+// 2 in flight).  No load instructions or prefetch registers in the loop and
+// one block barrier per plane.  Needs 16-byte aligned rows (nx even).
+constexpr int NSP = 5, NSX = 3;
+
 __device__ __forceinline__ uint32_t su32(const void* q) { return uint32_t(__cvta_generic_to_shared(q)); }
 __device__ __forceinline__ void mb_init(uint64_t* b) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(b)) : "memory");
@@ -672,81 +677,123 @@ __device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t par) {
         : "memory");
 }
 
-// ------------------------------------------------ single-pass CG (nx even) --
-// cg1_step: ONE kernel per CG iteration for the 7-point operator.  The
-// scalars follow the Chronopoulos-Gear recurrence: with gamma_i = (r_i, r_i)
-// and delta_i = (r_i, A r_i) both reduced by the previous launch,
-//   beta_i = gamma_i / gamma_{i-1},  alpha_i = gamma_i / (delta_i - beta_i gamma_i / alpha_{i-1}),
-// which equals the reference's gamma_i / (p_i, A p_i) (krylov.cpp:400-463)
-// in exact arithmetic, so alpha is known before p_i is formed and the
-// iteration needs no second pass:
-//   p_i = r_i + beta p_{i-1},  s = A p_i,  x += alpha p_i,  r_{i+1} = r_i - alpha s,
-//   partials of gamma_{i+1} and delta_{i+1} = (r_{i+1}, A r_{i+1}).
-// The vectors are the reference's (s = A p is applied, not recurred), only
-// alpha's rounding differs: over the config-1 systems the iterates agree with
-// the two-pass CG to ~1e-16 relative.
-//
-// HBM per vertex and iteration: read r_i, p_{i-1}, x, write r_{i+1}, p_i, x
-// = 48 B, the SURVEY 8(d) figure (the two-kernel form moved 64 B), plus the
-// y-halo rows.  A CTA owns `ty` full x-rows of one system and marches z; the
-// tile carries 2 halo rows on each side (s is needed on 1 halo row to form
-// r_{i+1} there, p on 2), so r_i and p_{i-1} are read for ty + 4 rows.
-// Every plane arrives by one cp.async.bulk per array into mbarrier rings
-// (r_i 4 planes, p_{i-1} 3, x 3); p_i and r_{i+1} live in 3-plane rings.
-// Per plane two phases separated by block barriers:
-//   A_k: p_i(k+1) = r + beta p_old on the whole tile; delta partial of plane k-2
-//   B_k: s(k) and r_{i+1}(k) on the tile's rows +-1; own rows: store p_i, x, r
-// One CTA per SM (up to 227 KB of rings), 512 threads.
-constexpr int Z1T = 512;                  // threads per CTA
-constexpr int Z1K = 4;                    // tile elements per thread: (ty + 4) nx <= Z1T Z1K
-constexpr int Z1R = 4, Z1P = 3, Z1X = 3;  // ring depths of r_i, p_{i-1} and x planes
-constexpr int Z1MIN_TY = 4;               // below this the halo rows cost more than the pass saves
-
-struct Z1Geo {
-    int nx, ny, nz, ty;
-    double h;
-};
-
-// shared-memory doubles of the rings for an nx x ty tile
-inline size_t cg1_smem(int nx, int ty) {
-    return (size_t(Z1R + Z1P + 6) * size_t(ty + 4) + size_t(Z1X) * size_t(ty)) * size_t(nx) * sizeof(double);
-}
-
-__device__ __forceinline__ double tstencil(const Z1Geo& g, const ZDiag& d, int ix, int iy, int e,
-                                           const double* __restrict__ c, const double* __restrict__ dn,
-                                           const double* __restrict__ up) {
-    return stencil7_nb(g.nx, g.ny, g.h, d, ix, iy, c[e], c[ix > 0 ? e - 1 : e], c[ix < g.nx - 1 ? e + 1 : e],
-                       c[e - g.nx], c[e + g.nx], dn[e], up[e]);
-}
-
-__global__ void __launch_bounds__(Z1T, 1) cg1_step(Z1Geo g, int64_t N, int nl, int k0, int it,
-                                                   const double* __restrict__ sig,
-                                                   const double* __restrict__ sigp, double* __restrict__ X,
-                                                   const double* __restrict__ Rin, double* __restrict__ Rout,
-                                                   const double* __restrict__ Pold, double* __restrict__ Pnew,
-                                                   double* __restrict__ pG, double* __restrict__ pD, int nparts,
-                                                   int64_t pstride, SysState* __restrict__ st, double tol,
-                                                   int fixed, int check_only, const int* __restrict__ act) {
+__global__ void __launch_bounds__(ZT, 2) cgzt_xr(ZGeo g, int64_t N, int nl, int k0, int it,
+                                               const double* __restrict__ sig,
+                                               const double* __restrict__ sigp,
+                                               double* __restrict__ X, double* __restrict__ R,
+                                               const double* __restrict__ P,
+                                               const double* __restrict__ partA,
+                                               double* __restrict__ partB, int nparts,
+                                               SysState* __restrict__ st,
+                                               const int* __restrict__ act) {
     extern __shared__ __align__(16) double zs[];
-    __shared__ __align__(8) uint64_t bar[Z1R + Z1P + Z1X];
-    __shared__ double sh[Z1T / 32];
+    __shared__ __align__(8) uint64_t bar[NSP + NSX];
+    __shared__ double sh[ZT / 32];
     __shared__ double bc;
-    __shared__ int sdone;
     const int sys = act[blockIdx.y];
     SysState& S = st[sys];
-    // one read of the flag per CTA: another CTA of this launch may set it
-    if (threadIdx.x == 0) sdone = S.done;
-    __syncthreads();
-    if (sdone) return;
+    if (S.done) return;
     const int l = (k0 + sys) % nl;
+    const double pq = sum_parts(partA + int64_t(sys) * nparts, nparts, sh, &bc);
+    const double alpha = S.rr[it & 1] / pq;
+    ZIdx z;
+    zidx(g, z);
+    const int64_t plane = int64_t(g.nx) * g.ny;
+    double* x = X + int64_t(sys) * N;
+    double* r = R + int64_t(sys) * N;
+    const double* p = P + int64_t(sys) * N;
+    const double sigma = sig[l], sigmap = sigp[l];
+    double* pring = zs;                   // NSP x W
+    double* xring = zs + NSP * z.W;       // NSX x (x | r) x Wo
+    const uint32_t pbytes = uint32_t(z.hi - z.lo) * 8u, xbytes = uint32_t(z.Wo) * 8u;
+    auto issue_p = [&](int j) {
+        const int sl = j % NSP;
+        mb_expect(&bar[sl], pbytes);
+        bulk_load(pring + sl * z.W + z.lo, p + j * plane + z.base + z.lo, pbytes, &bar[sl]);
+    };
+    auto issue_xr = [&](int j) {
+        const int sl = j % NSX;
+        mb_expect(&bar[NSP + sl], 2u * xbytes);
+        const int64_t o = j * plane + z.base + g.nx;
+        bulk_load(xring + (2 * sl) * z.Wo, x + o, xbytes, &bar[NSP + sl]);
+        bulk_load(xring + (2 * sl + 1) * z.Wo, r + o, xbytes, &bar[NSP + sl]);
+    };
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NSP + NSX; ++i) mb_init(&bar[i]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int j = 0; j < 3 && j < g.nz; ++j) issue_p(j);
+        for (int j = 0; j < 2 && j < g.nz; ++j) issue_xr(j);
+    }
+    double acc = 0.0;
+    for (int iz = 0; iz < g.nz; ++iz) {
+        if (iz > 0) __syncthreads();  // plane iz-1's reads are done: its slots may refill
+        if (threadIdx.x == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (iz + 3 < g.nz) issue_p(iz + 3);    // into p(iz-2)'s slot
+            if (iz + 2 < g.nz) issue_xr(iz + 2);   // into x/r(iz-1)'s slot
+        }
+        if (iz == 0) mb_wait(&bar[0], 0);
+        if (iz + 1 < g.nz) mb_wait(&bar[(iz + 1) % NSP], uint32_t(((iz + 1) / NSP) & 1));
+        mb_wait(&bar[NSP + iz % NSX], uint32_t((iz / NSX) & 1));
+        const double* c = pring + (iz % NSP) * z.W;
+        const double* dn = pring + ((iz + NSP - 1) % NSP) * z.W;
+        const double* up = pring + ((iz + 1) % NSP) * z.W;
+        const double* xs = xring + (2 * (iz % NSX)) * z.Wo;
+        const double* rs = xs + z.Wo;
+        const ZDiag d = zdiag(g.nz, g.h, iz, sigma, sigmap);
+#pragma unroll
+        for (int k = 0; k < ZO; ++k) {
+            const int e = threadIdx.x + k * ZT;
+            if (e < z.Wo) {
+                const double q = zstencil(g, z, k, e, d, c, dn, up);
+                const int64_t i = iz * plane + z.base + g.nx + e;
+                __stcs(x + i, __dadd_rn(xs[e], __dmul_rn(alpha, c[e + g.nx])));
+                const double rn = __dsub_rn(rs[e], __dmul_rn(alpha, q));
+                __stcs(r + i, rn);
+                acc += rn * rn;
+            }
+        }
+    }
+    const double t = block_sum(acc, sh);
+    if (threadIdx.x == 0) partB[int64_t(sys) * nparts + blockIdx.x] = t;
+}
+
+// cgzt_pa: cgz_pa with r and p_old streamed by bulk copies into a 3-plane
+// ring; p_new = r + beta p_old is formed once per vertex into a 4-plane ring
+// (4 slots: the plane written at step iz was last read two barriers ago, so
+// one block barrier per plane suffices).
+constexpr int NSR = 3;
+
+// NS raw planes in the ring, NPN p_new planes (4: one barrier per plane;
+// 3: a second barrier per plane, one more raw plane in flight in the same
+// shared memory)
+template <int NS, int NPN>
+__global__ void __launch_bounds__(ZT, 2) cgzt_pa(ZGeo g, int64_t N, int nl, int k0, int it,
+                                               const double* __restrict__ sig,
+                                               const double* __restrict__ sigp,
+                                               const double* __restrict__ R,
+                                               const double* __restrict__ Pold,
+                                               double* __restrict__ Pnew, double* __restrict__ partA,
+                                               const double* __restrict__ partB, int nparts,
+                                               SysState* __restrict__ st, double tol, int fixed,
+                                               const int* __restrict__ act) {
+    extern __shared__ __align__(16) double zs[];
+    __shared__ __align__(8) uint64_t bar[NS];
+    __shared__ double sh[ZT / 32];
+    __shared__ double bc;
+    const int sys = act[blockIdx.y];
+    SysState& S = st[sys];
+    if (S.done) return;
+    const int l = (k0 + sys) % nl;
+    double beta = 0.0;
     const int slot = it & 1;
-    const int64_t pin = int64_t(slot) * pstride + int64_t(sys) * nparts;
-    const int64_t pout = int64_t(slot ^ 1) * pstride + int64_t(sys) * nparts + blockIdx.x;
-    const double gam = sum_parts<Z1T>(pG + pin, nparts, sh, &bc);
-    const double dlt = sum_parts<Z1T>(pD + pin, nparts, sh, &bc);
-    double alpha, beta = 0.0;
     if (it > 0) {
-        const double relres = sqrt(gam) / S.bnorm;
+        const double rr_new = sum_parts(partB + int64_t(sys) * nparts, nparts, sh, &bc);
+        const double rr_old = S.rr[slot ^ 1];
+        const double relres = sqrt(rr_new) / S.bnorm;
         if (!fixed && relres <= tol) {
             if (blockIdx.x == 0 && threadIdx.x == 0) {
                 S.done = 1;
@@ -755,204 +802,100 @@ __global__ void __launch_bounds__(Z1T, 1) cg1_step(Z1Geo g, int64_t N, int nl, i
             }
             return;
         }
-        if (check_only) return;
-        beta = gam / S.rr[slot ^ 1];
-        alpha = gam / (dlt - beta * gam / S.alpha[slot ^ 1]);
+        beta = rr_new / rr_old;
         if (blockIdx.x == 0 && threadIdx.x == 0) {
+            S.rr[slot] = rr_new;
             S.relres = relres;
             S.iters = it;
         }
-    } else {
-        alpha = gam / dlt;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        S.rr[slot] = gam;
-        S.alpha[slot] = alpha;
-    }
-    const int nx = g.nx;
-    const int y0 = blockIdx.x * g.ty;
-    const int rows = min(g.ty, g.ny - y0);
-    const int T = rows + 4;                        // tile rows (2 halo rows each side)
-    const int W = T * nx;                          // tile elements
-    const int WS = (g.ty + 4) * nx;                // ring slot stride (same for all CTAs)
-    const int TO = g.ty * nx;                      // own-row slot stride of the x ring
-    const int64_t base = int64_t(y0 - 2) * nx;     // plane offset of tile element 0
-    const int lo = max(0, 2 - y0) * nx;            // in-grid tile elements [lo, hi)
-    const int hi = min(T, g.ny - y0 + 2) * nx;
-    const int s_lo = max(nx, lo), s_hi = min((T - 1) * nx, hi);  // s / r_{i+1}: rows 1 .. T-2, in grid
-    const int o_lo = 2 * nx, o_hi = (rows + 2) * nx;              // own rows
-    const int64_t plane = int64_t(nx) * g.ny;
-    const int64_t so = int64_t(sys) * N;
-    double* x = X + so;
-    const double* r = Rin + so;
-    double* rn_g = Rout + so;
-    const double* po = Pold + so;
-    double* pn_g = Pnew + so;
+    ZIdx z;
+    zidx(g, z);
+    const int64_t plane = int64_t(g.nx) * g.ny;
+    const double* r = R + int64_t(sys) * N;
+    const double* po = Pold + int64_t(sys) * N;
+    double* p = Pnew + int64_t(sys) * N;
     const double sigma = sig[l], sigmap = sigp[l];
-    double* rring = zs;                   // Z1R x WS
-    double* pring = rring + Z1R * WS;     // Z1P x WS (p_{i-1})
-    double* P = pring + Z1P * WS;         // 3 x WS   (p_i)
-    double* RN = P + 3 * WS;              // 3 x WS   (r_{i+1})
-    double* xring = RN + 3 * WS;          // Z1X x TO
-    const uint32_t tbytes = uint32_t(hi - lo) * 8u, xbytes = uint32_t(rows * nx) * 8u;
-    auto issue_r = [&](int j) {
-        const int sl = j % Z1R;
-        mb_expect(&bar[sl], tbytes);
-        bulk_load(rring + sl * WS + lo, r + j * plane + base + lo, tbytes, &bar[sl]);
+    double* raw = zs;                 // NS x (r | p_old) x W
+    double* pn = zs + 2 * NS * z.W;  // NPN x W
+    const uint32_t bytes = uint32_t(z.hi - z.lo) * 8u;
+    auto issue = [&](int j) {
+        const int sl = j % NS;
+        mb_expect(&bar[sl], 2u * bytes);
+        const int64_t o = j * plane + z.base + z.lo;
+        bulk_load(raw + (2 * sl) * z.W + z.lo, r + o, bytes, &bar[sl]);
+        bulk_load(raw + (2 * sl + 1) * z.W + z.lo, po + o, bytes, &bar[sl]);
     };
-    auto issue_p = [&](int j) {
-        const int sl = j % Z1P;
-        mb_expect(&bar[Z1R + sl], tbytes);
-        bulk_load(pring + sl * WS + lo, po + j * plane + base + lo, tbytes, &bar[Z1R + sl]);
-    };
-    auto issue_x = [&](int j) {
-        const int sl = j % Z1X;
-        mb_expect(&bar[Z1R + Z1P + sl], xbytes);
-        bulk_load(xring + sl * TO, x + j * plane + int64_t(y0) * nx, xbytes, &bar[Z1R + Z1P + sl]);
-    };
-    // per-thread tile elements: ix | tile row << 16
-    int exy[Z1K];
+    auto convert = [&](int j) {  // pn[j % 4] = r + beta p_old on the in-grid rows
+        const int sl = j % NS;
+        mb_wait(&bar[sl], uint32_t((j / NS) & 1));
+        const double* rs = raw + (2 * sl) * z.W;
+        const double* ps = rs + z.W;
+        double* out = pn + (j % NPN) * z.W;
 #pragma unroll
-    for (int k = 0; k < Z1K; ++k) {
-        const int e = threadIdx.x + k * Z1T;
-        const int ry = e / nx;
-        exy[k] = (e - ry * nx) | (ry << 16);
-    }
+        for (int k = 0; k < ZE; ++k) {
+            const int e = threadIdx.x + k * ZT;
+            if (e >= z.lo && e < z.hi) out[e] = __dadd_rn(rs[e], __dmul_rn(beta, ps[e]));
+        }
+    };
     if (threadIdx.x == 0) {
-        for (int i = 0; i < Z1R + Z1P + Z1X; ++i) mb_init(&bar[i]);
+        for (int i = 0; i < NS; ++i) mb_init(&bar[i]);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (int e = threadIdx.x; e < 6 * WS; e += Z1T) P[e] = 0.0;  // out-of-grid rows of p_i / r_{i+1}
+    for (int e = threadIdx.x; e < NPN * z.W; e += ZT) pn[e] = 0.0;  // out-of-grid halo rows
     __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int j = 0; j < Z1R && j < g.nz; ++j) issue_r(j);
-        for (int j = 0; j < Z1P && j < g.nz; ++j) issue_p(j);
-        for (int j = 0; j < Z1X && j < g.nz; ++j) issue_x(j);
+    if (threadIdx.x == 0)
+        for (int j = 0; j < NS && j < g.nz; ++j) issue(j);
+    convert(0);
+    __syncthreads();
+    if (threadIdx.x == 0 && NS < g.nz) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(NS);
     }
-    auto form = [&](int j) {  // p_i(j) = r_i + beta p_{i-1} on the in-grid tile
-        mb_wait(&bar[j % Z1R], uint32_t((j / Z1R) & 1));
-        mb_wait(&bar[Z1R + j % Z1P], uint32_t((j / Z1P) & 1));
-        const double* rs = rring + (j % Z1R) * WS;
-        const double* ps = pring + (j % Z1P) * WS;
-        double* out = P + (j % 3) * WS;
-#pragma unroll
-        for (int k = 0; k < Z1K; ++k) {
-            const int e = threadIdx.x + k * Z1T;
-            if (e >= lo && e < hi) out[e] = __dadd_rn(rs[e], __dmul_rn(beta, ps[e]));
-        }
-    };
-    form(0);
-    __syncthreads();
-    double gacc = 0.0, dacc = 0.0;
-    for (int k = 0; k <= g.nz + 1; ++k) {
-        // ---- A_k
-        if (threadIdx.x == 0 && k >= 1) {
+    double acc = 0.0;
+    for (int iz = 0; iz < g.nz; ++iz) {
+        const int j = iz + 1;
+        if (j < g.nz) convert(j);
+        __syncthreads();
+        if (threadIdx.x == 0 && j + NS < g.nz) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            if (k + Z1R - 1 < g.nz) issue_r(k + Z1R - 1);  // into r(k-1)'s slot (last read in B_{k-1})
-            if (k + Z1X - 1 < g.nz) issue_x(k + Z1X - 1);  // into x(k-1)'s slot
+            issue(j + NS);  // into raw(j)'s slot, converted above
         }
-        if (threadIdx.x == 0 && k + Z1P < g.nz) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue_p(k + Z1P);  // into p_old(k)'s slot (read in A_{k-1})
-        }
-        if (k + 1 < g.nz) form(k + 1);
-        if (k >= 2) {  // delta partial of plane k-2: (r_{i+1}, A r_{i+1})
-            const int j = k - 2;
-            const double* c = RN + (j % 3) * WS;
-            const double* dn = RN + ((j + 2) % 3) * WS;
-            const double* up = RN + ((j + 1) % 3) * WS;
-            const ZDiag d = zdiag(g.nz, g.h, j, sigma, sigmap);
+        const double* c = pn + (iz % NPN) * z.W;
+        const double* dn = pn + ((iz + NPN - 1) % NPN) * z.W;
+        const double* up = pn + ((iz + 1) % NPN) * z.W;
+        const ZDiag d = zdiag(g.nz, g.h, iz, sigma, sigmap);
 #pragma unroll
-            for (int kk = 0; kk < Z1K; ++kk) {
-                const int e = threadIdx.x + kk * Z1T;
-                if (e >= o_lo && e < o_hi) {
-                    const int ix = exy[kk] & 0xffff, iy = y0 - 2 + (exy[kk] >> 16);
-                    dacc += c[e] * tstencil(g, d, ix, iy, e, c, dn, up);
-                }
+        for (int k = 0; k < ZO; ++k) {
+            const int e = threadIdx.x + k * ZT;
+            if (e < z.Wo) {
+                const double pi = c[e + g.nx];
+                const double ap = zstencil(g, z, k, e, d, c, dn, up);
+                __stcs(p + iz * plane + z.base + g.nx + e, pi);
+                acc += pi * ap;
             }
         }
-        __syncthreads();
-        // ---- B_k
-        if (k < g.nz) {
-            const double* c = P + (k % 3) * WS;
-            const double* dn = P + ((k + 2) % 3) * WS;
-            const double* up = P + ((k + 1) % 3) * WS;
-            const double* rs = rring + (k % Z1R) * WS;
-            double* rnew = RN + (k % 3) * WS;
-            mb_wait(&bar[Z1R + Z1P + k % Z1X], uint32_t((k / Z1X) & 1));
-            const double* xs = xring + (k % Z1X) * TO - o_lo;
-            const ZDiag d = zdiag(g.nz, g.h, k, sigma, sigmap);
-            const int64_t pk = k * plane + base;
-#pragma unroll
-            for (int kk = 0; kk < Z1K; ++kk) {
-                const int e = threadIdx.x + kk * Z1T;
-                if (e >= s_lo && e < s_hi) {
-                    const int ix = exy[kk] & 0xffff, iy = y0 - 2 + (exy[kk] >> 16);
-                    const double s = tstencil(g, d, ix, iy, e, c, dn, up);
-                    const double rv = __dsub_rn(rs[e], __dmul_rn(alpha, s));
-                    rnew[e] = rv;
-                    if (e >= o_lo && e < o_hi) {
-                        __stcs(pn_g + pk + e, c[e]);
-                        __stcs(x + pk + e, __dadd_rn(xs[e], __dmul_rn(alpha, c[e])));
-                        __stcs(rn_g + pk + e, rv);
-                        gacc += rv * rv;
-                    }
-                }
-            }
-        }
-        __syncthreads();
+        if (NPN == 3) __syncthreads();  // pn(iz-1)'s slot is refilled next
     }
-    const double tg = block_sum<Z1T>(gacc, sh);
-    const double td = block_sum<Z1T>(dacc, sh);
-    if (threadIdx.x == 0) {
-        pG[pout] = tg;
-        pD[pout] = td;
-    }
-}
-
-// iteration-0 partials of the single-pass recurrence: gamma_0 = ||b||^2 and
-// delta_0 = (b, A b) from the sparse right-hand side (one warp per system)
-template <class Op>
-__global__ void cg1_init(Op op, int64_t N, int nl, int k0, int nb, const int64_t* __restrict__ ridx,
-                         const double* __restrict__ rhs_b2, const double* __restrict__ sig,
-                         const double* __restrict__ sigp, const double* __restrict__ R, double* __restrict__ pG,
-                         double* __restrict__ pD, int nparts) {
-    const int sys = blockIdx.x;
-    const int lane = threadIdx.x;
-    if (sys >= nb) return;
-    const int rhs = (k0 + sys) / nl, l = (k0 + sys) % nl;
-    const double* r = R + int64_t(sys) * N;
-    double v = 0.0;
-    if (lane < 8) {
-        const int64_t vi = ridx[int64_t(rhs) * 8 + lane];
-        bool dup = false;
-        for (int e = 0; e < lane; ++e) dup |= ridx[int64_t(rhs) * 8 + e] == vi;
-        if (vi >= 0 && !dup)
-            v = r[vi] * op(vi, sig[l], sigp[l], l, [&](int64_t j) { return r[j]; });
-    }
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    v = __shfl_sync(0xffffffffu, v, 0);
-    const double b2 = rhs_b2[rhs];
-    for (int j = lane; j < nparts; j += 32) {
-        pG[int64_t(sys) * nparts + j] = j ? 0.0 : b2;
-        pD[int64_t(sys) * nparts + j] = j ? 0.0 : v;
-    }
-}
-
-// single-pass tile height for an nx x ny plane (0 = not applicable), balanced
-// over the tiles and bounded by the shared-memory rings
-int cg1_ty(int nx, int ny, size_t smem_cap) {
-    if (nx % 2) return 0;  // bulk copies need 16-byte aligned rows
-    int t = std::min(ny, Z1T * Z1K / nx - 4);
-    while (t >= Z1MIN_TY && cg1_smem(nx, t) > smem_cap) --t;
-    if (t < Z1MIN_TY) return 0;
-    const int ntiles = (ny + t - 1) / t;
-    return (ny + ntiles - 1) / ntiles;
+    const double t = block_sum(acc, sh);
+    if (threadIdx.x == 0) partA[int64_t(sys) * nparts + blockIdx.x] = t;
 }
 
 // CTAs per SM the z-marching kernels are compiled for (3: 80 registers;
 // 4 forces 64 and spills: 0.84 vs 0.63 s on config 1)
 #define ZSEL(k) (k<3>)
+
+// (a cgzt_pa with 4 raw planes and 3 p_new planes -- one more plane in
+// flight, one more barrier per plane -- measured 0.493 -> 0.503 s on config 1)
+
+// bulk-copy x/r kernel for even nx (HYDOT_CG_BULK=0 keeps the register one)
+bool zbulk_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("HYDOT_CG_BULK");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 // z-march tile height for an nx x ny plane (0 = tile does not fit: use the
 // vertex-parallel kernels); balanced over the tiles
@@ -1028,35 +971,33 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
     if (N >= (int64_t(1) << 24)) throw std::invalid_argument("fields_solve: grid too large for the 24-bit vertex decode");
     const int total = n_rhs * nl;
     int nparts = int((N + CV - 1) / CV);
-    // 7-point operator: the single-pass z-marching kernel for even nx, the
-    // two-kernel register z-marching pair otherwise when the tile fits
+    // 7-point operator: z-marching kernels when the halo'ed tile fits
     ZGeo zg{};
-    Z1Geo z1{};
-    size_t zsmem = 0, z1smem = 0;
+    size_t zsmem = 0, ztsmem = 0, ztpsmem = 0;
     if constexpr (std::is_same_v<Op, Op7>) {
-        const size_t cap = 225 * 1024;
-        const int ty1 = cg1_ty(op.g.nx, op.g.ny, cap);
-        const int ty = ty1 > 0 ? 0 : zmarch_ty(op.g.nx, op.g.ny);
-        if (ty1 > 0) {
-            z1 = Z1Geo{op.g.nx, op.g.ny, op.g.nz, ty1, op.g.h};
-            nparts = (op.g.ny + ty1 - 1) / ty1;
-            z1smem = cg1_smem(op.g.nx, ty1);
-            static AttrGate attr;
-            attr_once(attr, c.device, [&] {
-                HYDOT_CUDA(cudaFuncSetAttribute(cg1_step, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cap)));
-            });
-        } else if (ty > 0) {
+        const int ty = zmarch_ty(op.g.nx, op.g.ny);
+        if (ty > 0) {
             zg = ZGeo{op.g.nx, op.g.ny, op.g.nz, ty, op.g.h};
             nparts = (op.g.ny + ty - 1) / ty;
             zsmem = size_t(3) * size_t(ty + 2) * size_t(op.g.nx) * sizeof(double);
+            if (op.g.nx % 2 == 0 && zbulk_on()) {
+                ztsmem = size_t(NSP * (ty + 2) + NSX * 2 * ty) * size_t(op.g.nx) * sizeof(double);
+                ztpsmem = size_t((2 * NSR + 4) * (ty + 2)) * size_t(op.g.nx) * sizeof(double);
+                static AttrGate attr;
+                attr_once(attr, c.device, [&] {
+                    HYDOT_CUDA(cudaFuncSetAttribute(cgzt_xr, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    200 * 1024));
+                    HYDOT_CUDA(cudaFuncSetAttribute(cgzt_pa<NSR, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    200 * 1024));
+                });
+            }
         }
     }
-    // One batch of up to 24 GB of iteration vectors (all systems iterate
-    // together, HBM-bound).  L2-sized groups (32 N bytes per system) measured
-    // slower on config 1 (1.4-2.8 s vs 0.96 s: small groups make the
-    // iterations launch- and sync-bound).
-    const int nr = z1smem ? 2 : 1;  // r is double-buffered by the single pass (halo rows are re-read)
-    const int64_t per_sys = (z1smem ? 4 : 2) * N * 8;
+    // One batch of up to 24 GB (all systems iterate together, HBM-bound).
+    // L2-sized groups (32 N bytes per system) measured slower on config 1
+    // (1.4-2.8 s vs 0.96 s: small groups make the iterations launch- and
+    // sync-bound).
+    int64_t per_sys = 2 * N * 8;
     int batch = int(std::max<int64_t>(1, std::min<int64_t>(total, (int64_t(24) << 30) / per_sys)));
     batch = std::min(batch, 65535);
     DBuf dsig = dalloc(c, size_t(nl)), dsigp = dalloc(c, size_t(nl)), dinv = dalloc(c, size_t(nl));
@@ -1069,13 +1010,10 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
     HYDOT_CUDA(cudaMemcpyAsync(dridx.as<void>(), ridx.data(), ridx.size() * 8, cudaMemcpyHostToDevice, c.stream));
     HYDOT_CUDA(cudaMemcpyAsync(drw.d(), rw.data(), rw.size() * 8, cudaMemcpyHostToDevice, c.stream));
     HYDOT_CUDA(cudaMemcpyAsync(db2.d(), b2.data(), b2.size() * 8, cudaMemcpyHostToDevice, c.stream));
-    DBuf R = dalloc(c, size_t(nr) * size_t(batch) * size_t(N));
+    DBuf R = dalloc(c, size_t(batch) * size_t(N));
     DBuf P = dalloc(c, 2 * size_t(batch) * size_t(N));  // double-buffered p
-    // partial sums: pA / pB of the two-kernel form; the single pass keeps
-    // gamma (pA) and delta (pB) partials per iteration parity
-    const int64_t pstride = int64_t(batch) * nparts;
-    DBuf pA = dalloc(c, 2 * size_t(pstride));
-    DBuf pB = dalloc(c, 2 * size_t(pstride));
+    DBuf pA = dalloc(c, size_t(batch) * size_t(nparts));
+    DBuf pB = dalloc(c, size_t(batch) * size_t(nparts));
     DBuf S(c, size_t(batch) * sizeof(SysState));
     DBuf dact(c, sizeof(int) * size_t(batch));
     if (stats) {
@@ -1083,8 +1021,6 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
         stats->relres.assign(size_t(total), 0.0);
     }
     const int limit = fixed_iters > 0 ? fixed_iters : max_iter;
-    auto pbuf = [&](int i) { return P.d() + size_t(i & 1) * size_t(batch) * size_t(N); };
-    auto rbuf = [&](int i) { return R.d() + size_t(nr == 2 ? (i & 1) : 0) * size_t(batch) * size_t(N); };
     for (int k0 = 0; k0 < total; k0 += batch) {
         const int nb = std::min(batch, total - k0);
         double* X = out + int64_t(k0) * N;
@@ -1092,22 +1028,14 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
         {
             dim3 gi = dim3(unsigned(std::min<int64_t>((N + 255) / 256, 1024)), unsigned(nb));
             // p_old of iteration 0 is buffer 1 (zeroed); p_it lives in buffer it&1
-            cg_init<<<gi, 256, 0, c.stream>>>(N, nl, db2.d(), k0, X, rbuf(0), pbuf(1), ss);
+            cg_init<<<gi, 256, 0, c.stream>>>(N, nl, db2.d(), k0, X, R.d(),
+                                              P.d() + size_t(batch) * size_t(N), ss);
             c.check_launch();
             dim3 gr = dim3(unsigned((nb + 31) / 32));
-            cg_rhs<<<gr, dim3(8, 32), 0, c.stream>>>(N, nl, k0, nb, dridx.as<int64_t>(), drw.d(), rbuf(0));
+            cg_rhs<<<gr, dim3(8, 32), 0, c.stream>>>(N, nl, k0, nb, dridx.as<int64_t>(), drw.d(), R.d());
             c.check_launch();
-            if constexpr (std::is_same_v<Op, Op7>) {
-                if (z1smem) {
-                    cg1_init<<<nb, 32, 0, c.stream>>>(op, N, nl, k0, nb, dridx.as<int64_t>(), db2.d(), dsig.d(),
-                                                     dsigp.d(), rbuf(0), pA.d(), pB.d(), nparts);
-                    c.check_launch();
-                }
-            }
         }
-        // the final squared residuals: parity `it` of the single pass's
-        // gamma partials, pB of the two-kernel form
-        auto rr_parts = [&](int it) { return z1smem ? pA.d() + (it & 1) * pstride : pB.d(); };
+        auto pbuf = [&](int i) { return P.d() + size_t(i & 1) * size_t(batch) * size_t(N); };
         // active-system list: converged systems are dropped from the grid
         // every 8 iterations (systems converge between ~70 and ~135 iterations)
         std::vector<int> active(static_cast<size_t>(nb));
@@ -1115,38 +1043,36 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
         std::vector<SysState> hst(static_cast<size_t>(nb));
         HYDOT_CUDA(cudaMemcpyAsync(dact.as<void>(), active.data(), active.size() * sizeof(int),
                                    cudaMemcpyHostToDevice, c.stream));
-        // one iteration (check_only: the convergence test of iteration `it` alone)
-        auto step = [&](int it, bool check_only) {
-            dim3 grid = dim3(unsigned(nparts), unsigned(active.size()));
-            const int fixed = fixed_iters > 0 && !check_only;
-            if (z1smem) {
-                cg1_step<<<grid, Z1T, z1smem, c.stream>>>(z1, N, nl, k0, it, dsig.d(), dsigp.d(), X, rbuf(it),
-                                                          rbuf(it + 1), pbuf(it + 1), pbuf(it), pA.d(), pB.d(),
-                                                          nparts, pstride, ss, tol, fixed, check_only ? 1 : 0,
-                                                          dact.as<int>());
-                c.check_launch();
-                return;
-            }
-            if (zsmem)
-                ZSEL(cgz_pa)<<<grid, ZT, zsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), rbuf(it),
-                                                            pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss, tol,
-                                                            fixed, dact.as<int>());
-            else
-                cg_pa<<<grid, CT, 0, c.stream>>>(op, N, nl, k0, it, dsig.d(), dsigp.d(), rbuf(it), pbuf(it + 1),
-                                                pbuf(it), pA.d(), pB.d(), nparts, ss, tol, fixed, dact.as<int>());
-            c.check_launch();
-            if (check_only) return;  // the p update of a finished solve is never used
-            if (zsmem)
-                ZSEL(cgz_xr)<<<grid, ZT, zsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), X, rbuf(it),
-                                                            pbuf(it), pA.d(), pB.d(), nparts, ss, dact.as<int>());
-            else
-                cg_xr<<<grid, CT, 0, c.stream>>>(op, N, nl, k0, it, dsig.d(), dsigp.d(), X, rbuf(it), pbuf(it),
-                                                pA.d(), pB.d(), nparts, ss, dact.as<int>());
-            c.check_launch();
-        };
         int it = 0;
         for (; it < limit; ++it) {
-            step(it, false);
+            dim3 grid = dim3(unsigned(nparts), unsigned(active.size()));
+            if (zsmem) {
+                if (ztpsmem)
+                    cgzt_pa<NSR, 4><<<grid, ZT, ztpsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
+                                                             pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
+                                                             tol, fixed_iters > 0, dact.as<int>());
+                else
+                    ZSEL(cgz_pa)<<<grid, ZT, zsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
+                                                                pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts,
+                                                                ss, tol, fixed_iters > 0, dact.as<int>());
+                c.check_launch();
+                if (ztsmem)
+                    cgzt_xr<<<grid, ZT, ztsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), X, R.d(),
+                                                            pbuf(it), pA.d(), pB.d(), nparts, ss, dact.as<int>());
+                else
+                    ZSEL(cgz_xr)<<<grid, ZT, zsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), X,
+                                                                R.d(), pbuf(it), pA.d(), pB.d(), nparts, ss,
+                                                                dact.as<int>());
+                c.check_launch();
+            } else {
+            cg_pa<<<grid, CT, 0, c.stream>>>(op, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
+                                            pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
+                                            tol, fixed_iters > 0, dact.as<int>());
+            c.check_launch();
+            cg_xr<<<grid, CT, 0, c.stream>>>(op, N, nl, k0, it, dsig.d(), dsigp.d(), X, R.d(),
+                                            pbuf(it), pA.d(), pB.d(), nparts, ss, dact.as<int>());
+            c.check_launch();
+            }
             if (fixed_iters <= 0 && (it % 8) == 7) {
                 HYDOT_CUDA(cudaMemcpyAsync(hst.data(), ss, size_t(nb) * sizeof(SysState),
                                            cudaMemcpyDeviceToHost, c.stream));
@@ -1167,11 +1093,26 @@ void cg_batch(Ctx& c, const Op& op, int64_t N, int nl, const double* sigma, cons
                 }
             }
         }
-        // one more convergence check for systems finishing on the last step
-        if (fixed_iters <= 0 && it >= limit) step(it, true);
+        if (fixed_iters <= 0 && it >= limit) {
+            // one more convergence check for systems finishing on the last step
+            dim3 grid = dim3(unsigned(nparts), unsigned(active.size()));
+            if (ztpsmem)
+                cgzt_pa<NSR, 4><<<grid, ZT, ztpsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
+                                                         pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
+                                                         tol, 0, dact.as<int>());
+            else if (zsmem)
+                ZSEL(cgz_pa)<<<grid, ZT, zsmem, c.stream>>>(zg, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
+                                                      pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
+                                                      tol, 0, dact.as<int>());
+            else
+                cg_pa<<<grid, CT, 0, c.stream>>>(op, N, nl, k0, it, dsig.d(), dsigp.d(), R.d(),
+                                                pbuf(it + 1), pbuf(it), pA.d(), pB.d(), nparts, ss,
+                                                tol, 0, dact.as<int>());
+            c.check_launch();
+        }
         {
             dim3 gf = dim3(unsigned(std::min<int64_t>((N + 255) / 256, 1024)), unsigned(nb));
-            cg_finish<<<gf, CT, 0, c.stream>>>(N, nl, k0, it, X, dinv.d(), rr_parts(it), nparts, ss);
+            cg_finish<<<gf, CT, 0, c.stream>>>(N, nl, k0, it, X, dinv.d(), pB.d(), nparts, ss);
             c.check_launch();
         }
         if (stats) {
