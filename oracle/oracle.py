@@ -576,3 +576,135 @@ def fem_fields(geom, sigma, sigmap, inv_D, points, tol=1e-10, max_iter=20000, fi
                                          _d(pts), len(pts), tol, max_iter, fixed_iters, threads, _d(out),
                                          iters.ctypes.data_as(_ip), _d(rel)))
     return out, iters, rel
+
+
+# ------------------------------------------------------------- Krylov -----
+# The reference's recycled shifted-family solver (krylov_oracle.cpp;
+# krylov.cpp:21-463) on the FEM operator above.
+_kry_ready = False
+
+
+def _kry_lib():
+    global _kry_ready
+    L = lib()
+    if not _kry_ready:
+        g6 = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double]
+        L.oracle_krylov_last_error.restype = C.c_char_p
+        L.oracle_krylov_apply.argtypes = g6 + [C.c_double, C.c_int, C.c_double, C.c_double, _dp, _dp, _dp]
+        L.oracle_krylov_multishift.argtypes = g6 + [C.c_double, _dp, C.c_int, _dp, C.c_int, C.c_double,
+                                                    _dp, _dp, _dp, _dp, _ip]
+        L.oracle_krylov_harmonic_ritz.argtypes = [C.c_int, _dp, C.c_int, _dp, _dp, _ip]
+        L.oracle_krylov_deflation.argtypes = g6 + [C.c_double, C.c_int, _dp, _dp, C.c_int, _dp, _dp, _dp,
+                                                   _dp, _ip]
+        L.oracle_krylov_shifted_dense.argtypes = [C.c_int64, C.c_int, _dp, _dp, _dp, C.c_double, C.c_double,
+                                                  C.c_int, _dp, _dp, _ip]
+        L.oracle_krylov_solve_family.argtypes = g6 + [_dp, C.c_int, _dp, _dp, _ip, C.c_double, _dp, _ip,
+                                                      _ip, _dp, _ip, _dp, _ip]
+        _kry_ready = True
+    return L
+
+
+def _kcheck(rc):
+    if rc != 0:
+        msg = _kry_lib().oracle_krylov_last_error().decode()
+        raise (ValueError if rc == 1 else RuntimeError)(msg)
+
+
+class SolverConfig:
+    """krylov::SolverConfig (krylov.hpp:13-23), same defaults."""
+
+    def __init__(self, arnoldi_steps=80, deflation_dim=10, restart=50, tol=1e-8, max_restarts=40,
+                 center_shifts=True, jacobi=False, explicit_qr_update=False, threads=1):
+        self.arnoldi_steps, self.deflation_dim, self.restart = arnoldi_steps, deflation_dim, restart
+        self.tol, self.max_restarts, self.center_shifts = tol, max_restarts, center_shifts
+        self.jacobi, self.explicit_qr_update, self.threads = jacobi, explicit_qr_update, threads
+
+    def ints(self):
+        return np.array([self.arnoldi_steps, self.deflation_dim, self.restart, self.max_restarts,
+                         int(self.center_shifts), int(self.jacobi), int(self.explicit_qr_update),
+                         self.threads], dtype=np.int32)
+
+
+def krylov_apply(geom, sbar, x, sigma=0.0, sp=0.0, which=0):
+    """TransformedFamily.apply(sigma, sp, x) (which=0) or Rs x (which=1); also M^-1/2."""
+    x = _f64(x)
+    y = np.empty_like(x)
+    d = np.empty_like(x)
+    _kcheck(_kry_lib().oracle_krylov_apply(*geom, sbar, which, sigma, sp, _d(x), _d(y), _d(d)))
+    return y, d
+
+
+def krylov_multishift(geom, sbar, b, sigmas, n, tol):
+    """multishift_gmres on transform_family(sbar) with rhs M^-1/2 b:
+    (X, relres, V (N x (s+1)), Tbar ((s+1) x s), breakdown)."""
+    N = geom[0] * geom[1] * geom[2]
+    sig = _f64(sigmas)
+    X = np.zeros((N, len(sig)), order="F")
+    rel = np.zeros(len(sig))
+    V = np.zeros((N, n + 1), order="F")
+    T = np.zeros((n + 1, n), order="F")
+    info = np.zeros(2, dtype=np.int32)
+    _kcheck(_kry_lib().oracle_krylov_multishift(*geom, sbar, _d(_f64(b)), len(sig), _d(sig), n, tol, _d(X),
+                                                _d(rel), _d(V), _d(T), info.ctypes.data_as(_ip)))
+    s = int(info[0])
+    return X, rel, V[:, :s + 1].copy(order="F"), T[:s + 1, :s].copy(order="F"), bool(info[1])
+
+
+def krylov_harmonic_ritz(T, k):
+    T = np.asfortranarray(T, dtype=np.float64)
+    n = T.shape[1]
+    Z = np.zeros((n, k), order="F")
+    th = np.zeros(k)
+    info = np.zeros(1, dtype=np.int32)
+    _kcheck(_kry_lib().oracle_krylov_harmonic_ritz(n, _d(T), k, _d(Z), _d(th), info.ctypes.data_as(_ip)))
+    return Z, th, bool(info[0])
+
+
+def krylov_deflation(geom, sbar, V, T, Z):
+    """build_deflation_basis: (U, C, RU, rank_reduced)."""
+    V = np.asfortranarray(V, dtype=np.float64)
+    T = np.asfortranarray(T, dtype=np.float64)
+    Z = np.asfortranarray(Z, dtype=np.float64)
+    N, s, k = V.shape[0], T.shape[1], Z.shape[1]
+    U, Cm, RU = (np.zeros((N, k), order="F") for _ in range(3))
+    info = np.zeros(2, dtype=np.int32)
+    _kcheck(_kry_lib().oracle_krylov_deflation(*geom, sbar, s, _d(V), _d(T), k, _d(Z), _d(U), _d(Cm), _d(RU),
+                                               info.ctypes.data_as(_ip)))
+    ko = int(info[0])
+    return U[:, :ko].copy(order="F"), Cm[:, :ko].copy(order="F"), RU[:, :ko].copy(order="F"), bool(info[1])
+
+
+def krylov_shifted_dense(U, Cm, RU, sigma, sp, force_qr=False):
+    """ShiftedDeflation(U, C, RU; sigma, sp): dense (C_j, U_j, cholesky_failed)."""
+    U, Cm, RU = (np.asfortranarray(a, dtype=np.float64) for a in (U, Cm, RU))
+    N, k = U.shape
+    Cj, Uj = np.zeros((N, k), order="F"), np.zeros((N, k), order="F")
+    info = np.zeros(1, dtype=np.int32)
+    _kcheck(_kry_lib().oracle_krylov_shifted_dense(N, k, _d(U), _d(Cm), _d(RU), sigma, sp, int(force_qr),
+                                                   _d(Cj), _d(Uj), info.ctypes.data_as(_ip)))
+    return Cj, Uj, bool(info[0])
+
+
+def krylov_solve_family(geom, b, shifts, cfg=None):
+    """solve_family (krylov.cpp:400-463) for one rhs b (original variables):
+    dict(X (N x nshift), iters, matvecs, relres, converged, phase1_relres,
+    phase1_steps, defl_k, rank_reduced, pencil_shifted, breakdown,
+    all_converged, first_failure)."""
+    cfg = cfg or SolverConfig()
+    N = geom[0] * geom[1] * geom[2]
+    sh = np.asarray(shifts, dtype=np.float64).reshape(-1, 2)
+    ns = len(sh)
+    sig, sigp = np.ascontiguousarray(sh[:, 0]), np.ascontiguousarray(sh[:, 1])
+    X = np.zeros((N, ns), order="F")
+    it, mv, cv = (np.zeros(ns, dtype=np.int32) for _ in range(3))
+    rel, p1 = np.zeros(ns), np.zeros(ns)
+    info = np.zeros(7, dtype=np.int32)
+    ci = cfg.ints()
+    _kcheck(_kry_lib().oracle_krylov_solve_family(
+        *geom, _d(_f64(b)), ns, _d(sig), _d(sigp), ci.ctypes.data_as(_ip), cfg.tol, _d(X),
+        it.ctypes.data_as(_ip), mv.ctypes.data_as(_ip), _d(rel), cv.ctypes.data_as(_ip), _d(p1),
+        info.ctypes.data_as(_ip)))
+    return dict(X=X, iters=it, matvecs=mv, relres=rel, converged=cv.astype(bool), phase1_relres=p1,
+                phase1_steps=int(info[0]), defl_k=int(info[1]), rank_reduced=bool(info[2]),
+                pencil_shifted=bool(info[3]), breakdown=bool(info[4]), all_converged=bool(info[5]),
+                first_failure=int(info[6]))
