@@ -154,6 +154,70 @@ hydot_status hydot_fields_solve_fem(hydot_ctx ctx, const hydot_grid_geom* geom, 
                                     double tol, int max_iter, int fixed_iters, double* out_dev,
                                     int* iters_h, double* relres_h);
 
+/* ------------------------------------------------------------ krylov -- */
+/* The reference's recycled shifted-family solver (krylov.hpp, krylov.cpp:
+ * 21-463) on the FEM operator above.  hydot_krylov_config is
+ * krylov::SolverConfig (krylov.hpp:13-23) without `threads` (the device
+ * solves every shift of every right-hand side of a batch together);
+ * hydot_krylov_config_default gives the reference defaults (80, 10, 50,
+ * 1e-8, 40, center, no Jacobi, Gram/Cholesky update). */
+typedef struct hydot_krylov_config {
+    int arnoldi_steps;      /* phase-1 basis size n (<= 200) */
+    int deflation_dim;      /* k harmonic Ritz vectors (<= 32) */
+    int restart;            /* m, augmented GMRES cycle length (<= 200) */
+    double tol;             /* relative residual target */
+    int max_restarts;
+    int center_shifts;      /* sbar' = mean sigma' folded into Ks */
+    int jacobi;             /* fixed diagonal right preconditioner */
+    int explicit_qr_update; /* bypass the Gram/Cholesky basis update */
+} hydot_krylov_config;
+void hydot_krylov_config_default(hydot_krylov_config* cfg);
+
+/* krylov::IterationStats (krylov.hpp:109-114) per (rhs, shift), plus the
+ * phase-1 least-squares residual of that shift (MultishiftResult::relres). */
+typedef struct hydot_krylov_stats {
+    int iterations; /* inner Arnoldi steps of phase 2 */
+    int matvecs;
+    double relres;
+    int converged;
+    double phase1_relres;
+} hydot_krylov_stats;
+
+/* Per right-hand side: FamilyResult (krylov.hpp:128-134) summary and the
+ * phase-1 / deflation facts (ArnoldiData::steps, breakdown, HarmonicRitz::
+ * pencil_shifted, DeflationBasis::k / rank_reduced, ShiftedDeflation::
+ * cholesky_failed count). */
+typedef struct hydot_krylov_family {
+    int phase1_steps;
+    int deflation_k;
+    int rank_reduced;
+    int pencil_shifted;
+    int breakdown;
+    int cholesky_failed;
+    int all_converged;
+    int first_failure; /* shift index, -1 if none */
+} hydot_krylov_family;
+
+/* krylov::solve_family (krylov.hpp:137-141, krylov.cpp:400-463) for n_rhs
+ * right-hand sides b_dev (n_rhs x N, device) and the shifts (sigma_j,
+ * sigma'_j): X_dev[(r*n_shifts + j)*N + v] = x_{r,j} in the original
+ * variables.  stats_h: n_rhs*n_shifts entries, fam_h: n_rhs (both nullable).
+ * Like the reference, unconverged systems are reported, not raised;
+ * b = 0 is HYDOT_EINVAL ("multishift_gmres: b must be nonzero"). */
+hydot_status hydot_solve_family_fem(hydot_ctx ctx, const hydot_grid_geom* geom, int n_shifts,
+                                    const double* sigma_h, const double* sigma_prime_h, const double* b_dev,
+                                    int n_rhs, const hydot_krylov_config* cfg, double* X_dev,
+                                    hydot_krylov_stats* stats_h, hydot_krylov_family* fam_h);
+/* born::compute_fields (born.cpp:39-80) with that solver: the point sources
+ * of hydot_fields_solve_fem, X scaled by inv_D per wavelength, same output
+ * layout; an unconverged system raises HYDOT_ERUNTIME ("field solve failed
+ * at point p, wavelength index l", born.cpp:58-61). */
+hydot_status hydot_fields_solve_fem_gmres(hydot_ctx ctx, const hydot_grid_geom* geom, int n_lambda,
+                                          const double* sigma_h, const double* sigma_prime_h,
+                                          const double* inv_D_h, const double* points_h, int n_points,
+                                          const hydot_krylov_config* cfg, double* out_dev,
+                                          hydot_krylov_stats* stats_h, hydot_krylov_family* fam_h);
+
 /* --------------------------------------------------------------- born -- */
 /* born::assemble_H_block (born.hpp:61-62, born.cpp:82-98):
  *   out[(d*n_lambda + l)*ld + v] = (-nu) * ((phi_d[v,l] * phi_s[v,l]) * w[v])

@@ -58,6 +58,23 @@ class GridGeom(C.Structure):
                 ("Ly", C.c_double), ("Lz", C.c_double)]
 
 
+class KrylovConfig(C.Structure):
+    _fields_ = [("arnoldi_steps", C.c_int), ("deflation_dim", C.c_int), ("restart", C.c_int),
+                ("tol", C.c_double), ("max_restarts", C.c_int), ("center_shifts", C.c_int),
+                ("jacobi", C.c_int), ("explicit_qr_update", C.c_int)]
+
+
+class KrylovStats(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("matvecs", C.c_int), ("relres", C.c_double),
+                ("converged", C.c_int), ("phase1_relres", C.c_double)]
+
+
+class KrylovFamily(C.Structure):
+    _fields_ = [("phase1_steps", C.c_int), ("deflation_k", C.c_int), ("rank_reduced", C.c_int),
+                ("pencil_shifted", C.c_int), ("breakdown", C.c_int), ("cholesky_failed", C.c_int),
+                ("all_converged", C.c_int), ("first_failure", C.c_int)]
+
+
 class PalsParams(C.Structure):
     _fields_ = [("np", C.c_int), ("alpha", _dp), ("beta", _dp), ("centers", _dp),
                 ("tau_level", C.c_double), ("eps_H", C.c_double), ("nu_norm", C.c_double)]
@@ -168,6 +185,13 @@ SIGNATURES = {
     "hydot_apply_fem": (C.c_int, [_vp, C.POINTER(GridGeom), C.c_double, C.c_double, _dp, _dp]),
     "hydot_fields_solve_fem": (C.c_int, [_vp, C.POINTER(GridGeom), C.c_int, _dp, _dp, _dp, _dp, C.c_int,
                                          C.c_double, C.c_int, C.c_int, _dp, _ip, _dp]),
+    "hydot_krylov_config_default": (None, [C.POINTER(KrylovConfig)]),
+    "hydot_solve_family_fem": (C.c_int, [_vp, C.POINTER(GridGeom), C.c_int, _dp, _dp, _dp, C.c_int,
+                                         C.POINTER(KrylovConfig), _dp, C.POINTER(KrylovStats),
+                                         C.POINTER(KrylovFamily)]),
+    "hydot_fields_solve_fem_gmres": (C.c_int, [_vp, C.POINTER(GridGeom), C.c_int, _dp, _dp, _dp, _dp,
+                                               C.c_int, C.POINTER(KrylovConfig), _dp,
+                                               C.POINTER(KrylovStats), C.POINTER(KrylovFamily)]),
 }
 
 _LIB = None

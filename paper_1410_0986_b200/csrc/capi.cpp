@@ -296,6 +296,39 @@ hydot_status hydot_fields_solve_fem(hydot_ctx ctx, const hydot_grid_geom* geom, 
     });
 }
 
+void hydot_krylov_config_default(hydot_krylov_config* cfg) {
+    if (!cfg) return;
+    *cfg = hydot_krylov_config{80, 10, 50, 1e-8, 40, 1, 0, 0};  // krylov.hpp:13-23
+}
+
+hydot_status hydot_solve_family_fem(hydot_ctx ctx, const hydot_grid_geom* geom, int n_shifts,
+                                    const double* sigma_h, const double* sigma_prime_h, const double* b_dev,
+                                    int n_rhs, const hydot_krylov_config* cfg, double* X_dev,
+                                    hydot_krylov_stats* stats_h, hydot_krylov_family* fam_h) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!geom || !sigma_h || !sigma_prime_h || !b_dev || !cfg || !X_dev)
+            throw std::invalid_argument("hydot_solve_family_fem: null argument");
+        const int64_t N = int64_t(geom->nx) * geom->ny * geom->nz;
+        solve_family_fem(c, *geom, n_shifts, sigma_h, sigma_prime_h, b_dev, n_rhs, *cfg, nullptr, X_dev, N, stats_h,
+                         fam_h);
+    });
+}
+
+hydot_status hydot_fields_solve_fem_gmres(hydot_ctx ctx, const hydot_grid_geom* geom, int n_lambda,
+                                          const double* sigma_h, const double* sigma_prime_h,
+                                          const double* inv_D_h, const double* points_h, int n_points,
+                                          const hydot_krylov_config* cfg, double* out_dev,
+                                          hydot_krylov_stats* stats_h, hydot_krylov_family* fam_h) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!geom || !sigma_h || !sigma_prime_h || !inv_D_h || !points_h || !cfg || !out_dev)
+            throw std::invalid_argument("hydot_fields_solve_fem_gmres: null argument");
+        fields_solve_fem_gmres(c, *geom, n_lambda, sigma_h, sigma_prime_h, inv_D_h, points_h, n_points, *cfg,
+                               out_dev, stats_h, fam_h);
+    });
+}
+
 hydot_status hydot_apply7(hydot_ctx ctx, const hydot_grid7* grid, double sigma,
                           double sigma_prime, const double* x_dev, double* y_dev) {
     return guard(ctx ? ctx->c.get() : nullptr, [&] {

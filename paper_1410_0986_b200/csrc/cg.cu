@@ -1262,6 +1262,10 @@ FemSetup fem_setup(Ctx& c, const hydot_grid_geom& g) {
 
 }  // namespace
 
+void fem_element_host(double hx, double hy, double hz, double Ke[64], double Me[64], double Re[16]) {
+    fem_element_matrices(hx, hy, hz, Ke, Me, Re);
+}
+
 void apply_fem(Ctx& c, const hydot_grid_geom& g, double sigma, double sigmap, const double* x, double* y) {
     FemSetup f = fem_setup(c, g);
     int blocks = int(std::min<int64_t>((f.N + 255) / 256, int64_t(c.num_sms) * 16));
@@ -1270,15 +1274,15 @@ void apply_fem(Ctx& c, const hydot_grid_geom& g, double sigma, double sigmap, co
     c.sync();
 }
 
-void fields_solve_fem(Ctx& c, const hydot_grid_geom& g, int nl, const double* sigma, const double* sigmap,
-                      const double* inv_D, const double* points, int n_pts, double tol, int max_iter,
-                      int fixed_iters, double* out, CGStats* stats) {
-    if (nl <= 0 || n_pts <= 0) throw std::invalid_argument("compute_fields: no wavelengths");
-    FemSetup f = fem_setup(c, g);
-    // source_rhs (born.cpp:27-35): trilinear point_source_vector
-    // (grid.cpp:212-237) with the Dirichlet vertices zeroed
-    std::vector<int64_t> ridx(size_t(n_pts) * 8, -1);
-    std::vector<double> rw(size_t(n_pts) * 8, 0.0), b2(size_t(n_pts), 0.0);
+// source_rhs (born.cpp:27-35): trilinear point_source_vector (grid.cpp:212-237)
+// with the Dirichlet vertices zeroed -- 8 (vertex, weight) pairs per point
+// (vertex -1 = no entry) and the squared norm of each source vector
+void fem_point_weights(const hydot_grid_geom& g, const double* points, int n_pts, std::vector<int64_t>& ridx,
+                       std::vector<double>& rw, std::vector<double>& b2) {
+    const double hx = 2 * g.Lx / (g.nx - 1), hy = 2 * g.Ly / (g.ny - 1), hz = g.Lz / (g.nz - 1);
+    ridx.assign(size_t(n_pts) * 8, -1);
+    rw.assign(size_t(n_pts) * 8, 0.0);
+    b2.assign(size_t(n_pts), 0.0);
     auto clamp_cell = [](double t, int ncells) {
         int cc = int(std::floor(t));
         return cc < 0 ? 0 : (cc > ncells - 1 ? ncells - 1 : cc);
@@ -1287,7 +1291,7 @@ void fields_solve_fem(Ctx& c, const hydot_grid_geom& g, int nl, const double* si
         const double rx = points[3 * s], ry = points[3 * s + 1], rz = points[3 * s + 2];
         if (!(rx >= -g.Lx && rx <= g.Lx && ry >= -g.Ly && ry <= g.Ly && rz >= 0.0 && rz <= g.Lz))
             throw std::invalid_argument("point_source_vector: point outside domain");
-        const double tx = (rx + g.Lx) / f.hx, ty = (ry + g.Ly) / f.hy, tz = rz / f.hz;
+        const double tx = (rx + g.Lx) / hx, ty = (ry + g.Ly) / hy, tz = rz / hz;
         const int cx = clamp_cell(tx, g.nx - 1), cy = clamp_cell(ty, g.ny - 1), cz = clamp_cell(tz, g.nz - 1);
         const double xi = 2 * (tx - cx) - 1, eta = 2 * (ty - cy) - 1, zeta = 2 * (tz - cz) - 1;
         double nrm2 = 0.0;
@@ -1303,6 +1307,16 @@ void fields_solve_fem(Ctx& c, const hydot_grid_geom& g, int nl, const double* si
         if (nrm2 == 0.0) throw std::invalid_argument("source support falls entirely on the Dirichlet boundary");
         b2[size_t(s)] = nrm2;
     }
+}
+
+void fields_solve_fem(Ctx& c, const hydot_grid_geom& g, int nl, const double* sigma, const double* sigmap,
+                      const double* inv_D, const double* points, int n_pts, double tol, int max_iter,
+                      int fixed_iters, double* out, CGStats* stats) {
+    if (nl <= 0 || n_pts <= 0) throw std::invalid_argument("compute_fields: no wavelengths");
+    FemSetup f = fem_setup(c, g);
+    std::vector<int64_t> ridx;
+    std::vector<double> rw, b2;
+    fem_point_weights(g, points, n_pts, ridx, rw, b2);
     cg_batch(c, f.op, f.N, nl, sigma, sigmap, inv_D, ridx, rw, b2, n_pts, tol, max_iter, fixed_iters, out, stats);
 }
 

@@ -286,6 +286,20 @@ void fields_solve_fem(Ctx& c, const hydot_grid_geom& g, int nl, const double* si
                       const double* inv_D, const double* points, int n_pts, double tol, int max_iter,
                       int fixed_iters, double* out, CGStats* stats);
 
+// the 8 trilinear (vertex, weight) pairs of each FEM point source (born.cpp:27-35)
+void fem_point_weights(const hydot_grid_geom& g, const double* points, int n_pts, std::vector<int64_t>& ridx,
+                       std::vector<double>& rw, std::vector<double>& b2);
+// gmres.cu: krylov::solve_family (krylov.cpp:400-463) on the FEM operator for
+// n_rhs device right-hand sides b_dev (n_rhs x N); X (original variables,
+// times mult[shift] when given) at X_dev + (r * nsh + j) * x_stride
+void solve_family_fem(Ctx& c, const hydot_grid_geom& g, int nsh, const double* sigma, const double* sigmap,
+                      const double* b_dev, int n_rhs, const hydot_krylov_config& cfg, const double* mult,
+                      double* X_dev, int64_t x_stride, hydot_krylov_stats* stats, hydot_krylov_family* fam);
+// compute_fields (born.cpp:39-80) with the reference's solver on its operator
+void fields_solve_fem_gmres(Ctx& c, const hydot_grid_geom& g, int nl, const double* sigma, const double* sigmap,
+                            const double* inv_D, const double* points, int n_pts, const hydot_krylov_config& cfg,
+                            double* out, hydot_krylov_stats* stats, hydot_krylov_family* fam);
+
 // forward.cpp: full_diffusion_forward (experiments.cpp:154-206) for the
 // 7-point operator; outputs ns x nd x nl measurements (device)
 void full_forward(Ctx& c, const hydot_grid7& g, int nl, const double* sigma, const double* sigmap,
