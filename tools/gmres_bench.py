@@ -53,7 +53,7 @@ def main():
                 F, fam = krylov.compute_fields_fem_gmres(ctx, geom, st.sigma, st.sigma_prime, st.inv_D, xyz,
                                                          krylov.SolverConfig(tol=a.tol))
                 its = [s.iterations for f in fam for s in f.stats]
-                info = dict(phase1_steps=[f.phase1_steps for f in fam][:4], deflation_k=fam[0].deflation_k,
+                info = dict(phase1_steps=[f.phase1_matvecs for f in fam][:4], deflation_k=fam[0].deflation_k,
                             phase2_iters_total=int(sum(its)), phase2_iters_max=int(max(its)),
                             relres_max=float(max(s.relres for f in fam for s in f.stats)),
                             matvecs_total=int(sum(s.matvecs for f in fam for s in f.stats)))
