@@ -272,6 +272,33 @@ hydot_status hydot_randsvd(hydot_ctx ctx, int64_t m, int64_t n, const double* a_
                            double eps, int p, int kprobe, uint64_t seed, int category, int r0,
                            hydot_factor* out, hydot_ledger* ledger_h);
 
+/* lowrank::LinOp (lowrank.hpp:56-63): a matrix-free operator given by
+ * callbacks on DEVICE operands (column-major, unit column stride).  mv / rmv
+ * are A x and A^T y; mm / rmm are the optional block forms A X (X cols x k,
+ * ldx; Y rows x k, ldy) and A^T Y -- when NULL the columns go through mv /
+ * rmv one by one, as apply_mm does (lowrank.cpp:95-107).  A callback must
+ * enqueue its work on `stream` (a cudaStream_t: its inputs are ready there
+ * and its output is consumed there) and return 0; any other value aborts
+ * the call with HYDOT_ERUNTIME. */
+typedef int (*hydot_mv_fn)(void* user, const double* x_dev, double* y_dev, void* stream);
+typedef int (*hydot_mm_fn)(void* user, int64_t k, const double* X_dev, int64_t ldx, double* Y_dev,
+                           int64_t ldy, void* stream);
+typedef struct {
+    int64_t rows, cols;
+    hydot_mv_fn mv, rmv;
+    hydot_mm_fn mm, rmm;
+    void* user;
+} hydot_linop;
+
+/* lowrank::randsvd (lowrank.hpp:70-72, lowrank.cpp:131-199) on a LinOp: the
+ * same sketch passes, Gaussian stream, accept / double / Q = I decisions and
+ * ledger as hydot_randsvd; the Q = I branch takes A^T as rmm(I_rows) like
+ * the reference (lowrank.cpp:159-164, 184).  With the dense products as
+ * callbacks it returns hydot_randsvd's factor. */
+hydot_status hydot_randsvd_linop(hydot_ctx ctx, const hydot_linop* A, double eps, int p, int kprobe,
+                                 uint64_t seed, int category, int r0, hydot_factor* out,
+                                 hydot_ledger* ledger_h);
+
 /* lowrank::agglomerate (lowrank.hpp:98-100, lowrank.cpp:321-359); the
  * reference hard-codes p=20, kprobe=10 (lowrank.cpp:344). */
 hydot_status hydot_agglomerate(hydot_ctx ctx, hydot_factor f1, hydot_factor f2, double eps,

@@ -40,6 +40,16 @@ class Provider(C.Structure):
                 ("user", C.c_void_p)]
 
 
+MV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
+MM_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                    C.c_void_p)
+
+
+class LinOp(C.Structure):
+    _fields_ = [("rows", C.c_int64), ("cols", C.c_int64), ("mv", MV_FN), ("rmv", MV_FN),
+                ("mm", MM_FN), ("rmm", MM_FN), ("user", C.c_void_p)]
+
+
 class BornFields(C.Structure):
     _fields_ = [("N", C.c_int64), ("n_lambda", C.c_int), ("n_sources", C.c_int),
                 ("n_det", C.c_int), ("incident_dev_h", C.POINTER(_dp)),
@@ -133,6 +143,9 @@ SIGNATURES = {
     "hydot_randsvd": (C.c_int, [_vp, C.c_int64, C.c_int64, _dp, C.c_int64, C.c_double, C.c_int,
                                 C.c_int, C.c_uint64, C.c_int, C.c_int, C.POINTER(_vp),
                                 C.POINTER(Ledger)]),
+    "hydot_randsvd_linop": (C.c_int, [_vp, C.POINTER(LinOp), C.c_double, C.c_int, C.c_int,
+                                      C.c_uint64, C.c_int, C.c_int, C.POINTER(_vp),
+                                      C.POINTER(Ledger)]),
     "hydot_agglomerate": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_uint64, C.c_int, C.c_int,
                                     C.c_int, C.POINTER(_vp), C.POINTER(Ledger)]),
     "hydot_tolerance_schedule": (C.c_int, [C.c_double, C.c_int, C.c_int, _dp]),

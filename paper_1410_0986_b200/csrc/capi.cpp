@@ -482,6 +482,42 @@ hydot_status hydot_randsvd(hydot_ctx ctx, int64_t m, int64_t n, const double* a_
     });
 }
 
+hydot_status hydot_randsvd_linop(hydot_ctx ctx, const hydot_linop* A, double eps, int p, int kprobe,
+                                 uint64_t seed, int category, int r0, hydot_factor* out,
+                                 hydot_ledger* ledger_h) {
+    return guard(ctx ? ctx->c.get() : nullptr, [&] {
+        Ctx& c = ctx_of(ctx);
+        if (!out || !A || A->rows < 0 || A->cols < 0)
+            throw std::invalid_argument("randsvd: bad operator");
+        const bool empty = A->rows == 0 || A->cols == 0;
+        if (!empty && ((!A->mm && !A->mv) || (!A->rmm && !A->rmv)))
+            throw std::invalid_argument("randsvd: operator without products");
+        LinOpDev op;
+        op.rows = A->rows;
+        op.cols = A->cols;
+        // apply_mm (lowrank.cpp:95-107): the block form if present, else by columns
+        auto product = [&c, A](hydot_mm_fn blk, hydot_mv_fn col, int64_t in_rows, int64_t out_rows) {
+            return [&c, A, blk, col, in_rows, out_rows](int64_t k, const double* X, double* Y) {
+                int rc = 0;
+                if (blk) {
+                    rc = blk(A->user, k, X, in_rows, Y, out_rows, c.stream);
+                } else {
+                    for (int64_t j = 0; j < k && rc == 0; ++j)
+                        rc = col(A->user, X + j * in_rows, Y + j * out_rows, c.stream);
+                }
+                if (rc != 0) throw std::runtime_error("randsvd: operator callback failed");
+            };
+        };
+        op.mm = product(A->mm, A->mv, A->cols, A->rows);
+        op.rmm = product(A->rmm, A->rmv, A->rows, A->cols);
+        Ledger l;
+        Factor f = randsvd(c, op, eps, p, kprobe, seed, &l, category, r0);
+        c.sync();
+        ledger_out(l, ledger_h);
+        *out = wrap(ctx->c, std::move(f));
+    });
+}
+
 hydot_status hydot_agglomerate(hydot_ctx ctx, hydot_factor f1, hydot_factor f2, double eps,
                                uint64_t seed, int rank_hint, int p, int kprobe, hydot_factor* out,
                                hydot_ledger* ledger_h) {

@@ -356,8 +356,29 @@ bool trace_randsvd() {
     return on;
 }
 
+namespace {
+Factor randsvd_impl(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, const LinOpDev* op,
+                    double eps, int p, int kprobe, uint64_t seed, Ledger* l, int cat, int r0,
+                    bool lazy_v);
+}
+
 Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, double eps, int p,
                int kprobe, uint64_t seed, Ledger* l, int cat, int r0, bool lazy_v) {
+    return randsvd_impl(c, m, n, At, lda, nullptr, eps, p, kprobe, seed, l, cat, r0, lazy_v);
+}
+
+Factor randsvd(Ctx& c, const LinOpDev& A, double eps, int p, int kprobe, uint64_t seed, Ledger* l,
+               int cat, int r0) {
+    if (A.rows > 0 && A.cols > 0 && (!A.mm || !A.rmm))
+        throw std::invalid_argument("randsvd: operator without products");
+    return randsvd_impl(c, A.rows, A.cols, nullptr, 0, &A, eps, p, kprobe, seed, l, cat, r0, false);
+}
+
+namespace {
+// At != nullptr: dense operator (row-major A); else the callbacks of *op
+Factor randsvd_impl(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, const LinOpDev* op,
+                    double eps, int p, int kprobe, uint64_t seed, Ledger* l, int cat, int r0,
+                    bool lazy_v) {
     Factor f;
     f.rows = m;
     f.cols = n;
@@ -384,7 +405,7 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
         // capped at 16 GB (config 1's root needs 3.8 GB); cudaMemGetInfo is
         // not used here -- it cost 2 % of the step and most of the e2e overlap
         const bool small = double(n) * double(m) * 16.0 <= 16.0 * double(1ull << 30);
-        if (!(rs1 >= nmax && m <= n) && rs2 >= nmax && m <= n && n >= 2 * m && m > 48 && small &&
+        if (At && !(rs1 >= nmax && m <= n) && rs2 >= nmax && m <= n && n >= 2 * m && m > 48 && small &&
             async_v_on() && speculate_on()) {
             // speculation is optional: if its buffers do not fit, run without it
             try {
@@ -446,7 +467,10 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
         const int64_t w = rs + kprobe;
         const double* Om = rng->take(n * w);  // [Omega1 | Omega2], n x (rs+k)
         YP = dalloc(c, size_t(m * w));
-        dgemm(c, true, false, m, w, n, 1.0, At, lda, Om, n, 0.0, YP.d(), m);
+        if (At)
+            dgemm(c, true, false, m, w, n, 1.0, At, lda, Om, n, 0.0, YP.d(), m);
+        else
+            op->mm(w, Om, YP.d());  // [Y | P] = A [Omega1 | Omega2]
         charge(l, cat, 2.0 * double(m) * double(n) * double(rs));      // apply_mm Y
         charge(l, cat, 2.0 * double(m) * double(n) * double(kprobe));  // apply_mm P
         svdY = fast_thin_svd(c, YP.d(), m, false, m, rs, l, cat);
@@ -476,13 +500,24 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
     DBuf Bt;
     const double* Btp;
     int64_t ldb;
-    if (identity) {
+    if (identity && At) {
         qc = m;
         Btp = At;  // A^T I = A^T (exact)
         ldb = lda;
+    } else if (identity) {
+        qc = m;
+        DBuf I = dalloc(c, size_t(m * m));
+        set_identity(c, m, m, I.d(), m);
+        Bt = dalloc(c, size_t(n * m));
+        op->rmm(m, I.d(), Bt.d());  // apply_mm(A, I, true)
+        Btp = Bt.d();
+        ldb = n;
     } else {
         Bt = dalloc(c, size_t(n * qc));
-        dgemm(c, false, false, n, qc, m, 1.0, At, lda, svdY.U.d(), m, 0.0, Bt.d(), n);
+        if (At)
+            dgemm(c, false, false, n, qc, m, 1.0, At, lda, svdY.U.d(), m, 0.0, Bt.d(), n);
+        else
+            op->rmm(qc, svdY.U.d(), Bt.d());
         Btp = Bt.d();
         ldb = n;
     }
@@ -528,6 +563,7 @@ Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, doub
     if (!lazy_v) materialize_v_async(c, f);
     return f;
 }
+}  // namespace
 
 Factor agglomerate(Ctx& c, const Factor& f1, const Factor& f2, double eps, uint64_t seed,
                    Ledger* l, int rank_hint, int p, int kprobe, bool lazy_v) {

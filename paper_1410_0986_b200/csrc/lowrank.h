@@ -73,6 +73,19 @@ SVDd thin_svd(Ctx& c, const double* S, int64_t ld, bool trans, int64_t m, int64_
 Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, double eps, int p,
                int kprobe, uint64_t seed, Ledger* l, int cat, int r0, bool lazy_v = false);
 
+// LinOp (lowrank.hpp:56-63) with device operands: mm forms Y (m x k, ld m)
+// = A X from X (n x k, ld n), rmm forms X (n x k, ld n) = A^T Y; both
+// column-major, enqueued on c.stream.
+struct LinOpDev {
+    int64_t rows = 0, cols = 0;
+    std::function<void(int64_t k, const double* X, double* Y)> mm, rmm;
+};
+// randsvd on a matrix-free operator: the same branch structure, stream and
+// ledger; the Q = I branch obtains A^T as rmm(I_m) like the reference's
+// apply_mm(A, Q, true) with Q = I (lowrank.cpp:159-164, 184)
+Factor randsvd(Ctx& c, const LinOpDev& A, double eps, int p, int kprobe, uint64_t seed, Ledger* l,
+               int cat, int r0);
+
 Factor agglomerate(Ctx& c, const Factor& f1, const Factor& f2, double eps, uint64_t seed,
                    Ledger* l, int rank_hint, int p, int kprobe, bool lazy_v = false);
 

@@ -129,10 +129,103 @@ def _f64cuda(ctx, A):
     return A.to(device=f"cuda:{ctx.device}", dtype=torch.float64).contiguous()
 
 
-def randsvd(ctx: Context, A: torch.Tensor, eps: float, p: int = 20, kprobe: int = 10,
+@dataclass
+class LinOp:
+    """LinOp (lowrank.hpp:56-63): rows, cols and the products mv (A x), rmv
+    (A^T y) and, optionally, the block forms mm (A X) / rmm (A^T Y).  The
+    callables take and return float64 CUDA tensors (vectors for mv / rmv,
+    (cols x k) -> (rows x k) matrices for mm, the reverse for rmm) and must
+    work on the current torch stream."""
+    rows: int = 0
+    cols: int = 0
+    mv: Optional[Callable] = None
+    rmv: Optional[Callable] = None
+    mm: Optional[Callable] = None
+    rmm: Optional[Callable] = None
+
+
+def dense_op(A: torch.Tensor) -> LinOp:
+    """dense_op (lowrank.cpp:111-120): the four products of a dense CUDA
+    matrix as a LinOp.  randsvd also takes the tensor itself (the library's
+    own DMMA products); this form is for code written against LinOp."""
+    return LinOp(rows=A.shape[0], cols=A.shape[1], mv=lambda x: A @ x, rmv=lambda y: A.T @ y,
+                 mm=lambda X: A @ X, rmm=lambda Y: A.T @ Y)
+
+
+def _randsvd_linop(ctx, A: LinOp, eps, p, kprobe, seed, ledger, cat, r0):
+    dev = torch.device(f"cuda:{ctx.device}")
+    err: list = []
+
+    def view(ptr, rows, k, ld):
+        # column-major (rows x k, ld) device memory as a (k, ld) row-major tensor
+        n = (k - 1) * ld + rows
+        flat = _tensor_from_ptr(ptr, n, dev)
+        return flat.as_strided((k, rows), (ld, 1))
+
+    def run(fn, stream, body):
+        try:
+            ext = torch.cuda.ExternalStream(stream, device=dev)
+            with torch.cuda.stream(ext):
+                body()
+            return 0
+        except Exception as e:  # reported through the status code
+            err.append(e)
+            return 1
+
+    def mk_mv(fn, nin, nout):
+        if fn is None:
+            return _lib.MV_FN()
+
+        def cb(user, x, y, stream):
+            def body():
+                out = fn(view(x, nin, 1, nin)[0])
+                view(y, nout, 1, nout)[0].copy_(out.reshape(nout))
+            return run(fn, stream, body)
+        return _lib.MV_FN(cb)
+
+    def mk_mm(fn, nin, nout):
+        if fn is None:
+            return _lib.MM_FN()
+
+        def cb(user, k, X, ldx, Y, ldy, stream):
+            def body():
+                out = fn(view(X, nin, k, ldx).T)
+                view(Y, nout, k, ldy).copy_(out.reshape(nout, k).T)
+            return run(fn, stream, body)
+        return _lib.MM_FN(cb)
+
+    op = _lib.LinOp(A.rows, A.cols, mk_mv(A.mv, A.cols, A.rows), mk_mv(A.rmv, A.rows, A.cols),
+                    mk_mm(A.mm, A.cols, A.rows), mk_mm(A.rmm, A.rows, A.cols), None)
+    h = C.c_void_p()
+    led = Ledger()
+    st = lib().hydot_randsvd_linop(ctx.h, C.byref(op), eps, p, kprobe, _seed(seed), cat, r0,
+                                   C.byref(h), C.byref(led))
+    if err:
+        raise err[0]
+    check(st, ctx.h)
+    if ledger is not None:
+        for f in ("leaf", "agglomeration", "recompress", "other", "kernel_tally"):
+            setattr(ledger, f, getattr(ledger, f) + getattr(led, f))
+    return LowRankFactor(ctx, h)
+
+
+def _tensor_from_ptr(ptr, n, dev):
+    """n float64 values at device address ptr as a torch tensor (no copy)."""
+    class _Mem:
+        pass
+    m = _Mem()
+    m.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f8", "data": (int(ptr), False),
+                                  "version": 2}
+    return torch.as_tensor(m, device=dev)
+
+
+def randsvd(ctx: Context, A, eps: float, p: int = 20, kprobe: int = 10,
             seed: int = 0, ledger: Optional[Ledger] = None, cat: int = OTHER, r0: int = 1):
-    """randsvd(dense_op(A), ...) (lowrank.hpp:70-72, lowrank.cpp:131-199).
-    A: m x n (row-major torch tensor; any device)."""
+    """randsvd (lowrank.hpp:70-72, lowrank.cpp:131-199).  A: a LinOp
+    (matrix-free: hydot_randsvd_linop), or an m x n tensor standing for
+    dense_op(A) (row-major torch tensor; any device)."""
+    if isinstance(A, LinOp):
+        return _randsvd_linop(ctx, A, eps, p, kprobe, seed, ledger, cat, r0)
     A = _f64cuda(ctx, A)
     m, n = A.shape
     h = C.c_void_p()

@@ -387,3 +387,87 @@ def test_streamed_fields_provider_equals_resident_fields(ctx):
     assert len(prov.log) == cfg.n_sources and max(e["relres_max"] for e in prov.log) <= 1e-10
     D1, D2 = r1.factor.dense(), r2.factor.dense()
     assert float(torch.linalg.norm(D1 - D2)) <= 1e-13 * float(torch.linalg.norm(D1))
+
+
+# ---- matrix-free LinOp (lowrank.hpp:56-63; hydot_randsvd_linop) -------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,r,noise,eps,r0,block", [
+    (60, 400, 8, 0.0, 1e-8, 1, True),       # exact rank, block products
+    (60, 400, 8, 0.0, 1e-8, 1, False),      # the same through mv / rmv column by column
+    (40, 55, 7, 0.0, 1e-10, 1, True),       # Q = I branch: A^T = rmm(I)
+    (200, 3000, 12, 1e-9, 1e-6, 1, True),   # adaptive sketch: several passes
+    (80, 32768, 30, 1e-8, 6.6e-9, 43, True),
+])
+def test_randsvd_linop_matches_dense_and_oracle(ctx, oracle, m, n, r, noise, eps, r0, block):
+    from paper_1410_0986_b200 import lowrank as lr
+    from paper_1410_0986_b200._lib import Ledger
+    rng = np.random.default_rng(m + n)
+    A = random_lowrank(rng, m, n, r, noise) * np.exp(-np.arange(n) / n)[None, :]
+    Ad = torch.as_tensor(A).to(f"cuda:{ctx.device}")
+    calls = {"mv": 0, "rmv": 0, "mm": 0, "rmm": 0}
+
+    def count(name, fn):
+        def g(x):
+            calls[name] += 1
+            return fn(x)
+        return g
+    op = lr.LinOp(rows=m, cols=n, mv=count("mv", lambda x: Ad @ x), rmv=count("rmv", lambda y: Ad.T @ y))
+    if block:
+        op.mm = count("mm", lambda X: Ad @ X)
+        op.rmm = count("rmm", lambda Y: Ad.T @ Y)
+    seed = 20240811 + 0x9e3779b97f4a7c15
+    lo, ld = Ledger(), Ledger()
+    fo = oracle.randsvd(A, eps, 20, 10, seed, oracle.LEAF, r0)
+    fd = lr.randsvd(ctx, A, eps, 20, 10, seed, ledger=ld, cat=lr.LEAF, r0=r0)
+    fg = lr.randsvd(ctx, op, eps, 20, 10, seed, ledger=lo, cat=lr.LEAF, r0=r0)
+    assert fg.rank() == fo.rank == fd.rank()
+    assert fg.flagged == fo.flagged
+    Dg = fg.dense().cpu().numpy()
+    assert fro(Dg - fo.dense()) <= 1e-8 * fro(A)
+    assert fro(Dg - fd.dense().cpu().numpy()) <= 1e-10 * fro(A)
+    sg = np.linalg.norm(fg.V.cpu().numpy(), axis=0)
+    so = np.linalg.norm(fo.V, axis=0)
+    assert np.all(np.abs(sg - so) <= 1e-8 * so[0])
+    # apply_mm charges the same flops whichever form runs (lowrank.cpp:95-98)
+    assert lo.leaf == ld.leaf and lo.kernel_tally == ld.kernel_tally
+    if block:
+        assert calls["mv"] == calls["rmv"] == 0 and calls["mm"] >= 0 and calls["rmm"] == 1
+    else:
+        assert calls["mm"] == calls["rmm"] == 0 and calls["rmv"] >= fg.rank()
+
+
+@pytest.mark.gpu
+def test_randsvd_linop_matrix_free_product_operator(ctx, oracle):
+    # an operator that is never formed: A = diag(w) L R^T diag(c)
+    from paper_1410_0986_b200 import lowrank as lr
+    rng = np.random.default_rng(11)
+    m, n, k = 96, 5000, 9
+    L, R = rng.standard_normal((m, k)), rng.standard_normal((n, k))
+    w, cs = np.exp(rng.standard_normal(m)), np.exp(-np.arange(n) / n)
+    dev = f"cuda:{ctx.device}"
+    Ld, Rd, wd, cd = (torch.as_tensor(a).to(dev) for a in (L, R, w, cs))
+    op = lr.LinOp(rows=m, cols=n,
+                  mm=lambda X: wd[:, None] * (Ld @ (Rd.T @ (cd[:, None] * X))),
+                  rmm=lambda Y: cd[:, None] * (Rd @ (Ld.T @ (wd[:, None] * Y))))
+    A = (w[:, None] * (L @ R.T)) * cs[None, :]
+    fo = oracle.randsvd(A, 1e-9, 20, 10, 5, oracle.OTHER, 1)
+    fg = lr.randsvd(ctx, op, 1e-9, 20, 10, 5)
+    assert fg.rank() == fo.rank == k
+    assert fro(fg.dense().cpu().numpy() - A) <= 10 * 1e-9 * fro(A)   # test_lowrank.cpp:48-63 bound
+    assert fro(fg.dense().cpu().numpy() - fo.dense()) <= 1e-8 * fro(A)
+
+
+@pytest.mark.gpu
+def test_randsvd_linop_errors(ctx):
+    from paper_1410_0986_b200 import lowrank as lr
+    with pytest.raises(ValueError):
+        lr.randsvd(ctx, lr.LinOp(rows=4, cols=5), 1e-6)            # no products at all
+    with pytest.raises(ValueError):
+        lr.randsvd(ctx, lr.LinOp(rows=4, cols=5, mv=lambda x: x), 1e-6)   # no adjoint
+
+    def boom(X):
+        raise KeyError("operator failed")
+    with pytest.raises(KeyError):
+        lr.randsvd(ctx, lr.LinOp(rows=4, cols=50, mm=boom, rmm=boom), 1e-6)
+    f = lr.randsvd(ctx, lr.LinOp(rows=0, cols=5), 1e-6)            # lowrank.cpp:148-152
+    assert f.rank() == 0
