@@ -407,10 +407,11 @@ def run_b200(args):
 # gemm and qr_panel launches and are not candidates)
 KERNEL_CLASSES = {
     "gemm": ("tensor", "dgemm_kernel + splitk_reduce (DMMA m16n8k4.f64)"),
-    "svd_jacobi_large": ("tensor", "jacobi_coop_k (one-sided Jacobi; flops = reference BDCSVD "
-                                   "count 14*max*min^2, lowrank.cpp:38-41)"),
+    "svd_jacobi_large": ("tensor", "bjacobi (block one-sided Jacobi, DMMA) / jacobi_rblk_k (register point "
+                                   "driver); flops = reference BDCSVD count 14*max*min^2, lowrank.cpp:38-41"),
     "svd_jacobi_small": ("tensor", "jacobi_smem_k"),
-    "qr_panel": ("tensor", "qr_panel_coop (Householder panel, 2*m*32^2 flops)"),
+    "qr_panel": ("tensor", "cqr_pass_k / cqr_v_k (CholeskyQR3 + Householder reconstruction) and "
+                           "qr_panel_cta (2*m*32^2 flops)"),
     "skinny_tn": ("hbm", "skinny_tn_k (V^T X, b<=16)"),
     "skinny_nn": ("hbm", "skinny_nn_k (U Z, b<=16)"),
     "born_block": ("hbm", "born_block_k"),

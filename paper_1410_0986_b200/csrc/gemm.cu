@@ -279,14 +279,34 @@ void run_tiles(Ctx& c, bool ta, bool tb, int64_t m, int64_t n, int64_t k, double
     using T = Tile<BM, BN, WM, WN>;
     int64_t tm = (m + BM - 1) / BM, tn = (n + BN - 1) / BN;
     int64_t tiles = tm * tn;
-    int64_t target = int64_t(c.num_sms) * (BM == 64 ? 4 : 1);
+    // Split K when the output tiles alone leave the device under-filled.  The
+    // slice count minimises waves x (k per slice + fixed per-CTA cost) + the
+    // slice reduction, with a wave = the CTAs resident at once (MIN_CTAS per
+    // SM): filling 4/3 of a wave (the earlier 4-per-SM target with 3
+    // resident) ran two rounds for the price of 1.33 (ncu: 592 CTAs, 70 % of
+    // the DMMA pipe on W = V^T C of the tall QRs).
+    const int64_t wave = int64_t(c.num_sms) * T::MIN_CTAS;
     int64_t splits = 1;
-    if (tiles < target) {
-        splits = (target + tiles - 1) / tiles;
-        splits = std::min<int64_t>(splits, (k + 255) / 256);  // >= 256 k per slice
-        splits = std::min<int64_t>(splits, 128);
-        int64_t cap = (int64_t(512) << 20) / (8 * m * n);     // workspace <= 512 MB
-        splits = std::max<int64_t>(1, std::min(splits, std::max<int64_t>(cap, 1)));
+    if (tiles < wave) {
+        int64_t smax = std::min<int64_t>((k + 255) / 256, 128);          // >= 256 k per slice
+        const int64_t cap = (int64_t(512) << 20) / (8 * m * n);          // workspace <= 512 MB
+        smax = std::max<int64_t>(1, std::min(smax, std::max<int64_t>(cap, 1)));
+        double best = 0.0;
+        for (int64_t sp = 1; sp <= smax; ++sp) {
+            int64_t kc = (k + sp - 1) / sp;
+            kc = (kc + BK - 1) / BK * BK;
+            const int64_t ns = (k + kc - 1) / kc;
+            if (ns != sp) continue;  // same slices as a smaller count
+            const double waves = double((tiles * sp + wave - 1) / wave);
+            // k-steps of one CTA: its slice + prologue / epilogue; the
+            // reduction reads sp partial tiles (in k-steps of a full wave)
+            double cost = waves * (double(kc) + 48.0);
+            if (sp > 1) cost += 32.0 + 2.7e-5 * double(sp) * double(m) * double(n);
+            if (sp == 1 || cost < best) {
+                best = cost;
+                splits = sp;
+            }
+        }
     }
     int64_t kchunk = (k + splits - 1) / splits;
     kchunk = (kchunk + BK - 1) / BK * BK;

@@ -224,6 +224,7 @@ void gather_cols(Ctx& c, int64_t rows, int64_t cols, const double* src, int64_t 
 double frob_diff(Ctx& c, int64_t rows, int64_t cols, const double* A, int64_t lda,
                  const double* B, int64_t ldb);  // ||A - B||_F (synchronises)
 void col_norms(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, double* out_dev);
+void normalize(Ctx& c, int64_t n, double* x, double* nrm_dev);  // x /= ||x||, *nrm_dev = ||x||
 // ||offdiag(A)||_F / ||A||_F of an n x n matrix (synchronises)
 double offdiag_ratio(Ctx& c, int64_t n, const double* A, int64_t lda);
 void scatter_rows(Ctx& c, int64_t rows, int64_t cols, const double* src, int64_t lds,
@@ -241,9 +242,20 @@ struct QRFact {
     DBuf a;    // m x n: R in the upper triangle, Householder vectors below
     DBuf tau;  // n
     DBuf T;    // kQRBlock x n : block reflector triangles
+    DBuf flag;  // device int: raised when a CholeskyQR panel had to be left (see geqrf)
+    bool unverified = false;  // flag not read yet (QRCheck::Deferred)
 };
 constexpr int kQRBlock = 128;  // block-reflector width (qr.cu)
-void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f);
+// Tall panels are factored by CholeskyQR + Householder reconstruction, which
+// leaves a panel it cannot orthonormalise and raises f.flag; the
+// factorisation is then redone with Householder panels (Safe).
+//   Now:      the flag is read at the end (one stream synchronisation) and the redo happens inside
+//   Deferred: no synchronisation; the caller must call geqrf_verify after joining the stream and,
+//             when it returns false, redo with geqrf(..., QRCheck::Safe)
+//   Safe:     Householder panels only
+enum class QRCheck { Now, Deferred, Safe };
+void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f, QRCheck chk = QRCheck::Now);
+bool geqrf_verify(Ctx& c, QRFact& f);  // synchronises c.stream
 // Y (m x k) := Q Y (trans=false) or Q^T Y.  nz_rows >= 0 (Q Y only): Y's
 // rows >= nz_rows are zero on entry (the Q [Z; 0] products).
 void apply_q(Ctx& c, const QRFact& f, bool trans, int64_t k, double* Y, int64_t ldy, int64_t nz_rows = -1);

@@ -230,6 +230,11 @@ SVDd fast_thin_svd_impl(Ctx& c, const double* S, int64_t ld, bool trans, int64_t
                 perm = std::move(spec->perm);
                 dperm = std::move(spec->dperm);
                 qf = std::move(spec->qf);
+                if (!geqrf_verify(c, qf)) {  // a CholeskyQR panel was left: Householder panels
+                    DBuf As = dalloc(c, size_t(m * n));
+                    gather_cols(c, m, n, Lp, ldl, dperm.as<int>(), As.d(), m);
+                    geqrf(c, m, n, As.d(), m, qf, QRCheck::Safe);
+                }
             } else {
                 presort_perm(c, m, n, Lp, ldl, perm);
                 dperm = DBuf(c, size_t(n) * sizeof(int));
@@ -349,17 +354,70 @@ void materialize_v_async(Ctx& c, Factor& f) {
 
 // HYDOT_TRACE_RANDSVD=1: one stderr line per sketch pass / Q = I decision
 bool trace_randsvd() {
-    static const bool on = [] {
-        const char* e = std::getenv("HYDOT_TRACE_RANDSVD");
-        return e && e[0] == '1';
-    }();
-    return on;
+    const char* e = std::getenv("HYDOT_TRACE_RANDSVD");
+    return e && e[0] == '1';
 }
 
 namespace {
 Factor randsvd_impl(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, const LinOpDev* op,
                     double eps, int p, int kprobe, uint64_t seed, Ledger* l, int cat, int r0,
                     bool lazy_v);
+
+// what fast_thin_svd charges for an m x n matrix (lowrank.cpp:62-93)
+double fast_thin_svd_flops(double m, double n) {
+    if (n >= 2 * m && m > 0) return fast_thin_svd_flops(n, m);
+    if (m >= 2 * n && n > 0) return 2.0 * qr_flops(m, n) + svd_flops(n, n);
+    return svd_flops(m, n);
+}
+
+// HYDOT_REJECT_BOUND=0: every sketch pass is evaluated in full (read per
+// call: the parity test runs both ways in one process)
+bool reject_bound_on() {
+    const char* e = std::getenv("HYDOT_REJECT_BOUND");
+    return !(e && e[0] == '0');
+}
+// candidate ranks from which the bound is tried: below, the p extra columns
+// of Y capture too much of the residual for the bound to decide
+constexpr int64_t kRejectBoundMinRank = 600;
+constexpr double kRejectMargin = 1.05;
+constexpr int kPowerIters = 40;
+
+// A sketch pass that will be rejected, decided without the SVD of Y.  The
+// reference tests er = |P - Q Q^T P|_F against eps sigma_1(Y) with Q the r
+// leading left singular vectors of Y (lowrank.cpp:167-176).  range(Q) lies in
+// range(Y), so with the Householder QR Y = Q_Y R
+//     er >= lb = |(Q_Y^T P)[rs:m, :]|_F,
+// and sigma_1(Y) comes from a power iteration on Y^T Y (|Y^T Y x| with unit
+// x, a lower estimate that must have settled to 2e-3).  The caller rejects
+// when lb > 1.05 eps sigma_est: the same decision as the reference's, at the
+// cost of one QR instead of the QR + Jacobi SVD + two Q applications.  A
+// pass the bound cannot decide is evaluated in full.
+bool sketch_lower_bound(Ctx& c, int64_t m, int64_t rs, int kprobe, const double* YP, double& lb, double& sig) {
+    StageTimer _t(c, "reject_bound", m, rs);
+    if (m <= rs) return false;
+    QRFact qf;
+    geqrf(c, m, rs, YP, m, qf);
+    DBuf Pc = dalloc(c, size_t(m * kprobe));
+    copy2d(c, m, kprobe, YP + m * rs, m, Pc.d(), m);
+    apply_q(c, qf, true, kprobe, Pc.d(), m);
+    DBuf zero = dalloc(c, size_t((m - rs) * kprobe));
+    fill(c, m - rs, kprobe, 0.0, zero.d(), m - rs);
+    DBuf x = dalloc(c, size_t(rs)), y = dalloc(c, size_t(m)), hist = dalloc(c, size_t(kPowerIters));
+    fill(c, rs, 1, 1.0, x.d(), rs);
+    for (int it = 0; it < kPowerIters; ++it) {
+        skinny_nn(c, m, rs, 1, YP, m, x.d(), rs, y.d(), m);   // y = Y x
+        skinny_tn(c, m, rs, 1, YP, m, y.d(), m, x.d(), rs);   // x = Y^T y
+        normalize(c, rs, x.d(), hist.d() + it);               // |Y^T Y x_it| -> sigma_1^2 from below
+    }
+    lb = frob_diff(c, m - rs, kprobe, Pc.d() + rs, m, zero.d(), m - rs);
+    std::vector<double> h(static_cast<size_t>(kPowerIters));
+    c.d2h(h.data(), hist.d(), h.size());
+    const double last = h.back(), before = h[size_t(kPowerIters - 9)];
+    if (!(last > 0.0) || !std::isfinite(last) || !std::isfinite(lb)) return false;
+    if (last > before * (1.0 + 2e-3)) return false;  // not settled
+    sig = std::sqrt(last);
+    return true;
+}
 }
 
 Factor randsvd(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda, double eps, int p,
@@ -437,7 +495,7 @@ Factor randsvd_impl(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda,
             try {
                 DBuf As = dalloc(c, size_t(n * m));
                 gather_cols(c, n, m, At, lda, spec->dperm.as<int>(), As.d(), n);
-                geqrf(c, n, m, As.d(), n, spec->qf);
+                geqrf(c, n, m, As.d(), n, spec->qf, QRCheck::Deferred);  // verified by the consumer
                 HYDOT_CUDA(cudaEventCreateWithFlags(&spec->ev, cudaEventDisableTiming));
                 HYDOT_CUDA(cudaEventRecord(spec->ev, side));
             } catch (const std::bad_alloc&) {
@@ -473,6 +531,24 @@ Factor randsvd_impl(Ctx& c, int64_t m, int64_t n, const double* At, int64_t lda,
             op->mm(w, Om, YP.d());  // [Y | P] = A [Omega1 | Omega2]
         charge(l, cat, 2.0 * double(m) * double(n) * double(rs));      // apply_mm Y
         charge(l, cat, 2.0 * double(m) * double(n) * double(kprobe));  // apply_mm P
+        if (r < nmax && r >= kRejectBoundMinRank && reject_bound_on()) {
+            double lb = 0.0, sig = 0.0;
+            const bool ok = sketch_lower_bound(c, m, rs, kprobe, YP.d(), lb, sig);
+            const bool reject = ok && lb > kRejectMargin * eps * sig;
+            if (trace_randsvd())
+                fprintf(stderr, "[randsvd] m=%lld n=%lld r=%lld rs=%lld er>=%.3e thr~%.3e %s\n", (long long)m,
+                        (long long)n, (long long)r, (long long)rs, lb, eps * sig,
+                        reject ? "reject (bound)" : "undecided");
+            if (reject) {
+                // the reference's pass: SVD of Y, Q^T P, Q (Q^T P) (lowrank.cpp:167-175)
+                const double q = double(std::min<int64_t>(r, rs));
+                charge(l, cat, fast_thin_svd_flops(double(m), double(rs)));
+                charge(l, cat, 2.0 * q * double(kprobe) * double(m));
+                charge(l, cat, 2.0 * double(m) * double(kprobe) * q);
+                r = std::min<int64_t>(2 * r, nmax);  // :181
+                continue;
+            }
+        }
         svdY = fast_thin_svd(c, YP.d(), m, false, m, rs, l, cat);
         qc = std::min<int64_t>(r, svdY.k);
         const double sigma_top = svdY.s.empty() ? 0.0 : svdY.s[0];
@@ -627,11 +703,10 @@ Factor recompress(Ctx& c, const Factor& f, double eps, int rank, Ledger* l) {
     // stream next to QR(V) (or QR(Z)); `side_done` orders the frees of qu
     // (allocated on the side stream) after every use on c.stream
     cudaStream_t main = c.stream;
-    // only when both cooperative panel grids (<= one CTA per 64 rows, at
-    // most one per SM) fit on the device together: two partially resident
-    // cooperative grids must never wait on each other
-    auto panel_ctas = [&](int64_t rows) { return std::min<int64_t>(c.num_sms, (rows + 63) / 64); };
-    const bool overlap = async_v_on() && panel_ctas(M) + panel_ctas(lv ? lv->zr : N) <= c.num_sms;
+    // the first attempt of either QR launches no cooperative kernel (tall
+    // panels by CholeskyQR, short ones in one CTA); a Householder redo runs
+    // on the main stream after the join (qu) or beside ordinary kernels (qv)
+    const bool overlap = async_v_on();
     struct SideJoin {
         Ctx& c;
         cudaStream_t main;
@@ -661,7 +736,7 @@ Factor recompress(Ctx& c, const Factor& f, double eps, int rank, Ledger* l) {
         cudaEventDestroy(ev0);
         c.stream = c.side;
         try {
-            geqrf(c, M, r, f.U.d(), M, qu);  // :564
+            geqrf(c, M, r, f.U.d(), M, qu, QRCheck::Deferred);  // :564 (verified after the join)
         } catch (...) {
             c.stream = main;
             throw;
@@ -679,6 +754,7 @@ Factor recompress(Ctx& c, const Factor& f, double eps, int rank, Ledger* l) {
     if (ev_u) {
         HYDOT_CUDA(cudaStreamWaitEvent(main, ev_u, 0));
         cudaEventDestroy(ev_u);
+        if (!geqrf_verify(c, qu)) geqrf(c, M, r, f.U.d(), M, qu, QRCheck::Safe);
     }
     c.coop_unchained = unchain.prev;  // later cooperative launches chain again
     const int64_t vm = lv ? lv->zr : N;

@@ -361,25 +361,35 @@ __global__ void __launch_bounds__(LT) larft_k(int jb, const double* __restrict__
 }
 
 }  // namespace
-// returns the device flag (0 ok, 1 zero panel, 2 fall back to Householder)
-const int* panel_cqr(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, double* work,
-                     double* scratch);
+// a panel left untouched (Q not orthonormal) raises *sticky to 2
+// (T, ldt): the panel's compact-WY triangle; form_v: work[0 .. mr jb) = explicit V on return
+void panel_cqr(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, double* work,
+               double* scratch, int* sticky, double* T, int64_t ldt, bool form_v);
 int64_t cqr_scratch_doubles(const Ctx& c);
 namespace {
 
-void panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, const PanelBufs& pbuf,
-           double* work, double* cqr_scratch) {
+// sticky != nullptr: tall panels by CholeskyQR (a failed panel raises
+// *sticky and the caller redoes the factorisation with sticky == nullptr:
+// cooperative Householder panels)
+// Returns true when the CholeskyQR path also produced the sub-panel's T
+// (into Tsub, ld NB) and, with want_v, its explicit V in work.
+bool panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, const PanelBufs& pbuf,
+           double* work, double* cqr_scratch, int* sticky, double* Tsub, bool want_v) {
     StageTimer _t(c, "qr_panel", mr, jb, -1, 2.0 * double(mr) * jb * jb, 16.0 * double(mr) * jb);
     // the same launches split by kind (one CTA on-chip / cooperative tall)
-    StageTimer _k(c, mr <= kCtaRows ? "qr_panel_cta" : "qr_panel_cqr", mr, jb, -1, 2.0 * double(mr) * jb * jb,
-                  16.0 * double(mr) * jb);
+    StageTimer _k(c, mr <= kCtaRows ? "qr_panel_cta" : (sticky ? "qr_panel_cqr" : "qr_panel_coop"), mr, jb, -1,
+                  2.0 * double(mr) * jb * jb, 16.0 * double(mr) * jb);
     const int* only_if = nullptr;
-    if (mr > kCtaRows) {
-        // tall: shifted CholeskyQR3 + Householder reconstruction (qr_cqr.cu);
-        // a panel whose Q comes out non-orthonormal (numerically rank-deficient
-        // within the panel) is redone by the cooperative Householder kernel
-        // below, which then runs only on that device flag
-        only_if = panel_cqr(c, mr, jb, P, ld, tau, work, cqr_scratch);
+    if (mr > kCtaRows && sticky) {
+        // tall: shifted CholeskyQR3 + Householder reconstruction (qr_cqr.cu).
+        // A panel whose Q comes out non-orthonormal (numerically rank-deficient
+        // within the panel) is left untouched and flagged; geqrf checks the
+        // flag once at its end and redoes the factorisation with the
+        // cooperative Householder kernel below.  (Launching that kernel after
+        // every panel on the device flag cost a cooperative launch -- a full
+        // drain of both streams -- per panel.)
+        panel_cqr(c, mr, jb, P, ld, tau, work, cqr_scratch, sticky, Tsub, NB, want_v);
+        return true;
     }
     static AttrGate attr;
     const size_t smem_cap = 200 * 1024;
@@ -391,7 +401,7 @@ void panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, const
         });
         qr_panel_cta<<<1, CT, size_t(mr) * jb * sizeof(double), c.stream>>>(int(mr), jb, P, ld, tau);
         c.check_launch();
-        return;
+        return false;
     }
     int G = c.num_sms;
     int64_t rows_per = (mr + G - 1) / G;
@@ -419,6 +429,7 @@ void panel(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, const
     else
         c.coop_launch((void*)qr_panel_coop<false>, dim3(G), dim3(PT), args, 0);
     c.count();
+    return false;
 }
 
 void form_v_launch(Ctx& c, int64_t mr, int jb, const double* P, int64_t ld, double* V) {
@@ -541,8 +552,10 @@ void larft(Ctx& c, int jb, const double* G, int64_t ldg, const double* tau, doub
 
 }  // namespace
 
-void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f) {
-    StageTimer _t(c, "qr_geqrf", m, n, -1, 2.0 * double(m) * double(n) * double(n));
+namespace {
+// one pass of the blocked factorisation; sticky (device int, may be null):
+// see panel()
+void geqrf_run(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f, int* sticky) {
     f.m = m;
     f.n = n;
     // buffers may be preallocated by the caller (on another stream)
@@ -574,12 +587,16 @@ void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f
             const int pb = std::min(PB, jb - p0);
             const int64_t pr = mr - p0;
             double* Pp = Pb + p0 + int64_t(p0) * m;
-            panel(c, pr, pb, Pp, m, f.tau.d() + j0 + p0, pbuf, V.d(), cqr.d());
             const int rest = jb - p0 - pb;
+            const bool have_tv =
+                panel(c, pr, pb, Pp, m, f.tau.d() + j0 + p0, pbuf, V.d(), cqr.d(), sticky, Tp.d(), rest > 0);
             if (rest > 0) {
                 // apply this sub-panel's reflector to the rest of the block
-                form_v_launch(c, pr, pb, Pp, m, V.d());
-                gram_t32(c, pr, pb, Pp, m, f.tau.d() + j0 + p0, Tp.d(), gpart.d(), gticket.as<unsigned>());
+                // (the CholeskyQR panel leaves V and T behind)
+                if (!have_tv) {
+                    form_v_launch(c, pr, pb, Pp, m, V.d());
+                    gram_t32(c, pr, pb, Pp, m, f.tau.d() + j0 + p0, Tp.d(), gpart.d(), gticket.as<unsigned>());
+                }
                 double* Cm = Pp + int64_t(pb) * m;
                 dgemm(c, true, false, pb, rest, pr, 1.0, V.d(), pr, Cm, m, 0.0, W.d(), pb);
                 dgemm(c, true, false, pb, rest, pb, 1.0, Tp.d(), NB, W.d(), pb, 0.0, W2.d(), pb);
@@ -598,6 +615,44 @@ void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f
             dgemm(c, false, false, mr, nr, jb, -1.0, V.d(), mr, W2.d(), jb, 1.0, Cm, m);
         }
     }
+}
+}  // namespace
+
+void geqrf(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f, QRCheck chk) {
+    StageTimer _t(c, "qr_geqrf", m, n, -1, 2.0 * double(m) * double(n) * double(n));
+    f.unverified = false;
+    // CholeskyQR panels only exist above kCtaRows rows
+    const bool tall = chk != QRCheck::Safe && m > kCtaRows && std::min(m, n) > 0;
+    if (!tall) {
+        geqrf_run(c, m, n, A, lda, f, nullptr);
+        return;
+    }
+    if (f.flag.bytes() < sizeof(int)) f.flag = DBuf(c, sizeof(int));
+    HYDOT_CUDA(cudaMemsetAsync(f.flag.as<void>(), 0, sizeof(int), c.stream));
+    geqrf_run(c, m, n, A, lda, f, f.flag.as<int>());
+    f.unverified = true;
+    if (chk == QRCheck::Now && !geqrf_verify(c, f)) geqrf(c, m, n, A, lda, f, QRCheck::Safe);
+}
+
+bool geqrf_verify(Ctx& c, QRFact& f) {
+    if (!f.unverified) return true;
+    int v = 0;
+    HYDOT_CUDA(cudaMemcpyAsync(&v, f.flag.as<void>(), sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    f.unverified = false;
+    static const bool stats = [] {  // HYDOT_QR_STATS=1: report factorisations that are redone
+        const char* e = std::getenv("HYDOT_QR_STATS");
+        return e && e[0] == '1';
+    }();
+    if (stats) {
+        static long n_all = 0, n_redo = 0;
+        ++n_all;
+        n_redo += v != 0;
+        if (v != 0 || n_all % 100 == 0)
+            fprintf(stderr, "[geqrf] m=%lld n=%lld %s (factorisations %ld, redone %ld)\n", (long long)f.m,
+                    (long long)f.n, v ? "redo by Householder panels" : "ok", n_all, n_redo);
+    }
+    return v == 0;
 }
 
 void apply_q(Ctx& c, const QRFact& f, bool trans, int64_t k, double* Y, int64_t ldy, int64_t nz_rows) {

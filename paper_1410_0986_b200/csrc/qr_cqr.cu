@@ -69,7 +69,10 @@ struct CqrBufs {
     unsigned* ticket;  // last-CTA ticket (self-resetting)
     double* R;         // 3 x W x W: R1, R2, R3 (upper, column-major W x W)
     double* U;         // W x W: U of the top block's LU
-    int* status;       // [0]: 1 = zero panel, 2 = Q not orthonormal (fall back)
+    int* status;       // [0]: 1 = zero panel, 2 = Q not orthonormal (panel left untouched)
+    int* sticky;       // the factorisation's flag: raised to 2 when any panel is left untouched
+    double* T;         // jb x jb compact-WY triangle of the panel's reflectors (ld ldt), may be null
+    int64_t ldt;
 };
 
 // |G3 - I| bound below which Q2 is treated as orthonormal (then Q = Q2 R3^-1
@@ -274,6 +277,8 @@ __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const doubl
             P[r + int64_t(cc) * ldp] = 0.0;
         }
         for (int j = threadIdx.x; j < jb; j += RT) tau[j] = 0.0;
+        if (b.T)
+            for (int e = threadIdx.x; e < jb * jb; e += RT) b.T[e % jb + int64_t(e / jb) * b.ldt] = 0.0;
         for (int64_t e = threadIdx.x; e < (mr - jb) * jb; e += RT)
             P[jb + e % (mr - jb) + int64_t(e / (mr - jb)) * ldp] = 0.0;
         if (threadIdx.x == 0) *b.ticket = 0u;
@@ -292,6 +297,7 @@ __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const doubl
         if (bad) {
             if (threadIdx.x == 0) {
                 b.status[0] = 2;
+                atomicMax(b.sticky, 2);
                 *b.ticket = 0u;
             }
             return;
@@ -379,13 +385,41 @@ __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const doubl
             b.U[e] = (r < jb && cc < jb) ? (r <= cc ? Qt[e] : 0.0) : (r == cc ? 1.0 : 0.0);
         }
         for (int k = threadIdx.x; k < jb; k += RT) tau[k] = -sgn[k] * Qt[k + k * W];
+        if (b.T) {
+            // T = -U S V_1^-T (Ballard et al.; equal to dlarft's T of these
+            // reflectors to rounding): row r of T solves t V_1^T = -(U S)(r, :),
+            // a unit upper triangular system
+            double* Vt = R1s;  // V_1^T (unit upper); R1 is no longer needed
+            __shared__ double one[W];
+            for (int e = threadIdx.x; e < W * W; e += RT) {
+                const int r = e % W, cc = e / W;
+                Vt[e] = r < cc ? ((r < jb && cc < jb) ? Qt[cc + r * W] : 0.0) : (r == cc ? 1.0 : 0.0);
+            }
+            if (threadIdx.x < W) one[threadIdx.x] = 1.0;
+            __syncthreads();
+            if (threadIdx.x < W) {
+                const int r = threadIdx.x;
+                double x[W];
+#pragma unroll
+                for (int j = 0; j < W; ++j) x[j] = (r < jb && j >= r && j < jb) ? -Qt[r + j * W] * sgn[j] : 0.0;
+                if (r < jb) {
+                    row_solve(x, Vt, one, jb);
+#pragma unroll
+                    for (int j = 0; j < W; ++j)
+                        if (j < jb) b.T[r + int64_t(j) * b.ldt] = x[j];
+                }
+            }
+        }
     }
     if (threadIdx.x == 0) *b.ticket = 0u;
 }
 
 // rows >= jb: V = Q2 R3^-1 U^-1 written below the panel's top block
+// Vout (ld mr, may be null): the explicit unit lower-trapezoidal V of the
+// panel (ones on the diagonal, zeros above) that the block update consumes
 __global__ void __launch_bounds__(RT) cqr_v_k(int64_t mr, int jb, const double* __restrict__ Q2, int64_t ldq,
-                                              double* __restrict__ P, int64_t ldp, CqrBufs b) {
+                                              double* __restrict__ P, int64_t ldp, double* __restrict__ Vout,
+                                              CqrBufs b) {
     extern __shared__ __align__(16) double dyn[];
     __shared__ double R3[W * W], Us[W * W], i3[W], iu[W];
     if (b.status[0]) return;
@@ -398,6 +432,11 @@ __global__ void __launch_bounds__(RT) cqr_v_k(int64_t mr, int jb, const double* 
         i3[threadIdx.x] = 1.0 / R3[threadIdx.x * (W + 1)];
         iu[threadIdx.x] = 1.0 / Us[threadIdx.x * (W + 1)];
     }
+    if (Vout && blockIdx.x == 0)  // top block: the LU's strict lower part (written by the previous launch)
+        for (int e = threadIdx.x; e < jb * jb; e += RT) {
+            const int r = e % jb, cc = e / jb;
+            Vout[r + int64_t(cc) * mr] = r > cc ? P[r + int64_t(cc) * ldp] : (r == cc ? 1.0 : 0.0);
+        }
     const int64_t ntiles = (mr + RT - 1) / RT;
     int64_t tt = blockIdx.x;
     if (tt < ntiles) stage_tile(dyn, Q2, ldq, tt * RT, mr, jb);
@@ -418,7 +457,10 @@ __global__ void __launch_bounds__(RT) cqr_v_k(int64_t mr, int jb, const double* 
             row_solve(x, Us, iu, jb);
 #pragma unroll
             for (int j = 0; j < W; ++j)
-                if (j < jb) P[i + int64_t(j) * ldp] = x[j];
+                if (j < jb) {
+                    P[i + int64_t(j) * ldp] = x[j];
+                    if (Vout) Vout[i + int64_t(j) * mr] = x[j];
+                }
         }
         __syncthreads();
     }
@@ -430,12 +472,16 @@ __global__ void __launch_bounds__(RT) cqr_v_k(int64_t mr, int jb, const double* 
 // Factor the mr x jb (jb <= 32) panel P (ld) in place like the Householder
 // panels of qr.cu: R above the diagonal, V below (unit diagonal implied),
 // tau.  `work` holds 2 mr x 32 doubles (Q1, Q2), `scratch` cqr_scratch_doubles()
-// (it must outlive the caller's use of the returned flag).  Returns the
-// device status flag: 2 = P untouched, the caller factors it by Householder.
+// (per-panel state).  A panel whose Q does not come out orthonormal is left
+// untouched and raises *sticky (device) to 2: the caller then redoes the
+// whole factorisation by Householder panels (geqrf, qr.cu).
 int64_t cqr_scratch_doubles(const Ctx& c) { return int64_t(c.num_sms) * 6 * GSZ + 4 * W * W + 2; }
 
-const int* panel_cqr(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, double* work,
-                     double* scratch) {
+// T (ld ldt, may be null) receives the panel's compact-WY triangle and, when
+// form_v is set, work[0 .. mr jb) the explicit V (ld mr) -- Q1's space, free
+// by the last pass.
+void panel_cqr(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, double* work,
+               double* scratch, int* sticky, double* T, int64_t ldt, bool form_v) {
     if (jb < 1 || jb > W || mr < int64_t(W)) throw std::invalid_argument("panel_cqr: shape");
     // one CTA per SM: each streams ~1/148 of the rows; fewer partials keep
     // the last CTA's reduction short
@@ -444,7 +490,7 @@ const int* panel_cqr(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* 
     double* small = scratch + int64_t(c.num_sms) * 6 * GSZ;
     unsigned* ints = reinterpret_cast<unsigned*>(small + 4 * W * W);
     HYDOT_CUDA(cudaMemsetAsync(ints, 0, 2 * sizeof(unsigned), c.stream));
-    CqrBufs b{part, ints, small, small + 3 * W * W, reinterpret_cast<int*>(ints + 1)};
+    CqrBufs b{part, ints, small, small + 3 * W * W, reinterpret_cast<int*>(ints + 1), sticky, T, ldt};
     double* Q1 = work;
     double* Q2 = work + mr * W;
     const double shift = 11.0 * (double(mr) * jb + double(jb) * (jb + 1)) * 1.1102230246251565e-16;
@@ -462,25 +508,8 @@ const int* panel_cqr(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* 
     c.check_launch();
     cqr_pass_k<2><<<grid, RT, smem, c.stream>>>(mr, jb, Q1, mr, Q2, mr, P, ld, tau, b, 0.0);
     c.check_launch();
-    cqr_v_k<<<grid, RT, smem, c.stream>>>(mr, jb, Q2, mr, P, ld, b);
+    cqr_v_k<<<grid, RT, smem, c.stream>>>(mr, jb, Q2, mr, P, ld, form_v ? Q1 : nullptr, b);
     c.check_launch();
-    static const bool stats = [] {  // HYDOT_QR_STATS=1: report panels that fall back
-        const char* e = std::getenv("HYDOT_QR_STATS");
-        return e && e[0] == '1';
-    }();
-    if (stats) {
-        int st = 0;
-        HYDOT_CUDA(cudaMemcpyAsync(&st, b.status, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
-        static long n_all = 0, n_fb = 0, n_zero = 0;
-        ++n_all;
-        n_fb += st == 2;
-        n_zero += st == 1;
-        if (st == 2 || (n_all % 500) == 0)
-            fprintf(stderr, "[cqr] mr=%lld jb=%d status=%d (panels %ld, fallbacks %ld, zero %ld)\n", (long long)mr,
-                    jb, st, n_all, n_fb, n_zero);
-    }
-    return b.status;
 }
 
 }  // namespace hydot

@@ -134,7 +134,32 @@ __global__ void sum_partials(int n, const double* __restrict__ part, double* out
     if (threadIdx.x == 0) *out = sh[0];
 }
 
+// x <- x / ||x||_2 (one CTA), the norm stored to *nrm
+__global__ void __launch_bounds__(1024) normalize_k(int64_t n, double* __restrict__ x, double* __restrict__ nrm) {
+    __shared__ double sh[32];
+    __shared__ double tot;
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc += x[i] * x[i];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) tot = sqrt(v);
+    }
+    __syncthreads();
+    const double t = tot, inv = t > 0.0 ? 1.0 / t : 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] *= inv;
+    if (threadIdx.x == 0) *nrm = t;
+}
+
 }  // namespace
+
+void normalize(Ctx& c, int64_t n, double* x, double* nrm_dev) {
+    normalize_k<<<1, 1024, 0, c.stream>>>(n, x, nrm_dev);
+    c.check_launch();
+}
 
 void Ctx::d2h(double* dst, const double* src, size_t n) {
     if (pinned_len < n) {

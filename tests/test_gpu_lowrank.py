@@ -471,3 +471,85 @@ def test_randsvd_linop_errors(ctx):
         lr.randsvd(ctx, lr.LinOp(rows=4, cols=50, mm=boom, rmm=boom), 1e-6)
     f = lr.randsvd(ctx, lr.LinOp(rows=0, cols=5), 1e-6)            # lowrank.cpp:148-152
     assert f.rank() == 0
+
+
+# ---- rejected sketch passes decided by the QR lower bound --------------------
+def _graded(rng, m, n, decades):
+    Q1, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    Q2, _ = np.linalg.qr(rng.standard_normal((n, m)))
+    return (Q1 * np.logspace(0, -decades, m)) @ Q2.T
+
+
+@pytest.mark.parametrize("m,n,decades,eps,r0,expect_bound", [
+    (900, 6000, 10.0, 3e-10, 700, True),    # merge-like: slow decay, pass at r = 700 rejected (er ~ 7 thr), then Q = I
+    (1300, 5000, 11.0, 3e-10, 950, True),   # er ~ 4.7 thr
+    (1300, 5000, 11.0, 3e-10, 1000, None),  # er ~ 1.8 thr: the bound may or may not decide
+    (900, 6000, 30.0, 3e-10, 700, False),   # fast decay: the pass is accepted (bound undecided -> full path)
+])
+def test_reject_bound_same_result_as_full_evaluation(ctx, oracle, capfd, monkeypatch, m, n, decades, eps, r0,
+                                                     expect_bound):
+    from paper_1410_0986_b200 import lowrank as lr
+    from paper_1410_0986_b200._lib import Ledger
+    rng = np.random.default_rng(m + r0)
+    A = _graded(rng, m, n, decades)
+    monkeypatch.setenv("HYDOT_TRACE_RANDSVD", "1")
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("HYDOT_REJECT_BOUND", mode)
+        led = Ledger()
+        capfd.readouterr()
+        f = lr.randsvd(ctx, A, eps, 20, 10, 99, ledger=led, cat=lr.AGGLOMERATION, r0=r0)
+        out[mode] = (f, led, capfd.readouterr().err)
+    f0, l0, t0 = out["0"]
+    f1, l1, t1 = out["1"]
+    assert "(bound)" not in t0 and "undecided" not in t0
+    # the decision sequence (accept / reject per pass, Q = I) is the same
+    seq = lambda t: [("reject" if "reject" in ln else "accept" if "accept" in ln else "identity")
+                     for ln in t.splitlines() if ln.startswith("[randsvd]") and "undecided" not in ln]
+    assert seq(t0) == seq(t1)
+    if expect_bound is not None:
+        assert ("reject (bound)" in t1) == expect_bound   # the shortcut decided this pass
+    assert f1.rank() == f0.rank() and f1.flagged == f0.flagged
+    assert l1.kernel_tally == l0.kernel_tally and l1.agglomeration == l0.agglomeration
+    D0, D1 = f0.dense().cpu().numpy(), f1.dense().cpu().numpy()
+    if "reject (bound)" in t1 and "accept" not in t1:
+        assert np.array_equal(D0, D1)          # a rejected pass leaves no trace in the result
+    else:
+        assert fro(D0 - D1) <= 1e-12 * fro(A)
+    fo = oracle.randsvd(A, eps, 20, 10, 99, oracle.AGGLOMERATION, r0)
+    assert f1.rank() == fo.rank and f1.flagged == fo.flagged
+    assert fro(D1 - fo.dense()) <= 1e-8 * fro(A)
+
+
+# ---- CholeskyQR panels that give up: the deferred Householder redo ----------
+def test_speculative_tall_qr_redo_on_rank_deficient_input(ctx):
+    # an exactly rank-deficient A with a tolerance no sketch pass can meet: the pass is
+    # rejected, the Q = I branch consumes the speculative QR of A^T started on the side
+    # stream, whose CholeskyQR panels cannot orthonormalise dependent columns -- the
+    # consumer must notice (geqrf_verify) and redo it with Householder panels
+    from paper_1410_0986_b200 import lowrank as lr
+    rng = np.random.default_rng(21)
+    m, n, k = 100, 20000, 10
+    A = rng.standard_normal((m, k)) @ rng.standard_normal((k, n))
+    f = lr.randsvd(ctx, A, 1e-17, 20, 10, 3, r0=60)
+    assert f.rank() >= k
+    assert fro(f.dense().cpu().numpy() - A) <= 1e-12 * fro(A)
+    s = np.linalg.norm(f.V.cpu().numpy(), axis=0)
+    s_ref = np.linalg.svd(A, compute_uv=False)
+    assert np.all(np.abs(s[:k] - s_ref[:k]) <= 1e-12 * s_ref[0])
+
+
+def test_recompress_redo_on_rank_deficient_factor(ctx, oracle):
+    # QR(U) of recompress runs on the side stream with deferred verification
+    from paper_1410_0986_b200 import lowrank as lr
+    rng = np.random.default_rng(22)
+    M, N, r, k = 3000, 5000, 64, 6
+    U = rng.standard_normal((M, k)) @ rng.standard_normal((k, r))      # rank 6 of 64 columns
+    V = rng.standard_normal((N, r))
+    g = lr.LowRankFactor.from_tensors(ctx, torch.as_tensor(U), torch.as_tensor(V))
+    out = lr.recompress(ctx, g, 1e-10)
+    H = U @ V.T
+    assert out.rank() == k
+    assert fro(out.dense().cpu().numpy() - H) <= 1e-10 * fro(H)
+    o = oracle.recompress(oracle.Factor.make(U, V), 1e-10)
+    assert o.rank == out.rank()
