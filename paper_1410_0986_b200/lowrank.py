@@ -164,7 +164,9 @@ def _randsvd_linop(ctx, A: LinOp, eps, p, kprobe, seed, ledger, cat, r0):
 
     def run(fn, stream, body):
         try:
-            ext = torch.cuda.ExternalStream(stream, device=dev)
+            # a NULL cudaStream_t (the legacy default stream) arrives as None
+            ext = (torch.cuda.ExternalStream(stream, device=dev) if stream
+                   else torch.cuda.default_stream(dev))
             with torch.cuda.stream(ext):
                 body()
             return 0
