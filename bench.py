@@ -101,7 +101,7 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
-        sms, mx, reasons = [], None, set()
+        sms, pw, mx, reasons, capped = [], [], None, set(), 0
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -112,11 +112,25 @@ class ClockSampler:
                 mx = float(parts[2])
             except ValueError:
                 continue
+            try:
+                pw.append(float(parts[3]))
+            except ValueError:
+                pass
             for nm, v in zip(names, parts[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sms)}
+                    capped += nm == "sw_power_cap"
+        out = {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
+               "reasons": sorted(reasons), "samples": len(sms)}
+        if sms:
+            # the spread under load: an FP64 tensor-core step runs into the board power cap, and
+            # how often decides the step time (the median alone hides it)
+            q = sorted(sms)
+            out.update({"sm_mhz_min": q[0], "sm_mhz_p10": q[len(q) // 10], "sm_mhz_mean": round(sum(sms) / len(sms), 1),
+                        "power_cap_samples": capped})
+        if pw:
+            out.update({"power_w_mean": round(sum(pw) / len(pw), 1), "power_w_max": max(pw)})
+        return out
 
 
 # --------------------------------------------------------------- b200 arm --

@@ -1,6 +1,7 @@
 // capi.cpp -- the C ABI (include/hydot_b200.h) over the device drivers.
 // Status mapping keeps the reference's exception classes:
 // std::invalid_argument -> HYDOT_EINVAL, std::runtime_error -> HYDOT_ERUNTIME.
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -165,6 +166,34 @@ hydot_status hydot_ctx_destroy(hydot_ctx ctx) {
             cudaStreamDestroy(c.side);
             c.side = nullptr;
         }
+        for (auto& h : c.hp)
+            if (h) {
+                cudaStreamSynchronize(h);
+                cudaStreamDestroy(h);
+                h = nullptr;
+            }
+        if (const char* e = std::getenv("HYDOT_POOL_STATS"); e && e[0] == '1') {
+            // high-water marks of the pools (reserved = mapped from the device, used = handed out)
+            auto report = [](const char* name, cudaMemPool_t p) {
+                if (!p) return;
+                uint64_t rh = 0, uh = 0, rc = 0;
+                cudaMemPoolGetAttribute(p, cudaMemPoolAttrReservedMemHigh, &rh);
+                cudaMemPoolGetAttribute(p, cudaMemPoolAttrUsedMemHigh, &uh);
+                cudaMemPoolGetAttribute(p, cudaMemPoolAttrReservedMemCurrent, &rc);
+                fprintf(stderr, "[pool] %s reserved_high=%.2f GB used_high=%.2f GB reserved_now=%.2f GB\n", name,
+                        double(rh) / double(1ull << 30), double(uh) / double(1ull << 30),
+                        double(rc) / double(1ull << 30));
+            };
+            cudaMemPool_t def = nullptr;
+            if (cudaDeviceGetDefaultMemPool(&def, c.device) == cudaSuccess) report("default", def);
+            report("side", c.side_pool);
+            report("hp", c.hp_pool);
+        }
+        for (cudaMemPool_t* p : {&c.side_pool, &c.hp_pool})
+            if (*p) {
+                cudaMemPoolDestroy(*p);
+                *p = nullptr;
+            }
         if (c.coop_ev) cudaEventDestroy(c.coop_ev);
         c.coop_ev = nullptr;
         if (c.pinned) cudaFreeHost(c.pinned);

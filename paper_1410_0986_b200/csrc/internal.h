@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -54,6 +55,60 @@ struct Ctx {
     cudaStream_t side_stream() {
         if (!side) HYDOT_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
         return side;
+    }
+    // High-priority streams for the panel chain of a look-ahead QR (qr.cu):
+    // [1] serves a factorisation issued on the side stream, [0] any other,
+    // so that the two factorisations that may be in flight at once (the
+    // speculative tall QR beside the main stream's) never queue behind each
+    // other.  Created on demand.
+    cudaStream_t hp[2] = {nullptr, nullptr};
+    cudaStream_t hp_stream(int which) {
+        if (!hp[which]) {
+            int least = 0, greatest = 0;
+            HYDOT_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            HYDOT_CUDA(cudaStreamCreateWithPriority(&hp[which], cudaStreamNonBlocking, greatest));
+        }
+        return hp[which];
+    }
+    // Memory pools.  The context stream allocates from the device's default
+    // pool; the side stream and the high-priority streams each have a pool of
+    // their own.  A block freed in one stream's order can serve another
+    // stream only once that free has completed, so with one shared pool the
+    // host, running ahead of the device, kept finding the other streams'
+    // blocks still pending and grew the pool instead (or, with the device
+    // memory exhausted, made the streams wait for each other): step times
+    // that depended on how far ahead the host happened to be.  Separate pools
+    // reach their own steady state after one step.  HYDOT_STREAM_POOLS=0
+    // keeps everything in the default pool.
+    cudaMemPool_t side_pool = nullptr, hp_pool = nullptr;
+    cudaMemPool_t make_pool() {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        cudaMemPool_t p = nullptr;
+        HYDOT_CUDA(cudaMemPoolCreate(&p, &props));
+        uint64_t thr = UINT64_MAX;  // keep freed memory cached
+        HYDOT_CUDA(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr));
+        return p;
+    }
+    // the pool that serves allocations ordered on s (nullptr: the default pool)
+    cudaMemPool_t pool_for(cudaStream_t s) {
+        static const bool on = [] {
+            const char* e = std::getenv("HYDOT_STREAM_POOLS");
+            return !(e && e[0] == '0');
+        }();
+        if (!on || !s) return nullptr;
+        if (s == side) {
+            if (!side_pool) side_pool = make_pool();
+            return side_pool;
+        }
+        if (s == hp[0] || s == hp[1]) {
+            if (!hp_pool) hp_pool = make_pool();
+            return hp_pool;
+        }
+        return nullptr;
     }
     // Cooperative launches of both streams form one chain (each waits for
     // the previous one to finish): a cooperative grid then only ever shares
@@ -145,7 +200,8 @@ class DBuf {
         s_ = c.stream;
         n_ = bytes;
         if (bytes) {
-            cudaError_t e = cudaMallocAsync(&p_, bytes, s_);
+            cudaMemPool_t pool = c.pool_for(s_);
+            cudaError_t e = pool ? cudaMallocFromPoolAsync(&p_, bytes, pool, s_) : cudaMallocAsync(&p_, bytes, s_);
             if (e != cudaSuccess) {
                 p_ = nullptr;
                 cudaGetLastError();  // do not leave the failed allocation as the sticky last error

