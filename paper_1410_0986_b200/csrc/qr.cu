@@ -587,15 +587,17 @@ void block_update(Ctx& c, int64_t mr, int jb, const double* V, const double* T, 
 //
 // Look-ahead (tall mode, n >= 3 blocks): the panel chain is latency-bound
 // (four streaming passes + three single-CTA tails per 32 columns) and the
-// trailing update is one large DMMA product, so they run side by side.  Block
-// j's reflector is applied first to the next block's columns only, on a
-// high-priority stream H that then goes straight on to factor block j + 1;
-// the rest of block j's trailing update runs meanwhile on the caller's
-// stream S.  Order: R(j) on S waits for block j's V and T; the next-block
-// update N(j + 1) on H waits for R(j), which covers its columns.  The
-// arithmetic of every column is that of the in-line order (same kernels, same
-// operands); only the split of the trailing product into two column ranges
-// differs.
+// trailing update is DMMA work, so part of it runs beside the next block's
+// panels.  Of block j's update C -= V (T^T (V^T C)), the products W = V^T C
+// and W2 = T^T W are formed for all trailing columns on a high-priority
+// stream H (W = V^T C is a split-K product whose CTAs live for ~1 ms: beside
+// it the panel kernels would wait that long for SM slots, which an earlier
+// version that overlapped the whole update measured), then C -= V W2 is
+// applied on H to the next block's columns only, H goes on to factor block
+// j + 1, and the rest of C -= V W2 (short CTAs) runs meanwhile on the caller's
+// stream S.  Order: S waits for W2 (event evH); H waits for S's update (evR)
+// before it reads the trailing columns again for block j + 1's V^T C.  Every
+// column sees the same operations in the same order as in line.
 void geqrf_run(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFact& f, int* sticky) {
     f.m = m;
     f.n = n;
@@ -621,7 +623,7 @@ void geqrf_run(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFac
     DBuf G = dalloc(c, size_t(NB) * NB);
     DBuf W = dalloc(c, size_t(NB) * size_t(std::max<int64_t>(n, 1)));
     DBuf W2 = dalloc(c, size_t(NB) * size_t(std::max<int64_t>(n, 1)));
-    DBuf Wr, W2r;  // R's products (stream S)
+    DBuf Wr, W2r;  // the block-level products (W2r is read on S while H factors the next block)
     if (ahead) {
         Wr = dalloc(c, size_t(NB) * size_t(n));
         W2r = dalloc(c, size_t(NB) * size_t(n));
@@ -685,16 +687,20 @@ void geqrf_run(Ctx& c, int64_t m, int64_t n, const double* A, int64_t lda, QRFac
             block_update(c, mr, jb, Vblk, Tj, nr, Cm, m, W.d(), W2.d());
             continue;
         }
-        // N(j) on H: the next block's columns (the previous R covers them)
+        // on H: W2 = T^T (V^T C) for every trailing column (S's part of the
+        // previous update must have landed), C -= V W2 on the next block
         const int64_t nn = std::min<int64_t>(NB, nr);
         if (r_pending) HYDOT_CUDA(cudaStreamWaitEvent(H, evR, 0));
-        block_update(c, mr, jb, Vblk, Tj, nn, Cm, m, W.d(), W2.d());
-        HYDOT_CUDA(cudaEventRecord(evH, H));
-        // R(j) on S: everything beyond, beside the next block's panels
-        c.stream = S;
-        HYDOT_CUDA(cudaStreamWaitEvent(S, evH, 0));
+        r_pending = false;
+        dgemm(c, true, false, jb, nr, mr, 1.0, Vblk, mr, Cm, m, 0.0, Wr.d(), jb);
+        dgemm(c, true, false, jb, nr, jb, 1.0, Tj, NB, Wr.d(), jb, 0.0, W2r.d(), jb);
+        dgemm(c, false, false, mr, nn, jb, -1.0, Vblk, mr, W2r.d(), jb, 1.0, Cm, m);
         if (nr > nn) {
-            block_update(c, mr, jb, Vblk, Tj, nr - nn, Cm + nn * m, m, Wr.d(), W2r.d());
+            HYDOT_CUDA(cudaEventRecord(evH, H));
+            // on S: the remaining columns, beside block j + 1's panels
+            c.stream = S;
+            HYDOT_CUDA(cudaStreamWaitEvent(S, evH, 0));
+            dgemm(c, false, false, mr, nr - nn, jb, -1.0, Vblk, mr, W2r.d() + nn * jb, jb, 1.0, Cm + nn * m, m);
             HYDOT_CUDA(cudaEventRecord(evR, S));
             r_pending = true;
         }

@@ -173,7 +173,7 @@ def test_householder_qr_tall_rank_deficient(ctx):
 def test_householder_qr_lookahead_equals_inline(ctx, monkeypatch, m, n):
     """geqrf with look-ahead (qr.cu: the next block's panels on a high-priority
     stream beside the rest of the trailing update) against the in-line order
-    (HYDOT_QR_LOOKAHEAD=0): the same Householder QR -- identical R to rounding,
+    (HYDOT_QR_LOOKAHEAD=0): the same Householder QR -- bitwise identical R,
     orthonormal Q, A = Q R -- repeated to catch an ordering race."""
     from paper_1410_0986_b200 import lowrank as lr
     rng = np.random.default_rng(m + n)
@@ -190,9 +190,9 @@ def test_householder_qr_lookahead_equals_inline(ctx, monkeypatch, m, n):
         if mode in out:   # run to run: bitwise
             assert np.array_equal(out[mode], R)
         out[mode] = R
-    # the split of the trailing product changes its split-K only: R agrees to rounding
-    assert np.max(np.abs(out["0"] - out["1"]) / np.linalg.norm(A, axis=0).max()) <= 1e-13
-    assert np.allclose(np.diag(out["0"]), np.diag(out["1"]), rtol=1e-9, atol=1e-14 * np.abs(out["0"]).max())
+    # every column sees the same kernels on the same operands in the same order (only the
+    # k = 128 product C -= V W2 is split by columns, and it has no split-K): bitwise equal
+    assert np.array_equal(out["0"], out["1"])
 
 
 @pytest.mark.parametrize("m,n", [(40, 55), (70, 70), (300, 70), (20000, 60), (90, 400), (250, 250)])
