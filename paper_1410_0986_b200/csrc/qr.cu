@@ -554,11 +554,16 @@ void larft(Ctx& c, int jb, const double* G, int64_t ldg, const double* tau, doub
 }  // namespace
 
 namespace {
-// HYDOT_QR_LOOKAHEAD=0: every block's trailing update in line (read per call:
-// the tests run both ways in one process)
+// HYDOT_QR_LOOKAHEAD=1 turns the look-ahead below on (read per call: the
+// tests run both ways in one process).  Off by default: measured on the
+// B200 it takes 3-6 % off an isolated tall factorisation (262144 x 1542:
+// 78.9 -> 74.5 ms) but the config-2 step stays within its run-to-run noise
+// (the tall QRs already run beside other work on the side stream), while the
+// products that share the SMs with the panels stretch (GEMM class 0.69 ->
+// 0.64 of the FP64 peak).  profiles/lookahead_r02.txt.
 bool lookahead_on() {
     const char* e = std::getenv("HYDOT_QR_LOOKAHEAD");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
 }
 
 // restores the context stream; on an exception the panel stream is drained
